@@ -1,0 +1,157 @@
+/*
+ * geosink_b200.h -- C ABI of the B200-native Geodesic Sinkhorn engine (libgeosink_b200.so).
+ *
+ * This is the drop-in boundary for the reference library's hot path (`geosink`, a static C++
+ * library with no FFI of its own). Each entry point replaces one reference
+ * routine, cited as proj/<file>:<line> under /root/reference; the C++ drop-in layer
+ * (include/geosink/*.hpp) and the Python mirror (paper_2211_00805_b200/) are thin callers of
+ * these functions. Plain pointers and sizes only; no exceptions cross this boundary.
+ *
+ * Status codes: 0 = ok; 1..16 = reference errc + 1 (proj/include/geosink/errors.hpp:10-30,
+ * e.g. 11 = KernelNotPositive, 12 = Disconnected); GS_ERR_CUDA / GS_ERR_NCCL for device and
+ * collective failures. gs_last_error() returns "<ErrcName>: <message>" exactly as the
+ * reference's geosink::Error::what() would (errors.hpp:54-57).
+ *
+ * Memory: every array argument lives on the host (GS_MEM_HOST) or on the context's device
+ * (GS_MEM_DEVICE), selected per call with `mem`. Vertex signals are `width` contiguous
+ * n-vectors (vector p at p*n), the layout of the reference's std::vector<Distribution> inputs.
+ * Graphs and filters are device-resident handles owned by the caller.
+ *
+ * Threading: a context owns one device and one CUDA stream; calls on one context are
+ * serialised and stream-ordered. Separate contexts are independent.
+ */
+#ifndef GEOSINK_B200_H
+#define GEOSINK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_OK 0
+#define GS_ERR_CUDA 100
+#define GS_ERR_NCCL 101
+#define GS_ERR_UNSUPPORTED 102
+
+#define GS_MEM_HOST 0
+#define GS_MEM_DEVICE 1
+
+/* LaplacianKind (graph.hpp:10) */
+#define GS_LAPLACIAN_COMBINATORIAL 0
+#define GS_LAPLACIAN_NORMALIZED 1
+
+/* kNN edge kernels: the reference's alpha decay (graph.hpp:26-33) and the BASELINE
+ * Gaussian exp(-d^2/sigma^2) with sigma = median k-NN bandwidth (extension) */
+#define GS_KERNEL_ALPHA_DECAY 0
+#define GS_KERNEL_GAUSSIAN_MEDIAN 1
+
+/* gs_sinkhorn flags */
+#define GS_FLAG_SINGLE 1             /* sinkhorn_single messages (transport.cpp:132-134) */
+#define GS_FLAG_NO_STAGNATION_ABORT 2 /* bench-only deviation: never raise Disconnected */
+
+typedef struct gs_ctx gs_ctx;
+typedef struct gs_graph gs_graph;   /* SparseSymMatrix on device (sparse.hpp:23-61) */
+typedef struct gs_filter gs_filter; /* HeatFilter on device (heat.hpp:25-54) */
+
+/* ---- context ------------------------------------------------------------------------- */
+int gs_ctx_create(int device, gs_ctx** out);
+void gs_ctx_destroy(gs_ctx* ctx);
+const char* gs_last_error(const gs_ctx* ctx);
+int gs_ctx_synchronize(gs_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the own stream. */
+int gs_ctx_set_stream(gs_ctx* ctx, void* stream);
+void* gs_ctx_stream(gs_ctx* ctx);
+/* Per-kernel-class device timing with CUDA events around every launch (bench evidence). */
+int gs_ctx_set_timing(gs_ctx* ctx, int enable);
+/* class: 0 = Chebyshev step kernels, 1 = epilogue/finalise kernels. Returns launches, ms. */
+int gs_ctx_timing(gs_ctx* ctx, int kernel_class, int64_t* launches, double* total_ms);
+/* Number of engine kernel launches issued on this context so far. */
+int64_t gs_ctx_launch_count(const gs_ctx* ctx);
+
+/* ---- SparseSymMatrix (sparse.hpp:23-61, sparse.cpp:15-116) --------------------------- */
+/* from_triplets (sparse.cpp:15-53): mirror, sort, merge agreeing duplicates, drop zeros. */
+int gs_graph_from_triplets(gs_ctx* ctx, int n, int64_t m, const int* rows, const int* cols,
+                           const double* vals, int mem, gs_graph** out);
+/* Upload an already valid symmetric CSR (both triangles, rows sorted by column). */
+int gs_graph_from_csr(gs_ctx* ctx, int n, int64_t nnz, const int* row_offsets,
+                      const int* col_indices, const double* values, int mem, gs_graph** out);
+void gs_graph_destroy(gs_graph* g);
+int gs_graph_info(const gs_graph* g, int* n, int64_t* nnz);
+int gs_graph_download(gs_ctx* ctx, const gs_graph* g, int* row_offsets, int* col_indices,
+                      double* values, int mem);
+/* y = A x (sparse.cpp:70-99); x, y are `width` contiguous n-vectors. */
+int gs_graph_multiply(gs_ctx* ctx, const gs_graph* g, const double* x, double* y, int width,
+                      int mem);
+int gs_graph_gershgorin(gs_ctx* ctx, const gs_graph* g, double* out); /* sparse.cpp:107-116 */
+
+/* ---- graph construction (graph.hpp:26-42, graph.cpp:30-194) -------------------------- */
+/* select_knn (graph.cpp:30-71): points row-major n x d; nbrs n x k; eps n. */
+int gs_knn(gs_ctx* ctx, const double* points, int n, int d, int k, int mem, int* nbrs,
+           double* eps);
+/* knn_alpha_decay_graph (graph.cpp:75-108) / Gaussian-median extension; sigma_out optional */
+int gs_knn_graph(gs_ctx* ctx, const double* points, int n, int d, int k, int kernel,
+                 double param, int mem, gs_graph** out, double* sigma_out);
+/* laplacian (graph.cpp:110-165); lambda via estimate_lambda_max for the combinatorial kind;
+ * rounds_out (optional): power rounds used, -1 = Gershgorin fallback. */
+int gs_laplacian(gs_ctx* ctx, const gs_graph* A, int kind, gs_graph** L_out,
+                 double* lambda_bound, int* rounds_out);
+int gs_lambda_max(gs_ctx* ctx, const gs_graph* L, double* out, int* rounds_out);
+
+/* ---- heat operator (heat.hpp:19-54, heat.cpp:14-131) --------------------------------- */
+int gs_heat_coefficients(gs_ctx* ctx, double t, int degree, double* out /* degree+1 */);
+int gs_filter_create(gs_ctx* ctx, const gs_graph* L, int kind, double lambda_bound, double t,
+                     int degree, gs_filter** out);
+void gs_filter_destroy(gs_filter* f);
+int gs_filter_info(const gs_filter* f, int* n, double* t, double* t_eff, double* scale,
+                   int* degree, int* kind);
+int gs_filter_coefficients(const gs_filter* f, double* out /* degree+1 */);
+const gs_graph* gs_filter_scaled(const gs_filter* f);
+/* p_K(L_s) X for `width` contiguous n-vectors (heat.cpp:98-131). */
+int gs_filter_apply(gs_ctx* ctx, const gs_filter* f, const double* X, double* Y, int width,
+                    int mem);
+
+/* ---- transport (transport.hpp:58-69, transport.cpp:108-255) -------------------------- */
+/* P pairs against one filter (geodesic_sinkhorn_batch; P = 1 + GS_FLAG_SINGLE is
+ * geodesic_sinkhorn). mus, nus, out_v, out_w: P contiguous n-vectors; a: n. On Disconnected
+ * fail_pair / fail_sweep (optional) name the pair and sweep. */
+int gs_sinkhorn(gs_ctx* ctx, const gs_filter* f, const double* a, const double* mus,
+                const double* nus, int P, int max_iter, double tol, int flags, int mem,
+                double* out_v, double* out_w, double* out_cost, double* out_kl, int* out_iters,
+                int* out_conv, double* out_err, int* fail_pair, int* fail_sweep);
+
+/* ---- barycenter (barycenter.hpp:36-42, barycenter.cpp:45-107) ------------------------ */
+/* Optional collective hook for member-sharded barycenters: sums `count` doubles of the
+ * device buffer across ranks (op 0 = sum, 1 = max) on `stream`. NULL = single rank. */
+typedef int (*gs_allreduce_fn)(void* user, double* device_buf, int64_t count, int op,
+                               void* stream);
+typedef struct {
+  gs_allreduce_fn allreduce;
+  void* user;
+} gs_comm;
+
+/* members, out_V, out_W: m contiguous n-vectors; alphas: m or NULL (uniform). With a comm,
+ * the caller passes its local members and their alphas (global weights). */
+int gs_barycenter(gs_ctx* ctx, const gs_filter* f, const double* a, const double* members,
+                  int m, const double* alphas, int max_iter, double tol, int mem,
+                  const gs_comm* comm, double* out_bary, double* out_V, double* out_W,
+                  int* out_iters, int* out_conv, double* out_err);
+
+/* ---- seeded RNG (rng.hpp:13-68), host-side ---------------------------------------------- */
+typedef struct gs_rng gs_rng;
+gs_rng* gs_rng_create(uint64_t seed);
+void gs_rng_destroy(gs_rng* r);
+uint64_t gs_rng_bits(gs_rng* r);
+double gs_rng_uniform(gs_rng* r);
+double gs_rng_uniform_range(gs_rng* r, double lo, double hi);
+double gs_rng_normal(gs_rng* r);
+uint64_t gs_rng_below(gs_rng* r, uint64_t n);
+uint64_t gs_rng_seed_mix(uint64_t a, uint64_t b);
+/* repeating draw pattern: kind 0 = lo + (hi-lo)*uniform, 1 = hi*normal (+lo), 2 = below(hi) */
+void gs_rng_fill_pattern(gs_rng* r, double* out, int64_t count, const int* kind,
+                         const double* lo, const double* hi, int npat);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

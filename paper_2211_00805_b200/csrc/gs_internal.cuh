@@ -1,0 +1,136 @@
+// gs_internal.cuh -- shared declarations of the B200 Geodesic Sinkhorn engine.
+//
+// Rounding contract: every translation unit is compiled with -fmad=false; fused operations are
+// written as fma() exactly where oracle/geosink_oracle.c writes them, so the device reproduces
+// the oracle bit for bit on every + - * / sqrt fma path (log/exp/pow are the only libdevice vs
+// glibc differences).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "geosink_b200.h"
+
+// errc numbering (proj/include/geosink/errors.hpp:10-30)
+enum gs_errc {
+  ERRC_DIMENSION_MISMATCH = 0, ERRC_DUPLICATE_POINTS, ERRC_NEGATIVE_WEIGHT,
+  ERRC_NON_POSITIVE_TIME, ERRC_LENGTH_MISMATCH, ERRC_TOO_LARGE, ERRC_INDEX_OUT_OF_RANGE,
+  ERRC_SIZE_MISMATCH, ERRC_DEGENERATE_INPUT, ERRC_INVALID_ARGUMENT, ERRC_KERNEL_NOT_POSITIVE,
+  ERRC_DISCONNECTED, ERRC_SOLVE_FAILURE, ERRC_NUMERICAL_UNDERFLOW, ERRC_DEGENERATE_PLAN,
+  ERRC_IO_ERROR
+};
+
+const char* gs_errc_name(int errc);
+
+struct gs_status;
+
+struct gs_event_pair {
+  cudaEvent_t a, b;
+  int cls;
+};
+
+struct gs_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int64_t launches = 0;
+  // timing ring (gs_ctx_set_timing)
+  bool timing = false;
+  std::vector<gs_event_pair> pending;
+  std::vector<gs_event_pair> pool;
+  int64_t t_launches[2] = {0, 0};
+  double t_ms[2] = {0.0, 0.0};
+  // pinned status mirror for host polling
+  gs_status* h_status = nullptr;
+};
+
+struct gs_graph {
+  int n = 0;
+  int64_t nnz = 0;
+  int* offs = nullptr;    // n+1
+  int* cols = nullptr;    // nnz
+  double* vals = nullptr; // nnz
+  int device = 0;
+};
+
+struct gs_filter {
+  gs_graph* scaled = nullptr;
+  double t = 0, t_eff = 0, scale = 1;
+  int degree = 0, kind = 0;
+  std::vector<double> coeffs;  // host mirror (heat.hpp:37)
+  double* d_coeffs = nullptr;
+};
+
+// ---- error plumbing ----------------------------------------------------------------------
+int gs_fail(gs_ctx* ctx, int errc, const std::string& what);  // returns errc + 1
+int gs_cuda_fail(gs_ctx* ctx, cudaError_t e, const char* where);
+
+#define GS_CUDA(ctx, expr)                                   \
+  do {                                                       \
+    cudaError_t _e = (expr);                                 \
+    if (_e != cudaSuccess) return gs_cuda_fail(ctx, _e, #expr); \
+  } while (0)
+
+#define GS_TRY(expr)          \
+  do {                        \
+    int _rc = (expr);         \
+    if (_rc != 0) return _rc; \
+  } while (0)
+
+// ---- launch accounting / timing ------------------------------------------------------------
+void gs_launch_begin(gs_ctx* ctx, int cls);
+void gs_launch_end(gs_ctx* ctx, int cls);
+
+// ---- device scratch ------------------------------------------------------------------------
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  cudaError_t alloc(size_t count, cudaStream_t stream) {
+    release();
+    s = stream;
+    n = count;
+    return cudaMallocAsync((void**)&p, (count ? count : 1) * sizeof(T), stream);
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+};
+
+// ---- shared device helpers ----------------------------------------------------------------
+#define GS_FLOOR 1e-300
+#define GS_CEIL 1e300
+#define DET_T 256
+#define DET_J 16
+#define DET_CHUNK (DET_T * DET_J)
+
+// Global status word layout shared by kernels and the host poll.
+struct gs_status {
+  int error;      // 0 or errc + 1
+  int fail_pair;  // Disconnected pair
+  int fail_sweep; // sweep of the failure
+  int n_active;   // active columns after the last control step
+  int done;       // barycenter converged / finished
+  int pad[3];
+};
+
+// ---- internal entry points shared across translation units -----------------------------------
+int gs_graph_alloc(gs_ctx* ctx, int n, int64_t nnz, gs_graph** out);
+int gs_copy_in(gs_ctx* ctx, void* dst, const void* src, size_t bytes, int mem);
+int gs_copy_out(gs_ctx* ctx, void* dst, const void* src, size_t bytes, int mem);
+int gs_lambda_max_impl(gs_ctx* ctx, const gs_graph* L, double* out, int* rounds_out);
+int gs_coefficients_impl(gs_ctx* ctx, double t, int degree, double* d_out, double* h_out);
+int gs_csr_from_sorted_entries(gs_ctx* ctx, int n, int64_t m, const unsigned long long* d_keys,
+                               const double* d_vals, bool check_dups, gs_graph** out);

@@ -1,0 +1,640 @@
+"""Python mirror of the reference `geosink` public API over the B200 engine's C ABI.
+
+Names, argument meaning and error behaviour follow /root/reference/proj/include/geosink/*.hpp:
+  SparseSymMatrix            sparse.hpp:23-61        (device-resident CSR handle)
+  knn_alpha_decay_graph      graph.hpp:26-33
+  laplacian / GraphLaplacian graph.hpp:10-37
+  estimate_lambda_max        graph.hpp:39-42
+  heat_chebyshev_coefficients heat.hpp:12-19
+  HeatFilter                 heat.hpp:21-54
+  Distribution, SinkhornParams, TransportResult   transport.hpp:14-49
+  geodesic_sinkhorn[_batch]  transport.hpp:51-69
+  DistributionFamily, BarycenterResult, sinkhorn_barycenter, barycentric_distance
+                             barycenter.hpp:11-42
+Errors surface as `Error` carrying the reference `errc` name (errors.hpp:10-85). Every compute
+call runs on the GPU through libgeosink_b200.so; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+import threading
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _capi
+
+# ---------------------------------------------------------------------------------- errors
+ERRC = [
+    "dimension_mismatch", "duplicate_points", "negative_weight", "non_positive_time",
+    "length_mismatch", "too_large", "index_out_of_range", "size_mismatch", "degenerate_input",
+    "invalid_argument", "kernel_not_positive", "disconnected", "solve_failure",
+    "numerical_underflow", "degenerate_plan", "io_error",
+]
+errc = enum.IntEnum("errc", {name: i for i, name in enumerate(ERRC)})
+_NUMERICAL = {errc.kernel_not_positive, errc.disconnected, errc.solve_failure,
+              errc.numerical_underflow, errc.degenerate_plan, errc.io_error}
+
+
+class Error(RuntimeError):
+    """geosink::Error (errors.hpp:54-79): message is "<ErrcName>: <what>"."""
+
+    def __init__(self, code, what: str):
+        super().__init__(what)
+        self.code = code
+
+    def is_validation(self) -> bool:
+        return self.code not in _NUMERICAL if isinstance(self.code, errc) else False
+
+    def is_io(self) -> bool:
+        return self.code == errc.io_error
+
+
+class DeviceError(RuntimeError):
+    """CUDA / NCCL failure inside the engine."""
+
+
+def _raise(rc: int, ctx) -> None:
+    if rc == 0:
+        return
+    msg = _capi.load().gs_last_error(ctx).decode() if ctx else ""
+    if 1 <= rc <= len(ERRC):
+        raise Error(errc(rc - 1), msg)
+    raise DeviceError(f"engine status {rc}: {msg}")
+
+
+# ---------------------------------------------------------------------------------- context
+class Context:
+    """One device + one CUDA stream (gs_ctx). A process-wide default exists per device."""
+
+    _defaults = {}
+    _lock = threading.Lock()
+
+    def __init__(self, device: int = 0):
+        lib = _capi.load()
+        h = C.c_void_p()
+        rc = lib.gs_ctx_create(device, C.byref(h))
+        if rc != 0:
+            raise _capi.EngineUnavailable(
+                f"gs_ctx_create(device={device}) failed with status {rc}: no usable CUDA device")
+        self.handle = h
+        self.device = device
+        self.lib = lib
+
+    @classmethod
+    def default(cls, device: int = 0) -> "Context":
+        with cls._lock:
+            ctx = cls._defaults.get(device)
+            if ctx is None:
+                ctx = cls._defaults[device] = Context(device)
+            return ctx
+
+    def check(self, rc: int):
+        _raise(rc, self.handle)
+
+    def synchronize(self):
+        self.check(self.lib.gs_ctx_synchronize(self.handle))
+
+    def set_stream(self, stream_ptr: int | None):
+        self.check(self.lib.gs_ctx_set_stream(self.handle, stream_ptr))
+
+    def set_timing(self, on: bool):
+        self.check(self.lib.gs_ctx_set_timing(self.handle, int(on)))
+
+    def timing(self, cls: int):
+        n = C.c_int64()
+        ms = C.c_double()
+        self.check(self.lib.gs_ctx_timing(self.handle, cls, C.byref(n), C.byref(ms)))
+        return n.value, ms.value
+
+    def launch_count(self) -> int:
+        return int(self.lib.gs_ctx_launch_count(self.handle))
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.lib.gs_ctx_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def _ctx(ctx: Optional[Context]) -> Context:
+    return ctx or Context.default()
+
+
+def _f64(x) -> np.ndarray:
+    return np.ascontiguousarray(x, dtype=np.float64)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+# ---------------------------------------------------------------------------------- sparse
+@dataclass
+class Triplet:
+    row: int
+    col: int
+    value: float
+
+
+class SparseSymMatrix:
+    """Device-resident symmetric CSR (sparse.hpp:23-61). Host accessors download on demand."""
+
+    def __init__(self, handle, ctx: Context):
+        self._h = handle
+        self._ctx = ctx
+        n = C.c_int()
+        nnz = C.c_int64()
+        ctx.lib.gs_graph_info(handle, C.byref(n), C.byref(nnz))
+        self._n, self._nnz = n.value, nnz.value
+        self._host = None
+        self._owned = True
+
+    @classmethod
+    def _borrow(cls, handle, ctx, owner):
+        m = cls(handle, ctx)
+        m._owned = False
+        m._owner = owner
+        return m
+
+    @staticmethod
+    def from_triplets(n: int, entries, ctx: Optional[Context] = None) -> "SparseSymMatrix":
+        """sparse.cpp:15-53. `entries`: iterable of (row, col, value) or Triplet."""
+        ctx = _ctx(ctx)
+        ent = list(entries)
+        rows = np.array([e.row if isinstance(e, Triplet) else e[0] for e in ent], np.int32)
+        cols = np.array([e.col if isinstance(e, Triplet) else e[1] for e in ent], np.int32)
+        vals = np.array([e.value if isinstance(e, Triplet) else e[2] for e in ent], np.float64)
+        return SparseSymMatrix.from_arrays(n, rows, cols, vals, ctx)
+
+    @staticmethod
+    def from_arrays(n, rows, cols, vals, ctx: Optional[Context] = None) -> "SparseSymMatrix":
+        ctx = _ctx(ctx)
+        rows = np.ascontiguousarray(rows, np.int32)
+        cols = np.ascontiguousarray(cols, np.int32)
+        vals = _f64(vals)
+        h = C.c_void_p()
+        ctx.check(ctx.lib.gs_graph_from_triplets(ctx.handle, int(n), rows.size, _ptr(rows),
+                                                 _ptr(cols), _ptr(vals), _capi.GS_MEM_HOST,
+                                                 C.byref(h)))
+        return SparseSymMatrix(h, ctx)
+
+    @staticmethod
+    def from_csr(n, offs, cols, vals, ctx: Optional[Context] = None) -> "SparseSymMatrix":
+        ctx = _ctx(ctx)
+        offs = np.ascontiguousarray(offs, np.int32)
+        cols = np.ascontiguousarray(cols, np.int32)
+        vals = _f64(vals)
+        h = C.c_void_p()
+        ctx.check(ctx.lib.gs_graph_from_csr(ctx.handle, int(n), cols.size, _ptr(offs), _ptr(cols),
+                                            _ptr(vals), _capi.GS_MEM_HOST, C.byref(h)))
+        return SparseSymMatrix(h, ctx)
+
+    def size(self) -> int:
+        return self._n
+
+    def stored_entries(self) -> int:
+        return self._nnz
+
+    def _download(self):
+        if self._host is None:
+            offs = np.empty(self._n + 1, np.int32)
+            cols = np.empty(max(self._nnz, 1), np.int32)
+            vals = np.empty(max(self._nnz, 1), np.float64)
+            self._ctx.check(self._ctx.lib.gs_graph_download(self._ctx.handle, self._h, _ptr(offs),
+                                                            _ptr(cols), _ptr(vals),
+                                                            _capi.GS_MEM_HOST))
+            self._host = (offs, cols[: self._nnz], vals[: self._nnz])
+        return self._host
+
+    def row_offsets(self):
+        return self._download()[0]
+
+    def col_indices(self):
+        return self._download()[1]
+
+    def values(self):
+        return self._download()[2]
+
+    def coeff(self, i: int, j: int) -> float:
+        if not (0 <= i < self._n and 0 <= j < self._n):
+            raise Error(errc.index_out_of_range, "IndexOutOfRange: coeff index")
+        offs, cols, vals = self._download()
+        lo, hi = offs[i], offs[i + 1]
+        k = np.searchsorted(cols[lo:hi], j)
+        return float(vals[lo + k]) if k < hi - lo and cols[lo + k] == j else 0.0
+
+    def to_dense(self) -> np.ndarray:
+        offs, cols, vals = self._download()
+        d = np.zeros((self._n, self._n))
+        d[np.repeat(np.arange(self._n), np.diff(offs)), cols] = vals
+        return d
+
+    def multiply(self, x) -> np.ndarray:
+        """y = A x (sparse.cpp:70-99); x is (n,) or row-major (n, B) as RowMajorXd."""
+        x = _f64(x)
+        if x.shape[0] != self._n:
+            raise Error(errc.length_mismatch, "LengthMismatch: matvec size")
+        cols = _f64(x.reshape(self._n, -1).T)  # B contiguous n-vectors
+        out = np.empty_like(cols)
+        self._ctx.check(self._ctx.lib.gs_graph_multiply(self._ctx.handle, self._h, _ptr(cols),
+                                                        _ptr(out), cols.shape[0],
+                                                        _capi.GS_MEM_HOST))
+        return out.T.reshape(x.shape).copy()
+
+    def gershgorin_bound(self) -> float:
+        out = C.c_double()
+        self._ctx.check(self._ctx.lib.gs_graph_gershgorin(self._ctx.handle, self._h, C.byref(out)))
+        return out.value
+
+    def max_abs(self) -> float:
+        v = self.values()
+        return float(np.abs(v).max()) if v.size else 0.0
+
+    def __del__(self):
+        try:
+            if self._owned and self._h:
+                self._ctx.lib.gs_graph_destroy(self._h)
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------------- graph
+class LaplacianKind(enum.IntEnum):
+    combinatorial = 0
+    normalized = 1
+
+
+def laplacian_kind_from_string(s: str) -> LaplacianKind:
+    if s == "combinatorial":
+        return LaplacianKind.combinatorial
+    if s == "normalized":
+        return LaplacianKind.normalized
+    raise Error(errc.invalid_argument, f"InvalidArgument: unknown laplacian kind '{s}'")
+
+
+@dataclass
+class GraphLaplacian:
+    matrix: SparseSymMatrix
+    kind: LaplacianKind = LaplacianKind.combinatorial
+    lambda_max_bound: float = 0.0
+    power_rounds: int = 0  # engine diagnostic: power-iteration rounds, -1 = Gershgorin fallback
+
+    def size(self) -> int:
+        return self.matrix.size()
+
+
+def _points(points) -> np.ndarray:
+    pts = _f64(points)
+    if pts.ndim == 1:
+        pts = pts.reshape(-1, 1)
+    return pts
+
+
+def select_knn(points, k: int, ctx: Optional[Context] = None):
+    """graph.cpp:30-71: (neighbours n x k ascending by (d^2, index), eps_k)."""
+    ctx = _ctx(ctx)
+    pts = _points(points)
+    n, d = pts.shape
+    nb = np.empty((n, k), np.int32)
+    eps = np.empty(n, np.float64)
+    ctx.check(ctx.lib.gs_knn(ctx.handle, _ptr(pts), n, d, k, _capi.GS_MEM_HOST, _ptr(nb), _ptr(eps)))
+    return nb, eps
+
+
+def knn_alpha_decay_graph(points, k: int, alpha: float,
+                          ctx: Optional[Context] = None) -> SparseSymMatrix:
+    """graph.cpp:75-108."""
+    ctx = _ctx(ctx)
+    pts = _points(points)
+    n, d = pts.shape
+    h = C.c_void_p()
+    ctx.check(ctx.lib.gs_knn_graph(ctx.handle, _ptr(pts), n, d, int(k), 0, float(alpha),
+                                   _capi.GS_MEM_HOST, C.byref(h), None))
+    return SparseSymMatrix(h, ctx)
+
+
+def knn_gaussian_graph(points, k: int, ctx: Optional[Context] = None):
+    """BASELINE extension: w = exp(-d^2 / sigma^2), sigma = median k-NN bandwidth.
+    Returns (SparseSymMatrix, sigma)."""
+    ctx = _ctx(ctx)
+    pts = _points(points)
+    n, d = pts.shape
+    h = C.c_void_p()
+    sigma = C.c_double()
+    ctx.check(ctx.lib.gs_knn_graph(ctx.handle, _ptr(pts), n, d, int(k), 1, 0.0, _capi.GS_MEM_HOST,
+                                   C.byref(h), C.byref(sigma)))
+    return SparseSymMatrix(h, ctx), sigma.value
+
+
+def laplacian(A: SparseSymMatrix, kind: LaplacianKind) -> GraphLaplacian:
+    """graph.cpp:110-165."""
+    ctx = A._ctx
+    h = C.c_void_p()
+    lam = C.c_double()
+    rounds = C.c_int()
+    ctx.check(ctx.lib.gs_laplacian(ctx.handle, A._h, int(kind), C.byref(h), C.byref(lam),
+                                   C.byref(rounds)))
+    return GraphLaplacian(SparseSymMatrix(h, ctx), LaplacianKind(int(kind)), lam.value, rounds.value)
+
+
+def estimate_lambda_max(L: SparseSymMatrix) -> float:
+    """graph.cpp:167-194."""
+    ctx = L._ctx
+    lam = C.c_double()
+    rounds = C.c_int()
+    ctx.check(ctx.lib.gs_lambda_max(ctx.handle, L._h, C.byref(lam), C.byref(rounds)))
+    return lam.value
+
+
+# ---------------------------------------------------------------------------------- heat
+def heat_chebyshev_coefficients(t: float, degree: int, ctx: Optional[Context] = None) -> np.ndarray:
+    """heat.cpp:34-70, computed on the device."""
+    ctx = _ctx(ctx)
+    if degree < 1:
+        raise Error(errc.invalid_argument, "InvalidArgument: Chebyshev degree must be >= 1")
+    out = np.empty(degree + 1, np.float64)
+    ctx.check(ctx.lib.gs_heat_coefficients(ctx.handle, float(t), int(degree), _ptr(out)))
+    return out
+
+
+class HeatFilter:
+    """heat.hpp:25-54: p_K(L_s) with L_s = scale * L on the device."""
+
+    def __init__(self, laplacian: GraphLaplacian, t: float, degree: int):
+        ctx = laplacian.matrix._ctx
+        self._ctx = ctx
+        h = C.c_void_p()
+        ctx.check(ctx.lib.gs_filter_create(ctx.handle, laplacian.matrix._h, int(laplacian.kind),
+                                           float(laplacian.lambda_max_bound), float(t),
+                                           int(degree), C.byref(h)))
+        self._h = h
+        n = C.c_int()
+        tt, te, sc = C.c_double(), C.c_double(), C.c_double()
+        dg, kd = C.c_int(), C.c_int()
+        ctx.lib.gs_filter_info(h, C.byref(n), C.byref(tt), C.byref(te), C.byref(sc), C.byref(dg),
+                               C.byref(kd))
+        self._n, self._t, self._teff, self._scale = n.value, tt.value, te.value, sc.value
+        self._degree, self._kind = dg.value, LaplacianKind(kd.value)
+        self._coeff = np.empty(self._degree + 1, np.float64)
+        ctx.lib.gs_filter_coefficients(h, _ptr(self._coeff))
+
+    def size(self) -> int:
+        return self._n
+
+    def time(self) -> float:
+        return self._t
+
+    def effective_time(self) -> float:
+        return self._teff
+
+    def scale(self) -> float:
+        return self._scale
+
+    def degree(self) -> int:
+        return self._degree
+
+    def kind(self) -> LaplacianKind:
+        return self._kind
+
+    def coefficients(self) -> np.ndarray:
+        return self._coeff.copy()
+
+    def scaled_laplacian(self) -> SparseSymMatrix:
+        return SparseSymMatrix._borrow(self._ctx.lib.gs_filter_scaled(self._h), self._ctx, self)
+
+    def apply(self, f) -> np.ndarray:
+        """heat.cpp:98-131: (n,) vector or row-major (n, B) signals."""
+        x = _f64(f)
+        if x.shape[0] != self._n:
+            raise Error(errc.length_mismatch, "LengthMismatch: signal length")
+        cols = _f64(x.reshape(self._n, -1).T)
+        out = np.empty_like(cols)
+        self._ctx.check(self._ctx.lib.gs_filter_apply(self._ctx.handle, self._h, _ptr(cols),
+                                                      _ptr(out), cols.shape[0],
+                                                      _capi.GS_MEM_HOST))
+        return out.T.reshape(x.shape).copy()
+
+    def __del__(self):
+        try:
+            if self._h:
+                self._ctx.lib.gs_filter_destroy(self._h)
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------------- transport
+class Distribution:
+    """transport.hpp:15-27."""
+
+    def __init__(self, weights=None, validate: bool = True):
+        self.weights = _f64(weights) if weights is not None else np.zeros(0)
+        if weights is not None and validate:
+            self.validate()
+
+    @staticmethod
+    def uniform(n: int) -> "Distribution":
+        if n < 1:
+            raise Error(errc.invalid_argument, "InvalidArgument: empty support")
+        return Distribution(np.full(n, 1.0 / n))
+
+    @staticmethod
+    def indicator(n: int, vertices: Sequence[int]) -> "Distribution":
+        if len(vertices) == 0:
+            raise Error(errc.invalid_argument, "InvalidArgument: empty indicator set")
+        w = np.zeros(n)
+        for v in vertices:
+            if not 0 <= v < n:
+                raise Error(errc.index_out_of_range, "IndexOutOfRange: indicator vertex out of range")
+            w[v] += 1.0
+        return Distribution(w / w.sum())
+
+    @staticmethod
+    def from_weights(w) -> "Distribution":
+        w = _f64(w).copy()
+        if w.size < 1:
+            raise Error(errc.invalid_argument, "InvalidArgument: empty weight vector")
+        if not (w >= 0.0).all():
+            raise Error(errc.invalid_argument, "InvalidArgument: weights must be non-negative")
+        total = w.sum()
+        if not (total > 0.0 and math.isfinite(total)):
+            raise Error(errc.invalid_argument, "InvalidArgument: weights must have positive mass")
+        w /= total
+        w /= w.sum()
+        return Distribution(w)
+
+    def size(self) -> int:
+        return int(self.weights.size)
+
+    def validate(self) -> None:
+        w = self.weights
+        if w.size < 1:
+            raise Error(errc.length_mismatch, "LengthMismatch: empty distribution")
+        if not np.isfinite(w).all():
+            raise Error(errc.invalid_argument, "InvalidArgument: non-finite weights")
+        if not (w >= 0.0).all():
+            raise Error(errc.invalid_argument, "InvalidArgument: negative weights")
+        if not abs(w.sum() - 1.0) <= 1e-12:
+            raise Error(errc.invalid_argument, "InvalidArgument: distribution must sum to 1")
+
+
+@dataclass
+class SinkhornParams:
+    max_iter: int = 500
+    tol: float = 1e-6
+
+
+@dataclass
+class TransportResult:
+    v: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    w: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    cost: float = 0.0
+    kl: float = 0.0
+    lambda_: float = 0.0
+    iterations: int = 0
+    converged: bool = False
+    marginal_error: float = math.inf
+
+    def kl_form_cost(self) -> float:
+        return math.sqrt(self.lambda_ * max(0.0, 1.0 + self.kl))
+
+    def normalized_cost(self) -> float:
+        return 2.0 * self.kl_form_cost()
+
+    def dual_cost(self) -> float:
+        return self.lambda_ * (1.0 + self.kl)
+
+
+def _stack(dists, n) -> np.ndarray:
+    arr = np.empty((len(dists), n), np.float64)
+    for p, d in enumerate(dists):
+        w = d.weights if isinstance(d, Distribution) else _f64(d)
+        if w.size != n:
+            raise Error(errc.length_mismatch,
+                        "LengthMismatch: distributions must live on the filter's graph")
+        arr[p] = w
+    return arr
+
+
+def _sinkhorn(filter: HeatFilter, mus, nus, a, params: SinkhornParams, flags: int):
+    ctx = filter._ctx
+    n = filter.size()
+    if len(mus) != len(nus):
+        raise Error(errc.size_mismatch, "SizeMismatch: pair lists differ in length")
+    P = len(mus)
+    if P == 0:
+        return []
+    M = _stack(mus, n)
+    N = _stack(nus, n)
+    a = _f64(a)
+    if a.size != n:
+        raise Error(errc.length_mismatch,
+                    "LengthMismatch: vertex weights must live on the filter's graph")
+    v = np.empty((P, n))
+    w = np.empty((P, n))
+    cost = np.empty(P)
+    kl = np.empty(P)
+    it = np.empty(P, np.int32)
+    conv = np.empty(P, np.int32)
+    err = np.empty(P)
+    fp, fs = C.c_int(), C.c_int()
+    ctx.check(ctx.lib.gs_sinkhorn(ctx.handle, filter._h, _ptr(a), _ptr(M), _ptr(N), P,
+                                  int(params.max_iter), float(params.tol), flags,
+                                  _capi.GS_MEM_HOST, _ptr(v), _ptr(w), _ptr(cost), _ptr(kl),
+                                  _ptr(it), _ptr(conv), _ptr(err), C.byref(fp), C.byref(fs)))
+    lam = 4.0 * filter.time()
+    return [TransportResult(v[p].copy(), w[p].copy(), float(cost[p]), float(kl[p]), lam, int(it[p]),
+                            bool(conv[p]), float(err[p])) for p in range(P)]
+
+
+def geodesic_sinkhorn(filter: HeatFilter, mu: Distribution, nu: Distribution, a,
+                      params: SinkhornParams = SinkhornParams()) -> TransportResult:
+    """transport.cpp:243-247 (sinkhorn_single semantics and messages)."""
+    return _sinkhorn(filter, [mu], [nu], a, params, _capi.GS_FLAG_SINGLE)[0]
+
+
+def geodesic_sinkhorn_batch(filter: HeatFilter, mus: List[Distribution], nus: List[Distribution],
+                            a, params: SinkhornParams = SinkhornParams(),
+                            no_stagnation_abort: bool = False) -> List[TransportResult]:
+    """transport.cpp:249-255. `no_stagnation_abort` is the bench-only deviation."""
+    flags = _capi.GS_FLAG_NO_STAGNATION_ABORT if no_stagnation_abort else 0
+    return _sinkhorn(filter, mus, nus, a, params, flags)
+
+
+# ---------------------------------------------------------------------------------- barycenter
+@dataclass
+class DistributionFamily:
+    members: List[Distribution] = field(default_factory=list)
+    alphas: Optional[np.ndarray] = None  # None / empty means uniform
+    label: str = ""
+
+    def resolved_alphas(self) -> np.ndarray:
+        if self.alphas is None or len(self.alphas) == 0:
+            return np.full(len(self.members), 1.0 / len(self.members))
+        return _f64(self.alphas)
+
+    def validate(self, n: int) -> None:
+        if not self.members:
+            raise Error(errc.invalid_argument, "InvalidArgument: family must be non-empty")
+        for m in self.members:
+            m.validate()
+            if m.size() != n:
+                raise Error(errc.length_mismatch,
+                            "LengthMismatch: family members must share the graph")
+        al = self.resolved_alphas()
+        if al.size != len(self.members):
+            raise Error(errc.length_mismatch, "LengthMismatch: one alpha per member required")
+        if not (al >= 0.0).all():
+            raise Error(errc.invalid_argument, "InvalidArgument: alphas must be non-negative")
+        if not abs(al.sum() - 1.0) <= 1e-9:
+            raise Error(errc.invalid_argument, "InvalidArgument: alphas must sum to 1")
+
+
+@dataclass
+class BarycenterResult:
+    barycenter: Distribution
+    scalings: list
+    iterations: int = 0
+    converged: bool = False
+    marginal_error: float = math.inf
+
+
+def sinkhorn_barycenter(filter: HeatFilter, family: DistributionFamily, a,
+                        params: SinkhornParams = SinkhornParams()) -> BarycenterResult:
+    """barycenter.cpp:45-99."""
+    ctx = filter._ctx
+    n = filter.size()
+    family.validate(n)
+    a = _f64(a)
+    if a.size != n:
+        raise Error(errc.length_mismatch,
+                    "LengthMismatch: vertex weights must live on the filter's graph")
+    members = _stack(family.members, n)
+    m = members.shape[0]
+    al = family.resolved_alphas()
+    bary = np.empty(n)
+    V = np.empty((m, n))
+    W = np.empty((m, n))
+    it = np.zeros(1, np.int32)
+    conv = np.zeros(1, np.int32)
+    err = np.zeros(1)
+    ctx.check(ctx.lib.gs_barycenter(ctx.handle, filter._h, _ptr(a), _ptr(members), m, _ptr(al),
+                                    int(params.max_iter), float(params.tol), _capi.GS_MEM_HOST,
+                                    None, _ptr(bary), _ptr(V), _ptr(W), _ptr(it), _ptr(conv),
+                                    _ptr(err)))
+    return BarycenterResult(Distribution(bary, validate=False),
+                            [(V[c].copy(), W[c].copy()) for c in range(m)], int(it[0]),
+                            bool(conv[0]), float(err[0]))
+
+
+def barycentric_distance(filter: HeatFilter, family_t: DistributionFamily,
+                         family_c: DistributionFamily, a,
+                         params: SinkhornParams = SinkhornParams()) -> float:
+    """barycenter.cpp:101-107."""
+    bt = sinkhorn_barycenter(filter, family_t, a, params)
+    bc = sinkhorn_barycenter(filter, family_c, a, params)
+    return geodesic_sinkhorn(filter, bt.barycenter, bc.barycenter, a, params).cost

@@ -1,0 +1,318 @@
+"""GPU parity: the CUDA engine (through its C ABI) against the CPU oracle on the same seeded
+inputs. Integer/index work and every + - * / sqrt fma path must be bit-exact; paths through
+log/exp/pow (libdevice vs glibc) are held to the north-star tolerance, 1e-9 relative in fp64."""
+import numpy as np
+import pytest
+
+import pyoracle as po
+from helpers import (acceptance_graph, engine_filter, oracle_filter, path_graph,
+                     random_connected_graph, random_distribution, random_signal, rel)
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9  # north_star: distances and barycenters within 1e-9 relative in fp64
+
+
+@pytest.fixture(scope="module")
+def gs(ctx):
+    import paper_2211_00805_b200 as gs
+    return gs
+
+
+# --------------------------------------------------------------------------- coefficients
+@pytest.mark.parametrize("t,deg", [(0.5, 30), (1.0, 30), (5.0, 50), (20.0, 110), (7.95, 30),
+                                   (15.33, 30), (50.3, 30), (1e-12, 10), (0.0, 5)])
+def test_coefficients_bit_exact(gs, t, deg):
+    dev = gs.heat_chebyshev_coefficients(t, deg)
+    ref = po.heat_coefficients(t, deg)
+    assert np.array_equal(dev, ref)
+
+
+def test_coefficient_validation(gs):
+    with pytest.raises(gs.Error) as e:
+        gs.heat_chebyshev_coefficients(1.0, 0)
+    assert e.value.code == gs.errc.invalid_argument
+    with pytest.raises(gs.Error) as e:
+        gs.heat_chebyshev_coefficients(-1.0, 5)
+    assert e.value.code == gs.errc.non_positive_time
+
+
+# --------------------------------------------------------------------------- sparse / laplacian
+@pytest.mark.parametrize("n,seed", [(3, 1), (50, 3), (200, 7), (1000, 11)])
+def test_from_triplets_and_laplacian_bit_exact(gs, n, seed):
+    r, c, v = random_connected_graph(n, seed)
+    A = gs.SparseSymMatrix.from_arrays(n, r, c, v)
+    Ao = po.from_triplets(n, r, c, v)
+    assert np.array_equal(A.row_offsets(), Ao.offs)
+    assert np.array_equal(A.col_indices(), Ao.cols)
+    assert np.array_equal(A.values(), Ao.vals)
+    for kind in (0, 1):
+        lap = gs.laplacian(A, gs.LaplacianKind(kind))
+        Lo, lam_o, rounds_o = po.laplacian(Ao, kind)
+        assert np.array_equal(lap.matrix.row_offsets(), Lo.offs)
+        assert np.array_equal(lap.matrix.col_indices(), Lo.cols)
+        assert np.array_equal(lap.matrix.values(), Lo.vals)
+        assert lap.lambda_max_bound == lam_o
+        assert lap.power_rounds == rounds_o
+
+
+def test_triplet_validation_and_duplicates(gs):
+    with pytest.raises(gs.Error) as e:
+        gs.SparseSymMatrix.from_triplets(2, [(0, 2, 1.0)])
+    assert e.value.code == gs.errc.index_out_of_range
+    with pytest.raises(gs.Error) as e:
+        gs.SparseSymMatrix.from_triplets(2, [(0, 1, float("nan"))])
+    assert e.value.code == gs.errc.invalid_argument
+    with pytest.raises(gs.Error) as e:
+        gs.SparseSymMatrix.from_triplets(2, [(0, 1, 1.0), (1, 0, 2.0)])
+    assert "conflicting duplicate" in str(e.value)
+    m = gs.SparseSymMatrix.from_triplets(3, [(0, 1, 1.0), (1, 0, 1.0), (1, 2, 0.0)])
+    assert m.stored_entries() == 2  # agreeing duplicate merged, explicit zero dropped
+    z = gs.SparseSymMatrix.from_triplets(4, [])
+    assert z.stored_entries() == 0 and gs.estimate_lambda_max(z) == 0.0
+
+
+def test_negative_weight_rejected(gs):
+    A = gs.SparseSymMatrix.from_triplets(2, [(0, 1, -0.5)])
+    with pytest.raises(gs.Error) as e:
+        gs.laplacian(A, gs.LaplacianKind.combinatorial)
+    assert e.value.code == gs.errc.negative_weight
+
+
+def test_isolated_vertex_identity_row(gs):
+    A = gs.SparseSymMatrix.from_triplets(3, [(0, 1, 2.0)])
+    L = gs.laplacian(A, gs.LaplacianKind.normalized)
+    assert L.matrix.coeff(2, 2) == 1.0 and L.matrix.coeff(2, 0) == 0.0
+
+
+def test_spmm_and_gershgorin_bit_exact(gs):
+    n = 300
+    r, c, v = random_connected_graph(n, 5)
+    A = gs.SparseSymMatrix.from_arrays(n, r, c, v)
+    Ao = po.from_triplets(n, r, c, v)
+    rng = np.random.default_rng(0)
+    for width in (1, 3, 8, 17):
+        x = rng.standard_normal((n, width)) if width > 1 else rng.standard_normal(n)
+        assert np.array_equal(A.multiply(x), po.spmm(Ao, x))
+    assert A.gershgorin_bound() == po.gershgorin(Ao)
+
+
+# --------------------------------------------------------------------------- filter
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("width", [1, 2, 3, 5, 8, 13, 64])
+def test_filter_apply_bit_exact(gs, kind, width):
+    n = 257
+    r, c, v = acceptance_graph(n, 1000 + n)
+    f, _ = engine_filter(r, c, v, n, kind, 1.0, 30)
+    fo = oracle_filter(r, c, v, n, kind, 1.0, 30)
+    assert np.array_equal(f.coefficients(), fo.coeffs)
+    X = np.random.default_rng(width).standard_normal((n, width))
+    if width == 1:
+        X = X[:, 0]
+    assert np.array_equal(f.apply(X), fo.apply(X))
+
+
+def test_two_vertex_closed_form(gs):
+    """test_heat.cpp:135-150."""
+    f, _ = engine_filter(np.array([0], np.int32), np.array([1], np.int32), np.array([1.0]), 2, 0,
+                         1.0, 10)
+    out = f.apply(np.array([1.0, 0.0]))
+    assert abs(out[0] - 0.5676676416) <= 1e-6 * 0.5676676416
+    assert abs(out[1] - 0.4323323584) <= 1e-6 * 0.4323323584
+    p = 0.5 * (1 + np.exp(-2.0))
+    q = 0.5 * (1 - np.exp(-2.0))
+    assert np.max(np.abs(out - [p, q])) <= 1e-9
+
+
+def test_batched_equals_single(gs):
+    """test_heat.cpp:167-179: batched application equals per-signal application."""
+    r, c, v = random_connected_graph(40, 9)
+    f, _ = engine_filter(r, c, v, 40, 1, 1.2, 25)
+    from paper_2211_00805_b200.rng import Rng
+    rng = Rng(10)
+    batch = np.stack([random_signal(40, rng) for _ in range(7)], axis=1)
+    out = f.apply(batch)
+    for col in range(7):
+        assert np.array_equal(out[:, col], f.apply(batch[:, col].copy()))
+
+
+# --------------------------------------------------------------------------- Sinkhorn
+def _pairs(n, P, seed):
+    from paper_2211_00805_b200.rng import Rng
+    rng = Rng(seed)
+    mus = [random_distribution(n, rng) for _ in range(P)]
+    nus = [random_distribution(n, rng) for _ in range(P)]
+    return mus, nus
+
+
+@pytest.mark.parametrize("P", [1, 4, 9])
+def test_sinkhorn_batch_matches_oracle(gs, P):
+    n = 120
+    r, c, v = random_connected_graph(n, 21)
+    f, _ = engine_filter(r, c, v, n, 1, 0.9, 30)
+    fo = oracle_filter(r, c, v, n, 1, 0.9, 30)
+    mus, nus = _pairs(n, P, 7)
+    a = np.full(n, 1.0 / n)
+    res = gs.geodesic_sinkhorn_batch(f, [gs.Distribution(m) for m in mus],
+                                     [gs.Distribution(x) for x in nus], a, gs.SinkhornParams(400, 1e-9))
+    ref = po.sinkhorn_batch(fo, a, np.array(mus), np.array(nus), 400, 1e-9)
+    for p in range(P):
+        assert res[p].iterations == ref["iterations"][p]
+        assert res[p].converged == ref["converged"][p]
+        assert rel(res[p].cost, ref["cost"][p]) <= TOL
+        assert rel(res[p].kl, ref["kl"][p]) <= TOL
+        assert np.array_equal(res[p].v, ref["v"][p])
+        assert np.array_equal(res[p].w, ref["w"][p])
+        assert rel(res[p].marginal_error, ref["marginal_error"][p]) <= 1e-6
+
+
+def test_sinkhorn_mixed_convergence(gs):
+    """Pairs converge at different sweeps: the compaction semantics (transport.cpp:210-226)."""
+    n = 90
+    r, c, v = random_connected_graph(n, 4)
+    f, _ = engine_filter(r, c, v, n, 0, 1.0, 30)
+    fo = oracle_filter(r, c, v, n, 0, 1.0, 30)
+    mus, nus = _pairs(n, 6, 3)
+    nus[2] = mus[2]  # self transport converges fast
+    a = np.full(n, 1.0 / n)
+    res = gs.geodesic_sinkhorn_batch(f, [gs.Distribution(m) for m in mus],
+                                     [gs.Distribution(x) for x in nus], a, gs.SinkhornParams(60, 1e-8))
+    ref = po.sinkhorn_batch(fo, a, np.array(mus), np.array(nus), 60, 1e-8)
+    assert len(set(int(x) for x in ref["iterations"])) > 1
+    for p in range(6):
+        assert res[p].iterations == ref["iterations"][p]
+        assert res[p].converged == ref["converged"][p]
+        assert np.array_equal(res[p].v, ref["v"][p])
+        assert rel(res[p].cost, ref["cost"][p]) <= TOL
+
+
+def test_disconnected_raises_like_reference(gs):
+    """test_transport.cpp:354-367 + batch message with the pair index."""
+    f, _ = engine_filter(np.array([0, 2], np.int32), np.array([1, 3], np.int32), np.array([1.0, 1.0]),
+                         4, 0, 1.0, 20)
+    a = np.full(4, 0.25)
+    mu = gs.Distribution.indicator(4, [0])
+    nu = gs.Distribution.indicator(4, [3])
+    with pytest.raises(gs.Error) as e:
+        gs.geodesic_sinkhorn(f, mu, nu, a, gs.SinkhornParams(500, 1e-9))
+    assert e.value.code == gs.errc.disconnected
+    assert "same graph component" in str(e.value)
+    ok = gs.Distribution.indicator(4, [1])
+    with pytest.raises(gs.Error) as e:
+        gs.geodesic_sinkhorn_batch(f, [mu, mu], [ok, nu], a, gs.SinkhornParams(500, 1e-9))
+    assert e.value.code == gs.errc.disconnected
+    assert str(e.value).endswith("for pair 1")
+
+
+def test_kernel_not_positive(gs):
+    """test_transport.cpp:369-382."""
+    n = 40
+    r, c, v = random_connected_graph(n, 40)
+    f, _ = engine_filter(r, c, v, n, 1, 50.0, 3)
+    a = np.full(n, 1.0 / n)
+    with pytest.raises(gs.Error) as e:
+        gs.geodesic_sinkhorn(f, gs.Distribution.indicator(n, [7]), gs.Distribution.indicator(n, [20]),
+                             a, gs.SinkhornParams(100, 1e-9))
+    assert e.value.code == gs.errc.kernel_not_positive
+
+
+def test_distribution_validation(gs):
+    n = 10
+    r, c, v = random_connected_graph(n, 2)
+    f, _ = engine_filter(r, c, v, n, 1, 1.0, 10)
+    good = np.full(n, 0.1)
+    bad = np.full(n, 0.2)
+    with pytest.raises(gs.Error) as e:
+        gs.geodesic_sinkhorn(f, gs.Distribution(good), gs.Distribution(bad, validate=False), good)
+    assert "sum to 1" in str(e.value)
+    with pytest.raises(gs.Error) as e:
+        gs.geodesic_sinkhorn(f, gs.Distribution(good), gs.Distribution(good), -good)
+    assert "vertex weights must be positive" in str(e.value)
+
+
+# --------------------------------------------------------------------------- barycenter
+@pytest.mark.parametrize("m,kind", [(1, 1), (3, 1), (8, 0), (11, 1)])
+def test_barycenter_matches_oracle(gs, m, kind):
+    n = 100
+    r, c, v = random_connected_graph(n, 12)
+    f, _ = engine_filter(r, c, v, n, kind, 0.8, 30)
+    fo = oracle_filter(r, c, v, n, kind, 0.8, 30)
+    from paper_2211_00805_b200.rng import Rng
+    rng = Rng(8 + m)
+    members = [random_distribution(n, rng) for _ in range(m)]
+    a = np.full(n, 1.0 / n)
+    fam = gs.DistributionFamily([gs.Distribution(x) for x in members])
+    res = gs.sinkhorn_barycenter(f, fam, a, gs.SinkhornParams(300, 1e-8))
+    ref = po.barycenter(fo, a, np.array(members), None, 300, 1e-8)
+    assert res.iterations == ref["iterations"]
+    assert res.converged == ref["converged"]
+    assert rel(res.barycenter.weights, ref["barycenter"]) <= TOL
+    for cidx in range(m):
+        assert rel(res.scalings[cidx][0], ref["V"][cidx]) <= TOL
+        assert rel(res.scalings[cidx][1], ref["W"][cidx]) <= TOL
+
+
+def test_barycentric_distance(gs):
+    n = 30
+    r, c, v = random_connected_graph(n, 14)
+    f, _ = engine_filter(r, c, v, n, 1, 0.7, 30)
+    from paper_2211_00805_b200.rng import Rng
+    rng = Rng(13)
+    t_fam = gs.DistributionFamily([gs.Distribution(random_distribution(n, rng)) for _ in range(2)])
+    c_fam = gs.DistributionFamily([gs.Distribution(random_distribution(n, rng)) for _ in range(2)])
+    a = np.full(n, 1.0 / n)
+    tc = gs.barycentric_distance(f, t_fam, c_fam, a, gs.SinkhornParams(500, 1e-8))
+    ct = gs.barycentric_distance(f, c_fam, t_fam, a, gs.SinkhornParams(500, 1e-8))
+    assert abs(tc - ct) <= 1e-8 * (1 + abs(tc))
+
+
+# --------------------------------------------------------------------------- kNN
+def test_knn_tie_break_lower_index(gs):
+    """test_graph.cpp:50-58."""
+    pts = np.array([[0, 0], [1, 0], [0, 1], [-1, 0], [0, -1]], np.float64)
+    A = gs.knn_alpha_decay_graph(pts, 2, 2.0)
+    assert A.coeff(2, 3) > 0.0
+    assert A.coeff(3, 4) == 0.0
+    assert A.coeff(1, 4) > 0.0
+
+
+def test_knn_three_collinear(gs):
+    """test_graph.cpp:41-48."""
+    A = gs.knn_alpha_decay_graph(np.array([[0.0], [1.0], [2.0]]), 1, 2.0)
+    assert abs(A.coeff(0, 1) - np.exp(-1.0)) <= 1e-12 * np.exp(-1.0)
+    assert abs(A.coeff(1, 2) - np.exp(-1.0)) <= 1e-12 * np.exp(-1.0)
+    assert A.coeff(0, 2) == 0.0 and A.coeff(0, 0) == 0.0
+
+
+def test_knn_duplicates_raise(gs):
+    with pytest.raises(gs.Error) as e:
+        gs.knn_alpha_decay_graph(np.array([[1.0], [1.0]]), 1, 40.0)
+    assert e.value.code == gs.errc.duplicate_points
+
+
+@pytest.mark.parametrize("n,d,k", [(500, 3, 10), (700, 30, 15), (300, 2, 4)])
+def test_knn_indices_bit_exact(gs, n, d, k):
+    from paper_2211_00805_b200.rng import Rng
+    pts = Rng(n + d).normals(n * d).reshape(n, d)
+    nb, eps = gs.select_knn(pts, k)
+    nbo, epso = po.knn(pts, k)
+    assert np.array_equal(nb, nbo)
+    assert np.array_equal(eps, epso)
+
+
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_knn_graph_matches_oracle(gs, kernel):
+    from paper_2211_00805_b200.rng import Rng
+    n, d, k = 400, 3, 10
+    pts = Rng(5).normals(n * d).reshape(n, d)
+    if kernel == 0:
+        A = gs.knn_alpha_decay_graph(pts, k, 40.0)
+        sigma = None
+    else:
+        A, sigma = gs.knn_gaussian_graph(pts, k)
+    Ao, sigma_o = po.knn_graph(pts, k, kernel, 40.0)
+    assert np.array_equal(A.row_offsets(), Ao.offs)
+    assert np.array_equal(A.col_indices(), Ao.cols)
+    assert rel(A.values(), Ao.vals) <= 1e-13
+    if sigma is not None:
+        assert sigma == sigma_o
