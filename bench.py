@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""Benchmark of the Chebyshev-Sinkhorn hot path (BASELINE.json config 1) on B200.
+
+One "step" = one full batched geodesic Sinkhorn run (geodesic_sinkhorn_batch,
+proj/src/transport.cpp:144-239): 64 source/target pairs on a 200,000-vertex swiss-roll kNN graph,
+200 sweeps, each sweep = two 30-step Chebyshev heat applications over the 64-column batch.
+
+  value  : sweeps/s over the whole job (N ranks x 200 sweeps x K steps / max-over-ranks time),
+           inputs resident in HBM, device pointers through the C ABI.
+  e2e    : the same metric through the public API with host buffers (H2D of mu/nu/a and D2H of
+           v/w/cost/kl inside the timed region).
+  roofline: the dominant kernel (k_cheb_step) -- algorithmic bytes per launch (SURVEY.md §8(d):
+           nnz*(8+4) + 4(n+1) + 5*n*B*8) / its average CUDA-event duration in the timed region.
+  cpu_baseline: the oracle restatement (oracle/, -O3 -march=native OpenMP) on this host, bounded
+           sample of the same batch on the GPU-built graph.
+
+Multi-GPU (torchrun): weak scaling, each rank runs its own 64 pairs on a replica of the graph,
+no data-path collective (pairs are independent); timing is max over ranks.
+`--impl reference` times the CPU reference path (the oracle port; the reference C++ library
+cannot be built here) on the same config, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Chebyshev-Sinkhorn iterations/sec and achieved HBM GB/s vs peak, 1/2/4/8 B200"
+UNIT = "sweeps/s"
+TOL_RUN_ALL = 5e-324  # smallest positive double: the loop never exits early
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    smax.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, val in zip(names, parts[5:9]):
+                    if val.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None, "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def algorithmic_bytes_per_step(n, nnz, B, sv=8):
+    """matrix values + int32 indices + int32 offsets + 5 vector streams."""
+    return nnz * (sv + 4) + 4 * (n + 1) + 5 * n * B * sv
+
+
+# --------------------------------------------------------------------------- CPU legs
+def cpu_sinkhorn_sample(L_host, lam, cfg, sweeps, native=True):
+    """Time `sweeps` batched sweeps of the oracle on the GPU-built Laplacian; returns sweeps/s."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+
+    lib = po.lib(native=native)
+    Lo = po.CSR(L_host[0], L_host[1], L_host[2], L_host[3])
+    fo = po.Filter(Lo, 0, lam, cfg.t, cfg.degree)
+    n = cfg.roll.s.size
+    a = np.full(n, 1.0 / n)
+    t0 = time.perf_counter()
+    po.sinkhorn_batch(fo, a, cfg.mus, cfg.nus, sweeps, TOL_RUN_ALL, flags=1, L=lib)
+    dt = time.perf_counter() - t0
+    return sweeps / dt, dt
+
+
+def run_reference(args):
+    """--impl reference: the CPU reference path (oracle port, all host threads), rank 0 only."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    from paper_2211_00805_b200 import workloads
+
+    lib = po.lib(native=True)
+    cfg = workloads.config1(args.n, args.pairs, seed=1, pair_seed=2)
+    t0 = time.perf_counter()
+    A, sigma = po.knn_graph(cfg.roll.points, cfg.k, 1, 0.0)
+    L, lam, rounds = po.laplacian(A, 0)
+    fo = po.Filter(L, 0, lam, cfg.t, cfg.degree)
+    setup_s = time.perf_counter() - t0
+    n = args.n
+    a = np.full(n, 1.0 / n)
+    sweeps = args.ref_sweeps
+
+    def step():
+        po.sinkhorn_batch(fo, a, cfg.mus, cfg.nus, sweeps, TOL_RUN_ALL, flags=1, L=lib)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    value = args.steps * sweeps / dt
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * dt / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": config_dict(args, A.nnz, lam, rounds, sigma, extra={"setup_s": setup_s}),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{sweeps} sweep(s) of the 64-pair batch per step on the full "
+                                   f"n={n} graph (oracle restatement, OpenMP, -march=native)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(args, nnz_A, lam, rounds, sigma, extra=None):
+    d = {
+        "workload": (f"config1: swiss roll n={args.n}, k=10 symmetrised kNN, Gaussian weights "
+                     f"sigma=median eps_10, combinatorial L, t=1, K=30, {args.pairs} pairs x "
+                     f"{args.sweeps} sweeps (2 x {args.pairs}-column applies per sweep), fp64"),
+        "n": args.n, "pairs": args.pairs, "sweeps_per_step": args.sweeps, "degree": 30,
+        "nnz_adjacency": int(nnz_A), "lambda_max_bound": lam, "lambda_rounds": rounds,
+        "sigma": sigma, "stagnation_abort": "disabled (bench-only, DESIGN.md)",
+        "tol": "5e-324 (all sweeps run)",
+        "l2": "working set > 0.8 GB >> 126 MB L2; no flush needed between steps",
+    }
+    if extra:
+        d.update(extra)
+    return d
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_engine(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_00805_b200 as gs
+    from paper_2211_00805_b200 import _capi, workloads
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = gs.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    lib = ctx.lib
+
+    # ---- setup: graph build + Laplacian + lambda + filter, all on the device -------------------
+    cfg = workloads.config1(args.n, args.pairs, seed=1, pair_seed=2 + 1000 * rank)
+    t0 = time.perf_counter()
+    A, sigma = gs.knn_gaussian_graph(cfg.roll.points, cfg.k, ctx=ctx)
+    t_graph = time.perf_counter() - t0
+    lap = gs.laplacian(A, gs.LaplacianKind.combinatorial)
+    filt = gs.HeatFilter(lap, cfg.t, cfg.degree)
+    t_prep = time.perf_counter() - t0 - t_graph
+    n, P = args.n, args.pairs
+    nnz_L = lap.matrix.stored_entries()
+
+    dev = torch.device("cuda", local)
+    M = torch.from_numpy(cfg.mus).to(dev)
+    N = torch.from_numpy(cfg.nus).to(dev)
+    a = torch.full((n,), 1.0 / n, dtype=torch.float64, device=dev)
+    ov = torch.empty((P, n), dtype=torch.float64, device=dev)
+    ow = torch.empty_like(ov)
+    oc = torch.empty(P, dtype=torch.float64, device=dev)
+    ok = torch.empty_like(oc)
+    oi = torch.empty(P, dtype=torch.int32, device=dev)
+    occ = torch.empty_like(oi)
+    oe = torch.empty_like(oc)
+    import ctypes as C
+    fp, fs = C.c_int(), C.c_int()
+    flags = _capi.GS_FLAG_NO_STAGNATION_ABORT
+
+    def step():
+        ctx.check(lib.gs_sinkhorn(ctx.handle, filt._h, a.data_ptr(), M.data_ptr(), N.data_ptr(), P,
+                                  args.sweeps, TOL_RUN_ALL, flags, _capi.GS_MEM_DEVICE,
+                                  ov.data_ptr(), ow.data_ptr(), oc.data_ptr(), ok.data_ptr(),
+                                  oi.data_ptr(), occ.data_ptr(), oe.data_ptr(), C.byref(fp),
+                                  C.byref(fs)))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else args.warmup):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    ctx.set_timing(True)
+    l0 = ctx.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    launches = ctx.launch_count() - l0
+    step_n, step_ms = ctx.timing(0)
+    epi_n, epi_ms = ctx.timing(1)
+    ctx.set_timing(False)
+    elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    value = world * args.sweeps * args.steps / (elapsed_ms / 1000.0)
+
+    # ---- roofline of the dominant kernel ------------------------------------------------------
+    peak, peak_kind = peaks()
+    bytes_step = algorithmic_bytes_per_step(n, nnz_L, P)
+    avg_step_ms = step_ms / max(step_n, 1)
+    achieved = bytes_step / (avg_step_ms / 1000.0) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "cheb_step_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the public API with host buffers --------------------------------------------
+    Mh = torch.from_numpy(cfg.mus).pin_memory()
+    Nh = torch.from_numpy(cfg.nus).pin_memory()
+    ah = torch.full((n,), 1.0 / n, dtype=torch.float64).pin_memory()
+    vh = torch.empty((P, n), dtype=torch.float64).pin_memory()
+    wh = torch.empty_like(vh).pin_memory()
+    ch = np.empty(P)
+    kh = np.empty(P)
+    ih = np.empty(P, np.int32)
+    cvh = np.empty(P, np.int32)
+    eh = np.empty(P)
+
+    def step_host():
+        ctx.check(lib.gs_sinkhorn(ctx.handle, filt._h, ah.data_ptr(), Mh.data_ptr(), Nh.data_ptr(),
+                                  P, args.sweeps, TOL_RUN_ALL, flags, _capi.GS_MEM_HOST,
+                                  vh.data_ptr(), wh.data_ptr(), ch.ctypes.data, kh.ctypes.data,
+                                  ih.ctypes.data, cvh.ctypes.data, eh.ctypes.data, C.byref(fp),
+                                  C.byref(fs)))
+
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    step_host()
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        step_host()
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    barrier()
+    e2e_value = world * args.sweeps * e2e_steps / e2e_s
+    h2d = 2 * P * n * 8 + n * 8
+    d2h = 2 * P * n * 8 + P * (8 + 8 + 4 + 4 + 8)
+
+    # ---- CPU baseline (rank 0, N = 1) ---------------------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        offs = lap.matrix.row_offsets().copy()
+        cols = lap.matrix.col_indices().copy()
+        vals = lap.matrix.values().copy()
+        sweeps = args.cpu_sweeps
+        v, dt = cpu_sinkhorn_sample((n, offs, cols, vals), lap.lambda_max_bound, cfg, sweeps)
+        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{sweeps} sweep(s) of the same 64-pair batch on the GPU-built n={n} "
+                         f"graph, oracle restatement -O3 -march=native OpenMP ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": config_dict(args, A.stored_entries(), lap.lambda_max_bound,
+                                  lap.power_rounds, sigma,
+                                  extra={"nnz_L": int(nnz_L), "graph_build_s": t_graph,
+                                         "prepare_s": t_prep,
+                                         "parallelism": f"replicas x{world} (pairs per rank)",
+                                         "column_sweeps_per_s": value * P}),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": "k_cheb_step<8,*> (fused Chebyshev step)",
+                         "bytes_per_launch": bytes_step, "avg_launch_ms": avg_step_ms,
+                         "launches_timed": step_n,
+                         "share_of_step": step_ms / max(elapsed_ms * (1 if world == 1 else 1), 1e-9)},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "epilogue_kernels": {"launches": epi_n, "ms": epi_ms},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=200_000)
+    ap.add_argument("--pairs", type=int, default=64)
+    ap.add_argument("--sweeps", type=int, default=200)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-sweeps", type=int, default=1)
+    ap.add_argument("--ref-sweeps", type=int, default=1)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_engine(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -25,6 +25,7 @@
 // a sum and goes through fixed-order per-CTA partials + a fixed-order finalise (deterministic).
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -88,6 +89,7 @@ __device__ __forceinline__ void st_vec(double* p, const double (&v)[VEC]) {
 struct ColState {
   // per column (Bpad entries each)
   int* active;                 // nullable
+  int* gactive;                // active columns per group (nullable)
   unsigned long long* cmin;    // min of the apply output
   unsigned long long* cmax;    // max |next T_0|
   double* thr;                 // positivity threshold of the current apply
@@ -122,12 +124,7 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step(const StepArgs A) {
   const int tile = blockIdx.x / A.Gl;
   const int g = A.g0 + blockIdx.x % A.Gl;
   const int* act = A.cs.active;
-  if (act) {
-    bool any = false;
-#pragma unroll
-    for (int c = 0; c < GW; ++c) any |= act[g * GW + c] != 0;
-    if (!any) return;
-  }
+  if (A.cs.gactive && A.cs.gactive[g] == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = lane / LPR, q = lane % LPR;
   const int row = tile * L::ROWS + warp * RPW + sub;
@@ -138,32 +135,74 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step(const StepArgs A) {
   double y[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) y[e] = 0.0;
-  if (valid) {
-    int p = __ldg(A.offs + row);
-    const int pe = __ldg(A.offs + row + 1);
-    for (; p + 4 <= pe; p += 4) {
-      int cc[4];
-      double vv[4];
-      double xx[4][VEC];
+  if constexpr (LPR == 1) {
+    if (valid) {
+      int p = __ldg(A.offs + row);
+      const int pe = __ldg(A.offs + row + 1);
+      for (; p + 4 <= pe; p += 4) {
+        int cc[4];
+        double vv[4];
+        double xx[4][VEC];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        cc[u] = __ldg(A.cols + p + u);
-        vv[u] = __ldg(A.vals + p + u);
+        for (int u = 0; u < 4; ++u) {
+          cc[u] = __ldg(A.cols + p + u);
+          vv[u] = __ldg(A.vals + p + u);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ld_vec<VEC>(Tp + (size_t)cc[u] * GW, xx[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) y[e] = fma(vv[u], xx[u][e], y[e]);
       }
+      for (; p < pe; ++p) {
+        const int c = __ldg(A.cols + p);
+        const double v = __ldg(A.vals + p);
+        double x[VEC];
+        ld_vec<VEC>(Tp + (size_t)c * GW, x);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) ld_vec<VEC>(Tp + (size_t)cc[u] * GW, xx[u]);
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) y[e] = fma(vv[u], xx[u][e], y[e]);
+        for (int e = 0; e < VEC; ++e) y[e] = fma(v, x[e], y[e]);
+      }
     }
-    for (; p < pe; ++p) {
-      const int c = __ldg(A.cols + p);
-      const double v = __ldg(A.vals + p);
-      double x[VEC];
-      ld_vec<VEC>(Tp + (size_t)c * GW, x);
+  } else {
+    // the LPR lanes of a row load LPR consecutive (col, val) entries with one coalesced access
+    // and broadcast them by shuffle; the fma chain still runs in CSR order.
+    const unsigned mask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
+    const int pb = valid ? __ldg(A.offs + row) : 0;
+    const int pe = valid ? __ldg(A.offs + row + 1) : 0;
+    for (int p0 = pb; p0 < pe; p0 += LPR) {
+      int myc = 0;
+      double myv = 0.0;
+      if (p0 + q < pe) {
+        myc = __ldg(A.cols + p0 + q);
+        myv = __ldg(A.vals + p0 + q);
+      }
+      const int cnt = min(LPR, pe - p0);
+      int u = 0;
+      for (; u + 4 <= cnt; u += 4) {
+        int cc[4];
+        double vv[4];
+        double xx[4][VEC];
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) y[e] = fma(v, x[e], y[e]);
+        for (int j = 0; j < 4; ++j) {
+          cc[j] = __shfl_sync(mask, myc, u + j, LPR);
+          vv[j] = __shfl_sync(mask, myv, u + j, LPR);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ld_vec<VEC>(Tp + (size_t)cc[j] * GW, xx[j]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) y[e] = fma(vv[j], xx[j][e], y[e]);
+      }
+      for (; u < cnt; ++u) {
+        const int c = __shfl_sync(mask, myc, u, LPR);
+        const double v = __shfl_sync(mask, myv, u, LPR);
+        double x[VEC];
+        ld_vec<VEC>(Tp + (size_t)c * GW, x);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) y[e] = fma(v, x[e], y[e]);
+      }
     }
   }
   const size_t idx = gbase + (size_t)row * GW;
@@ -322,6 +361,8 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const FinArgs F) {
 // ---- Sinkhorn control (transport.cpp:184-226), one thread, columns in pair order ------------
 struct CtlArgs {
   int* active;
+  int* gactive;
+  int GW;
   const double* errcol;
   int* iters;
   int* conv;
@@ -357,10 +398,14 @@ __global__ void k_sk_control(const CtlArgs C) {
       ++na;
     } else {
       C.active[c] = 0;
+      C.gactive[c / C.GW] -= 1;
     }
   }
   if (s == C.max_iter) {
-    for (int c = 0; c < C.P; ++c) C.active[c] = 0;
+    for (int c = 0; c < C.P; ++c) {
+      if (C.active[c]) C.gactive[c / C.GW] -= 1;
+      C.active[c] = 0;
+    }
     na = 0;
   }
   st->n_active = na;
@@ -369,7 +414,7 @@ __global__ void k_sk_control(const CtlArgs C) {
 // ---- layout conversion -------------------------------------------------------------------
 // column-major (width contiguous n-vectors) <-> grouped row-major (G x n x GW)
 __global__ void k_pack(const double* __restrict__ src, double* __restrict__ dst, int n, int width,
-                       int GW, int G, double fill) {
+                       int GW, int G, double fill, const int* __restrict__ order) {
   const int64_t total = (int64_t)G * n * GW;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -378,18 +423,20 @@ __global__ void k_pack(const double* __restrict__ src, double* __restrict__ dst,
     const int i = (int)(r % n);
     const int g = (int)(r / n);
     const int col = g * GW + c;
-    dst[e] = col < width ? (src ? src[(size_t)col * n + i] : fill) : 0.0;
+    const int o = order ? order[i] : i;
+    dst[e] = col < width ? (src ? src[(size_t)col * n + o] : fill) : 0.0;
   }
 }
 
 __global__ void k_unpack(const double* __restrict__ src, double* __restrict__ dst, int n,
                          int width, int GW, const double* __restrict__ alt,
-                         const int* __restrict__ sel) {
+                         const int* __restrict__ sel, const int* __restrict__ newpos) {
   const int64_t total = (int64_t)width * n;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int col = (int)(e / n);
-    const int i = (int)(e % n);
+    const int i0 = (int)(e % n);
+    const int i = newpos ? newpos[i0] : i0;
     const int g = col / GW, c = col % GW;
     const size_t idx = ((size_t)g * n + i) * GW + c;
     const double* s = (alt && sel && (sel[col] & 1)) ? alt : src;
@@ -667,6 +714,12 @@ __global__ void k_fill_key(unsigned long long* x, int n, unsigned long long v) {
   if (i < n) x[i] = v;
 }
 
+__global__ void k_gather(const double* __restrict__ src, const int* __restrict__ order, int n,
+                         double* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[order[i]];
+}
+
 __global__ void k_scale_vals(double* v, int64_t nnz, double scale) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e < nnz) v[e] = v[e] * scale;
@@ -678,15 +731,18 @@ inline unsigned grid_for(int64_t work, int threads = kThreads) {
   return (unsigned)(b < 1 ? 1 : b);
 }
 
+// Columns per group: the next power of two >= B, at most 64 (one warp per 512-byte row).
 int choose_gw(int width) {
-  if (width >= 8) return 8;
-  if (width >= 4) return 4;
-  if (width >= 2) return 2;
-  return 1;
+  int g = 1;
+  while (g < width && g < 64) g <<= 1;
+  return g;
 }
 
 int rows_per_cta(int gw) {
   switch (gw) {
+    case 64: return Lay<64>::ROWS;
+    case 32: return Lay<32>::ROWS;
+    case 16: return Lay<16>::ROWS;
     case 8: return Lay<8>::ROWS;
     case 4: return Lay<4>::ROWS;
     case 2: return Lay<2>::ROWS;
@@ -708,6 +764,9 @@ void launch_step_gw(const StepArgs& A, int mode, cudaStream_t s) {
 void launch_step(gs_ctx* ctx, int gw, const StepArgs& A, int mode) {
   gs_launch_begin(ctx, 0);
   switch (gw) {
+    case 64: launch_step_gw<64>(A, mode, ctx->stream); break;
+    case 32: launch_step_gw<32>(A, mode, ctx->stream); break;
+    case 16: launch_step_gw<16>(A, mode, ctx->stream); break;
     case 8: launch_step_gw<8>(A, mode, ctx->stream); break;
     case 4: launch_step_gw<4>(A, mode, ctx->stream); break;
     case 2: launch_step_gw<2>(A, mode, ctx->stream); break;
@@ -722,7 +781,7 @@ struct Work {
   DevBuf<double> T[2], acc;
   DevBuf<unsigned long long> cmin, cmax;
   DevBuf<double> thr, errcol, part_err;
-  DevBuf<int> active;
+  DevBuf<int> active, gactive;
   DevBuf<gs_status> status;
   int init(gs_ctx* ctx, int n_, int B_, bool want_err) {
     cudaStream_t s = ctx->stream;
@@ -742,6 +801,13 @@ struct Work {
     GS_CUDA(ctx, errcol.alloc(Bpad, s));
     GS_CUDA(ctx, part_err.alloc(want_err ? (size_t)tiles * Bpad : 1, s));
     GS_CUDA(ctx, active.alloc(Bpad, s));
+    GS_CUDA(ctx, gactive.alloc(G, s));
+    {
+      std::vector<int> ga(G);
+      for (int g = 0; g < G; ++g) ga[g] = std::min(GW, B - g * GW);
+      GS_CUDA(ctx, cudaMemcpyAsync(gactive.get(), ga.data(), G * sizeof(int), cudaMemcpyHostToDevice, s));
+      GS_CUDA(ctx, cudaStreamSynchronize(s));
+    }
     GS_CUDA(ctx, status.alloc(1, s));
     GS_CUDA(ctx, cudaMemsetAsync(status.get(), 0, sizeof(gs_status), s));
     GS_CUDA(ctx, cudaMemsetAsync(thr.get(), 0, Bpad * sizeof(double), s));
@@ -753,6 +819,7 @@ struct Work {
   ColState cs() {
     ColState c;
     c.active = active.get();
+    c.gactive = gactive.get();
     c.cmin = cmin.get();
     c.cmax = cmax.get();
     c.thr = thr.get();
@@ -767,7 +834,7 @@ struct Work {
 int run_apply(gs_ctx* ctx, const gs_filter* f, Work& w, int a0, int mode, const double* a,
               const double* M, const double* Vcur, double* Wout, bool use_active,
               bool use_status) {
-  const gs_graph* S = f->scaled;
+  const gs_graph* S = f->perm;
   const int K = f->degree;
   StepArgs A{};
   A.offs = S->offs;
@@ -782,7 +849,10 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work& w, int a0, int mode, const 
   A.b0h = f->coeffs[0] / 2.0;
   A.status = use_status ? w.status.get() : nullptr;
   A.cs = w.cs();
-  if (!use_active) A.cs.active = nullptr;
+  if (!use_active) {
+    A.cs.active = nullptr;
+    A.cs.gactive = nullptr;
+  }
   A.a = a;
   A.M = M;
   A.Vcur = Vcur;
@@ -855,6 +925,14 @@ extern "C" int gs_filter_create(gs_ctx* ctx, const gs_graph* L, int kind, double
       rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "coefficient allocation failed");
   }
   if (!rc) rc = gs_coefficients_impl(ctx, f->t_eff, degree, f->d_coeffs, f->coeffs.data());
+  if (!rc) {
+    const int n = L->n;
+    if (cudaMalloc((void**)&f->order, ((size_t)n + 1) * sizeof(int)) != cudaSuccess ||
+        cudaMalloc((void**)&f->newpos, ((size_t)n + 1) * sizeof(int)) != cudaSuccess)
+      rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "permutation allocation failed");
+  }
+  if (!rc) rc = gs_bfs_order(ctx, f->scaled, f->order, f->newpos);
+  if (!rc) rc = gs_permute_graph(ctx, f->scaled, f->order, f->newpos, &f->perm);
   if (rc) {
     gs_filter_destroy(f);
     return rc;
@@ -866,6 +944,9 @@ extern "C" int gs_filter_create(gs_ctx* ctx, const gs_graph* L, int kind, double
 extern "C" void gs_filter_destroy(gs_filter* f) {
   if (!f) return;
   gs_graph_destroy(f->scaled);
+  gs_graph_destroy(f->perm);
+  cudaFree(f->order);
+  cudaFree(f->newpos);
   cudaFree(f->d_coeffs);
   delete f;
 }
@@ -925,11 +1006,11 @@ extern "C" int gs_filter_apply(gs_ctx* ctx, const gs_filter* f, const double* X,
     dY = yout.get();
   }
   gs_launch_begin(ctx, 1);
-  k_pack<<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, 0.0);
+  k_pack<<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, 0.0, f->order);
   gs_launch_end(ctx, 1);
   run_apply(ctx, f, w, 0, MODE_NONE, nullptr, nullptr, nullptr, nullptr, false, false);
   gs_launch_begin(ctx, 1);
-  k_unpack<<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.acc.get(), dY, n, width, w.GW, nullptr, nullptr);
+  k_unpack<<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.acc.get(), dY, n, width, w.GW, nullptr, nullptr, f->newpos);
   gs_launch_end(ctx, 1);
   GS_TRY(finish_out(ctx, yout, Y, (size_t)width * n, mem));
   GS_CUDA(ctx, cudaStreamSynchronize(s));
@@ -953,7 +1034,7 @@ extern "C" int gs_graph_multiply(gs_ctx* ctx, const gs_graph* g, const double* x
     dY = yout.get();
   }
   gs_launch_begin(ctx, 1);
-  k_pack<<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, 0.0);
+  k_pack<<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, 0.0, nullptr);
   gs_launch_end(ctx, 1);
   StepArgs A{};
   A.offs = g->offs;
@@ -968,7 +1049,7 @@ extern "C" int gs_graph_multiply(gs_ctx* ctx, const gs_graph* g, const double* x
   A.Tout = w.T[1].get();
   launch_step(ctx, w.GW, A, MODE_NONE);
   gs_launch_begin(ctx, 1);
-  k_unpack<<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.T[1].get(), dY, n, width, w.GW, nullptr, nullptr);
+  k_unpack<<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.T[1].get(), dY, n, width, w.GW, nullptr, nullptr, nullptr);
   gs_launch_end(ctx, 1);
   GS_TRY(finish_out(ctx, yout, y, (size_t)width * n, mem));
   GS_CUDA(ctx, cudaStreamSynchronize(s));
@@ -1047,6 +1128,7 @@ extern "C" int gs_sinkhorn(gs_ctx* ctx, const gs_filter* f, const double* a, con
   GS_TRY(stage_in(ctx, bmu, mus, (size_t)P * n, mem, &dmu));
   GS_TRY(stage_in(ctx, bnu, nus, (size_t)P * n, mem, &dnu));
   GS_TRY(stage_in(ctx, ba, a, (size_t)n, mem, &da));
+  const double* da_user = da;
   {
     std::vector<double> smu, snu;
     std::vector<int> fmu, gmu, fnu, gnu;
@@ -1057,7 +1139,7 @@ extern "C" int gs_sinkhorn(gs_ctx* ctx, const gs_filter* f, const double* a, con
       GS_TRY(check_distribution(ctx, n, smu[p], fmu[p], gmu[p]));
       GS_TRY(check_distribution(ctx, n, snu[p], fnu[p], gnu[p]));
       if (bad_a < 0) {
-        const int rc = check_weights(ctx, da, n);
+        const int rc = check_weights(ctx, da_user, n);
         if (rc) return rc;
         bad_a = 0;
       }
@@ -1065,6 +1147,13 @@ extern "C" int gs_sinkhorn(gs_ctx* ctx, const gs_filter* f, const double* a, con
       if (max_iter < 1) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "max_iter must be >= 1");
     }
   }
+  // vertex weights in the filter's locality order
+  DevBuf<double> aperm;
+  GS_CUDA(ctx, aperm.alloc(n, s));
+  gs_launch_begin(ctx, 1);
+  k_gather<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(da_user, f->order, n, aperm.get());
+  gs_launch_end(ctx, 1);
+  da = aperm.get();
   // ---- workspace -----------------------------------------------------------------------------
   Work w;
   GS_TRY(w.init(ctx, n, P, true));
@@ -1098,8 +1187,8 @@ extern "C" int gs_sinkhorn(gs_ctx* ctx, const gs_filter* f, const double* a, con
     GS_CUDA(ctx, cudaMemcpyAsync(errv.get(), inf.data(), w.Bpad * sizeof(double), cudaMemcpyHostToDevice, s));
   }
   gs_launch_begin(ctx, 1);
-  k_pack<<<grid_for((int64_t)len), kThreads, 0, s>>>(dmu, M.get(), n, P, w.GW, w.G, 0.0);
-  k_pack<<<grid_for((int64_t)len), kThreads, 0, s>>>(dnu, N.get(), n, P, w.GW, w.G, 0.0);
+  k_pack<<<grid_for((int64_t)len), kThreads, 0, s>>>(dmu, M.get(), n, P, w.GW, w.G, 0.0, f->order);
+  k_pack<<<grid_for((int64_t)len), kThreads, 0, s>>>(dnu, N.get(), n, P, w.GW, w.G, 0.0, f->order);
   k_sk_init<<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.T[0].get(), n, w.GW, w.G, P, w.cmax.get());
   gs_launch_end(ctx, 1);
   run_finalize(ctx, w, 0, 1, 0, ERRC_KERNEL_NOT_POSITIVE + 1, true);  // threshold of the first apply
@@ -1115,6 +1204,8 @@ extern "C" int gs_sinkhorn(gs_ctx* ctx, const gs_filter* f, const double* a, con
   bool ev_used[2] = {false, false};
   CtlArgs C{};
   C.active = w.active.get();
+  C.gactive = w.gactive.get();
+  C.GW = w.GW;
   C.errcol = w.errcol.get();
   C.iters = iters.get();
   C.conv = conv.get();
@@ -1190,13 +1281,13 @@ extern "C" int gs_sinkhorn(gs_ctx* ctx, const gs_filter* f, const double* a, con
   }
   if (out_v) {
     gs_launch_begin(ctx, 1);
-    k_unpack<<<grid_for((int64_t)P * n), kThreads, 0, s>>>(V[0].get(), dv, n, P, w.GW, V[1].get(), final_sweep.get());
+    k_unpack<<<grid_for((int64_t)P * n), kThreads, 0, s>>>(V[0].get(), dv, n, P, w.GW, V[1].get(), final_sweep.get(), f->newpos);
     gs_launch_end(ctx, 1);
     if (mem != GS_MEM_DEVICE) GS_TRY(finish_out(ctx, ov, out_v, (size_t)P * n, mem));
   }
   if (out_w) {
     gs_launch_begin(ctx, 1);
-    k_unpack<<<grid_for((int64_t)P * n), kThreads, 0, s>>>(W.get(), dw, n, P, w.GW, nullptr, nullptr);
+    k_unpack<<<grid_for((int64_t)P * n), kThreads, 0, s>>>(W.get(), dw, n, P, w.GW, nullptr, nullptr, f->newpos);
     gs_launch_end(ctx, 1);
     if (mem != GS_MEM_DEVICE) GS_TRY(finish_out(ctx, ow, out_w, (size_t)P * n, mem));
   }
@@ -1257,6 +1348,12 @@ extern "C" int gs_barycenter(gs_ctx* ctx, const gs_filter* f, const double* a,
   }
   GS_TRY(check_weights(ctx, da, n));
   if (!(tol > 0.0 && max_iter >= 1)) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "bad parameters");
+  DevBuf<double> aperm;
+  GS_CUDA(ctx, aperm.alloc(n, s));
+  gs_launch_begin(ctx, 1);
+  k_gather<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(da, f->order, n, aperm.get());
+  gs_launch_end(ctx, 1);
+  da = aperm.get();
 
   Work w;
   GS_TRY(w.init(ctx, n, m, true));
@@ -1290,7 +1387,7 @@ extern "C" int gs_barycenter(gs_ctx* ctx, const gs_filter* f, const double* a,
   }
   gs_launch_begin(ctx, 1);
   k_fill<<<grid_for(n), kThreads, 0, s>>>(bary.get(), n, 1.0 / n);
-  k_pack<<<grid_for((int64_t)len), kThreads, 0, s>>>(dmem, Mb.get(), n, m, w.GW, w.G, 0.0);
+  k_pack<<<grid_for((int64_t)len), kThreads, 0, s>>>(dmem, Mb.get(), n, m, w.GW, w.G, 0.0, f->order);
   k_sk_init<<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.T[0].get(), n, w.GW, w.G, m, w.cmax.get());
   gs_launch_end(ctx, 1);
   run_finalize(ctx, w, 0, 1, 0, 0, false);
@@ -1377,7 +1474,14 @@ extern "C" int gs_barycenter(gs_ctx* ctx, const gs_filter* f, const double* a,
     k_scale_div<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(bary.get(), mass.get(), n);
     gs_launch_end(ctx, 1);
   }
-  GS_TRY(gs_copy_out(ctx, out_bary, bary.get(), (size_t)n * sizeof(double), mem));
+  {
+    DevBuf<double> bu;
+    GS_CUDA(ctx, bu.alloc(n, s));
+    gs_launch_begin(ctx, 1);
+    k_gather<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(bary.get(), f->newpos, n, bu.get());
+    gs_launch_end(ctx, 1);
+    GS_TRY(gs_copy_out(ctx, out_bary, bu.get(), (size_t)n * sizeof(double), mem));
+  }
   // final V lives in V[iters & 1] (V_s of the last sweep), W is single-buffered
   DevBuf<int> sel;
   GS_CUDA(ctx, sel.alloc(m, s));
@@ -1396,13 +1500,13 @@ extern "C" int gs_barycenter(gs_ctx* ctx, const gs_filter* f, const double* a,
   }
   if (out_V) {
     gs_launch_begin(ctx, 1);
-    k_unpack<<<grid_for((int64_t)m * n), kThreads, 0, s>>>(V[0].get(), dv, n, m, w.GW, V[1].get(), sel.get());
+    k_unpack<<<grid_for((int64_t)m * n), kThreads, 0, s>>>(V[0].get(), dv, n, m, w.GW, V[1].get(), sel.get(), f->newpos);
     gs_launch_end(ctx, 1);
     if (mem != GS_MEM_DEVICE) GS_TRY(finish_out(ctx, ov, out_V, (size_t)m * n, mem));
   }
   if (out_W) {
     gs_launch_begin(ctx, 1);
-    k_unpack<<<grid_for((int64_t)m * n), kThreads, 0, s>>>(W.get(), dw, n, m, w.GW, nullptr, nullptr);
+    k_unpack<<<grid_for((int64_t)m * n), kThreads, 0, s>>>(W.get(), dw, n, m, w.GW, nullptr, nullptr, f->newpos);
     gs_launch_end(ctx, 1);
     if (mem != GS_MEM_DEVICE) GS_TRY(finish_out(ctx, ow, out_W, (size_t)m * n, mem));
   }

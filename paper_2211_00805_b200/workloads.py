@@ -1,0 +1,125 @@
+"""Seeded synthetic inputs for the BASELINE.json configs (host-side input generation).
+
+All draws go through geosink::Rng semantics (rng.hpp:13-68) so a config is reproducible from
+its seed on any host. Decisions recorded in DESIGN.md ("Workloads"):
+  * swiss roll: per point draw s ~ U(1.5pi, 4.5pi), h ~ U(0, 20), then three N(0, 0.1^2)
+    noise terms, in that order; x = (s cos s + nx, h + ny, s sin s + nz);
+  * graph: symmetrised k-NN, Gaussian weights exp(-d^2/sigma^2), sigma = median eps_k;
+  * bump "width" = Gaussian standard deviation; mixtures are equal-weight sums of bumps;
+  * Gaussian mixtures in R^d: means ~ N(0, 5^2 I), isotropic sigma = 1, balanced components
+    (point i belongs to component i mod C);
+  * cluster-subset members: uniform over a random `frac` subset of the points of the chosen
+    clusters.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from .rng import Rng
+
+TWO_PI = 2.0 * math.pi
+
+
+def _normalise(w: np.ndarray) -> np.ndarray:
+    w = np.array(w, np.float64)
+    w /= w.sum()
+    w /= w.sum()
+    return w
+
+
+@dataclass
+class SwissRoll:
+    points: np.ndarray  # n x 3
+    s: np.ndarray
+    h: np.ndarray
+
+
+def swiss_roll(n: int, seed: int, noise: float = 0.1) -> SwissRoll:
+    raw = Rng(seed).pattern(5 * n, [("u", 1.5 * math.pi, 4.5 * math.pi), ("u", 0.0, 20.0),
+                                    ("n", 0.0, noise), ("n", 0.0, noise), ("n", 0.0, noise)])
+    raw = raw.reshape(n, 5)
+    s, h = raw[:, 0].copy(), raw[:, 1].copy()
+    pts = np.empty((n, 3))
+    pts[:, 0] = s * np.cos(s) + raw[:, 2]
+    pts[:, 1] = h + raw[:, 3]
+    pts[:, 2] = s * np.sin(s) + raw[:, 4]
+    return SwissRoll(pts, s, h)
+
+
+def bump_in_s(roll: SwissRoll, centre: float, width: float) -> np.ndarray:
+    """Config 0/3: normalised Gaussian bump in the roll parameter s."""
+    return _normalise(np.exp(-((roll.s - centre) ** 2) / (2.0 * width * width)))
+
+
+def bump_mixture_pairs(roll: SwissRoll, pairs: int, seed: int, bumps: int = 3,
+                       wmin: float = 0.3, wmax: float = 1.0):
+    """Config 1: `pairs` (source, target) distributions, each a normalised equal-weight mixture of
+    `bumps` Gaussian bumps in (s, h) with centres s ~ U(1.5pi, 4.5pi), h ~ U(0, 20) and widths
+    ~ U(wmin, wmax). Returns (mus, nus) shaped (pairs, n)."""
+    rng = Rng(seed)
+    out = np.empty((2 * pairs, roll.s.size))
+    for q in range(2 * pairs):
+        dens = np.zeros(roll.s.size)
+        for _ in range(bumps):
+            sc = rng.uniform(1.5 * math.pi, 4.5 * math.pi)
+            hc = rng.uniform(0.0, 20.0)
+            w = rng.uniform(wmin, wmax)
+            dens += np.exp(-((roll.s - sc) ** 2 + (roll.h - hc) ** 2) / (2.0 * w * w))
+        out[q] = _normalise(dens)
+    return out[0::2].copy(), out[1::2].copy()
+
+
+@dataclass
+class Mixture:
+    points: np.ndarray  # n x d
+    labels: np.ndarray  # n
+
+
+def gaussian_mixture(n: int, d: int, components: int, seed: int, mean_scale: float = 5.0,
+                     sigma: float = 1.0) -> Mixture:
+    rng = Rng(seed)
+    means = rng.pattern(components * d, [("n", 0.0, mean_scale)]).reshape(components, d)
+    labels = (np.arange(n) % components).astype(np.int32)
+    noise = rng.pattern(n * d, [("n", 0.0, sigma)]).reshape(n, d)
+    return Mixture(means[labels] + noise, labels)
+
+
+def cluster_subset_members(mix: Mixture, members: int, clusters_each: int, frac: float, seed: int,
+                           cluster_pool=None) -> np.ndarray:
+    """Configs 2/4: each member uniform over a random `frac` subset of the points of
+    `clusters_each` random clusters drawn from `cluster_pool` (default: all)."""
+    rng = Rng(seed)
+    pool = np.arange(mix.labels.max() + 1) if cluster_pool is None else np.asarray(cluster_pool)
+    n = mix.labels.size
+    out = np.zeros((members, n))
+    for m in range(members):
+        chosen = []
+        avail = list(pool)
+        for _ in range(min(clusters_each, len(avail))):
+            chosen.append(avail.pop(rng.below(len(avail))))
+        idx = np.flatnonzero(np.isin(mix.labels, chosen))
+        keep = rng.pattern(idx.size, [("u", 0.0, 1.0)]) < frac
+        sel = idx[keep] if keep.any() else idx[:1]
+        out[m, sel] = 1.0
+        out[m] = _normalise(out[m])
+    return out
+
+
+@dataclass
+class Config1:
+    roll: SwissRoll
+    mus: np.ndarray
+    nus: np.ndarray
+    k: int = 10
+    t: float = 1.0
+    degree: int = 30
+    sweeps: int = 200
+
+
+def config1(n: int = 200_000, pairs: int = 64, seed: int = 1, pair_seed: int = 2) -> Config1:
+    roll = swiss_roll(n, seed)
+    mus, nus = bump_mixture_pairs(roll, pairs, pair_seed)
+    return Config1(roll, mus, nus)
