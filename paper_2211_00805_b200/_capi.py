@@ -92,7 +92,7 @@ def load(path: str | None = None):
     global _LIB
     if _LIB is not None:
         return _LIB
-    path = path or LIB_PATH
+    path = path or os.environ.get("GS_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise EngineUnavailable(
             f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")

@@ -29,16 +29,20 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile every source and link lib/libgeosink_b200.so (or `out`, for tuning variants
+    built with extra -D defines)."""
+    lib = out or LIB
+    if not force and out is None and not _stale():
         return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    tag = "" if out is None else "_" + os.path.basename(out).replace(".so", "")
     objs = []
     procs = []
     for src in SOURCES:
-        obj = os.path.join(PKG, "lib", src.rsplit(".", 1)[0] + ".o")
-        cmd = ["nvcc", *NVCC_FLAGS, "-dc" if False else "-c", "-I", os.path.join(ROOT, "include"),
-               "-o", obj, os.path.join(CSRC, src)]
+        obj = os.path.join(PKG, "lib", src.rsplit(".", 1)[0] + tag + ".o")
+        cmd = ["nvcc", *NVCC_FLAGS, *["-D" + d for d in defines], "-c", "-I",
+               os.path.join(ROOT, "include"), "-o", obj, os.path.join(CSRC, src)]
         cmd = [c for c in cmd if c != "-shared"]
         procs.append((subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT), cmd))
         objs.append(obj)
@@ -49,14 +53,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if p.returncode != 0:
             sys.stderr.write(out.decode())
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    link = ["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs]
+    link = ["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib, *objs]
     subprocess.run(link, check=True)
-    with open(os.path.join(PKG, "lib", "ptxas.log"), "w") as f:
+    with open(os.path.join(PKG, "lib", "ptxas" + tag + ".log"), "w") as f:
         f.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs,
+                out=outs[0] if outs else None))

@@ -34,6 +34,14 @@
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef GS_ROWS_PER_CTA
+#define GS_ROWS_PER_CTA 4
+#endif
+constexpr int kRowsPerCta = GS_ROWS_PER_CTA;  // row blocks per CTA (L1 reuse across a block)
+#ifndef GS_EARLY_LOADS
+#define GS_EARLY_LOADS 0
+#endif
+constexpr bool kEarlyLoads = GS_EARLY_LOADS != 0;
 
 enum StepMode { MODE_NONE = 0, MODE_SK_PSI = 1, MODE_SK_PHI = 2, MODE_BARY_PSI = 3 };
 
@@ -116,22 +124,38 @@ struct StepArgs {
   double* Wout;         // PSI: W; PHI: V of the next sweep
 };
 
+// One row of one Chebyshev step for the calling lane group; epilogue partials accumulate in
+// mn/mx/er. Own-row streaming loads (T_{k-1}[i], T_{k-2}[i], acc[i], epilogue operands) are issued
+// before the neighbour gathers so HBM reads overlap the gather latency.
 template <int GW, int MODE>
-__global__ void __launch_bounds__(kThreads) k_cheb_step(const StepArgs A) {
+__device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int sub, int q,
+                                         double (&mn)[Lay<GW>::VEC], double (&mx)[Lay<GW>::VEC],
+                                         double (&er)[Lay<GW>::VEC]) {
   using L = Lay<GW>;
-  constexpr int VEC = L::VEC, LPR = L::LPR, RPW = L::RPW;
-  if (A.status && (A.status->error || A.status->done)) return;
-  const int tile = blockIdx.x / A.Gl;
-  const int g = A.g0 + blockIdx.x % A.Gl;
-  const int* act = A.cs.active;
-  if (A.cs.gactive && A.cs.gactive[g] == 0) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int sub = lane / LPR, q = lane % LPR;
-  const int row = tile * L::ROWS + warp * RPW + sub;
+  constexpr int VEC = L::VEC, LPR = L::LPR;
   const bool valid = row < A.n;
   const size_t gbase = (size_t)g * A.n * GW + q * VEC;
+  const size_t idx = gbase + (size_t)(valid ? row : 0) * GW;
   const double* __restrict__ Tp = A.Tprev + gbase;
-
+  // ---- own-row loads (before the gathers when GS_EARLY_LOADS) ------------------------------
+  double tp[VEC], t2[VEC], a0[VEC], op1[VEC], op2[VEC];
+  double ai = 0.0;
+  auto own_loads = [&]() {
+    if (valid && A.k != 0) {
+      ld_vec<VEC>(A.Tprev + idx, tp);
+      if (A.k >= 2) {
+        ld_vec_rw<VEC>(A.Tout + idx, t2);
+        ld_vec_rw<VEC>(A.acc + idx, a0);
+      }
+      if constexpr (MODE == MODE_SK_PSI || MODE == MODE_SK_PHI) {
+        ld_vec<VEC>(A.M + idx, op1);
+        ai = __ldg(A.a + row);
+      }
+      if constexpr (MODE == MODE_SK_PHI) ld_vec_rw<VEC>(A.Vcur + idx, op2);
+    }
+  };
+  if constexpr (kEarlyLoads) own_loads();
+  // ---- y = L_s T_{k-1} (row) ------------------------------------------------------------------
   double y[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) y[e] = 0.0;
@@ -205,85 +229,94 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step(const StepArgs A) {
       }
     }
   }
-  const size_t idx = gbase + (size_t)row * GW;
+  if (!valid) return;
   if (A.k == 0) {  // plain SpMM (sparse.cpp:85-99)
-    if (valid) st_vec<VEC>(A.Tout + idx, y);
+    st_vec<VEC>(A.Tout + idx, y);
     return;
   }
+  if constexpr (!kEarlyLoads) own_loads();
+  // ---- recurrence (heat.cpp:121-130) ----------------------------------------------------------
   double t[VEC], ac[VEC];
-  if (valid) {
-    double tp[VEC];
-    ld_vec<VEC>(A.Tprev + idx, tp);
-    if (A.k == 1) {
+  if (A.k == 1) {
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) {
-        t[e] = y[e] - tp[e];
-        ac[e] = fma(A.bk, t[e], A.b0h * tp[e]);
-      }
-    } else {
-      double t2[VEC], a0[VEC];
-      ld_vec_rw<VEC>(A.Tout + idx, t2);
-      ld_vec_rw<VEC>(A.acc + idx, a0);
+    for (int e = 0; e < VEC; ++e) {
+      t[e] = y[e] - tp[e];
+      ac[e] = fma(A.bk, t[e], A.b0h * tp[e]);
+    }
+  } else {
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) {
-        t[e] = 2.0 * (y[e] - tp[e]) - t2[e];
-        ac[e] = fma(A.bk, t[e], a0[e]);
-      }
+    for (int e = 0; e < VEC; ++e) {
+      t[e] = 2.0 * (y[e] - tp[e]) - t2[e];
+      ac[e] = fma(A.bk, t[e], a0[e]);
     }
   }
   if constexpr (MODE == MODE_NONE) {
-    if (valid) {
-      st_vec<VEC>(A.Tout + idx, t);
+    st_vec<VEC>(A.Tout + idx, t);
+    st_vec<VEC>(A.acc + idx, ac);
+  } else {
+    // ---- fused epilogue of the last step ----------------------------------------------------
+    const int* act = A.cs.active;
+    const int col0 = g * GW + q * VEC;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) mn[e] = fmin(mn[e], ac[e]);
+    if constexpr (MODE == MODE_SK_PSI) {
+      double w[VEC], t0[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        w[e] = op1[e] / fmax(ac[e], GS_FLOOR);      // transport.cpp:180
+        t0[e] = ai * w[e];                          // transport.cpp:172
+        mx[e] = fmax(mx[e], fabs(t0[e]));
+      }
+      st_vec<VEC>(A.Tout + idx, t0);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        if (!act || act[col0 + e]) A.Wout[idx + e] = w[e];
+    } else if constexpr (MODE == MODE_SK_PHI) {
+      double vn[VEC], t0[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        er[e] = er[e] + fabs(op2[e] * ac[e] - op1[e]);  // transport.cpp:184
+        vn[e] = op1[e] / fmax(ac[e], GS_FLOOR);         // transport.cpp:178
+        t0[e] = ai * vn[e];
+        mx[e] = fmax(mx[e], fabs(t0[e]));
+      }
+      st_vec<VEC>(A.Tout + idx, t0);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        if (!act || act[col0 + e]) A.Wout[idx + e] = vn[e];
+    } else {  // MODE_BARY_PSI
       st_vec<VEC>(A.acc + idx, ac);
     }
-    return;
-  } else {
-    // ---- fused epilogue of the last step --------------------------------------------------
-    const int col0 = g * GW + q * VEC;
-    double mn[VEC], mx[VEC], er[VEC];
+  }
+}
+
+// A CTA owns RPC x (8 warps x RPW) consecutive rows of one column group; at each of its RPC
+// iterations the 8 warps cover a contiguous block, so neighbouring gathers share L1 lines.
+#ifndef GS_MIN_BLOCKS
+#define GS_MIN_BLOCKS 1
+#endif
+template <int GW, int MODE, int RPC>
+__global__ void __launch_bounds__(kThreads, GS_MIN_BLOCKS) k_cheb_step(const StepArgs A) {
+  using L = Lay<GW>;
+  constexpr int VEC = L::VEC, LPR = L::LPR, RPW = L::RPW;
+  constexpr int BLOCK_ROWS = (kThreads / 32) * RPW;
+  if (A.status && (A.status->error || A.status->done)) return;
+  const int tile = blockIdx.x / A.Gl;
+  const int g = A.g0 + blockIdx.x % A.Gl;
+  if (A.cs.gactive && A.cs.gactive[g] == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / LPR, q = lane % LPR;
+  double mn[VEC], mx[VEC], er[VEC];
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      mn[e] = INFINITY;
-      mx[e] = 0.0;
-      er[e] = 0.0;
-    }
-    if (valid) {
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) mn[e] = ac[e];
-      if constexpr (MODE == MODE_SK_PSI) {
-        double nu[VEC], w[VEC], t0[VEC];
-        ld_vec<VEC>(A.M + idx, nu);
-        const double ai = __ldg(A.a + row);
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          w[e] = nu[e] / fmax(ac[e], GS_FLOOR);      // transport.cpp:180
-          t0[e] = ai * w[e];                          // transport.cpp:172
-          mx[e] = fabs(t0[e]);
-        }
-        st_vec<VEC>(A.Tout + idx, t0);
-#pragma unroll
-        for (int e = 0; e < VEC; ++e)
-          if (!act || act[col0 + e]) A.Wout[idx + e] = w[e];
-      } else if constexpr (MODE == MODE_SK_PHI) {
-        double mu[VEC], v[VEC], vn[VEC], t0[VEC];
-        ld_vec<VEC>(A.M + idx, mu);
-        ld_vec_rw<VEC>(A.Vcur + idx, v);
-        const double ai = __ldg(A.a + row);
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          er[e] = fabs(v[e] * ac[e] - mu[e]);         // transport.cpp:184
-          vn[e] = mu[e] / fmax(ac[e], GS_FLOOR);      // transport.cpp:178
-          t0[e] = ai * vn[e];
-          mx[e] = fabs(t0[e]);
-        }
-        st_vec<VEC>(A.Tout + idx, t0);
-#pragma unroll
-        for (int e = 0; e < VEC; ++e)
-          if (!act || act[col0 + e]) A.Wout[idx + e] = vn[e];
-      } else {  // MODE_BARY_PSI
-        st_vec<VEC>(A.acc + idx, ac);
-      }
-    }
+  for (int e = 0; e < VEC; ++e) {
+    mn[e] = INFINITY;
+    mx[e] = 0.0;
+    er[e] = 0.0;
+  }
+  const int base = tile * (BLOCK_ROWS * RPC) + warp * RPW + sub;
+#pragma unroll 1
+  for (int j = 0; j < RPC; ++j) cheb_row<GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er);
+  if constexpr (MODE != MODE_NONE) {
     // warp: combine rows with the same column slot (lane bits >= log2(LPR))
 #pragma unroll
     for (int off = LPR; off < 32; off <<= 1) {
@@ -740,24 +773,25 @@ int choose_gw(int width) {
 
 int rows_per_cta(int gw) {
   switch (gw) {
-    case 64: return Lay<64>::ROWS;
-    case 32: return Lay<32>::ROWS;
-    case 16: return Lay<16>::ROWS;
-    case 8: return Lay<8>::ROWS;
-    case 4: return Lay<4>::ROWS;
-    case 2: return Lay<2>::ROWS;
-    default: return Lay<1>::ROWS;
+    case 64: return Lay<64>::ROWS * kRowsPerCta;
+    case 32: return Lay<32>::ROWS * kRowsPerCta;
+    case 16: return Lay<16>::ROWS * kRowsPerCta;
+    case 8: return Lay<8>::ROWS * kRowsPerCta;
+    case 4: return Lay<4>::ROWS * kRowsPerCta;
+    case 2: return Lay<2>::ROWS * kRowsPerCta;
+    default: return Lay<1>::ROWS * kRowsPerCta;
   }
 }
 
 template <int GW>
 void launch_step_gw(const StepArgs& A, int mode, cudaStream_t s) {
+  constexpr int RPC = kRowsPerCta;
   dim3 grid((unsigned)(A.tiles * A.Gl));
   switch (mode) {
-    case MODE_NONE: k_cheb_step<GW, MODE_NONE><<<grid, kThreads, 0, s>>>(A); break;
-    case MODE_SK_PSI: k_cheb_step<GW, MODE_SK_PSI><<<grid, kThreads, 0, s>>>(A); break;
-    case MODE_SK_PHI: k_cheb_step<GW, MODE_SK_PHI><<<grid, kThreads, 0, s>>>(A); break;
-    default: k_cheb_step<GW, MODE_BARY_PSI><<<grid, kThreads, 0, s>>>(A); break;
+    case MODE_NONE: k_cheb_step<GW, MODE_NONE, RPC><<<grid, kThreads, 0, s>>>(A); break;
+    case MODE_SK_PSI: k_cheb_step<GW, MODE_SK_PSI, RPC><<<grid, kThreads, 0, s>>>(A); break;
+    case MODE_SK_PHI: k_cheb_step<GW, MODE_SK_PHI, RPC><<<grid, kThreads, 0, s>>>(A); break;
+    default: k_cheb_step<GW, MODE_BARY_PSI, RPC><<<grid, kThreads, 0, s>>>(A); break;
   }
 }
 

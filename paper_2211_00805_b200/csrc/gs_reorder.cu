@@ -11,6 +11,7 @@
 // and results scattered back through it when unpacked.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <vector>
 
 #include "gs_internal.cuh"
@@ -114,6 +115,49 @@ __global__ void k_perm_fill(const int* __restrict__ offs, const int* __restrict_
   }
 }
 
+// global level of each vertex (component base + BFS level; isolated block last)
+__global__ void k_global_level(const int* level, const int* comp, const long long* base, int n,
+                               int ncomp, int* gl) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = comp[i] >= 0 ? comp[i] : ncomp;
+  gl[i] = (int)(base[c] + level[i]);
+}
+
+__global__ void k_level_keys(const int* gl, int n, unsigned long long* keys) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) keys[i] = ((unsigned long long)(unsigned)gl[i] << 32) | (unsigned)i;
+}
+
+// Cuthill-McKee key of the vertices of global level G: the smallest position among their
+// neighbours on level G-1 (vertices starting a component have none and keep their index order).
+__global__ void k_cm_keys(const unsigned long long* bylevel, int start, int cnt,
+                          const int* __restrict__ offs, const int* __restrict__ cols,
+                          const int* __restrict__ gl, const int* __restrict__ pos, int G,
+                          unsigned long long* keys) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt) return;
+  const int v = (int)(bylevel[start + t] & 0xFFFFFFFFull);
+  unsigned best = 0xFFFFFFFFu;
+  for (int p = offs[v]; p < offs[v + 1]; ++p) {
+    const int u = cols[p];
+    if (gl[u] == G - 1) best = min(best, (unsigned)pos[u]);
+  }
+  keys[t] = ((unsigned long long)best << 32) | (unsigned)v;
+}
+
+__global__ void k_cm_assign(const unsigned long long* sorted, int start, int cnt, int* pos) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < cnt) pos[(int)(sorted[t] & 0xFFFFFFFFull)] = start + t;
+}
+
+__global__ void k_pos_to_order(const int* pos, int n, int* order, int* newpos) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  newpos[i] = pos[i];
+  order[pos[i]] = i;
+}
+
 }  // namespace
 
 // Computes order[new] = old and newpos[old] = new on the device.
@@ -194,21 +238,59 @@ int gs_bfs_order(gs_ctx* ctx, const gs_graph* g, int* d_order, int* d_newpos) {
   for (size_t c = 0; c < depth.size(); ++c) base[c + 1] = base[c] + depth[c];
   const int ncomp = (int)depth.size() - 1;
   DevBuf<long long> dbase;
-  DevBuf<unsigned long long> keys, keys2;
+  DevBuf<unsigned long long> keys, keys2, lk, lk2;
+  DevBuf<int> gl, pos;
   GS_CUDA(ctx, dbase.alloc(base.size(), s));
   GS_CUDA(ctx, keys.alloc(n, s));
   GS_CUDA(ctx, keys2.alloc(n, s));
+  GS_CUDA(ctx, gl.alloc(n, s));
+  GS_CUDA(ctx, pos.alloc(n, s));
   GS_CUDA(ctx, cudaMemcpyAsync(dbase.get(), base.data(), base.size() * sizeof(long long), cudaMemcpyHostToDevice, s));
   gs_launch_begin(ctx, 1);
-  k_order_keys<<<nblk(n), kThreads, 0, s>>>(level.get(), comp.get(), dbase.get(), n, ncomp, keys.get());
+  k_global_level<<<nblk(n), kThreads, 0, s>>>(level.get(), comp.get(), dbase.get(), n, ncomp, gl.get());
   gs_launch_end(ctx, 1);
+  gs_launch_begin(ctx, 1);
+  k_level_keys<<<nblk(n), kThreads, 0, s>>>(gl.get(), n, keys.get());
+  gs_launch_end(ctx, 1);
+  {
+    size_t tb = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tb, keys.get(), keys2.get(), n, 0, 64, s);
+    DevBuf<unsigned char> tmp;
+    GS_CUDA(ctx, tmp.alloc(tb, s));
+    cub::DeviceRadixSort::SortKeys(tmp.get(), tb, keys.get(), keys2.get(), n, 0, 64, s);
+  }
+  // level start offsets (host): histogram of global levels
+  const int nlev = (int)base.back();
+  std::vector<int> hgl(n), cnt(nlev + 1, 0);
+  GS_CUDA(ctx, cudaMemcpyAsync(hgl.data(), gl.get(), n * sizeof(int), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  for (int i = 0; i < n; ++i) cnt[hgl[i]]++;
+  std::vector<int> lstart(nlev + 1, 0);
+  for (int G = 0; G < nlev; ++G) lstart[G + 1] = lstart[G] + cnt[G];
+  int maxcnt = 1;
+  for (int G = 0; G < nlev; ++G) maxcnt = std::max(maxcnt, cnt[G]);
+  GS_CUDA(ctx, lk.alloc(maxcnt, s));
+  GS_CUDA(ctx, lk2.alloc(maxcnt, s));
   size_t tb = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, tb, keys.get(), keys2.get(), n, 0, 64, s);
+  cub::DeviceRadixSort::SortKeys(nullptr, tb, lk.get(), lk2.get(), maxcnt, 0, 64, s);
   DevBuf<unsigned char> tmp;
   GS_CUDA(ctx, tmp.alloc(tb, s));
-  cub::DeviceRadixSort::SortKeys(tmp.get(), tb, keys.get(), keys2.get(), n, 0, 64, s);
+  // levels in order; each level sorted by (min parent position, index)
+  for (int G = 0; G < nlev; ++G) {
+    const int c = cnt[G];
+    if (c == 0) continue;
+    gs_launch_begin(ctx, 1);
+    k_cm_keys<<<nblk(c), kThreads, 0, s>>>(keys2.get(), lstart[G], c, g->offs, g->cols, gl.get(),
+                                            pos.get(), G, lk.get());
+    gs_launch_end(ctx, 1);
+    size_t tb2 = tb;
+    cub::DeviceRadixSort::SortKeys(tmp.get(), tb2, lk.get(), lk2.get(), c, 0, 64, s);
+    gs_launch_begin(ctx, 1);
+    k_cm_assign<<<nblk(c), kThreads, 0, s>>>(lk2.get(), lstart[G], c, pos.get());
+    gs_launch_end(ctx, 1);
+  }
   gs_launch_begin(ctx, 1);
-  k_order_from_keys<<<nblk(n), kThreads, 0, s>>>(keys2.get(), n, d_order, d_newpos);
+  k_pos_to_order<<<nblk(n), kThreads, 0, s>>>(pos.get(), n, d_order, d_newpos);
   gs_launch_end(ctx, 1);
   GS_CUDA(ctx, cudaStreamSynchronize(s));
   return GS_OK;
