@@ -107,6 +107,8 @@ int gs_filter_info(const gs_filter* f, int* n, double* t, double* t_eff, double*
                    int* degree, int* kind);
 int gs_filter_coefficients(const gs_filter* f, double* out /* degree+1 */);
 const gs_graph* gs_filter_scaled(const gs_filter* f);
+/* The filter's internal vertex order (order[new] = old, n entries; locality renumbering). */
+int gs_filter_order(gs_ctx* ctx, const gs_filter* f, int* order, int mem);
 /* p_K(L_s) X for `width` contiguous n-vectors (heat.cpp:98-131). */
 int gs_filter_apply(gs_ctx* ctx, const gs_filter* f, const double* X, double* Y, int width,
                     int mem);

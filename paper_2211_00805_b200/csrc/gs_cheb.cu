@@ -42,6 +42,18 @@ constexpr int kRowsPerCta = GS_ROWS_PER_CTA;  // row blocks per CTA (L1 reuse ac
 #define GS_EARLY_LOADS 0
 #endif
 constexpr bool kEarlyLoads = GS_EARLY_LOADS != 0;
+#ifndef GS_GATHER_BATCH
+#define GS_GATHER_BATCH 4
+#endif
+constexpr int kGatherBatch = GS_GATHER_BATCH;  // neighbour rows in flight per lane
+#ifndef GS_PREFETCH
+#define GS_PREFETCH 1
+#endif
+#ifndef GS_PREFETCH_STAGES
+#define GS_PREFETCH_STAGES 2
+#endif
+constexpr bool kPrefetch = GS_PREFETCH != 0;
+constexpr int kPrefetchStages = GS_PREFETCH_STAGES;
 
 enum StepMode { MODE_NONE = 0, MODE_SK_PSI = 1, MODE_SK_PHI = 2, MODE_BARY_PSI = 3 };
 
@@ -94,6 +106,16 @@ __device__ __forceinline__ void st_vec(double* p, const double (&v)[VEC]) {
   }
 }
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 struct ColState {
   // per column (Bpad entries each)
   int* active;                 // nullable
@@ -130,7 +152,8 @@ struct StepArgs {
 template <int GW, int MODE>
 __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int sub, int q,
                                          double (&mn)[Lay<GW>::VEC], double (&mx)[Lay<GW>::VEC],
-                                         double (&er)[Lay<GW>::VEC]) {
+                                         double (&er)[Lay<GW>::VEC],
+                                         const double* pre = nullptr, int pre_stride = 0) {
   using L = Lay<GW>;
   constexpr int VEC = L::VEC, LPR = L::LPR;
   const bool valid = row < A.n;
@@ -142,10 +165,19 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
   double ai = 0.0;
   auto own_loads = [&]() {
     if (valid && A.k != 0) {
-      ld_vec<VEC>(A.Tprev + idx, tp);
-      if (A.k >= 2) {
-        ld_vec_rw<VEC>(A.Tout + idx, t2);
-        ld_vec_rw<VEC>(A.acc + idx, a0);
+      if (pre) {  // prefetched by cp.async into shared memory (k_cheb_step pipeline)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          tp[e] = pre[e];
+          t2[e] = pre[pre_stride + e];
+          a0[e] = pre[2 * pre_stride + e];
+        }
+      } else {
+        ld_vec<VEC>(A.Tprev + idx, tp);
+        if (A.k >= 2) {
+          ld_vec_rw<VEC>(A.Tout + idx, t2);
+          ld_vec_rw<VEC>(A.acc + idx, a0);
+        }
       }
       if constexpr (MODE == MODE_SK_PSI || MODE == MODE_SK_PHI) {
         ld_vec<VEC>(A.M + idx, op1);
@@ -194,6 +226,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
     const unsigned mask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
     const int pb = valid ? __ldg(A.offs + row) : 0;
     const int pe = valid ? __ldg(A.offs + row + 1) : 0;
+    constexpr int GB = kGatherBatch;
     for (int p0 = pb; p0 < pe; p0 += LPR) {
       int myc = 0;
       double myv = 0.0;
@@ -203,21 +236,39 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
       }
       const int cnt = min(LPR, pe - p0);
       int u = 0;
-      for (; u + 4 <= cnt; u += 4) {
-        int cc[4];
-        double vv[4];
-        double xx[4][VEC];
+      for (; u + GB <= cnt; u += GB) {
+        int cc[GB];
+        double vv[GB];
+        double xx[GB][VEC];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < GB; ++j) {
           cc[j] = __shfl_sync(mask, myc, u + j, LPR);
           vv[j] = __shfl_sync(mask, myv, u + j, LPR);
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ld_vec<VEC>(Tp + (size_t)cc[j] * GW, xx[j]);
+        for (int j = 0; j < GB; ++j) ld_vec<VEC>(Tp + (size_t)cc[j] * GW, xx[j]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < GB; ++j)
 #pragma unroll
           for (int e = 0; e < VEC; ++e) y[e] = fma(vv[j], xx[j][e], y[e]);
+      }
+      if constexpr (GB > 4) {
+        for (; u + 4 <= cnt; u += 4) {
+          int cc[4];
+          double vv[4];
+          double xx[4][VEC];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            cc[j] = __shfl_sync(mask, myc, u + j, LPR);
+            vv[j] = __shfl_sync(mask, myv, u + j, LPR);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) ld_vec<VEC>(Tp + (size_t)cc[j] * GW, xx[j]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) y[e] = fma(vv[j], xx[j][e], y[e]);
+        }
       }
       for (; u < cnt; ++u) {
         const int c = __shfl_sync(mask, myc, u, LPR);
@@ -314,8 +365,39 @@ __global__ void __launch_bounds__(kThreads, GS_MIN_BLOCKS) k_cheb_step(const Ste
     er[e] = 0.0;
   }
   const int base = tile * (BLOCK_ROWS * RPC) + warp * RPW + sub;
+  if constexpr (kPrefetch && VEC == 2) {
+    // Own-row operands of the next row block (T_{k-1}[i], T_{k-2}[i], acc[i]) are copied to shared
+    // memory with cp.async while this block's neighbour gathers run: DRAM reads stay in flight
+    // without holding registers. Each lane reads back only the 16 bytes it copied.
+    constexpr int STG = kPrefetchStages;
+    __shared__ __align__(16) double s_pre[STG][3][kThreads * 2];
+    const size_t gbase = (size_t)g * A.n * GW + q * VEC;
+    auto issue = [&](int j) {
+      const int row = base + j * BLOCK_ROWS;
+      if (j < RPC && row < A.n && A.k != 0) {
+        const size_t idx = gbase + (size_t)row * GW;
+        double* d = &s_pre[j % STG][0][threadIdx.x * 2];
+        cp_async16(d, A.Tprev + idx);
+        if (A.k >= 2) {
+          cp_async16(d + kThreads * 2, A.Tout + idx);
+          cp_async16(d + 2 * kThreads * 2, A.acc + idx);
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int j = 0; j < STG - 1; ++j) issue(j);
 #pragma unroll 1
-  for (int j = 0; j < RPC; ++j) cheb_row<GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er);
+    for (int j = 0; j < RPC; ++j) {
+      issue(j + STG - 1);
+      cp_async_wait<STG - 1>();
+      cheb_row<GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er,
+                         &s_pre[j % STG][0][threadIdx.x * 2], kThreads * 2);
+    }
+  } else {
+#pragma unroll 1
+    for (int j = 0; j < RPC; ++j) cheb_row<GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er);
+  }
   if constexpr (MODE != MODE_NONE) {
     // warp: combine rows with the same column slot (lane bits >= log2(LPR))
 #pragma unroll
@@ -1002,6 +1084,11 @@ extern "C" int gs_filter_coefficients(const gs_filter* f, double* out) {
 }
 
 extern "C" const gs_graph* gs_filter_scaled(const gs_filter* f) { return f->scaled; }
+
+extern "C" int gs_filter_order(gs_ctx* ctx, const gs_filter* f, int* order, int mem) {
+  GS_TRY(gs_copy_out(ctx, order, f->order, (size_t)f->scaled->n * sizeof(int), mem));
+  return gs_ctx_synchronize(ctx);
+}
 
 // Input staging: returns a device pointer to `count` doubles (the caller's when mem = DEVICE).
 static int stage_in(gs_ctx* ctx, DevBuf<double>& buf, const double* src, size_t count, int mem,

@@ -407,6 +407,13 @@ class HeatFilter:
     def scaled_laplacian(self) -> SparseSymMatrix:
         return SparseSymMatrix._borrow(self._ctx.lib.gs_filter_scaled(self._h), self._ctx, self)
 
+    def vertex_order(self) -> np.ndarray:
+        """Engine diagnostic: internal locality order (order[new] = old)."""
+        out = np.empty(self._n, np.int32)
+        self._ctx.check(self._ctx.lib.gs_filter_order(self._ctx.handle, self._h, _ptr(out),
+                                                      _capi.GS_MEM_HOST))
+        return out
+
     def apply(self, f) -> np.ndarray:
         """heat.cpp:98-131: (n,) vector or row-major (n, B) signals."""
         x = _f64(f)
