@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "gs_internal.cuh"
@@ -54,6 +55,14 @@ constexpr int kGatherBatch = GS_GATHER_BATCH;  // neighbour rows in flight per l
 #endif
 constexpr bool kPrefetch = GS_PREFETCH != 0;
 constexpr int kPrefetchStages = GS_PREFETCH_STAGES;
+constexpr int kTileRows = 32;  // rows per staged block (gs_tiles.cu plan granularity)
+#ifndef GS_TILE_PERSIST
+#define GS_TILE_PERSIST 1
+#endif
+constexpr bool kTilePersist = GS_TILE_PERSIST != 0;
+#ifndef GS_TILE_SMEM_BUDGET
+#define GS_TILE_SMEM_BUDGET (100 * 1024)
+#endif
 
 enum StepMode { MODE_NONE = 0, MODE_SK_PSI = 1, MODE_SK_PHI = 2, MODE_BARY_PSI = 3 };
 
@@ -144,16 +153,24 @@ struct StepArgs {
   const double* M;      // PSI: N (targets); PHI: M (sources / members)
   const double* Vcur;   // PHI: V of this sweep
   double* Wout;         // PSI: W; PHI: V of the next sweep
+  // staged-neighbour path (k_cheb_tile)
+  const unsigned short* slot;
+  const int* bfirst;
+  const int* bcount;
+  const int* rstart;
+  const int* rlen;
+  const int* lbase;
 };
 
 // One row of one Chebyshev step for the calling lane group; epilogue partials accumulate in
 // mn/mx/er. Own-row streaming loads (T_{k-1}[i], T_{k-2}[i], acc[i], epilogue operands) are issued
 // before the neighbour gathers so HBM reads overlap the gather latency.
-template <int GW, int MODE>
+template <int GW, int MODE, bool SMEM = false>
 __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int sub, int q,
                                          double (&mn)[Lay<GW>::VEC], double (&mx)[Lay<GW>::VEC],
                                          double (&er)[Lay<GW>::VEC],
-                                         const double* pre = nullptr, int pre_stride = 0) {
+                                         const double* pre = nullptr, int pre_stride = 0,
+                                         const double* sx = nullptr) {
   using L = Lay<GW>;
   constexpr int VEC = L::VEC, LPR = L::LPR;
   const bool valid = row < A.n;
@@ -227,32 +244,48 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
     const int pb = valid ? __ldg(A.offs + row) : 0;
     const int pe = valid ? __ldg(A.offs + row + 1) : 0;
     constexpr int GB = kGatherBatch;
+    // gather source: global T_{k-1} (L1/L2) or the block's staged window in shared memory
+    auto gather = [&](int c, double (&x)[VEC]) {
+      if constexpr (SMEM) {
+        const double* p = sx + (size_t)c * GW + q * VEC;
+        if constexpr (VEC == 2) {
+          const double2 t = *reinterpret_cast<const double2*>(p);
+          x[0] = t.x;
+          x[1] = t.y;
+        } else {
+          x[0] = p[0];
+        }
+      } else {
+        ld_vec<VEC>(Tp + (size_t)c * GW, x);
+      }
+    };
     for (int p0 = pb; p0 < pe; p0 += LPR) {
       int myc = 0;
       double myv = 0.0;
       if (p0 + q < pe) {
-        myc = __ldg(A.cols + p0 + q);
+        myc = SMEM ? (int)__ldg(A.slot + p0 + q) : __ldg(A.cols + p0 + q);
         myv = __ldg(A.vals + p0 + q);
       }
       const int cnt = min(LPR, pe - p0);
       int u = 0;
-      for (; u + GB <= cnt; u += GB) {
-        int cc[GB];
-        double vv[GB];
-        double xx[GB][VEC];
+      constexpr int GBX = SMEM ? 8 : GB;
+      for (; u + GBX <= cnt; u += GBX) {
+        int cc[GBX];
+        double vv[GBX];
+        double xx[GBX][VEC];
 #pragma unroll
-        for (int j = 0; j < GB; ++j) {
+        for (int j = 0; j < GBX; ++j) {
           cc[j] = __shfl_sync(mask, myc, u + j, LPR);
           vv[j] = __shfl_sync(mask, myv, u + j, LPR);
         }
 #pragma unroll
-        for (int j = 0; j < GB; ++j) ld_vec<VEC>(Tp + (size_t)cc[j] * GW, xx[j]);
+        for (int j = 0; j < GBX; ++j) gather(cc[j], xx[j]);
 #pragma unroll
-        for (int j = 0; j < GB; ++j)
+        for (int j = 0; j < GBX; ++j)
 #pragma unroll
           for (int e = 0; e < VEC; ++e) y[e] = fma(vv[j], xx[j][e], y[e]);
       }
-      if constexpr (GB > 4) {
+      if constexpr (GBX > 4) {
         for (; u + 4 <= cnt; u += 4) {
           int cc[4];
           double vv[4];
@@ -263,7 +296,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
             vv[j] = __shfl_sync(mask, myv, u + j, LPR);
           }
 #pragma unroll
-          for (int j = 0; j < 4; ++j) ld_vec<VEC>(Tp + (size_t)cc[j] * GW, xx[j]);
+          for (int j = 0; j < 4; ++j) gather(cc[j], xx[j]);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -274,7 +307,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
         const int c = __shfl_sync(mask, myc, u, LPR);
         const double v = __shfl_sync(mask, myv, u, LPR);
         double x[VEC];
-        ld_vec<VEC>(Tp + (size_t)c * GW, x);
+        gather(c, x);
 #pragma unroll
         for (int e = 0; e < VEC; ++e) y[e] = fma(v, x[e], y[e]);
       }
@@ -341,6 +374,12 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
   }
 }
 
+template <int GW, int MODE>
+__device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int tile, int warp, int sub,
+                                               int q, double (&mn)[Lay<GW>::VEC],
+                                               double (&mx)[Lay<GW>::VEC],
+                                               double (&er)[Lay<GW>::VEC]);
+
 // A CTA owns RPC x (8 warps x RPW) consecutive rows of one column group; at each of its RPC
 // iterations the 8 warps cover a contiguous block, so neighbouring gathers share L1 lines.
 #ifndef GS_MIN_BLOCKS
@@ -398,7 +437,17 @@ __global__ void __launch_bounds__(kThreads, GS_MIN_BLOCKS) k_cheb_step(const Ste
 #pragma unroll 1
     for (int j = 0; j < RPC; ++j) cheb_row<GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er);
   }
-  if constexpr (MODE != MODE_NONE) {
+  if constexpr (MODE != MODE_NONE) block_epilogue<GW, MODE>(A, g, tile, warp, sub, q, mn, mx, er);
+}
+
+template <int GW, int MODE>
+__device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int tile, int warp, int sub,
+                                               int q, double (&mn)[Lay<GW>::VEC],
+                                               double (&mx)[Lay<GW>::VEC],
+                                               double (&er)[Lay<GW>::VEC]) {
+  using L = Lay<GW>;
+  constexpr int VEC = L::VEC, LPR = L::LPR;
+  {
     // warp: combine rows with the same column slot (lane bits >= log2(LPR))
 #pragma unroll
     for (int off = LPR; off < 32; off <<= 1) {
@@ -433,6 +482,158 @@ __global__ void __launch_bounds__(kThreads, GS_MIN_BLOCKS) k_cheb_step(const Ste
       if constexpr (MODE == MODE_SK_PSI || MODE == MODE_SK_PHI) atomicMax(A.cs.cmax + col, dkey(a_mx));
       if constexpr (MODE == MODE_SK_PHI) A.cs.part_err[(size_t)tile * A.Bpad + col] = a_er;
     }
+  }
+}
+
+// ---- staged-neighbour step: one CTA per (block of kTileRows rows, column group) -------------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+
+template <int GW, int MODE>
+__global__ void __launch_bounds__(kThreads) k_cheb_tile(const StepArgs A) {
+  using L = Lay<GW>;
+  constexpr int VEC = L::VEC, LPR = L::LPR, RPW = L::RPW;
+  constexpr int BLOCK_ROWS = (kThreads / 32) * RPW;
+  constexpr int PASSES = kTileRows / BLOCK_ROWS;
+  static_assert(PASSES >= 1 && kTileRows % BLOCK_ROWS == 0, "tile rows");
+  extern __shared__ __align__(128) double sx[];
+  __shared__ __align__(8) unsigned long long mbar;
+  if (A.status && (A.status->error || A.status->done)) return;
+  const int b = blockIdx.x / A.Gl;
+  const int g = A.g0 + blockIdx.x % A.Gl;
+  if (A.cs.gactive && A.cs.gactive[g] == 0) return;
+  const unsigned bar = smem_u32(&mbar);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // stage every run of T_{k-1} rows this block references with one TMA bulk copy each
+    const int first = A.bfirst[b], cnt = first < 0 ? 0 : A.bcount[b];
+    unsigned bytes = 0;
+    for (int r = 0; r < cnt; ++r) bytes += (unsigned)A.rlen[first + r] * GW * 8u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+                 : "memory");
+    const double* src0 = A.Tprev + (size_t)g * A.n * GW;
+    for (int r = 0; r < cnt; ++r) {
+      const int run = first + r;
+      const double* src = src0 + (size_t)A.rstart[run] * GW;
+      const unsigned dst = smem_u32(sx + (size_t)A.lbase[run] * GW);
+      const unsigned sz = (unsigned)A.rlen[run] * GW * 8u;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+          "l"(src), "r"(sz), "r"(bar)
+          : "memory");
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / LPR, q = lane % LPR;
+  double mn[VEC], mx[VEC], er[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    mn[e] = INFINITY;
+    mx[e] = 0.0;
+    er[e] = 0.0;
+  }
+  // wait for the staged window (phase 0)
+  {
+    unsigned done = 0;
+    while (!done) {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
+    }
+  }
+  const int base = b * kTileRows + warp * RPW + sub;
+#pragma unroll 1
+  for (int j = 0; j < PASSES; ++j)
+    cheb_row<GW, MODE, true>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er, nullptr, 0, sx);
+  if constexpr (MODE != MODE_NONE) block_epilogue<GW, MODE>(A, g, b, warp, sub, q, mn, mx, er);
+}
+
+// Persistent, double-buffered variant: each CTA walks (block, group) items with a stride of
+// gridDim.x; TMA stages item i+1's neighbour window into the other buffer while item i computes.
+template <int GW, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_cheb_tilep(const StepArgs A, int max_slots) {
+  using L = Lay<GW>;
+  constexpr int VEC = L::VEC, LPR = L::LPR, RPW = L::RPW;
+  constexpr int BLOCK_ROWS = (kThreads / 32) * RPW;
+  constexpr int PASSES = kTileRows / BLOCK_ROWS;
+  extern __shared__ __align__(128) double sx[];
+  __shared__ __align__(8) unsigned long long mbar[2];
+  if (A.status && (A.status->error || A.status->done)) return;
+  const int total = A.tiles * A.Gl;
+  const size_t stage_elems = (size_t)max_slots * GW;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[0])) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&mbar[1])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int item, int stage) {  // thread 0 only
+    const int b = item / A.Gl, g = A.g0 + item % A.Gl;
+    const bool live = !(A.cs.gactive && A.cs.gactive[g] == 0);
+    const int first = A.bfirst[b], cnt = (first < 0 || !live) ? 0 : A.bcount[b];
+    unsigned bytes = 0;
+    for (int r = 0; r < cnt; ++r) bytes += (unsigned)A.rlen[first + r] * GW * 8u;
+    const unsigned bar = smem_u32(&mbar[stage]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+                 : "memory");
+    const double* src0 = A.Tprev + (size_t)g * A.n * GW;
+    double* dst0 = sx + stage * stage_elems;
+    for (int r = 0; r < cnt; ++r) {
+      const int run = first + r;
+      const double* src = src0 + (size_t)A.rstart[run] * GW;
+      const unsigned dst = smem_u32(dst0 + (size_t)A.lbase[run] * GW);
+      const unsigned sz = (unsigned)A.rlen[run] * GW * 8u;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+          "l"(src), "r"(sz), "r"(bar)
+          : "memory");
+    }
+  };
+  if (threadIdx.x == 0 && (int)blockIdx.x < total) issue(blockIdx.x, 0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / LPR, q = lane % LPR;
+  unsigned phase[2] = {0u, 0u};
+  int it = 0;
+  for (int item = blockIdx.x; item < total; item += gridDim.x, ++it) {
+    const int stage = it & 1;
+    const int next = item + gridDim.x;
+    if (threadIdx.x == 0 && next < total) issue(next, stage ^ 1);
+    {
+      const unsigned bar = smem_u32(&mbar[stage]);
+      unsigned done = 0;
+      while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(phase[stage])
+            : "memory");
+      }
+      phase[stage] ^= 1u;
+    }
+    const int b = item / A.Gl, g = A.g0 + item % A.Gl;
+    if (!(A.cs.gactive && A.cs.gactive[g] == 0)) {
+      double mn[VEC], mx[VEC], er[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        mn[e] = INFINITY;
+        mx[e] = 0.0;
+        er[e] = 0.0;
+      }
+      const int base = b * kTileRows + warp * RPW + sub;
+      const double* stg = sx + stage * stage_elems;
+#pragma unroll 1
+      for (int j = 0; j < PASSES; ++j)
+        cheb_row<GW, MODE, true>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er, nullptr, 0, stg);
+      if constexpr (MODE != MODE_NONE) block_epilogue<GW, MODE>(A, g, b, warp, sub, q, mn, mx, er);
+    }
+    __syncthreads();  // every warp is done with this stage before it is refilled
   }
 }
 
@@ -877,6 +1078,54 @@ void launch_step_gw(const StepArgs& A, int mode, cudaStream_t s) {
   }
 }
 
+template <int GW, int MODE>
+void launch_tile_mode(const StepArgs& A, size_t smem, cudaStream_t s) {
+  if constexpr (kTilePersist) {
+    static size_t configured = 0;
+    const size_t sm2 = 2 * smem;
+    if (sm2 > 48 * 1024 && sm2 > configured) {
+      cudaFuncSetAttribute(k_cheb_tilep<GW, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+      configured = sm2;
+    }
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cheb_tilep<GW, MODE>, kThreads, sm2);
+    if (per_sm < 1) per_sm = 1;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int total = A.tiles * A.Gl;
+    const int grid = std::min(total, nsm * per_sm);
+    k_cheb_tilep<GW, MODE><<<(unsigned)std::max(grid, 1), kThreads, sm2, s>>>(A, (int)(smem / (GW * 8)));
+  } else {
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      cudaFuncSetAttribute(k_cheb_tile<GW, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      configured = smem;
+    }
+    k_cheb_tile<GW, MODE><<<(unsigned)(A.tiles * A.Gl), kThreads, smem, s>>>(A);
+  }
+}
+
+template <int GW>
+void launch_tile_gw(const StepArgs& A, int mode, size_t smem, cudaStream_t s) {
+  switch (mode) {
+    case MODE_NONE: launch_tile_mode<GW, MODE_NONE>(A, smem, s); break;
+    case MODE_SK_PSI: launch_tile_mode<GW, MODE_SK_PSI>(A, smem, s); break;
+    case MODE_SK_PHI: launch_tile_mode<GW, MODE_SK_PHI>(A, smem, s); break;
+    default: launch_tile_mode<GW, MODE_BARY_PSI>(A, smem, s); break;
+  }
+}
+
+void launch_tile(gs_ctx* ctx, int gw, const StepArgs& A, int mode, size_t smem) {
+  gs_launch_begin(ctx, 0);
+  switch (gw) {
+    case 64: launch_tile_gw<64>(A, mode, smem, ctx->stream); break;
+    case 32: launch_tile_gw<32>(A, mode, smem, ctx->stream); break;
+    default: launch_tile_gw<16>(A, mode, smem, ctx->stream); break;
+  }
+  gs_launch_end(ctx, 0);
+}
+
 void launch_step(gs_ctx* ctx, int gw, const StepArgs& A, int mode) {
   gs_launch_begin(ctx, 0);
   switch (gw) {
@@ -894,19 +1143,30 @@ void launch_step(gs_ctx* ctx, int gw, const StepArgs& A, int mode) {
 // Workspace for one batched run: grouped buffers + per-column state.
 struct Work {
   int n = 0, B = 0, GW = 1, G = 1, Bpad = 1, tiles = 0;
+  bool tile = false;     // staged-neighbour kernel (k_cheb_tile)
+  size_t tile_smem = 0;
   DevBuf<double> T[2], acc;
   DevBuf<unsigned long long> cmin, cmax;
   DevBuf<double> thr, errcol, part_err;
   DevBuf<int> active, gactive;
   DevBuf<gs_status> status;
-  int init(gs_ctx* ctx, int n_, int B_, bool want_err) {
+  int init(gs_ctx* ctx, int n_, int B_, bool want_err, const gs_filter* f = nullptr) {
     cudaStream_t s = ctx->stream;
     n = n_;
     B = B_;
     GW = choose_gw(B);
+    const char* env = getenv("GS_TILE");
+    // staged-neighbour path: experimental, opt-in with GS_TILE=1 (slower than k_cheb_step so far;
+    // profiles/r01_summary.md)
+    tile = f && f->tiles.max_slots > 0 && GW >= 16 && env && env[0] == '1';
+    if (tile) {
+      while (GW > 16 && (size_t)f->tiles.max_slots * GW * 8 > (size_t)GS_TILE_SMEM_BUDGET) GW >>= 1;
+      tile_smem = (size_t)f->tiles.max_slots * GW * 8;
+      if (tile_smem > (size_t)GS_TILE_SMEM_BUDGET) tile = false;
+    }
     G = (B + GW - 1) / GW;
     Bpad = G * GW;
-    tiles = (n + rows_per_cta(GW) - 1) / rows_per_cta(GW);
+    tiles = tile ? f->tiles.nblocks : (n + rows_per_cta(GW) - 1) / rows_per_cta(GW);
     const size_t len = (size_t)Bpad * n;
     GS_CUDA(ctx, T[0].alloc(len, s));
     GS_CUDA(ctx, T[1].alloc(len, s));
@@ -973,12 +1233,19 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work& w, int a0, int mode, const 
   A.M = M;
   A.Vcur = Vcur;
   A.Wout = Wout;
+  A.slot = f->tiles.slot;
+  A.bfirst = f->tiles.bfirst;
+  A.bcount = f->tiles.bcount;
+  A.rstart = f->tiles.rstart;
+  A.rlen = f->tiles.rlen;
+  A.lbase = f->tiles.lbase;
   for (int k = 1; k <= K; ++k) {
     A.k = k;
     A.bk = f->coeffs[k];
     A.Tprev = w.T[(a0 + k - 1) & 1].get();
     A.Tout = w.T[(a0 + k) & 1].get();
-    launch_step(ctx, w.GW, A, k == K ? mode : MODE_NONE);
+    if (w.tile) launch_tile(ctx, w.GW, A, k == K ? mode : MODE_NONE, w.tile_smem);
+    else launch_step(ctx, w.GW, A, k == K ? mode : MODE_NONE);
   }
   return (a0 + K) & 1;
 }
@@ -1049,6 +1316,10 @@ extern "C" int gs_filter_create(gs_ctx* ctx, const gs_graph* L, int kind, double
   }
   if (!rc) rc = gs_bfs_order(ctx, f->scaled, f->order, f->newpos);
   if (!rc) rc = gs_permute_graph(ctx, f->scaled, f->order, f->newpos, &f->perm);
+  if (!rc) {
+    rc = gs_tiles_build(ctx, f->perm, kTileRows, &f->tiles);
+    if (!rc && f->tiles.max_slots >= 65536) gs_tiles_release(f->tiles);  // 16-bit slots only
+  }
   if (rc) {
     gs_filter_destroy(f);
     return rc;
@@ -1061,6 +1332,7 @@ extern "C" void gs_filter_destroy(gs_filter* f) {
   if (!f) return;
   gs_graph_destroy(f->scaled);
   gs_graph_destroy(f->perm);
+  gs_tiles_release(f->tiles);
   cudaFree(f->order);
   cudaFree(f->newpos);
   cudaFree(f->d_coeffs);
@@ -1117,7 +1389,7 @@ extern "C" int gs_filter_apply(gs_ctx* ctx, const gs_filter* f, const double* X,
   if (width == 0 || n == 0) return GS_OK;
   cudaStream_t s = ctx->stream;
   Work w;
-  GS_TRY(w.init(ctx, n, width, false));
+  GS_TRY(w.init(ctx, n, width, false, f));
   DevBuf<double> xin, yout;
   const double* dX = nullptr;
   GS_TRY(stage_in(ctx, xin, X, (size_t)width * n, mem, &dX));
@@ -1277,7 +1549,7 @@ extern "C" int gs_sinkhorn(gs_ctx* ctx, const gs_filter* f, const double* a, con
   da = aperm.get();
   // ---- workspace -----------------------------------------------------------------------------
   Work w;
-  GS_TRY(w.init(ctx, n, P, true));
+  GS_TRY(w.init(ctx, n, P, true, f));
   const size_t len = (size_t)w.Bpad * n;
   DevBuf<double> M, N, V[2], W;
   GS_CUDA(ctx, M.alloc(len, s));
@@ -1477,7 +1749,7 @@ extern "C" int gs_barycenter(gs_ctx* ctx, const gs_filter* f, const double* a,
   da = aperm.get();
 
   Work w;
-  GS_TRY(w.init(ctx, n, m, true));
+  GS_TRY(w.init(ctx, n, m, true, f));
   const size_t len = (size_t)w.Bpad * n;
   DevBuf<double> Mb, V[2], W, lb, bary, part, mass, dal, errbuf, derr;
   DevBuf<unsigned long long> lbmax;
