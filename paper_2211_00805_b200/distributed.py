@@ -1,0 +1,113 @@
+"""Multi-GPU plumbing (one process per GPU, torch.distributed over NCCL on NVLink/NVSwitch).
+
+The only real exchange on the hot path is the member-sharded barycenter
+(configs 2 and 4): every rank owns a contiguous share of the family's members and, per sweep,
+  * allreduce(SUM) of the n-vector sum_i alpha_i ln clamp(psi_i) over ranks
+    (barycenter.cpp:75-78; the reference's member-order sum is re-associated across ranks), and
+  * allreduce(MAX) of the per-rank marginal error (barycenter.cpp:86),
+after which every rank computes the same barycenter. The engine calls these through the C ABI
+hook `gs_comm.allreduce(user, buf, count, op, stream)`; `TorchAllreduce` implements it with
+torch.distributed on the engine's stream (NCCL for device buffers, gloo for host buffers).
+Distance pairs (config 1) need no collective: ranks run independent pair shards.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import numpy as np
+
+from . import _capi
+from .geosink import (BarycenterResult, Distribution, DistributionFamily, HeatFilter,
+                      SinkhornParams, _f64, _ptr, _stack)
+
+
+def member_shard(m: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous share [lo, hi) of m members for `rank` (sizes differ by at most one)."""
+    base, extra = divmod(m, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a raw device pointer (no copy)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8",
+                                         "data": (ptr, False), "version": 3}
+
+
+class TorchAllreduce:
+    """gs_comm hook over torch.distributed. Keeps the ctypes callback alive."""
+
+    def __init__(self, group=None, device_buffers: bool = True):
+        import torch
+        import torch.distributed as dist
+
+        self._torch, self._dist, self._group = torch, dist, group
+        self._device = device_buffers
+        self.calls = 0
+        self.error: Optional[BaseException] = None
+
+        def _hook(user, buf, count, op, stream):
+            try:
+                self.calls += 1
+                rop = dist.ReduceOp.SUM if op == 0 else dist.ReduceOp.MAX
+                if self._device:
+                    t = torch.as_tensor(_CudaArray(buf, count), device="cuda")
+                    with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                        dist.all_reduce(t, op=rop, group=self._group)
+                else:
+                    arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(C.c_double)), shape=(count,))
+                    t = torch.from_numpy(arr)
+                    dist.all_reduce(t, op=rop, group=self._group)
+                return 0
+            except BaseException as e:  # surfaced by the caller after the engine returns
+                self.error = e
+                return 1
+
+        self._cb = _capi.ALLREDUCE_FN(_hook)
+        self.comm = _capi.GsComm(self._cb, None)
+
+    def __call__(self, buf_ptr: int, count: int, op: int, stream: int = 0) -> int:
+        """Invoke the hook directly (used by host-side tests)."""
+        return self._cb(None, buf_ptr, count, op, stream)
+
+
+def sharded_sinkhorn_barycenter(filter: HeatFilter, family: DistributionFamily, a,
+                                params: SinkhornParams = SinkhornParams(),
+                                group=None) -> BarycenterResult:
+    """sinkhorn_barycenter (barycenter.cpp:45-99) with the members sharded over the ranks of
+    `group`; every rank passes the full family and gets the full barycenter plus the scalings
+    of its own members (others are None)."""
+    import torch.distributed as dist
+
+    ctx = filter._ctx
+    n = filter.size()
+    family.validate(n)
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    m = len(family.members)
+    lo, hi = member_shard(m, world, rank)
+    al = family.resolved_alphas()[lo:hi].copy()
+    local = _stack(family.members[lo:hi], n)
+    a = _f64(a)
+    bary = np.empty(n)
+    V = np.empty((hi - lo, n))
+    W = np.empty((hi - lo, n))
+    it = np.zeros(1, np.int32)
+    conv = np.zeros(1, np.int32)
+    err = np.zeros(1)
+    hook = TorchAllreduce(group, device_buffers=True)
+    rc = ctx.lib.gs_barycenter(ctx.handle, filter._h, _ptr(a), _ptr(local), hi - lo, _ptr(al),
+                               int(params.max_iter), float(params.tol), _capi.GS_MEM_HOST,
+                               C.byref(hook.comm), _ptr(bary), _ptr(V), _ptr(W), _ptr(it),
+                               _ptr(conv), _ptr(err))
+    if hook.error is not None:
+        raise hook.error
+    ctx.check(rc)
+    scal = [None] * m
+    for c in range(lo, hi):
+        scal[c] = (V[c - lo].copy(), W[c - lo].copy())
+    return BarycenterResult(Distribution(bary, validate=False), scal, int(it[0]), bool(conv[0]),
+                            float(err[0]))

@@ -3,6 +3,10 @@ import sys
 
 import pytest
 
+# the oracle's OpenMP loops are tiny at test sizes; avoid spin-waiting thread oversubscription
+os.environ.setdefault("OMP_NUM_THREADS", "2")
+os.environ.setdefault("OMP_WAIT_POLICY", "passive")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 for p in (ROOT, os.path.join(ROOT, "oracle"), os.path.join(ROOT, "tests")):
     if p not in sys.path:
