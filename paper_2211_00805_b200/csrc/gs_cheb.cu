@@ -55,7 +55,15 @@ constexpr int kGatherBatch = GS_GATHER_BATCH;  // neighbour rows in flight per l
 #endif
 constexpr bool kPrefetch = GS_PREFETCH != 0;
 constexpr int kPrefetchStages = GS_PREFETCH_STAGES;
-constexpr int kTileRows = 32;  // rows per staged block (gs_tiles.cu plan granularity)
+#ifndef GS_PREFETCH_IDX
+#define GS_PREFETCH_IDX 0
+#endif
+constexpr bool kPrefetchIdx = GS_PREFETCH_IDX != 0;  // (col, val) prefetch: opt-in, not faster
+constexpr int kTileRows = 32;
+#ifndef GS_SMQUEUE
+#define GS_SMQUEUE 0
+#endif
+constexpr bool kSmQueue = GS_SMQUEUE != 0;  // rows per staged block (gs_tiles.cu plan granularity)
 #ifndef GS_TILE_PERSIST
 #define GS_TILE_PERSIST 1
 #endif
@@ -119,6 +127,14 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -153,6 +169,7 @@ struct StepArgs {
   const double* M;      // PSI: N (targets); PHI: M (sources / members)
   const double* Vcur;   // PHI: V of this sweep
   double* Wout;         // PSI: W; PHI: V of the next sweep
+  int* counters;        // per-SM work queues (k_cheb_smq), nullable
   // staged-neighbour path (k_cheb_tile)
   const unsigned short* slot;
   const int* bfirst;
@@ -170,7 +187,9 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
                                          double (&mn)[Lay<GW>::VEC], double (&mx)[Lay<GW>::VEC],
                                          double (&er)[Lay<GW>::VEC],
                                          const double* pre = nullptr, int pre_stride = 0,
-                                         const double* sx = nullptr) {
+                                         const double* sx = nullptr,
+                                         const int* pre_c = nullptr, const double* pre_v = nullptr,
+                                         int pre_pb = 0, int pre_pe = 0) {
   using L = Lay<GW>;
   constexpr int VEC = L::VEC, LPR = L::LPR;
   const bool valid = row < A.n;
@@ -241,8 +260,8 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
     // the LPR lanes of a row load LPR consecutive (col, val) entries with one coalesced access
     // and broadcast them by shuffle; the fma chain still runs in CSR order.
     const unsigned mask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (sub * LPR));
-    const int pb = valid ? __ldg(A.offs + row) : 0;
-    const int pe = valid ? __ldg(A.offs + row + 1) : 0;
+    const int pb = pre_c ? pre_pb : (valid ? __ldg(A.offs + row) : 0);
+    const int pe = pre_c ? pre_pe : (valid ? __ldg(A.offs + row + 1) : 0);
     constexpr int GB = kGatherBatch;
     // gather source: global T_{k-1} (L1/L2) or the block's staged window in shared memory
     auto gather = [&](int c, double (&x)[VEC]) {
@@ -263,8 +282,13 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
       int myc = 0;
       double myv = 0.0;
       if (p0 + q < pe) {
-        myc = SMEM ? (int)__ldg(A.slot + p0 + q) : __ldg(A.cols + p0 + q);
-        myv = __ldg(A.vals + p0 + q);
+        if (pre_c && p0 == pb) {  // first chunk prefetched by cp.async (k_cheb_step pipeline)
+          myc = pre_c[q];
+          myv = pre_v[q];
+        } else {
+          myc = SMEM ? (int)__ldg(A.slot + p0 + q) : __ldg(A.cols + p0 + q);
+          myv = __ldg(A.vals + p0 + q);
+        }
       }
       const int cnt = min(LPR, pe - p0);
       int u = 0;
@@ -405,21 +429,43 @@ __global__ void __launch_bounds__(kThreads, GS_MIN_BLOCKS) k_cheb_step(const Ste
   }
   const int base = tile * (BLOCK_ROWS * RPC) + warp * RPW + sub;
   if constexpr (kPrefetch && VEC == 2) {
-    // Own-row operands of the next row block (T_{k-1}[i], T_{k-2}[i], acc[i]) are copied to shared
-    // memory with cp.async while this block's neighbour gathers run: DRAM reads stay in flight
-    // without holding registers. Each lane reads back only the 16 bytes it copied.
+    // Own-row operands of the next row block (T_{k-1}[i], T_{k-2}[i], acc[i]) -- and, with one
+    // warp per row, the row's first 32 (col, val) entries -- are copied to shared memory with
+    // cp.async while this block's neighbour gathers run: DRAM/L2 reads stay in flight without
+    // holding registers. Each lane reads back only what it copied itself.
     constexpr int STG = kPrefetchStages;
+    constexpr bool IDX = LPR == 32 && kPrefetchIdx;
     __shared__ __align__(16) double s_pre[STG][3][kThreads * 2];
+    __shared__ __align__(16) int s_col[IDX ? STG : 1][IDX ? kThreads : 1];
+    __shared__ __align__(16) double s_val[IDX ? STG : 1][IDX ? kThreads : 1];
     const size_t gbase = (size_t)g * A.n * GW + q * VEC;
+    // row offsets of this warp's RPC rows: lane j holds offs[row_j], offs[row_j + 1]
+    int o_lo = 0, o_hi = 0;
+    if constexpr (IDX) {
+      const int rj = base + lane * BLOCK_ROWS;
+      if (lane < RPC && rj < A.n) {
+        o_lo = __ldg(A.offs + rj);
+        o_hi = __ldg(A.offs + rj + 1);
+      }
+    }
     auto issue = [&](int j) {
       const int row = base + j * BLOCK_ROWS;
-      if (j < RPC && row < A.n && A.k != 0) {
-        const size_t idx = gbase + (size_t)row * GW;
-        double* d = &s_pre[j % STG][0][threadIdx.x * 2];
-        cp_async16(d, A.Tprev + idx);
-        if (A.k >= 2) {
-          cp_async16(d + kThreads * 2, A.Tout + idx);
-          cp_async16(d + 2 * kThreads * 2, A.acc + idx);
+      if (j < RPC && row < A.n) {
+        if (A.k != 0) {
+          const size_t idx = gbase + (size_t)row * GW;
+          double* d = &s_pre[j % STG][0][threadIdx.x * 2];
+          cp_async16(d, A.Tprev + idx);
+          if (A.k >= 2) {
+            cp_async16(d + kThreads * 2, A.Tout + idx);
+            cp_async16(d + 2 * kThreads * 2, A.acc + idx);
+          }
+        }
+        if constexpr (IDX) {
+          const int pb = __shfl_sync(0xffffffffu, o_lo, j), pe = __shfl_sync(0xffffffffu, o_hi, j);
+          if (pb + q < pe) {
+            cp_async4(&s_col[j % STG][threadIdx.x], A.cols + pb + q);
+            cp_async8(&s_val[j % STG][threadIdx.x], A.vals + pb + q);
+          }
         }
       }
       cp_async_commit();
@@ -430,8 +476,15 @@ __global__ void __launch_bounds__(kThreads, GS_MIN_BLOCKS) k_cheb_step(const Ste
     for (int j = 0; j < RPC; ++j) {
       issue(j + STG - 1);
       cp_async_wait<STG - 1>();
-      cheb_row<GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er,
-                         &s_pre[j % STG][0][threadIdx.x * 2], kThreads * 2);
+      if constexpr (IDX) {
+        const int pb = __shfl_sync(0xffffffffu, o_lo, j), pe = __shfl_sync(0xffffffffu, o_hi, j);
+        cheb_row<GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er,
+                           &s_pre[j % STG][0][threadIdx.x * 2], kThreads * 2, nullptr,
+                           &s_col[j % STG][warp * 32], &s_val[j % STG][warp * 32], pb, pe);
+      } else {
+        cheb_row<GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er,
+                           &s_pre[j % STG][0][threadIdx.x * 2], kThreads * 2);
+      }
     }
   } else {
 #pragma unroll 1
@@ -481,6 +534,54 @@ __device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int til
       atomicMin(A.cs.cmin + col, dkey(a_mn));
       if constexpr (MODE == MODE_SK_PSI || MODE == MODE_SK_PHI) atomicMax(A.cs.cmax + col, dkey(a_mx));
       if constexpr (MODE == MODE_SK_PHI) A.cs.part_err[(size_t)tile * A.Bpad + col] = a_er;
+    }
+  }
+}
+
+// ---- per-SM work queues: every SM drains a contiguous range of row blocks ---------------------
+// A CTA reads %smid and takes the next block of that SM's range (then steals from the following
+// SMs once its own range is empty, so completion never depends on CTA placement). All CTAs
+// resident on an SM work on adjacent rows, so the Cuthill-McKee neighbour window they gather is
+// shared in that SM's L1.
+__device__ __forceinline__ unsigned smid_u32() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+template <int GW, int MODE, int RPC>
+__global__ void __launch_bounds__(kThreads) k_cheb_smq(const StepArgs A, int* counters, int nsm) {
+  using L = Lay<GW>;
+  constexpr int VEC = L::VEC, LPR = L::LPR, RPW = L::RPW;
+  constexpr int BLOCK_ROWS = (kThreads / 32) * RPW;
+  if (A.status && (A.status->error || A.status->done)) return;
+  __shared__ int s_item;
+  const int total = A.tiles * A.Gl;  // items = (tile, group)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / LPR, q = lane % LPR;
+  const int home = (int)(smid_u32() % (unsigned)nsm);
+  for (int probe = 0; probe < nsm; ++probe) {
+    const int s = (home + probe) % nsm;
+    const int lo = (int)((long long)total * s / nsm), hi = (int)((long long)total * (s + 1) / nsm);
+    for (;;) {
+      if (threadIdx.x == 0) s_item = lo + atomicAdd(counters + s, 1);
+      __syncthreads();
+      const int item = s_item;
+      __syncthreads();
+      if (item >= hi) break;
+      const int tile = item / A.Gl, g = A.g0 + item % A.Gl;
+      if (A.cs.gactive && A.cs.gactive[g] == 0) continue;
+      double mn[VEC], mx[VEC], er[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        mn[e] = INFINITY;
+        mx[e] = 0.0;
+        er[e] = 0.0;
+      }
+      const int base = tile * (BLOCK_ROWS * RPC) + warp * RPW + sub;
+#pragma unroll 1
+      for (int j = 0; j < RPC; ++j) cheb_row<GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er);
+      if constexpr (MODE != MODE_NONE) block_epilogue<GW, MODE>(A, g, tile, warp, sub, q, mn, mx, er);
     }
   }
 }
@@ -1066,9 +1167,30 @@ int rows_per_cta(int gw) {
   }
 }
 
+template <int GW, int MODE>
+void launch_smq_mode(const StepArgs& A, int* counters, cudaStream_t s) {
+  constexpr int RPC = kRowsPerCta;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cheb_smq<GW, MODE, RPC>, kThreads, 0);
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaMemsetAsync(counters, 0, nsm * sizeof(int), s);
+  k_cheb_smq<GW, MODE, RPC><<<(unsigned)(nsm * std::max(per_sm, 1)), kThreads, 0, s>>>(A, counters, nsm);
+}
+
 template <int GW>
 void launch_step_gw(const StepArgs& A, int mode, cudaStream_t s) {
   constexpr int RPC = kRowsPerCta;
+  if (kSmQueue && A.counters) {
+    switch (mode) {
+      case MODE_NONE: launch_smq_mode<GW, MODE_NONE>(A, A.counters, s); break;
+      case MODE_SK_PSI: launch_smq_mode<GW, MODE_SK_PSI>(A, A.counters, s); break;
+      case MODE_SK_PHI: launch_smq_mode<GW, MODE_SK_PHI>(A, A.counters, s); break;
+      default: launch_smq_mode<GW, MODE_BARY_PSI>(A, A.counters, s); break;
+    }
+    return;
+  }
   dim3 grid((unsigned)(A.tiles * A.Gl));
   switch (mode) {
     case MODE_NONE: k_cheb_step<GW, MODE_NONE, RPC><<<grid, kThreads, 0, s>>>(A); break;
@@ -1148,7 +1270,7 @@ struct Work {
   DevBuf<double> T[2], acc;
   DevBuf<unsigned long long> cmin, cmax;
   DevBuf<double> thr, errcol, part_err;
-  DevBuf<int> active, gactive;
+  DevBuf<int> active, gactive, counters;
   DevBuf<gs_status> status;
   int init(gs_ctx* ctx, int n_, int B_, bool want_err, const gs_filter* f = nullptr) {
     cudaStream_t s = ctx->stream;
@@ -1177,6 +1299,7 @@ struct Work {
     GS_CUDA(ctx, errcol.alloc(Bpad, s));
     GS_CUDA(ctx, part_err.alloc(want_err ? (size_t)tiles * Bpad : 1, s));
     GS_CUDA(ctx, active.alloc(Bpad, s));
+    GS_CUDA(ctx, counters.alloc(1024, s));
     GS_CUDA(ctx, gactive.alloc(G, s));
     {
       std::vector<int> ga(G);
@@ -1233,6 +1356,7 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work& w, int a0, int mode, const 
   A.M = M;
   A.Vcur = Vcur;
   A.Wout = Wout;
+  A.counters = w.counters.get();
   A.slot = f->tiles.slot;
   A.bfirst = f->tiles.bfirst;
   A.bcount = f->tiles.bcount;
