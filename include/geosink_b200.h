@@ -49,6 +49,7 @@ extern "C" {
 /* gs_sinkhorn flags */
 #define GS_FLAG_SINGLE 1             /* sinkhorn_single messages (transport.cpp:132-134) */
 #define GS_FLAG_NO_STAGNATION_ABORT 2 /* bench-only deviation: never raise Disconnected */
+#define GS_FLAG_FP32 4                /* optional fp32 mode (vectors and L_s in fp32) */
 
 typedef struct gs_ctx gs_ctx;
 typedef struct gs_graph gs_graph;   /* SparseSymMatrix on device (sparse.hpp:23-61) */
@@ -112,6 +113,9 @@ int gs_filter_order(gs_ctx* ctx, const gs_filter* f, int* order, int mem);
 /* p_K(L_s) X for `width` contiguous n-vectors (heat.cpp:98-131). */
 int gs_filter_apply(gs_ctx* ctx, const gs_filter* f, const double* X, double* Y, int width,
                     int mem);
+/* Same with flags (GS_FLAG_FP32 selects the fp32 mode). */
+int gs_filter_apply_ex(gs_ctx* ctx, const gs_filter* f, const double* X, double* Y, int width,
+                       int mem, int flags);
 
 /* ---- transport (transport.hpp:58-69, transport.cpp:108-255) -------------------------- */
 /* P pairs against one filter (geodesic_sinkhorn_batch; P = 1 + GS_FLAG_SINGLE is
@@ -138,6 +142,11 @@ int gs_barycenter(gs_ctx* ctx, const gs_filter* f, const double* a, const double
                   int m, const double* alphas, int max_iter, double tol, int mem,
                   const gs_comm* comm, double* out_bary, double* out_V, double* out_W,
                   int* out_iters, int* out_conv, double* out_err);
+/* Same with flags (GS_FLAG_FP32 selects the fp32 mode). */
+int gs_barycenter_ex(gs_ctx* ctx, const gs_filter* f, const double* a, const double* members,
+                     int m, const double* alphas, int max_iter, double tol, int mem,
+                     const gs_comm* comm, int flags, double* out_bary, double* out_V,
+                     double* out_W, int* out_iters, int* out_conv, double* out_err);
 
 /* ---- seeded RNG (rng.hpp:13-68), host-side ---------------------------------------------- */
 typedef struct gs_rng gs_rng;

@@ -19,6 +19,7 @@ GS_MEM_HOST = 0
 GS_MEM_DEVICE = 1
 GS_FLAG_SINGLE = 1
 GS_FLAG_NO_STAGNATION_ABORT = 2
+GS_FLAG_FP32 = 4
 
 # (name, restype, argtypes) for every symbol declared in include/geosink_b200.h
 _vp = C.c_void_p
@@ -66,10 +67,13 @@ SIGNATURES = {
     "gs_filter_scaled": (_vp, [_vp]),
     "gs_filter_order": (_i, [_vp, _vp, _vp, _i]),
     "gs_filter_apply": (_i, [_vp, _vp, _vp, _vp, _i, _i]),
+    "gs_filter_apply_ex": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i]),
     "gs_sinkhorn": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _d, _i, _i, _vp, _vp, _vp, _vp, _vp,
                          _vp, _vp, _pi, _pi]),
     "gs_barycenter": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _d, _i, _vp, _vp, _vp, _vp, _vp,
                            _vp, _vp]),
+    "gs_barycenter_ex": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _d, _i, _vp, _i, _vp, _vp, _vp,
+                              _vp, _vp, _vp]),
     "gs_rng_create": (_vp, [C.c_uint64]),
     "gs_rng_destroy": (None, [_vp]),
     "gs_rng_bits": (C.c_uint64, [_vp]),

@@ -57,19 +57,6 @@ struct gs_graph {
   int device = 0;
 };
 
-// Neighbour staging plan (gs_tiles.cu): per block of R rows of the locality-ordered L_s, the runs
-// of column rows it references and, per CSR entry, the column's slot in the staged window.
-struct gs_tileplan {
-  int R = 0, nblocks = 0, nruns = 0, max_slots = 0, max_runs = 0;
-  double mean_slots = 0.0;
-  int* bfirst = nullptr;   // first run of each block (-1 when the block has no entries)
-  int* bcount = nullptr;   // runs per block
-  int* rstart = nullptr;   // first row of each run
-  int* rlen = nullptr;     // rows per run
-  int* lbase = nullptr;    // slot of the run's first row inside its block's window
-  unsigned short* slot = nullptr;  // per entry of the permuted CSR
-};
-
 struct gs_filter {
   gs_graph* scaled = nullptr;   // L_s in the caller's vertex order (heat.hpp:47)
   gs_graph* perm = nullptr;     // L_s with rows renumbered for locality (gs_reorder.cu)
@@ -79,7 +66,7 @@ struct gs_filter {
   int degree = 0, kind = 0;
   std::vector<double> coeffs;  // host mirror (heat.hpp:37)
   double* d_coeffs = nullptr;
-  gs_tileplan tiles;           // staging plan over `perm` (empty when not built)
+  float* vals32 = nullptr;     // fp32 copy of perm->vals (optional fp32 mode)
 };
 
 // ---- error plumbing ----------------------------------------------------------------------
@@ -152,7 +139,5 @@ int gs_coefficients_impl(gs_ctx* ctx, double t, int degree, double* d_out, doubl
 int gs_bfs_order(gs_ctx* ctx, const gs_graph* g, int* d_order, int* d_newpos);
 int gs_permute_graph(gs_ctx* ctx, const gs_graph* g, const int* d_order, const int* d_newpos,
                      gs_graph** out);
-int gs_tiles_build(gs_ctx* ctx, const gs_graph* g, int R, gs_tileplan* out);
-void gs_tiles_release(gs_tileplan& t);
 int gs_csr_from_sorted_entries(gs_ctx* ctx, int n, int64_t m, const unsigned long long* d_keys,
                                const double* d_vals, bool check_dups, gs_graph** out);

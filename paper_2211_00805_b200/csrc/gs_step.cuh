@@ -1,0 +1,437 @@
+// gs_step.cuh -- the fused Chebyshev step kernel, templated on the scalar type S (double: the
+// reference-exact path; float: the optional fp32 mode).
+//
+// Reference path: HeatFilter::apply (proj/src/heat.cpp:116-131) over
+// SparseSymMatrix::multiply (proj/src/sparse.cpp:85-99), called twice per sweep by sinkhorn_many
+// (proj/src/transport.cpp:144-239) and sinkhorn_barycenter (proj/src/barycenter.cpp:45-99).
+//
+// Layout ("grouped row-major"): a block of B vertex signals is G = B/GW column groups, each an
+// n x GW row-major array (GW <= 64). A row segment of GW*sizeof(S) bytes is read by LPR lanes with
+// 16-byte vector loads; a warp covers 32/LPR rows. A CTA covers RPC consecutive blocks of
+// (8 warps x rows-per-warp) rows of one group, so neighbouring gathers share L1 lines (the
+// vertices are in Cuthill-McKee order, gs_reorder.cu).
+//
+// One step k >= 2 (heat.cpp:124-130), per row i and column:
+//     y   = sum_p vals[p] * T_{k-1}[cols[p]]        (fma chain from +0, CSR order)
+//     T_k = 2 * (y - T_{k-1}[i]) - T_{k-2}[i]        (T_k overwrites T_{k-2} in place)
+//     acc = fma(b_k, T_k, acc)
+// Step 1: T_1 = y - T_0, acc = fma(b_1, T_1, (b_0/2) * T_0). The last step (k = K) does not store
+// T_K; its epilogue consumes acc = p_K(L_s) x in registers:
+//     SK_PSI  : psi -> colmin; W = N / max(psi, floor); next T_0 = a * W; colmax |T_0|
+//     SK_PHI  : phi -> colmin; err += |V phi - M|; V' = M / max(phi, floor); next T_0 = a * V'
+//     BARY_PSI: psi -> colmin and stored for the log-domain geometric mean.
+// Column min/max are order-free (atomics on order-preserving keys of the double value); the L1
+// error is accumulated in double through fixed-order per-CTA partials (deterministic).
+#pragma once
+
+#include <cfloat>
+#include <cstring>
+#include <type_traits>
+
+#include "gs_internal.cuh"
+
+namespace gsk {
+
+constexpr int kThreads = 256;
+#ifndef GS_ROWS_PER_CTA
+#define GS_ROWS_PER_CTA 4
+#endif
+constexpr int kRowsPerCta = GS_ROWS_PER_CTA;
+#ifndef GS_GATHER_BATCH
+#define GS_GATHER_BATCH 4
+#endif
+constexpr int kGatherBatch = GS_GATHER_BATCH;  // neighbour rows in flight per lane
+#ifndef GS_PREFETCH_STAGES
+#define GS_PREFETCH_STAGES 2
+#endif
+constexpr int kPrefetchStages = GS_PREFETCH_STAGES;
+
+enum StepMode { MODE_NONE = 0, MODE_SK_PSI = 1, MODE_SK_PHI = 2, MODE_BARY_PSI = 3 };
+
+// ---- precision traits --------------------------------------------------------------------------
+template <typename S>
+struct Prec;
+template <>
+struct Prec<double> {
+  static constexpr double floor = 1e-300;  // kDivisionFloor (transport.cpp:13, barycenter.cpp:9)
+  static constexpr double slack = 1e-12;   // positivity slack (transport.cpp:24,33)
+  __device__ static __forceinline__ double fmat(double a, double b, double c) { return fma(a, b, c); }
+};
+template <>
+struct Prec<float> {
+  // fp32 mode has no reference (SURVEY §7 hard part 7): 1e-300 underflows and 1e-12 is below
+  // fp32 epsilon, so the floor is FLT_MIN and the slack 64 FLT_EPSILON.
+  static constexpr float floor = FLT_MIN;
+  static constexpr double slack = 64.0 * (double)FLT_EPSILON;
+  __device__ static __forceinline__ float fmat(float a, float b, float c) { return fmaf(a, b, c); }
+};
+
+template <int GW, typename S>
+struct Lay {
+  static constexpr int VEC = GW * (int)sizeof(S) >= 16 ? 16 / (int)sizeof(S) : GW;
+  static constexpr int LPR = GW / VEC;                 // lanes per row
+  static constexpr int RPW = 32 / LPR;                 // rows per warp
+  static constexpr int ROWS = (kThreads / 32) * RPW;   // rows per CTA block
+};
+
+// order-preserving uint64 keys for doubles (atomic min/max of signed values)
+__device__ __forceinline__ unsigned long long dkey(double x) {
+  unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dunkey(unsigned long long k) {
+  unsigned long long b = (k & 0x8000000000000000ull) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  return __longlong_as_double((long long)b);
+}
+constexpr unsigned long long KEY_POS_INF = 0xFFF0000000000000ull;  // dkey(+inf)
+constexpr unsigned long long KEY_ZERO = 0x8000000000000000ull;     // dkey(+0.0)
+
+// 16/8/4-byte vector moves between memory and a register array (explicit components, so the
+// array stays in registers)
+template <typename S, int VEC, bool RO>
+__device__ __forceinline__ void ld_vec_impl(const S* p, S (&v)[VEC]) {
+  if constexpr (std::is_same<S, double>::value && VEC == 2) {
+    const double2 t = RO ? __ldg(reinterpret_cast<const double2*>(p)) : *reinterpret_cast<const double2*>(p);
+    v[0] = t.x;
+    v[1] = t.y;
+  } else if constexpr (std::is_same<S, float>::value && VEC == 4) {
+    const float4 t = RO ? __ldg(reinterpret_cast<const float4*>(p)) : *reinterpret_cast<const float4*>(p);
+    v[0] = t.x;
+    v[1] = t.y;
+    v[2] = t.z;
+    v[3] = t.w;
+  } else if constexpr (std::is_same<S, float>::value && VEC == 2) {
+    const float2 t = RO ? __ldg(reinterpret_cast<const float2*>(p)) : *reinterpret_cast<const float2*>(p);
+    v[0] = t.x;
+    v[1] = t.y;
+  } else {
+    static_assert(VEC == 1, "vector width");
+    v[0] = RO ? __ldg(p) : *p;
+  }
+}
+template <typename S, int VEC>
+__device__ __forceinline__ void ld_vec(const S* p, S (&v)[VEC]) {  // read-only path
+  ld_vec_impl<S, VEC, true>(p, v);
+}
+template <typename S, int VEC>
+__device__ __forceinline__ void ld_vec_rw(const S* p, S (&v)[VEC]) {
+  ld_vec_impl<S, VEC, false>(p, v);
+}
+template <typename S, int VEC>
+__device__ __forceinline__ void st_vec(S* p, const S (&v)[VEC]) {
+  if constexpr (std::is_same<S, double>::value && VEC == 2) {
+    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+  } else if constexpr (std::is_same<S, float>::value && VEC == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  } else if constexpr (std::is_same<S, float>::value && VEC == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+  } else {
+    *p = v[0];
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+struct ColState {  // per column (Bpad entries each)
+  int* active;               // nullable
+  int* gactive;              // active columns per group (nullable)
+  unsigned long long* cmin;  // min of the apply output
+  unsigned long long* cmax;  // max |next T_0|
+  double* thr;               // positivity threshold of the current apply
+  double* errcol;            // L1 marginal error
+  double* part_err;          // [tiles][Bpad]
+};
+
+struct StepArgs {  // vector pointers are S* of the launch's precision
+  const int* __restrict__ offs;
+  const int* __restrict__ cols;
+  const void* vals;
+  int n, tiles, g0, Gl, Bpad;
+  const void* Tprev;  // T_{k-1}
+  void* Tout;         // T_{k-2} in, T_k out (or next T_0 / SpMM output)
+  void* acc;
+  double bk, b0h;
+  int k;              // 0 = plain SpMM into Tout
+  const gs_status* status;
+  ColState cs;
+  const void* a;      // n (epilogue)
+  const void* M;      // PSI: N (targets); PHI: M (sources / members)
+  const void* Vcur;   // PHI: V of this sweep
+  void* Wout;         // PSI: W; PHI: V of the next sweep
+};
+
+// One row of one Chebyshev step; epilogue partials accumulate in mn/mx/er (double).
+template <typename S, int GW, int MODE>
+__device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int sub, int q,
+                                         double (&mn)[Lay<GW, S>::VEC],
+                                         double (&mx)[Lay<GW, S>::VEC],
+                                         double (&er)[Lay<GW, S>::VEC], const S* pre,
+                                         int pre_stride) {
+  using L = Lay<GW, S>;
+  constexpr int VEC = L::VEC, LPR = L::LPR;
+  using P = Prec<S>;
+  const bool valid = row < A.n;
+  const size_t gbase = (size_t)g * A.n * GW + q * VEC;
+  const size_t idx = gbase + (size_t)(valid ? row : 0) * GW;
+  const S* __restrict__ Tp = static_cast<const S*>(A.Tprev) + gbase;
+  const S* __restrict__ vals = static_cast<const S*>(A.vals);
+  // ---- y = L_s T_{k-1} (row) ------------------------------------------------------------------
+  S y[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) y[e] = S(0);
+  if constexpr (LPR == 1) {
+    if (valid) {
+      int p = __ldg(A.offs + row);
+      const int pe = __ldg(A.offs + row + 1);
+      for (; p + 4 <= pe; p += 4) {
+        int cc[4];
+        S vv[4];
+        S xx[4][VEC];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          cc[u] = __ldg(A.cols + p + u);
+          vv[u] = __ldg(vals + p + u);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) ld_vec<S, VEC>(Tp + (size_t)cc[u] * GW, xx[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) y[e] = P::fmat(vv[u], xx[u][e], y[e]);
+      }
+      for (; p < pe; ++p) {
+        const int c = __ldg(A.cols + p);
+        const S v = __ldg(vals + p);
+        S x[VEC];
+        ld_vec<S, VEC>(Tp + (size_t)c * GW, x);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) y[e] = P::fmat(v, x[e], y[e]);
+      }
+    }
+  } else {
+    // the LPR lanes of a row load LPR consecutive (col, val) entries with one coalesced access
+    // and broadcast them by shuffle; the fma chain still runs in CSR order.
+    const int sub_lane0 = sub * LPR;
+    const unsigned mask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << sub_lane0);
+    const int pb = valid ? __ldg(A.offs + row) : 0;
+    const int pe = valid ? __ldg(A.offs + row + 1) : 0;
+    constexpr int GB = kGatherBatch;
+    for (int p0 = pb; p0 < pe; p0 += LPR) {
+      int myc = 0;
+      S myv = S(0);
+      if (p0 + q < pe) {
+        myc = __ldg(A.cols + p0 + q);
+        myv = __ldg(vals + p0 + q);
+      }
+      const int cnt = min(LPR, pe - p0);
+      int u = 0;
+      for (; u + GB <= cnt; u += GB) {
+        int cc[GB];
+        S vv[GB];
+        S xx[GB][VEC];
+#pragma unroll
+        for (int j = 0; j < GB; ++j) {
+          cc[j] = __shfl_sync(mask, myc, u + j, LPR);
+          vv[j] = __shfl_sync(mask, myv, u + j, LPR);
+        }
+#pragma unroll
+        for (int j = 0; j < GB; ++j) ld_vec<S, VEC>(Tp + (size_t)cc[j] * GW, xx[j]);
+#pragma unroll
+        for (int j = 0; j < GB; ++j)
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) y[e] = P::fmat(vv[j], xx[j][e], y[e]);
+      }
+      for (; u < cnt; ++u) {
+        const int c = __shfl_sync(mask, myc, u, LPR);
+        const S v = __shfl_sync(mask, myv, u, LPR);
+        S x[VEC];
+        ld_vec<S, VEC>(Tp + (size_t)c * GW, x);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) y[e] = P::fmat(v, x[e], y[e]);
+      }
+    }
+  }
+  if (!valid) return;
+  if (A.k == 0) {  // plain SpMM (sparse.cpp:85-99)
+    st_vec<S, VEC>(static_cast<S*>(A.Tout) + idx, y);
+    return;
+  }
+  // ---- own-row operands (prefetched into shared memory by cp.async when `pre`) ---------------
+  S tp[VEC], t2[VEC], a0[VEC];
+  if (pre) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      tp[e] = pre[e];
+      t2[e] = pre[pre_stride + e];
+      a0[e] = pre[2 * pre_stride + e];
+    }
+  } else {
+    ld_vec<S, VEC>(static_cast<const S*>(A.Tprev) + idx, tp);
+    if (A.k >= 2) {
+      ld_vec_rw<S, VEC>(static_cast<const S*>(A.Tout) + idx, t2);
+      ld_vec_rw<S, VEC>(static_cast<const S*>(A.acc) + idx, a0);
+    }
+  }
+  // ---- recurrence (heat.cpp:121-130) ----------------------------------------------------------
+  const S bk = S(A.bk);
+  S t[VEC], ac[VEC];
+  if (A.k == 1) {
+    const S b0h = S(A.b0h);
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      t[e] = y[e] - tp[e];
+      ac[e] = P::fmat(bk, t[e], b0h * tp[e]);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      t[e] = S(2) * (y[e] - tp[e]) - t2[e];
+      ac[e] = P::fmat(bk, t[e], a0[e]);
+    }
+  }
+  if constexpr (MODE == MODE_NONE) {
+    st_vec<S, VEC>(static_cast<S*>(A.Tout) + idx, t);
+    st_vec<S, VEC>(static_cast<S*>(A.acc) + idx, ac);
+  } else {
+    // ---- fused epilogue of the last step --------------------------------------------------
+    const int* act = A.cs.active;
+    const int col0 = g * GW + q * VEC;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) mn[e] = fmin(mn[e], (double)ac[e]);
+    if constexpr (MODE == MODE_SK_PSI || MODE == MODE_SK_PHI) {
+      S op1[VEC], nx[VEC], t0[VEC];
+      ld_vec<S, VEC>(static_cast<const S*>(A.M) + idx, op1);
+      const S ai = __ldg(static_cast<const S*>(A.a) + row);
+      if constexpr (MODE == MODE_SK_PHI) {
+        S v[VEC];
+        ld_vec_rw<S, VEC>(static_cast<const S*>(A.Vcur) + idx, v);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) er[e] = er[e] + (double)fabs(v[e] * ac[e] - op1[e]);  // transport.cpp:184
+      }
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        nx[e] = op1[e] / fmax(ac[e], P::floor);  // W (transport.cpp:180) / V' (:178)
+        t0[e] = ai * nx[e];                      // a .* x (transport.cpp:172)
+        mx[e] = fmax(mx[e], (double)fabs(t0[e]));
+      }
+      st_vec<S, VEC>(static_cast<S*>(A.Tout) + idx, t0);
+      S* wo = static_cast<S*>(A.Wout) + idx;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        if (!act || act[col0 + e]) wo[e] = nx[e];
+    } else {  // MODE_BARY_PSI
+      st_vec<S, VEC>(static_cast<S*>(A.acc) + idx, ac);
+    }
+  }
+}
+
+// CTA-level fold of the epilogue partials: min/max by atomics on keys, error partial per tile.
+template <typename S, int GW, int MODE>
+__device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int tile, int warp, int sub,
+                                               int q, double (&mn)[Lay<GW, S>::VEC],
+                                               double (&mx)[Lay<GW, S>::VEC],
+                                               double (&er)[Lay<GW, S>::VEC]) {
+  using L = Lay<GW, S>;
+  constexpr int VEC = L::VEC, LPR = L::LPR;
+#pragma unroll
+  for (int off = LPR; off < 32; off <<= 1) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      mn[e] = fmin(mn[e], __shfl_xor_sync(0xffffffffu, mn[e], off));
+      mx[e] = fmax(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], off));
+      er[e] = er[e] + __shfl_xor_sync(0xffffffffu, er[e], off);
+    }
+  }
+  __shared__ double s_mn[kThreads / 32][GW], s_mx[kThreads / 32][GW], s_er[kThreads / 32][GW];
+  if (sub == 0) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      s_mn[warp][q * VEC + e] = mn[e];
+      s_mx[warp][q * VEC + e] = mx[e];
+      s_er[warp][q * VEC + e] = er[e];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < GW) {
+    const int c = threadIdx.x;
+    double a_mn = s_mn[0][c], a_mx = s_mx[0][c], a_er = s_er[0][c];
+#pragma unroll
+    for (int w = 1; w < kThreads / 32; ++w) {
+      a_mn = fmin(a_mn, s_mn[w][c]);
+      a_mx = fmax(a_mx, s_mx[w][c]);
+      a_er = a_er + s_er[w][c];
+    }
+    const int col = g * GW + c;
+    atomicMin(A.cs.cmin + col, dkey(a_mn));
+    if constexpr (MODE == MODE_SK_PSI || MODE == MODE_SK_PHI) atomicMax(A.cs.cmax + col, dkey(a_mx));
+    if constexpr (MODE == MODE_SK_PHI) A.cs.part_err[(size_t)tile * A.Bpad + col] = a_er;
+  }
+}
+
+// A CTA owns RPC x (8 warps x rows-per-warp) consecutive rows of one column group. Own-row
+// operands of the next row block (T_{k-1}[i], T_{k-2}[i], acc[i]) are copied to shared memory with
+// cp.async while this block's neighbour gathers run (16-byte vector rows only).
+template <typename S, int GW, int MODE, int RPC>
+__global__ void __launch_bounds__(kThreads) k_cheb_step(const StepArgs A) {
+  using L = Lay<GW, S>;
+  constexpr int VEC = L::VEC, LPR = L::LPR, RPW = L::RPW;
+  constexpr int BLOCK_ROWS = (kThreads / 32) * RPW;
+  constexpr bool PREFETCH = VEC * sizeof(S) == 16;
+  if (A.status && (A.status->error || A.status->done)) return;
+  const int tile = blockIdx.x / A.Gl;
+  const int g = A.g0 + blockIdx.x % A.Gl;
+  if (A.cs.gactive && A.cs.gactive[g] == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / LPR, q = lane % LPR;
+  double mn[VEC], mx[VEC], er[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    mn[e] = INFINITY;
+    mx[e] = 0.0;
+    er[e] = 0.0;
+  }
+  const int base = tile * (BLOCK_ROWS * RPC) + warp * RPW + sub;
+  if constexpr (PREFETCH) {
+    constexpr int STG = kPrefetchStages;
+    constexpr int PS = kThreads * VEC;  // elements per operand per stage
+    __shared__ __align__(16) S s_pre[STG][3][PS];
+    const size_t gbase = (size_t)g * A.n * GW + q * VEC;
+    auto issue = [&](int j) {
+      const int row = base + j * BLOCK_ROWS;
+      if (j < RPC && row < A.n && A.k != 0) {
+        const size_t idx = gbase + (size_t)row * GW;
+        S* d = &s_pre[j % STG][0][threadIdx.x * VEC];
+        cp_async16(d, static_cast<const S*>(A.Tprev) + idx);
+        if (A.k >= 2) {
+          cp_async16(d + PS, static_cast<const S*>(A.Tout) + idx);
+          cp_async16(d + 2 * PS, static_cast<const S*>(A.acc) + idx);
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int j = 0; j < STG - 1; ++j) issue(j);
+#pragma unroll 1
+    for (int j = 0; j < RPC; ++j) {
+      issue(j + STG - 1);
+      cp_async_wait<STG - 1>();
+      cheb_row<S, GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er,
+                            &s_pre[j % STG][0][threadIdx.x * VEC], PS);
+    }
+  } else {
+#pragma unroll 1
+    for (int j = 0; j < RPC; ++j)
+      cheb_row<S, GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er, nullptr, 0);
+  }
+  if constexpr (MODE != MODE_NONE) block_epilogue<S, GW, MODE>(A, g, tile, warp, sub, q, mn, mx, er);
+}
+
+}  // namespace gsk

@@ -414,16 +414,18 @@ class HeatFilter:
                                                       _capi.GS_MEM_HOST))
         return out
 
-    def apply(self, f) -> np.ndarray:
-        """heat.cpp:98-131: (n,) vector or row-major (n, B) signals."""
+    def apply(self, f, fp32: bool = False) -> np.ndarray:
+        """heat.cpp:98-131: (n,) vector or row-major (n, B) signals. fp32=True runs the optional
+        fp32 mode (vectors and L_s in fp32; results returned as float64)."""
         x = _f64(f)
         if x.shape[0] != self._n:
             raise Error(errc.length_mismatch, "LengthMismatch: signal length")
         cols = _f64(x.reshape(self._n, -1).T)
         out = np.empty_like(cols)
-        self._ctx.check(self._ctx.lib.gs_filter_apply(self._ctx.handle, self._h, _ptr(cols),
-                                                      _ptr(out), cols.shape[0],
-                                                      _capi.GS_MEM_HOST))
+        self._ctx.check(self._ctx.lib.gs_filter_apply_ex(self._ctx.handle, self._h, _ptr(cols),
+                                                         _ptr(out), cols.shape[0],
+                                                         _capi.GS_MEM_HOST,
+                                                         _capi.GS_FLAG_FP32 if fp32 else 0))
         return out.T.reshape(x.shape).copy()
 
     def __del__(self):
@@ -559,16 +561,21 @@ def _sinkhorn(filter: HeatFilter, mus, nus, a, params: SinkhornParams, flags: in
 
 
 def geodesic_sinkhorn(filter: HeatFilter, mu: Distribution, nu: Distribution, a,
-                      params: SinkhornParams = SinkhornParams()) -> TransportResult:
+                      params: SinkhornParams = SinkhornParams(), fp32: bool = False) -> TransportResult:
     """transport.cpp:243-247 (sinkhorn_single semantics and messages)."""
-    return _sinkhorn(filter, [mu], [nu], a, params, _capi.GS_FLAG_SINGLE)[0]
+    flags = _capi.GS_FLAG_SINGLE | (_capi.GS_FLAG_FP32 if fp32 else 0)
+    return _sinkhorn(filter, [mu], [nu], a, params, flags)[0]
 
 
 def geodesic_sinkhorn_batch(filter: HeatFilter, mus: List[Distribution], nus: List[Distribution],
                             a, params: SinkhornParams = SinkhornParams(),
-                            no_stagnation_abort: bool = False) -> List[TransportResult]:
-    """transport.cpp:249-255. `no_stagnation_abort` is the bench-only deviation."""
+                            no_stagnation_abort: bool = False,
+                            fp32: bool = False) -> List[TransportResult]:
+    """transport.cpp:249-255. `no_stagnation_abort` is the bench-only deviation (DESIGN.md);
+    `fp32` the optional fp32 mode."""
     flags = _capi.GS_FLAG_NO_STAGNATION_ABORT if no_stagnation_abort else 0
+    if fp32:
+        flags |= _capi.GS_FLAG_FP32
     return _sinkhorn(filter, mus, nus, a, params, flags)
 
 
@@ -611,7 +618,8 @@ class BarycenterResult:
 
 
 def sinkhorn_barycenter(filter: HeatFilter, family: DistributionFamily, a,
-                        params: SinkhornParams = SinkhornParams()) -> BarycenterResult:
+                        params: SinkhornParams = SinkhornParams(),
+                        fp32: bool = False) -> BarycenterResult:
     """barycenter.cpp:45-99."""
     ctx = filter._ctx
     n = filter.size()
@@ -629,10 +637,10 @@ def sinkhorn_barycenter(filter: HeatFilter, family: DistributionFamily, a,
     it = np.zeros(1, np.int32)
     conv = np.zeros(1, np.int32)
     err = np.zeros(1)
-    ctx.check(ctx.lib.gs_barycenter(ctx.handle, filter._h, _ptr(a), _ptr(members), m, _ptr(al),
-                                    int(params.max_iter), float(params.tol), _capi.GS_MEM_HOST,
-                                    None, _ptr(bary), _ptr(V), _ptr(W), _ptr(it), _ptr(conv),
-                                    _ptr(err)))
+    ctx.check(ctx.lib.gs_barycenter_ex(ctx.handle, filter._h, _ptr(a), _ptr(members), m, _ptr(al),
+                                       int(params.max_iter), float(params.tol), _capi.GS_MEM_HOST,
+                                       None, _capi.GS_FLAG_FP32 if fp32 else 0, _ptr(bary), _ptr(V),
+                                       _ptr(W), _ptr(it), _ptr(conv), _ptr(err)))
     return BarycenterResult(Distribution(bary, validate=False),
                             [(V[c].copy(), W[c].copy()) for c in range(m)], int(it[0]),
                             bool(conv[0]), float(err[0]))
