@@ -108,6 +108,11 @@ def dist_env():
     return rank, world, local
 
 
+def _max_rel(a, b):
+    ok = np.isfinite(a) & np.isfinite(b) & (b != 0)
+    return float(np.max(np.abs(a[ok] - b[ok]) / np.abs(b[ok]))) if ok.any() else None
+
+
 def algorithmic_bytes_per_step(n, nnz, B, sv=8):
     """matrix values + int32 indices + int32 offsets + 5 vector streams."""
     return nnz * (sv + 4) + 4 * (n + 1) + 5 * n * B * sv
@@ -140,7 +145,7 @@ def run_reference(args):
     from paper_2211_00805_b200 import workloads
 
     lib = po.lib(native=True)
-    cfg = workloads.config1(args.n, args.pairs, seed=1, pair_seed=2)
+    cfg = make_config(args)
     t0 = time.perf_counter()
     A, sigma = po.knn_graph(cfg.roll.points, cfg.k, 1, 0.0)
     L, lam, rounds = po.laplacian(A, 0)
@@ -176,9 +181,20 @@ def run_reference(args):
     return 0
 
 
+def make_config(args, rank=0):
+    from paper_2211_00805_b200 import workloads
+    if args.config == 0:
+        # config 0: one pair of s-bumps at 2pi / 4pi (width 0.5) on the n=2000 roll, 100 sweeps
+        roll = workloads.swiss_roll(args.n, 1)
+        mu = workloads.bump_in_s(roll, 2 * math.pi, 0.5)[None, :]
+        nu = workloads.bump_in_s(roll, 4 * math.pi, 0.5)[None, :]
+        return workloads.Config1(roll, mu, nu, sweeps=args.sweeps)
+    return workloads.config1(args.n, args.pairs, seed=1, pair_seed=2 + 1000 * rank)
+
+
 def config_dict(args, nnz_A, lam, rounds, sigma, extra=None):
     d = {
-        "workload": (f"config1: swiss roll n={args.n}, k=10 symmetrised kNN, Gaussian weights "
+        "workload": (f"config{args.config}: swiss roll n={args.n}, k=10 symmetrised kNN, Gaussian weights "
                      f"sigma=median eps_10, combinatorial L, t=1, K=30, {args.pairs} pairs x "
                      f"{args.sweeps} sweeps (2 x {args.pairs}-column applies per sweep), fp64"),
         "n": args.n, "pairs": args.pairs, "sweeps_per_step": args.sweeps, "degree": 30,
@@ -205,12 +221,15 @@ def run_engine(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx = gs.Context(local)
-    stream = torch.cuda.current_stream()
+    # a dedicated non-blocking stream shared by torch and the engine (the legacy default stream
+    # serialises stream-ordered allocations and cannot be graph-captured)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     lib = ctx.lib
 
     # ---- setup: graph build + Laplacian + lambda + filter, all on the device -------------------
-    cfg = workloads.config1(args.n, args.pairs, seed=1, pair_seed=2 + 1000 * rank)
+    cfg = make_config(args, rank)
     t0 = time.perf_counter()
     A, sigma = gs.knn_gaussian_graph(cfg.roll.points, cfg.k, ctx=ctx)
     t_graph = time.perf_counter() - t0
@@ -278,6 +297,17 @@ def run_engine(args):
     elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
     value = world * args.sweeps * args.steps / (elapsed_ms / 1000.0)
 
+    if step_n == 0:
+        # small problems replay CUDA graphs (no per-launch events): time the step kernel in one
+        # extra non-graph run of the same workload
+        os.environ["GS_GRAPH"] = "0"
+        ctx.set_timing(True)
+        step()
+        torch.cuda.synchronize()
+        step_n, step_ms = ctx.timing(0)
+        ctx.set_timing(False)
+        del os.environ["GS_GRAPH"]
+
     # ---- roofline of the dominant kernel ------------------------------------------------------
     peak, peak_kind = peaks()
     bytes_step = algorithmic_bytes_per_step(n, nnz_L, P)
@@ -325,6 +355,45 @@ def run_engine(args):
     h2d = 2 * P * n * 8 + n * 8
     d2h = 2 * P * n * 8 + P * (8 + 8 + 4 + 4 + 8)
 
+    # ---- fp32 mode on the same workload (config 1 is specified "fp64 and fp32") ------------------
+    fp32 = None
+    if not args.no_fp32:
+        flags32 = flags | _capi.GS_FLAG_FP32
+
+        def step32():
+            ctx.check(lib.gs_sinkhorn(ctx.handle, filt._h, a.data_ptr(), M.data_ptr(), N.data_ptr(),
+                                      P, args.sweeps, TOL_RUN_ALL, flags32, _capi.GS_MEM_DEVICE,
+                                      ov.data_ptr(), ow.data_ptr(), oc.data_ptr(), ok.data_ptr(),
+                                      oi.data_ptr(), occ.data_ptr(), oe.data_ptr(), C.byref(fp),
+                                      C.byref(fs)))
+
+        step32()  # warm-up of the fp32 instantiation
+        step()
+        cost64 = oc.cpu().numpy().copy()
+        step32()
+        cost32 = oc.cpu().numpy().copy()
+        torch.cuda.synchronize()
+        barrier()
+        ctx.set_timing(True)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        k32 = max(1, min(args.steps, 2))
+        e0.record(stream)
+        for _ in range(k32):
+            step32()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        n32, ms32 = ctx.timing(0)
+        ctx.set_timing(False)
+        el32 = max_over_ranks(e0.elapsed_time(e1))
+        bytes32 = nnz_L * (4 + 4) + 4 * (n + 1) + 5 * n * P * 4
+        avg32 = ms32 / max(n32, 1)
+        fp32 = {"value": world * args.sweeps * k32 / (el32 / 1000.0), "unit": UNIT, "steps": k32,
+                "avg_step_kernel_ms": avg32, "bytes_per_launch": bytes32,
+                "achieved_GBs": bytes32 / (avg32 / 1000.0) / 1e9,
+                "max_rel_cost_vs_fp64": _max_rel(cost32, cost64),
+                "finite_costs": int(np.isfinite(cost32).sum()), "pairs": int(P)}
+
     # ---- CPU baseline (rank 0, N = 1) ---------------------------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -361,6 +430,7 @@ def run_engine(args):
             "clocks": clocks,
             "epilogue_kernels": {"launches": epi_n, "ms": epi_ms},
             "cpu_baseline": cpu,
+            "fp32_mode": fp32,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -381,7 +451,16 @@ def main():
     ap.add_argument("--cpu-sweeps", type=int, default=1)
     ap.add_argument("--ref-sweeps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true")
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1])
     args = ap.parse_args()
+    if args.config == 0:  # BASELINE.json configs[0]: n=2000, one pair, 100 sweeps
+        if args.n == 200_000:
+            args.n = 2000
+        if args.pairs == 64:
+            args.pairs = 1
+        if args.sweeps == 200:
+            args.sweeps = 100
     if args.impl == "reference":
         return run_reference(args)
     return run_engine(args)

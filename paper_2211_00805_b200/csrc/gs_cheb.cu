@@ -70,14 +70,15 @@ struct CtlArgs {
   int* final_sweep;
   double* err_out;
   gs_status* status;
-  int P, sweep, max_iter, no_abort;
+  int* sweep_ctr;  // device sweep counter (so a captured sweep can be replayed)
+  int P, max_iter, no_abort;
   double tol;
 };
 
 __global__ void k_sk_control(const CtlArgs C) {
   gs_status* st = C.status;
-  if (st->error) return;
-  const int s = C.sweep;
+  const int s = ++(*C.sweep_ctr);
+  if (st->error || s > C.max_iter) return;
   int na = 0;
   for (int c = 0; c < C.P; ++c) {
     if (!C.active[c]) continue;
@@ -450,21 +451,29 @@ int choose_gw(int width) {
 }
 
 template <typename S>
-int rows_per_cta(int gw) {
+int rows_per_block(int gw) {  // rows covered by one CTA pass (8 warps)
   switch (gw) {
-    case 64: return Lay<64, S>::ROWS * kRowsPerCta;
-    case 32: return Lay<32, S>::ROWS * kRowsPerCta;
-    case 16: return Lay<16, S>::ROWS * kRowsPerCta;
-    case 8: return Lay<8, S>::ROWS * kRowsPerCta;
-    case 4: return Lay<4, S>::ROWS * kRowsPerCta;
-    case 2: return Lay<2, S>::ROWS * kRowsPerCta;
-    default: return Lay<1, S>::ROWS * kRowsPerCta;
+    case 64: return Lay<64, S>::ROWS;
+    case 32: return Lay<32, S>::ROWS;
+    case 16: return Lay<16, S>::ROWS;
+    case 8: return Lay<8, S>::ROWS;
+    case 4: return Lay<4, S>::ROWS;
+    case 2: return Lay<2, S>::ROWS;
+    default: return Lay<1, S>::ROWS;
   }
 }
 
-template <typename S, int GW>
-void launch_step_gw(const StepArgs& A, int mode, cudaStream_t s) {
-  constexpr int RPC = kRowsPerCta;
+// Row blocks per CTA: kRowsPerCta (L1 reuse across consecutive blocks) unless that leaves fewer
+// than two CTAs per SM, in which case 1 (small, latency-bound problems such as config 0).
+template <typename S>
+int choose_rpc(int n, int gw, int groups) {
+  const int64_t ctas = (int64_t)groups * ((n + rows_per_block<S>(gw) * kRowsPerCta - 1) /
+                                          (rows_per_block<S>(gw) * kRowsPerCta));
+  return ctas < 2 * 148 ? 1 : kRowsPerCta;
+}
+
+template <typename S, int GW, int RPC>
+void launch_step_rpc(const StepArgs& A, int mode, cudaStream_t s) {
   dim3 grid((unsigned)(A.tiles * A.Gl));
   switch (mode) {
     case MODE_NONE: k_cheb_step<S, GW, MODE_NONE, RPC><<<grid, kThreads, 0, s>>>(A); break;
@@ -474,17 +483,23 @@ void launch_step_gw(const StepArgs& A, int mode, cudaStream_t s) {
   }
 }
 
+template <typename S, int GW>
+void launch_step_gw(const StepArgs& A, int mode, int rpc, cudaStream_t s) {
+  if (rpc == 1) launch_step_rpc<S, GW, 1>(A, mode, s);
+  else launch_step_rpc<S, GW, kRowsPerCta>(A, mode, s);
+}
+
 template <typename S>
-void launch_step(gs_ctx* ctx, int gw, const StepArgs& A, int mode) {
+void launch_step(gs_ctx* ctx, int gw, int rpc, const StepArgs& A, int mode) {
   gs_launch_begin(ctx, 0);
   switch (gw) {
-    case 64: launch_step_gw<S, 64>(A, mode, ctx->stream); break;
-    case 32: launch_step_gw<S, 32>(A, mode, ctx->stream); break;
-    case 16: launch_step_gw<S, 16>(A, mode, ctx->stream); break;
-    case 8: launch_step_gw<S, 8>(A, mode, ctx->stream); break;
-    case 4: launch_step_gw<S, 4>(A, mode, ctx->stream); break;
-    case 2: launch_step_gw<S, 2>(A, mode, ctx->stream); break;
-    default: launch_step_gw<S, 1>(A, mode, ctx->stream); break;
+    case 64: launch_step_gw<S, 64>(A, mode, rpc, ctx->stream); break;
+    case 32: launch_step_gw<S, 32>(A, mode, rpc, ctx->stream); break;
+    case 16: launch_step_gw<S, 16>(A, mode, rpc, ctx->stream); break;
+    case 8: launch_step_gw<S, 8>(A, mode, rpc, ctx->stream); break;
+    case 4: launch_step_gw<S, 4>(A, mode, rpc, ctx->stream); break;
+    case 2: launch_step_gw<S, 2>(A, mode, rpc, ctx->stream); break;
+    default: launch_step_gw<S, 1>(A, mode, rpc, ctx->stream); break;
   }
   gs_launch_end(ctx, 0);
 }
@@ -492,7 +507,7 @@ void launch_step(gs_ctx* ctx, int gw, const StepArgs& A, int mode) {
 // Workspace for one batched run: grouped buffers (precision S) + per-column state.
 template <typename S>
 struct Work {
-  int n = 0, B = 0, GW = 1, G = 1, Bpad = 1, tiles = 0;
+  int n = 0, B = 0, GW = 1, G = 1, Bpad = 1, tiles = 0, rpc = 1;
   DevBuf<S> T[2], acc;
   DevBuf<unsigned long long> cmin, cmax;
   DevBuf<double> thr, errcol, part_err;
@@ -505,7 +520,8 @@ struct Work {
     GW = choose_gw(B);
     G = (B + GW - 1) / GW;
     Bpad = G * GW;
-    tiles = (n + rows_per_cta<S>(GW) - 1) / rows_per_cta<S>(GW);
+    rpc = choose_rpc<S>(n, GW, G);
+    tiles = (n + rows_per_block<S>(GW) * rpc - 1) / (rows_per_block<S>(GW) * rpc);
     const size_t len = (size_t)Bpad * n;
     GS_CUDA(ctx, T[0].alloc(len, s));
     GS_CUDA(ctx, T[1].alloc(len, s));
@@ -587,7 +603,7 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
     A.bk = f->coeffs[k];
     A.Tprev = w.T[(a0 + k - 1) & 1].get();
     A.Tout = w.T[(a0 + k) & 1].get();
-    launch_step<S>(ctx, w.GW, A, k == K ? mode : MODE_NONE);
+    launch_step<S>(ctx, w.GW, w.rpc, A, k == K ? mode : MODE_NONE);
   }
   return (a0 + K) & 1;
 }
@@ -779,28 +795,68 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   C.max_iter = max_iter;
   C.no_abort = (flags & GS_FLAG_NO_STAGNATION_ABORT) ? 1 : 0;
   C.tol = tol;
-  for (int sweep = 1; sweep <= max_iter; ++sweep) {  // transport.cpp:177-227
-    if (sweep >= 3) {
-      const int slot = (sweep - 2) & 1;
-      cudaEventSynchronize(ev[slot]);
-      const gs_status st = hst[slot];
-      if (st.error || st.n_active == 0) break;
-    }
+  DevBuf<int> sweep_ctr;
+  GS_CUDA(ctx, sweep_ctr.alloc(1, s));
+  GS_CUDA(ctx, cudaMemsetAsync(sweep_ctr.get(), 0, sizeof(int), s));
+  C.sweep_ctr = sweep_ctr.get();
+  // one sweep (transport.cpp:177-227); `parity` selects the V ping-pong buffers
+  auto issue_sweep = [&](int parity) {
     // psi = H(a * V_s); W_s = N / max(psi, floor); T_0 = a * W_s
     a0 = run_apply<S>(ctx, f, w, a0, MODE_SK_PSI, da, N.get(), nullptr, W.get(), true, true);
     run_finalize<S>(ctx, w, 1, 1, 0, knp, true);
     // phi = H(a * W_s); err; V_{s+1} = M / max(phi, floor); T_0 = a * V_{s+1}
-    a0 = run_apply<S>(ctx, f, w, a0, MODE_SK_PHI, da, M.get(), V[sweep & 1].get(),
-                      V[(sweep + 1) & 1].get(), true, true);
+    a0 = run_apply<S>(ctx, f, w, a0, MODE_SK_PHI, da, M.get(), V[parity].get(), V[parity ^ 1].get(),
+                      true, true);
     run_finalize<S>(ctx, w, 1, 1, 1, knp, true);
-    C.sweep = sweep;
     gs_launch_begin(ctx, 1);
     k_sk_control<<<1, 1, 0, s>>>(C);
     gs_launch_end(ctx, 1);
-    const int slot = sweep & 1;
+  };
+  // Small problems are launch-latency bound: capture two sweeps (odd, even parity) once as a CUDA
+  // graph and replay it; kernels of sweeps past convergence / max_iter exit immediately.
+  const char* genv = getenv("GS_GRAPH");
+  const bool use_graph = genv ? genv[0] == '1' : ((size_t)n * w.Bpad <= ((size_t)1 << 20));
+  cudaGraphExec_t gexec = nullptr;
+  int64_t graph_launches = 0;
+  if (use_graph && max_iter >= 2) {
+    cudaGraph_t graph = nullptr;
+    const int64_t l0 = ctx->launches;
+    ctx->capturing = true;
+    cudaError_t ce = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    if (ce == cudaSuccess) {
+      issue_sweep(1);
+      issue_sweep(0);
+      ce = cudaStreamEndCapture(s, &graph);
+    }
+    ctx->capturing = false;
+    graph_launches = ctx->launches - l0;
+    ctx->launches = l0;
+    if (ce == cudaSuccess) ce = cudaGraphInstantiate(&gexec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) {
+      cudaGetLastError();
+      gexec = nullptr;
+    }
+  }
+  const int step_sweeps = gexec ? 2 : 1;
+  for (int sweep = 1, it = 0; sweep <= max_iter; sweep += step_sweeps, ++it) {
+    if (it >= 2) {
+      const int slot = (it - 2) & 1;
+      cudaEventSynchronize(ev[slot]);
+      const gs_status st = hst[slot];
+      if (st.error || st.n_active == 0) break;
+    }
+    if (gexec) {
+      GS_CUDA(ctx, cudaGraphLaunch(gexec, s));
+      ctx->launches += graph_launches;
+    } else {
+      issue_sweep(sweep & 1);
+    }
+    const int slot = it & 1;
     cudaMemcpyAsync(&hst[slot], w.status.get(), sizeof(gs_status), cudaMemcpyDeviceToHost, s);
     cudaEventRecord(ev[slot], s);
   }
+  if (gexec) cudaGraphExecDestroy(gexec);
   GS_CUDA(ctx, cudaStreamSynchronize(s));
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
@@ -1222,7 +1278,7 @@ extern "C" int gs_graph_multiply(gs_ctx* ctx, const gs_graph* g, const double* x
   A.k = 0;
   A.Tprev = w.T[0].get();
   A.Tout = w.T[1].get();
-  launch_step<double>(ctx, w.GW, A, MODE_NONE);
+  launch_step<double>(ctx, w.GW, w.rpc, A, MODE_NONE);
   gs_launch_begin(ctx, 1);
   k_unpack<double><<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.T[1].get(), dY, n, width, w.GW, nullptr, nullptr, nullptr);
   gs_launch_end(ctx, 1);

@@ -120,7 +120,7 @@ extern "C" int gs_ctx_timing(gs_ctx* ctx, int cls, int64_t* launches, double* to
 
 void gs_launch_begin(gs_ctx* ctx, int cls) {
   ctx->launches++;
-  if (!ctx->timing) return;
+  if (!ctx->timing || ctx->capturing) return;
   if (ctx->pending.size() >= 8192) drain_timing(ctx, 4096);
   gs_event_pair p;
   if (!ctx->pool.empty()) {
@@ -137,7 +137,7 @@ void gs_launch_begin(gs_ctx* ctx, int cls) {
 
 void gs_launch_end(gs_ctx* ctx, int cls) {
   (void)cls;
-  if (!ctx->timing || ctx->pending.empty()) return;
+  if (!ctx->timing || ctx->capturing || ctx->pending.empty()) return;
   cudaEventRecord(ctx->pending.back().b, ctx->stream);
 }
 

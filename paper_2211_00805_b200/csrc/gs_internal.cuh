@@ -46,6 +46,8 @@ struct gs_ctx {
   double t_ms[2] = {0.0, 0.0};
   // pinned status mirror for host polling
   gs_status* h_status = nullptr;
+  // CUDA-graph capture in progress: launches are counted, not timed
+  bool capturing = false;
 };
 
 struct gs_graph {
