@@ -101,6 +101,22 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
+class _StdoutToStderr:
+    """Route fd 1 to stderr while NCCL initialises (its version banner would corrupt the single
+    JSON line the driver reads from stdout)."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -219,7 +235,9 @@ def run_engine(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        with _StdoutToStderr():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
     ctx = gs.Context(local)
     # a dedicated non-blocking stream shared by torch and the engine (the legacy default stream
     # serialises stream-ordered allocations and cannot be graph-captured)
@@ -438,6 +456,141 @@ def run_engine(args):
     return 0
 
 
+# --------------------------------------------------------------------------- config 2 (barycenter)
+def run_engine_bary(args):
+    """Config 2: member-sharded barycenter. Every rank builds the same graph; members are split
+    over the ranks; per sweep one NCCL allreduce(SUM) of the n-vector log-sum and one
+    allreduce(MAX) of the marginal error (paper_2211_00805_b200/distributed.py). Strong scaling:
+    the 8-member family is fixed, value = barycenter sweeps/s."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_00805_b200 as gs
+    from paper_2211_00805_b200 import _capi, workloads
+    from paper_2211_00805_b200.distributed import TorchAllreduce, member_shard
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    with _StdoutToStderr():
+        if world > 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("nccl", init_method="tcp://127.0.0.1:%d" % _free_port(),
+                                    rank=0, world_size=1, device_id=torch.device("cuda", local))
+        dist.barrier()
+    ctx = gs.Context(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    lib = ctx.lib
+    cfg = workloads.config2(args.n, args.members)
+    t0 = time.perf_counter()
+    A, sigma = gs.knn_gaussian_graph(cfg.mix.points, cfg.k, ctx=ctx)
+    t_graph = time.perf_counter() - t0
+    lap = gs.laplacian(A, gs.LaplacianKind.combinatorial)
+    filt = gs.HeatFilter(lap, cfg.t, cfg.degree)
+    n, m = args.n, args.members
+    lo, hi = member_shard(m, world, rank)
+    dev = torch.device("cuda", local)
+    Mloc = torch.from_numpy(np.ascontiguousarray(cfg.members[lo:hi])).to(dev)
+    al = torch.full((hi - lo,), 1.0 / m, dtype=torch.float64, device=dev)
+    a = torch.full((n,), 1.0 / n, dtype=torch.float64, device=dev)
+    bary = torch.empty(n, dtype=torch.float64, device=dev)
+    Vo = torch.empty((hi - lo, n), dtype=torch.float64, device=dev)
+    Wo = torch.empty_like(Vo)
+    it = np.zeros(1, np.int32)
+    conv = np.zeros(1, np.int32)
+    err = np.zeros(1)
+    hook = TorchAllreduce(None, device_buffers=True)
+
+    def step():
+        rc = lib.gs_barycenter_ex(ctx.handle, filt._h, a.data_ptr(), Mloc.data_ptr(), hi - lo,
+                                  al.data_ptr(), args.sweeps, TOL_RUN_ALL, _capi.GS_MEM_DEVICE,
+                                  C.byref(hook.comm), 0, bary.data_ptr(), Vo.data_ptr(),
+                                  Wo.data_ptr(), it.ctypes.data, conv.ctypes.data, err.ctypes.data)
+        if hook.error is not None:
+            raise hook.error
+        ctx.check(rc)
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    ctx.set_timing(True)
+    l0 = ctx.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = sampler.stop()
+    step_n, step_ms = ctx.timing(0)
+    ctx.set_timing(False)
+    launches = ctx.launch_count() - l0
+    elapsed = max_over_ranks(e0.elapsed_time(e1))
+    value = args.sweeps * args.steps / (elapsed / 1000.0)
+    peak, peak_kind = peaks()
+    nnz_L = lap.matrix.stored_entries()
+    B = hi - lo
+    bytes_step = algorithmic_bytes_per_step(n, nnz_L, B)
+    avg = step_ms / max(step_n, 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyoracle as po
+        L = lap.matrix
+        Lo = po.CSR(n, L.row_offsets().copy(), L.col_indices().copy(), L.values().copy())
+        fo = po.Filter(Lo, 0, lap.lambda_max_bound, cfg.t, cfg.degree)
+        t1 = time.perf_counter()
+        po.barycenter(fo, np.full(n, 1.0 / n), cfg.members, None, 1, TOL_RUN_ALL, L=po.lib(native=True))
+        dt = time.perf_counter() - t1
+        cpu = {"value": 1.0 / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": f"1 barycenter sweep of the 8-member family on the GPU-built n={n} graph ({dt:.1f} s)"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "barycenter sweeps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"config2: {n} points in R^30 (20-component mixture), k=15 "
+                                   f"Gaussian-median graph, t=0.5, K=30, m={m} members sharded "
+                                   f"over {world} rank(s), {args.sweeps} sweeps",
+                       "nnz_L": int(nnz_L), "lambda_max_bound": lap.lambda_max_bound,
+                       "lambda_rounds": lap.power_rounds, "graph_build_s": t_graph,
+                       "members_per_rank": B, "allreduce_calls": hook.calls,
+                       "parallelism": f"member sharding x{world}, NCCL allreduce per sweep"},
+            "roofline": {"bound": "hbm", "achieved": bytes_step / (avg / 1000.0) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": bytes_step / (avg / 1000.0) / 1e9 / peak,
+                         "traffic": None, "peak_kind": peak_kind, "bytes_per_launch": bytes_step,
+                         "avg_launch_ms": avg, "launches_timed": step_n},
+            "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": cpu,
+            "iterations": int(it[0]), "marginal_error": float(err[0]),
+        }), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
+def _free_port():
+    import socket
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    p_ = s_.getsockname()[1]
+    s_.close()
+    return p_
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -452,7 +605,8 @@ def main():
     ap.add_argument("--ref-sweeps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1])
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2])
+    ap.add_argument("--members", type=int, default=8)
     args = ap.parse_args()
     if args.config == 0:  # BASELINE.json configs[0]: n=2000, one pair, 100 sweeps
         if args.n == 200_000:
@@ -461,6 +615,14 @@ def main():
             args.pairs = 1
         if args.sweeps == 200:
             args.sweeps = 100
+    if args.config == 2:
+        if args.n == 200_000:
+            args.n = 1_000_000
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "config 2 reference arm needs an "
+                              "O(n^2 d) CPU kNN at n=1e6; use the default config"}))
+            return 0
+        return run_engine_bary(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_engine(args)

@@ -123,3 +123,22 @@ def config1(n: int = 200_000, pairs: int = 64, seed: int = 1, pair_seed: int = 2
     roll = swiss_roll(n, seed)
     mus, nus = bump_mixture_pairs(roll, pairs, pair_seed)
     return Config1(roll, mus, nus)
+
+
+@dataclass
+class Config2:
+    mix: Mixture
+    members: np.ndarray  # m x n
+    k: int = 15
+    t: float = 0.5
+    degree: int = 30
+    sweeps: int = 200
+
+
+def config2(n: int = 1_000_000, m: int = 8, d: int = 30, components: int = 20, seed: int = 3,
+            member_seed: int = 4) -> Config2:
+    """Config 2: 20-component Gaussian mixture in R^30 (means ~ N(0, 5^2 I), sigma = 1); m members,
+    each uniform over a random 60% subset of the points of 4 random clusters."""
+    mix = gaussian_mixture(n, d, components, seed)
+    members = cluster_subset_members(mix, m, 4, 0.6, member_seed)
+    return Config2(mix, members)
