@@ -508,6 +508,7 @@ void launch_step(gs_ctx* ctx, int gw, int rpc, const StepArgs& A, int mode) {
 template <typename S>
 struct Work {
   int n = 0, B = 0, GW = 1, G = 1, Bpad = 1, tiles = 0, rpc = 1;
+  int lay = 0;  // filter layout: 0 for one-warp-per-row groups, 1 (degree-sorted) for narrower
   DevBuf<S> T[2], acc;
   DevBuf<unsigned long long> cmin, cmax;
   DevBuf<double> thr, errcol, part_err;
@@ -520,6 +521,7 @@ struct Work {
     GW = choose_gw(B);
     G = (B + GW - 1) / GW;
     Bpad = G * GW;
+    lay = GW >= 32 ? 0 : 1;
     rpc = choose_rpc<S>(n, GW, G);
     tiles = (n + rows_per_block<S>(GW) * rpc - 1) / (rows_per_block<S>(GW) * rpc);
     const size_t len = (size_t)Bpad * n;
@@ -565,9 +567,9 @@ struct Work {
 };
 
 template <typename S>
-const void* filter_vals(const gs_filter* f) {
-  if constexpr (sizeof(S) == 4) return f->vals32;
-  else return f->perm->vals;
+const void* layout_vals(const gs_layout& L) {
+  if constexpr (sizeof(S) == 4) return L.vals32;
+  else return L.perm->vals;
 }
 
 // One full filter application on the workspace: T0 in T[a0]; K steps; the last step uses `mode`
@@ -575,12 +577,13 @@ const void* filter_vals(const gs_filter* f) {
 template <typename S>
 int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, const S* a, const S* M,
               const S* Vcur, S* Wout, bool use_active, bool use_status) {
-  const gs_graph* G = f->perm;
+  const gs_layout& Ly = f->lay[w.lay];
+  const gs_graph* G = Ly.perm;
   const int K = f->degree;
   StepArgs A{};
   A.offs = G->offs;
   A.cols = G->cols;
-  A.vals = filter_vals<S>(f);
+  A.vals = layout_vals<S>(Ly);
   A.n = w.n;
   A.tiles = w.tiles;
   A.g0 = 0;
@@ -707,11 +710,11 @@ int filter_apply_impl(gs_ctx* ctx, const gs_filter* f, const double* dX, double*
   Work<S> w;
   GS_TRY(w.init(ctx, n, width, false));
   gs_launch_begin(ctx, 1);
-  k_pack<S><<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, f->order);
+  k_pack<S><<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, f->lay[w.lay].order);
   gs_launch_end(ctx, 1);
   run_apply<S>(ctx, f, w, 0, MODE_NONE, nullptr, nullptr, nullptr, nullptr, false, false);
   gs_launch_begin(ctx, 1);
-  k_unpack<S><<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.acc.get(), dY, n, width, w.GW, nullptr, nullptr, f->newpos);
+  k_unpack<S><<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.acc.get(), dY, n, width, w.GW, nullptr, nullptr, f->lay[w.lay].newpos);
   gs_launch_end(ctx, 1);
   GS_CUDA(ctx, cudaStreamSynchronize(s));
   return GS_OK;
@@ -725,15 +728,15 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
                   int* out_conv, double* out_err, int* fail_pair, int* fail_sweep) {
   const int n = f->scaled->n;
   cudaStream_t s = ctx->stream;
+  Work<S> w;
+  GS_TRY(w.init(ctx, n, P, true));
   // vertex weights in the filter's locality order and the engine precision
   DevBuf<S> aperm;
   GS_CUDA(ctx, aperm.alloc(n, s));
   gs_launch_begin(ctx, 1);
-  k_gather_to<S><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(da_user, f->order, n, aperm.get());
+  k_gather_to<S><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(da_user, f->lay[w.lay].order, n, aperm.get());
   gs_launch_end(ctx, 1);
   const S* da = aperm.get();
-  Work<S> w;
-  GS_TRY(w.init(ctx, n, P, true));
   const size_t len = (size_t)w.Bpad * n;
   DevBuf<S> M, N, V[2], W;
   GS_CUDA(ctx, M.alloc(len, s));
@@ -763,10 +766,10 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
     GS_CUDA(ctx, cudaStreamSynchronize(s));
   }
   gs_launch_begin(ctx, 1);
-  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dmu, M.get(), n, P, w.GW, w.G, f->order);
+  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dmu, M.get(), n, P, w.GW, w.G, f->lay[w.lay].order);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
-  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dnu, N.get(), n, P, w.GW, w.G, f->order);
+  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dnu, N.get(), n, P, w.GW, w.G, f->lay[w.lay].order);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
   k_sk_init<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.T[0].get(), n, w.GW, w.G, P, w.cmax.get());
@@ -898,13 +901,13 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   }
   if (out_v) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)P * n), kThreads, 0, s>>>(V[0].get(), dv, n, P, w.GW, V[1].get(), final_sweep.get(), f->newpos);
+    k_unpack<S><<<grid_for((int64_t)P * n), kThreads, 0, s>>>(V[0].get(), dv, n, P, w.GW, V[1].get(), final_sweep.get(), f->lay[w.lay].newpos);
     gs_launch_end(ctx, 1);
     GS_TRY(finish_out(ctx, ov, out_v, (size_t)P * n, mem));
   }
   if (out_w) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)P * n), kThreads, 0, s>>>(W.get(), dw, n, P, w.GW, nullptr, nullptr, f->newpos);
+    k_unpack<S><<<grid_for((int64_t)P * n), kThreads, 0, s>>>(W.get(), dw, n, P, w.GW, nullptr, nullptr, f->lay[w.lay].newpos);
     gs_launch_end(ctx, 1);
     GS_TRY(finish_out(ctx, ow, out_w, (size_t)P * n, mem));
   }
@@ -931,14 +934,14 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
                     int* out_iters, int* out_conv, double* out_err) {
   const int n = f->scaled->n;
   cudaStream_t s = ctx->stream;
+  Work<S> w;
+  GS_TRY(w.init(ctx, n, m, true));
   DevBuf<S> aperm;
   GS_CUDA(ctx, aperm.alloc(n, s));
   gs_launch_begin(ctx, 1);
-  k_gather_to<S><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(da_user, f->order, n, aperm.get());
+  k_gather_to<S><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(da_user, f->lay[w.lay].order, n, aperm.get());
   gs_launch_end(ctx, 1);
   const S* da = aperm.get();
-  Work<S> w;
-  GS_TRY(w.init(ctx, n, m, true));
   const size_t len = (size_t)w.Bpad * n;
   DevBuf<S> Mb, V[2], W;
   DevBuf<double> lb, bary, part, mass, dal, errbuf, derr;
@@ -972,7 +975,7 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   k_fill<<<grid_for(n), kThreads, 0, s>>>(bary.get(), n, 1.0 / n);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
-  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dmem, Mb.get(), n, m, w.GW, w.G, f->order);
+  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dmem, Mb.get(), n, m, w.GW, w.G, f->lay[w.lay].order);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
   k_sk_init<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.T[0].get(), n, w.GW, w.G, m, w.cmax.get());
@@ -1077,7 +1080,7 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
     DevBuf<double> bu;
     GS_CUDA(ctx, bu.alloc(n, s));
     gs_launch_begin(ctx, 1);
-    k_gather<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(bary.get(), f->newpos, n, bu.get());
+    k_gather<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(bary.get(), f->lay[w.lay].newpos, n, bu.get());
     gs_launch_end(ctx, 1);
     GS_TRY(gs_copy_out(ctx, out_bary, bu.get(), (size_t)n * sizeof(double), mem));
   }
@@ -1099,13 +1102,13 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   }
   if (out_V) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)m * n), kThreads, 0, s>>>(V[0].get(), dv, n, m, w.GW, V[1].get(), sel.get(), f->newpos);
+    k_unpack<S><<<grid_for((int64_t)m * n), kThreads, 0, s>>>(V[0].get(), dv, n, m, w.GW, V[1].get(), sel.get(), f->lay[w.lay].newpos);
     gs_launch_end(ctx, 1);
     GS_TRY(finish_out(ctx, ov, out_V, (size_t)m * n, mem));
   }
   if (out_W) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)m * n), kThreads, 0, s>>>(W.get(), dw, n, m, w.GW, nullptr, nullptr, f->newpos);
+    k_unpack<S><<<grid_for((int64_t)m * n), kThreads, 0, s>>>(W.get(), dw, n, m, w.GW, nullptr, nullptr, f->lay[w.lay].newpos);
     gs_launch_end(ctx, 1);
     GS_TRY(finish_out(ctx, ow, out_W, (size_t)m * n, mem));
   }
@@ -1160,21 +1163,29 @@ extern "C" int gs_filter_create(gs_ctx* ctx, const gs_graph* L, int kind, double
       rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "coefficient allocation failed");
   }
   if (!rc) rc = gs_coefficients_impl(ctx, f->t_eff, degree, f->d_coeffs, f->coeffs.data());
+  // two locality layouts (gs_reorder.cu): plain Cuthill-McKee, and CM with degree-sorted
+  // windows of 256 rows for narrow batches (several rows per warp)
+  int sigma = 256;
+  if (const char* e = getenv("GS_SIGMA")) sigma = atoi(e);
   if (!rc) {
     const int n = L->n;
-    if (cudaMalloc((void**)&f->order, ((size_t)n + 1) * sizeof(int)) != cudaSuccess ||
-        cudaMalloc((void**)&f->newpos, ((size_t)n + 1) * sizeof(int)) != cudaSuccess)
-      rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "permutation allocation failed");
+    for (int l = 0; l < 2 && !rc; ++l)
+      if (cudaMalloc((void**)&f->lay[l].order, ((size_t)n + 1) * sizeof(int)) != cudaSuccess ||
+          cudaMalloc((void**)&f->lay[l].newpos, ((size_t)n + 1) * sizeof(int)) != cudaSuccess)
+        rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "permutation allocation failed");
   }
-  if (!rc) rc = gs_bfs_order(ctx, f->scaled, f->order, f->newpos);
-  if (!rc) rc = gs_permute_graph(ctx, f->scaled, f->order, f->newpos, &f->perm);
-  if (!rc) {  // fp32 copy of the permuted values for the optional fp32 mode
-    const int64_t nnz = f->perm->nnz;
-    if (cudaMalloc((void**)&f->vals32, (size_t)(nnz ? nnz : 1) * sizeof(float)) != cudaSuccess) {
+  if (!rc) rc = gs_bfs_order(ctx, f->scaled, f->lay[0].order, f->lay[0].newpos, sigma,
+                             f->lay[1].order, f->lay[1].newpos);
+  for (int l = 0; l < 2 && !rc; ++l) {
+    gs_layout& Ly = f->lay[l];
+    rc = gs_permute_graph(ctx, f->scaled, Ly.order, Ly.newpos, &Ly.perm);
+    if (rc) break;
+    const int64_t nnz = Ly.perm->nnz;  // fp32 copy of the permuted values (optional fp32 mode)
+    if (cudaMalloc((void**)&Ly.vals32, (size_t)(nnz ? nnz : 1) * sizeof(float)) != cudaSuccess) {
       rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "fp32 value allocation failed");
     } else if (nnz > 0) {
       gs_launch_begin(ctx, 1);
-      k_to_float<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(f->perm->vals, nnz, f->vals32);
+      k_to_float<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(Ly.perm->vals, nnz, Ly.vals32);
       gs_launch_end(ctx, 1);
       if (cudaStreamSynchronize(s) != cudaSuccess) rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "fp32 copy failed");
     }
@@ -1190,10 +1201,12 @@ extern "C" int gs_filter_create(gs_ctx* ctx, const gs_graph* L, int kind, double
 extern "C" void gs_filter_destroy(gs_filter* f) {
   if (!f) return;
   gs_graph_destroy(f->scaled);
-  gs_graph_destroy(f->perm);
-  cudaFree(f->order);
-  cudaFree(f->newpos);
-  cudaFree(f->vals32);
+  for (auto& Ly : f->lay) {
+    gs_graph_destroy(Ly.perm);
+    cudaFree(Ly.order);
+    cudaFree(Ly.newpos);
+    cudaFree(Ly.vals32);
+  }
   cudaFree(f->d_coeffs);
   delete f;
 }
@@ -1217,7 +1230,7 @@ extern "C" int gs_filter_coefficients(const gs_filter* f, double* out) {
 extern "C" const gs_graph* gs_filter_scaled(const gs_filter* f) { return f->scaled; }
 
 extern "C" int gs_filter_order(gs_ctx* ctx, const gs_filter* f, int* order, int mem) {
-  GS_TRY(gs_copy_out(ctx, order, f->order, (size_t)f->scaled->n * sizeof(int), mem));
+  GS_TRY(gs_copy_out(ctx, order, f->lay[0].order, (size_t)f->scaled->n * sizeof(int), mem));
   return gs_ctx_synchronize(ctx);
 }
 

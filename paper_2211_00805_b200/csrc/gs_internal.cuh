@@ -59,16 +59,23 @@ struct gs_graph {
   int device = 0;
 };
 
+// One locality layout of the filter's operator (gs_reorder.cu): renumbered rows + fp32 copy.
+struct gs_layout {
+  gs_graph* perm = nullptr;  // L_s with rows renumbered (entries kept in original column order)
+  int* order = nullptr;      // order[new] = old
+  int* newpos = nullptr;     // newpos[old] = new
+  float* vals32 = nullptr;   // fp32 copy of perm->vals (optional fp32 mode)
+};
+
 struct gs_filter {
   gs_graph* scaled = nullptr;   // L_s in the caller's vertex order (heat.hpp:47)
-  gs_graph* perm = nullptr;     // L_s with rows renumbered for locality (gs_reorder.cu)
-  int* order = nullptr;         // order[new] = old
-  int* newpos = nullptr;        // newpos[old] = new
+  // lay[0]: Cuthill-McKee order (wide batches, one warp per row);
+  // lay[1]: CM with degree-sorted windows (narrow batches, several rows per warp)
+  gs_layout lay[2];
   double t = 0, t_eff = 0, scale = 1;
   int degree = 0, kind = 0;
   std::vector<double> coeffs;  // host mirror (heat.hpp:37)
   double* d_coeffs = nullptr;
-  float* vals32 = nullptr;     // fp32 copy of perm->vals (optional fp32 mode)
 };
 
 // ---- error plumbing ----------------------------------------------------------------------
@@ -138,7 +145,8 @@ int gs_copy_in(gs_ctx* ctx, void* dst, const void* src, size_t bytes, int mem);
 int gs_copy_out(gs_ctx* ctx, void* dst, const void* src, size_t bytes, int mem);
 int gs_lambda_max_impl(gs_ctx* ctx, const gs_graph* L, double* out, int* rounds_out);
 int gs_coefficients_impl(gs_ctx* ctx, double t, int degree, double* d_out, double* h_out);
-int gs_bfs_order(gs_ctx* ctx, const gs_graph* g, int* d_order, int* d_newpos);
+int gs_bfs_order(gs_ctx* ctx, const gs_graph* g, int* d_order, int* d_newpos, int sigma,
+                 int* d_order_sig, int* d_newpos_sig);
 int gs_permute_graph(gs_ctx* ctx, const gs_graph* g, const int* d_order, const int* d_newpos,
                      gs_graph** out);
 int gs_csr_from_sorted_entries(gs_ctx* ctx, int n, int64_t m, const unsigned long long* d_keys,

@@ -12,6 +12,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "gs_internal.cuh"
@@ -151,6 +152,30 @@ __global__ void k_cm_assign(const unsigned long long* sorted, int start, int cnt
   if (t < cnt) pos[(int)(sorted[t] & 0xFFFFFFFFull)] = start + t;
 }
 
+// SELL-C-sigma style: within windows of `sigma` consecutive CM positions, rows are ordered by
+// length (longest first), so rows that share a warp (narrow column groups) have similar lengths.
+__global__ void k_sigma_keys(const int* pos, const int* offs, int n, int sigma,
+                             unsigned long long* keys) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int p = pos[i];
+  const unsigned len = (unsigned)min(offs[i + 1] - offs[i], (1 << 20) - 1);
+  const unsigned long long win = (unsigned long long)(p / sigma);
+  keys[i] = (win << 44) | ((unsigned long long)((1u << 20) - 1u - len) << 24) |
+            (unsigned long long)(p % sigma);
+}
+
+__global__ void k_sigma_assign(const unsigned long long* sorted_keys, const int* sorted_vertex, int n,
+                               int* pos) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) pos[sorted_vertex[r]] = r;
+}
+
+__global__ void k_iota(int* x, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = i;
+}
+
 __global__ void k_pos_to_order(const int* pos, int n, int* order, int* newpos) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -161,7 +186,8 @@ __global__ void k_pos_to_order(const int* pos, int n, int* order, int* newpos) {
 }  // namespace
 
 // Computes order[new] = old and newpos[old] = new on the device.
-int gs_bfs_order(gs_ctx* ctx, const gs_graph* g, int* d_order, int* d_newpos) {
+int gs_bfs_order(gs_ctx* ctx, const gs_graph* g, int* d_order, int* d_newpos, int sigma,
+                 int* d_order_sig, int* d_newpos_sig) {
   const int n = g->n;
   if (n == 0) return GS_OK;
   cudaStream_t s = ctx->stream;
@@ -292,6 +318,35 @@ int gs_bfs_order(gs_ctx* ctx, const gs_graph* g, int* d_order, int* d_newpos) {
   gs_launch_begin(ctx, 1);
   k_pos_to_order<<<nblk(n), kThreads, 0, s>>>(pos.get(), n, d_order, d_newpos);
   gs_launch_end(ctx, 1);
+  // second layout: degree-sorted windows of `sigma` CM positions (narrow column groups)
+  if (d_order_sig && sigma > 1) {
+    DevBuf<unsigned long long> sk, sk2;
+    DevBuf<int> vid, vid2;
+    GS_CUDA(ctx, sk.alloc(n, s));
+    GS_CUDA(ctx, sk2.alloc(n, s));
+    GS_CUDA(ctx, vid.alloc(n, s));
+    GS_CUDA(ctx, vid2.alloc(n, s));
+    gs_launch_begin(ctx, 1);
+    k_sigma_keys<<<nblk(n), kThreads, 0, s>>>(pos.get(), g->offs, n, sigma, sk.get());
+    gs_launch_end(ctx, 1);
+    gs_launch_begin(ctx, 1);
+    k_iota<<<nblk(n), kThreads, 0, s>>>(vid.get(), n);
+    gs_launch_end(ctx, 1);
+    size_t tb3 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tb3, sk.get(), sk2.get(), vid.get(), vid2.get(), n, 0, 64, s);
+    DevBuf<unsigned char> tmp3;
+    GS_CUDA(ctx, tmp3.alloc(tb3, s));
+    cub::DeviceRadixSort::SortPairs(tmp3.get(), tb3, sk.get(), sk2.get(), vid.get(), vid2.get(), n, 0, 64, s);
+    gs_launch_begin(ctx, 1);
+    k_sigma_assign<<<nblk(n), kThreads, 0, s>>>(sk2.get(), vid2.get(), n, pos.get());
+    gs_launch_end(ctx, 1);
+    gs_launch_begin(ctx, 1);
+    k_pos_to_order<<<nblk(n), kThreads, 0, s>>>(pos.get(), n, d_order_sig, d_newpos_sig);
+    gs_launch_end(ctx, 1);
+  } else if (d_order_sig) {
+    cudaMemcpyAsync(d_order_sig, d_order, n * sizeof(int), cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(d_newpos_sig, d_newpos, n * sizeof(int), cudaMemcpyDeviceToDevice, s);
+  }
   GS_CUDA(ctx, cudaStreamSynchronize(s));
   return GS_OK;
 }
