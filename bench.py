@@ -297,7 +297,7 @@ def run_engine(args):
     barrier()
     torch.cuda.synchronize()
     sampler.start()
-    ctx.set_timing(True)
+    ctx.set_timing(True, period=args.timing_period)
     l0 = ctx.launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -309,6 +309,7 @@ def run_engine(args):
     barrier()
     clocks = sampler.stop()
     launches = ctx.launch_count() - l0
+    steps_total = args.steps * (1 + 2 * args.sweeps) * 30  # step-kernel launches in the region
     step_n, step_ms = ctx.timing(0)
     epi_n, epi_ms = ctx.timing(1)
     ctx.set_timing(False)
@@ -440,8 +441,8 @@ def run_engine(args):
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": "k_cheb_step<8,*> (fused Chebyshev step)",
                          "bytes_per_launch": bytes_step, "avg_launch_ms": avg_step_ms,
-                         "launches_timed": step_n,
-                         "share_of_step": step_ms / max(elapsed_ms * (1 if world == 1 else 1), 1e-9)},
+                         "launches_timed": step_n, "timing_period": args.timing_period,
+                         "share_of_step": avg_step_ms * steps_total / max(elapsed_ms, 1e-9)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps},
             "gpu_launches": int(launches),
@@ -607,6 +608,8 @@ def main():
     ap.add_argument("--no-fp32", action="store_true")
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2])
     ap.add_argument("--members", type=int, default=8)
+    ap.add_argument("--timing-period", type=int, default=8,
+                    help="event-time every Nth engine launch inside the timed region")
     args = ap.parse_args()
     if args.config == 0:  # BASELINE.json configs[0]: n=2000, one pair, 100 sweeps
         if args.n == 200_000:

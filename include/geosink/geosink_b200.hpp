@@ -425,6 +425,32 @@ inline std::vector<TransportResult> geodesic_sinkhorn_batch(const HeatFilter& fi
   return detail::sinkhorn(filter, mus, nus, a, params, 0);
 }
 
+// ---- next: plan rows, graph file IO ---------------------------------------------
+// transport.cpp:314-324
+inline std::vector<double> plan_row(const TransportResult& result, const HeatFilter& filter,
+                                    const std::vector<double>& a, int i) {
+  const int n = filter.size();
+  if ((int)result.v.size() != n || (int)result.w.size() != n)
+    detail::fail(errc::length_mismatch, "LengthMismatch", "result does not match the filter's graph");
+  std::vector<double> row(n);
+  detail::check(gs_plan_rows(detail::ctx(), filter.handle(), a.data(), result.v.data(),
+                             result.w.data(), &i, 1, GS_MEM_HOST, row.data()));
+  return row;
+}
+
+// sparse.cpp:137-174
+inline void save_graph(const SparseSymMatrix& m, const std::string& path) {
+  if (gs_graph_save(detail::ctx(), m.handle(), path.c_str()) != 0)
+    detail::fail(errc::io_error, "IoError", "cannot write '" + path + "'");
+}
+inline SparseSymMatrix load_graph(const std::string& path) {
+  gs_graph* g = nullptr;
+  const int rc = gs_graph_load(detail::ctx(), path.c_str(), &g);
+  if (rc == 16) detail::fail(errc::io_error, "IoError", "cannot read graph file '" + path + "'");
+  detail::check(rc);
+  return SparseSymMatrix(g, true);
+}
+
 // ---- barycenter.hpp:11-42 ---------------------------------------------------------------------
 struct DistributionFamily {
   std::vector<Distribution> members;

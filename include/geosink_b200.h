@@ -63,7 +63,8 @@ int gs_ctx_synchronize(gs_ctx* ctx);
 /* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the own stream. */
 int gs_ctx_set_stream(gs_ctx* ctx, void* stream);
 void* gs_ctx_stream(gs_ctx* ctx);
-/* Per-kernel-class device timing with CUDA events around every launch (bench evidence). */
+/* Per-kernel-class device timing with CUDA events around launches (bench evidence):
+ * enable = 1 times every launch, N > 1 every Nth launch of each class, 0 turns timing off. */
 int gs_ctx_set_timing(gs_ctx* ctx, int enable);
 /* class: 0 = Chebyshev step kernels, 1 = epilogue/finalise kernels. Returns launches, ms. */
 int gs_ctx_timing(gs_ctx* ctx, int kernel_class, int64_t* launches, double* total_ms);
@@ -125,6 +126,16 @@ int gs_sinkhorn(gs_ctx* ctx, const gs_filter* f, const double* a, const double* 
                 const double* nus, int P, int max_iter, double tol, int flags, int mem,
                 double* out_v, double* out_w, double* out_cost, double* out_kl, int* out_iters,
                 int* out_conv, double* out_err, int* fail_pair, int* fail_sweep);
+
+/* plan_row (transport.cpp:314-324), batched: out row q = max(v[rows[q]] * H e_rows[q] .* a .* w, 0);
+ * a, v, w: n; rows: nrows; out: nrows contiguous n-vectors. */
+int gs_plan_rows(gs_ctx* ctx, const gs_filter* f, const double* a, const double* v,
+                 const double* w, const int* rows, int nrows, int mem, double* out);
+
+/* ---- graph text format (sparse.cpp:137-174) ------------------------------------------ */
+/* Status 16 (errc::io_error + 1) on file errors; "IoError" semantics of the reference. */
+int gs_graph_save(gs_ctx* ctx, const gs_graph* g, const char* path);
+int gs_graph_load(gs_ctx* ctx, const char* path, gs_graph** out);
 
 /* ---- barycenter (barycenter.hpp:36-42, barycenter.cpp:45-107) ------------------------ */
 /* Optional collective hook for member-sharded barycenters: sums `count` doubles of the

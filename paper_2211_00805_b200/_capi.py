@@ -74,6 +74,9 @@ SIGNATURES = {
                            _vp, _vp]),
     "gs_barycenter_ex": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _d, _i, _vp, _i, _vp, _vp, _vp,
                               _vp, _vp, _vp]),
+    "gs_plan_rows": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp]),
+    "gs_graph_save": (_i, [_vp, _vp, C.c_char_p]),
+    "gs_graph_load": (_i, [_vp, C.c_char_p, _pvp]),
     "gs_rng_create": (_vp, [C.c_uint64]),
     "gs_rng_destroy": (None, [_vp]),
     "gs_rng_bits": (C.c_uint64, [_vp]),

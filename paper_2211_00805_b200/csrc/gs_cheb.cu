@@ -1398,3 +1398,65 @@ extern "C" int gs_barycenter(gs_ctx* ctx, const gs_filter* f, const double* a,
   return gs_barycenter_ex(ctx, f, a, members, m, alphas, max_iter, tol, mem, comm, 0, out_bary,
                           out_V, out_W, out_iters, out_conv, out_err);
 }
+
+// ============================================================================================
+// Plan rows (transport.cpp:314-324): row i of diag(v) H_t diag(a .* w) through one filter
+// application to the unit impulse e_i, clamped at zero -- batched over `nrows` impulses, which is
+// the same Chebyshev kernel with B = nrows (the paper's displacement-interpolation use case).
+// ============================================================================================
+namespace {
+__global__ void k_impulses(const int* rows, int nrows, int n, double* X) {
+  const int64_t total = (int64_t)nrows * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(e / n), i = (int)(e % n);
+    X[e] = i == rows[q] ? 1.0 : 0.0;
+  }
+}
+
+__global__ void k_plan_rows(const int* rows, int nrows, int n, const double* a, const double* v,
+                            const double* w, double* Y) {
+  const int64_t total = (int64_t)nrows * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(e / n), j = (int)(e % n);
+    const double r = v[rows[q]] * (Y[e] * (a[j] * w[j]));
+    Y[e] = fmax(r, 0.0);
+  }
+}
+}  // namespace
+
+extern "C" int gs_plan_rows(gs_ctx* ctx, const gs_filter* f, const double* a, const double* v,
+                            const double* w, const int* rows, int nrows, int mem, double* out) {
+  const int n = f->scaled->n;
+  if (nrows <= 0) return GS_OK;
+  cudaStream_t s = ctx->stream;
+  std::vector<int> hrows(nrows);
+  if (mem == GS_MEM_DEVICE) {
+    GS_CUDA(ctx, cudaMemcpy(hrows.data(), rows, nrows * sizeof(int), cudaMemcpyDeviceToHost));
+  } else {
+    memcpy(hrows.data(), rows, nrows * sizeof(int));
+  }
+  for (int q = 0; q < nrows; ++q)
+    if (hrows[q] < 0 || hrows[q] >= n) return gs_fail(ctx, ERRC_INDEX_OUT_OF_RANGE, "plan row index");
+  DevBuf<double> ba, bv, bw, X, Y;
+  DevBuf<int> drows;
+  const double *da, *dv, *dw;
+  GS_TRY(stage_in(ctx, ba, a, n, mem, &da));
+  GS_TRY(stage_in(ctx, bv, v, n, mem, &dv));
+  GS_TRY(stage_in(ctx, bw, w, n, mem, &dw));
+  GS_CUDA(ctx, drows.alloc(nrows, s));
+  GS_CUDA(ctx, cudaMemcpyAsync(drows.get(), hrows.data(), nrows * sizeof(int), cudaMemcpyHostToDevice, s));
+  GS_CUDA(ctx, X.alloc((size_t)nrows * n, s));
+  GS_CUDA(ctx, Y.alloc((size_t)nrows * n, s));
+  gs_launch_begin(ctx, 1);
+  k_impulses<<<grid_for((int64_t)nrows * n), kThreads, 0, s>>>(drows.get(), nrows, n, X.get());
+  gs_launch_end(ctx, 1);
+  GS_TRY(filter_apply_impl<double>(ctx, f, X.get(), Y.get(), nrows));
+  gs_launch_begin(ctx, 1);
+  k_plan_rows<<<grid_for((int64_t)nrows * n), kThreads, 0, s>>>(drows.get(), nrows, n, da, dv, dw, Y.get());
+  gs_launch_end(ctx, 1);
+  GS_TRY(gs_copy_out(ctx, out, Y.get(), (size_t)nrows * n * sizeof(double), mem));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  return GS_OK;
+}

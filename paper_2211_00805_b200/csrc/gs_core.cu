@@ -104,8 +104,10 @@ static void drain_timing(gs_ctx* ctx, size_t keep) {
 extern "C" int gs_ctx_set_timing(gs_ctx* ctx, int enable) {
   drain_timing(ctx, 0);
   ctx->timing = enable != 0;
+  ctx->timing_period = enable > 1 ? enable : 1;  // enable = N > 1: sample every Nth launch
   ctx->t_launches[0] = ctx->t_launches[1] = 0;
   ctx->t_ms[0] = ctx->t_ms[1] = 0.0;
+  ctx->t_seen[0] = ctx->t_seen[1] = 0;
   return GS_OK;
 }
 
@@ -120,7 +122,10 @@ extern "C" int gs_ctx_timing(gs_ctx* ctx, int cls, int64_t* launches, double* to
 
 void gs_launch_begin(gs_ctx* ctx, int cls) {
   ctx->launches++;
+  ctx->t_open = false;
   if (!ctx->timing || ctx->capturing) return;
+  if ((ctx->t_seen[cls]++ % ctx->timing_period) != 0) return;
+  ctx->t_open = true;
   if (ctx->pending.size() >= 8192) drain_timing(ctx, 4096);
   gs_event_pair p;
   if (!ctx->pool.empty()) {
@@ -137,7 +142,8 @@ void gs_launch_begin(gs_ctx* ctx, int cls) {
 
 void gs_launch_end(gs_ctx* ctx, int cls) {
   (void)cls;
-  if (!ctx->timing || ctx->capturing || ctx->pending.empty()) return;
+  if (!ctx->timing || ctx->capturing || !ctx->t_open || ctx->pending.empty()) return;
+  ctx->t_open = false;
   cudaEventRecord(ctx->pending.back().b, ctx->stream);
 }
 

@@ -44,6 +44,9 @@ struct gs_ctx {
   std::vector<gs_event_pair> pool;
   int64_t t_launches[2] = {0, 0};
   double t_ms[2] = {0.0, 0.0};
+  int timing_period = 1;         // time every Nth launch of a class (sampling)
+  int64_t t_seen[2] = {0, 0};
+  bool t_open = false;
   // pinned status mirror for host polling
   gs_status* h_status = nullptr;
   // CUDA-graph capture in progress: launches are counted, not timed

@@ -101,8 +101,9 @@ class Context:
     def set_stream(self, stream_ptr: int | None):
         self.check(self.lib.gs_ctx_set_stream(self.handle, stream_ptr))
 
-    def set_timing(self, on: bool):
-        self.check(self.lib.gs_ctx_set_timing(self.handle, int(on)))
+    def set_timing(self, on, period: int = 1):
+        """Event-time engine launches per class; `period` > 1 samples every Nth launch."""
+        self.check(self.lib.gs_ctx_set_timing(self.handle, (period if period > 1 else 1) if on else 0))
 
     def timing(self, cls: int):
         n = C.c_int64()
@@ -653,3 +654,42 @@ def barycentric_distance(filter: HeatFilter, family_t: DistributionFamily,
     bt = sinkhorn_barycenter(filter, family_t, a, params)
     bc = sinkhorn_barycenter(filter, family_c, a, params)
     return geodesic_sinkhorn(filter, bt.barycenter, bc.barycenter, a, params).cost
+
+
+# ---------------------------------------------------------------------------------- next (§8(f))
+def plan_rows(result: TransportResult, filter: HeatFilter, a, rows) -> np.ndarray:
+    """plan_row (transport.cpp:314-324) for several rows at once: (len(rows), n) array."""
+    ctx = filter._ctx
+    n = filter.size()
+    if result.v.size != n or result.w.size != n:
+        raise Error(errc.length_mismatch, "LengthMismatch: result does not match the filter's graph")
+    rows = np.ascontiguousarray(np.atleast_1d(rows), np.int32)
+    out = np.empty((rows.size, n))
+    a = _f64(a)
+    ctx.check(ctx.lib.gs_plan_rows(ctx.handle, filter._h, _ptr(a), _ptr(_f64(result.v)),
+                                   _ptr(_f64(result.w)), _ptr(rows), rows.size, _capi.GS_MEM_HOST,
+                                   _ptr(out)))
+    return out
+
+
+def plan_row(result: TransportResult, filter: HeatFilter, a, i: int) -> np.ndarray:
+    """transport.cpp:314-324."""
+    return plan_rows(result, filter, a, [i])[0]
+
+
+def save_graph(m: SparseSymMatrix, path: str) -> None:
+    """sparse.cpp:137-157."""
+    rc = m._ctx.lib.gs_graph_save(m._ctx.handle, m._h, path.encode())
+    if rc:
+        raise Error(errc.io_error, f"IoError: cannot write '{path}'")
+
+
+def load_graph(path: str, ctx: Optional[Context] = None) -> SparseSymMatrix:
+    """sparse.cpp:159-174."""
+    ctx = _ctx(ctx)
+    h = C.c_void_p()
+    rc = ctx.lib.gs_graph_load(ctx.handle, path.encode(), C.byref(h))
+    if rc == 16:
+        raise Error(errc.io_error, f"IoError: cannot read graph file '{path}'")
+    ctx.check(rc)
+    return SparseSymMatrix(h, ctx)

@@ -209,6 +209,28 @@ int main() {
     const double ct = barycentric_distance(f, c, t, a, {500, 1e-8});
     CHECK(std::abs(tc - ct) <= 1e-8 * (1.0 + std::abs(tc)));
   }
+  // plan rows rebuild the marginals (acceptance.cpp:168-197); graph file round trip
+  {
+    Rng rng(4);
+    const auto lap = laplacian(random_connected_graph(50, 3), LaplacianKind::normalized);
+    const HeatFilter f(lap, 1.0, 40);
+    const std::vector<double> a(50, 1.0 / 50);
+    const auto mu = random_distribution(50, rng), nu = random_distribution(50, rng);
+    const auto res = geodesic_sinkhorn(f, mu, nu, a, {5000, 1e-6});
+    CHECK(res.converged);
+    double err = 0.0;
+    for (int i = 0; i < 50; ++i) {
+      const auto row = plan_row(res, f, a, i);
+      double srow = 0.0;
+      for (double x : row) srow += x;
+      err += std::abs(srow - mu.weights[i]);
+    }
+    CHECK(err <= 1e-6);
+    save_graph(lap.matrix, "/tmp/geosink_dropin_graph.txt");
+    const auto back = load_graph("/tmp/geosink_dropin_graph.txt");
+    CHECK(back.stored_entries() == lap.matrix.stored_entries() && back.values() == lap.matrix.values());
+    CHECK_THROWS_CODE(load_graph("/tmp/does/not/exist.txt"), errc::io_error);
+  }
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail;
 }

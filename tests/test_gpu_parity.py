@@ -316,3 +316,36 @@ def test_knn_graph_matches_oracle(gs, kernel):
     assert rel(A.values(), Ao.vals) <= 1e-13
     if sigma is not None:
         assert sigma == sigma_o
+
+
+# --------------------------------------------------------------------------- §8(f) next items
+def test_plan_rows_rebuild_marginals(gs):
+    """acceptance.cpp:168-197 (criterion 4): plan rows of a converged run rebuild mu and nu."""
+    n = 80
+    r, c, v = acceptance_graph(n, 480)
+    f, _ = engine_filter(r, c, v, n, 1, 1.0, 40)
+    from paper_2211_00805_b200.rng import Rng
+    rng = Rng(4)
+    mu, nu = random_distribution(n, rng), random_distribution(n, rng)
+    a = np.full(n, 1.0 / n)
+    res = gs.geodesic_sinkhorn(f, gs.Distribution(mu), gs.Distribution(nu), a, gs.SinkhornParams(5000, 1e-6))
+    assert res.converged
+    plan = gs.plan_rows(res, f, a, np.arange(n))
+    assert np.abs(plan.sum(1) - mu).sum() <= 1e-6
+    assert np.abs(plan.sum(0) - nu).sum() <= 1e-6
+    assert np.array_equal(gs.plan_row(res, f, a, 7), plan[7])
+
+
+def test_graph_file_round_trip(gs, tmp_path):
+    """test_graph.cpp:141-150: save/load is exact."""
+    from paper_2211_00805_b200.rng import Rng
+    pts = Rng(5).normals(40 * 2).reshape(40, 2)
+    A = gs.knn_alpha_decay_graph(pts, 3, 40.0)
+    path = str(tmp_path / "g.txt")
+    gs.save_graph(A, path)
+    B = gs.load_graph(path)
+    assert B.size() == A.size() and B.stored_entries() == A.stored_entries()
+    assert np.array_equal(B.to_dense(), A.to_dense())
+    with pytest.raises(gs.Error) as e:
+        gs.load_graph(str(tmp_path / "missing.txt"))
+    assert e.value.code == gs.errc.io_error
