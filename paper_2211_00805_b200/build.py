@@ -33,7 +33,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
     """Compile every source and link lib/libgeosink_b200.so (or `out`, for tuning variants
     built with extra -D defines)."""
     lib = out or LIB
-    if not force and out is None and not _stale():
+    if not force and out is None and not defines and not _stale():
         return LIB
     os.makedirs(os.path.dirname(lib), exist_ok=True)
     tag = "" if out is None else "_" + os.path.basename(out).replace(".so", "")

@@ -467,6 +467,15 @@ int rows_per_block(int gw) {  // rows covered by one CTA pass (8 warps)
 // than two CTAs per SM, in which case 1 (small, latency-bound problems such as config 0).
 template <typename S>
 int choose_rpc(int n, int gw, int groups) {
+  static const int forced = [] {
+    const char* e = getenv("GS_RPC");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 1) return 1;
+  if (forced > 1) return kRowsPerCta;
+  // rows of <= 64 bytes spread over several lanes (config 2's B = 8 fp64): consecutive row blocks
+  // share few L1 lines (kNN graphs in R^30), so short CTAs win by shrinking the tail wave
+  if (gw * (int)sizeof(S) <= 64 && gw * (int)sizeof(S) > 16) return 1;
   const int64_t ctas = (int64_t)groups * ((n + rows_per_block<S>(gw) * kRowsPerCta - 1) /
                                           (rows_per_block<S>(gw) * kRowsPerCta));
   return ctas < 2 * 148 ? 1 : kRowsPerCta;

@@ -40,11 +40,21 @@ constexpr int kRowsPerCta = GS_ROWS_PER_CTA;
 #ifndef GS_GATHER_BATCH
 #define GS_GATHER_BATCH 4
 #endif
-constexpr int kGatherBatch = GS_GATHER_BATCH;  // neighbour rows in flight per lane
+constexpr int kGatherBatch = GS_GATHER_BATCH;  // neighbour rows in flight per lane (wide rows)
+#ifndef GS_NARROW_GATHER_BATCH
+#define GS_NARROW_GATHER_BATCH 8
+#endif
 #ifndef GS_PREFETCH_STAGES
 #define GS_PREFETCH_STAGES 2
 #endif
 constexpr int kPrefetchStages = GS_PREFETCH_STAGES;
+#ifndef GS_CHUNK_ENTRIES
+#define GS_CHUNK_ENTRIES 0
+#endif
+constexpr int kChunkEntries = GS_CHUNK_ENTRIES;  // narrow rows: gathers in flight per row (0 = off)
+#ifndef GS_CHUNK_MAX_LPR
+#define GS_CHUNK_MAX_LPR 8
+#endif
 
 enum StepMode { MODE_NONE = 0, MODE_SK_PSI = 1, MODE_SK_PHI = 2, MODE_BARY_PSI = 3 };
 
@@ -66,12 +76,22 @@ struct Prec<float> {
   __device__ static __forceinline__ float fmat(float a, float b, float c) { return fmaf(a, b, c); }
 };
 
+// bytes per lane for narrow rows (16 < GW * sizeof(S) <= 64): 8 gives more lanes per row, hence more
+// (col, val) entries per coalesced index load and more gathers in flight per row
+#ifndef GS_NARROW_VEC_BYTES
+#define GS_NARROW_VEC_BYTES 8
+#endif
 template <int GW, typename S>
 struct Lay {
-  static constexpr int VEC = GW * (int)sizeof(S) >= 16 ? 16 / (int)sizeof(S) : GW;
+  static constexpr bool NARROW = GW * (int)sizeof(S) <= 64 && GW * (int)sizeof(S) > 16;
+  static constexpr int VB = NARROW ? GS_NARROW_VEC_BYTES : 16;
+  static constexpr int VEC = GW * (int)sizeof(S) >= VB ? (VB >= (int)sizeof(S) ? VB / (int)sizeof(S) : 1) : GW;
   static constexpr int LPR = GW / VEC;                 // lanes per row
   static constexpr int RPW = 32 / LPR;                 // rows per warp
   static constexpr int ROWS = (kThreads / 32) * RPW;   // rows per CTA block
+  // gathers in flight per row: narrow rows have few registers per gather, so go deeper
+  static constexpr int GB = NARROW ? (GS_NARROW_GATHER_BATCH < LPR ? GS_NARROW_GATHER_BATCH : LPR)
+                                   : kGatherBatch;
 };
 
 // order-preserving uint64 keys for doubles (atomic min/max of signed values)
@@ -128,6 +148,39 @@ __device__ __forceinline__ void st_vec(S* p, const S (&v)[VEC]) {
   } else {
     *p = v[0];
   }
+}
+
+// streaming loads of the CSR entries (used once per step): keep them out of L1 so the neighbour
+// rows of T_{k-1} stay resident (GS_IDX_NOALLOC)
+#ifndef GS_IDX_NOALLOC
+#define GS_IDX_NOALLOC 0
+#endif
+__device__ __forceinline__ int ld_idx(const int* p) {
+#if GS_IDX_NOALLOC
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double ld_idx(const double* p) {
+#if GS_IDX_NOALLOC
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ float ld_idx(const float* p) {
+#if GS_IDX_NOALLOC
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+#else
+  return __ldg(p);
+#endif
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -216,6 +269,51 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
         for (int e = 0; e < VEC; ++e) y[e] = P::fmat(v, x[e], y[e]);
       }
     }
+  } else if constexpr (LPR <= GS_CHUNK_MAX_LPR && kChunkEntries > 0) {
+    // narrow rows (several rows per warp): each lane holds U = CH/LPR (col, val) entries of its
+    // row; all CH gathers of a chunk are issued before the fma chain consumes them in CSR order,
+    // and the next chunk's entries are loaded meanwhile -- the index latency is off the chain.
+    constexpr int CH = kChunkEntries < LPR ? LPR : kChunkEntries;
+    constexpr int U = CH / LPR;
+    const int sub_lane0 = sub * LPR;
+    const unsigned mask = ((1u << LPR) - 1u) << sub_lane0;
+    const int pb = valid ? __ldg(A.offs + row) : 0;
+    const int pe = valid ? __ldg(A.offs + row + 1) : 0;
+    int pc[U];
+    S pv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int p = pb + u * LPR + q;
+      pc[u] = p < pe ? ld_idx(A.cols + p) : 0;
+      pv[u] = p < pe ? ld_idx(vals + p) : S(0);
+    }
+    for (int p0 = pb; p0 < pe; p0 += CH) {
+      int nc[U];
+      S nv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int p = p0 + CH + u * LPR + q;
+        nc[u] = p < pe ? ld_idx(A.cols + p) : 0;
+        nv[u] = p < pe ? ld_idx(vals + p) : S(0);
+      }
+      const int cnt = min(CH, pe - p0);
+      S xx[CH][VEC];
+#pragma unroll
+      for (int e = 0; e < CH; ++e)
+        if (e < cnt) ld_vec<S, VEC>(Tp + (size_t)__shfl_sync(mask, pc[e / LPR], e % LPR, LPR) * GW, xx[e]);
+#pragma unroll
+      for (int e = 0; e < CH; ++e)
+        if (e < cnt) {
+          const S v = __shfl_sync(mask, pv[e / LPR], e % LPR, LPR);
+#pragma unroll
+          for (int f = 0; f < VEC; ++f) y[f] = P::fmat(v, xx[e][f], y[f]);
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        pc[u] = nc[u];
+        pv[u] = nv[u];
+      }
+    }
   } else {
     // the LPR lanes of a row load LPR consecutive (col, val) entries with one coalesced access
     // and broadcast them by shuffle; the fma chain still runs in CSR order.
@@ -223,13 +321,13 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
     const unsigned mask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << sub_lane0);
     const int pb = valid ? __ldg(A.offs + row) : 0;
     const int pe = valid ? __ldg(A.offs + row + 1) : 0;
-    constexpr int GB = kGatherBatch;
+    constexpr int GB = L::GB;
     for (int p0 = pb; p0 < pe; p0 += LPR) {
       int myc = 0;
       S myv = S(0);
       if (p0 + q < pe) {
-        myc = __ldg(A.cols + p0 + q);
-        myv = __ldg(vals + p0 + q);
+        myc = ld_idx(A.cols + p0 + q);
+        myv = ld_idx(vals + p0 + q);
       }
       const int cnt = min(LPR, pe - p0);
       int u = 0;
