@@ -137,15 +137,54 @@ int gs_plan_rows(gs_ctx* ctx, const gs_filter* f, const double* a, const double*
 int gs_graph_save(gs_ctx* ctx, const gs_graph* g, const char* path);
 int gs_graph_load(gs_ctx* ctx, const char* path, gs_graph** out);
 
-/* ---- barycenter (barycenter.hpp:36-42, barycenter.cpp:45-107) ------------------------ */
-/* Optional collective hook for member-sharded barycenters: sums `count` doubles of the
- * device buffer across ranks (op 0 = sum, 1 = max) on `stream`. NULL = single rank. */
+/* ---- collective hooks (multi-process runs) ---------------------------- */
+/* allreduce: reduces `count` doubles of the device buffer in place across ranks (op 0 = sum,
+ * 1 = max) on `stream`. alltoallv: rank r sends send_bytes[q] bytes (consecutive slices of
+ * sendbuf, rank order) to every rank q and receives recv_bytes[q] bytes from q into consecutive
+ * slices of recvbuf; device buffers, on `stream`. Return 0 on success. The engine never links a
+ * collective library itself: the caller's runtime (torch.distributed over NCCL, MPI, ...) does
+ * the transfer. */
 typedef int (*gs_allreduce_fn)(void* user, double* device_buf, int64_t count, int op,
                                void* stream);
+typedef int (*gs_alltoallv_fn)(void* user, const void* sendbuf, const int64_t* send_bytes,
+                               void* recvbuf, const int64_t* recv_bytes, int nranks, void* stream);
 typedef struct {
   gs_allreduce_fn allreduce;
   void* user;
+  gs_alltoallv_fn alltoallv; /* row-partitioned runs only; may be NULL otherwise */
 } gs_comm;
+
+/* ---- row partitions (row-partitioned multi-GPU applies) ----------------- */
+/* The reference is single-process (OpenMP rows, heat.cpp:116-131 over sparse.cpp:85-99); this
+ * splits the same products by rows. Part `part` of `nparts` owns a contiguous nnz-balanced range
+ * of the filter's locality order plus the halo rows its products read; every rank builds its part
+ * from its own replica of the filter. Per-part vectors are n_local = row_end - row_begin values
+ * in the order gs_part_vertices lists (original vertex ids). */
+typedef struct gs_part gs_part;
+int gs_part_create(gs_ctx* ctx, const gs_filter* f, int nparts, int part, gs_part** out);
+void gs_part_destroy(gs_part* p);
+int gs_part_info(const gs_part* p, int* row_begin, int* row_end, int* n_halo, int64_t* nnz_local,
+                 int* n_send);
+/* rows sent to / received from each rank per exchange (nparts entries each, optional) */
+int gs_part_counts(const gs_part* p, int64_t* send_counts, int64_t* recv_counts);
+int gs_part_vertices(gs_ctx* ctx, const gs_part* p, int* out, int mem);
+/* HeatFilter::apply on this part's rows (heat.cpp:116-131): X, Y are `width` contiguous
+ * n_local-vectors; one halo exchange per Chebyshev step through comm->alltoallv (nparts > 1).
+ * flags: GS_FLAG_FP32. Results equal gs_filter_apply's rows bit for bit. */
+int gs_part_filter_apply(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const double* X,
+                         double* Y, int width, int flags, int mem);
+/* geodesic_sinkhorn_batch on this part's rows (transport.cpp:144-239): a, mus, nus, out_v, out_w
+ * hold n_local values per vector; per-column reductions (positivity min/max, L1 error, cost/KL
+ * sums, validation sums) are allreduced so every rank takes the same decisions and returns the
+ * same scalars. Arguments otherwise as gs_sinkhorn. */
+int gs_part_sinkhorn(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const double* a,
+                     const double* mus, const double* nus, int P, int max_iter, double tol,
+                     int flags, int mem, double* out_v, double* out_w, double* out_cost,
+                     double* out_kl, int* out_iters, int* out_conv, double* out_err,
+                     int* fail_pair, int* fail_sweep);
+
+/* ---- barycenter (barycenter.hpp:36-42, barycenter.cpp:45-107) ------------------------ */
+/* `comm` (optional, allreduce only) makes a member-sharded barycenter: NULL = single rank. */
 
 /* members, out_V, out_W: m contiguous n-vectors; alphas: m or NULL (uniform). With a comm,
  * the caller passes its local members and their alphas (global weights). */

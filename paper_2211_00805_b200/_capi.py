@@ -32,10 +32,12 @@ _pd = C.POINTER(C.c_double)
 _pvp = C.POINTER(C.c_void_p)
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p)
+ALLTOALLV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p,
+                           C.POINTER(C.c_int64), C.c_int, C.c_void_p)
 
 
 class GsComm(C.Structure):
-    _fields_ = [("allreduce", ALLREDUCE_FN), ("user", C.c_void_p)]
+    _fields_ = [("allreduce", ALLREDUCE_FN), ("user", C.c_void_p), ("alltoallv", ALLTOALLV_FN)]
 
 
 SIGNATURES = {
@@ -77,6 +79,14 @@ SIGNATURES = {
     "gs_plan_rows": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp]),
     "gs_graph_save": (_i, [_vp, _vp, C.c_char_p]),
     "gs_graph_load": (_i, [_vp, C.c_char_p, _pvp]),
+    "gs_part_create": (_i, [_vp, _vp, _i, _i, _pvp]),
+    "gs_part_destroy": (None, [_vp]),
+    "gs_part_info": (_i, [_vp, _pi, _pi, _pi, _pi64, _pi]),
+    "gs_part_counts": (_i, [_vp, _vp, _vp]),
+    "gs_part_vertices": (_i, [_vp, _vp, _vp, _i]),
+    "gs_part_filter_apply": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _i]),
+    "gs_part_sinkhorn": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _d, _i, _i, _vp, _vp, _vp,
+                              _vp, _vp, _vp, _vp, _pi, _pi]),
     "gs_rng_create": (_vp, [C.c_uint64]),
     "gs_rng_destroy": (None, [_vp]),
     "gs_rng_bits": (C.c_uint64, [_vp]),

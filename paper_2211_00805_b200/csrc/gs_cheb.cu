@@ -115,7 +115,7 @@ __global__ void k_sk_control(const CtlArgs C) {
 // ---- layout conversion: column-major fp64 (API) <-> grouped row-major S (engine) ------------
 template <typename S>
 __global__ void k_pack(const double* __restrict__ src, S* __restrict__ dst, int n, int width,
-                       int GW, int G, const int* __restrict__ order) {
+                       int GW, int G, const int* __restrict__ order, int64_t ld) {
   const int64_t total = (int64_t)G * n * GW;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -125,14 +125,14 @@ __global__ void k_pack(const double* __restrict__ src, S* __restrict__ dst, int 
     const int g = (int)(r / n);
     const int col = g * GW + c;
     const int o = order ? order[i] : i;
-    dst[e] = col < width ? S(src[(size_t)col * n + o]) : S(0);
+    dst[((size_t)g * ld + i) * GW + c] = col < width ? S(src[(size_t)col * n + o]) : S(0);
   }
 }
 
 template <typename S>
 __global__ void k_unpack(const S* __restrict__ src, double* __restrict__ dst, int n, int width,
                          int GW, const S* __restrict__ alt, const int* __restrict__ sel,
-                         const int* __restrict__ newpos) {
+                         const int* __restrict__ newpos, int64_t ld) {
   const int64_t total = (int64_t)width * n;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -140,7 +140,7 @@ __global__ void k_unpack(const S* __restrict__ src, double* __restrict__ dst, in
     const int i0 = (int)(e % n);
     const int i = newpos ? newpos[i0] : i0;
     const int g = col / GW, c = col % GW;
-    const size_t idx = ((size_t)g * n + i) * GW + c;
+    const size_t idx = ((size_t)g * ld + i) * GW + c;
     const S* s = (alt && sel && (sel[col] & 1)) ? alt : src;
     dst[e] = (double)s[idx];
   }
@@ -163,16 +163,17 @@ __global__ void k_gather(const double* __restrict__ src, const int* __restrict__
 // T_0 = a * 1 for the initial phi apply (transport.cpp:171-176 with W = 1), colmax |T_0|
 template <typename S>
 __global__ void k_sk_init(const S* __restrict__ a, S* __restrict__ T0, int n, int GW, int G, int B,
-                          unsigned long long* cmax) {
+                          unsigned long long* cmax, int64_t ld) {
   const int64_t total = (int64_t)G * n * GW;
   double local = 0.0;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(e % GW);
     const int i = (int)((e / GW) % n);
-    const int col = (int)((e / GW) / n) * GW + c;
+    const int g = (int)((e / GW) / n);
+    const int col = g * GW + c;
     const S v = col < B ? a[i] * S(1) : S(0);
-    T0[e] = v;
+    T0[((size_t)g * ld + i) * GW + c] = v;
     if (col < B) local = fmax(local, (double)fabs(v));
   }
   __shared__ double sh[kThreads];
@@ -231,7 +232,7 @@ __global__ void k_sk_cost_partial(const S* __restrict__ a, const S* __restrict__
                                   const S* __restrict__ N, const S* __restrict__ V0,
                                   const S* __restrict__ V1, const S* __restrict__ W,
                                   const int* __restrict__ final_sweep, int n, int GW,
-                                  double* part /* [chunks][P][4] */, int P) {
+                                  double* part /* [chunks][P][4] */, int P, int64_t ld) {
   const int col = blockIdx.y;
   const int64_t c = blockIdx.x;
   const int g = col / GW, cc = col % GW;
@@ -240,7 +241,7 @@ __global__ void k_sk_cost_partial(const S* __restrict__ a, const S* __restrict__
   for (int j = 0; j < DET_J; ++j) {
     const int64_t i = c * DET_CHUNK + (int64_t)j * DET_T + threadIdx.x;
     if (i >= n) break;
-    const size_t idx = ((size_t)g * n + i) * GW + cc;
+    const size_t idx = ((size_t)g * ld + i) * GW + cc;
     const double mu = M[idx], nu = N[idx], ai = a[i];
     if (mu > 0.0) {
       const double lv = log((double)V[idx]);
@@ -517,23 +518,25 @@ void launch_step(gs_ctx* ctx, int gw, int rpc, const StepArgs& A, int mode) {
 template <typename S>
 struct Work {
   int n = 0, B = 0, GW = 1, G = 1, Bpad = 1, tiles = 0, rpc = 1;
+  int64_t ld = 0;  // rows per column group: n, or local + halo rows of a row partition
   int lay = 0;  // filter layout: 0 for one-warp-per-row groups, 1 (degree-sorted) for narrower
   DevBuf<S> T[2], acc;
   DevBuf<unsigned long long> cmin, cmax;
   DevBuf<double> thr, errcol, part_err;
   DevBuf<int> active, gactive;
   DevBuf<gs_status> status;
-  int init(gs_ctx* ctx, int n_, int B_, bool want_err) {
+  int init(gs_ctx* ctx, int n_, int B_, bool want_err, int64_t ld_ = -1) {
     cudaStream_t s = ctx->stream;
     n = n_;
     B = B_;
+    ld = ld_ < 0 ? n_ : ld_;
     GW = choose_gw(B);
     G = (B + GW - 1) / GW;
     Bpad = G * GW;
     lay = GW >= 32 ? 0 : 1;
     rpc = choose_rpc<S>(n, GW, G);
     tiles = (n + rows_per_block<S>(GW) * rpc - 1) / (rows_per_block<S>(GW) * rpc);
-    const size_t len = (size_t)Bpad * n;
+    const size_t len = (size_t)Bpad * (ld > 0 ? ld : 1);
     GS_CUDA(ctx, T[0].alloc(len, s));
     GS_CUDA(ctx, T[1].alloc(len, s));
     GS_CUDA(ctx, acc.alloc(len, s));
@@ -594,6 +597,7 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
   A.cols = G->cols;
   A.vals = layout_vals<S>(Ly);
   A.n = w.n;
+  A.ld = w.ld;
   A.tiles = w.tiles;
   A.g0 = 0;
   A.Gl = w.G;
@@ -719,11 +723,11 @@ int filter_apply_impl(gs_ctx* ctx, const gs_filter* f, const double* dX, double*
   Work<S> w;
   GS_TRY(w.init(ctx, n, width, false));
   gs_launch_begin(ctx, 1);
-  k_pack<S><<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, f->lay[w.lay].order);
+  k_pack<S><<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
   gs_launch_end(ctx, 1);
   run_apply<S>(ctx, f, w, 0, MODE_NONE, nullptr, nullptr, nullptr, nullptr, false, false);
   gs_launch_begin(ctx, 1);
-  k_unpack<S><<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.acc.get(), dY, n, width, w.GW, nullptr, nullptr, f->lay[w.lay].newpos);
+  k_unpack<S><<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.acc.get(), dY, n, width, w.GW, nullptr, nullptr, f->lay[w.lay].newpos, (int64_t)n);
   gs_launch_end(ctx, 1);
   GS_CUDA(ctx, cudaStreamSynchronize(s));
   return GS_OK;
@@ -775,13 +779,13 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
     GS_CUDA(ctx, cudaStreamSynchronize(s));
   }
   gs_launch_begin(ctx, 1);
-  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dmu, M.get(), n, P, w.GW, w.G, f->lay[w.lay].order);
+  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dmu, M.get(), n, P, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
-  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dnu, N.get(), n, P, w.GW, w.G, f->lay[w.lay].order);
+  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dnu, N.get(), n, P, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
-  k_sk_init<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.T[0].get(), n, w.GW, w.G, P, w.cmax.get());
+  k_sk_init<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.T[0].get(), n, w.GW, w.G, P, w.cmax.get(), (int64_t)n);
   gs_launch_end(ctx, 1);
   const int knp = ERRC_KERNEL_NOT_POSITIVE + 1;
   run_finalize<S>(ctx, w, 0, 1, 0, knp, true);  // threshold of the first apply
@@ -894,7 +898,8 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   GS_CUDA(ctx, dkl.alloc(P, s));
   gs_launch_begin(ctx, 1);
   k_sk_cost_partial<S><<<dim3((unsigned)nchunks, P), kThreads, 0, s>>>(
-      da, M.get(), N.get(), V[0].get(), V[1].get(), W.get(), final_sweep.get(), n, w.GW, part.get(), P);
+      da, M.get(), N.get(), V[0].get(), V[1].get(), W.get(), final_sweep.get(), n, w.GW, part.get(), P,
+      (int64_t)n);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
   k_sk_cost_final<<<(P + 63) / 64, 64, 0, s>>>(part.get(), nchunks, P, 4.0 * f->t, dcost.get(), dkl.get());
@@ -910,13 +915,13 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   }
   if (out_v) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)P * n), kThreads, 0, s>>>(V[0].get(), dv, n, P, w.GW, V[1].get(), final_sweep.get(), f->lay[w.lay].newpos);
+    k_unpack<S><<<grid_for((int64_t)P * n), kThreads, 0, s>>>(V[0].get(), dv, n, P, w.GW, V[1].get(), final_sweep.get(), f->lay[w.lay].newpos, (int64_t)n);
     gs_launch_end(ctx, 1);
     GS_TRY(finish_out(ctx, ov, out_v, (size_t)P * n, mem));
   }
   if (out_w) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)P * n), kThreads, 0, s>>>(W.get(), dw, n, P, w.GW, nullptr, nullptr, f->lay[w.lay].newpos);
+    k_unpack<S><<<grid_for((int64_t)P * n), kThreads, 0, s>>>(W.get(), dw, n, P, w.GW, nullptr, nullptr, f->lay[w.lay].newpos, (int64_t)n);
     gs_launch_end(ctx, 1);
     GS_TRY(finish_out(ctx, ow, out_w, (size_t)P * n, mem));
   }
@@ -984,10 +989,10 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   k_fill<<<grid_for(n), kThreads, 0, s>>>(bary.get(), n, 1.0 / n);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
-  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dmem, Mb.get(), n, m, w.GW, w.G, f->lay[w.lay].order);
+  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dmem, Mb.get(), n, m, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
-  k_sk_init<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.T[0].get(), n, w.GW, w.G, m, w.cmax.get());
+  k_sk_init<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.T[0].get(), n, w.GW, w.G, m, w.cmax.get(), (int64_t)n);
   gs_launch_end(ctx, 1);
   run_finalize<S>(ctx, w, 0, 1, 0, 0, false);
   const int knp = ERRC_KERNEL_NOT_POSITIVE + 1;
@@ -1111,13 +1116,13 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   }
   if (out_V) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)m * n), kThreads, 0, s>>>(V[0].get(), dv, n, m, w.GW, V[1].get(), sel.get(), f->lay[w.lay].newpos);
+    k_unpack<S><<<grid_for((int64_t)m * n), kThreads, 0, s>>>(V[0].get(), dv, n, m, w.GW, V[1].get(), sel.get(), f->lay[w.lay].newpos, (int64_t)n);
     gs_launch_end(ctx, 1);
     GS_TRY(finish_out(ctx, ov, out_V, (size_t)m * n, mem));
   }
   if (out_W) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)m * n), kThreads, 0, s>>>(W.get(), dw, n, m, w.GW, nullptr, nullptr, f->lay[w.lay].newpos);
+    k_unpack<S><<<grid_for((int64_t)m * n), kThreads, 0, s>>>(W.get(), dw, n, m, w.GW, nullptr, nullptr, f->lay[w.lay].newpos, (int64_t)n);
     gs_launch_end(ctx, 1);
     GS_TRY(finish_out(ctx, ow, out_W, (size_t)m * n, mem));
   }
@@ -1129,6 +1134,487 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   if (out_iters) *out_iters = h_iters;
   if (out_conv) *out_conv = h_conv;
   if (out_err) *out_err = h_err;
+  return GS_OK;
+}
+
+
+// ============================================================================================
+// Row-partitioned applies (gs_part.cu). The grouped buffers hold nl local rows
+// followed by nh halo rows per column group (Work::ld = nl + nh); before every Chebyshev step the
+// rows other ranks read are packed, exchanged through comm->alltoallv and unpacked into the halo.
+// Per-column reductions are combined through comm->allreduce before any decision is taken, so all
+// ranks follow the same control path (and make the same number of collective calls).
+// ============================================================================================
+template <typename S>
+__global__ void k_halo_pack(const S* __restrict__ T, int64_t ld, int GW, int Bpad,
+                            const int* __restrict__ rows, int ns, S* __restrict__ buf) {
+  const int64_t total = (int64_t)ns * Bpad;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e / Bpad), col = (int)(e % Bpad);
+    buf[e] = T[((size_t)(col / GW) * ld + rows[j]) * GW + (col % GW)];
+  }
+}
+
+template <typename S>
+__global__ void k_halo_unpack(const S* __restrict__ buf, int nh, int nl, int64_t ld, int GW, int Bpad,
+                              S* __restrict__ T) {
+  const int64_t total = (int64_t)nh * Bpad;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(e / Bpad), col = (int)(e % Bpad);
+    T[((size_t)(col / GW) * ld + nl + j) * GW + (col % GW)] = buf[e];
+  }
+}
+
+// local half of k_finalize: fold this rank's error tiles; export -min and max of every column
+__global__ void __launch_bounds__(kThreads) k_fin_local(const FinArgs F, double* stat) {
+  const int col = blockIdx.x;
+  if (col >= F.B) return;
+  __shared__ double sh[kThreads];
+  double acc = 0.0;
+  if (F.has_err) {
+    for (int t = threadIdx.x; t < F.tiles; t += kThreads) acc = acc + F.cs.part_err[(size_t)t * F.Bpad + col];
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = kThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = sh[threadIdx.x] + sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  if (F.has_err) F.cs.errcol[col] = sh[0];
+  stat[col] = -dunkey(F.cs.cmin[col]);
+  stat[F.Bpad + col] = dunkey(F.cs.cmax[col]);
+}
+
+// global half: the positivity check and the next threshold from the combined column extrema
+__global__ void k_fin_global(const FinArgs F, const double* stat) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= F.B) return;
+  const bool act = !F.cs.active || F.cs.active[col];
+  if (F.check && act && F.status->error == 0) {
+    const double mn = -stat[col];
+    if (!(mn >= -F.cs.thr[col])) atomicCAS(&F.status->error, 0, F.knp_code);
+  }
+  if (F.has_next) F.cs.thr[col] = F.slack * stat[F.Bpad + col];
+  F.cs.cmin[col] = KEY_POS_INF;
+  F.cs.cmax[col] = KEY_ZERO;
+}
+
+__global__ void k_sk_cost_sums(const double* part, int64_t nchunks, int P, double* sums) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= P) return;
+  double s[4] = {0, 0, 0, 0};
+  for (int64_t c = 0; c < nchunks; ++c)
+    for (int q = 0; q < 4; ++q) s[q] = s[q] + part[((size_t)c * P + col) * 4 + q];
+  for (int q = 0; q < 4; ++q) sums[(size_t)col * 4 + q] = s[q];
+}
+
+__global__ void k_sk_cost_from_sums(const double* sums, int P, double lambda, double* cost, double* kl) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= P) return;
+  const double* s = sums + (size_t)col * 4;
+  cost[col] = lambda * (s[0] + s[1]);
+  kl[col] = s[2] + s[3] - 1.0;
+}
+
+__global__ void k_int_to_double(const int* __restrict__ x, int n, double* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = (double)x[i];
+}
+
+int hook_fail(gs_ctx* ctx, const char* what) {
+  ctx->err = std::string("NcclError: ") + what + " hook failed";
+  return GS_ERR_NCCL;
+}
+
+int allreduce(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, double* buf, int64_t count, int op) {
+  if (p->nparts == 1 || count == 0) return GS_OK;
+  if (comm->allreduce(comm->user, buf, count, op, (void*)ctx->stream)) return hook_fail(ctx, "allreduce");
+  return GS_OK;
+}
+
+template <typename S>
+struct Halo {
+  DevBuf<S> send, recv;
+  std::vector<int64_t> sb, rb;  // bytes per rank
+  int init(gs_ctx* ctx, const gs_part* p, int Bpad) {
+    sb.resize(p->nparts);
+    rb.resize(p->nparts);
+    for (int q = 0; q < p->nparts; ++q) {
+      sb[q] = p->send_counts[q] * Bpad * (int64_t)sizeof(S);
+      rb[q] = p->recv_counts[q] * Bpad * (int64_t)sizeof(S);
+    }
+    GS_CUDA(ctx, send.alloc((size_t)p->ns * Bpad, ctx->stream));
+    GS_CUDA(ctx, recv.alloc((size_t)p->nh * Bpad, ctx->stream));
+    return GS_OK;
+  }
+};
+
+template <typename S>
+int halo_exchange(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const Work<S>& w, S* T, Halo<S>& h) {
+  if (p->nparts == 1) return GS_OK;
+  cudaStream_t s = ctx->stream;
+  if (p->ns > 0) {
+    gs_launch_begin(ctx, 1);
+    k_halo_pack<S><<<grid_for((int64_t)p->ns * w.Bpad), kThreads, 0, s>>>(T, w.ld, w.GW, w.Bpad, p->send_rows, p->ns, h.send.get());
+    gs_launch_end(ctx, 1);
+  }
+  if (comm->alltoallv(comm->user, h.send.get(), h.sb.data(), h.recv.get(), h.rb.data(), p->nparts, (void*)s))
+    return hook_fail(ctx, "alltoallv");
+  if (p->nh > 0) {
+    gs_launch_begin(ctx, 1);
+    k_halo_unpack<S><<<grid_for((int64_t)p->nh * w.Bpad), kThreads, 0, s>>>(h.recv.get(), p->nh, p->nl, w.ld, w.GW, w.Bpad, T);
+    gs_launch_end(ctx, 1);
+  }
+  return GS_OK;
+}
+
+// run_apply over this part's rows, one halo exchange of T_{k-1} before every step
+template <typename S>
+int run_apply_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& w, Halo<S>& h, int a0,
+                   int mode, const S* a, const S* M, const S* Vcur, S* Wout, bool use_active,
+                   bool use_status, int* next) {
+  const gs_filter* f = p->f;
+  const int K = f->degree;
+  StepArgs A{};
+  A.offs = p->local->offs;
+  A.cols = p->local->cols;
+  if constexpr (sizeof(S) == 4) A.vals = p->vals32;
+  else A.vals = p->local->vals;
+  A.n = w.n;
+  A.ld = w.ld;
+  A.tiles = w.tiles;
+  A.g0 = 0;
+  A.Gl = w.G;
+  A.Bpad = w.Bpad;
+  A.acc = w.acc.get();
+  A.b0h = f->coeffs[0] / 2.0;
+  A.status = use_status ? w.status.get() : nullptr;
+  A.cs = w.cs();
+  if (!use_active) {
+    A.cs.active = nullptr;
+    A.cs.gactive = nullptr;
+  }
+  A.a = a;
+  A.M = M;
+  A.Vcur = Vcur;
+  A.Wout = Wout;
+  for (int k = 1; k <= K; ++k) {
+    A.k = k;
+    A.bk = f->coeffs[k];
+    A.Tprev = w.T[(a0 + k - 1) & 1].get();
+    A.Tout = w.T[(a0 + k) & 1].get();
+    GS_TRY(halo_exchange<S>(ctx, p, comm, w, w.T[(a0 + k - 1) & 1].get(), h));
+    if (w.tiles > 0) launch_step<S>(ctx, w.GW, w.rpc, A, k == K ? mode : MODE_NONE);
+  }
+  *next = (a0 + K) & 1;
+  return GS_OK;
+}
+
+template <typename S>
+int run_finalize_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& w, double* stat,
+                      int check, int has_next, int has_err, int knp_code, bool use_active) {
+  FinArgs F{};
+  F.cs = w.cs();
+  if (!use_active) F.cs.active = nullptr;
+  F.B = w.B;
+  F.tiles = w.tiles;
+  F.Bpad = w.Bpad;
+  F.check = check;
+  F.has_next = has_next;
+  F.has_err = has_err;
+  F.status = w.status.get();
+  F.knp_code = knp_code;
+  F.slack = Prec<S>::slack;
+  gs_launch_begin(ctx, 1);
+  k_fin_local<<<w.B, kThreads, 0, ctx->stream>>>(F, stat);
+  gs_launch_end(ctx, 1);
+  GS_TRY(allreduce(ctx, p, comm, stat, 2 * (int64_t)w.Bpad, 1));
+  if (has_err) GS_TRY(allreduce(ctx, p, comm, w.errcol.get(), w.B, 0));
+  gs_launch_begin(ctx, 1);
+  k_fin_global<<<(w.B + kThreads - 1) / kThreads, kThreads, 0, ctx->stream>>>(F, stat);
+  gs_launch_end(ctx, 1);
+  return GS_OK;
+}
+
+template <typename S>
+int filter_apply_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const double* dX,
+                           double* dY, int width) {
+  const int nl = p->nl;
+  cudaStream_t s = ctx->stream;
+  Work<S> w;
+  GS_TRY(w.init(ctx, nl, width, false, (int64_t)nl + p->nh));
+  Halo<S> h;
+  GS_TRY(h.init(ctx, p, w.Bpad));
+  if (nl > 0) {
+    gs_launch_begin(ctx, 1);
+    k_pack<S><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(dX, w.T[0].get(), nl, width, w.GW, w.G, nullptr, w.ld);
+    gs_launch_end(ctx, 1);
+  }
+  int next = 0;
+  GS_TRY(run_apply_part<S>(ctx, p, comm, w, h, 0, MODE_NONE, nullptr, nullptr, nullptr, nullptr, false, false, &next));
+  if (nl > 0) {
+    gs_launch_begin(ctx, 1);
+    k_unpack<S><<<grid_for((int64_t)width * nl), kThreads, 0, s>>>(w.acc.get(), dY, nl, width, w.GW, nullptr, nullptr, nullptr, w.ld);
+    gs_launch_end(ctx, 1);
+  }
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  return GS_OK;
+}
+
+// geodesic Sinkhorn batch on one part (transport.cpp:144-239; same control as sinkhorn_impl)
+template <typename S>
+int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const double* da_user,
+                       const double* dmu, const double* dnu, int P, int max_iter, double tol, int flags,
+                       int mem, double* out_v, double* out_w, double* out_cost, double* out_kl,
+                       int* out_iters, int* out_conv, double* out_err, int* fail_pair, int* fail_sweep) {
+  const int nl = p->nl;
+  cudaStream_t s = ctx->stream;
+  Work<S> w;
+  GS_TRY(w.init(ctx, nl, P, true, (int64_t)nl + p->nh));
+  Halo<S> h;
+  GS_TRY(h.init(ctx, p, w.Bpad));
+  DevBuf<double> stat;
+  GS_CUDA(ctx, stat.alloc(2 * (size_t)w.Bpad, s));
+  DevBuf<S> aloc;
+  GS_CUDA(ctx, aloc.alloc(nl, s));
+  if (nl > 0) {
+    gs_launch_begin(ctx, 1);
+    k_gather_to<S><<<(nl + kThreads - 1) / kThreads, kThreads, 0, s>>>(da_user, nullptr, nl, aloc.get());
+    gs_launch_end(ctx, 1);
+  }
+  const S* da = aloc.get();
+  const size_t len = (size_t)w.Bpad * w.ld;
+  DevBuf<S> M, N, V[2], W;
+  GS_CUDA(ctx, M.alloc(len, s));
+  GS_CUDA(ctx, N.alloc(len, s));
+  GS_CUDA(ctx, V[0].alloc(len, s));
+  GS_CUDA(ctx, V[1].alloc(len, s));
+  GS_CUDA(ctx, W.alloc(len, s));
+  DevBuf<int> iters, conv, stag, final_sweep;
+  DevBuf<double> errv;
+  GS_CUDA(ctx, iters.alloc(w.Bpad, s));
+  GS_CUDA(ctx, conv.alloc(w.Bpad, s));
+  GS_CUDA(ctx, stag.alloc(w.Bpad, s));
+  GS_CUDA(ctx, final_sweep.alloc(w.Bpad, s));
+  GS_CUDA(ctx, errv.alloc(w.Bpad, s));
+  GS_CUDA(ctx, cudaMemsetAsync(iters.get(), 0, w.Bpad * sizeof(int), s));
+  GS_CUDA(ctx, cudaMemsetAsync(conv.get(), 0, w.Bpad * sizeof(int), s));
+  GS_CUDA(ctx, cudaMemsetAsync(stag.get(), 0, w.Bpad * sizeof(int), s));
+  GS_CUDA(ctx, cudaMemsetAsync(final_sweep.get(), 0, w.Bpad * sizeof(int), s));
+  GS_CUDA(ctx, cudaMemsetAsync(V[0].get(), 0, len * sizeof(S), s));
+  GS_CUDA(ctx, cudaMemsetAsync(W.get(), 0, len * sizeof(S), s));
+  {
+    std::vector<int> act(w.Bpad, 0);
+    for (int q = 0; q < P; ++q) act[q] = 1;
+    GS_CUDA(ctx, cudaMemcpyAsync(w.active.get(), act.data(), w.Bpad * sizeof(int), cudaMemcpyHostToDevice, s));
+    std::vector<double> inf(w.Bpad, INFINITY);
+    GS_CUDA(ctx, cudaMemcpyAsync(errv.get(), inf.data(), w.Bpad * sizeof(double), cudaMemcpyHostToDevice, s));
+    GS_CUDA(ctx, cudaStreamSynchronize(s));
+  }
+  if (nl > 0) {
+    gs_launch_begin(ctx, 1);
+    k_pack<S><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(dmu, M.get(), nl, P, w.GW, w.G, nullptr, w.ld);
+    gs_launch_end(ctx, 1);
+    gs_launch_begin(ctx, 1);
+    k_pack<S><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(dnu, N.get(), nl, P, w.GW, w.G, nullptr, w.ld);
+    gs_launch_end(ctx, 1);
+    gs_launch_begin(ctx, 1);
+    k_sk_init<S><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(da, w.T[0].get(), nl, w.GW, w.G, P, w.cmax.get(), w.ld);
+    gs_launch_end(ctx, 1);
+  }
+  const int knp = ERRC_KERNEL_NOT_POSITIVE + 1;
+  int a0 = 0;
+  GS_TRY(run_finalize_part<S>(ctx, p, comm, w, stat.get(), 0, 1, 0, knp, true));
+  GS_TRY(run_apply_part<S>(ctx, p, comm, w, h, 0, MODE_SK_PHI, da, M.get(), V[0].get(), V[1].get(), true, true, &a0));
+  GS_TRY(run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 0, knp, true));
+  CtlArgs C{};
+  C.active = w.active.get();
+  C.gactive = w.gactive.get();
+  C.GW = w.GW;
+  C.errcol = w.errcol.get();
+  C.iters = iters.get();
+  C.conv = conv.get();
+  C.stag = stag.get();
+  C.final_sweep = final_sweep.get();
+  C.err_out = errv.get();
+  C.status = w.status.get();
+  C.P = P;
+  C.max_iter = max_iter;
+  C.no_abort = (flags & GS_FLAG_NO_STAGNATION_ABORT) ? 1 : 0;
+  C.tol = tol;
+  DevBuf<int> sweep_ctr;
+  GS_CUDA(ctx, sweep_ctr.alloc(1, s));
+  GS_CUDA(ctx, cudaMemsetAsync(sweep_ctr.get(), 0, sizeof(int), s));
+  C.sweep_ctr = sweep_ctr.get();
+  gs_status* hst = ctx->h_status;
+  cudaEvent_t ev[2];
+  cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+  int rc = GS_OK;
+  for (int sweep = 1, it = 0; sweep <= max_iter; ++sweep, ++it) {
+    if (it >= 2) {  // every rank sees the same status (same global reductions) -> same exit sweep
+      const int slot = (it - 2) & 1;
+      cudaEventSynchronize(ev[slot]);
+      const gs_status st = hst[slot];
+      if (st.error || st.n_active == 0) break;
+    }
+    rc = run_apply_part<S>(ctx, p, comm, w, h, a0, MODE_SK_PSI, da, N.get(), nullptr, W.get(), true, true, &a0);
+    if (!rc) rc = run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 0, knp, true);
+    if (!rc)
+      rc = run_apply_part<S>(ctx, p, comm, w, h, a0, MODE_SK_PHI, da, M.get(), V[sweep & 1].get(),
+                             V[(sweep & 1) ^ 1].get(), true, true, &a0);
+    if (!rc) rc = run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 1, knp, true);
+    if (rc) break;
+    gs_launch_begin(ctx, 1);
+    k_sk_control<<<1, 1, 0, s>>>(C);
+    gs_launch_end(ctx, 1);
+    const int slot = it & 1;
+    cudaMemcpyAsync(&hst[slot], w.status.get(), sizeof(gs_status), cudaMemcpyDeviceToHost, s);
+    cudaEventRecord(ev[slot], s);
+  }
+  cudaStreamSynchronize(s);
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  if (rc) return rc;
+  gs_status st;
+  GS_CUDA(ctx, cudaMemcpy(&st, w.status.get(), sizeof st, cudaMemcpyDeviceToHost));
+  if (st.error) {
+    if (st.error == ERRC_DISCONNECTED + 1) {
+      if (fail_pair) *fail_pair = st.fail_pair;
+      if (fail_sweep) *fail_sweep = st.fail_sweep;
+      if (flags & GS_FLAG_SINGLE)
+        return gs_fail(ctx, ERRC_DISCONNECTED,
+                       "marginal error stagnated above 0.5; are mu and nu in the same graph component?");
+      return gs_fail(ctx, ERRC_DISCONNECTED,
+                     "marginal error stagnated above 0.5 for pair " + std::to_string(st.fail_pair));
+    }
+    return gs_fail(ctx, ERRC_KERNEL_NOT_POSITIVE, kKnpTransport);
+  }
+  // ---- cost / KL: local DET-chunk partials, combined across ranks ---------------------------------
+  const int64_t nchunks = (nl + DET_CHUNK - 1) / DET_CHUNK;
+  DevBuf<double> part, sums, dcost, dkl;
+  GS_CUDA(ctx, part.alloc((size_t)(nchunks ? nchunks : 1) * P * 4, s));
+  GS_CUDA(ctx, sums.alloc((size_t)P * 4, s));
+  GS_CUDA(ctx, dcost.alloc(P, s));
+  GS_CUDA(ctx, dkl.alloc(P, s));
+  if (nchunks > 0) {
+    gs_launch_begin(ctx, 1);
+    k_sk_cost_partial<S><<<dim3((unsigned)nchunks, P), kThreads, 0, s>>>(
+        da, M.get(), N.get(), V[0].get(), V[1].get(), W.get(), final_sweep.get(), nl, w.GW, part.get(), P, w.ld);
+    gs_launch_end(ctx, 1);
+  }
+  gs_launch_begin(ctx, 1);
+  k_sk_cost_sums<<<(P + 63) / 64, 64, 0, s>>>(part.get(), nchunks, P, sums.get());
+  gs_launch_end(ctx, 1);
+  GS_TRY(allreduce(ctx, p, comm, sums.get(), 4 * (int64_t)P, 0));
+  gs_launch_begin(ctx, 1);
+  k_sk_cost_from_sums<<<(P + 63) / 64, 64, 0, s>>>(sums.get(), P, 4.0 * p->f->t, dcost.get(), dkl.get());
+  gs_launch_end(ctx, 1);
+  DevBuf<double> ov, ow;
+  double* dv = out_v;
+  double* dw = out_w;
+  if (mem != GS_MEM_DEVICE) {
+    GS_CUDA(ctx, ov.alloc((size_t)P * nl, s));
+    GS_CUDA(ctx, ow.alloc((size_t)P * nl, s));
+    dv = ov.get();
+    dw = ow.get();
+  }
+  if (out_v && nl > 0) {
+    gs_launch_begin(ctx, 1);
+    k_unpack<S><<<grid_for((int64_t)P * nl), kThreads, 0, s>>>(V[0].get(), dv, nl, P, w.GW, V[1].get(), final_sweep.get(), nullptr, w.ld);
+    gs_launch_end(ctx, 1);
+    GS_TRY(finish_out(ctx, ov, out_v, (size_t)P * nl, mem));
+  }
+  if (out_w && nl > 0) {
+    gs_launch_begin(ctx, 1);
+    k_unpack<S><<<grid_for((int64_t)P * nl), kThreads, 0, s>>>(W.get(), dw, nl, P, w.GW, nullptr, nullptr, nullptr, w.ld);
+    gs_launch_end(ctx, 1);
+    GS_TRY(finish_out(ctx, ow, out_w, (size_t)P * nl, mem));
+  }
+  auto out_small = [&](void* dst, const void* src, size_t bytes) -> int {
+    if (!dst) return GS_OK;
+    GS_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes,
+                                 mem == GS_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    return GS_OK;
+  };
+  GS_TRY(out_small(out_cost, dcost.get(), P * sizeof(double)));
+  GS_TRY(out_small(out_kl, dkl.get(), P * sizeof(double)));
+  GS_TRY(out_small(out_iters, iters.get(), P * sizeof(int)));
+  GS_TRY(out_small(out_conv, conv.get(), P * sizeof(int)));
+  GS_TRY(out_small(out_err, errv.get(), P * sizeof(double)));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  return GS_OK;
+}
+
+// Distribution::validate (transport.cpp:96-102) of P local column slices, sums combined across
+// ranks: returns per-column global sum, non-finite and negative flags on the host.
+int validate_columns_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const double* d, int P,
+                          std::vector<double>& sums, std::vector<int>& nonfinite, std::vector<int>& negative) {
+  cudaStream_t s = ctx->stream;
+  DevBuf<double> dsum, dflags;
+  DevBuf<int> dnf, dng;
+  GS_CUDA(ctx, dsum.alloc(P, s));
+  GS_CUDA(ctx, dflags.alloc(2 * (size_t)P, s));
+  GS_CUDA(ctx, dnf.alloc(P, s));
+  GS_CUDA(ctx, dng.alloc(P, s));
+  GS_CUDA(ctx, cudaMemsetAsync(dnf.get(), 0, P * sizeof(int), s));
+  GS_CUDA(ctx, cudaMemsetAsync(dng.get(), 0, P * sizeof(int), s));
+  gs_launch_begin(ctx, 1);
+  k_validate_cols<<<dim3(1, P), kThreads, 0, s>>>(d, p->nl, dsum.get(), dnf.get(), dng.get());
+  gs_launch_end(ctx, 1);
+  gs_launch_begin(ctx, 1);
+  k_int_to_double<<<(P + kThreads - 1) / kThreads, kThreads, 0, s>>>(dnf.get(), P, dflags.get());
+  gs_launch_end(ctx, 1);
+  gs_launch_begin(ctx, 1);
+  k_int_to_double<<<(P + kThreads - 1) / kThreads, kThreads, 0, s>>>(dng.get(), P, dflags.get() + P);
+  gs_launch_end(ctx, 1);
+  GS_TRY(allreduce(ctx, p, comm, dsum.get(), P, 0));
+  GS_TRY(allreduce(ctx, p, comm, dflags.get(), 2 * (int64_t)P, 1));
+  std::vector<double> fl(2 * (size_t)P);
+  sums.resize(P);
+  GS_CUDA(ctx, cudaMemcpyAsync(sums.data(), dsum.get(), P * sizeof(double), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaMemcpyAsync(fl.data(), dflags.get(), 2 * P * sizeof(double), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  nonfinite.assign(P, 0);
+  negative.assign(P, 0);
+  for (int q = 0; q < P; ++q) {
+    nonfinite[q] = fl[q] > 0.0;
+    negative[q] = fl[P + q] > 0.0;
+  }
+  return GS_OK;
+}
+
+// collective half of check_weights: *bad = some rank holds a non-positive weight
+int weights_bad_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const double* da, bool* bad_out) {
+  cudaStream_t s = ctx->stream;
+  DevBuf<int> bad;
+  DevBuf<double> dbad;
+  GS_CUDA(ctx, bad.alloc(1, s));
+  GS_CUDA(ctx, dbad.alloc(1, s));
+  GS_CUDA(ctx, cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+  if (p->nl > 0) {
+    gs_launch_begin(ctx, 1);
+    k_validate_weights<<<(p->nl + 255) / 256, 256, 0, s>>>(da, p->nl, bad.get());
+    gs_launch_end(ctx, 1);
+  }
+  gs_launch_begin(ctx, 1);
+  k_int_to_double<<<1, 1, 0, s>>>(bad.get(), 1, dbad.get());
+  gs_launch_end(ctx, 1);
+  GS_TRY(allreduce(ctx, p, comm, dbad.get(), 1, 1));
+  double h = 0.0;
+  GS_CUDA(ctx, cudaMemcpyAsync(&h, dbad.get(), sizeof(double), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  *bad_out = h > 0.0;
+  return GS_OK;
+}
+
+int check_part_comm(gs_ctx* ctx, const gs_part* p, const gs_comm* comm) {
+  if (!p) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "null partition");
+  if (p->nparts > 1 && (!comm || !comm->allreduce || !comm->alltoallv))
+    return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "a partition of several ranks needs allreduce and alltoallv hooks");
   return GS_OK;
 }
 
@@ -1287,13 +1773,14 @@ extern "C" int gs_graph_multiply(gs_ctx* ctx, const gs_graph* g, const double* x
     dY = yout.get();
   }
   gs_launch_begin(ctx, 1);
-  k_pack<double><<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, nullptr);
+  k_pack<double><<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, nullptr, (int64_t)n);
   gs_launch_end(ctx, 1);
   StepArgs A{};
   A.offs = g->offs;
   A.cols = g->cols;
   A.vals = g->vals;
   A.n = n;
+  A.ld = n;
   A.tiles = w.tiles;
   A.Gl = w.G;
   A.Bpad = w.Bpad;
@@ -1302,7 +1789,7 @@ extern "C" int gs_graph_multiply(gs_ctx* ctx, const gs_graph* g, const double* x
   A.Tout = w.T[1].get();
   launch_step<double>(ctx, w.GW, w.rpc, A, MODE_NONE);
   gs_launch_begin(ctx, 1);
-  k_unpack<double><<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.T[1].get(), dY, n, width, w.GW, nullptr, nullptr, nullptr);
+  k_unpack<double><<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.T[1].get(), dY, n, width, w.GW, nullptr, nullptr, nullptr, (int64_t)n);
   gs_launch_end(ctx, 1);
   GS_TRY(finish_out(ctx, yout, y, (size_t)width * n, mem));
   GS_CUDA(ctx, cudaStreamSynchronize(s));
@@ -1468,4 +1955,68 @@ extern "C" int gs_plan_rows(gs_ctx* ctx, const gs_filter* f, const double* a, co
   GS_TRY(gs_copy_out(ctx, out, Y.get(), (size_t)nrows * n * sizeof(double), mem));
   GS_CUDA(ctx, cudaStreamSynchronize(s));
   return GS_OK;
+}
+
+// ============================================================================================
+// Row-partitioned entry points (gs_part.cu)
+// ============================================================================================
+extern "C" int gs_part_filter_apply(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const double* X,
+                                    double* Y, int width, int flags, int mem) {
+  GS_TRY(check_part_comm(ctx, p, comm));
+  if (width < 0) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "width");
+  if (width == 0) return GS_OK;
+  const int nl = p->nl;
+  DevBuf<double> xin, yout;
+  const double* dX = nullptr;
+  GS_TRY(stage_in(ctx, xin, X, (size_t)width * nl, mem, &dX));
+  double* dY = Y;
+  if (mem != GS_MEM_DEVICE) {
+    GS_CUDA(ctx, yout.alloc((size_t)width * nl, ctx->stream));
+    dY = yout.get();
+  }
+  const int rc = (flags & GS_FLAG_FP32) ? filter_apply_part_impl<float>(ctx, p, comm, dX, dY, width)
+                                        : filter_apply_part_impl<double>(ctx, p, comm, dX, dY, width);
+  if (rc) return rc;
+  GS_TRY(finish_out(ctx, yout, Y, (size_t)width * nl, mem));
+  GS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GS_OK;
+}
+
+extern "C" int gs_part_sinkhorn(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const double* a,
+                                const double* mus, const double* nus, int P, int max_iter, double tol,
+                                int flags, int mem, double* out_v, double* out_w, double* out_cost,
+                                double* out_kl, int* out_iters, int* out_conv, double* out_err,
+                                int* fail_pair, int* fail_sweep) {
+  if (fail_pair) *fail_pair = -1;
+  if (fail_sweep) *fail_sweep = 0;
+  GS_TRY(check_part_comm(ctx, p, comm));
+  const int nl = p->nl;
+  if (P < 0) return gs_fail(ctx, ERRC_SIZE_MISMATCH, "pair lists differ in length");
+  if (P == 0) return GS_OK;
+  DevBuf<double> bmu, bnu, ba;
+  const double *dmu, *dnu, *da;
+  GS_TRY(stage_in(ctx, bmu, mus, (size_t)P * nl, mem, &dmu));
+  GS_TRY(stage_in(ctx, bnu, nus, (size_t)P * nl, mem, &dnu));
+  GS_TRY(stage_in(ctx, ba, a, (size_t)nl, mem, &da));
+  {  // check_transport_inputs (transport.cpp:56-66) on the combined column sums, pair order
+    std::vector<double> smu, snu;
+    std::vector<int> fmu, gmu, fnu, gnu;
+    GS_TRY(validate_columns_part(ctx, p, comm, dmu, P, smu, fmu, gmu));
+    GS_TRY(validate_columns_part(ctx, p, comm, dnu, P, snu, fnu, gnu));
+    bool wbad = false;
+    GS_TRY(weights_bad_part(ctx, p, comm, da, &wbad));  // collective: every rank calls it once
+    const int n = p->n_global;
+    for (int q = 0; q < P; ++q) {
+      GS_TRY(check_distribution(ctx, n, smu[q], fmu[q], gmu[q]));
+      GS_TRY(check_distribution(ctx, n, snu[q], fnu[q], gnu[q]));
+      if (q == 0 && wbad) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "vertex weights must be positive");
+      if (!(tol > 0.0)) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "tolerance must be positive");
+      if (max_iter < 1) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "max_iter must be >= 1");
+    }
+  }
+  if (flags & GS_FLAG_FP32)
+    return sinkhorn_part_impl<float>(ctx, p, comm, da, dmu, dnu, P, max_iter, tol, flags, mem, out_v, out_w,
+                                     out_cost, out_kl, out_iters, out_conv, out_err, fail_pair, fail_sweep);
+  return sinkhorn_part_impl<double>(ctx, p, comm, da, dmu, dnu, P, max_iter, tol, flags, mem, out_v, out_w,
+                                    out_cost, out_kl, out_iters, out_conv, out_err, fail_pair, fail_sweep);
 }

@@ -81,6 +81,23 @@ struct gs_filter {
   double* d_coeffs = nullptr;
 };
 
+// One rank's row partition of a filter (gs_part.cu; SURVEY.md §8(e) "row partitioning"): a
+// contiguous nnz-balanced range [row_begin, row_end) of the filter's Cuthill-McKee order (lay[0]).
+// Local rows keep their CSR entries in the original order with columns renumbered: [0, nl) local
+// rows, [nl, nl + nh) halo rows sorted by (owner rank, position). Rows this rank sends to rank q
+// (its rows adjacent to q's range, ascending) are send_rows[send_offs[q] .. send_offs[q + 1]).
+struct gs_part {
+  const gs_filter* f = nullptr;
+  int nparts = 1, part = 0;
+  int n_global = 0, row_begin = 0, row_end = 0, nl = 0, nh = 0, ns = 0;
+  gs_graph* local = nullptr;
+  float* vals32 = nullptr;
+  int* vertices = nullptr;   // nl: original vertex id of each local row
+  int* send_rows = nullptr;  // ns local row indices
+  std::vector<int> bounds;   // nparts + 1 positions
+  std::vector<int64_t> send_counts, recv_counts;  // rows per rank
+};
+
 // ---- error plumbing ----------------------------------------------------------------------
 int gs_fail(gs_ctx* ctx, int errc, const std::string& what);  // returns errc + 1
 int gs_cuda_fail(gs_ctx* ctx, cudaError_t e, const char* where);

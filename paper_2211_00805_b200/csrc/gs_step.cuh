@@ -208,6 +208,7 @@ struct StepArgs {  // vector pointers are S* of the launch's precision
   const int* __restrict__ cols;
   const void* vals;
   int n, tiles, g0, Gl, Bpad;
+  int64_t ld;         // rows per column group (n, or local + halo rows for a row partition)
   const void* Tprev;  // T_{k-1}
   void* Tout;         // T_{k-2} in, T_k out (or next T_0 / SpMM output)
   void* acc;
@@ -232,7 +233,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
   constexpr int VEC = L::VEC, LPR = L::LPR;
   using P = Prec<S>;
   const bool valid = row < A.n;
-  const size_t gbase = (size_t)g * A.n * GW + q * VEC;
+  const size_t gbase = (size_t)g * A.ld * GW + q * VEC;
   const size_t idx = gbase + (size_t)(valid ? row : 0) * GW;
   const S* __restrict__ Tp = static_cast<const S*>(A.Tprev) + gbase;
   const S* __restrict__ vals = static_cast<const S*>(A.vals);
@@ -501,7 +502,7 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step(const StepArgs A) {
     constexpr int STG = kPrefetchStages;
     constexpr int PS = kThreads * VEC;  // elements per operand per stage
     __shared__ __align__(16) S s_pre[STG][3][PS];
-    const size_t gbase = (size_t)g * A.n * GW + q * VEC;
+    const size_t gbase = (size_t)g * A.ld * GW + q * VEC;
     auto issue = [&](int j) {
       const int row = base + j * BLOCK_ROWS;
       if (j < RPC && row < A.n && A.k != 0) {

@@ -5,10 +5,12 @@ The only real exchange on the hot path is the member-sharded 
   * allreduce(SUM) of the n-vector sum_i alpha_i ln clamp(psi_i) over ranks
     (barycenter.cpp:75-78; the reference's member-order sum is re-associated across ranks), and
   * allreduce(MAX) of the per-rank marginal error (barycenter.cpp:86),
-after which every rank computes the same barycenter. The engine calls these through the C ABI
-hook `gs_comm.allreduce(user, buf, count, op, stream)`; `TorchAllreduce` implements it with
-torch.distributed on the engine's stream (NCCL for device buffers, gloo for host buffers).
-Distance pairs (config 1) need no collective: ranks run independent pair shards.
+after which every rank computes the same barycenter. Row-partitioned runs (config 3; the graph
+split into contiguous row ranges, RowPartition) add one halo exchange per Chebyshev step
+(`gs_comm.alltoallv`) and allreduces of the per-column reductions. The engine calls both through
+the C ABI hooks; `TorchComm` implements them with torch.distributed on the engine's stream (NCCL
+for device buffers, gloo for host buffers). Distance pairs (config 1) need no collective: ranks
+run independent pair shards.
 """
 from __future__ import annotations
 
@@ -19,7 +21,7 @@ import numpy as np
 
 from . import _capi
 from .geosink import (BarycenterResult, Distribution, DistributionFamily, HeatFilter,
-                      SinkhornParams, _f64, _ptr, _stack)
+                      RowPartition, SinkhornParams, _f64, _ptr, _stack)
 
 
 def member_shard(m: int, world: int, rank: int) -> tuple[int, int]:
@@ -37,8 +39,17 @@ class _CudaArray:
                                          "data": (ptr, False), "version": 3}
 
 
-class TorchAllreduce:
-    """gs_comm hook over torch.distributed. Keeps the ctypes callback alive."""
+class _CudaBytes:
+    """__cuda_array_interface__ byte view of a raw device pointer (no copy)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "|u1",
+                                         "data": (ptr or 0, False), "version": 3}
+
+
+class TorchComm:
+    """gs_comm hooks over torch.distributed (allreduce + alltoallv). Keeps the ctypes callbacks
+    alive; an exception inside a hook is stored in `error` and re-raised by the caller."""
 
     def __init__(self, group=None, device_buffers: bool = True):
         import torch
@@ -66,12 +77,74 @@ class TorchAllreduce:
                 self.error = e
                 return 1
 
+        def _a2a(user, sendbuf, send_bytes, recvbuf, recv_bytes, nranks, stream):
+            try:
+                self.a2a_calls += 1
+                sb = [int(send_bytes[q]) for q in range(nranks)]
+                rb = [int(recv_bytes[q]) for q in range(nranks)]
+                if self._device:
+                    snd = torch.as_tensor(_CudaBytes(sendbuf, sum(sb)), device="cuda")
+                    rcv = torch.as_tensor(_CudaBytes(recvbuf, sum(rb)), device="cuda")
+                    with torch.cuda.stream(torch.cuda.ExternalStream(stream)):
+                        dist.all_to_all_single(rcv, snd, output_split_sizes=rb,
+                                               input_split_sizes=sb, group=self._group)
+                else:
+                    snd = torch.from_numpy(_host_bytes(sendbuf, sum(sb)))
+                    rcv = torch.from_numpy(_host_bytes(recvbuf, sum(rb)))
+                    dist.all_to_all_single(rcv, snd, output_split_sizes=rb, input_split_sizes=sb,
+                                           group=self._group)
+                return 0
+            except BaseException as e:
+                self.error = e
+                return 1
+
+        self.a2a_calls = 0
         self._cb = _capi.ALLREDUCE_FN(_hook)
-        self.comm = _capi.GsComm(self._cb, None)
+        self._cb_a2a = _capi.ALLTOALLV_FN(_a2a)
+        self.comm = _capi.GsComm(self._cb, None, self._cb_a2a)
 
     def __call__(self, buf_ptr: int, count: int, op: int, stream: int = 0) -> int:
-        """Invoke the hook directly (used by host-side tests)."""
+        """Invoke the allreduce hook directly (used by host-side tests)."""
         return self._cb(None, buf_ptr, count, op, stream)
+
+    def alltoallv(self, send_ptr: int, send_bytes, recv_ptr: int, recv_bytes, stream: int = 0) -> int:
+        """Invoke the alltoallv hook directly (used by host-side tests)."""
+        k = len(send_bytes)
+        sb = (C.c_int64 * k)(*send_bytes)
+        rb = (C.c_int64 * k)(*recv_bytes)
+        return self._cb_a2a(None, send_ptr, sb, recv_ptr, rb, k, stream)
+
+
+TorchAllreduce = TorchComm  # earlier name (allreduce-only hook)
+
+
+def _host_bytes(ptr: int, count: int) -> np.ndarray:
+    if count == 0:
+        return np.zeros(0, np.uint8)
+    return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(count,))
+
+
+def partitioned_sinkhorn(filter: HeatFilter, mus, nus, a, params: SinkhornParams = SinkhornParams(),
+                         group=None, **kw):
+    """geodesic_sinkhorn_batch with the graph's rows split over the ranks of `group` (one halo
+    exchange per Chebyshev step). Every rank passes the full inputs and gets (partition, results)
+    where results[p].v / .w hold the rows listed by partition.vertices."""
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    part = RowPartition(filter, world, rank)
+    vid = part.vertices
+    take = lambda d: (d.weights if isinstance(d, Distribution) else _f64(d))[vid]
+    hook = TorchComm(group, device_buffers=True)
+    try:
+        res = part.sinkhorn([take(m) for m in mus], [take(v) for v in nus], _f64(a)[vid], params,
+                            comm=hook.comm, **kw)
+    except Exception:
+        if hook.error is not None:
+            raise hook.error
+        raise
+    return part, res
 
 
 def sharded_sinkhorn_barycenter(filter: HeatFilter, family: DistributionFamily, a,

@@ -580,6 +580,95 @@ def geodesic_sinkhorn_batch(filter: HeatFilter, mus: List[Distribution], nus: Li
     return _sinkhorn(filter, mus, nus, a, params, flags)
 
 
+# ------------------------------------------------------------------------------ row partitions
+class RowPartition:
+    """One rank's rows of a filter for row-partitioned multi-GPU runs (gs_part_*; SURVEY.md
+    §8(e)). The reference is single-process; this splits HeatFilter::apply (heat.cpp:116-131) and
+    sinkhorn_many (transport.cpp:144-239) by rows. Local vectors are indexed like `vertices`
+    (original vertex ids of this part's rows); `comm` is a gs_comm (distributed.TorchComm.comm)
+    and may be None only for a single part."""
+
+    def __init__(self, filter: HeatFilter, nparts: int, part: int, ctx: Optional[Context] = None):
+        self.filter = filter
+        self._ctx = ctx if ctx is not None else filter._ctx
+        self.nparts, self.part = int(nparts), int(part)
+        h = C.c_void_p()
+        self._ctx.check(self._ctx.lib.gs_part_create(self._ctx.handle, filter._h, self.nparts,
+                                                     self.part, C.byref(h)))
+        self._h = h
+        rb, re_, nh, ns = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        nnz = C.c_int64()
+        self._ctx.check(self._ctx.lib.gs_part_info(h, C.byref(rb), C.byref(re_), C.byref(nh),
+                                                   C.byref(nnz), C.byref(ns)))
+        self.row_begin, self.row_end = rb.value, re_.value
+        self.n_local = self.row_end - self.row_begin
+        self.n_halo, self.n_send, self.nnz_local = nh.value, ns.value, nnz.value
+        self.send_counts = np.zeros(self.nparts, np.int64)
+        self.recv_counts = np.zeros(self.nparts, np.int64)
+        self._ctx.check(self._ctx.lib.gs_part_counts(h, _ptr(self.send_counts),
+                                                     _ptr(self.recv_counts)))
+        self.vertices = np.empty(self.n_local, np.int32)
+        self._ctx.check(self._ctx.lib.gs_part_vertices(self._ctx.handle, h, _ptr(self.vertices),
+                                                       _capi.GS_MEM_HOST))
+
+    def _comm(self, comm):
+        return C.byref(comm) if comm is not None else None
+
+    def apply(self, f_local, comm=None, fp32: bool = False) -> np.ndarray:
+        """H f on this part's rows: (n_local,) or (n_local, B) local signals."""
+        x = _f64(f_local)
+        if x.shape[0] != self.n_local:
+            raise Error(errc.length_mismatch, "LengthMismatch: signal length")
+        cols = _f64(x.reshape(self.n_local, -1).T)
+        out = np.empty_like(cols)
+        self._ctx.check(self._ctx.lib.gs_part_filter_apply(
+            self._ctx.handle, self._h, self._comm(comm), _ptr(cols), _ptr(out), cols.shape[0],
+            _capi.GS_FLAG_FP32 if fp32 else 0, _capi.GS_MEM_HOST))
+        return out.T.reshape(x.shape).copy()
+
+    def sinkhorn(self, mus_local, nus_local, a_local, params: SinkhornParams = SinkhornParams(),
+                 comm=None, no_stagnation_abort: bool = False, fp32: bool = False,
+                 single: bool = False) -> List[TransportResult]:
+        """geodesic_sinkhorn_batch on local rows; v, w of each result are local rows, the scalars
+        (cost, kl, iterations, converged, marginal_error) are global and equal on every rank."""
+        nl = self.n_local
+        if len(mus_local) != len(nus_local):
+            raise Error(errc.size_mismatch, "SizeMismatch: pair lists differ in length")
+        P = len(mus_local)
+        if P == 0:
+            return []
+        M = _stack(mus_local, nl)
+        N = _stack(nus_local, nl)
+        a = _f64(a_local)
+        if a.size != nl:
+            raise Error(errc.length_mismatch,
+                        "LengthMismatch: vertex weights must live on the filter's graph")
+        flags = (_capi.GS_FLAG_NO_STAGNATION_ABORT if no_stagnation_abort else 0) | \
+                (_capi.GS_FLAG_FP32 if fp32 else 0) | (_capi.GS_FLAG_SINGLE if single else 0)
+        v = np.empty((P, nl))
+        w = np.empty((P, nl))
+        cost = np.empty(P)
+        kl = np.empty(P)
+        it = np.empty(P, np.int32)
+        conv = np.empty(P, np.int32)
+        err = np.empty(P)
+        fp, fs = C.c_int(), C.c_int()
+        self._ctx.check(self._ctx.lib.gs_part_sinkhorn(
+            self._ctx.handle, self._h, self._comm(comm), _ptr(a), _ptr(M), _ptr(N), P,
+            int(params.max_iter), float(params.tol), flags, _capi.GS_MEM_HOST, _ptr(v), _ptr(w),
+            _ptr(cost), _ptr(kl), _ptr(it), _ptr(conv), _ptr(err), C.byref(fp), C.byref(fs)))
+        lam = 4.0 * self.filter.time()
+        return [TransportResult(v[p].copy(), w[p].copy(), float(cost[p]), float(kl[p]), lam,
+                                int(it[p]), bool(conv[p]), float(err[p])) for p in range(P)]
+
+    def __del__(self):
+        try:
+            if self._h:
+                self._ctx.lib.gs_part_destroy(self._h)
+        except Exception:
+            pass
+
+
 # ---------------------------------------------------------------------------------- barycenter
 @dataclass
 class DistributionFamily:

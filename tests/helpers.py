@@ -88,3 +88,46 @@ def rel(a, b):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-300)))
+
+
+def partition_plan(offs, cols, vals, order, nparts):
+    """numpy restatement of the row-partition rules of gs_part.cu: vertices renumbered by
+    `order` (order[new] = old), nnz-balanced contiguous ranges, halo rows sorted by position
+    (hence by owner), send rows per destination ascending, local CSR with entries kept in the
+    original order and columns renumbered to [0, nl) local / nl + halo index."""
+    offs, cols, vals = np.asarray(offs), np.asarray(cols), np.asarray(vals)
+    order = np.asarray(order)
+    n = order.size
+    newpos = np.empty(n, np.int64)
+    newpos[order] = np.arange(n)
+    poffs = np.concatenate([[0], np.cumsum(np.diff(offs)[order])])
+    nnz = int(poffs[-1])
+    bounds = [0] + [int(np.searchsorted(poffs, nnz * p // nparts, side="left"))
+                    for p in range(1, nparts)] + [n]
+    owner = np.searchsorted(np.array(bounds), np.arange(n), side="right") - 1
+    parts = []
+    for p in range(nparts):
+        rb, re = bounds[p], bounds[p + 1]
+        halo, sends = set(), [set() for _ in range(nparts)]
+        for r in range(rb, re):
+            o = order[r]
+            for c in newpos[cols[offs[o]:offs[o + 1]]]:
+                if not rb <= c < re:
+                    halo.add(int(c))
+                    sends[owner[c]].add(r - rb)
+        halo = np.array(sorted(halo), np.int64)
+        hidx = {int(c): i for i, c in enumerate(halo)}
+        lo_offs, lo_cols, lo_vals = [0], [], []
+        for r in range(rb, re):
+            o = order[r]
+            for c, v in zip(newpos[cols[offs[o]:offs[o + 1]]], vals[offs[o]:offs[o + 1]]):
+                lo_cols.append(c - rb if rb <= c < re else (re - rb) + hidx[int(c)])
+                lo_vals.append(v)
+            lo_offs.append(len(lo_cols))
+        recv = np.bincount(owner[halo], minlength=nparts) if halo.size else np.zeros(nparts, int)
+        parts.append(dict(rb=rb, re=re, vertices=order[rb:re], nh=int(halo.size), halo=halo,
+                          recv=recv, send_rows=[np.array(sorted(s), np.int64) for s in sends],
+                          send=np.array([len(s) for s in sends]),
+                          offs=np.array(lo_offs), cols=np.array(lo_cols, np.int64),
+                          vals=np.array(lo_vals)))
+    return parts

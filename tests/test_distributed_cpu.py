@@ -9,7 +9,7 @@ import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2211_00805_b200.distributed import TorchAllreduce, member_shard
+from paper_2211_00805_b200.distributed import TorchAllreduce, member_shard  # noqa: F401
 
 
 def _free_port():
@@ -122,3 +122,79 @@ def test_sharded_barycenter_gloo_world2():
         assert rel <= 1e-12, res
         assert it == it_ref and conv == conv_ref
         assert calls == 2 + 2 * it
+
+
+def _part_worker(rank, world, port, q):
+    """Row-partitioned Chebyshev apply (heat.cpp:116-131 split by rows) on the
+    partition plan of tests/helpers.py, with the halo exchange through TorchComm.alltoallv
+    (gloo, host buffers): the rows must match the oracle's unpartitioned apply."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        for p in (root, os.path.join(root, "oracle"), os.path.join(root, "tests")):
+            sys.path.insert(0, p)
+        import pyoracle as po
+        import scipy.sparse as sp
+        from helpers import partition_plan, random_connected_graph
+        from paper_2211_00805_b200.distributed import TorchComm
+
+        n, B = 90, 2
+        r, c, v = random_connected_graph(n, 13)
+        L, lam, _ = po.laplacian(po.from_triplets(n, r, c, v), 0)
+        fo = po.Filter(L, 0, lam, 1.0, 30)
+        Ls = fo.scaled
+        order = np.random.default_rng(3).permutation(n).astype(np.int32)  # any locality order
+        plan = partition_plan(Ls.offs, Ls.cols, Ls.vals, order, world)[rank]
+        nl, nh = plan["re"] - plan["rb"], plan["nh"]
+        Lloc = sp.csr_matrix((plan["vals"], plan["cols"], plan["offs"]), shape=(nl, nl + nh))
+        hook = TorchComm(device_buffers=False)
+
+        def exchange(T):  # fill the halo rows of T (nl + nh rows) from their owners
+            send = np.ascontiguousarray(np.concatenate([T[rows] for rows in plan["send_rows"]]))
+            recv = np.empty((nh, B))
+            sb = [len(rows) * B * 8 for rows in plan["send_rows"]]
+            rb = [int(k) * B * 8 for k in plan["recv"]]
+            assert hook.alltoallv(send.ctypes.data, sb, recv.ctypes.data, rb) == 0
+            T[nl:] = recv
+
+        X = np.random.default_rng(5).standard_normal((n, B))
+        b, K = fo.coeffs, fo.degree
+        T0 = np.zeros((nl + nh, B))
+        T0[:nl] = X[plan["vertices"]]
+        exchange(T0)
+        T1 = np.zeros_like(T0)
+        T1[:nl] = Lloc @ T0 - T0[:nl]
+        acc = 0.5 * b[0] * T0[:nl] + b[1] * T1[:nl]
+        Tm2, Tm1 = T0, T1
+        for k in range(2, K + 1):
+            exchange(Tm1)
+            Tk = np.zeros_like(T0)
+            Tk[:nl] = 2.0 * (Lloc @ Tm1 - Tm1[:nl]) - Tm2[:nl]
+            acc = acc + b[k] * Tk[:nl]
+            Tm2, Tm1 = Tm1, Tk
+        ref = fo.apply(X)[plan["vertices"]]
+        q.put((rank, float(np.abs(acc - ref).max() / np.abs(ref).max()), hook.a2a_calls, nh))
+    except BaseException as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_partitioned_apply_gloo_world2():
+    world = 2
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_part_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for res in out:
+        assert len(res) == 4, res
+        rank, err, calls, nh = res
+        assert err <= 1e-12, res
+        assert calls == 30 and nh > 0
