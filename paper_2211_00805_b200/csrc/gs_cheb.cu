@@ -578,6 +578,27 @@ struct Work {
   }
 };
 
+// Deferred-accumulation schedule (StepArgs::acc_terms): step k holds the own rows T_{k-2},
+// T_{k-1}, T_k, so acc may lag by up to two steps; it is brought up to date whenever waiting one
+// more step would leave a pending term out of reach, and at the last step. K = 30 updates acc at
+// steps 2, 5, ..., 29, 30 instead of every step.
+struct AccSchedule {
+  int last = 0;       // highest T index already in acc
+  bool init = false;  // acc holds (b_0 / 2) T_0 + ...
+  void step(const gs_filter* f, int K, int k, StepArgs& A) {
+    const bool must = k == K || (!init && k >= 2) || (init && last < k - 2);
+    A.acc_terms = must ? k - last : 0;
+    A.acc_init = must && !init;
+    A.store_t = k < K;
+    A.bk1 = k >= 1 ? f->coeffs[k - 1] : 0.0;
+    A.bk2 = k >= 2 ? f->coeffs[k - 2] : 0.0;
+    if (must) {
+      last = k;
+      init = true;
+    }
+  }
+};
+
 template <typename S>
 const void* layout_vals(const gs_layout& L) {
   if constexpr (sizeof(S) == 4) return L.vals32;
@@ -614,9 +635,11 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
   A.M = M;
   A.Vcur = Vcur;
   A.Wout = Wout;
+  AccSchedule sched;
   for (int k = 1; k <= K; ++k) {
     A.k = k;
     A.bk = f->coeffs[k];
+    sched.step(f, K, k, A);
     A.Tprev = w.T[(a0 + k - 1) & 1].get();
     A.Tout = w.T[(a0 + k) & 1].get();
     launch_step<S>(ctx, w.GW, w.rpc, A, k == K ? mode : MODE_NONE);
@@ -1301,9 +1324,11 @@ int run_apply_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& 
   A.M = M;
   A.Vcur = Vcur;
   A.Wout = Wout;
+  AccSchedule sched;
   for (int k = 1; k <= K; ++k) {
     A.k = k;
     A.bk = f->coeffs[k];
+    sched.step(f, K, k, A);
     A.Tprev = w.T[(a0 + k - 1) & 1].get();
     A.Tout = w.T[(a0 + k) & 1].get();
     GS_TRY(halo_exchange<S>(ctx, p, comm, w, w.T[(a0 + k - 1) & 1].get(), h));

@@ -214,6 +214,13 @@ struct StepArgs {  // vector pointers are S* of the launch's precision
   void* acc;
   double bk, b0h;
   int k;              // 0 = plain SpMM into Tout
+  // deferred accumulation: acc += b_j T_j is applied for up to three steps at once (the own rows
+  // T_{k-2}, T_{k-1}, T_k are all at hand in step k), oldest term first -- the same fma chain
+  // as one update per step, with a third of the acc traffic (host schedule: acc_schedule)
+  int acc_terms;      // 0 = defer; 1..3 = add b_{k-j+1..k} T_{k-j+1..k}
+  int acc_init;       // 1 = no acc yet: start from (b_0 / 2) T_0 (T_0 = own row of T_{k-1} or T_{k-2})
+  int store_t;        // 0 = T_k is never read again (last step)
+  double bk1, bk2;    // b_{k-1}, b_{k-2}
   const gs_status* status;
   ColState cs;
   const void* a;      // n (epilogue)
@@ -364,6 +371,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
     return;
   }
   // ---- own-row operands (prefetched into shared memory by cp.async when `pre`) ---------------
+  const bool read_acc = A.acc_terms > 0 && !A.acc_init;
   S tp[VEC], t2[VEC], a0[VEC];
   if (pre) {
 #pragma unroll
@@ -374,31 +382,32 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
     }
   } else {
     ld_vec<S, VEC>(static_cast<const S*>(A.Tprev) + idx, tp);
-    if (A.k >= 2) {
-      ld_vec_rw<S, VEC>(static_cast<const S*>(A.Tout) + idx, t2);
-      ld_vec_rw<S, VEC>(static_cast<const S*>(A.acc) + idx, a0);
-    }
+    if (A.k >= 2) ld_vec_rw<S, VEC>(static_cast<const S*>(A.Tout) + idx, t2);
+    if (read_acc) ld_vec_rw<S, VEC>(static_cast<const S*>(A.acc) + idx, a0);
   }
   // ---- recurrence (heat.cpp:121-130) ----------------------------------------------------------
-  const S bk = S(A.bk);
   S t[VEC], ac[VEC];
   if (A.k == 1) {
-    const S b0h = S(A.b0h);
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      t[e] = y[e] - tp[e];
-      ac[e] = P::fmat(bk, t[e], b0h * tp[e]);
-    }
+    for (int e = 0; e < VEC; ++e) t[e] = y[e] - tp[e];
   } else {
 #pragma unroll
+    for (int e = 0; e < VEC; ++e) t[e] = S(2) * (y[e] - tp[e]) - t2[e];
+  }
+  // acc = fma(b_k, T_k, acc) for the pending steps, oldest first (heat.cpp:122,129)
+  if (A.acc_terms > 0) {
+    const S bk = S(A.bk), bk1 = S(A.bk1), bk2 = S(A.bk2), b0h = S(A.b0h);
+#pragma unroll
     for (int e = 0; e < VEC; ++e) {
-      t[e] = S(2) * (y[e] - tp[e]) - t2[e];
-      ac[e] = P::fmat(bk, t[e], a0[e]);
+      S base = A.acc_init ? b0h * (A.k == 1 ? tp[e] : t2[e]) : a0[e];
+      if (A.acc_terms >= 3) base = P::fmat(bk2, t2[e], base);
+      if (A.acc_terms >= 2) base = P::fmat(bk1, tp[e], base);
+      ac[e] = P::fmat(bk, t[e], base);
     }
   }
   if constexpr (MODE == MODE_NONE) {
-    st_vec<S, VEC>(static_cast<S*>(A.Tout) + idx, t);
-    st_vec<S, VEC>(static_cast<S*>(A.acc) + idx, ac);
+    if (A.store_t) st_vec<S, VEC>(static_cast<S*>(A.Tout) + idx, t);
+    if (A.acc_terms > 0) st_vec<S, VEC>(static_cast<S*>(A.acc) + idx, ac);
   } else {
     // ---- fused epilogue of the last step --------------------------------------------------
     const int* act = A.cs.active;
@@ -478,8 +487,12 @@ __device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int til
 // A CTA owns RPC x (8 warps x rows-per-warp) consecutive rows of one column group. Own-row
 // operands of the next row block (T_{k-1}[i], T_{k-2}[i], acc[i]) are copied to shared memory with
 // cp.async while this block's neighbour gathers run (16-byte vector rows only).
+// resident CTAs per SM the register allocation must allow (0 = compiler's choice)
+#ifndef GS_MIN_BLOCKS
+#define GS_MIN_BLOCKS 5
+#endif
 template <typename S, int GW, int MODE, int RPC>
-__global__ void __launch_bounds__(kThreads) k_cheb_step(const StepArgs A) {
+__global__ void __launch_bounds__(kThreads, MODE == MODE_NONE ? GS_MIN_BLOCKS : 0) k_cheb_step(const StepArgs A) {
   using L = Lay<GW, S>;
   constexpr int VEC = L::VEC, LPR = L::LPR, RPW = L::RPW;
   constexpr int BLOCK_ROWS = (kThreads / 32) * RPW;
@@ -509,10 +522,8 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step(const StepArgs A) {
         const size_t idx = gbase + (size_t)row * GW;
         S* d = &s_pre[j % STG][0][threadIdx.x * VEC];
         cp_async16(d, static_cast<const S*>(A.Tprev) + idx);
-        if (A.k >= 2) {
-          cp_async16(d + PS, static_cast<const S*>(A.Tout) + idx);
-          cp_async16(d + 2 * PS, static_cast<const S*>(A.acc) + idx);
-        }
+        if (A.k >= 2) cp_async16(d + PS, static_cast<const S*>(A.Tout) + idx);
+        if (A.acc_terms > 0 && !A.acc_init) cp_async16(d + 2 * PS, static_cast<const S*>(A.acc) + idx);
       }
       cp_async_commit();
     };
