@@ -851,10 +851,13 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
     k_sk_control<<<1, 1, 0, s>>>(C);
     gs_launch_end(ctx, 1);
   };
-  // Small problems are launch-latency bound: capture two sweeps (odd, even parity) once as a CUDA
-  // graph and replay it; kernels of sweeps past convergence / max_iter exit immediately.
+  // Two sweeps (odd, even parity) are captured once as a CUDA graph and replayed: one host launch
+  // per two sweeps instead of ~126, so the GPU never waits on the host's launch path (small
+  // problems are launch-latency bound; on config 1 per-kernel launches left 11-25% of the GPU idle
+  // under host-side stalls). Kernels of sweeps past convergence / max_iter exit immediately.
+  // GS_GRAPH=0 selects per-kernel launches.
   const char* genv = getenv("GS_GRAPH");
-  const bool use_graph = genv ? genv[0] == '1' : ((size_t)n * w.Bpad <= ((size_t)1 << 20));
+  const bool use_graph = genv ? genv[0] != '0' : true;
   cudaGraphExec_t gexec = nullptr;
   int64_t graph_launches = 0;
   if (use_graph && max_iter >= 2) {
