@@ -505,11 +505,13 @@ def run_engine_bary(args):
     conv = np.zeros(1, np.int32)
     err = np.zeros(1)
     hook = TorchAllreduce(None, device_buffers=True)
+    # one rank has nothing to reduce: without the hook the engine replays sweeps as a CUDA graph
+    comm_arg = C.byref(hook.comm) if world > 1 else None
 
     def step():
         rc = lib.gs_barycenter_ex(ctx.handle, filt._h, a.data_ptr(), Mloc.data_ptr(), hi - lo,
                                   al.data_ptr(), args.sweeps, TOL_RUN_ALL, _capi.GS_MEM_DEVICE,
-                                  C.byref(hook.comm), 0, bary.data_ptr(), Vo.data_ptr(),
+                                  comm_arg, 0, bary.data_ptr(), Vo.data_ptr(),
                                   Wo.data_ptr(), it.ctypes.data, conv.ctypes.data, err.ctypes.data)
         if hook.error is not None:
             raise hook.error
@@ -547,6 +549,36 @@ def run_engine_bary(args):
     B = hi - lo
     bytes_step = algorithmic_bytes_per_step(n, nnz_L, B)
     avg = step_ms / max(step_n, 1)
+
+    # ---- e2e through the C ABI with host buffers (members, alphas, a in; bary, V, W out) ---------
+    Mh = torch.from_numpy(np.ascontiguousarray(cfg.members[lo:hi])).pin_memory()
+    alh = torch.full((hi - lo,), 1.0 / m, dtype=torch.float64).pin_memory()
+    ah = torch.full((n,), 1.0 / n, dtype=torch.float64).pin_memory()
+    bh = torch.empty(n, dtype=torch.float64).pin_memory()
+    Vh = torch.empty((hi - lo, n), dtype=torch.float64).pin_memory()
+    Wh = torch.empty_like(Vh).pin_memory()
+
+    def step_host():
+        rc = lib.gs_barycenter_ex(ctx.handle, filt._h, ah.data_ptr(), Mh.data_ptr(), hi - lo,
+                                  alh.data_ptr(), args.sweeps, TOL_RUN_ALL, _capi.GS_MEM_HOST,
+                                  comm_arg, 0, bh.data_ptr(), Vh.data_ptr(),
+                                  Wh.data_ptr(), it.ctypes.data, conv.ctypes.data, err.ctypes.data)
+        if hook.error is not None:
+            raise hook.error
+        ctx.check(rc)
+
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        step_host()
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    dist.barrier()
+    e2e = {"value": args.sweeps * e2e_steps / e2e_s, "unit": "barycenter sweeps/s",
+           "h2d_bytes_per_step": (hi - lo) * n * 8 + (hi - lo) * 8 + n * 8,
+           "d2h_bytes_per_step": n * 8 + 2 * (hi - lo) * n * 8 + 4 + 4 + 8, "steps": e2e_steps}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -571,12 +603,13 @@ def run_engine_bary(args):
                        "nnz_L": int(nnz_L), "lambda_max_bound": lap.lambda_max_bound,
                        "lambda_rounds": lap.power_rounds, "graph_build_s": t_graph,
                        "members_per_rank": B, "allreduce_calls": hook.calls,
-                       "parallelism": f"member sharding x{world}, NCCL allreduce per sweep"},
+                       "parallelism": f"member sharding x{world}, NCCL allreduce per sweep" if world > 1
+                       else "one rank: no collective, sweeps replayed as a CUDA graph"},
             "roofline": {"bound": "hbm", "achieved": bytes_step / (avg / 1000.0) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": bytes_step / (avg / 1000.0) / 1e9 / peak,
                          "traffic": None, "peak_kind": peak_kind, "bytes_per_launch": bytes_step,
                          "avg_launch_ms": avg, "launches_timed": step_n},
-            "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": cpu,
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": cpu,
             "iterations": int(it[0]), "marginal_error": float(err[0]),
         }), flush=True)
     dist.destroy_process_group()

@@ -398,8 +398,9 @@ __global__ void k_bary_errlocal(const double* errcol, int m, double* errbuf) {
   *errbuf = e;
 }
 
-__global__ void k_bary_control(const double* errbuf, gs_status* st, int sweep, double tol,
+__global__ void k_bary_control(const double* errbuf, gs_status* st, int* sweep_ctr, double tol,
                                int* iters, int* conv, double* err_out, int max_iter) {
+  const int sweep = ++(*sweep_ctr);  // device counter: a captured sweep can be replayed
   if (st->error || st->done) return;
   const double err = *errbuf;
   *err_out = err;
@@ -1029,14 +1030,14 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   cudaEvent_t ev[2];
   cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
+  DevBuf<int> sweep_ctr;
+  GS_CUDA(ctx, sweep_ctr.alloc(1, s));
+  GS_CUDA(ctx, cudaMemsetAsync(sweep_ctr.get(), 0, sizeof(int), s));
+  const bool hooked = comm && comm->allreduce;
   int hook_rc = 0;
-  for (int sweep = 1; sweep <= max_iter; ++sweep) {
-    if (sweep >= 3) {
-      const int slot = (sweep - 2) & 1;
-      cudaEventSynchronize(ev[slot]);
-      const gs_status st = hst[slot];
-      if (st.error || st.done) break;
-    }
+  // one sweep (barycenter.cpp:70-86); `parity` selects the V ping-pong buffers. Kernels of sweeps
+  // past convergence / max_iter exit on the status word (or recompute unchanged values).
+  auto issue_sweep = [&](int parity) -> int {
     // psi = H(a * V) (barycenter.cpp:71)
     a0 = run_apply<S>(ctx, f, w, a0, MODE_BARY_PSI, da, nullptr, nullptr, nullptr, false, true);
     run_finalize<S>(ctx, w, 1, 0, 0, knp, false);
@@ -1044,11 +1045,11 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
     gs_launch_begin(ctx, 1);
     k_bary_lb<S><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(w.acc.get(), dal.get(), n, m, w.GW, lb.get(), w.status.get());
     gs_launch_end(ctx, 1);
-    if (comm && comm->allreduce) {
-      hook_rc = comm->allreduce(comm->user, lb.get(), n, 0, (void*)s);
-      if (hook_rc) break;
+    if (hooked) {
+      const int rc = comm->allreduce(comm->user, lb.get(), n, 0, (void*)s);
+      if (rc) return rc;
     }
-    GS_CUDA(ctx, cudaMemsetAsync(lbmax.get(), 0, sizeof(unsigned long long), s));
+    cudaMemsetAsync(lbmax.get(), 0, sizeof(unsigned long long), s);
     gs_launch_begin(ctx, 1);
     k_max_key<<<grid_for(n), kThreads, 0, s>>>(lb.get(), n, lbmax.get());
     gs_launch_end(ctx, 1);
@@ -1069,24 +1070,70 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
     gs_launch_end(ctx, 1);
     run_finalize<S>(ctx, w, 0, 1, 0, knp, false);
     // phi = H(a * W); err; V' = M / max(phi, floor) (barycenter.cpp:85-86, 70)
-    a0 = run_apply<S>(ctx, f, w, a0, MODE_SK_PHI, da, Mb.get(), V[sweep & 1].get(),
-                      V[(sweep + 1) & 1].get(), false, true);
+    a0 = run_apply<S>(ctx, f, w, a0, MODE_SK_PHI, da, Mb.get(), V[parity].get(), V[parity ^ 1].get(),
+                      false, true);
     run_finalize<S>(ctx, w, 1, 1, 1, knp, false);
     gs_launch_begin(ctx, 1);
     k_bary_errlocal<<<1, 1, 0, s>>>(w.errcol.get(), m, errbuf.get());
     gs_launch_end(ctx, 1);
-    if (comm && comm->allreduce) {
-      hook_rc = comm->allreduce(comm->user, errbuf.get(), 1, 1, (void*)s);
-      if (hook_rc) break;
+    if (hooked) {
+      const int rc = comm->allreduce(comm->user, errbuf.get(), 1, 1, (void*)s);
+      if (rc) return rc;
     }
     gs_launch_begin(ctx, 1);
-    k_bary_control<<<1, 1, 0, s>>>(errbuf.get(), w.status.get(), sweep, tol, diters.get(),
+    k_bary_control<<<1, 1, 0, s>>>(errbuf.get(), w.status.get(), sweep_ctr.get(), tol, diters.get(),
                                    dconv.get(), derr.get(), max_iter);
     gs_launch_end(ctx, 1);
-    const int slot = sweep & 1;
+    return 0;
+  };
+  // Without collective hooks, two sweeps (odd, even parity) are captured once as a CUDA graph and
+  // replayed (as in sinkhorn_impl); hooks call back into the host every sweep, so no capture.
+  cudaGraphExec_t gexec = nullptr;
+  int64_t graph_launches = 0;
+  const char* genv = getenv("GS_GRAPH");
+  if (!hooked && (genv ? genv[0] != '0' : true) && max_iter >= 2) {
+    cudaGraph_t graph = nullptr;
+    const int64_t l0 = ctx->launches;
+    const int a0_saved = a0;
+    ctx->capturing = true;
+    cudaError_t ce = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    if (ce == cudaSuccess) {
+      issue_sweep(1);
+      issue_sweep(0);
+      ce = cudaStreamEndCapture(s, &graph);
+    }
+    ctx->capturing = false;
+    graph_launches = ctx->launches - l0;
+    ctx->launches = l0;
+    if (ce == cudaSuccess) ce = cudaGraphInstantiate(&gexec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) {
+      cudaGetLastError();
+      gexec = nullptr;
+    }
+    a0 = a0_saved;  // two sweeps = 4 applies of K steps: the buffer parity returns to a0 (K even)
+    if (gexec && ((4 * f->degree) & 1)) a0 ^= 1;
+  }
+  const int step_sweeps = gexec ? 2 : 1;
+  for (int sweep = 1, it = 0; sweep <= max_iter; sweep += step_sweeps, ++it) {
+    if (it >= 2) {
+      const int slot = (it - 2) & 1;
+      cudaEventSynchronize(ev[slot]);
+      const gs_status st = hst[slot];
+      if (st.error || st.done) break;
+    }
+    if (gexec) {
+      GS_CUDA(ctx, cudaGraphLaunch(gexec, s));
+      ctx->launches += graph_launches;
+    } else {
+      hook_rc = issue_sweep(sweep & 1);
+      if (hook_rc) break;
+    }
+    const int slot = it & 1;
     cudaMemcpyAsync(&hst[slot], w.status.get(), sizeof(gs_status), cudaMemcpyDeviceToHost, s);
     cudaEventRecord(ev[slot], s);
   }
+  if (gexec) cudaGraphExecDestroy(gexec);
   GS_CUDA(ctx, cudaStreamSynchronize(s));
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
