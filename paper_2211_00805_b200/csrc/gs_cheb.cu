@@ -368,27 +368,47 @@ __global__ void k_bary_mass_check(const double* mass, gs_status* st) {
   if (!(*mass > 0.0)) st->error = 1000 + ERRC_KERNEL_NOT_POSITIVE + 1;  // "collapsed" variant
 }
 
-// bary /= mass; W_c = bary / max(psi_c, floor); T_0 = a * W_c; colmax |T_0|
+constexpr int kBaryColChunk = 2048;  // columns per shared-memory max pass of k_bary_w
+
+// bary /= mass; W_c = bary / max(psi_c, floor); T_0 = a * W_c; colmax |T_0| (order-free max:
+// warp shuffle, one shared-memory atomic per warp, one global atomic per CTA and column)
 template <typename S>
 __global__ void k_bary_w(double* __restrict__ bary, const double* __restrict__ mass,
                          const S* __restrict__ psi, const S* __restrict__ a, int n, int m, int GW,
                          S* __restrict__ W, S* __restrict__ T0, unsigned long long* cmax,
                          const gs_status* st) {
-  if (st->error || st->done) return;
+  __shared__ unsigned long long s_max[kBaryColChunk];
+  if (st->error || st->done) return;  // the same status word for the whole grid
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool ok = i < n;
   const double ms = *mass;
-  if (i < n) {
-    const double b = bary[i] / ms;
+  double b = 0.0, ai = 0.0;
+  if (ok) {
+    b = bary[i] / ms;
     bary[i] = b;
-    const double ai = a[i];
-    for (int c = 0; c < m; ++c) {
-      const size_t idx = ((size_t)(c / GW) * n + i) * GW + (c % GW);
-      const double w = b / fmax((double)psi[idx], (double)Prec<S>::floor);
-      W[idx] = S(w);
-      const S t0 = S(ai * w);
-      T0[idx] = t0;
-      atomicMax(cmax + c, dkey(fabs((double)t0)));
+    ai = a[i];
+  }
+  for (int c0 = 0; c0 < m; c0 += kBaryColChunk) {
+    const int cn = min(kBaryColChunk, m - c0);
+    for (int c = threadIdx.x; c < cn; c += blockDim.x) s_max[c] = KEY_ZERO;
+    __syncthreads();
+    for (int c = c0; c < c0 + cn; ++c) {
+      double v = 0.0;
+      if (ok) {
+        const size_t idx = ((size_t)(c / GW) * n + i) * GW + (c % GW);
+        const double w = b / fmax((double)psi[idx], (double)Prec<S>::floor);
+        W[idx] = S(w);
+        const S t0 = S(ai * w);
+        T0[idx] = t0;
+        v = fabs((double)t0);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if ((threadIdx.x & 31) == 0) atomicMax(&s_max[c - c0], dkey(v));
     }
+    __syncthreads();
+    for (int c = threadIdx.x; c < cn; c += blockDim.x) atomicMax(cmax + c0 + c, s_max[c]);
+    __syncthreads();
   }
 }
 
