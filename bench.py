@@ -616,6 +616,193 @@ def run_engine_bary(args):
     return 0
 
 
+# --------------------------------------------------------------------------- config 3 (row partitions)
+def run_engine_rows(args):
+    """Config 3: n = 2e7 swiss roll, k = 10 Gaussian-median graph (grid kNN), combinatorial L,
+    t = 1, K = 30, fp32, one pair (config 0's bumps at 2 pi / 4 pi), 100 sweeps. Rows are
+    partitioned over the ranks (gs_part_*: contiguous nnz-balanced ranges of the CM order, one halo
+    exchange per Chebyshev step through NCCL all_to_all_single, allreduced column reductions);
+    strong scaling, value = sweeps/s. One rank runs the unpartitioned path (the same rows, sweeps
+    replayed as CUDA graphs)."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_00805_b200 as gs
+    from paper_2211_00805_b200 import _capi, workloads
+    from paper_2211_00805_b200.distributed import TorchComm
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        with _StdoutToStderr():
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+    ctx = gs.Context(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    lib = ctx.lib
+    n = args.n
+    t0 = time.perf_counter()
+    roll = workloads.swiss_roll(n, 1)
+    A, sigma = gs.knn_gaussian_graph(roll.points, 10, ctx=ctx)
+    lap = gs.laplacian(A, gs.LaplacianKind.combinatorial)
+    filt = gs.HeatFilter(lap, 1.0, 30)
+    setup_s = time.perf_counter() - t0
+    mu = workloads.bump_in_s(roll, 2 * math.pi, 0.5)
+    nu = workloads.bump_in_s(roll, 4 * math.pi, 0.5)
+    a = np.full(n, 1.0 / n)
+    flags = _capi.GS_FLAG_NO_STAGNATION_ABORT | _capi.GS_FLAG_FP32
+    dev = torch.device("cuda", local)
+    hook = None
+    comm = None
+    part = None
+    if world > 1:
+        part = gs.RowPartition(filt, world, rank, ctx=ctx)
+        vid = part.vertices.astype(np.int64)
+        hook = TorchComm(None, device_buffers=True)
+        comm = C.byref(hook.comm)
+        nnz_loc = part.nnz_local
+    else:
+        vid = np.arange(n)
+        nnz_loc = lap.matrix.stored_entries()
+    nl = vid.size
+    Md = torch.from_numpy(mu[vid].copy()).to(dev)
+    Nd = torch.from_numpy(nu[vid].copy()).to(dev)
+    ad = torch.from_numpy(a[vid].copy()).to(dev)
+    vd = torch.empty(nl, dtype=torch.float64, device=dev)
+    wd = torch.empty_like(vd)
+    cost, kl, err = np.empty(1), np.empty(1), np.empty(1)
+    it, conv = np.empty(1, np.int32), np.empty(1, np.int32)
+    fp, fs = C.c_int(), C.c_int()
+
+    dsc = torch.empty(3, dtype=torch.float64, device=dev)  # cost, kl, err (device-mode outputs)
+    dsi = torch.empty(2, dtype=torch.int32, device=dev)    # iterations, converged
+
+    def run(mem, M, N, av, v, w):
+        if mem == _capi.GS_MEM_DEVICE:
+            p0, pi = dsc.data_ptr(), dsi.data_ptr()
+            small = (p0, p0 + 8, pi, pi + 4, p0 + 16)
+        else:
+            small = (cost.ctypes.data, kl.ctypes.data, it.ctypes.data, conv.ctypes.data,
+                     err.ctypes.data)
+        outs = (v, w, *small, C.byref(fp), C.byref(fs))
+        if part is None:
+            rc = lib.gs_sinkhorn(ctx.handle, filt._h, av, M, N, 1, args.sweeps, TOL_RUN_ALL, flags,
+                                 mem, *outs)
+        else:
+            rc = lib.gs_part_sinkhorn(ctx.handle, part._h, comm, av, M, N, 1, args.sweeps,
+                                      TOL_RUN_ALL, flags, mem, *outs)
+        if hook is not None and hook.error is not None:
+            raise hook.error
+        ctx.check(rc)
+
+    def step():
+        run(_capi.GS_MEM_DEVICE, Md.data_ptr(), Nd.data_ptr(), ad.data_ptr(), vd.data_ptr(),
+            wd.data_ptr())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    ctx.set_timing(True, period=args.timing_period)
+    l0 = ctx.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    step_n, step_ms = ctx.timing(0)
+    ctx.set_timing(False)
+    launches = ctx.launch_count() - l0
+    elapsed = max_over_ranks(e0.elapsed_time(e1))
+    value = args.sweeps * args.steps / (elapsed / 1000.0)
+    peak, peak_kind = peaks()
+    bytes_step = algorithmic_bytes_per_step(nl, nnz_loc, 1, sv=4)
+    avg = step_ms / max(step_n, 1)
+    # ---- e2e through the C ABI with host buffers ------------------------------------------------
+    Mh = torch.from_numpy(mu[vid].copy()).pin_memory()
+    Nh = torch.from_numpy(nu[vid].copy()).pin_memory()
+    ah = torch.from_numpy(a[vid].copy()).pin_memory()
+    vh = torch.empty(nl, dtype=torch.float64).pin_memory()
+    wh = torch.empty_like(vh).pin_memory()
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    torch.cuda.synchronize()
+    barrier()
+    t1 = time.perf_counter()
+    for _ in range(e2e_steps):
+        run(_capi.GS_MEM_HOST, Mh.data_ptr(), Nh.data_ptr(), ah.data_ptr(), vh.data_ptr(), wh.data_ptr())
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t1)
+    barrier()
+    e2e = {"value": args.sweeps * e2e_steps / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": 3 * nl * 8, "d2h_bytes_per_step": 2 * nl * 8 + 8 + 8 + 4 + 4 + 8,
+           "steps": e2e_steps}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:  # bounded sample: one K = 30 fp64 apply (half a sweep) of the oracle on this graph
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import pyoracle as po
+            L = lap.matrix
+            Lo = po.CSR(n, L.row_offsets().copy(), L.col_indices().copy(), L.values().copy())
+            fo = po.Filter(Lo, 0, lap.lambda_max_bound, 1.0, 30)
+            x = mu.copy()
+            t2 = time.perf_counter()
+            fo.apply(x)
+            dt = time.perf_counter() - t2
+            cpu = {"value": 0.5 / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"one K=30 fp64 apply (half a sweep) of the oracle on the GPU-built "
+                             f"n={n} graph, OpenMP ({dt:.1f} s)"}
+        except Exception as e:  # host memory / time limits: report why
+            cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"not run: {type(e).__name__}"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"config3: swiss roll n={n}, k=10 Gaussian-median graph (grid "
+                                   f"kNN), combinatorial L, t=1, K=30, fp32, 1 pair, "
+                                   f"{args.sweeps} sweeps, rows partitioned over {world} rank(s)",
+                       "nnz_L": int(lap.matrix.stored_entries()), "rows_local": int(nl),
+                       "nnz_local": int(nnz_loc),
+                       "halo_rows": int(part.n_halo) if part is not None else 0,
+                       "setup_s": setup_s, "sigma": sigma, "lambda_max_bound": lap.lambda_max_bound,
+                       "stagnation_abort": "disabled (bench-only, DESIGN.md)",
+                       "l2": "working set > 2 GB >> 126 MB L2; no flush needed between steps",
+                       "parallelism": (f"row partitions x{world}, halo all_to_all per step"
+                                       if world > 1 else "one rank: unpartitioned rows, CUDA-graph sweeps")},
+            "roofline": {"bound": "hbm", "achieved": bytes_step / (avg / 1000.0) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": bytes_step / (avg / 1000.0) / 1e9 / peak,
+                         "traffic": None, "peak_kind": peak_kind, "bytes_per_launch": bytes_step,
+                         "avg_launch_ms": avg, "launches_timed": step_n},
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": cpu,
+            "iterations": int(it[0]), "marginal_error": float(err[0]),
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def _free_port():
     import socket
     s_ = socket.socket()
@@ -639,7 +826,7 @@ def main():
     ap.add_argument("--ref-sweeps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2])
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3])
     ap.add_argument("--members", type=int, default=8)
     ap.add_argument("--timing-period", type=int, default=8,
                     help="event-time every Nth engine launch inside the timed region")
@@ -659,6 +846,16 @@ def main():
                               "O(n^2 d) CPU kNN at n=1e6; use the default config"}))
             return 0
         return run_engine_bary(args)
+    if args.config == 3:
+        if args.n == 200_000:
+            args.n = 20_000_000
+        if args.sweeps == 200:
+            args.sweeps = 100
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "config 3 reference arm needs an "
+                              "O(n^2) CPU kNN at n=2e7; use the default config"}))
+            return 0
+        return run_engine_rows(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_engine(args)

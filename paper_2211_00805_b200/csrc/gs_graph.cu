@@ -144,6 +144,173 @@ void launch_knn_k(const double* pts, const double* sq, int n, int d, int k, int*
   }
 }
 
+// ---- exact kNN on a uniform grid for low-dimensional clouds (d <= 3) --------------------------
+// Same distance arithmetic as k_knn and the same (d2, index) order -- candidates are compared
+// lexicographically, so the visiting order does not matter and the result equals the brute-force
+// selection bit for bit (select_knn, graph.cpp:30-71). Cells are visited in cube shells of growing
+// Chebyshev radius R around the query's cell; the search stops once the k-th candidate is closer
+// than R cell widths (with a rounding slack for the Gram-form distance), or the grid is exhausted.
+struct Grid {
+  double lo[3], inv_h, h;
+  int dim[3];
+  int d;
+};
+
+__device__ __forceinline__ int grid_coord(const Grid& G, double x, int q) {
+  int c = (int)floor((x - G.lo[q]) * G.inv_h);
+  return c < 0 ? 0 : (c >= G.dim[q] ? G.dim[q] - 1 : c);
+}
+
+__device__ __forceinline__ long long grid_cell(const Grid& G, const double* x) {
+  long long id = 0;
+  for (int q = G.d - 1; q >= 0; --q) id = id * G.dim[q] + grid_coord(G, x[q], q);
+  return id;
+}
+
+__global__ void k_grid_count(const double* __restrict__ pts, int n, Grid G, int* __restrict__ cell,
+                             int* __restrict__ counts) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = (int)grid_cell(G, pts + (size_t)i * G.d);
+  cell[i] = c;
+  atomicAdd(counts + c, 1);
+}
+
+__global__ void k_grid_fill(const int* __restrict__ cell, int n, int* __restrict__ cursor,
+                            int* __restrict__ items) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) items[atomicAdd(cursor + cell[i], 1)] = i;
+}
+
+template <int KMAX>
+__global__ void __launch_bounds__(128) k_knn_grid(const double* __restrict__ pts,
+                                                  const double* __restrict__ sq, int n, Grid G,
+                                                  const int* __restrict__ start,
+                                                  const int* __restrict__ items, double max_sq, int k,
+                                                  int* __restrict__ nbrs, double* __restrict__ eps) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int qi = items[t];  // queries in cell order: neighbouring threads search the same cells
+  const int d = G.d;
+  double xq[3] = {0.0, 0.0, 0.0};
+  for (int q = 0; q < d; ++q) xq[q] = pts[(size_t)qi * d + q];
+  const double sqq = sq[qi];
+  int cq[3] = {0, 0, 0};
+  for (int q = 0; q < d; ++q) cq[q] = grid_coord(G, xq[q], q);
+  double bd[KMAX];
+  int bi[KMAX];
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s) {
+    bd[s] = INFINITY;
+    bi[s] = 0x7fffffff;
+  }
+  // Gram-form d2 differs from the exact squared distance by a few ulps of |xq|^2 + |xj|^2
+  const double slack = 1e-9 * (sqq + max_sq) + 1e-300;
+  const int rmax = max(G.dim[0], max(d > 1 ? G.dim[1] : 1, d > 2 ? G.dim[2] : 1));
+  for (int R = 0; R <= rmax; ++R) {
+    const int lo0 = cq[0] - R, hi0 = cq[0] + R;
+    const int lo1 = d > 1 ? cq[1] - R : 0, hi1 = d > 1 ? cq[1] + R : 0;
+    const int lo2 = d > 2 ? cq[2] - R : 0, hi2 = d > 2 ? cq[2] + R : 0;
+    for (int c2 = lo2; c2 <= hi2; ++c2) {
+      if (d > 2 && (c2 < 0 || c2 >= G.dim[2])) continue;
+      for (int c1 = lo1; c1 <= hi1; ++c1) {
+        if (d > 1 && (c1 < 0 || c1 >= G.dim[1])) continue;
+        const bool inner12 = (d < 3 || (c2 > lo2 && c2 < hi2)) && (d < 2 || (c1 > lo1 && c1 < hi1));
+        // on the shell: interior (c1, c2) rows only contribute their two end cells
+        for (int c0 = lo0; c0 <= hi0; c0 += (inner12 && R > 0) ? (hi0 - lo0) : 1) {
+          if (c0 < 0 || c0 >= G.dim[0]) {
+            if (inner12 && R > 0 && c0 == hi0) break;
+            continue;
+          }
+          const long long cell = ((long long)c2 * (d > 1 ? G.dim[1] : 1) + c1) * G.dim[0] + c0;
+          for (int e = start[cell]; e < start[cell + 1]; ++e) {
+            const int j = items[e];
+            if (j == qi) continue;
+            const double* xj = pts + (size_t)j * d;
+            double g = 0.0;
+            for (int q = 0; q < d; ++q) g = fma(xq[q], xj[q], g);
+            double d2 = (sqq + sq[j]) - 2.0 * g;
+            if (!(d2 > 0.0)) d2 = 0.0;
+            double wd = bd[0];
+            int wi = bi[0];
+#pragma unroll
+            for (int s = 0; s < KMAX; ++s)
+              if (s == k - 1) {
+                wd = bd[s];
+                wi = bi[s];
+              }
+            if (!(d2 < wd || (d2 == wd && j < wi))) continue;
+#pragma unroll
+            for (int s = KMAX - 1; s > 0; --s) {
+              if (s < k) {
+                if (bd[s - 1] > d2 || (bd[s - 1] == d2 && bi[s - 1] > j)) {
+                  bd[s] = bd[s - 1];
+                  bi[s] = bi[s - 1];
+                } else if (bd[s] > d2 || (bd[s] == d2 && bi[s] > j)) {
+                  bd[s] = d2;
+                  bi[s] = j;
+                }
+              }
+            }
+            if (bd[0] > d2 || (bd[0] == d2 && bi[0] > j)) {
+              bd[0] = d2;
+              bi[0] = j;
+            }
+          }
+          if (inner12 && R > 0 && c0 == hi0) break;
+        }
+      }
+    }
+    // every point outside the searched cube is at least R cell widths away
+    double wd = bd[0];
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s)
+      if (s == k - 1) wd = bd[s];
+    const double reach = (double)R * G.h;
+    if (wd + slack < reach * reach) break;
+  }
+  int last = 0;
+#pragma unroll
+  for (int s = 0; s < KMAX; ++s) {
+    if (s < k) nbrs[(size_t)qi * k + s] = bi[s];
+    if (s == k - 1) last = bi[s];
+  }
+  double s2 = 0.0;
+  for (int q = 0; q < d; ++q) {
+    const double diff = xq[q] - pts[(size_t)last * d + q];
+    s2 = fma(diff, diff, s2);
+  }
+  eps[qi] = sqrt(s2);
+}
+
+__global__ void k_bbox(const double* __restrict__ pts, int n, int d, double* __restrict__ out /* 2*d */) {
+  __shared__ double smin[3][256], smax[3][256];
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    for (int q = 0; q < d; ++q) {
+      mn[q] = fmin(mn[q], pts[(size_t)i * d + q]);
+      mx[q] = fmax(mx[q], pts[(size_t)i * d + q]);
+    }
+  for (int q = 0; q < 3; ++q) {
+    smin[q][threadIdx.x] = mn[q];
+    smax[q][threadIdx.x] = mx[q];
+  }
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int q = 0; q < 3; ++q) {
+        smin[q][threadIdx.x] = fmin(smin[q][threadIdx.x], smin[q][threadIdx.x + s]);
+        smax[q][threadIdx.x] = fmax(smax[q][threadIdx.x], smax[q][threadIdx.x + s]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int q = 0; q < d; ++q) {
+      out[2 * (blockIdx.x * 3 + q)] = smin[q][0];
+      out[2 * (blockIdx.x * 3 + q) + 1] = smax[q][0];
+    }
+}
+
 __global__ void k_eps_check(const double* eps, int n, int* first_bad) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && !(eps[i] > 0.0)) atomicMin(first_bad, i);
@@ -608,6 +775,98 @@ extern "C" int gs_laplacian(gs_ctx* ctx, const gs_graph* A, int kind, gs_graph**
 }
 
 // ---- kNN -----------------------------------------------------------------------------------
+// Grid search for d <= 3 (GS_KNN=brute forces the tiled brute force, GS_KNN=grid the grid).
+static bool use_grid_knn(int n, int d) {
+  const char* e = getenv("GS_KNN");
+  if (e && e[0] == 'b') return false;
+  if (e && e[0] == 'g') return d <= 3;
+  return d <= 3 && n >= 32768;
+}
+
+static int knn_grid(gs_ctx* ctx, const double* dpts, const double* sq, int n, int d, int k, int* dnb,
+                    double* deps) {
+  cudaStream_t s = ctx->stream;
+  const int nb = 148 * 4;
+  DevBuf<double> part;
+  GS_CUDA(ctx, part.alloc((size_t)nb * 6, s));
+  gs_launch_begin(ctx, 1);
+  k_bbox<<<nb, 256, 0, s>>>(dpts, n, d, part.get());
+  gs_launch_end(ctx, 1);
+  std::vector<double> hp((size_t)nb * 6);
+  GS_CUDA(ctx, cudaMemcpyAsync(hp.data(), part.get(), hp.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  double max_sq = 0.0;
+  {
+    DevBuf<double> dmax;  // largest squared norm (for the rounding slack)
+    GS_CUDA(ctx, dmax.alloc(1, s));
+    std::vector<double> hsq(n);
+    GS_CUDA(ctx, cudaMemcpyAsync(hsq.data(), sq, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    GS_CUDA(ctx, cudaStreamSynchronize(s));
+    for (double v : hsq) max_sq = std::max(max_sq, v);
+  }
+  Grid G{};
+  G.d = d;
+  double ext[3] = {0.0, 0.0, 0.0};
+  for (int q = 0; q < d; ++q) {
+    double lo = INFINITY, hi = -INFINITY;
+    for (int b = 0; b < nb; ++b) {
+      lo = std::min(lo, hp[2 * (b * 3 + q)]);
+      hi = std::max(hi, hp[2 * (b * 3 + q) + 1]);
+    }
+    G.lo[q] = lo;
+    ext[q] = hi - lo;
+  }
+  // cell width: about 4 points per cell if they filled the bounding box (surfaces get more)
+  double vol = 1.0;
+  int used = 0;
+  for (int q = 0; q < d; ++q)
+    if (ext[q] > 0.0) {
+      vol *= ext[q];
+      ++used;
+    }
+  double h = used ? std::pow(vol * 4.0 / n, 1.0 / used) : 1.0;
+  if (!(h > 0.0) || !std::isfinite(h)) h = 1.0;
+  long long cells = 1;
+  for (;;) {
+    cells = 1;
+    for (int q = 0; q < d; ++q) {
+      G.dim[q] = (int)std::min<double>(ext[q] / h + 1.0, 1 << 20);
+      cells *= G.dim[q];
+    }
+    if (cells <= (long long)4 * n + 64) break;
+    h *= 1.25;
+  }
+  for (int q = d; q < 3; ++q) G.dim[q] = 1;
+  G.h = h;
+  G.inv_h = 1.0 / h;
+  DevBuf<int> cell, counts, start, items;
+  GS_CUDA(ctx, cell.alloc(n, s));
+  GS_CUDA(ctx, counts.alloc((size_t)cells + 1, s));
+  GS_CUDA(ctx, start.alloc((size_t)cells + 1, s));
+  GS_CUDA(ctx, items.alloc(n, s));
+  GS_CUDA(ctx, cudaMemsetAsync(counts.get(), 0, ((size_t)cells + 1) * sizeof(int), s));
+  gs_launch_begin(ctx, 1);
+  k_grid_count<<<nblk(n), kThreads, 0, s>>>(dpts, n, G, cell.get(), counts.get());
+  gs_launch_end(ctx, 1);
+  size_t tb = 0;
+  GS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tb, counts.get(), start.get(), (int)cells + 1, s));
+  DevBuf<unsigned char> tmp;
+  GS_CUDA(ctx, tmp.alloc(tb, s));
+  GS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp.get(), tb, counts.get(), start.get(), (int)cells + 1, s));
+  GS_CUDA(ctx, cudaMemcpyAsync(counts.get(), start.get(), ((size_t)cells + 1) * sizeof(int), cudaMemcpyDeviceToDevice, s));
+  gs_launch_begin(ctx, 1);
+  k_grid_fill<<<nblk(n), kThreads, 0, s>>>(cell.get(), n, counts.get(), items.get());
+  gs_launch_end(ctx, 1);
+  gs_launch_begin(ctx, 1);
+  if (k <= 16)
+    k_knn_grid<16><<<(n + 127) / 128, 128, 0, s>>>(dpts, sq, n, G, start.get(), items.get(), max_sq, k, dnb, deps);
+  else
+    k_knn_grid<32><<<(n + 127) / 128, 128, 0, s>>>(dpts, sq, n, G, start.get(), items.get(), max_sq, k, dnb, deps);
+  gs_launch_end(ctx, 1);
+  GS_CUDA(ctx, cudaGetLastError());
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  return GS_OK;
+}
+
 static int knn_device(gs_ctx* ctx, const double* dpts, int n, int d, int k, int* dnb, double* deps) {
   cudaStream_t s = ctx->stream;
   DevBuf<double> sq;
@@ -615,6 +874,7 @@ static int knn_device(gs_ctx* ctx, const double* dpts, int n, int d, int k, int*
   gs_launch_begin(ctx, 1);
   k_sqnorms<<<nblk(n), kThreads, 0, s>>>(dpts, n, d, sq.get());
   gs_launch_end(ctx, 1);
+  if (use_grid_knn(n, d)) return knn_grid(ctx, dpts, sq.get(), n, d, k, dnb, deps);
   gs_launch_begin(ctx, 1);
   if (k <= 16) launch_knn_k<16>(dpts, sq.get(), n, d, k, dnb, deps, s);
   else launch_knn_k<32>(dpts, sq.get(), n, d, k, dnb, deps, s);
