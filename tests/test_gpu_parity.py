@@ -112,6 +112,51 @@ def test_filter_apply_bit_exact(gs, kind, width):
     assert np.array_equal(f.apply(X), fo.apply(X))
 
 
+@pytest.mark.parametrize("deg", [1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("width", [1, 8, 64])
+def test_filter_apply_small_degree_bit_exact(gs, deg, width):
+    """The step kernel defers acc updates (three steps at most, the last step always): every
+    schedule boundary for K = 1..8, on the scalar, narrow and one-warp-per-row layouts."""
+    n = 300
+    r, c, v = acceptance_graph(n, 77 + deg)
+    f, _ = engine_filter(r, c, v, n, 0, 0.7, deg)
+    fo = oracle_filter(r, c, v, n, 0, 0.7, deg)
+    X = np.random.default_rng(deg).standard_normal((n, width))
+    if width == 1:
+        X = X[:, 0]
+    assert np.array_equal(f.apply(X), fo.apply(X))
+
+
+@pytest.mark.parametrize("deg", [1, 2, 3, 4, 7])
+def test_sinkhorn_small_degree_matches_oracle(gs, deg):
+    """Fused last-step epilogues at the schedule boundaries: same outcome as the oracle (results
+    bit for bit, or the same KernelNotPositive when a short expansion goes negative)."""
+    n = 90
+    r, c, v = acceptance_graph(n, 5 + deg)
+    f, _ = engine_filter(r, c, v, n, 1, 0.5, deg)
+    fo = oracle_filter(r, c, v, n, 1, 0.5, deg)
+    mus, nus = _pairs(n, 3, 40 + deg)
+    a = np.full(n, 1.0 / n)
+    try:
+        res = gs.geodesic_sinkhorn_batch(f, [gs.Distribution(m) for m in mus],
+                                         [gs.Distribution(x) for x in nus], a, gs.SinkhornParams(60, 1e-10))
+        err = None
+    except gs.Error as e:
+        res, err = None, e.code
+    try:
+        ref = po.sinkhorn_batch(fo, a, np.array(mus), np.array(nus), 60, 1e-10)
+        ref_status = 0
+    except po.OracleError as e:
+        ref, ref_status = None, e.status
+    if err is not None:
+        assert ref_status == int(err) + 1
+        return
+    assert ref_status == 0
+    for p, q in enumerate(res):
+        assert np.array_equal(q.v, ref["v"][p]) and np.array_equal(q.w, ref["w"][p])
+        assert q.iterations == ref["iterations"][p]
+
+
 def test_two_vertex_closed_form(gs):
     """test_heat.cpp:135-150."""
     f, _ = engine_filter(np.array([0], np.int32), np.array([1], np.int32), np.array([1.0]), 2, 0,
