@@ -40,7 +40,11 @@ constexpr int kRowsPerCta = GS_ROWS_PER_CTA;
 #ifndef GS_GATHER_BATCH
 #define GS_GATHER_BATCH 4
 #endif
-constexpr int kGatherBatch = GS_GATHER_BATCH;  // neighbour rows in flight per lane (wide rows)
+constexpr int kGatherBatch = GS_GATHER_BATCH;  // neighbour rows in flight per lane (wide fp64 rows)
+#ifndef GS_GATHER_BATCH32
+#define GS_GATHER_BATCH32 3
+#endif
+constexpr int kGatherBatch32 = GS_GATHER_BATCH32;  // wide fp32 rows (fewer registers -> 6 CTAs/SM)
 #ifndef GS_NARROW_GATHER_BATCH
 #define GS_NARROW_GATHER_BATCH 8
 #endif
@@ -91,7 +95,7 @@ struct Lay {
   static constexpr int ROWS = (kThreads / 32) * RPW;   // rows per CTA block
   // gathers in flight per row: narrow rows have few registers per gather, so go deeper
   static constexpr int GB = NARROW ? (GS_NARROW_GATHER_BATCH < LPR ? GS_NARROW_GATHER_BATCH : LPR)
-                                   : kGatherBatch;
+                                   : (sizeof(S) == 4 ? kGatherBatch32 : kGatherBatch);
 };
 
 // order-preserving uint64 keys for doubles (atomic min/max of signed values)
@@ -487,12 +491,16 @@ __device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int til
 // A CTA owns RPC x (8 warps x rows-per-warp) consecutive rows of one column group. Own-row
 // operands of the next row block (T_{k-1}[i], T_{k-2}[i], acc[i]) are copied to shared memory with
 // cp.async while this block's neighbour gathers run (16-byte vector rows only).
-// resident CTAs per SM the register allocation must allow (0 = compiler's choice)
+// resident CTAs per SM the register allocation of the plain step must allow (0 = compiler's choice)
 #ifndef GS_MIN_BLOCKS
 #define GS_MIN_BLOCKS 5
 #endif
+#ifndef GS_MIN_BLOCKS32
+#define GS_MIN_BLOCKS32 6
+#endif
 template <typename S, int GW, int MODE, int RPC>
-__global__ void __launch_bounds__(kThreads, MODE == MODE_NONE ? GS_MIN_BLOCKS : 0) k_cheb_step(const StepArgs A) {
+__global__ void __launch_bounds__(kThreads, MODE != MODE_NONE ? 0 : (sizeof(S) == 4 ? GS_MIN_BLOCKS32 : GS_MIN_BLOCKS))
+    k_cheb_step(const StepArgs A) {
   using L = Lay<GW, S>;
   constexpr int VEC = L::VEC, LPR = L::LPR, RPW = L::RPW;
   constexpr int BLOCK_ROWS = (kThreads / 32) * RPW;
