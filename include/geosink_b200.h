@@ -165,6 +165,8 @@ int gs_part_create(gs_ctx* ctx, const gs_filter* f, int nparts, int part, gs_par
 void gs_part_destroy(gs_part* p);
 int gs_part_info(const gs_part* p, int* row_begin, int* row_end, int* n_halo, int64_t* nnz_local,
                  int* n_send);
+/* local rows [lo, hi) read no halo row: computed while the exchange is in flight */
+int gs_part_interior(const gs_part* p, int* lo, int* hi);
 /* rows sent to / received from each rank per exchange (nparts entries each, optional) */
 int gs_part_counts(const gs_part* p, int64_t* send_counts, int64_t* recv_counts);
 int gs_part_vertices(gs_ctx* ctx, const gs_part* p, int* out, int mem);

@@ -83,6 +83,7 @@ SIGNATURES = {
     "gs_part_destroy": (None, [_vp]),
     "gs_part_info": (_i, [_vp, _pi, _pi, _pi, _pi64, _pi]),
     "gs_part_counts": (_i, [_vp, _vp, _vp]),
+    "gs_part_interior": (_i, [_vp, _pi, _pi]),
     "gs_part_vertices": (_i, [_vp, _vp, _vp, _i]),
     "gs_part_filter_apply": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _i]),
     "gs_part_sinkhorn": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _d, _i, _i, _vp, _vp, _vp,

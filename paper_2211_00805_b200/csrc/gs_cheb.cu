@@ -1345,17 +1345,70 @@ struct Halo {
   }
 };
 
+// Row ranges of one partitioned step: the interior rows (no halo reads) run while the halo is in
+// flight; the two boundary ranges after it has landed. One range when the part is alone.
+struct PartRanges {
+  int lo[3], hi[3], tile0[3], tiles[3], count, total;
+};
+
+inline PartRanges part_ranges(const gs_part* p, int rows_per_tile) {
+  PartRanges R{};
+  auto add = [&](int lo, int hi) {
+    const int c = R.count++;
+    R.lo[c] = lo;
+    R.hi[c] = hi;
+    R.tile0[c] = R.total;
+    R.tiles[c] = hi > lo ? (hi - lo + rows_per_tile - 1) / rows_per_tile : 0;
+    R.total += R.tiles[c];
+  };
+  if (p->nparts == 1) {
+    add(0, p->nl);
+  } else {
+    add(p->int_lo, p->int_hi);  // [0]: interior
+    add(0, p->int_lo);          // [1], [2]: boundary prefix and suffix
+    add(p->int_hi, p->nl);
+  }
+  return R;
+}
+
 template <typename S>
-int halo_exchange(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const Work<S>& w, S* T, Halo<S>& h) {
-  if (p->nparts == 1) return GS_OK;
+int part_tiles(const gs_part* p, const Work<S>& w) {
+  return part_ranges(p, rows_per_block<S>(w.GW) * w.rpc).total;
+}
+
+// pack the rows other parts read, then hand them to comm->alltoallv on the context's comm stream
+// (after the pack); the caller launches the interior rows meanwhile and calls halo_finish
+template <typename S>
+int halo_start(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const Work<S>& w, const S* T, Halo<S>& h) {
   cudaStream_t s = ctx->stream;
+  if (!ctx->comm_stream) {
+    GS_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    GS_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_packed, cudaEventDisableTiming));
+    GS_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_received, cudaEventDisableTiming));
+  }
   if (p->ns > 0) {
     gs_launch_begin(ctx, 1);
     k_halo_pack<S><<<grid_for((int64_t)p->ns * w.Bpad), kThreads, 0, s>>>(T, w.ld, w.GW, w.Bpad, p->send_rows, p->ns, h.send.get());
     gs_launch_end(ctx, 1);
   }
-  if (comm->alltoallv(comm->user, h.send.get(), h.sb.data(), h.recv.get(), h.rb.data(), p->nparts, (void*)s))
+  GS_CUDA(ctx, cudaEventRecord(ctx->ev_packed, s));
+  GS_CUDA(ctx, cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
+  return GS_OK;
+}
+
+template <typename S>
+int halo_exchange(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Halo<S>& h) {
+  if (comm->alltoallv(comm->user, h.send.get(), h.sb.data(), h.recv.get(), h.rb.data(), p->nparts,
+                      (void*)ctx->comm_stream))
     return hook_fail(ctx, "alltoallv");
+  GS_CUDA(ctx, cudaEventRecord(ctx->ev_received, ctx->comm_stream));
+  return GS_OK;
+}
+
+template <typename S>
+int halo_finish(gs_ctx* ctx, const gs_part* p, const Work<S>& w, S* T, Halo<S>& h) {
+  cudaStream_t s = ctx->stream;
+  GS_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_received, 0));
   if (p->nh > 0) {
     gs_launch_begin(ctx, 1);
     k_halo_unpack<S><<<grid_for((int64_t)p->nh * w.Bpad), kThreads, 0, s>>>(h.recv.get(), p->nh, p->nl, w.ld, w.GW, w.Bpad, T);
@@ -1394,15 +1447,35 @@ int run_apply_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& 
   A.M = M;
   A.Vcur = Vcur;
   A.Wout = Wout;
+  const PartRanges R = part_ranges(p, rows_per_block<S>(w.GW) * w.rpc);
+  auto launch_range = [&](int r, int m) {
+    if (R.tiles[r] == 0) return;
+    A.row0 = R.lo[r];
+    A.n = R.hi[r];
+    A.tiles = R.tiles[r];
+    A.tile0 = R.tile0[r];
+    launch_step<S>(ctx, w.GW, w.rpc, A, m);
+  };
   AccSchedule sched;
   for (int k = 1; k <= K; ++k) {
     A.k = k;
     A.bk = f->coeffs[k];
     sched.step(f, K, k, A);
-    A.Tprev = w.T[(a0 + k - 1) & 1].get();
+    S* Tprev = w.T[(a0 + k - 1) & 1].get();
+    A.Tprev = Tprev;
     A.Tout = w.T[(a0 + k) & 1].get();
-    GS_TRY(halo_exchange<S>(ctx, p, comm, w, w.T[(a0 + k - 1) & 1].get(), h));
-    if (w.tiles > 0) launch_step<S>(ctx, w.GW, w.rpc, A, k == K ? mode : MODE_NONE);
+    const int m = k == K ? mode : MODE_NONE;
+    if (p->nparts == 1) {
+      launch_range(0, m);
+      continue;
+    }
+    // T_{k-1}'s boundary rows go out while the interior rows (no halo reads) are computed
+    GS_TRY(halo_start<S>(ctx, p, comm, w, Tprev, h));
+    launch_range(0, m);
+    GS_TRY(halo_exchange<S>(ctx, p, comm, h));
+    GS_TRY(halo_finish<S>(ctx, p, w, Tprev, h));
+    launch_range(1, m);
+    launch_range(2, m);
   }
   *next = (a0 + K) & 1;
   return GS_OK;
@@ -1441,6 +1514,7 @@ int filter_apply_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, c
   cudaStream_t s = ctx->stream;
   Work<S> w;
   GS_TRY(w.init(ctx, nl, width, false, (int64_t)nl + p->nh));
+  w.tiles = part_tiles<S>(p, w);
   Halo<S> h;
   GS_TRY(h.init(ctx, p, w.Bpad));
   if (nl > 0) {
@@ -1469,6 +1543,8 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
   cudaStream_t s = ctx->stream;
   Work<S> w;
   GS_TRY(w.init(ctx, nl, P, true, (int64_t)nl + p->nh));
+  w.tiles = part_tiles<S>(p, w);  // error partials: one per tile of the (up to) three row ranges
+  GS_CUDA(ctx, w.part_err.alloc((size_t)(w.tiles ? w.tiles : 1) * w.Bpad, s));
   Halo<S> h;
   GS_TRY(h.init(ctx, p, w.Bpad));
   DevBuf<double> stat;

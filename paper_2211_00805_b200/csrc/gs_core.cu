@@ -68,6 +68,9 @@ extern "C" void gs_ctx_destroy(gs_ctx* ctx) {
     cudaEventDestroy(p.b);
   }
   if (ctx->h_status) cudaFreeHost(ctx->h_status);
+  if (ctx->ev_packed) cudaEventDestroy(ctx->ev_packed);
+  if (ctx->ev_received) cudaEventDestroy(ctx->ev_received);
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   delete ctx;
 }

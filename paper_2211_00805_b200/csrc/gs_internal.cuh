@@ -51,6 +51,9 @@ struct gs_ctx {
   gs_status* h_status = nullptr;
   // CUDA-graph capture in progress: launches are counted, not timed
   bool capturing = false;
+  // row-partitioned runs: halo exchanges run on a second stream, overlapped with interior rows
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_packed = nullptr, ev_received = nullptr;
 };
 
 struct gs_graph {
@@ -90,6 +93,7 @@ struct gs_part {
   const gs_filter* f = nullptr;
   int nparts = 1, part = 0;
   int n_global = 0, row_begin = 0, row_end = 0, nl = 0, nh = 0, ns = 0;
+  int int_lo = 0, int_hi = 0;  // local rows [int_lo, int_hi) read no halo row (interior)
   gs_graph* local = nullptr;
   float* vals32 = nullptr;
   int* vertices = nullptr;   // nl: original vertex id of each local row

@@ -97,6 +97,18 @@ __global__ void k_send_keys(const int* __restrict__ offs, const int* __restrict_
   }
 }
 
+// boundary rows (reading a halo row): the largest one in the first half, the smallest in the second
+__global__ void k_boundary_rows(const int* __restrict__ offs, const int* __restrict__ cols, int nl,
+                                int* lo_max, int* hi_min) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nl) return;
+  bool b = false;
+  for (int p = offs[r]; p < offs[r + 1] && !b; ++p) b = cols[p] >= nl;
+  if (!b) return;
+  if (r < nl / 2) atomicMax(lo_max, r);
+  else atomicMin(hi_min, r);
+}
+
 __global__ void k_low32(const unsigned long long* __restrict__ k, int m, int* __restrict__ out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < m) out[i] = (int)(k[i] & 0xFFFFFFFFull);
@@ -193,6 +205,22 @@ int part_build(gs_ctx* ctx, const gs_filter* f, int nparts, int part, gs_part* P
     gs_launch_end(ctx, 1);
     GS_CUDA(ctx, cudaMemcpyAsync(P->local->vals, g->vals + eb, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
   }
+  {  // interior rows: between the last boundary row of the first half and the first of the second
+    DevBuf<int> lh;
+    GS_CUDA(ctx, lh.alloc(2, s));
+    const int init[2] = {-1, nl};
+    GS_CUDA(ctx, cudaMemcpyAsync(lh.get(), init, sizeof init, cudaMemcpyHostToDevice, s));
+    if (nl > 0) {
+      gs_launch_begin(ctx, 1);
+      k_boundary_rows<<<blocks_for(nl), kT, 0, s>>>(P->local->offs, P->local->cols, nl, lh.get(), lh.get() + 1);
+      gs_launch_end(ctx, 1);
+    }
+    int hb[2];
+    GS_CUDA(ctx, cudaMemcpyAsync(hb, lh.get(), sizeof hb, cudaMemcpyDeviceToHost, s));
+    GS_CUDA(ctx, cudaStreamSynchronize(s));
+    P->int_lo = hb[0] + 1;
+    P->int_hi = hb[1] < P->int_lo ? P->int_lo : hb[1];
+  }
   GS_CUDA(ctx, cudaMalloc((void**)&P->vals32, (size_t)(m ? m : 1) * sizeof(float)));
   if (m > 0 && L.vals32) {
     gs_launch_begin(ctx, 1);
@@ -270,6 +298,13 @@ extern "C" int gs_part_info(const gs_part* p, int* row_begin, int* row_end, int*
   if (n_halo) *n_halo = p->nh;
   if (nnz_local) *nnz_local = p->local ? p->local->nnz : 0;
   if (n_send) *n_send = p->ns;
+  return GS_OK;
+}
+
+extern "C" int gs_part_interior(const gs_part* p, int* lo, int* hi) {
+  if (!p) return GS_ERR_UNSUPPORTED;
+  if (lo) *lo = p->int_lo;
+  if (hi) *hi = p->int_hi;
   return GS_OK;
 }
 

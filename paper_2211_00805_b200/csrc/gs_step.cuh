@@ -211,7 +211,8 @@ struct StepArgs {  // vector pointers are S* of the launch's precision
   const int* __restrict__ offs;
   const int* __restrict__ cols;
   const void* vals;
-  int n, tiles, g0, Gl, Bpad;
+  int n, tiles, g0, Gl, Bpad;  // rows [row0, n) in `tiles` CTA tiles per column group
+  int row0, tile0;             // first row; index of the first tile in the error partials
   int64_t ld;         // rows per column group (n, or local + halo rows for a row partition)
   const void* Tprev;  // T_{k-1}
   void* Tout;         // T_{k-2} in, T_k out (or next T_0 / SpMM output)
@@ -506,7 +507,8 @@ __global__ void __launch_bounds__(kThreads, MODE != MODE_NONE ? 0 : (sizeof(S) =
   constexpr int BLOCK_ROWS = (kThreads / 32) * RPW;
   constexpr bool PREFETCH = VEC * sizeof(S) == 16;
   if (A.status && (A.status->error || A.status->done)) return;
-  const int tile = blockIdx.x / A.Gl;
+  const int tl = blockIdx.x / A.Gl;
+  const int tile = A.tile0 + tl;
   const int g = A.g0 + blockIdx.x % A.Gl;
   if (A.cs.gactive && A.cs.gactive[g] == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -518,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, MODE != MODE_NONE ? 0 : (sizeof(S) =
     mx[e] = 0.0;
     er[e] = 0.0;
   }
-  const int base = tile * (BLOCK_ROWS * RPC) + warp * RPW + sub;
+  const int base = A.row0 + tl * (BLOCK_ROWS * RPC) + warp * RPW + sub;
   if constexpr (PREFETCH) {
     constexpr int STG = kPrefetchStages;
     constexpr int PS = kThreads * VEC;  // elements per operand per stage

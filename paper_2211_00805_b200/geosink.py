@@ -607,6 +607,9 @@ class RowPartition:
         self.recv_counts = np.zeros(self.nparts, np.int64)
         self._ctx.check(self._ctx.lib.gs_part_counts(h, _ptr(self.send_counts),
                                                      _ptr(self.recv_counts)))
+        lo, hi = C.c_int(), C.c_int()
+        self._ctx.check(self._ctx.lib.gs_part_interior(h, C.byref(lo), C.byref(hi)))
+        self.interior = (lo.value, hi.value)  # rows computed while the halo is in flight
         self.vertices = np.empty(self.n_local, np.int32)
         self._ctx.check(self._ctx.lib.gs_part_vertices(self._ctx.handle, h, _ptr(self.vertices),
                                                        _capi.GS_MEM_HOST))

@@ -125,7 +125,14 @@ def partition_plan(offs, cols, vals, order, nparts):
                 lo_vals.append(v)
             lo_offs.append(len(lo_cols))
         recv = np.bincount(owner[halo], minlength=nparts) if halo.size else np.zeros(nparts, int)
+        nl = re - rb
+        bnd = [i for i in range(nl) if (np.array(lo_cols[lo_offs[i]:lo_offs[i + 1]]) >= nl).any()]
+        lo_b = [i for i in bnd if i < nl // 2]
+        hi_b = [i for i in bnd if i >= nl // 2]
+        ilo = (max(lo_b) + 1) if lo_b else 0
+        ihi = max(min(hi_b) if hi_b else nl, ilo)
         parts.append(dict(rb=rb, re=re, vertices=order[rb:re], nh=int(halo.size), halo=halo,
+                          interior=(ilo, ihi),
                           recv=recv, send_rows=[np.array(sorted(s), np.int64) for s in sends],
                           send=np.array([len(s) for s in sends]),
                           offs=np.array(lo_offs), cols=np.array(lo_cols, np.int64),

@@ -65,6 +65,9 @@ def test_partition_plan_matches_model(gs, roll_filter, nparts):
         assert np.array_equal(part.recv_counts, m["recv"])
         assert np.array_equal(part.send_counts, m["send"])
         assert part.n_send == part.send_counts.sum()
+        assert part.interior == m["interior"]
+        if nparts > 1 and m["nh"] > 0:  # the overlap path has work on both sides of the exchange
+            assert m["interior"][1] > m["interior"][0]
     # what q receives from p is what p sends to q
     for p in range(nparts):
         for q in range(nparts):
