@@ -520,4 +520,75 @@ inline double barycentric_distance(const HeatFilter& filter, const DistributionF
   return geodesic_sinkhorn(filter, bt.barycenter, bc.barycenter, a, params).cost;
 }
 
+// ---- row partitions (multi-GPU row-partitioned applies) ---------------------
+// One rank's contiguous nnz-balanced rows of a filter. Local vectors are indexed like vertices()
+// (original vertex ids). `comm` carries the caller's collectives (allreduce + alltoallv on the
+// given stream); it may be null only for a single part.
+class RowPartition {
+ public:
+  RowPartition(const HeatFilter& filter, int nparts, int part) : filter_(&filter) {
+    gs_part* p = nullptr;
+    detail::check(gs_part_create(detail::ctx(), filter.handle(), nparts, part, &p));
+    h_ = std::shared_ptr<gs_part>(p, gs_part_destroy);
+    int rb = 0, re = 0;
+    detail::check(gs_part_info(p, &rb, &re, &n_halo_, nullptr, nullptr));
+    vertices_.resize(re - rb);
+    detail::check(gs_part_vertices(detail::ctx(), p, vertices_.data(), GS_MEM_HOST));
+  }
+  int size() const { return static_cast<int>(vertices_.size()); }
+  int halo_rows() const { return n_halo_; }
+  const std::vector<int>& vertices() const { return vertices_; }
+  // heat.cpp:98-114 on the local rows
+  std::vector<double> apply(const std::vector<double>& f_local, const gs_comm* comm = nullptr) const {
+    if ((int)f_local.size() != size()) detail::fail(errc::length_mismatch, "LengthMismatch", "signal length");
+    std::vector<double> y(f_local.size());
+    detail::check(gs_part_filter_apply(detail::ctx(), h_.get(), comm, f_local.data(), y.data(), 1, 0, GS_MEM_HOST));
+    return y;
+  }
+  // geodesic_sinkhorn_batch (transport.cpp:249-255) on the local rows: v, w local; scalars global
+  std::vector<TransportResult> sinkhorn(const std::vector<std::vector<double>>& mus_local,
+                                        const std::vector<std::vector<double>>& nus_local,
+                                        const std::vector<double>& a_local, const SinkhornParams& params = {},
+                                        const gs_comm* comm = nullptr, int flags = 0) const {
+    if (mus_local.size() != nus_local.size())
+      detail::fail(errc::size_mismatch, "SizeMismatch", "pair lists differ in length");
+    const int n = size(), P = static_cast<int>(mus_local.size());
+    if (P == 0) return {};
+    std::vector<double> M(size_t(P) * n), N(M.size()), v(M.size()), w(M.size());
+    for (int q = 0; q < P; ++q) {
+      if ((int)mus_local[q].size() != n || (int)nus_local[q].size() != n)
+        detail::fail(errc::length_mismatch, "LengthMismatch", "distributions must live on the partition");
+      std::copy(mus_local[q].begin(), mus_local[q].end(), M.begin() + size_t(q) * n);
+      std::copy(nus_local[q].begin(), nus_local[q].end(), N.begin() + size_t(q) * n);
+    }
+    if ((int)a_local.size() != n)
+      detail::fail(errc::length_mismatch, "LengthMismatch", "vertex weights must live on the partition");
+    std::vector<double> cost(P), kl(P), err(P);
+    std::vector<int> it(P), conv(P);
+    detail::check(gs_part_sinkhorn(detail::ctx(), h_.get(), comm, a_local.data(), M.data(), N.data(), P,
+                                   params.max_iter, params.tol, flags, GS_MEM_HOST, v.data(), w.data(),
+                                   cost.data(), kl.data(), it.data(), conv.data(), err.data(), nullptr,
+                                   nullptr));
+    std::vector<TransportResult> out(P);
+    for (int q = 0; q < P; ++q) {
+      out[q].v.assign(v.begin() + size_t(q) * n, v.begin() + size_t(q + 1) * n);
+      out[q].w.assign(w.begin() + size_t(q) * n, w.begin() + size_t(q + 1) * n);
+      out[q].cost = cost[q];
+      out[q].kl = kl[q];
+      out[q].lambda = 4.0 * filter_->time();
+      out[q].iterations = it[q];
+      out[q].converged = conv[q] != 0;
+      out[q].marginal_error = err[q];
+    }
+    return out;
+  }
+  gs_part* handle() const { return h_.get(); }
+
+ private:
+  const HeatFilter* filter_;
+  std::shared_ptr<gs_part> h_;
+  int n_halo_ = 0;
+  std::vector<int> vertices_;
+};
+
 }  // namespace geosink

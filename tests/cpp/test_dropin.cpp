@@ -231,6 +231,38 @@ int main() {
     CHECK(back.stored_entries() == lap.matrix.stored_entries() && back.values() == lap.matrix.values());
     CHECK_THROWS_CODE(load_graph("/tmp/does/not/exist.txt"), errc::io_error);
   }
+  // a single row partition reproduces the unpartitioned engine bit for bit (vertex order aside)
+  {
+    Rng rng(6);
+    const auto lap = laplacian(random_connected_graph(64, 21), LaplacianKind::combinatorial);
+    const HeatFilter f(lap, 0.9, 30);
+    const std::vector<double> a(64, 1.0 / 64);
+    const auto mu = random_distribution(64, rng), nu = random_distribution(64, rng);
+    const auto full = geodesic_sinkhorn_batch(f, {mu}, {nu}, a, {300, 1e-9});
+    const RowPartition part(f, 1, 0);
+    CHECK(part.size() == 64 && part.halo_rows() == 0);
+    std::vector<double> ml(64), nl(64), al(64);
+    for (int r = 0; r < 64; ++r) {
+      ml[r] = mu.weights[part.vertices()[r]];
+      nl[r] = nu.weights[part.vertices()[r]];
+      al[r] = a[part.vertices()[r]];
+    }
+    const auto loc = part.sinkhorn({ml}, {nl}, al, {300, 1e-9});
+    bool same = loc[0].iterations == full[0].iterations;
+    for (int r = 0; r < 64; ++r)
+      same = same && loc[0].v[r] == full[0].v[part.vertices()[r]] && loc[0].w[r] == full[0].w[part.vertices()[r]];
+    CHECK(same);
+    std::vector<double> x(64);
+    for (int r = 0; r < 64; ++r) x[r] = rng.normal();
+    const auto yf = f.apply(x);
+    std::vector<double> xl(64);
+    for (int r = 0; r < 64; ++r) xl[r] = x[part.vertices()[r]];
+    const auto yl = part.apply(xl);
+    bool same_apply = true;
+    for (int r = 0; r < 64; ++r) same_apply = same_apply && yl[r] == yf[part.vertices()[r]];
+    CHECK(same_apply);
+    CHECK_THROWS_CODE(RowPartition(f, 2, 5), errc::invalid_argument);
+  }
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail;
 }
