@@ -52,13 +52,6 @@ constexpr int kGatherBatch32 = GS_GATHER_BATCH32;  // wide fp32 rows (fewer regi
 #define GS_PREFETCH_STAGES 2
 #endif
 constexpr int kPrefetchStages = GS_PREFETCH_STAGES;
-#ifndef GS_CHUNK_ENTRIES
-#define GS_CHUNK_ENTRIES 0
-#endif
-constexpr int kChunkEntries = GS_CHUNK_ENTRIES;  // narrow rows: gathers in flight per row (0 = off)
-#ifndef GS_CHUNK_MAX_LPR
-#define GS_CHUNK_MAX_LPR 8
-#endif
 
 enum StepMode { MODE_NONE = 0, MODE_SK_PSI = 1, MODE_SK_PHI = 2, MODE_BARY_PSI = 3 };
 
@@ -154,37 +147,10 @@ __device__ __forceinline__ void st_vec(S* p, const S (&v)[VEC]) {
   }
 }
 
-// streaming loads of the CSR entries (used once per step): keep them out of L1 so the neighbour
-// rows of T_{k-1} stay resident (GS_IDX_NOALLOC)
-#ifndef GS_IDX_NOALLOC
-#define GS_IDX_NOALLOC 0
-#endif
-__device__ __forceinline__ int ld_idx(const int* p) {
-#if GS_IDX_NOALLOC
-  int v;
-  asm volatile("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-#else
+// CSR entry loads (read-only path)
+template <typename T>
+__device__ __forceinline__ T ld_idx(const T* p) {
   return __ldg(p);
-#endif
-}
-__device__ __forceinline__ double ld_idx(const double* p) {
-#if GS_IDX_NOALLOC
-  double v;
-  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
-  return v;
-#else
-  return __ldg(p);
-#endif
-}
-__device__ __forceinline__ float ld_idx(const float* p) {
-#if GS_IDX_NOALLOC
-  float v;
-  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
-  return v;
-#else
-  return __ldg(p);
-#endif
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -280,51 +246,6 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
         ld_vec<S, VEC>(Tp + (size_t)c * GW, x);
 #pragma unroll
         for (int e = 0; e < VEC; ++e) y[e] = P::fmat(v, x[e], y[e]);
-      }
-    }
-  } else if constexpr (LPR <= GS_CHUNK_MAX_LPR && kChunkEntries > 0) {
-    // narrow rows (several rows per warp): each lane holds U = CH/LPR (col, val) entries of its
-    // row; all CH gathers of a chunk are issued before the fma chain consumes them in CSR order,
-    // and the next chunk's entries are loaded meanwhile -- the index latency is off the chain.
-    constexpr int CH = kChunkEntries < LPR ? LPR : kChunkEntries;
-    constexpr int U = CH / LPR;
-    const int sub_lane0 = sub * LPR;
-    const unsigned mask = ((1u << LPR) - 1u) << sub_lane0;
-    const int pb = valid ? __ldg(A.offs + row) : 0;
-    const int pe = valid ? __ldg(A.offs + row + 1) : 0;
-    int pc[U];
-    S pv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int p = pb + u * LPR + q;
-      pc[u] = p < pe ? ld_idx(A.cols + p) : 0;
-      pv[u] = p < pe ? ld_idx(vals + p) : S(0);
-    }
-    for (int p0 = pb; p0 < pe; p0 += CH) {
-      int nc[U];
-      S nv[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int p = p0 + CH + u * LPR + q;
-        nc[u] = p < pe ? ld_idx(A.cols + p) : 0;
-        nv[u] = p < pe ? ld_idx(vals + p) : S(0);
-      }
-      const int cnt = min(CH, pe - p0);
-      S xx[CH][VEC];
-#pragma unroll
-      for (int e = 0; e < CH; ++e)
-        if (e < cnt) ld_vec<S, VEC>(Tp + (size_t)__shfl_sync(mask, pc[e / LPR], e % LPR, LPR) * GW, xx[e]);
-#pragma unroll
-      for (int e = 0; e < CH; ++e)
-        if (e < cnt) {
-          const S v = __shfl_sync(mask, pv[e / LPR], e % LPR, LPR);
-#pragma unroll
-          for (int f = 0; f < VEC; ++f) y[f] = P::fmat(v, xx[e][f], y[f]);
-        }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        pc[u] = nc[u];
-        pv[u] = nv[u];
       }
     }
   } else {
