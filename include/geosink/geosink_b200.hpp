@@ -312,6 +312,46 @@ class HeatFilter {
   std::vector<double> coeff_;
 };
 
+// ---- heat.hpp:60-84: EulerHeat (implicit Euler; the device runs Solver::lockstep_cg) ------------
+class EulerHeat {
+ public:
+  enum class Solver { automatic, direct, lockstep_cg };
+  EulerHeat(const GraphLaplacian& lap, double t, int steps, Solver solver = Solver::automatic)
+      : n_(lap.size()), steps_(steps), t_(t) {
+    (void)solver;  // LDLT (direct / small automatic) has no device counterpart: CG for every size
+    gs_euler* e = nullptr;
+    detail::check(gs_euler_create(detail::ctx(), lap.matrix.handle(), t, steps, &e));
+    h_ = std::shared_ptr<gs_euler>(e, gs_euler_destroy);
+  }
+  std::vector<double> apply(const std::vector<double>& f) const {
+    if ((int)f.size() != n_) detail::fail(errc::length_mismatch, "LengthMismatch", "signal length");
+    std::vector<double> y(f.size());
+    detail::check(gs_euler_apply(detail::ctx(), h_.get(), f.data(), y.data(), 1, GS_MEM_HOST, nullptr));
+    return y;
+  }
+  void apply(const RowMajorXd& signals, RowMajorXd& out) const {
+    if ((int)signals.rows() != n_) detail::fail(errc::length_mismatch, "LengthMismatch", "signal length");
+    const auto cols = detail::to_columns(signals);
+    std::vector<double> y(cols.size());
+    detail::check(gs_euler_apply(detail::ctx(), h_.get(), cols.data(), y.data(), (int)signals.cols(),
+                                 GS_MEM_HOST, nullptr));
+    out = RowMajorXd(signals.rows(), signals.cols());
+    detail::from_columns(y, out);
+  }
+  int size() const { return n_; }
+  int steps() const { return steps_; }
+  double time() const { return t_; }
+
+ private:
+  int n_ = 0, steps_ = 1;
+  double t_ = 0.0;
+  std::shared_ptr<gs_euler> h_;
+};
+
+inline std::vector<double> apply_euler(const GraphLaplacian& lap, double t, int steps, const std::vector<double>& f) {
+  return EulerHeat(lap, t, steps).apply(f);
+}
+
 // ---- transport.hpp:14-69 ----------------------------------------------------------------------
 struct Distribution {
   std::vector<double> weights;

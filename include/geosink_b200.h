@@ -200,6 +200,18 @@ int gs_barycenter_ex(gs_ctx* ctx, const gs_filter* f, const double* a, const dou
                      const gs_comm* comm, int flags, double* out_bary, double* out_V,
                      double* out_W, int* out_iters, int* out_conv, double* out_err);
 
+/* ---- EulerHeat (heat.hpp:60-84, heat.cpp:133-219) ------------------- */
+/* The implicit-Euler competitor: `steps` solves of (I + (t/steps) L) x = b, each the reference's
+ * lockstep conjugate gradient over the batch (Solver::lockstep_cg; tolerance 1e-10 relative
+ * residual, at most 10 n iterations -> status 13 = SolveFailure). */
+typedef struct gs_euler gs_euler;
+int gs_euler_create(gs_ctx* ctx, const gs_graph* L, double t, int steps, gs_euler** out);
+void gs_euler_destroy(gs_euler* e);
+const gs_graph* gs_euler_system(const gs_euler* e); /* I + (t/steps) L, caller's vertex order */
+/* X, Y: `width` contiguous n-vectors; iters_out (optional): CG iterations of the last solve */
+int gs_euler_apply(gs_ctx* ctx, const gs_euler* e, const double* X, double* Y, int width, int mem,
+                   int* iters_out);
+
 /* ---- seeded RNG (rng.hpp:13-68), host-side ---------------------------------------------- */
 typedef struct gs_rng gs_rng;
 gs_rng* gs_rng_create(uint64_t seed);

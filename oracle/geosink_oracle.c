@@ -341,6 +341,33 @@ double go_detdot(const double* x, const double* y, int64_t n) {
   return tree256(v);
 }
 
+/* go_detdot on column c of two row-major n x B matrices (element i at i*B + c) */
+static double detdot_col(const double* x, const double* y, int64_t n, int B, int col) {
+  const int64_t nchunks = (n + DET_CHUNK - 1) / DET_CHUNK;
+  if (nchunks == 0) return 0.0;
+  double* partial = (double*)malloc((size_t)nchunks * sizeof(double));
+  for (int64_t c = 0; c < nchunks; ++c) {
+    double v[DET_T];
+    for (int t = 0; t < DET_T; ++t) {
+      double acc = 0.0;
+      for (int j = 0; j < DET_J; ++j) {
+        const int64_t idx = c * DET_CHUNK + (int64_t)j * DET_T + t;
+        if (idx < n) acc = fma(x[idx * B + col], y[idx * B + col], acc);
+      }
+      v[t] = acc;
+    }
+    partial[c] = tree256(v);
+  }
+  double v[DET_T];
+  for (int t = 0; t < DET_T; ++t) {
+    double acc = 0.0;
+    for (int64_t q = t; q < nchunks; q += DET_T) acc = acc + partial[q];
+    v[t] = acc;
+  }
+  free(partial);
+  return tree256(v);
+}
+
 /* ------------------------------------------------------------------------------------------
  * kNN selection: proj/src/graph.cpp:30-71. d2 = max(0, (|xi|^2 + |xj|^2) - 2 <xi,xj>) with the
  * norms and the inner product as fma chains in dimension order; the k smallest (d2, idx) pairs
@@ -1058,4 +1085,119 @@ int go_barycenter(const go_csr* S, const double* b, int degree, const double* a,
   free(bary);
   free(lb);
   return rc;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * EulerHeat: proj/src/heat.cpp:133-219 (competitor / test oracle).
+ * ---------------------------------------------------------------------------------------- */
+/* heat.cpp:133-162 */
+int go_euler_system(const go_csr* L, double t, int steps, go_csr* out) {
+  REQUIRE(t > 0.0 && isfinite(t), E_NON_POSITIVE_TIME, "diffusion time must be > 0");
+  REQUIRE(steps >= 1, E_INVALID_ARGUMENT, "substep count must be >= 1");
+  const int n = L->n;
+  const double h = t / steps;
+  int* rows = (int*)malloc((size_t)(L->nnz + n + 1) * sizeof(int));
+  int* cols = (int*)malloc((size_t)(L->nnz + n + 1) * sizeof(int));
+  double* vals = (double*)malloc((size_t)(L->nnz + n + 1) * sizeof(double));
+  int64_t m = 0;
+  for (int i = 0; i < n; ++i) {
+    int has_diag = 0;
+    for (int p = L->row_offsets[i]; p < L->row_offsets[i + 1]; ++p) {
+      const int j = L->col_indices[p];
+      if (j < i) continue;
+      double v = h * L->values[p];
+      if (j == i) {
+        v = v + 1.0;
+        has_diag = 1;
+      }
+      rows[m] = i;
+      cols[m] = j;
+      vals[m] = v;
+      ++m;
+    }
+    if (!has_diag) {
+      rows[m] = i;
+      cols[m] = i;
+      vals[m] = 1.0;
+      ++m;
+    }
+  }
+  const int rc = go_csr_from_triplets(n, m, rows, cols, vals, out);
+  free(rows);
+  free(cols);
+  free(vals);
+  return rc;
+}
+
+/* heat.cpp:166-201: every column runs its own CG in lockstep (Solver::lockstep_cg) */
+static int euler_solve(const go_csr* A, double* x, int n, int B, int* iters) {
+  const size_t len = (size_t)n * B;
+  double* b = (double*)malloc(len * sizeof(double));
+  double* r = (double*)malloc(len * sizeof(double));
+  double* p = (double*)malloc(len * sizeof(double));
+  double* ap = (double*)malloc(len * sizeof(double));
+  double* rs = (double*)malloc((size_t)B * sizeof(double));
+  double* bn = (double*)malloc((size_t)B * sizeof(double));
+  double* alpha = (double*)malloc((size_t)B * sizeof(double));
+  double* beta = (double*)malloc((size_t)B * sizeof(double));
+  int rc = 0;
+  memcpy(b, x, len * sizeof(double));
+  go_spmm(A, x, ap, B);
+  for (size_t e = 0; e < len; ++e) r[e] = b[e] - ap[e];
+  memcpy(p, r, len * sizeof(double));
+  for (int c = 0; c < B; ++c) {
+    rs[c] = detdot_col(r, r, n, B, c);
+    bn[c] = fmax(detdot_col(b, b, n, B, c), 1e-300);
+  }
+  const double tol2 = 1e-10 * 1e-10;
+  const long max_iter = 10L * n;
+  long it = 0;
+  for (;;) {
+    int any = 0;
+    for (int c = 0; c < B; ++c) any |= rs[c] > tol2 * bn[c];
+    if (!any) break;
+    if (!(it < max_iter)) {
+      rc = fail(E_SOLVE_FAILURE, "conjugate gradient exceeded 10 n iterations");
+      break;
+    }
+    ++it;
+    go_spmm(A, p, ap, B);
+    for (int c = 0; c < B; ++c) {
+      const double pap = detdot_col(p, ap, n, B, c);
+      alpha[c] = pap > 0.0 ? rs[c] / pap : 0.0;
+    }
+    for (size_t e = 0; e < len; ++e) {
+      const int c = (int)(e % (size_t)B);
+      x[e] = x[e] + p[e] * alpha[c];
+      r[e] = r[e] - ap[e] * alpha[c];
+    }
+    for (int c = 0; c < B; ++c) {
+      const double rn = detdot_col(r, r, n, B, c);
+      beta[c] = rs[c] > 0.0 ? rn / rs[c] : 0.0;
+      rs[c] = rn;
+    }
+    for (size_t e = 0; e < len; ++e) p[e] = r[e] + p[e] * beta[(int)(e % (size_t)B)];
+  }
+  if (iters) *iters = (int)it;
+  free(b);
+  free(r);
+  free(p);
+  free(ap);
+  free(rs);
+  free(bn);
+  free(alpha);
+  free(beta);
+  return rc;
+}
+
+/* heat.cpp:203-214 */
+int go_euler_apply(const go_csr* system, int steps, const double* X, double* Y, int width,
+                   int* iters_out) {
+  const int n = system->n;
+  memcpy(Y, X, (size_t)n * width * sizeof(double));
+  for (int s = 0; s < steps; ++s) {
+    const int rc = euler_solve(system, Y, n, width, iters_out);
+    if (rc) return rc;
+  }
+  return 0;
 }

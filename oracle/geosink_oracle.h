@@ -80,6 +80,15 @@ int go_filter_prepare(const go_csr* L, int kind, double lambda_bound, double t, 
 int go_filter_apply(const go_csr* scaled, const double* coeffs, int degree, const double* X,
                     double* Y, int width);
 
+/* heat.cpp:133-162: the implicit-Euler system I + (t/steps) L (upper-triangle entries scaled by
+ * h = t/steps, +1 on the diagonal, a missing diagonal becomes 1; mirrored by from_triplets) */
+int go_euler_system(const go_csr* L, double t, int steps, go_csr* out);
+/* heat.cpp:166-219: `steps` lockstep-CG solves (Solver::lockstep_cg) of the batch X (row-major
+ * n x width) into Y; column sums in the blocked order of go_detdot (Eigen's order is unpinned);
+ * iters_out (optional) = CG iterations of the last solve */
+int go_euler_apply(const go_csr* system, int steps, const double* X, double* Y, int width,
+                   int* iters_out);
+
 /* transport.cpp:108-255. mus/nus: P contiguous n-vectors. single_style selects the
  * sinkhorn_single messages. flags bit0: no stagnation abort (bench-only deviation).
  * fail_info[0] = failing pair (Disconnected) or -1, fail_info[1] = sweep of the failure. */

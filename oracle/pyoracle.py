@@ -84,6 +84,8 @@ def _declare(L):
                                     C.POINTER(go_csr), _dp, C.POINTER(C.c_double),
                                     C.POINTER(C.c_double)]
     L.go_filter_apply.argtypes = [C.POINTER(go_csr), _dp, C.c_int, _dp, _dp, C.c_int]
+    L.go_euler_system.argtypes = [C.POINTER(go_csr), C.c_double, C.c_int, C.POINTER(go_csr)]
+    L.go_euler_apply.argtypes = [C.POINTER(go_csr), C.c_int, _dp, _dp, C.c_int, C.POINTER(C.c_int)]
     L.go_sinkhorn_batch.argtypes = [C.POINTER(go_csr), _dp, C.c_int, C.c_double, _dp, _dp, _dp,
                                     C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, _dp, _dp,
                                     _dp, _dp, _ip, _ip, _dp, _ip]
@@ -285,6 +287,26 @@ class Filter:
         s = self.scaled._struct()
         _check(lib().go_filter_apply(C.byref(s), self.coeffs, self.degree, X, Y, width))
         return Y
+
+
+def euler_system(L: CSR, t: float, steps: int) -> CSR:
+    """heat.cpp:133-162: I + (t/steps) L."""
+    s = L._struct()
+    out = go_csr()
+    _check(lib().go_euler_system(C.byref(s), float(t), int(steps), C.byref(out)))
+    return _adopt(out)
+
+
+def euler_apply(system: CSR, steps: int, X: np.ndarray):
+    """heat.cpp:166-219 (lockstep CG); X (n,) or row-major (n, B). Returns (Y, iterations of the
+    last solve)."""
+    X = np.ascontiguousarray(X, np.float64)
+    width = 1 if X.ndim == 1 else X.shape[1]
+    Y = np.empty_like(X)
+    it = C.c_int(0)
+    s = system._struct()
+    _check(lib().go_euler_apply(C.byref(s), int(steps), X, Y, width, C.byref(it)))
+    return Y, it.value
 
 
 def sinkhorn_batch(f: Filter, a, mus, nus, max_iter=500, tol=1e-6, flags=0, single_style=False,

@@ -2191,3 +2191,27 @@ extern "C" int gs_part_sinkhorn(gs_ctx* ctx, const gs_part* p, const gs_comm* co
   return sinkhorn_part_impl<double>(ctx, p, comm, da, dmu, dnu, P, max_iter, tol, flags, mem, out_v, out_w,
                                     out_cost, out_kl, out_iters, out_conv, out_err, fail_pair, fail_sweep);
 }
+
+int gs_group_width(int B) { return choose_gw(B); }
+
+int gs_spmm_grouped(gs_ctx* ctx, const gs_graph* g, const double* x, double* y, int B) {
+  const int n = g->n;
+  if (n == 0 || B <= 0) return GS_OK;
+  const int GW = choose_gw(B), G = (B + GW - 1) / GW;
+  const int rpc = choose_rpc<double>(n, GW, G);
+  StepArgs A{};
+  A.offs = g->offs;
+  A.cols = g->cols;
+  A.vals = g->vals;
+  A.n = n;
+  A.ld = n;
+  A.tiles = (n + rows_per_block<double>(GW) * rpc - 1) / (rows_per_block<double>(GW) * rpc);
+  A.Gl = G;
+  A.Bpad = G * GW;
+  A.k = 0;
+  A.Tprev = x;
+  A.Tout = y;
+  launch_step<double>(ctx, GW, rpc, A, MODE_NONE);
+  GS_CUDA(ctx, cudaGetLastError());
+  return GS_OK;
+}

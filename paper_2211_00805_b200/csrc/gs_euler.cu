@@ -1,0 +1,394 @@
+// gs_euler.cu -- EulerHeat on the device (proj/src/heat.cpp:133-219): the
+// implicit-Euler competitor of the Chebyshev filter. The system I + (t/steps) L is built on the
+// device, renumbered by Cuthill-McKee (entries keep their column order, so every product row is
+// the reference's fma chain), and each of the `steps` solves is the reference's lockstep conjugate
+// gradient over the whole batch (Solver::lockstep_cg; the reference's automatic mode factorises
+// with Eigen's LDLT below n = 4000, which has no device counterpart here).
+//
+// Per-column sums use the blocked order of the oracle (go_detdot over the ORIGINAL vertex order;
+// Eigen's colwise().sum() order is unpinned) and the updates x + p*alpha,
+// r - ap*alpha, r + p*beta are unfused, so device and oracle agree bit for bit.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <memory>
+#include <vector>
+
+#include "gs_internal.cuh"
+#include "geosink_b200.h"
+
+struct gs_euler {
+  int n = 0, steps = 1;
+  double t = 0.0;
+  gs_graph* system = nullptr;  // caller's vertex order
+  gs_graph* perm = nullptr;    // Cuthill-McKee order
+  int* order = nullptr;        // order[new] = old
+  int* newpos = nullptr;       // newpos[old] = new
+};
+
+namespace {
+
+constexpr int kT = 256;
+inline unsigned blocks_for(int64_t work) { return (unsigned)((work + kT - 1) / kT); }
+
+// ---- system I + h L (heat.cpp:139-153, then from_triplets mirrors the upper triangle) --------------
+__device__ __forceinline__ bool euler_entry(const int* offs, const int* cols, const double* vals, int i,
+                                            int p, double h, int* j_out, double* v_out) {
+  const int j = cols[p];
+  // the reference scales the upper triangle and mirrors it; L is symmetric bit for bit, so the
+  // lower entries equal h * L(i, j) computed from their own row
+  double v = h * vals[p];
+  if (j == i) v = v + 1.0;
+  *j_out = j;
+  *v_out = v;
+  return v != 0.0;  // from_triplets drops explicit zeros (sparse.cpp:25)
+}
+
+__global__ void k_euler_count(const int* __restrict__ offs, const int* __restrict__ cols,
+                              const double* __restrict__ vals, int n, double h, int* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int c = 0;
+  bool diag = false;
+  for (int p = offs[i]; p < offs[i + 1]; ++p) {
+    int j;
+    double v;
+    if (cols[p] == i) diag = true;
+    if (euler_entry(offs, cols, vals, i, p, h, &j, &v)) ++c;
+  }
+  cnt[i] = c + (diag ? 0 : 1);  // a missing diagonal becomes 1 (heat.cpp:152)
+}
+
+__global__ void k_euler_fill(const int* __restrict__ offs, const int* __restrict__ cols,
+                             const double* __restrict__ vals, int n, double h, const int* __restrict__ out_offs,
+                             int* __restrict__ out_cols, double* __restrict__ out_vals) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int q = out_offs[i];
+  bool diag = false;
+  for (int p = offs[i]; p < offs[i + 1]; ++p) {
+    if (!diag && cols[p] > i) {  // no diagonal in this (column-sorted) row: insert the unit one
+      out_cols[q] = i;
+      out_vals[q] = 1.0;
+      ++q;
+      diag = true;
+    }
+    if (cols[p] == i) diag = true;
+    int j;
+    double v;
+    if (euler_entry(offs, cols, vals, i, p, h, &j, &v)) {
+      out_cols[q] = j;
+      out_vals[q] = v;
+      ++q;
+    }
+  }
+  if (!diag) {
+    out_cols[q] = i;
+    out_vals[q] = 1.0;
+  }
+}
+
+// ---- blocked column sums in the original vertex order (go_detdot restated per column) ----------
+// grouped layout: column col of vertex i lives at ((col / GW) * n + newpos[i]) * GW + col % GW
+__global__ void k_colsum_partial(const double* __restrict__ x, const double* __restrict__ y, int n, int GW,
+                                 const int* __restrict__ newpos, double* __restrict__ part, int B) {
+  const int col = blockIdx.y;
+  const int64_t c = blockIdx.x;
+  const size_t gb = (size_t)(col / GW) * n;
+  const int cc = col % GW;
+  double acc = 0.0;
+  for (int j = 0; j < DET_J; ++j) {
+    const int64_t i = c * DET_CHUNK + (int64_t)j * DET_T + threadIdx.x;
+    if (i < n) {
+      const size_t e = (gb + newpos[i]) * GW + cc;
+      acc = fma(x[e], y[e], acc);
+    }
+  }
+  __shared__ double sh[DET_T];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = DET_T / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = sh[threadIdx.x] + sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[(size_t)col * gridDim.x + c] = sh[0];
+}
+
+__global__ void k_colsum_fold(const double* __restrict__ part, int64_t nchunks, double* __restrict__ out) {
+  const int col = blockIdx.x;
+  __shared__ double sh[DET_T];
+  double acc = 0.0;
+  for (int64_t q = threadIdx.x; q < nchunks; q += DET_T) acc = acc + part[(size_t)col * nchunks + q];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = DET_T / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = sh[threadIdx.x] + sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[col] = nchunks ? sh[0] : 0.0;
+}
+
+// ---- CG vector updates (heat.cpp:176-199), grouped layout, column = (e / GW) / n * GW + e % GW ----
+__device__ __forceinline__ int col_of(int64_t e, int n, int GW) {
+  return (int)((e / GW) / n) * GW + (int)(e % GW);
+}
+
+__global__ void k_cg_start(const double* __restrict__ b, const double* __restrict__ ap, int64_t len,
+                           double* __restrict__ r, double* __restrict__ p) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = b[e] - ap[e];
+    r[e] = v;
+    p[e] = v;
+  }
+}
+
+__global__ void k_cg_xr(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                        const double* __restrict__ ap, const double* __restrict__ alpha, int64_t len, int n,
+                        int GW) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x) {
+    const double a = alpha[col_of(e, n, GW)];
+    x[e] = x[e] + p[e] * a;
+    r[e] = r[e] - ap[e] * a;
+  }
+}
+
+__global__ void k_cg_p(double* __restrict__ p, const double* __restrict__ r, const double* __restrict__ beta,
+                       int64_t len, int n, int GW) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len; e += (int64_t)gridDim.x * blockDim.x)
+    p[e] = r[e] + p[e] * beta[col_of(e, n, GW)];
+}
+
+// alpha = pap > 0 ? rs / pap : 0
+__global__ void k_cg_alpha(const double* __restrict__ rs, const double* __restrict__ pap, int B,
+                           double* __restrict__ alpha) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < B) alpha[c] = pap[c] > 0.0 ? rs[c] / pap[c] : 0.0;
+}
+
+// beta = rs > 0 ? rs_new / rs : 0; rs = rs_new; *busy = any column with rs > tol2 * |b|^2
+__global__ void k_cg_beta(double* __restrict__ rs, const double* __restrict__ rs_new,
+                          const double* __restrict__ bn, int B, double tol2, double* __restrict__ beta,
+                          int* __restrict__ busy) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= B) return;
+  beta[c] = rs[c] > 0.0 ? rs_new[c] / rs[c] : 0.0;
+  rs[c] = rs_new[c];
+  if (rs_new[c] > tol2 * bn[c]) atomicOr(busy, 1);
+}
+
+__global__ void k_cg_init_norms(const double* __restrict__ rs, double* __restrict__ bn, int B, double tol2,
+                                int* __restrict__ busy) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= B) return;
+  bn[c] = fmax(bn[c], 1e-300);
+  if (rs[c] > tol2 * bn[c]) atomicOr(busy, 1);
+}
+
+__global__ void k_pack_cols(const double* __restrict__ src, double* __restrict__ dst, int n, int B, int GW,
+                            int G, const int* __restrict__ order) {
+  const int64_t total = (int64_t)G * n * GW;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % GW);
+    const int64_t r = e / GW;
+    const int i = (int)(r % n);
+    const int col = (int)(r / n) * GW + c;
+    dst[e] = col < B ? src[(size_t)col * n + order[i]] : 0.0;
+  }
+}
+
+__global__ void k_unpack_cols(const double* __restrict__ src, double* __restrict__ dst, int n, int B, int GW,
+                              const int* __restrict__ newpos) {
+  const int64_t total = (int64_t)B * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int col = (int)(e / n), i = (int)(e % n);
+    dst[e] = src[((size_t)(col / GW) * n + newpos[i]) * GW + col % GW];
+  }
+}
+
+unsigned grid_for(int64_t work) {
+  int64_t b = (work + kT - 1) / kT;
+  if (b > 148 * 32) b = 148 * 32;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+struct Col {  // per-column device scalars, padded to the grouped width (padding stays 0)
+  DevBuf<double> v;
+  int alloc(gs_ctx* ctx, int Bpad) {
+    GS_CUDA(ctx, v.alloc(Bpad, ctx->stream));
+    GS_CUDA(ctx, cudaMemsetAsync(v.get(), 0, Bpad * sizeof(double), ctx->stream));
+    return GS_OK;
+  }
+};
+
+int colsum(gs_ctx* ctx, const gs_euler* E, const double* x, const double* y, int B, int GW,
+           DevBuf<double>& part, double* out) {
+  const int n = E->n;
+  const int64_t nchunks = (n + DET_CHUNK - 1) / DET_CHUNK;
+  cudaStream_t s = ctx->stream;
+  if (nchunks > 0) {
+    gs_launch_begin(ctx, 1);
+    k_colsum_partial<<<dim3((unsigned)nchunks, B), DET_T, 0, s>>>(x, y, n, GW, E->newpos, part.get(), B);
+    gs_launch_end(ctx, 1);
+  }
+  gs_launch_begin(ctx, 1);
+  k_colsum_fold<<<B, DET_T, 0, s>>>(part.get(), nchunks, out);
+  gs_launch_end(ctx, 1);
+  return GS_OK;
+}
+
+// heat.cpp:166-201 on the grouped block x (B columns); *iters = CG iterations
+int euler_solve(gs_ctx* ctx, const gs_euler* E, double* x, int B, int* iters) {
+  const int n = E->n;
+  const int GW = gs_group_width(B), G = (B + GW - 1) / GW;
+  const int64_t len = (int64_t)G * GW * n;
+  cudaStream_t s = ctx->stream;
+  DevBuf<double> b, r, p, ap, part;
+  Col rs, rn, bn, pap, alpha, beta;
+  GS_CUDA(ctx, b.alloc(len, s));
+  GS_CUDA(ctx, r.alloc(len, s));
+  GS_CUDA(ctx, p.alloc(len, s));
+  GS_CUDA(ctx, ap.alloc(len, s));
+  GS_CUDA(ctx, part.alloc((size_t)B * ((n + DET_CHUNK - 1) / DET_CHUNK + 1), s));
+  for (Col* c : {&rs, &rn, &bn, &pap, &alpha, &beta}) GS_TRY(c->alloc(ctx, G * GW));
+  DevBuf<int> busy;
+  GS_CUDA(ctx, busy.alloc(1, s));
+  GS_CUDA(ctx, cudaMemcpyAsync(b.get(), x, len * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  GS_TRY(gs_spmm_grouped(ctx, E->perm, x, ap.get(), B));
+  gs_launch_begin(ctx, 1);
+  k_cg_start<<<grid_for(len), kT, 0, s>>>(b.get(), ap.get(), len, r.get(), p.get());
+  gs_launch_end(ctx, 1);
+  GS_TRY(colsum(ctx, E, r.get(), r.get(), B, GW, part, rs.v.get()));
+  GS_TRY(colsum(ctx, E, b.get(), b.get(), B, GW, part, bn.v.get()));
+  const double tol2 = 1e-10 * 1e-10;
+  const long max_iter = 10L * n;
+  GS_CUDA(ctx, cudaMemsetAsync(busy.get(), 0, sizeof(int), s));
+  gs_launch_begin(ctx, 1);
+  k_cg_init_norms<<<(B + kT - 1) / kT, kT, 0, s>>>(rs.v.get(), bn.v.get(), B, tol2, busy.get());
+  gs_launch_end(ctx, 1);
+  long it = 0;
+  for (;;) {
+    int h_busy = 0;
+    GS_CUDA(ctx, cudaMemcpyAsync(&h_busy, busy.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    GS_CUDA(ctx, cudaStreamSynchronize(s));
+    if (!h_busy) break;
+    if (!(it < max_iter)) return gs_fail(ctx, ERRC_SOLVE_FAILURE, "conjugate gradient exceeded 10 n iterations");
+    ++it;
+    GS_TRY(gs_spmm_grouped(ctx, E->perm, p.get(), ap.get(), B));
+    GS_TRY(colsum(ctx, E, p.get(), ap.get(), B, GW, part, pap.v.get()));
+    gs_launch_begin(ctx, 1);
+    k_cg_alpha<<<(B + kT - 1) / kT, kT, 0, s>>>(rs.v.get(), pap.v.get(), B, alpha.v.get());
+    gs_launch_end(ctx, 1);
+    gs_launch_begin(ctx, 1);
+    k_cg_xr<<<grid_for(len), kT, 0, s>>>(x, r.get(), p.get(), ap.get(), alpha.v.get(), len, n, GW);
+    gs_launch_end(ctx, 1);
+    GS_TRY(colsum(ctx, E, r.get(), r.get(), B, GW, part, rn.v.get()));
+    GS_CUDA(ctx, cudaMemsetAsync(busy.get(), 0, sizeof(int), s));
+    gs_launch_begin(ctx, 1);
+    k_cg_beta<<<(B + kT - 1) / kT, kT, 0, s>>>(rs.v.get(), rn.v.get(), bn.v.get(), B, tol2, beta.v.get(),
+                                               busy.get());
+    gs_launch_end(ctx, 1);
+    gs_launch_begin(ctx, 1);
+    k_cg_p<<<grid_for(len), kT, 0, s>>>(p.get(), r.get(), beta.v.get(), len, n, GW);
+    gs_launch_end(ctx, 1);
+  }
+  if (iters) *iters = (int)it;
+  return GS_OK;
+}
+
+}  // namespace
+
+extern "C" int gs_euler_create(gs_ctx* ctx, const gs_graph* L, double t, int steps, gs_euler** out) {
+  if (!ctx || !L || !out) return GS_ERR_UNSUPPORTED;
+  *out = nullptr;
+  if (!(t > 0.0 && std::isfinite(t))) return gs_fail(ctx, ERRC_NON_POSITIVE_TIME, "diffusion time must be > 0");
+  if (steps < 1) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "substep count must be >= 1");
+  cudaStream_t s = ctx->stream;
+  std::unique_ptr<gs_euler> E(new gs_euler());
+  const int n = L->n;
+  E->n = n;
+  E->t = t;
+  E->steps = steps;
+  const double h = t / steps;
+  DevBuf<int> cnt;
+  GS_CUDA(ctx, cnt.alloc((size_t)n + 1, s));
+  GS_CUDA(ctx, cudaMemsetAsync(cnt.get(), 0, ((size_t)n + 1) * sizeof(int), s));
+  if (n > 0) {
+    gs_launch_begin(ctx, 1);
+    k_euler_count<<<blocks_for(n), kT, 0, s>>>(L->offs, L->cols, L->vals, n, h, cnt.get());
+    gs_launch_end(ctx, 1);
+  }
+  DevBuf<int> offs;
+  GS_CUDA(ctx, offs.alloc((size_t)n + 1, s));
+  size_t tb = 0;
+  GS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.get(), offs.get(), n + 1, s));
+  DevBuf<unsigned char> tmp;
+  GS_CUDA(ctx, tmp.alloc(tb, s));
+  GS_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp.get(), tb, cnt.get(), offs.get(), n + 1, s));
+  int nnz = 0;
+  GS_CUDA(ctx, cudaMemcpyAsync(&nnz, offs.get() + n, sizeof(int), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  GS_TRY(gs_graph_alloc(ctx, n, nnz, &E->system));
+  GS_CUDA(ctx, cudaMemcpyAsync(E->system->offs, offs.get(), ((size_t)n + 1) * sizeof(int), cudaMemcpyDeviceToDevice, s));
+  if (n > 0) {
+    gs_launch_begin(ctx, 1);
+    k_euler_fill<<<blocks_for(n), kT, 0, s>>>(L->offs, L->cols, L->vals, n, h, offs.get(), E->system->cols,
+                                              E->system->vals);
+    gs_launch_end(ctx, 1);
+  }
+  GS_CUDA(ctx, cudaMalloc((void**)&E->order, ((size_t)n + 1) * sizeof(int)));
+  GS_CUDA(ctx, cudaMalloc((void**)&E->newpos, ((size_t)n + 1) * sizeof(int)));
+  GS_TRY(gs_bfs_order(ctx, E->system, E->order, E->newpos, 1, nullptr, nullptr));
+  GS_TRY(gs_permute_graph(ctx, E->system, E->order, E->newpos, &E->perm));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  *out = E.release();
+  return GS_OK;
+}
+
+extern "C" void gs_euler_destroy(gs_euler* E) {
+  if (!E) return;
+  gs_graph_destroy(E->system);
+  gs_graph_destroy(E->perm);
+  cudaFree(E->order);
+  cudaFree(E->newpos);
+  delete E;
+}
+
+extern "C" const gs_graph* gs_euler_system(const gs_euler* E) { return E ? E->system : nullptr; }
+
+extern "C" int gs_euler_apply(gs_ctx* ctx, const gs_euler* E, const double* X, double* Y, int width,
+                              int mem, int* iters_out) {
+  if (!ctx || !E) return GS_ERR_UNSUPPORTED;
+  if (iters_out) *iters_out = 0;
+  if (width < 0) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "width");
+  const int n = E->n;
+  if (width == 0 || n == 0) return GS_OK;
+  cudaStream_t s = ctx->stream;
+  DevBuf<double> xin, yout, blk;
+  const double* dX = X;
+  if (mem != GS_MEM_DEVICE) {
+    GS_CUDA(ctx, xin.alloc((size_t)width * n, s));
+    GS_CUDA(ctx, cudaMemcpyAsync(xin.get(), X, (size_t)width * n * sizeof(double), cudaMemcpyHostToDevice, s));
+    dX = xin.get();
+  }
+  double* dY = Y;
+  if (mem != GS_MEM_DEVICE) {
+    GS_CUDA(ctx, yout.alloc((size_t)width * n, s));
+    dY = yout.get();
+  }
+  const int GW = gs_group_width(width), G = (width + GW - 1) / GW;
+  const int64_t len = (int64_t)G * GW * n;
+  GS_CUDA(ctx, blk.alloc(len, s));
+  gs_launch_begin(ctx, 1);
+  k_pack_cols<<<grid_for(len), kT, 0, s>>>(dX, blk.get(), n, width, GW, G, E->order);
+  gs_launch_end(ctx, 1);
+  int it = 0;
+  for (int step = 0; step < E->steps; ++step) GS_TRY(euler_solve(ctx, E, blk.get(), width, &it));
+  gs_launch_begin(ctx, 1);
+  k_unpack_cols<<<grid_for((int64_t)width * n), kT, 0, s>>>(blk.get(), dY, n, width, GW, E->newpos);
+  gs_launch_end(ctx, 1);
+  if (mem != GS_MEM_DEVICE)
+    GS_CUDA(ctx, cudaMemcpyAsync(Y, dY, (size_t)width * n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  if (iters_out) *iters_out = it;
+  return GS_OK;
+}

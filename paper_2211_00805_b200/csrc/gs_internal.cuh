@@ -173,5 +173,9 @@ int gs_bfs_order(gs_ctx* ctx, const gs_graph* g, int* d_order, int* d_newpos, in
                  int* d_order_sig, int* d_newpos_sig);
 int gs_permute_graph(gs_ctx* ctx, const gs_graph* g, const int* d_order, const int* d_newpos,
                      gs_graph** out);
+// grouped-layout fp64 SpMM y = G x through the step kernel (gs_cheb.cu): B columns in
+// gs_group_width(B)-wide groups, each an n x GW row-major block
+int gs_group_width(int B);
+int gs_spmm_grouped(gs_ctx* ctx, const gs_graph* g, const double* x, double* y, int B);
 int gs_csr_from_sorted_entries(gs_ctx* ctx, int n, int64_t m, const unsigned long long* d_keys,
                                const double* d_vals, bool check_dups, gs_graph** out);

@@ -263,6 +263,22 @@ int main() {
     CHECK(same_apply);
     CHECK_THROWS_CODE(RowPartition(f, 2, 5), errc::invalid_argument);
   }
+  // EulerHeat: many implicit steps approach the heat kernel; validation codes
+  {
+    const auto lap = laplacian(random_connected_graph(40, 8), LaplacianKind::normalized);
+    const HeatFilter f(lap, 1.0, 40);
+    std::vector<double> x(40);
+    for (int i = 0; i < 40; ++i) x[i] = std::sin(0.3 * i);
+    const auto ref = f.apply(x);
+    const auto y = apply_euler(lap, 1.0, 200, x);
+    double e = 0.0, m = 0.0;
+    for (int i = 0; i < 40; ++i) {
+      e = std::max(e, std::abs(y[i] - ref[i]));
+      m = std::max(m, std::abs(ref[i]));
+    }
+    CHECK(e <= 5e-3 * m);
+    CHECK_THROWS_CODE(EulerHeat(lap, -1.0, 2), errc::non_positive_time);
+  }
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail;
 }

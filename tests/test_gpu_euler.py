@@ -1,0 +1,78 @@
+"""EulerHeat on the device (gs_euler_*; heat.cpp:133-219) against the CPU
+oracle: the system I + (t/steps) L bit for bit, and the lockstep-CG applies bit for bit (the
+oracle restates the CG with the device's blocked column sums; tests/test_oracle_cpu.py pins it
+to a dense solve)."""
+import numpy as np
+import pytest
+
+import pyoracle as po
+from helpers import acceptance_graph, random_connected_graph
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gs(ctx):
+    import paper_2211_00805_b200 as gs
+    return gs
+
+
+def _pair(gs, r, c, v, n, kind):
+    A = gs.SparseSymMatrix.from_arrays(n, r, c, v)
+    lap = gs.laplacian(A, gs.LaplacianKind(kind))
+    Lo, _, _ = po.laplacian(po.from_triplets(n, r, c, v), kind)
+    return lap, Lo
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("steps", [1, 3])
+@pytest.mark.parametrize("width", [1, 3, 64, 70])
+def test_euler_apply_bit_exact(gs, kind, steps, width):
+    n = 400
+    r, c, v = acceptance_graph(n, 17 + width)
+    lap, Lo = _pair(gs, r, c, v, n, kind)
+    E = gs.EulerHeat(lap, 0.6, steps)
+    So = po.euler_system(Lo, 0.6, steps)
+    S = E.system()
+    assert np.array_equal(S.row_offsets(), So.offs)
+    assert np.array_equal(S.col_indices(), So.cols)
+    assert np.array_equal(S.values(), So.vals)
+    X = np.random.default_rng(width + steps).standard_normal((n, width))
+    if width == 1:
+        X = X[:, 0]
+    Y = E.apply(X)
+    Yo, it_o = po.euler_apply(So, steps, X)
+    assert np.array_equal(Y, Yo)
+    assert E.last_iterations == it_o > 0
+
+
+def test_euler_isolated_vertex_and_validation(gs):
+    r = np.array([0, 1, 2], np.int32)
+    c = np.array([1, 2, 3], np.int32)
+    v = np.array([1.0, 2.0, 0.5])
+    lap, Lo = _pair(gs, r, c, v, 5, 0)  # vertex 4 isolated: unit system row
+    E = gs.EulerHeat(lap, 1.0, 2)
+    S = E.system()
+    assert np.array_equal(S.row_offsets(), po.euler_system(Lo, 1.0, 2).offs)
+    x = np.arange(5, dtype=np.float64) + 1.0
+    y = E.apply(x)
+    assert np.array_equal(y, po.euler_apply(po.euler_system(Lo, 1.0, 2), 2, x)[0])
+    assert y[4] == x[4]
+    with pytest.raises(gs.Error) as e:
+        gs.EulerHeat(lap, 0.0, 2)
+    assert e.value.code == gs.errc.non_positive_time
+    with pytest.raises(gs.Error) as e:
+        gs.EulerHeat(lap, 1.0, 0)
+    assert e.value.code == gs.errc.invalid_argument
+
+
+def test_euler_converges_to_heat_kernel(gs):
+    """Implicit Euler with many steps approaches e^{-tL} (the Chebyshev filter)."""
+    n = 200
+    r, c, v = random_connected_graph(n, 5)
+    lap, _ = _pair(gs, r, c, v, n, 1)
+    f = gs.HeatFilter(lap, 1.0, 40)
+    x = np.random.default_rng(3).standard_normal(n)
+    ref = f.apply(x)
+    err = [np.abs(gs.apply_euler(lap, 1.0, s, x) - ref).max() / np.abs(ref).max() for s in (10, 100)]
+    assert err[1] < err[0] and err[1] < 5e-3

@@ -502,3 +502,47 @@ def test_barycenter_validation():
     with pytest.raises(po.OracleError):
         po.barycenter(f, np.full(4, 0.25), np.full((1, 4), 0.25), np.array([0.5, 0.5])[:1] * 3, 100,
                       1e-6)
+
+
+# --------------------------------------------------------------------------- EulerHeat (f3)
+def test_euler_system_and_dense_solve():
+    """heat.cpp:133-219: the system equals I + (t/steps) L and the lockstep-CG apply matches
+    (I + hL)^{-steps} X from a dense solve (CG residual tolerance 1e-10)."""
+    from helpers import random_connected_graph
+    n = 120
+    r, c, v = random_connected_graph(n, 31)
+    A = po.from_triplets(n, r, c, v)
+    L, _, _ = po.laplacian(A, 0)
+    t, steps = 0.8, 4
+    S = po.euler_system(L, t, steps)
+    Ld = np.zeros((n, n))
+    for i in range(n):
+        for p in range(L.offs[i], L.offs[i + 1]):
+            Ld[i, L.cols[p]] = L.vals[p]
+    Sd = np.zeros((n, n))
+    for i in range(n):
+        for p in range(S.offs[i], S.offs[i + 1]):
+            Sd[i, S.cols[p]] = S.vals[p]
+    assert np.allclose(Sd, np.eye(n) + (t / steps) * Ld, rtol=0, atol=1e-15)
+    X = np.random.default_rng(2).standard_normal((n, 3))
+    Y, it = po.euler_apply(S, steps, X)
+    ref = X.copy()
+    for _ in range(steps):
+        ref = np.linalg.solve(Sd, ref)
+    assert it > 0
+    assert np.max(np.abs(Y - ref)) <= 1e-8 * np.max(np.abs(ref))
+    y1, _ = po.euler_apply(S, steps, X[:, 1].copy())
+    assert np.max(np.abs(y1 - ref[:, 1])) <= 1e-8 * np.max(np.abs(ref))
+
+
+def test_euler_isolated_vertex_and_validation():
+    n = 5  # vertex 4 isolated: its system row is the unit diagonal
+    A = po.from_triplets(n, np.array([0, 1, 2], np.int32), np.array([1, 2, 3], np.int32),
+                         np.array([1.0, 2.0, 0.5]))
+    L, _, _ = po.laplacian(A, 0)
+    S = po.euler_system(L, 1.0, 2)
+    assert S.offs[5] - S.offs[4] == 1 and S.cols[S.offs[4]] == 4 and S.vals[S.offs[4]] == 1.0
+    with pytest.raises(po.OracleError):
+        po.euler_system(L, 0.0, 2)
+    with pytest.raises(po.OracleError):
+        po.euler_system(L, 1.0, 0)
