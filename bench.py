@@ -439,7 +439,7 @@ def run_engine(args):
                                          "column_sweeps_per_s": value * P}),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "k_cheb_step<8,*> (fused Chebyshev step)",
+                         "kernel": "k_cheb_step<double, 64, *, 4> (fused Chebyshev step, one warp per 512-byte row)",
                          "bytes_per_launch": bytes_step, "avg_launch_ms": avg_step_ms,
                          "launches_timed": step_n, "timing_period": args.timing_period,
                          "share_of_step": avg_step_ms * steps_total / max(elapsed_ms, 1e-9)},
@@ -828,8 +828,10 @@ def main():
     ap.add_argument("--no-fp32", action="store_true")
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3])
     ap.add_argument("--members", type=int, default=8)
-    ap.add_argument("--timing-period", type=int, default=8,
-                    help="event-time every Nth engine launch inside the timed region")
+    ap.add_argument("--timing-period", type=int, default=1,
+                    help="event-time every Nth engine launch inside the timed region (sweeps "
+                         "replayed as CUDA graphs are not split into launches: the timed launches "
+                         "are each call's initial apply)")
     args = ap.parse_args()
     if args.config == 0:  # BASELINE.json configs[0]: n=2000, one pair, 100 sweeps
         if args.n == 200_000:
