@@ -20,6 +20,9 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kKnnThreads = 128;
 constexpr int kKnnTile = 128;
+#ifndef GS_KNN_IL
+#define GS_KNN_IL 4  // candidates whose inner products run as interleaved fma chains
+#endif
 
 __device__ __forceinline__ double row_sqnorm(const double* p, int d) {
   double s = 0.0;
@@ -75,14 +78,25 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn(const double* __restrict__ 
     for (int e = threadIdx.x; e < cnt; e += kKnnThreads) s_sq[e] = sq[base + e];
     __syncthreads();
     if (!valid) continue;
-    for (int jj = 0; jj < cnt; ++jj) {
-      const int j = base + jj;
-      const double* xj = s_x + jj * d;
-      double g = 0.0;
+    // four candidates' inner products as independent fma chains (each in dimension order, as
+    // the oracle's), then the selection in ascending candidate order
+    constexpr int IL = GS_KNN_IL;
+    for (int j0 = 0; j0 < cnt; j0 += IL) {
+      double gg[IL];
+#pragma unroll
+      for (int u = 0; u < IL; ++u) gg[u] = 0.0;
 #pragma unroll
       for (int q = 0; q < DMAX; ++q)
-        if (q < d) g = fma(xq[q], xj[q], g);
-      double d2 = (sqq + s_sq[jj]) - 2.0 * g;
+        if (q < d)
+#pragma unroll
+          for (int u = 0; u < IL; ++u)
+            if (j0 + u < cnt) gg[u] = fma(xq[q], s_x[(j0 + u) * d + q], gg[u]);
+#pragma unroll
+      for (int u = 0; u < IL; ++u) {
+      const int jj = j0 + u;
+      if (jj >= cnt) break;
+      const int j = base + jj;
+      double d2 = (sqq + s_sq[jj]) - 2.0 * gg[u];
       if (!(d2 > 0.0)) d2 = 0.0;
       if (j == qi) continue;
       // current worst kept candidate is slot k-1
@@ -106,6 +120,7 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn(const double* __restrict__ 
       if (bd[0] > d2) {
         bd[0] = d2;
         bi[0] = j;
+      }
       }
     }
   }
