@@ -616,6 +616,181 @@ def run_engine_bary(args):
     return 0
 
 
+# --------------------------------------------------------------------------- config 4 (barycentric distance)
+def run_engine_bary_dist(args):
+    """Config 4: barycentric distance (barycenter.cpp:101-107) on n = 4e6 points in R^30 (40
+    clusters), k = 15, t = 0.5, K = 30: the barycenters of two 16-member groups (200 sweeps each,
+    members sharded over the ranks with one allreduce pair per sweep, as config 2), then the
+    geodesic Sinkhorn distance between them (200 sweeps, every rank). One step = one evaluation;
+    value = evaluations/s (strong scaling)."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_00805_b200 as gs
+    from paper_2211_00805_b200 import _capi, workloads
+    from paper_2211_00805_b200.distributed import TorchAllreduce, member_shard
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    with _StdoutToStderr():
+        if world > 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("nccl", init_method="tcp://127.0.0.1:%d" % _free_port(),
+                                    rank=0, world_size=1, device_id=torch.device("cuda", local))
+        dist.barrier()
+    ctx = gs.Context(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    lib = ctx.lib
+    n, m = args.n, args.members
+    t0 = time.perf_counter()
+    cfg = workloads.config4(n, m)
+    t_data = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    A, sigma = gs.knn_gaussian_graph(cfg.mix.points, cfg.k, ctx=ctx)
+    t_graph = time.perf_counter() - t0
+    lap = gs.laplacian(A, gs.LaplacianKind.combinatorial)
+    filt = gs.HeatFilter(lap, cfg.t, cfg.degree)
+    lo, hi = member_shard(m, world, rank)
+    B = hi - lo
+    dev = torch.device("cuda", local)
+    Ga = torch.from_numpy(np.ascontiguousarray(cfg.group_a[lo:hi])).to(dev)
+    Gb = torch.from_numpy(np.ascontiguousarray(cfg.group_b[lo:hi])).to(dev)
+    al = torch.full((B,), 1.0 / m, dtype=torch.float64, device=dev)
+    a = torch.full((n,), 1.0 / n, dtype=torch.float64, device=dev)
+    ba = torch.empty(n, dtype=torch.float64, device=dev)
+    bb = torch.empty_like(ba)
+    Vo = torch.empty((B, n), dtype=torch.float64, device=dev)
+    Wo = torch.empty_like(Vo)
+    vd = torch.empty(n, dtype=torch.float64, device=dev)
+    wd = torch.empty_like(vd)
+    dsc = torch.empty(3, dtype=torch.float64, device=dev)
+    dsi = torch.empty(2, dtype=torch.int32, device=dev)
+    it, conv, err = np.zeros(1, np.int32), np.zeros(1, np.int32), np.zeros(1)
+    hook = TorchAllreduce(None, device_buffers=True)
+    comm_arg = C.byref(hook.comm) if world > 1 else None
+    fp, fs = C.c_int(), C.c_int()
+    flags = _capi.GS_FLAG_NO_STAGNATION_ABORT
+
+    def bary(M, out):
+        rc = lib.gs_barycenter_ex(ctx.handle, filt._h, a.data_ptr(), M.data_ptr(), B, al.data_ptr(),
+                                  args.sweeps, TOL_RUN_ALL, _capi.GS_MEM_DEVICE, comm_arg, 0,
+                                  out.data_ptr(), Vo.data_ptr(), Wo.data_ptr(), it.ctypes.data,
+                                  conv.ctypes.data, err.ctypes.data)
+        if hook.error is not None:
+            raise hook.error
+        ctx.check(rc)
+
+    def step():
+        bary(Ga, ba)
+        bary(Gb, bb)
+        p0, pi = dsc.data_ptr(), dsi.data_ptr()
+        ctx.check(lib.gs_sinkhorn(ctx.handle, filt._h, a.data_ptr(), ba.data_ptr(), bb.data_ptr(), 1,
+                                  args.sweeps, TOL_RUN_ALL, flags | _capi.GS_FLAG_SINGLE,
+                                  _capi.GS_MEM_DEVICE, vd.data_ptr(), wd.data_ptr(), p0, p0 + 8,
+                                  pi, pi + 4, p0 + 16, C.byref(fp), C.byref(fs)))
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    ctx.set_timing(True, period=args.timing_period)
+    l0 = ctx.launch_count()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = sampler.stop()
+    step_n, step_ms = ctx.timing(0)
+    ctx.set_timing(False)
+    launches = ctx.launch_count() - l0
+    elapsed = max_over_ranks(e0.elapsed_time(e1))
+    value = args.steps / (elapsed / 1000.0)
+    distance = float(dsc[0].item())
+    # ---- e2e: the same evaluation through gs.barycentric_distance-equivalent host-buffer calls ----
+    Gah = torch.from_numpy(np.ascontiguousarray(cfg.group_a[lo:hi])).pin_memory()
+    Gbh = torch.from_numpy(np.ascontiguousarray(cfg.group_b[lo:hi])).pin_memory()
+    alh = torch.full((B,), 1.0 / m, dtype=torch.float64).pin_memory()
+    ah = torch.full((n,), 1.0 / n, dtype=torch.float64).pin_memory()
+    bah = torch.empty(n, dtype=torch.float64).pin_memory()
+    bbh = torch.empty_like(bah).pin_memory()
+    Vh = torch.empty((B, n), dtype=torch.float64).pin_memory()
+    Wh = torch.empty_like(Vh).pin_memory()
+    vh = torch.empty(n, dtype=torch.float64).pin_memory()
+    wh = torch.empty_like(vh).pin_memory()
+    cost_h, kl_h, err_h = np.zeros(1), np.zeros(1), np.zeros(1)
+    it_h, cv_h = np.zeros(1, np.int32), np.zeros(1, np.int32)
+
+    def step_host():
+        for M, out in ((Gah, bah), (Gbh, bbh)):
+            rc = lib.gs_barycenter_ex(ctx.handle, filt._h, ah.data_ptr(), M.data_ptr(), B, alh.data_ptr(),
+                                      args.sweeps, TOL_RUN_ALL, _capi.GS_MEM_HOST, comm_arg, 0,
+                                      out.data_ptr(), Vh.data_ptr(), Wh.data_ptr(), it.ctypes.data,
+                                      conv.ctypes.data, err.ctypes.data)
+            if hook.error is not None:
+                raise hook.error
+            ctx.check(rc)
+        ctx.check(lib.gs_sinkhorn(ctx.handle, filt._h, ah.data_ptr(), bah.data_ptr(), bbh.data_ptr(), 1,
+                                  args.sweeps, TOL_RUN_ALL, flags | _capi.GS_FLAG_SINGLE,
+                                  _capi.GS_MEM_HOST, vh.data_ptr(), wh.data_ptr(), cost_h.ctypes.data,
+                                  kl_h.ctypes.data, it_h.ctypes.data, cv_h.ctypes.data, err_h.ctypes.data,
+                                  C.byref(fp), C.byref(fs)))
+
+    torch.cuda.synchronize()
+    dist.barrier()
+    t1 = time.perf_counter()
+    step_host()
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t1)
+    e2e = {"value": 1.0 / e2e_s, "unit": "barycentric distances/s",
+           "h2d_bytes_per_step": 2 * (B * n * 8 + B * 8 + n * 8) + 2 * n * 8 + n * 8,
+           "d2h_bytes_per_step": 2 * (n * 8 + 2 * B * n * 8 + 16) + 2 * n * 8 + 32, "steps": 1}
+    peak, peak_kind = peaks()
+    nnz_L = lap.matrix.stored_entries()
+    bytes_step = algorithmic_bytes_per_step(n, nnz_L, B)
+    avg = step_ms / max(step_n, 1)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "barycentric distances/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"config4: {n} points in R^30 (40-component mixture), k=15 "
+                                   f"Gaussian-median graph, t=0.5, K=30; two {m}-member barycenters "
+                                   f"x {args.sweeps} sweeps (members sharded over {world} rank(s)) + "
+                                   f"their geodesic Sinkhorn distance ({args.sweeps} sweeps)",
+                       "nnz_L": int(nnz_L), "graph_build_s": t_graph, "data_s": t_data,
+                       "members_per_rank": B, "distance": distance,
+                       "sweeps_per_step": {"barycenter": 2 * args.sweeps, "distance": args.sweeps},
+                       "parallelism": (f"member sharding x{world}, NCCL allreduce per sweep"
+                                       if world > 1 else "one rank: no collective, CUDA-graph sweeps")},
+            "roofline": {"bound": "hbm", "achieved": bytes_step / (avg / 1000.0) / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": bytes_step / (avg / 1000.0) / 1e9 / peak,
+                         "traffic": None, "peak_kind": peak_kind, "bytes_per_launch": bytes_step,
+                         "avg_launch_ms": avg, "launches_timed": step_n,
+                         "note": "average over the barycenter (B = members/rank) and distance (B = 1) "
+                                 "step launches; bytes_per_launch is the barycenter step's"},
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": None,
+        }), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 # --------------------------------------------------------------------------- config 3 (row partitions)
 def run_engine_rows(args):
     """Config 3: n = 2e7 swiss roll, k = 10 Gaussian-median graph (grid kNN), combinatorial L,
@@ -826,7 +1001,7 @@ def main():
     ap.add_argument("--ref-sweeps", type=int, default=1)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")
-    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3])
+    ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
     ap.add_argument("--members", type=int, default=8)
     ap.add_argument("--timing-period", type=int, default=1,
                     help="event-time every Nth engine launch inside the timed region (sweeps "
@@ -848,6 +1023,16 @@ def main():
                               "O(n^2 d) CPU kNN at n=1e6; use the default config"}))
             return 0
         return run_engine_bary(args)
+    if args.config == 4:
+        if args.n == 200_000:
+            args.n = 4_000_000
+        if args.members == 8:
+            args.members = 16
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "config 4 reference arm needs an "
+                              "O(n^2 d) CPU kNN at n=4e6; use the default config"}))
+            return 0
+        return run_engine_bary_dist(args)
     if args.config == 3:
         if args.n == 200_000:
             args.n = 20_000_000

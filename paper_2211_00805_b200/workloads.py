@@ -142,3 +142,44 @@ def config2(n: int = 1_000_000, m: int = 8, d: int = 30, components: int = 20, s
     mix = gaussian_mixture(n, d, components, seed)
     members = cluster_subset_members(mix, m, 4, 0.6, member_seed)
     return Config2(mix, members)
+
+
+def _cluster_choice(rng: Rng, pool, count):
+    avail = list(pool)
+    return [avail.pop(rng.below(len(avail))) for _ in range(min(count, len(avail)))]
+
+
+@dataclass
+class Config4:
+    mix: Mixture
+    group_a: np.ndarray  # m x n
+    group_b: np.ndarray  # m x n
+    k: int = 15
+    t: float = 0.5
+    degree: int = 30
+    sweeps: int = 200
+
+
+def config4(n: int = 4_000_000, m: int = 16, d: int = 30, components: int = 40, seed: int = 5,
+            member_seed: int = 6) -> Config4:
+    """Config 4: 40-component Gaussian mixture in R^30 (means ~ N(0, 5^2 I), sigma = 1). Decisions
+    (DESIGN.md "Workloads"): a group-A member is uniform over the points of a random half (10) of
+    clusters 0-19; a group-B member is the same construction with 20% of its mass moved onto the
+    points of a random half of clusters 20-39 (a seeded mixture weight)."""
+    mix = gaussian_mixture(n, d, components, seed)
+    rng = Rng(member_seed)
+    lab = mix.labels
+
+    def uniform_over(clusters):
+        w = np.isin(lab, clusters).astype(np.float64)
+        return w / w.sum()
+
+    ga = np.empty((m, n))
+    gb = np.empty((m, n))
+    for q in range(m):
+        ga[q] = _normalise(uniform_over(_cluster_choice(rng, range(0, 20), 10)))
+    for q in range(m):
+        base = uniform_over(_cluster_choice(rng, range(0, 20), 10))
+        shift = uniform_over(_cluster_choice(rng, range(20, 40), 10))
+        gb[q] = _normalise(0.8 * base + 0.2 * shift)
+    return Config4(mix, ga, gb)
