@@ -454,6 +454,15 @@ __global__ void k_scale_vals(double* v, int64_t nnz, double scale) {
   if (e < nnz) v[e] = v[e] * scale;
 }
 
+// entries whose column lies within 256 rows of their row (layout order)
+__global__ void k_near_count(const int* __restrict__ offs, const int* __restrict__ cols, int n,
+                             unsigned long long* __restrict__ cnt) {
+  unsigned long long c = 0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    for (int p = offs[r]; p < offs[r + 1]; ++p) c += (unsigned)abs(cols[p] - r) <= 256u;
+  atomicAdd(cnt, c);
+}
+
 __global__ void k_to_float(const double* __restrict__ v, int64_t nnz, float* __restrict__ out) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e < nnz) out[e] = (float)v[e];
@@ -488,16 +497,20 @@ int rows_per_block(int gw) {  // rows covered by one CTA pass (8 warps)
 // Row blocks per CTA: kRowsPerCta (L1 reuse across consecutive blocks) unless that leaves fewer
 // than two CTAs per SM, in which case 1 (small, latency-bound problems such as config 0).
 template <typename S>
-int choose_rpc(int n, int gw, int groups) {
+int choose_rpc(int n, int gw, int groups, double near_frac = 1.0) {
   static const int forced = [] {
     const char* e = getenv("GS_RPC");
     return e ? atoi(e) : 0;
   }();
   if (forced == 1) return 1;
   if (forced > 1) return kRowsPerCta;
-  // rows of <= 64 bytes spread over several lanes (config 2's B = 8 fp64): consecutive row blocks
-  // share few L1 lines (kNN graphs in R^30), so short CTAs win by shrinking the tail wave
-  if (gw * (int)sizeof(S) <= 64 && gw * (int)sizeof(S) > 16) return 1;
+  // several lanes per row and fewer than 32 columns (the degree-sorted layout; configs 2 and 4:
+  // B = 8 and 16 fp64 on kNN graphs in R^30): consecutive row blocks share few L1 lines, so short
+  // CTAs win by shrinking the tail wave (config 2: 416 -> 351 us; config 4: 217 -> 151 us at 4e5)
+  if (gw < 32 && gw * (int)sizeof(S) > 16) return 1;
+  // graphs without index locality (kNN graphs in R^30: ~12% of entries within 256 rows in CM
+  // order, against ~50% on the swiss roll) get no L1 reuse between row blocks either
+  if (near_frac < 0.3) return 1;
   const int64_t ctas = (int64_t)groups * ((n + rows_per_block<S>(gw) * kRowsPerCta - 1) /
                                           (rows_per_block<S>(gw) * kRowsPerCta));
   return ctas < 2 * 148 ? 1 : kRowsPerCta;
@@ -546,7 +559,7 @@ struct Work {
   DevBuf<double> thr, errcol, part_err;
   DevBuf<int> active, gactive;
   DevBuf<gs_status> status;
-  int init(gs_ctx* ctx, int n_, int B_, bool want_err, int64_t ld_ = -1) {
+  int init(gs_ctx* ctx, int n_, int B_, bool want_err, int64_t ld_ = -1, const gs_filter* f = nullptr) {
     cudaStream_t s = ctx->stream;
     n = n_;
     B = B_;
@@ -555,7 +568,7 @@ struct Work {
     G = (B + GW - 1) / GW;
     Bpad = G * GW;
     lay = GW >= 32 ? 0 : 1;
-    rpc = choose_rpc<S>(n, GW, G);
+    rpc = choose_rpc<S>(n, GW, G, f ? f->lay[lay].near_frac : 1.0);
     tiles = (n + rows_per_block<S>(GW) * rpc - 1) / (rows_per_block<S>(GW) * rpc);
     const size_t len = (size_t)Bpad * (ld > 0 ? ld : 1);
     GS_CUDA(ctx, T[0].alloc(len, s));
@@ -765,7 +778,7 @@ int filter_apply_impl(gs_ctx* ctx, const gs_filter* f, const double* dX, double*
   const int n = f->scaled->n;
   cudaStream_t s = ctx->stream;
   Work<S> w;
-  GS_TRY(w.init(ctx, n, width, false));
+  GS_TRY(w.init(ctx, n, width, false, -1, f));
   gs_launch_begin(ctx, 1);
   k_pack<S><<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
   gs_launch_end(ctx, 1);
@@ -786,7 +799,7 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   const int n = f->scaled->n;
   cudaStream_t s = ctx->stream;
   Work<S> w;
-  GS_TRY(w.init(ctx, n, P, true));
+  GS_TRY(w.init(ctx, n, P, true, -1, f));
   // vertex weights in the filter's locality order and the engine precision
   DevBuf<S> aperm;
   GS_CUDA(ctx, aperm.alloc(n, s));
@@ -996,7 +1009,7 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   const int n = f->scaled->n;
   cudaStream_t s = ctx->stream;
   Work<S> w;
-  GS_TRY(w.init(ctx, n, m, true));
+  GS_TRY(w.init(ctx, n, m, true, -1, f));
   DevBuf<S> aperm;
   GS_CUDA(ctx, aperm.alloc(n, s));
   gs_launch_begin(ctx, 1);
@@ -1513,7 +1526,7 @@ int filter_apply_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, c
   const int nl = p->nl;
   cudaStream_t s = ctx->stream;
   Work<S> w;
-  GS_TRY(w.init(ctx, nl, width, false, (int64_t)nl + p->nh));
+  GS_TRY(w.init(ctx, nl, width, false, (int64_t)nl + p->nh, p->f));
   w.tiles = part_tiles<S>(p, w);
   Halo<S> h;
   GS_TRY(h.init(ctx, p, w.Bpad));
@@ -1542,7 +1555,7 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
   const int nl = p->nl;
   cudaStream_t s = ctx->stream;
   Work<S> w;
-  GS_TRY(w.init(ctx, nl, P, true, (int64_t)nl + p->nh));
+  GS_TRY(w.init(ctx, nl, P, true, (int64_t)nl + p->nh, p->f));
   w.tiles = part_tiles<S>(p, w);  // error partials: one per tile of the (up to) three row ranges
   GS_CUDA(ctx, w.part_err.alloc((size_t)(w.tiles ? w.tiles : 1) * w.Bpad, s));
   Halo<S> h;
@@ -1854,6 +1867,16 @@ extern "C" int gs_filter_create(gs_ctx* ctx, const gs_graph* L, int kind, double
       k_to_float<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(Ly.perm->vals, nnz, Ly.vals32);
       gs_launch_end(ctx, 1);
       if (cudaStreamSynchronize(s) != cudaSuccess) rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "fp32 copy failed");
+    }
+    if (!rc && nnz > 0) {  // index locality of this layout (choose_rpc)
+      DevBuf<unsigned long long> cnt;
+      unsigned long long h = 0;
+      if (cnt.alloc(1, s) == cudaSuccess && cudaMemsetAsync(cnt.get(), 0, sizeof h, s) == cudaSuccess) {
+        k_near_count<<<148 * 4, 256, 0, s>>>(Ly.perm->offs, Ly.perm->cols, Ly.perm->n, cnt.get());
+        if (cudaMemcpyAsync(&h, cnt.get(), sizeof h, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+            cudaStreamSynchronize(s) == cudaSuccess)
+          Ly.near_frac = (double)h / (double)nnz;
+      }
     }
   }
   if (rc) {

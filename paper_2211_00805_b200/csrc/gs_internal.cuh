@@ -71,6 +71,7 @@ struct gs_layout {
   int* order = nullptr;      // order[new] = old
   int* newpos = nullptr;     // newpos[old] = new
   float* vals32 = nullptr;   // fp32 copy of perm->vals (optional fp32 mode)
+  double near_frac = 1.0;    // fraction of entries within 256 rows of their row (L1 locality)
 };
 
 struct gs_filter {

@@ -78,9 +78,12 @@ struct Prec<float> {
 #ifndef GS_NARROW_VEC_BYTES
 #define GS_NARROW_VEC_BYTES 8
 #endif
+#ifndef GS_NARROW_MAX_BYTES
+#define GS_NARROW_MAX_BYTES 64  // widest row (GW * sizeof(S)) laid out as "narrow"
+#endif
 template <int GW, typename S>
 struct Lay {
-  static constexpr bool NARROW = GW * (int)sizeof(S) <= 64 && GW * (int)sizeof(S) > 16;
+  static constexpr bool NARROW = GW * (int)sizeof(S) <= GS_NARROW_MAX_BYTES && GW * (int)sizeof(S) > 16;
   static constexpr int VB = NARROW ? GS_NARROW_VEC_BYTES : 16;
   static constexpr int VEC = GW * (int)sizeof(S) >= VB ? (VB >= (int)sizeof(S) ? VB / (int)sizeof(S) : 1) : GW;
   static constexpr int LPR = GW / VEC;                 // lanes per row
