@@ -1,0 +1,181 @@
+"""kNN-graph benchmark driver (proj/src/bench.cpp:44-371): the paper's
+distance-ranking experiment on the device path.
+
+m clusters on a rotated swiss roll (make_swiss_roll, bench.cpp:59-100) -> alpha-decay kNN graph
+-> Laplacian -> heat filter -> geodesic Sinkhorn distances between all m(m-1)/2 pairs of cluster
+indicator distributions in ONE batched call -> Pearson / Spearman / precision@5 against the
+unrolled-spiral ground truth (bench.cpp:107-214). Only the `geodesic_sinkhorn` method runs here:
+the dense-Sinkhorn W1/W2 and Euler-Sinkhorn baselines are competitor methods.
+
+Draws follow geosink::Rng (rng.hpp:13-68) in the reference order; the random rotation is the
+Householder QR of a Gaussian matrix with R's diagonal made positive (numpy's LAPACK QR instead of
+Eigen's: the same Q up to rounding).
+"""
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List
+
+import numpy as np
+
+from . import geosink as gs
+from .rng import Rng
+
+
+@dataclass
+class KnnBenchConfig:  # bench.hpp:75-93
+    n_distributions: int = 15
+    samples_per_dist: int = 1000
+    noise_sigma: float = 3.0
+    ambient_dim: int = 10
+    seeds: List[int] = field(default_factory=lambda: [1])
+    k: int = 5
+    alpha: float = 40.0
+    kind: gs.LaplacianKind = gs.LaplacianKind.normalized
+    t: float = 20.0
+    degree: int = 100
+    sinkhorn: gs.SinkhornParams = field(default_factory=lambda: gs.SinkhornParams(500, 1e-6))
+    # bench-only deviation (as bench.py): run every pair to max_iter instead of raising
+    # Disconnected when a pair's marginal error stays above 0.5 for 50 sweeps
+    no_stagnation_abort: bool = False
+
+
+@dataclass
+class SwissRollSample:  # bench.hpp SwissRollSample
+    ambient: np.ndarray
+    intrinsic: np.ndarray
+    labels: np.ndarray
+    centers: np.ndarray
+
+
+def random_rotation(dim: int, rng: Rng) -> np.ndarray:
+    """bench.cpp:46-57."""
+    g = np.array([[rng.normal() for _ in range(dim)] for _ in range(dim)])
+    q, r = np.linalg.qr(g)
+    return q * np.where(np.diag(r) < 0.0, -1.0, 1.0)[None, :]
+
+
+def make_swiss_roll(m: int, per: int, noise: float, ambient_dim: int, seed: int) -> SwissRollSample:
+    """bench.cpp:59-100."""
+    if m < 1 or per < 1:
+        raise gs.Error(gs.errc.invalid_argument, "InvalidArgument: need at least one distribution and one sample")
+    if ambient_dim < 3:
+        raise gs.Error(gs.errc.invalid_argument, "InvalidArgument: ambient dimension must be >= 3")
+    if noise < 0.0:
+        raise gs.Error(gs.errc.invalid_argument, "InvalidArgument: noise sigma must be >= 0")
+    rng = Rng(seed)
+    centers = np.empty((m, 2))
+    for c in range(m):
+        centers[c, 0] = rng.uniform(1.5 * math.pi, 4.5 * math.pi)
+        centers[c, 1] = rng.uniform(0.0, 20.0)
+    n = m * per
+    intrinsic = np.empty((n, 2))
+    labels = np.repeat(np.arange(m), per).astype(np.int32)
+    flat = np.empty((n, 3))
+    for row in range(n):
+        c = labels[row]
+        s = centers[c, 0] + noise * rng.normal()
+        h = centers[c, 1] + noise * rng.normal()
+        intrinsic[row] = (s, h)
+        flat[row] = (s * math.cos(s), h, s * math.sin(s))
+    padded = np.zeros((n, ambient_dim))
+    padded[:, :3] = flat
+    rot = random_rotation(ambient_dim, rng)
+    return SwissRollSample(padded @ rot.T, intrinsic, labels, centers)
+
+
+def spiral_arclength(s: float) -> float:
+    """bench.cpp:102."""
+    return 0.5 * (s * math.sqrt(1.0 + s * s) + math.asinh(s))
+
+
+def ground_truth_distances(sample: SwissRollSample) -> np.ndarray:
+    """bench.cpp:104-122: distances between cluster centres on the unrolled spiral."""
+    un = np.array([[spiral_arclength(c[0]), c[1]] for c in sample.centers])
+    return np.sqrt(((un[:, None, :] - un[None, :, :]) ** 2).sum(-1))
+
+
+def _average_ranks(v: np.ndarray) -> np.ndarray:  # bench.cpp:128-146
+    order = sorted(range(v.size), key=lambda a: (v[a], a))
+    ranks = np.empty(v.size)
+    i = 0
+    while i < v.size:
+        j = i
+        while j + 1 < v.size and v[order[j + 1]] == v[order[i]]:
+            j += 1
+        for q in range(i, j + 1):
+            ranks[order[q]] = 0.5 * (i + j) + 1.0
+        i = j + 1
+    return ranks
+
+
+def _pearson(x: np.ndarray, y: np.ndarray) -> float:  # bench.cpp:148-155
+    xc, yc = x - x.mean(), y - y.mean()
+    den = np.linalg.norm(xc) * np.linalg.norm(yc)
+    if not den > 0.0:
+        raise gs.Error(gs.errc.degenerate_input, "DegenerateInput: constant input has no correlation")
+    return float(xc @ yc / den)
+
+
+def rank_metrics(pred: np.ndarray, truth: np.ndarray) -> Dict[str, float]:
+    """bench.cpp:161-214: Pearson and Spearman over the upper triangle, row-wise precision@5."""
+    m = pred.shape[0]
+    iu = np.triu_indices(m, 1)
+    up, ut = pred[iu], truth[iu]
+    k = min(5, m - 1)
+
+    def row_knn(mat, i):
+        idx = [j for j in range(m) if j != i]
+        return sorted(idx, key=lambda a: (mat[i, a], a))[:k]
+
+    hits = sum(len(set(row_knn(pred, i)) & set(row_knn(truth, i))) for i in range(m))
+    return {"pearson": _pearson(up, ut), "spearman": _pearson(_average_ranks(up), _average_ranks(ut)),
+            "p_at_5": hits / (m * k)}
+
+
+def knn_benchmark(config: KnnBenchConfig = KnnBenchConfig(), ctx=None) -> dict:
+    """bench.cpp:246-371 for the geodesic_sinkhorn method; wall times per phase as the reference
+    reports them (graph, prepare, distance)."""
+    if config.n_distributions < 3:
+        raise gs.Error(gs.errc.invalid_argument, "InvalidArgument: need at least three distributions")
+    m = config.n_distributions
+    per_seed, means = [], {"pearson": 0.0, "spearman": 0.0, "p_at_5": 0.0, "graph": 0.0,
+                           "prepare": 0.0, "distance": 0.0}
+    for seed in config.seeds:
+        sample = make_swiss_roll(m, config.samples_per_dist, config.noise_sigma, config.ambient_dim, seed)
+        truth = ground_truth_distances(sample)
+        n = sample.ambient.shape[0]
+        t0 = time.perf_counter()
+        A = gs.knn_alpha_decay_graph(sample.ambient, config.k, config.alpha, ctx=ctx)
+        lap = gs.laplacian(A, config.kind)
+        t_graph = time.perf_counter() - t0
+        groups = [np.flatnonzero(sample.labels == c) for c in range(m)]
+        mus, nus = [], []
+        for i in range(m):
+            for j in range(i + 1, m):
+                mus.append(gs.Distribution.indicator(n, groups[i]))
+                nus.append(gs.Distribution.indicator(n, groups[j]))
+        a = np.full(n, 1.0 / n)
+        t1 = time.perf_counter()
+        filt = gs.HeatFilter(lap, config.t, config.degree)
+        t_prep = time.perf_counter() - t1
+        t2 = time.perf_counter()
+        runs = gs.geodesic_sinkhorn_batch(filt, mus, nus, a, config.sinkhorn,
+                                          no_stagnation_abort=config.no_stagnation_abort)
+        t_dist = time.perf_counter() - t2
+        d = np.zeros((m, m))
+        q = 0
+        for i in range(m):
+            for j in range(i + 1, m):
+                d[i, j] = d[j, i] = runs[q].cost
+                q += 1
+        rep = rank_metrics(d, truth)
+        rep.update(graph=t_graph, prepare=t_prep, distance=t_dist)
+        per_seed.append({"seed": seed, "truth": truth, "distances": d, "report": rep,
+                         "iterations": [r.iterations for r in runs]})
+        for key in means:
+            means[key] += rep[key] / len(config.seeds)
+    means["total"] = means["graph"] + means["prepare"] + means["distance"]
+    return {"per_seed": per_seed, "mean_report": {"geodesic_sinkhorn": means}}

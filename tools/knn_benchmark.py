@@ -1,0 +1,14 @@
+"""Runs the paper's kNN distance-ranking benchmark (bench.cpp:246-371 defaults) on the device."""
+import json
+import sys
+
+sys.path.insert(0, ".")
+from paper_2211_00805_b200 import knn_bench as kb  # noqa: E402
+
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+seeds = [int(s) for s in args] or [1, 2, 3]
+res = kb.knn_benchmark(kb.KnnBenchConfig(seeds=seeds,
+                                         no_stagnation_abort="--no-stagnation-abort" in sys.argv))
+rep = res["mean_report"]["geodesic_sinkhorn"]
+iters = [max(s["iterations"]) for s in res["per_seed"]]
+print(json.dumps({"method": "geodesic_sinkhorn", "seeds": seeds, "max_iterations": iters, **rep}))
