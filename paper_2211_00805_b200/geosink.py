@@ -806,6 +806,34 @@ def barycentric_distance(filter: HeatFilter, family_t: DistributionFamily,
     return geodesic_sinkhorn(filter, bt.barycenter, bc.barycenter, a, params).cost
 
 
+def expected_barycenter_effect(filter: HeatFilter, family_t: DistributionFamily,
+                               family_c: DistributionFamily, features, a,
+                               params: SinkhornParams = SinkhornParams()) -> np.ndarray:
+    """barycenter.cpp:108-119: features^T (barycenter_t - barycenter_c); features n x d."""
+    F = _f64(features).reshape(filter.size(), -1)
+    bt = sinkhorn_barycenter(filter, family_t, a, params)
+    bc = sinkhorn_barycenter(filter, family_c, a, params)
+    return F.T @ (bt.barycenter.weights - bc.barycenter.weights)
+
+
+def tv_baseline_effect(family_t: DistributionFamily, family_c: DistributionFamily,
+                       features) -> np.ndarray:
+    """barycenter.cpp:121-135: features^T (mixture_t - mixture_c), mixtures alpha-weighted."""
+    F = _f64(features)
+    n = F.shape[0]
+    F = F.reshape(n, -1)
+    family_t.validate(n)
+    family_c.validate(n)
+
+    def mixture(fam):
+        mix = np.zeros(n)
+        for al, mem in zip(fam.resolved_alphas(), fam.members):
+            mix = mix + al * mem.weights
+        return mix
+
+    return F.T @ (mixture(family_t) - mixture(family_c))
+
+
 # ---------------------------------------------------------------------------------- next (§8(f))
 def plan_rows(result: TransportResult, filter: HeatFilter, a, rows) -> np.ndarray:
     """plan_row (transport.cpp:314-324) for several rows at once: (len(rows), n) array."""

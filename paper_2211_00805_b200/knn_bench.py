@@ -179,3 +179,72 @@ def knn_benchmark(config: KnnBenchConfig = KnnBenchConfig(), ctx=None) -> dict:
             means[key] += rep[key] / len(config.seeds)
     means["total"] = means["graph"] + means["prepare"] + means["distance"]
     return {"per_seed": per_seed, "mean_report": {"geodesic_sinkhorn": means}}
+
+
+# ---------------------------------------------------------------------------------------------
+# Expected-barycenter-effect experiment (bench.cpp:483-540; PAPER.md "Barycentric distance")
+# ---------------------------------------------------------------------------------------------
+@dataclass
+class EbeConfig:  # bench.hpp:152-167
+    has_outlier: bool = True
+    outlier_mean: float = -60.0
+    treatment_shift: float = 5.0
+    control_members: int = 10
+    treated_members: int = 10  # the outlier replaces one clean member
+    samples_per_member: int = 500
+    dim: int = 1
+    seed: int = 1
+    k: int = 5
+    alpha: float = 40.0
+    kind: gs.LaplacianKind = gs.LaplacianKind.normalized
+    t: float = 3.0
+    degree: int = 36
+    sinkhorn: gs.SinkhornParams = field(default_factory=lambda: gs.SinkhornParams(60, 1e-6))
+
+
+def make_ebe_points(config: EbeConfig) -> np.ndarray:
+    """bench.cpp:493-509: member blocks of N(shift e_0, I) samples, control first."""
+    rng = Rng(config.seed)
+    per, members = config.samples_per_member, config.control_members + config.treated_members
+    pts = np.empty((members * per, config.dim))
+    shifts = [0.0] * config.control_members
+    clean = config.treated_members - (1 if config.has_outlier else 0)
+    shifts += [config.treatment_shift] * clean
+    if config.has_outlier:
+        shifts.append(config.outlier_mean)
+    for mbr, shift in enumerate(shifts):
+        for q in range(per):
+            for d in range(config.dim):
+                pts[mbr * per + q, d] = (shift if d == 0 else 0.0) + rng.normal()
+    return pts
+
+
+def ebe_experiment(config: EbeConfig = EbeConfig(), ctx=None) -> dict:
+    """bench.cpp:483-540: heat-kernel barycenter effect tau and the TV baseline tau_tv."""
+    if not (config.control_members >= 1 and config.treated_members >= 1):
+        raise gs.Error(gs.errc.invalid_argument, "InvalidArgument: need at least one member per family")
+    if config.samples_per_member < 2:
+        raise gs.Error(gs.errc.invalid_argument, "InvalidArgument: need at least two samples")
+    if config.dim < 1:
+        raise gs.Error(gs.errc.invalid_argument, "InvalidArgument: dimension must be >= 1")
+    if config.has_outlier and config.treated_members < 2:
+        raise gs.Error(gs.errc.invalid_argument, "InvalidArgument: outlier needs at least two treated members")
+    pts = make_ebe_points(config)
+    n, per = pts.shape[0], config.samples_per_member
+    lap = gs.laplacian(gs.knn_alpha_decay_graph(pts, config.k, config.alpha, ctx=ctx), config.kind)
+    filt = gs.HeatFilter(lap, config.t, config.degree)
+    a = np.full(n, 1.0 / n)
+
+    def member(idx):
+        return gs.Distribution.indicator(n, range(idx * per, (idx + 1) * per))
+
+    members_total = config.control_members + config.treated_members
+    control = gs.DistributionFamily([member(c) for c in range(config.control_members)], label="control")
+    treated = gs.DistributionFamily([member(c) for c in range(config.control_members, members_total)],
+                                    label="treated")
+    bt = gs.sinkhorn_barycenter(filt, treated, a, config.sinkhorn)
+    bc = gs.sinkhorn_barycenter(filt, control, a, config.sinkhorn)
+    return {"tau": pts.T @ (bt.barycenter.weights - bc.barycenter.weights),
+            "tau_tv": gs.tv_baseline_effect(treated, control, pts), "graph_size": n,
+            "converged_treated": bt.converged, "converged_control": bc.converged,
+            "barycenters": (bt.barycenter.weights, bc.barycenter.weights), "points": pts}

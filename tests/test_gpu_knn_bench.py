@@ -53,3 +53,31 @@ def test_knn_benchmark_matches_oracle(ctx, m, per, noise, t, seed):
             q += 1
     rep = res["mean_report"]["geodesic_sinkhorn"]
     assert -1.0 <= rep["spearman"] <= 1.0 and 0.0 <= rep["p_at_5"] <= 1.0
+
+
+def test_ebe_experiment_matches_oracle(ctx):
+    """bench.cpp:483-540 on the device: the barycenters (and so tau) within 1e-9 of the oracle's;
+    the heat-kernel effect is robust to the outlier member where the TV baseline is not."""
+    from paper_2211_00805_b200 import knn_bench as kb
+    cfg = kb.EbeConfig(samples_per_member=60)
+    res = kb.ebe_experiment(cfg)
+    pts = res["points"]
+    n, per = pts.shape[0], cfg.samples_per_member
+    A = po.knn_graph(pts, cfg.k, 0, cfg.alpha)[0]
+    L, lam, _ = po.laplacian(A, int(cfg.kind))
+    fo = po.Filter(L, int(cfg.kind), lam, cfg.t, cfg.degree)
+
+    def fam(lo, hi):
+        out = []
+        for c in range(lo, hi):
+            w = np.zeros(n)
+            w[c * per:(c + 1) * per] = 1.0
+            out.append(w / w.sum())
+        return np.array(out)
+
+    a = np.full(n, 1.0 / n)
+    bt = po.barycenter(fo, a, fam(10, 20), None, cfg.sinkhorn.max_iter, cfg.sinkhorn.tol)["barycenter"]
+    bc = po.barycenter(fo, a, fam(0, 10), None, cfg.sinkhorn.max_iter, cfg.sinkhorn.tol)["barycenter"]
+    tau_ref = pts.T @ (bt - bc)
+    assert abs(res["tau"][0] - tau_ref[0]) <= 1e-9 * abs(tau_ref[0])
+    assert abs(res["tau"][0] - cfg.treatment_shift) < abs(res["tau_tv"][0] - cfg.treatment_shift)
