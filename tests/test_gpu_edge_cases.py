@@ -1,0 +1,102 @@
+"""Edge cases against the oracle: single-vertex graph, empty batches / widths, point masses,
+identical marginals, and a batch spanning two 64-column groups (the engine's grouped layout)."""
+import numpy as np
+import pytest
+
+import pyoracle as po
+from helpers import acceptance_graph, engine_filter, oracle_filter, random_distribution
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gs(ctx):
+    import paper_2211_00805_b200 as gs
+    return gs
+
+
+def _outcome(fn):
+    try:
+        return fn(), None
+    except Exception as e:  # engine Error or OracleError: compare the status / message
+        code = getattr(e, "status", None)
+        if code is None and hasattr(e, "code"):
+            code = int(e.code) + 1
+        return None, code
+
+
+def test_single_vertex_graph(gs):
+    f, lap = engine_filter(np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0), 1, 0, 1.0, 30)
+    fo = oracle_filter(np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0), 1, 0, 1.0, 30)
+    assert lap.lambda_max_bound == po.laplacian(po.from_triplets(1, [], [], []), 0)[1]
+    x = np.array([0.75])
+    assert np.array_equal(f.apply(x), fo.apply(x))
+    one = np.array([1.0])
+    res, err = _outcome(lambda: gs.geodesic_sinkhorn(f, gs.Distribution(one), gs.Distribution(one), one,
+                                                     gs.SinkhornParams(20, 1e-12)))
+    ref, ref_err = _outcome(lambda: po.sinkhorn_batch(fo, one, one[None], one[None], 20, 1e-12,
+                                                      single_style=True))
+    assert err == ref_err
+    if err is None:
+        assert res.iterations == ref["iterations"][0] and np.array_equal(res.v, ref["v"][0])
+
+
+def test_empty_batch_and_zero_width(gs):
+    n = 40
+    r, c, v = acceptance_graph(n, 3)
+    f, _ = engine_filter(r, c, v, n, 1, 1.0, 20)
+    assert gs.geodesic_sinkhorn_batch(f, [], [], np.full(n, 1.0 / n)) == []
+    assert f.apply(np.zeros((n, 0))).shape == (n, 0)
+
+
+@pytest.mark.parametrize("src,dst", [(0, 0), (0, 7), (3, 29)])
+def test_point_masses(gs, src, dst):
+    """Delta marginals (Distribution::indicator of one vertex): same outcome as the oracle."""
+    n = 30
+    r, c, v = acceptance_graph(n, 9)
+    f, _ = engine_filter(r, c, v, n, 1, 2.0, 40)
+    fo = oracle_filter(r, c, v, n, 1, 2.0, 40)
+    a = np.full(n, 1.0 / n)
+    mu, nu = np.zeros(n), np.zeros(n)
+    mu[src], nu[dst] = 1.0, 1.0
+    params = gs.SinkhornParams(400, 1e-8)
+    res, err = _outcome(lambda: gs.geodesic_sinkhorn_batch(f, [gs.Distribution(mu)], [gs.Distribution(nu)], a, params))
+    ref, ref_err = _outcome(lambda: po.sinkhorn_batch(fo, a, mu[None], nu[None], 400, 1e-8))
+    assert err == ref_err
+    if err is None:
+        assert res[0].iterations == ref["iterations"][0]
+        assert np.array_equal(res[0].v, ref["v"][0]) and np.array_equal(res[0].w, ref["w"][0])
+
+
+def test_identical_marginals(gs):
+    n = 60
+    r, c, v = acceptance_graph(n, 4)
+    f, _ = engine_filter(r, c, v, n, 0, 1.0, 30)
+    fo = oracle_filter(r, c, v, n, 0, 1.0, 30)
+    from paper_2211_00805_b200.rng import Rng
+    mu = random_distribution(n, Rng(5))
+    a = np.full(n, 1.0 / n)
+    res = gs.geodesic_sinkhorn_batch(f, [gs.Distribution(mu)], [gs.Distribution(mu)], a, gs.SinkhornParams(300, 1e-10))
+    ref = po.sinkhorn_batch(fo, a, mu[None], mu[None], 300, 1e-10)
+    assert res[0].iterations == ref["iterations"][0]
+    assert np.array_equal(res[0].v, ref["v"][0])
+
+
+def test_two_column_groups(gs):
+    """P = 70 pairs: two 64-column groups with masks retiring converged pairs per group."""
+    n = 150
+    r, c, v = acceptance_graph(n, 1001)
+    f, _ = engine_filter(r, c, v, n, 1, 1.0, 30)
+    fo = oracle_filter(r, c, v, n, 1, 1.0, 30)
+    from paper_2211_00805_b200.rng import Rng
+    rng = Rng(70)
+    mus = [random_distribution(n, rng) for _ in range(70)]
+    nus = [random_distribution(n, rng) for _ in range(70)]
+    a = np.full(n, 1.0 / n)
+    res = gs.geodesic_sinkhorn_batch(f, [gs.Distribution(m) for m in mus], [gs.Distribution(x) for x in nus], a,
+                                     gs.SinkhornParams(300, 1e-9))
+    ref = po.sinkhorn_batch(fo, a, np.array(mus), np.array(nus), 300, 1e-9)
+    assert len(set(int(i) for i in ref["iterations"])) > 1
+    for p in range(70):
+        assert res[p].iterations == ref["iterations"][p]
+        assert np.array_equal(res[p].v, ref["v"][p]) and np.array_equal(res[p].w, ref["w"][p])
