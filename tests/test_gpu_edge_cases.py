@@ -100,3 +100,31 @@ def test_two_column_groups(gs):
     for p in range(70):
         assert res[p].iterations == ref["iterations"][p]
         assert np.array_equal(res[p].v, ref["v"][p]) and np.array_equal(res[p].w, ref["w"][p])
+
+
+@pytest.mark.parametrize("max_iter", [1, 2, 7, 13])
+@pytest.mark.parametrize("graph", ["0", "1"])
+def test_max_iter_boundaries(gs, monkeypatch, max_iter, graph):
+    """Sweeps are replayed two at a time as a CUDA graph: an odd max_iter ends mid-replay, and
+    the extra sweep must change nothing (iterations, v/w from the right ping-pong buffer)."""
+    monkeypatch.setenv("GS_GRAPH", graph)
+    n = 80
+    r, c, v = acceptance_graph(n, 21)
+    f, _ = engine_filter(r, c, v, n, 1, 0.6, 30)
+    fo = oracle_filter(r, c, v, n, 1, 0.6, 30)
+    from paper_2211_00805_b200.rng import Rng
+    rng = Rng(3)
+    mus = [random_distribution(n, rng) for _ in range(3)]
+    nus = [random_distribution(n, rng) for _ in range(3)]
+    a = np.full(n, 1.0 / n)
+    res = gs.geodesic_sinkhorn_batch(f, [gs.Distribution(m) for m in mus], [gs.Distribution(x) for x in nus], a,
+                                     gs.SinkhornParams(max_iter, 1e-14))
+    ref = po.sinkhorn_batch(fo, a, np.array(mus), np.array(nus), max_iter, 1e-14)
+    for p in range(3):
+        assert res[p].iterations == ref["iterations"][p] == max_iter
+        assert np.array_equal(res[p].v, ref["v"][p]) and np.array_equal(res[p].w, ref["w"][p])
+    fam = gs.DistributionFamily([gs.Distribution(m) for m in mus])
+    bary = gs.sinkhorn_barycenter(f, fam, a, gs.SinkhornParams(max_iter, 1e-14))
+    bref = po.barycenter(fo, a, np.array(mus), None, max_iter, 1e-14)
+    assert bary.iterations == bref["iterations"]
+    assert np.abs(bary.barycenter.weights - bref["barycenter"]).max() <= 1e-12 * bref["barycenter"].max()
