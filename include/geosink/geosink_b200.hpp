@@ -341,6 +341,7 @@ class EulerHeat {
   int size() const { return n_; }
   int steps() const { return steps_; }
   double time() const { return t_; }
+  gs_euler* handle() const { return h_.get(); }
 
  private:
   int n_ = 0, steps_ = 1;
@@ -463,6 +464,45 @@ inline std::vector<TransportResult> geodesic_sinkhorn_batch(const HeatFilter& fi
                                                             const std::vector<double>& a,
                                                             const SinkhornParams& params = {}) {
   return detail::sinkhorn(filter, mus, nus, a, params, 0);
+}
+
+// transport.cpp:257-269: Sinkhorn over EulerHeat (the competitor of the Chebyshev filter)
+inline std::vector<TransportResult> euler_sinkhorn_batch(const EulerHeat& euler, const std::vector<Distribution>& mus,
+                                                         const std::vector<Distribution>& nus,
+                                                         const std::vector<double>& a,
+                                                         const SinkhornParams& params = {}, int flags = 0) {
+  if (mus.size() != nus.size()) detail::fail(errc::size_mismatch, "SizeMismatch", "pair lists differ in length");
+  const int n = euler.size(), P = static_cast<int>(mus.size());
+  if (P == 0) return {};
+  std::vector<double> M(size_t(P) * n), N(M.size()), v(M.size()), w(M.size());
+  for (int q = 0; q < P; ++q) {
+    if ((int)mus[q].size() != n || (int)nus[q].size() != n)
+      detail::fail(errc::length_mismatch, "LengthMismatch", "distributions must live on the filter's graph");
+    std::copy(mus[q].weights.begin(), mus[q].weights.end(), M.begin() + size_t(q) * n);
+    std::copy(nus[q].weights.begin(), nus[q].weights.end(), N.begin() + size_t(q) * n);
+  }
+  std::vector<double> cost(P), kl(P), err(P);
+  std::vector<int> it(P), conv(P);
+  detail::check(gs_euler_sinkhorn(detail::ctx(), euler.handle(), a.data(), M.data(), N.data(), P, params.max_iter,
+                                  params.tol, flags, GS_MEM_HOST, v.data(), w.data(), cost.data(), kl.data(),
+                                  it.data(), conv.data(), err.data(), nullptr, nullptr));
+  std::vector<TransportResult> out(P);
+  for (int q = 0; q < P; ++q) {
+    out[q].v.assign(v.begin() + size_t(q) * n, v.begin() + size_t(q + 1) * n);
+    out[q].w.assign(w.begin() + size_t(q) * n, w.begin() + size_t(q + 1) * n);
+    out[q].cost = cost[q];
+    out[q].kl = kl[q];
+    out[q].lambda = 4.0 * euler.time();
+    out[q].iterations = it[q];
+    out[q].converged = conv[q] != 0;
+    out[q].marginal_error = err[q];
+  }
+  return out;
+}
+
+inline TransportResult euler_sinkhorn(const EulerHeat& euler, const Distribution& mu, const Distribution& nu,
+                                      const std::vector<double>& a, const SinkhornParams& params = {}) {
+  return euler_sinkhorn_batch(euler, {mu}, {nu}, a, params, GS_FLAG_SINGLE)[0];
 }
 
 // ---- next: plan rows, graph file IO ---------------------------------------------

@@ -212,6 +212,15 @@ const gs_graph* gs_euler_system(const gs_euler* e); /* I + (t/steps) L, caller's
 int gs_euler_apply(gs_ctx* ctx, const gs_euler* e, const double* X, double* Y, int width, int mem,
                    int* iters_out);
 
+/* euler_sinkhorn[_batch] (transport.cpp:257-269): sinkhorn_many over EulerHeat. Arguments as
+ * gs_sinkhorn; converged pairs leave the lockstep-CG batch after every sweep, as in the
+ * reference's compaction (the CG couples the columns of a batch). */
+int gs_euler_sinkhorn(gs_ctx* ctx, const gs_euler* e, const double* a, const double* mus,
+                      const double* nus, int P, int max_iter, double tol, int flags, int mem,
+                      double* out_v, double* out_w, double* out_cost, double* out_kl,
+                      int* out_iters, int* out_conv, double* out_err, int* fail_pair,
+                      int* fail_sweep);
+
 /* ---- seeded RNG (rng.hpp:13-68), host-side ---------------------------------------------- */
 typedef struct gs_rng gs_rng;
 gs_rng* gs_rng_create(uint64_t seed);

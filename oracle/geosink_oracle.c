@@ -801,12 +801,25 @@ static int validate_distribution(const double* w, int n) {
 }
 
 /* transport.cpp:30-38 (filter_checked) on the n x B row-major block `in`; a-weighted */
-static int apply_weighted(const go_csr* S, const double* b, int degree, const double* a,
-                          const double* in, double* tmp, double* out, int n, int B,
-                          const char* msg) {
+/* the heat operator of sinkhorn_many (transport.cpp:144, template <class Op>): the Chebyshev
+ * filter or EulerHeat, applied to a row-major n x B block */
+typedef struct {
+  const go_csr* S;  /* filter: scaled Laplacian; Euler: the system I + (t/steps) L */
+  const double* b;  /* filter coefficients (NULL for Euler) */
+  int degree;       /* filter degree, or Euler steps */
+} heat_op;
+
+static int op_apply(const heat_op* op, const double* x, double* y, int B) {
+  if (op->b) return go_filter_apply(op->S, op->b, op->degree, x, y, B);
+  return go_euler_apply(op->S, op->degree, x, y, B, NULL);
+}
+
+static int apply_weighted(const heat_op* op, const double* a, const double* in, double* tmp,
+                          double* out, int n, int B, const char* msg) {
   for (int i = 0; i < n; ++i)
     for (int c = 0; c < B; ++c) tmp[(size_t)i * B + c] = a[i] * in[(size_t)i * B + c];
-  go_filter_apply(S, b, degree, tmp, out, B);
+  const int rc = op_apply(op, tmp, out, B);
+  if (rc) return rc;
   for (int c = 0; c < B; ++c) {
     double mx = 0.0, mn = INFINITY;
     for (int i = 0; i < n; ++i) {
@@ -827,12 +840,12 @@ static double weighted_log_sum(const double* a, const double* mu, const double* 
   return acc;
 }
 
-int go_sinkhorn_batch(const go_csr* S, const double* b, int degree, double t, const double* a,
-                      const double* mus, const double* nus, int P, int max_iter, double tol,
-                      int flags, int single_style, double* out_v, double* out_w,
-                      double* out_cost, double* out_kl, int* out_iters, int* out_conv,
-                      double* out_err, int* fail_info) {
-  const int n = S->n;
+static int sinkhorn_many(const heat_op* op, double t, const double* a, const double* mus,
+                         const double* nus, int P, int max_iter, double tol, int flags,
+                         int single_style, double* out_v, double* out_w, double* out_cost,
+                         double* out_kl, int* out_iters, int* out_conv, double* out_err,
+                         int* fail_info) {
+  const int n = op->S->n;
   if (fail_info) {
     fail_info[0] = -1;
     fail_info[1] = 0;
@@ -873,14 +886,14 @@ int go_sinkhorn_batch(const go_csr* S, const double* b, int degree, double t, co
       N[(size_t)i * P + p] = nus[(size_t)p * n + i];
       W[(size_t)i * P + p] = 1.0;
     }
-  int rc = apply_weighted(S, b, degree, a, W, tmp, phi, n, na, knp);
+  int rc = apply_weighted(op, a, W, tmp, phi, n, na, knp);
   for (int it = 1; rc == 0 && it <= max_iter && na > 0; ++it) {
     const int B = na;
     for (size_t e = 0; e < (size_t)n * B; ++e) V[e] = M[e] / fmax(phi[e], K_FLOOR);
-    rc = apply_weighted(S, b, degree, a, V, tmp, psi, n, B, knp);
+    rc = apply_weighted(op, a, V, tmp, psi, n, B, knp);
     if (rc) break;
     for (size_t e = 0; e < (size_t)n * B; ++e) W[e] = N[e] / fmax(psi[e], K_FLOOR);
-    rc = apply_weighted(S, b, degree, a, W, tmp, phi, n, B, knp);
+    rc = apply_weighted(op, a, W, tmp, phi, n, B, knp);
     if (rc) break;
     /* transport.cpp:184-226: per-column L1 errors, finalisation, stagnation, compaction */
     int* keep = (int*)malloc((size_t)B * sizeof(int));
@@ -958,6 +971,28 @@ int go_sinkhorn_batch(const go_csr* S, const double* b, int degree, double t, co
   return rc;
 }
 
+
+int go_sinkhorn_batch(const go_csr* S, const double* b, int degree, double t, const double* a,
+                      const double* mus, const double* nus, int P, int max_iter, double tol,
+                      int flags, int single_style, double* out_v, double* out_w,
+                      double* out_cost, double* out_kl, int* out_iters, int* out_conv,
+                      double* out_err, int* fail_info) {
+  const heat_op op = {S, b, degree};
+  return sinkhorn_many(&op, t, a, mus, nus, P, max_iter, tol, flags, single_style, out_v, out_w,
+                       out_cost, out_kl, out_iters, out_conv, out_err, fail_info);
+}
+
+/* transport.cpp:257-269: euler_sinkhorn[_batch] = sinkhorn_single / sinkhorn_many over EulerHeat */
+int go_euler_sinkhorn_batch(const go_csr* system, int steps, double t, const double* a,
+                            const double* mus, const double* nus, int P, int max_iter, double tol,
+                            int flags, int single_style, double* out_v, double* out_w,
+                            double* out_cost, double* out_kl, int* out_iters, int* out_conv,
+                            double* out_err, int* fail_info) {
+  const heat_op op = {system, NULL, steps};
+  return sinkhorn_many(&op, t, a, mus, nus, P, max_iter, tol, flags, single_style, out_v, out_w,
+                       out_cost, out_kl, out_iters, out_conv, out_err, fail_info);
+}
+
 /* ------------------------------------------------------------------------------------------
  * Barycenter: proj/src/barycenter.cpp:45-99
  * ---------------------------------------------------------------------------------------- */
@@ -1014,10 +1049,11 @@ int go_barycenter(const go_csr* S, const double* b, int degree, const double* a,
   *out_iters = 0;
   *out_conv = 0;
   *out_err = INFINITY;
-  int rc = apply_weighted(S, b, degree, a, W, tmp, phi, n, m, knp);
+  const heat_op op = {S, b, degree};
+  int rc = apply_weighted(&op, a, W, tmp, phi, n, m, knp);
   for (int it = 1; rc == 0 && it <= max_iter; ++it) {
     for (size_t e = 0; e < (size_t)n * m; ++e) V[e] = Mb[e] / fmax(phi[e], K_FLOOR);
-    rc = apply_weighted(S, b, degree, a, V, tmp, psi, n, m, knp);
+    rc = apply_weighted(&op, a, V, tmp, psi, n, m, knp);
     if (rc) break;
     /* barycenter.cpp:75-82: log-domain geometric mean, member order, floor/ceil clamp */
     double mx = -INFINITY;
@@ -1043,7 +1079,7 @@ int go_barycenter(const go_csr* S, const double* b, int degree, const double* a,
     for (int i = 0; i < n; ++i)
       for (int c = 0; c < m; ++c)
         W[(size_t)i * m + c] = bary[i] / fmax(psi[(size_t)i * m + c], K_FLOOR);
-    rc = apply_weighted(S, b, degree, a, W, tmp, phi, n, m, knp);
+    rc = apply_weighted(&op, a, W, tmp, phi, n, m, knp);
     if (rc) break;
     double err = 0.0;
     for (int c = 0; c < m; ++c) {

@@ -98,6 +98,13 @@ int go_sinkhorn_batch(const go_csr* scaled, const double* coeffs, int degree, do
                       double* out_cost, double* out_kl, int* out_iters, int* out_conv,
                       double* out_err, int* fail_info);
 
+/* transport.cpp:257-269: the same batch over EulerHeat (system from go_euler_system) */
+int go_euler_sinkhorn_batch(const go_csr* system, int steps, double t, const double* a,
+                            const double* mus, const double* nus, int P, int max_iter, double tol,
+                            int flags, int single_style, double* out_v, double* out_w,
+                            double* out_cost, double* out_kl, int* out_iters, int* out_conv,
+                            double* out_err, int* fail_info);
+
 /* barycenter.cpp:45-99. members: m contiguous n-vectors; alphas (m) or NULL for uniform.
  * out_V/out_W: m contiguous n-vectors. */
 int go_barycenter(const go_csr* scaled, const double* coeffs, int degree, const double* a,

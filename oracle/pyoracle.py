@@ -86,6 +86,9 @@ def _declare(L):
     L.go_filter_apply.argtypes = [C.POINTER(go_csr), _dp, C.c_int, _dp, _dp, C.c_int]
     L.go_euler_system.argtypes = [C.POINTER(go_csr), C.c_double, C.c_int, C.POINTER(go_csr)]
     L.go_euler_apply.argtypes = [C.POINTER(go_csr), C.c_int, _dp, _dp, C.c_int, C.POINTER(C.c_int)]
+    L.go_euler_sinkhorn_batch.argtypes = [C.POINTER(go_csr), C.c_int, C.c_double, _dp, _dp, _dp,
+                                          C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, _dp,
+                                          _dp, _dp, _dp, _ip, _ip, _dp, _ip]
     L.go_sinkhorn_batch.argtypes = [C.POINTER(go_csr), _dp, C.c_int, C.c_double, _dp, _dp, _dp,
                                     C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, _dp, _dp,
                                     _dp, _dp, _ip, _ip, _dp, _ip]
@@ -307,6 +310,27 @@ def euler_apply(system: CSR, steps: int, X: np.ndarray):
     s = system._struct()
     _check(lib().go_euler_apply(C.byref(s), int(steps), X, Y, width, C.byref(it)))
     return Y, it.value
+
+
+def euler_sinkhorn_batch(system: CSR, steps: int, t: float, a, mus, nus, max_iter=500, tol=1e-6,
+                         flags=0, single_style=False, L=None):
+    """transport.cpp:257-269: sinkhorn_many over EulerHeat (system from euler_system)."""
+    L = L or lib()
+    mus = np.ascontiguousarray(np.atleast_2d(mus), np.float64)
+    nus = np.ascontiguousarray(np.atleast_2d(nus), np.float64)
+    a = np.ascontiguousarray(a, np.float64)
+    P, n = mus.shape
+    v, w = np.zeros((P, n)), np.zeros((P, n))
+    cost, kl, err = np.zeros(P), np.zeros(P), np.zeros(P)
+    iters, conv = np.zeros(P, np.int32), np.zeros(P, np.int32)
+    fail_info = np.zeros(2, np.int32)
+    s = system._struct()
+    rc = L.go_euler_sinkhorn_batch(C.byref(s), int(steps), float(t), a, mus, nus, P, max_iter, tol,
+                                   flags, int(single_style), v, w, cost, kl, iters, conv, err,
+                                   fail_info)
+    _check(rc, L)
+    return dict(v=v, w=w, cost=cost, kl=kl, iterations=iters, converged=conv.astype(bool),
+                marginal_error=err)
 
 
 def sinkhorn_batch(f: Filter, a, mus, nus, max_iter=500, tol=1e-6, flags=0, single_style=False,

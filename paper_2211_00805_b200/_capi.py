@@ -92,6 +92,8 @@ SIGNATURES = {
     "gs_euler_destroy": (None, [_vp]),
     "gs_euler_system": (_vp, [_vp]),
     "gs_euler_apply": (_i, [_vp, _vp, _vp, _vp, _i, _i, _pi]),
+    "gs_euler_sinkhorn": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _d, _i, _i, _vp, _vp, _vp, _vp,
+                               _vp, _vp, _vp, _pi, _pi]),
     "gs_rng_create": (_vp, [C.c_uint64]),
     "gs_rng_destroy": (None, [_vp]),
     "gs_rng_bits": (C.c_uint64, [_vp]),

@@ -2009,23 +2009,7 @@ extern "C" int gs_sinkhorn(gs_ctx* ctx, const gs_filter* f, const double* a, con
   GS_TRY(stage_in(ctx, bmu, mus, (size_t)P * n, mem, &dmu));
   GS_TRY(stage_in(ctx, bnu, nus, (size_t)P * n, mem, &dnu));
   GS_TRY(stage_in(ctx, ba, a, (size_t)n, mem, &da));
-  {
-    std::vector<double> smu, snu;
-    std::vector<int> fmu, gmu, fnu, gnu;
-    GS_TRY(validate_columns(ctx, dmu, n, P, smu, fmu, gmu));
-    GS_TRY(validate_columns(ctx, dnu, n, P, snu, fnu, gnu));
-    bool a_checked = false;
-    for (int p = 0; p < P; ++p) {
-      GS_TRY(check_distribution(ctx, n, smu[p], fmu[p], gmu[p]));
-      GS_TRY(check_distribution(ctx, n, snu[p], fnu[p], gnu[p]));
-      if (!a_checked) {
-        GS_TRY(check_weights(ctx, da, n));
-        a_checked = true;
-      }
-      if (!(tol > 0.0)) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "tolerance must be positive");
-      if (max_iter < 1) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "max_iter must be >= 1");
-    }
-  }
+  GS_TRY(gs_check_transport_inputs(ctx, n, dmu, dnu, da, P, max_iter, tol));
   if (flags & GS_FLAG_FP32)
     return sinkhorn_impl<float>(ctx, f, da, dmu, dnu, P, max_iter, tol, flags, mem, out_v, out_w,
                                 out_cost, out_kl, out_iters, out_conv, out_err, fail_pair, fail_sweep);
@@ -2236,5 +2220,26 @@ int gs_spmm_grouped(gs_ctx* ctx, const gs_graph* g, const double* x, double* y, 
   A.Tout = y;
   launch_step<double>(ctx, GW, rpc, A, MODE_NONE);
   GS_CUDA(ctx, cudaGetLastError());
+  return GS_OK;
+}
+
+// check_transport_inputs (transport.cpp:56-66) over P device column pairs, in pair order
+int gs_check_transport_inputs(gs_ctx* ctx, int n, const double* dmu, const double* dnu, const double* da,
+                              int P, int max_iter, double tol) {
+  std::vector<double> smu, snu;
+  std::vector<int> fmu, gmu, fnu, gnu;
+  GS_TRY(validate_columns(ctx, dmu, n, P, smu, fmu, gmu));
+  GS_TRY(validate_columns(ctx, dnu, n, P, snu, fnu, gnu));
+  bool a_checked = false;
+  for (int p = 0; p < P; ++p) {
+    GS_TRY(check_distribution(ctx, n, smu[p], fmu[p], gmu[p]));
+    GS_TRY(check_distribution(ctx, n, snu[p], fnu[p], gnu[p]));
+    if (!a_checked) {
+      GS_TRY(check_weights(ctx, da, n));
+      a_checked = true;
+    }
+    if (!(tol > 0.0)) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "tolerance must be positive");
+    if (max_iter < 1) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "max_iter must be >= 1");
+  }
   return GS_OK;
 }

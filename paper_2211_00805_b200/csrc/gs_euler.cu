@@ -12,6 +12,7 @@
 
 #include <cmath>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "gs_internal.cuh"
@@ -295,6 +296,73 @@ int euler_solve(gs_ctx* ctx, const gs_euler* E, double* x, int B, int* iters) {
   return GS_OK;
 }
 
+// ---- euler_sinkhorn[_batch] (transport.cpp:144-239 over EulerHeat, transport.cpp:257-269) ------
+// Per-pair vectors are column-major (pair p at p * n, caller's vertex order). The lockstep CG runs
+// until every column of its batch converges, so the batch must hold exactly the reference's
+// active pairs in order: finished pairs are dropped after every sweep (transport.cpp:210-226).
+__global__ void k_es_weighted(const double* __restrict__ a, const double* __restrict__ src,
+                              const int* __restrict__ cols, int n, int B, double* __restrict__ out) {
+  const int64_t total = (int64_t)B * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / n), i = (int)(e % n);
+    out[e] = a[i] * (src ? src[(size_t)cols[c] * n + i] : 1.0);
+  }
+}
+
+// filter_checked (transport.cpp:21-38): min of the output vs 1e-12 max |input|, per column
+__global__ void k_es_check(const double* __restrict__ x, const double* __restrict__ y, int n,
+                           int* __restrict__ bad) {
+  const int c = blockIdx.x;
+  __shared__ double smn[kT], smx[kT];
+  double mn = INFINITY, mx = 0.0;
+  for (int i = threadIdx.x; i < n; i += kT) {
+    mn = fmin(mn, y[(size_t)c * n + i]);
+    mx = fmax(mx, fabs(x[(size_t)c * n + i]));
+  }
+  smn[threadIdx.x] = mn;
+  smx[threadIdx.x] = mx;
+  __syncthreads();
+  for (int s = kT / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      smn[threadIdx.x] = fmin(smn[threadIdx.x], smn[threadIdx.x + s]);
+      smx[threadIdx.x] = fmax(smx[threadIdx.x], smx[threadIdx.x + s]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && !(smn[0] >= -(1e-12 * smx[0]))) atomicExch(bad, 1);
+}
+
+// dst[pair] = num[pair] / max(den_c, floor) for the active pairs (den: batch column c)
+__global__ void k_es_divide(const double* __restrict__ num, const double* __restrict__ den,
+                            const int* __restrict__ cols, int n, int B, double* __restrict__ dst) {
+  const int64_t total = (int64_t)B * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e / n), i = (int)(e % n);
+    const size_t o = (size_t)cols[c] * n + i;
+    dst[o] = num[o] / fmax(den[e], 1e-300);
+  }
+}
+
+// marginal L1 error per active pair, summed in vertex order as the oracle does
+__global__ void k_es_err(const double* __restrict__ V, const double* __restrict__ phi,
+                         const double* __restrict__ M, const int* __restrict__ cols, int n, int B,
+                         double* __restrict__ err) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= B) return;
+  const size_t o = (size_t)cols[c] * n;
+  double e = 0.0;
+  for (int i = 0; i < n; ++i) e += fabs(V[o + i] * phi[(size_t)c * n + i] - M[o + i]);
+  err[c] = e;
+}
+
+// transport.cpp:41-54 (host, the oracle's order and libm)
+double plain_log_sum(const double* a, const double* mu, const double* s, int n) {
+  double acc = 0.0;
+  for (int i = 0; i < n; ++i)
+    if (mu[i] > 0.0) acc += a[i] * mu[i] * std::log(s[i]);
+  return acc;
+}
+
 }  // namespace
 
 extern "C" int gs_euler_create(gs_ctx* ctx, const gs_graph* L, double t, int steps, gs_euler** out) {
@@ -355,6 +423,24 @@ extern "C" void gs_euler_destroy(gs_euler* E) {
 
 extern "C" const gs_graph* gs_euler_system(const gs_euler* E) { return E ? E->system : nullptr; }
 
+// EulerHeat::apply on device column blocks (width contiguous n-vectors, caller's vertex order)
+static int euler_apply_dev(gs_ctx* ctx, const gs_euler* E, const double* dX, double* dY, int width, int* it) {
+  const int n = E->n;
+  cudaStream_t s = ctx->stream;
+  const int GW = gs_group_width(width), G = (width + GW - 1) / GW;
+  const int64_t len = (int64_t)G * GW * n;
+  DevBuf<double> blk;
+  GS_CUDA(ctx, blk.alloc(len, s));
+  gs_launch_begin(ctx, 1);
+  k_pack_cols<<<grid_for(len), kT, 0, s>>>(dX, blk.get(), n, width, GW, G, E->order);
+  gs_launch_end(ctx, 1);
+  for (int step = 0; step < E->steps; ++step) GS_TRY(euler_solve(ctx, E, blk.get(), width, it));
+  gs_launch_begin(ctx, 1);
+  k_unpack_cols<<<grid_for((int64_t)width * n), kT, 0, s>>>(blk.get(), dY, n, width, GW, E->newpos);
+  gs_launch_end(ctx, 1);
+  return GS_OK;
+}
+
 extern "C" int gs_euler_apply(gs_ctx* ctx, const gs_euler* E, const double* X, double* Y, int width,
                               int mem, int* iters_out) {
   if (!ctx || !E) return GS_ERR_UNSUPPORTED;
@@ -390,5 +476,156 @@ extern "C" int gs_euler_apply(gs_ctx* ctx, const gs_euler* E, const double* X, d
     GS_CUDA(ctx, cudaMemcpyAsync(Y, dY, (size_t)width * n * sizeof(double), cudaMemcpyDeviceToHost, s));
   GS_CUDA(ctx, cudaStreamSynchronize(s));
   if (iters_out) *iters_out = it;
+  return GS_OK;
+}
+
+extern "C" int gs_euler_sinkhorn(gs_ctx* ctx, const gs_euler* E, const double* a, const double* mus,
+                                 const double* nus, int P, int max_iter, double tol, int flags, int mem,
+                                 double* out_v, double* out_w, double* out_cost, double* out_kl,
+                                 int* out_iters, int* out_conv, double* out_err, int* fail_pair,
+                                 int* fail_sweep) {
+  if (!ctx || !E) return GS_ERR_UNSUPPORTED;
+  if (fail_pair) *fail_pair = -1;
+  if (fail_sweep) *fail_sweep = 0;
+  const int n = E->n;
+  if (P < 0) return gs_fail(ctx, ERRC_SIZE_MISMATCH, "pair lists differ in length");
+  if (P == 0) return GS_OK;
+  cudaStream_t s = ctx->stream;
+  const size_t len = (size_t)P * n;
+  DevBuf<double> bmu, bnu, ba;
+  const double *dM = mus, *dN = nus, *da = a;
+  auto stage = [&](DevBuf<double>& b, const double* src, size_t count, const double** out) -> int {
+    GS_CUDA(ctx, b.alloc(count, s));
+    GS_CUDA(ctx, cudaMemcpyAsync(b.get(), src, count * sizeof(double), cudaMemcpyHostToDevice, s));
+    *out = b.get();
+    return GS_OK;
+  };
+  if (mem != GS_MEM_DEVICE) {
+    GS_TRY(stage(bmu, mus, len, &dM));
+    GS_TRY(stage(bnu, nus, len, &dN));
+    GS_TRY(stage(ba, a, n, &da));
+  }
+  GS_TRY(gs_check_transport_inputs(ctx, n, dM, dN, da, P, max_iter, tol));
+  DevBuf<double> V, W, X, phi, psi, OV, OW, derr;
+  DevBuf<int> cols, bad;
+  for (DevBuf<double>* b : {&V, &W, &X, &phi, &psi, &OV, &OW}) GS_CUDA(ctx, b->alloc(len, s));
+  GS_CUDA(ctx, derr.alloc(P, s));
+  GS_CUDA(ctx, cols.alloc(P, s));
+  GS_CUDA(ctx, bad.alloc(1, s));
+  GS_CUDA(ctx, cudaMemsetAsync(V.get(), 0, len * sizeof(double), s));
+  std::vector<int> active(P), stagnant(P, 0), iters(P, 0), conv(P, 0);
+  std::vector<double> errs(P, INFINITY);
+  for (int p = 0; p < P; ++p) active[p] = p;
+  const char* knp = "heat approximation produced negative mass; increase the degree or diffusion time";
+  // X = a .* src[active] (src null: W = 1); out = E(X) checked
+  auto apply = [&](const double* src, int B, double* out) -> int {
+    gs_launch_begin(ctx, 1);
+    k_es_weighted<<<grid_for((int64_t)B * n), kT, 0, s>>>(da, src, cols.get(), n, B, X.get());
+    gs_launch_end(ctx, 1);
+    int it = 0;
+    GS_TRY(euler_apply_dev(ctx, E, X.get(), out, B, &it));
+    GS_CUDA(ctx, cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+    gs_launch_begin(ctx, 1);
+    k_es_check<<<B, kT, 0, s>>>(X.get(), out, n, bad.get());
+    gs_launch_end(ctx, 1);
+    int h = 0;
+    GS_CUDA(ctx, cudaMemcpyAsync(&h, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    GS_CUDA(ctx, cudaStreamSynchronize(s));
+    return h ? gs_fail(ctx, ERRC_KERNEL_NOT_POSITIVE, knp) : GS_OK;
+  };
+  GS_CUDA(ctx, cudaMemcpyAsync(cols.get(), active.data(), P * sizeof(int), cudaMemcpyHostToDevice, s));
+  GS_TRY(apply(nullptr, P, phi.get()));  // phi = H(a * 1)
+  int na = P;
+  for (int it = 1; it <= max_iter && na > 0; ++it) {
+    const int B = na;
+    gs_launch_begin(ctx, 1);
+    k_es_divide<<<grid_for((int64_t)B * n), kT, 0, s>>>(dM, phi.get(), cols.get(), n, B, V.get());
+    gs_launch_end(ctx, 1);
+    GS_TRY(apply(V.get(), B, psi.get()));
+    gs_launch_begin(ctx, 1);
+    k_es_divide<<<grid_for((int64_t)B * n), kT, 0, s>>>(dN, psi.get(), cols.get(), n, B, W.get());
+    gs_launch_end(ctx, 1);
+    GS_TRY(apply(W.get(), B, phi.get()));
+    gs_launch_begin(ctx, 1);
+    k_es_err<<<(B + kT - 1) / kT, kT, 0, s>>>(V.get(), phi.get(), dM, cols.get(), n, B, derr.get());
+    gs_launch_end(ctx, 1);
+    std::vector<double> e(B);
+    GS_CUDA(ctx, cudaMemcpyAsync(e.data(), derr.get(), B * sizeof(double), cudaMemcpyDeviceToHost, s));
+    GS_CUDA(ctx, cudaStreamSynchronize(s));
+    std::vector<int> keep;
+    for (int c = 0; c < B; ++c) {
+      const int pair = active[c];
+      iters[pair] = it;
+      errs[pair] = e[c];
+      const bool done = e[c] <= tol;
+      if (done) conv[pair] = 1;
+      if (done || it == max_iter) {  // transport.cpp:196-200: finalise v, w
+        GS_CUDA(ctx, cudaMemcpyAsync(OV.get() + (size_t)pair * n, V.get() + (size_t)pair * n, n * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, s));
+        GS_CUDA(ctx, cudaMemcpyAsync(OW.get() + (size_t)pair * n, W.get() + (size_t)pair * n, n * sizeof(double),
+                                     cudaMemcpyDeviceToDevice, s));
+      }
+      if (!done) {
+        stagnant[pair] = e[c] > 0.5 ? stagnant[pair] + 1 : 0;
+        if (!(flags & GS_FLAG_NO_STAGNATION_ABORT) && !(stagnant[pair] < 50)) {
+          if (fail_pair) *fail_pair = pair;
+          if (fail_sweep) *fail_sweep = it;
+          if (flags & GS_FLAG_SINGLE)
+            return gs_fail(ctx, ERRC_DISCONNECTED,
+                           "marginal error stagnated above 0.5; are mu and nu in the same graph component?");
+          return gs_fail(ctx, ERRC_DISCONNECTED, "marginal error stagnated above 0.5 for pair " + std::to_string(pair));
+        }
+        keep.push_back(c);
+      }
+    }
+    if ((int)keep.size() != B) {  // compaction (transport.cpp:210-226): phi keeps its batch order
+      for (int c = 0; c < (int)keep.size(); ++c)
+        if (keep[c] != c)
+          GS_CUDA(ctx, cudaMemcpyAsync(phi.get() + (size_t)c * n, phi.get() + (size_t)keep[c] * n, n * sizeof(double),
+                                       cudaMemcpyDeviceToDevice, s));
+      std::vector<int> still;
+      for (int c : keep) still.push_back(active[c]);
+      active = still;
+      na = (int)active.size();
+      if (na > 0)
+        GS_CUDA(ctx, cudaMemcpyAsync(cols.get(), active.data(), na * sizeof(int), cudaMemcpyHostToDevice, s));
+    }
+  }
+  // ---- outputs; cost / KL on the host in the oracle's order (transport.cpp:137-140) ----------------
+  std::vector<double> hv(len), hw(len), hmu(len), hnu(len), ha(n);
+  GS_CUDA(ctx, cudaMemcpyAsync(hv.data(), OV.get(), len * sizeof(double), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaMemcpyAsync(hw.data(), OW.get(), len * sizeof(double), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaMemcpyAsync(hmu.data(), dM, len * sizeof(double), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaMemcpyAsync(hnu.data(), dN, len * sizeof(double), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaMemcpyAsync(ha.data(), da, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  const double lambda = 4.0 * E->t;
+  std::vector<double> cost(P), kl(P);
+  for (int p = 0; p < P; ++p) {
+    const double *mu = &hmu[(size_t)p * n], *nu = &hnu[(size_t)p * n];
+    const double *v = &hv[(size_t)p * n], *w = &hw[(size_t)p * n];
+    cost[p] = lambda * (plain_log_sum(ha.data(), mu, v, n) + plain_log_sum(ha.data(), nu, w, n));
+    double k1 = 0.0, k2 = 0.0;
+    for (int i = 0; i < n; ++i)
+      if (mu[i] > 0.0) k1 += mu[i] * std::log(v[i]);
+    for (int i = 0; i < n; ++i)
+      if (nu[i] > 0.0) k2 += nu[i] * std::log(std::fmax(ha[i] * w[i], 1e-300));
+    kl[p] = k1 + k2 - 1.0;
+  }
+  auto put = [&](void* dst, const void* src, size_t bytes, bool host_src) -> int {
+    if (!dst) return GS_OK;
+    cudaMemcpyKind k = mem == GS_MEM_DEVICE ? (host_src ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice)
+                                            : (host_src ? cudaMemcpyHostToHost : cudaMemcpyDeviceToHost);
+    GS_CUDA(ctx, cudaMemcpyAsync(dst, src, bytes, k, s));
+    return GS_OK;
+  };
+  GS_TRY(put(out_v, OV.get(), len * sizeof(double), false));
+  GS_TRY(put(out_w, OW.get(), len * sizeof(double), false));
+  GS_TRY(put(out_cost, cost.data(), P * sizeof(double), true));
+  GS_TRY(put(out_kl, kl.data(), P * sizeof(double), true));
+  GS_TRY(put(out_iters, iters.data(), P * sizeof(int), true));
+  GS_TRY(put(out_conv, conv.data(), P * sizeof(int), true));
+  GS_TRY(put(out_err, errs.data(), P * sizeof(double), true));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
   return GS_OK;
 }

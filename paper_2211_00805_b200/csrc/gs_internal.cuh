@@ -178,5 +178,7 @@ int gs_permute_graph(gs_ctx* ctx, const gs_graph* g, const int* d_order, const i
 // gs_group_width(B)-wide groups, each an n x GW row-major block
 int gs_group_width(int B);
 int gs_spmm_grouped(gs_ctx* ctx, const gs_graph* g, const double* x, double* y, int B);
+int gs_check_transport_inputs(gs_ctx* ctx, int n, const double* dmu, const double* dnu, const double* da,
+                              int P, int max_iter, double tol);
 int gs_csr_from_sorted_entries(gs_ctx* ctx, int n, int64_t m, const unsigned long long* d_keys,
                                const double* d_vals, bool check_dups, gs_graph** out);

@@ -638,6 +638,43 @@ def geodesic_sinkhorn_batch(filter: HeatFilter, mus: List[Distribution], nus: Li
     return _sinkhorn(filter, mus, nus, a, params, flags)
 
 
+def _euler_sinkhorn(euler: "EulerHeat", mus, nus, a, params: SinkhornParams, flags: int):
+    ctx = euler._ctx
+    n = euler.size()
+    if len(mus) != len(nus):
+        raise Error(errc.size_mismatch, "SizeMismatch: pair lists differ in length")
+    P = len(mus)
+    if P == 0:
+        return []
+    M, N, a = _stack(mus, n), _stack(nus, n), _f64(a)
+    if a.size != n:
+        raise Error(errc.length_mismatch, "LengthMismatch: vertex weights must live on the filter's graph")
+    v, w = np.empty((P, n)), np.empty((P, n))
+    cost, kl, err = np.empty(P), np.empty(P), np.empty(P)
+    it, conv = np.empty(P, np.int32), np.empty(P, np.int32)
+    fp, fs = C.c_int(), C.c_int()
+    ctx.check(ctx.lib.gs_euler_sinkhorn(ctx.handle, euler._h, _ptr(a), _ptr(M), _ptr(N), P,
+                                        int(params.max_iter), float(params.tol), flags,
+                                        _capi.GS_MEM_HOST, _ptr(v), _ptr(w), _ptr(cost), _ptr(kl),
+                                        _ptr(it), _ptr(conv), _ptr(err), C.byref(fp), C.byref(fs)))
+    lam = 4.0 * euler.time()
+    return [TransportResult(v[p].copy(), w[p].copy(), float(cost[p]), float(kl[p]), lam, int(it[p]),
+                            bool(conv[p]), float(err[p])) for p in range(P)]
+
+
+def euler_sinkhorn(euler: "EulerHeat", mu: Distribution, nu: Distribution, a,
+                   params: SinkhornParams = SinkhornParams()) -> TransportResult:
+    """transport.cpp:257-261 (sinkhorn_single semantics over EulerHeat)."""
+    return _euler_sinkhorn(euler, [mu], [nu], a, params, _capi.GS_FLAG_SINGLE)[0]
+
+
+def euler_sinkhorn_batch(euler: "EulerHeat", mus, nus, a, params: SinkhornParams = SinkhornParams(),
+                         no_stagnation_abort: bool = False) -> List[TransportResult]:
+    """transport.cpp:263-269 (sinkhorn_many over EulerHeat)."""
+    return _euler_sinkhorn(euler, mus, nus, a, params,
+                           _capi.GS_FLAG_NO_STAGNATION_ABORT if no_stagnation_abort else 0)
+
+
 # ------------------------------------------------------------------------------ row partitions
 class RowPartition:
     """One rank's rows of a filter for row-partitioned multi-GPU runs (gs_part_*; SURVEY.md

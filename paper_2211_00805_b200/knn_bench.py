@@ -4,8 +4,9 @@ distance-ranking experiment on the device path.
 m clusters on a rotated swiss roll (make_swiss_roll, bench.cpp:59-100) -> alpha-decay kNN graph
 -> Laplacian -> heat filter -> geodesic Sinkhorn distances between all m(m-1)/2 pairs of cluster
 indicator distributions in ONE batched call -> Pearson / Spearman / precision@5 against the
-unrolled-spiral ground truth (bench.cpp:107-214). Only the `geodesic_sinkhorn` method runs here:
-the dense-Sinkhorn W1/W2 and Euler-Sinkhorn baselines are competitor methods.
+unrolled-spiral ground truth (bench.cpp:107-214). Methods: `geodesic_sinkhorn` and the
+`euler_sinkhorn` competitor (EulerHeat + the same Sinkhorn control); the dense-Sinkhorn W1/W2
+baselines are out of scope.
 
 Draws follow geosink::Rng (rng.hpp:13-68) in the reference order; the random rotation is the
 Householder QR of a Gaussian matrix with R's diagonal made positive (numpy's LAPACK QR instead of
@@ -37,6 +38,8 @@ class KnnBenchConfig:  # bench.hpp:75-93
     t: float = 20.0
     degree: int = 100
     sinkhorn: gs.SinkhornParams = field(default_factory=lambda: gs.SinkhornParams(500, 1e-6))
+    euler_steps: int = 30  # backward-Euler substeps
+    methods: List[str] = field(default_factory=lambda: ["geodesic_sinkhorn"])
     # bench-only deviation (as bench.py): run every pair to max_iter instead of raising
     # Disconnected when a pair's marginal error stays above 0.5 for 50 sweeps
     no_stagnation_abort: bool = False
@@ -141,8 +144,8 @@ def knn_benchmark(config: KnnBenchConfig = KnnBenchConfig(), ctx=None) -> dict:
     if config.n_distributions < 3:
         raise gs.Error(gs.errc.invalid_argument, "InvalidArgument: need at least three distributions")
     m = config.n_distributions
-    per_seed, means = [], {"pearson": 0.0, "spearman": 0.0, "p_at_5": 0.0, "graph": 0.0,
-                           "prepare": 0.0, "distance": 0.0}
+    keys = ("pearson", "spearman", "p_at_5", "graph", "prepare", "distance")
+    per_seed, means = [], {mth: dict.fromkeys(keys, 0.0) for mth in config.methods}
     for seed in config.seeds:
         sample = make_swiss_roll(m, config.samples_per_dist, config.noise_sigma, config.ambient_dim, seed)
         truth = ground_truth_distances(sample)
@@ -158,27 +161,38 @@ def knn_benchmark(config: KnnBenchConfig = KnnBenchConfig(), ctx=None) -> dict:
                 mus.append(gs.Distribution.indicator(n, groups[i]))
                 nus.append(gs.Distribution.indicator(n, groups[j]))
         a = np.full(n, 1.0 / n)
-        t1 = time.perf_counter()
-        filt = gs.HeatFilter(lap, config.t, config.degree)
-        t_prep = time.perf_counter() - t1
-        t2 = time.perf_counter()
-        runs = gs.geodesic_sinkhorn_batch(filt, mus, nus, a, config.sinkhorn,
-                                          no_stagnation_abort=config.no_stagnation_abort)
-        t_dist = time.perf_counter() - t2
-        d = np.zeros((m, m))
-        q = 0
-        for i in range(m):
-            for j in range(i + 1, m):
-                d[i, j] = d[j, i] = runs[q].cost
-                q += 1
-        rep = rank_metrics(d, truth)
-        rep.update(graph=t_graph, prepare=t_prep, distance=t_dist)
-        per_seed.append({"seed": seed, "truth": truth, "distances": d, "report": rep,
-                         "iterations": [r.iterations for r in runs]})
-        for key in means:
-            means[key] += rep[key] / len(config.seeds)
-    means["total"] = means["graph"] + means["prepare"] + means["distance"]
-    return {"per_seed": per_seed, "mean_report": {"geodesic_sinkhorn": means}}
+        seed_out = {"seed": seed, "truth": truth, "distances": {}, "reports": {}, "iterations": {}}
+        for method in config.methods:
+            t1 = time.perf_counter()
+            if method == "geodesic_sinkhorn":
+                op = gs.HeatFilter(lap, config.t, config.degree)
+                solve = gs.geodesic_sinkhorn_batch
+            elif method == "euler_sinkhorn":
+                op = gs.EulerHeat(lap, config.t, config.euler_steps)
+                solve = gs.euler_sinkhorn_batch
+            else:
+                raise gs.Error(gs.errc.invalid_argument, f"InvalidArgument: unknown benchmark method '{method}'")
+            t_prep = time.perf_counter() - t1
+            t2 = time.perf_counter()
+            runs = solve(op, mus, nus, a, config.sinkhorn, no_stagnation_abort=config.no_stagnation_abort)
+            t_dist = time.perf_counter() - t2
+            d = np.zeros((m, m))
+            q = 0
+            for i in range(m):
+                for j in range(i + 1, m):
+                    d[i, j] = d[j, i] = runs[q].cost
+                    q += 1
+            rep = rank_metrics(d, truth)
+            rep.update(graph=t_graph, prepare=t_prep, distance=t_dist)
+            seed_out["distances"][method] = d
+            seed_out["reports"][method] = rep
+            seed_out["iterations"][method] = [r.iterations for r in runs]
+            for key in keys:
+                means[method][key] += rep[key] / len(config.seeds)
+        per_seed.append(seed_out)
+    for mth in means:
+        means[mth]["total"] = means[mth]["graph"] + means[mth]["prepare"] + means[mth]["distance"]
+    return {"per_seed": per_seed, "mean_report": means}
 
 
 # ---------------------------------------------------------------------------------------------

@@ -76,3 +76,45 @@ def test_euler_converges_to_heat_kernel(gs):
     ref = f.apply(x)
     err = [np.abs(gs.apply_euler(lap, 1.0, s, x) - ref).max() / np.abs(ref).max() for s in (10, 100)]
     assert err[1] < err[0] and err[1] < 5e-3
+
+
+@pytest.mark.parametrize("P,steps", [(1, 2), (5, 3), (9, 1)])
+def test_euler_sinkhorn_matches_oracle(gs, P, steps):
+    """euler_sinkhorn_batch (transport.cpp:257-269): pairs converge at different sweeps, so the
+    lockstep-CG batch shrinks; v, w, iterations, cost and KL bit for bit with the oracle."""
+    from helpers import random_distribution
+    from paper_2211_00805_b200.rng import Rng
+    n = 120
+    r, c, v = acceptance_graph(n, 60 + P)
+    lap, Lo = _pair(gs, r, c, v, n, 1)
+    E = gs.EulerHeat(lap, 0.8, steps)
+    So = po.euler_system(Lo, 0.8, steps)
+    rng = Rng(P)
+    mus = [random_distribution(n, rng) for _ in range(P)]
+    nus = [random_distribution(n, rng) for _ in range(P)]
+    a = np.full(n, 1.0 / n)
+    res = gs.euler_sinkhorn_batch(E, [gs.Distribution(m) for m in mus], [gs.Distribution(x) for x in nus], a,
+                                  gs.SinkhornParams(300, 1e-9))
+    ref = po.euler_sinkhorn_batch(So, steps, 0.8, a, np.array(mus), np.array(nus), 300, 1e-9)
+    for p in range(P):
+        q = res[p]
+        assert q.iterations == ref["iterations"][p] and q.converged == ref["converged"][p]
+        assert np.array_equal(q.v, ref["v"][p]) and np.array_equal(q.w, ref["w"][p])
+        assert q.cost == ref["cost"][p] and q.kl == ref["kl"][p]
+        assert q.marginal_error == ref["marginal_error"][p]
+
+
+def test_euler_sinkhorn_errors_like_oracle(gs):
+    """Disconnected components: the same error (and message) as the oracle."""
+    A = gs.SparseSymMatrix.from_triplets(4, [(0, 1, 1.0), (2, 3, 1.0)])
+    lap = gs.laplacian(A, gs.LaplacianKind.combinatorial)
+    E = gs.EulerHeat(lap, 1.0, 2)
+    e = np.eye(4)
+    with pytest.raises(gs.Error) as ex:
+        gs.euler_sinkhorn(E, gs.Distribution(e[0]), gs.Distribution(e[3]), np.full(4, 0.25),
+                          gs.SinkhornParams(500, 1e-9))
+    Lo, _, _ = po.laplacian(po.from_triplets(4, [0, 2], [1, 3], [1.0, 1.0]), 0)
+    with pytest.raises(po.OracleError) as ref:
+        po.euler_sinkhorn_batch(po.euler_system(Lo, 1.0, 2), 2, 1.0, np.full(4, 0.25), e[0][None], e[3][None],
+                                500, 1e-9, single_style=True)
+    assert str(ex.value).endswith(str(ref.value))

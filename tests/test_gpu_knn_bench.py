@@ -45,7 +45,7 @@ def test_knn_benchmark_matches_oracle(ctx, m, per, noise, t, seed):
     if ref_err is not None or err is not None:
         assert err == ref_err  # same errc, message and failing pair
         return
-    d = res["per_seed"][0]["distances"]
+    d = res["per_seed"][0]["distances"]["geodesic_sinkhorn"]
     q = 0
     for i in range(m):
         for j in range(i + 1, m):

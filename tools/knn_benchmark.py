@@ -7,8 +7,9 @@ from paper_2211_00805_b200 import knn_bench as kb  # noqa: E402
 
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 seeds = [int(s) for s in args] or [1, 2, 3]
-res = kb.knn_benchmark(kb.KnnBenchConfig(seeds=seeds,
+methods = ["geodesic_sinkhorn"] + (["euler_sinkhorn"] if "--euler" in sys.argv else [])
+res = kb.knn_benchmark(kb.KnnBenchConfig(seeds=seeds, methods=methods,
                                          no_stagnation_abort="--no-stagnation-abort" in sys.argv))
-rep = res["mean_report"]["geodesic_sinkhorn"]
-iters = [max(s["iterations"]) for s in res["per_seed"]]
-print(json.dumps({"method": "geodesic_sinkhorn", "seeds": seeds, "max_iterations": iters, **rep}))
+for m in methods:
+    iters = [max(s["iterations"][m]) for s in res["per_seed"]]
+    print(json.dumps({"method": m, "seeds": seeds, "max_iterations": iters, **res["mean_report"][m]}))
