@@ -494,6 +494,15 @@ int rows_per_block(int gw) {  // rows covered by one CTA pass (8 warps)
   }
 }
 
+// Latency-bound one-column fp64 problems up to this many rows take one warp per row (GS_W1_MAX)
+inline int w1_max_rows() {
+  static const int v = [] {
+    const char* e = getenv("GS_W1_MAX");
+    return e ? atoi(e) : 32768;
+  }();
+  return v;
+}
+
 // Row blocks per CTA: kRowsPerCta (L1 reuse across consecutive blocks) unless that leaves fewer
 // than two CTAs per SM, in which case 1 (small, latency-bound problems such as config 0).
 template <typename S>
@@ -536,6 +545,17 @@ void launch_step_gw(const StepArgs& A, int mode, int rpc, cudaStream_t s) {
 template <typename S>
 void launch_step(gs_ctx* ctx, int gw, int rpc, const StepArgs& A, int mode) {
   gs_launch_begin(ctx, 0);
+  if (A.warp_rows) {  // small one-column problems: one warp per row
+    const dim3 grid((unsigned)(A.tiles * A.Gl));
+    switch (mode) {
+      case MODE_NONE: k_cheb_step_w1<S, MODE_NONE><<<grid, kThreads, 0, ctx->stream>>>(A); break;
+      case MODE_SK_PSI: k_cheb_step_w1<S, MODE_SK_PSI><<<grid, kThreads, 0, ctx->stream>>>(A); break;
+      case MODE_SK_PHI: k_cheb_step_w1<S, MODE_SK_PHI><<<grid, kThreads, 0, ctx->stream>>>(A); break;
+      default: k_cheb_step_w1<S, MODE_BARY_PSI><<<grid, kThreads, 0, ctx->stream>>>(A); break;
+    }
+    gs_launch_end(ctx, 0);
+    return;
+  }
   switch (gw) {
     case 64: launch_step_gw<S, 64>(A, mode, rpc, ctx->stream); break;
     case 32: launch_step_gw<S, 32>(A, mode, rpc, ctx->stream); break;
@@ -554,6 +574,7 @@ struct Work {
   int n = 0, B = 0, GW = 1, G = 1, Bpad = 1, tiles = 0, rpc = 1;
   int64_t ld = 0;  // rows per column group: n, or local + halo rows of a row partition
   int lay = 0;  // filter layout: 0 for one-warp-per-row groups, 1 (degree-sorted) for narrower
+  bool w1 = false;  // one-column fp64 problem small enough for the warp-per-row kernel
   DevBuf<S> T[2], acc;
   DevBuf<unsigned long long> cmin, cmax;
   DevBuf<double> thr, errcol, part_err;
@@ -570,6 +591,8 @@ struct Work {
     lay = GW >= 32 ? 0 : 1;
     rpc = choose_rpc<S>(n, GW, G, f ? f->lay[lay].near_frac : 1.0);
     tiles = (n + rows_per_block<S>(GW) * rpc - 1) / (rows_per_block<S>(GW) * rpc);
+    w1 = GW == 1 && sizeof(S) == 8 && n <= w1_max_rows();
+    if (w1) tiles = (n + kThreads / 32 - 1) / (kThreads / 32);
     const size_t len = (size_t)Bpad * (ld > 0 ? ld : 1);
     GS_CUDA(ctx, T[0].alloc(len, s));
     GS_CUDA(ctx, T[1].alloc(len, s));
@@ -651,6 +674,7 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
   A.offs = G->offs;
   A.cols = G->cols;
   A.vals = layout_vals<S>(Ly);
+  A.warp_rows = w.w1;
   A.n = w.n;
   A.ld = w.ld;
   A.tiles = w.tiles;

@@ -182,6 +182,7 @@ struct StepArgs {  // vector pointers are S* of the launch's precision
   const void* vals;
   int n, tiles, g0, Gl, Bpad;  // rows [row0, n) in `tiles` CTA tiles per column group
   int row0, tile0;             // first row; index of the first tile in the error partials
+  int warp_rows;               // one warp per row (k_cheb_step_w1; one-column fp64 problems)
   int64_t ld;         // rows per column group (n, or local + halo rows for a row partition)
   const void* Tprev;  // T_{k-1}
   void* Tout;         // T_{k-2} in, T_k out (or next T_0 / SpMM output)
@@ -202,6 +203,14 @@ struct StepArgs {  // vector pointers are S* of the launch's precision
   const void* Vcur;   // PHI: V of this sweep
   void* Wout;         // PSI: W; PHI: V of the next sweep
 };
+
+template <typename S, int GW, int MODE>
+__device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, int q,
+                                           const S (&y)[Lay<GW, S>::VEC],
+                                           double (&mn)[Lay<GW, S>::VEC],
+                                           double (&mx)[Lay<GW, S>::VEC],
+                                           double (&er)[Lay<GW, S>::VEC], const S* pre,
+                                           int pre_stride);
 
 // One row of one Chebyshev step; epilogue partials accumulate in mn/mx/er (double).
 template <typename S, int GW, int MODE>
@@ -295,6 +304,23 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
     }
   }
   if (!valid) return;
+  finish_row<S, GW, MODE>(A, g, row, q, y, mn, mx, er, pre, pre_stride);
+}
+
+// The rest of a row's step once y = (L_s T_{k-1})[row] is known: the recurrence, the deferred
+// acc update and the stores / fused epilogue (row < A.n).
+template <typename S, int GW, int MODE>
+__device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, int q,
+                                           const S (&y)[Lay<GW, S>::VEC],
+                                           double (&mn)[Lay<GW, S>::VEC],
+                                           double (&mx)[Lay<GW, S>::VEC],
+                                           double (&er)[Lay<GW, S>::VEC], const S* pre,
+                                           int pre_stride) {
+  using L = Lay<GW, S>;
+  constexpr int VEC = L::VEC;
+  using P = Prec<S>;
+  const size_t gbase = (size_t)g * A.ld * GW + q * VEC;
+  const size_t idx = gbase + (size_t)row * GW;
   if (A.k == 0) {  // plain SpMM (sparse.cpp:85-99)
     st_vec<S, VEC>(static_cast<S*>(A.Tout) + idx, y);
     return;
@@ -476,6 +502,39 @@ __global__ void __launch_bounds__(kThreads, MODE != MODE_NONE ? 0 : (sizeof(S) =
       cheb_row<S, GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er, nullptr, 0);
   }
   if constexpr (MODE != MODE_NONE) block_epilogue<S, GW, MODE>(A, g, tile, warp, sub, q, mn, mx, er);
+}
+
+// Small one-column problems (config 0: n = 2000, B = 1) are latency-bound: with one row per lane a
+// row's ~13 dependent entry loads run back to back. Here a warp takes one row: its lanes load
+// 32 entries and their T_{k-1} values in one round, then every lane folds the (val, x) pairs in
+// CSR order from shuffles -- the same fma chain -- and lane 0 finishes the row.
+template <typename S, int MODE>
+__global__ void __launch_bounds__(kThreads) k_cheb_step_w1(const StepArgs A) {
+  if (A.status && (A.status->error || A.status->done)) return;
+  const int tl = blockIdx.x / A.Gl;
+  const int g = A.g0 + blockIdx.x % A.Gl;
+  if (A.cs.gactive && A.cs.gactive[g] == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int row = A.row0 + tl * (kThreads / 32) + warp;
+  double mn[1] = {INFINITY}, mx[1] = {0.0}, er[1] = {0.0};
+  if (row < A.n) {
+    const S* __restrict__ Tp = static_cast<const S*>(A.Tprev) + (size_t)g * A.ld;
+    const S* __restrict__ vals = static_cast<const S*>(A.vals);
+    const int pb = __ldg(A.offs + row), pe = __ldg(A.offs + row + 1);
+    S y[1] = {S(0)};
+    for (int p0 = pb; p0 < pe; p0 += 32) {
+      S v = S(0), x = S(0);
+      if (p0 + lane < pe) {
+        v = __ldg(vals + p0 + lane);
+        x = __ldg(Tp + __ldg(A.cols + p0 + lane));
+      }
+      const int cnt = min(32, pe - p0);
+      for (int u = 0; u < cnt; ++u)
+        y[0] = Prec<S>::fmat(__shfl_sync(0xffffffffu, v, u), __shfl_sync(0xffffffffu, x, u), y[0]);
+    }
+    if (lane == 0) finish_row<S, 1, MODE>(A, g, row, 0, y, mn, mx, er, nullptr, 0);
+  }
+  if constexpr (MODE != MODE_NONE) block_epilogue<S, 1, MODE>(A, g, A.tile0 + tl, warp, lane, 0, mn, mx, er);
 }
 
 }  // namespace gsk
