@@ -253,6 +253,15 @@ def run_engine(args):
     t_graph = time.perf_counter() - t0
     lap = gs.laplacian(A, gs.LaplacianKind.combinatorial)
     filt = gs.HeatFilter(lap, cfg.t, cfg.degree)
+    if os.environ.get("GS_BENCH_ORDER"):  # experiment: host-computed locality order
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import orders
+        kind = os.environ["GS_BENCH_ORDER"]
+        Ls = filt.scaled_laplacian()
+        o = (orders.morton3(cfg.roll.points) if kind == "morton" else
+             orders.bisect_order(Ls.row_offsets(), Ls.col_indices(), args.n,
+                                 int(os.environ.get("GS_BENCH_LEAF", "64"))))
+        filt.set_vertex_order(o, 0)
     t_prep = time.perf_counter() - t0 - t_graph
     n, P = args.n, args.pairs
     nnz_L = lap.matrix.stored_entries()
@@ -334,7 +343,7 @@ def run_engine(args):
     achieved = bytes_step / (avg_step_ms / 1000.0) / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "cheb_step_traffic.json")
-    if os.path.exists(prof):
+    if args.config == 1 and os.path.exists(prof):  # ncu DRAM bytes of the config-1 step kernel
         try:
             with open(prof) as f:
                 traffic = json.load(f).get("dram_bytes_per_launch")
@@ -439,7 +448,10 @@ def run_engine(args):
                                          "column_sweeps_per_s": value * P}),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": "k_cheb_step<double, 64, *, 4> (fused Chebyshev step, one warp per 512-byte row)",
+                         "kernel": ("k_cheb_step<double, 64, *, 4> (fused Chebyshev step, one warp per 512-byte row)"
+                                    if args.config == 1 else
+                                    "k_cheb_step_w1<double, *> (fused Chebyshev step, one warp per row; "
+                                    "latency-bound: the 0.39 MB working set lives in L2, SURVEY §8(d))"),
                          "bytes_per_launch": bytes_step, "avg_launch_ms": avg_step_ms,
                          "launches_timed": step_n, "timing_period": args.timing_period,
                          "share_of_step": avg_step_ms * steps_total / max(elapsed_ms, 1e-9)},
@@ -825,6 +837,12 @@ def run_engine_rows(args):
     A, sigma = gs.knn_gaussian_graph(roll.points, 10, ctx=ctx)
     lap = gs.laplacian(A, gs.LaplacianKind.combinatorial)
     filt = gs.HeatFilter(lap, 1.0, 30)
+    if os.environ.get("GS_BENCH_ORDER") == "morton":  # experiment: host-computed locality order
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import orders
+        o = orders.morton3(roll.points)
+        filt.set_vertex_order(o, 0)
+        filt.set_vertex_order(o, 1)
     setup_s = time.perf_counter() - t0
     mu = workloads.bump_in_s(roll, 2 * math.pi, 0.5)
     nu = workloads.bump_in_s(roll, 4 * math.pi, 0.5)

@@ -111,6 +111,12 @@ int gs_filter_coefficients(const gs_filter* f, double* out /* degree+1 */);
 const gs_graph* gs_filter_scaled(const gs_filter* f);
 /* The filter's internal vertex order (order[new] = old, n entries; locality renumbering). */
 int gs_filter_order(gs_ctx* ctx, const gs_filter* f, int* order, int mem);
+/* Replace the locality order of layout 0 (wide column groups) or 1 (narrow ones) with a
+ * caller-supplied permutation (order[new] = old). Results are unchanged (each row keeps its
+ * entries in the original column order); only the memory locality of the gathers changes.
+ * Not a permutation of 0..n-1 -> invalid_argument (layout reset to the identity). No reference
+ * counterpart (the reference has no locality renumbering). */
+int gs_filter_set_order(gs_ctx* ctx, gs_filter* f, int layout, const int* order, int mem);
 /* p_K(L_s) X for `width` contiguous n-vectors (heat.cpp:98-131). */
 int gs_filter_apply(gs_ctx* ctx, const gs_filter* f, const double* X, double* Y, int width,
                     int mem);

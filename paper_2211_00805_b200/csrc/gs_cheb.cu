@@ -529,10 +529,10 @@ template <typename S, int GW, int RPC>
 void launch_step_rpc(const StepArgs& A, int mode, cudaStream_t s) {
   dim3 grid((unsigned)(A.tiles * A.Gl));
   switch (mode) {
-    case MODE_NONE: k_cheb_step<S, GW, MODE_NONE, RPC><<<grid, kThreads, 0, s>>>(A); break;
-    case MODE_SK_PSI: k_cheb_step<S, GW, MODE_SK_PSI, RPC><<<grid, kThreads, 0, s>>>(A); break;
-    case MODE_SK_PHI: k_cheb_step<S, GW, MODE_SK_PHI, RPC><<<grid, kThreads, 0, s>>>(A); break;
-    default: k_cheb_step<S, GW, MODE_BARY_PSI, RPC><<<grid, kThreads, 0, s>>>(A); break;
+    case MODE_NONE: k_cheb_step<S, GW, MODE_NONE, RPC><<<grid, kStepThreads, 0, s>>>(A); break;
+    case MODE_SK_PSI: k_cheb_step<S, GW, MODE_SK_PSI, RPC><<<grid, kStepThreads, 0, s>>>(A); break;
+    case MODE_SK_PHI: k_cheb_step<S, GW, MODE_SK_PHI, RPC><<<grid, kStepThreads, 0, s>>>(A); break;
+    default: k_cheb_step<S, GW, MODE_BARY_PSI, RPC><<<grid, kStepThreads, 0, s>>>(A); break;
   }
 }
 
@@ -1831,6 +1831,43 @@ int check_part_comm(gs_ctx* ctx, const gs_part* p, const gs_comm* comm) {
 // ============================================================================================
 // HeatFilter (heat.cpp:72-96): scaled Laplacian copy + coefficients, both on the device.
 // ============================================================================================
+// Renumbered operator, fp32 value copy and index-locality statistic of layout l (its order and
+// newpos already set).
+static int finish_layout(gs_ctx* ctx, gs_filter* f, int l) {
+  cudaStream_t s = ctx->stream;
+  int rc = GS_OK;
+  gs_layout& Ly = f->lay[l];
+  gs_graph_destroy(Ly.perm);
+  Ly.perm = nullptr;
+  cudaFree(Ly.vals32);
+  Ly.vals32 = nullptr;
+  Ly.near_frac = 1.0;
+  do {
+    rc = gs_permute_graph(ctx, f->scaled, Ly.order, Ly.newpos, &Ly.perm);
+    if (rc) break;
+    const int64_t nnz = Ly.perm->nnz;  // fp32 copy of the permuted values (optional fp32 mode)
+    if (cudaMalloc((void**)&Ly.vals32, (size_t)(nnz ? nnz : 1) * sizeof(float)) != cudaSuccess) {
+      rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "fp32 value allocation failed");
+    } else if (nnz > 0) {
+      gs_launch_begin(ctx, 1);
+      k_to_float<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(Ly.perm->vals, nnz, Ly.vals32);
+      gs_launch_end(ctx, 1);
+      if (cudaStreamSynchronize(s) != cudaSuccess) rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "fp32 copy failed");
+    }
+    if (!rc && nnz > 0) {  // index locality of this layout (choose_rpc)
+      DevBuf<unsigned long long> cnt;
+      unsigned long long h = 0;
+      if (cnt.alloc(1, s) == cudaSuccess && cudaMemsetAsync(cnt.get(), 0, sizeof h, s) == cudaSuccess) {
+        k_near_count<<<148 * 4, 256, 0, s>>>(Ly.perm->offs, Ly.perm->cols, Ly.perm->n, cnt.get());
+        if (cudaMemcpyAsync(&h, cnt.get(), sizeof h, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+            cudaStreamSynchronize(s) == cudaSuccess)
+          Ly.near_frac = (double)h / (double)nnz;
+      }
+    }
+  } while (0);
+  return rc;
+}
+
 extern "C" int gs_filter_create(gs_ctx* ctx, const gs_graph* L, int kind, double lambda_bound,
                                 double t, int degree, gs_filter** out) {
   *out = nullptr;
@@ -1879,30 +1916,7 @@ extern "C" int gs_filter_create(gs_ctx* ctx, const gs_graph* L, int kind, double
   }
   if (!rc) rc = gs_bfs_order(ctx, f->scaled, f->lay[0].order, f->lay[0].newpos, sigma,
                              f->lay[1].order, f->lay[1].newpos);
-  for (int l = 0; l < 2 && !rc; ++l) {
-    gs_layout& Ly = f->lay[l];
-    rc = gs_permute_graph(ctx, f->scaled, Ly.order, Ly.newpos, &Ly.perm);
-    if (rc) break;
-    const int64_t nnz = Ly.perm->nnz;  // fp32 copy of the permuted values (optional fp32 mode)
-    if (cudaMalloc((void**)&Ly.vals32, (size_t)(nnz ? nnz : 1) * sizeof(float)) != cudaSuccess) {
-      rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "fp32 value allocation failed");
-    } else if (nnz > 0) {
-      gs_launch_begin(ctx, 1);
-      k_to_float<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(Ly.perm->vals, nnz, Ly.vals32);
-      gs_launch_end(ctx, 1);
-      if (cudaStreamSynchronize(s) != cudaSuccess) rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "fp32 copy failed");
-    }
-    if (!rc && nnz > 0) {  // index locality of this layout (choose_rpc)
-      DevBuf<unsigned long long> cnt;
-      unsigned long long h = 0;
-      if (cnt.alloc(1, s) == cudaSuccess && cudaMemsetAsync(cnt.get(), 0, sizeof h, s) == cudaSuccess) {
-        k_near_count<<<148 * 4, 256, 0, s>>>(Ly.perm->offs, Ly.perm->cols, Ly.perm->n, cnt.get());
-        if (cudaMemcpyAsync(&h, cnt.get(), sizeof h, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
-            cudaStreamSynchronize(s) == cudaSuccess)
-          Ly.near_frac = (double)h / (double)nnz;
-      }
-    }
-  }
+  for (int l = 0; l < 2 && !rc; ++l) rc = finish_layout(ctx, f, l);
   if (rc) {
     gs_filter_destroy(f);
     return rc;
@@ -1945,6 +1959,48 @@ extern "C" const gs_graph* gs_filter_scaled(const gs_filter* f) { return f->scal
 extern "C" int gs_filter_order(gs_ctx* ctx, const gs_filter* f, int* order, int mem) {
   GS_TRY(gs_copy_out(ctx, order, f->lay[0].order, (size_t)f->scaled->n * sizeof(int), mem));
   return gs_ctx_synchronize(ctx);
+}
+
+// Caller-supplied locality order for layout `layout` (0: wide column groups, 1: narrow ones).
+// Results do not depend on it: every row keeps its entries in the original column order.
+__global__ void k_newpos_from_order(const int* order, int n, int* newpos, int* bad) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int o = order[r];
+  if (o < 0 || o >= n) {
+    *bad = 1;
+    return;
+  }
+  if (atomicExch(newpos + o, r) != -1) *bad = 1;
+}
+
+extern "C" int gs_filter_set_order(gs_ctx* ctx, gs_filter* f, int layout, const int* order, int mem) {
+  if (!f || layout < 0 || layout > 1) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "gs_filter_set_order: bad layout");
+  const int n = f->scaled->n;
+  if (n == 0) return GS_OK;
+  cudaStream_t s = ctx->stream;
+  gs_layout& Ly = f->lay[layout];
+  GS_CUDA(ctx, cudaMemcpyAsync(Ly.order, order, (size_t)n * sizeof(int),
+                               mem == GS_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+  GS_CUDA(ctx, cudaMemsetAsync(Ly.newpos, 0xff, (size_t)n * sizeof(int), s));
+  DevBuf<int> bad;
+  GS_CUDA(ctx, bad.alloc(1, s));
+  GS_CUDA(ctx, cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+  gs_launch_begin(ctx, 1);
+  k_newpos_from_order<<<(n + 255) / 256, 256, 0, s>>>(Ly.order, n, Ly.newpos, bad.get());
+  gs_launch_end(ctx, 1);
+  int hb = 0;
+  GS_CUDA(ctx, cudaMemcpyAsync(&hb, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  if (hb) {  // restore a valid state: identity
+    std::vector<int> id(n);
+    for (int i = 0; i < n; ++i) id[i] = i;
+    cudaMemcpy(Ly.order, id.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice);
+    cudaMemcpy(Ly.newpos, id.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice);
+    finish_layout(ctx, f, layout);
+    return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "gs_filter_set_order: order is not a permutation of 0..n-1");
+  }
+  return finish_layout(ctx, f, layout);
 }
 
 // heat.cpp:116-131

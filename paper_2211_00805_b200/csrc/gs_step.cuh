@@ -33,6 +33,10 @@
 namespace gsk {
 
 constexpr int kThreads = 256;
+#ifndef GS_STEP_THREADS
+#define GS_STEP_THREADS 256
+#endif
+constexpr int kStepThreads = GS_STEP_THREADS;  // threads of a k_cheb_step CTA
 #ifndef GS_ROWS_PER_CTA
 #define GS_ROWS_PER_CTA 4
 #endif
@@ -81,17 +85,30 @@ struct Prec<float> {
 #ifndef GS_NARROW_MAX_BYTES
 #define GS_NARROW_MAX_BYTES 64  // widest row (GW * sizeof(S)) laid out as "narrow"
 #endif
+// bytes per lane for wide rows (GW * sizeof(S) > GS_NARROW_MAX_BYTES): 16 = one 512-byte fp64 row
+// per warp; 32 or 64 put 2 or 4 rows in a warp, so one shuffle broadcasts (col, val) to all of
+// them (measured slower for fp64 config 1: 164 vs 148 us)
+#ifndef GS_WIDE_VEC_BYTES64
+#define GS_WIDE_VEC_BYTES64 16
+#endif
+#ifndef GS_WIDE_VEC_BYTES32
+#define GS_WIDE_VEC_BYTES32 16
+#endif
 template <int GW, typename S>
 struct Lay {
   static constexpr bool NARROW = GW * (int)sizeof(S) <= GS_NARROW_MAX_BYTES && GW * (int)sizeof(S) > 16;
-  static constexpr int VB = NARROW ? GS_NARROW_VEC_BYTES : 16;
+  static constexpr bool WIDE = GW * (int)sizeof(S) > GS_NARROW_MAX_BYTES;
+  static constexpr int WVB = sizeof(S) == 8 ? GS_WIDE_VEC_BYTES64 : GS_WIDE_VEC_BYTES32;
+  static constexpr int VB = NARROW ? GS_NARROW_VEC_BYTES : (WIDE ? WVB : 16);
   static constexpr int VEC = GW * (int)sizeof(S) >= VB ? (VB >= (int)sizeof(S) ? VB / (int)sizeof(S) : 1) : GW;
   static constexpr int LPR = GW / VEC;                 // lanes per row
   static constexpr int RPW = 32 / LPR;                 // rows per warp
-  static constexpr int ROWS = (kThreads / 32) * RPW;   // rows per CTA block
+  static constexpr int ROWS = (kStepThreads / 32) * RPW;  // rows per CTA block
   // gathers in flight per row: narrow rows have few registers per gather, so go deeper
+  // wider lanes keep the bytes in flight per lane: batch scaled down by VB / 16
+  static constexpr int GBW0 = (sizeof(S) == 4 ? kGatherBatch32 : kGatherBatch) * 16 / (VB > 16 ? VB : 16);
   static constexpr int GB = NARROW ? (GS_NARROW_GATHER_BATCH < LPR ? GS_NARROW_GATHER_BATCH : LPR)
-                                   : (sizeof(S) == 4 ? kGatherBatch32 : kGatherBatch);
+                                   : (GBW0 < 1 ? 1 : GBW0);
 };
 
 // order-preserving uint64 keys for doubles (atomic min/max of signed values)
@@ -110,7 +127,16 @@ constexpr unsigned long long KEY_ZERO = 0x8000000000000000ull;     // dkey(+0.0)
 // array stays in registers)
 template <typename S, int VEC, bool RO>
 __device__ __forceinline__ void ld_vec_impl(const S* p, S (&v)[VEC]) {
-  if constexpr (std::is_same<S, double>::value && VEC == 2) {
+  if constexpr (VEC * sizeof(S) > 16) {  // several 16-byte chunks
+    constexpr int C = 16 / (int)sizeof(S);
+#pragma unroll
+    for (int h = 0; h < VEC / C; ++h) {
+      S t[C];
+      ld_vec_impl<S, C, RO>(p + h * C, t);
+#pragma unroll
+      for (int e = 0; e < C; ++e) v[h * C + e] = t[e];
+    }
+  } else if constexpr (std::is_same<S, double>::value && VEC == 2) {
     const double2 t = RO ? __ldg(reinterpret_cast<const double2*>(p)) : *reinterpret_cast<const double2*>(p);
     v[0] = t.x;
     v[1] = t.y;
@@ -139,7 +165,16 @@ __device__ __forceinline__ void ld_vec_rw(const S* p, S (&v)[VEC]) {
 }
 template <typename S, int VEC>
 __device__ __forceinline__ void st_vec(S* p, const S (&v)[VEC]) {
-  if constexpr (std::is_same<S, double>::value && VEC == 2) {
+  if constexpr (VEC * sizeof(S) > 16) {
+    constexpr int C = 16 / (int)sizeof(S);
+#pragma unroll
+    for (int h = 0; h < VEC / C; ++h) {
+      S t[C];
+#pragma unroll
+      for (int e = 0; e < C; ++e) t[e] = v[h * C + e];
+      st_vec<S, C>(p + h * C, t);
+    }
+  } else if constexpr (std::is_same<S, double>::value && VEC == 2) {
     *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
   } else if constexpr (std::is_same<S, float>::value && VEC == 4) {
     *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
@@ -397,7 +432,7 @@ __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, in
 }
 
 // CTA-level fold of the epilogue partials: min/max by atomics on keys, error partial per tile.
-template <typename S, int GW, int MODE>
+template <typename S, int GW, int MODE, int NT = kStepThreads>
 __device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int tile, int warp, int sub,
                                                int q, double (&mn)[Lay<GW, S>::VEC],
                                                double (&mx)[Lay<GW, S>::VEC],
@@ -413,7 +448,7 @@ __device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int til
       er[e] = er[e] + __shfl_xor_sync(0xffffffffu, er[e], off);
     }
   }
-  __shared__ double s_mn[kThreads / 32][GW], s_mx[kThreads / 32][GW], s_er[kThreads / 32][GW];
+  __shared__ double s_mn[NT / 32][GW], s_mx[NT / 32][GW], s_er[NT / 32][GW];
   if (sub == 0) {
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
@@ -427,7 +462,7 @@ __device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int til
     const int c = threadIdx.x;
     double a_mn = s_mn[0][c], a_mx = s_mx[0][c], a_er = s_er[0][c];
 #pragma unroll
-    for (int w = 1; w < kThreads / 32; ++w) {
+    for (int w = 1; w < NT / 32; ++w) {
       a_mn = fmin(a_mn, s_mn[w][c]);
       a_mx = fmax(a_mx, s_mx[w][c]);
       a_er = a_er + s_er[w][c];
@@ -450,12 +485,13 @@ __device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int til
 #define GS_MIN_BLOCKS32 6
 #endif
 template <typename S, int GW, int MODE, int RPC>
-__global__ void __launch_bounds__(kThreads, MODE != MODE_NONE ? 0 : (sizeof(S) == 4 ? GS_MIN_BLOCKS32 : GS_MIN_BLOCKS))
+__global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0 : (sizeof(S) == 4 ? GS_MIN_BLOCKS32 : GS_MIN_BLOCKS))
     k_cheb_step(const StepArgs A) {
   using L = Lay<GW, S>;
   constexpr int VEC = L::VEC, LPR = L::LPR, RPW = L::RPW;
-  constexpr int BLOCK_ROWS = (kThreads / 32) * RPW;
-  constexpr bool PREFETCH = VEC * sizeof(S) == 16;
+  constexpr int BLOCK_ROWS = (kStepThreads / 32) * RPW;
+  constexpr bool PREFETCH = VEC * sizeof(S) >= 16 && (VEC * sizeof(S)) % 16 == 0;
+  constexpr int CH = (int)(VEC * sizeof(S) / 16);  // 16-byte cp.async chunks per operand
   if (A.status && (A.status->error || A.status->done)) return;
   const int tl = blockIdx.x / A.Gl;
   const int tile = A.tile0 + tl;
@@ -473,7 +509,7 @@ __global__ void __launch_bounds__(kThreads, MODE != MODE_NONE ? 0 : (sizeof(S) =
   const int base = A.row0 + tl * (BLOCK_ROWS * RPC) + warp * RPW + sub;
   if constexpr (PREFETCH) {
     constexpr int STG = kPrefetchStages;
-    constexpr int PS = kThreads * VEC;  // elements per operand per stage
+    constexpr int PS = kStepThreads * VEC;  // elements per operand per stage
     __shared__ __align__(16) S s_pre[STG][3][PS];
     const size_t gbase = (size_t)g * A.ld * GW + q * VEC;
     auto issue = [&](int j) {
@@ -481,9 +517,14 @@ __global__ void __launch_bounds__(kThreads, MODE != MODE_NONE ? 0 : (sizeof(S) =
       if (j < RPC && row < A.n && A.k != 0) {
         const size_t idx = gbase + (size_t)row * GW;
         S* d = &s_pre[j % STG][0][threadIdx.x * VEC];
-        cp_async16(d, static_cast<const S*>(A.Tprev) + idx);
-        if (A.k >= 2) cp_async16(d + PS, static_cast<const S*>(A.Tout) + idx);
-        if (A.acc_terms > 0 && !A.acc_init) cp_async16(d + 2 * PS, static_cast<const S*>(A.acc) + idx);
+        constexpr int CE = 16 / (int)sizeof(S);
+#pragma unroll
+        for (int h = 0; h < CH; ++h) {
+          cp_async16(d + h * CE, static_cast<const S*>(A.Tprev) + idx + h * CE);
+          if (A.k >= 2) cp_async16(d + PS + h * CE, static_cast<const S*>(A.Tout) + idx + h * CE);
+          if (A.acc_terms > 0 && !A.acc_init)
+            cp_async16(d + 2 * PS + h * CE, static_cast<const S*>(A.acc) + idx + h * CE);
+        }
       }
       cp_async_commit();
     };
@@ -534,7 +575,7 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step_w1(const StepArgs A) {
     }
     if (lane == 0) finish_row<S, 1, MODE>(A, g, row, 0, y, mn, mx, er, nullptr, 0);
   }
-  if constexpr (MODE != MODE_NONE) block_epilogue<S, 1, MODE>(A, g, A.tile0 + tl, warp, lane, 0, mn, mx, er);
+  if constexpr (MODE != MODE_NONE) block_epilogue<S, 1, MODE, kThreads>(A, g, A.tile0 + tl, warp, lane, 0, mn, mx, er);
 }
 
 }  // namespace gsk

@@ -415,6 +415,15 @@ class HeatFilter:
                                                       _capi.GS_MEM_HOST))
         return out
 
+    def set_vertex_order(self, order, layout: int = 0) -> None:
+        """Engine tuning: replace the locality order of a layout (0: wide column groups, 1: narrow
+        ones) with order[new] = old. Results are unchanged; only gather locality moves."""
+        o = np.ascontiguousarray(order, np.int32)
+        if o.shape != (self._n,):
+            raise Error(errc.invalid_argument, "order must have n entries")
+        self._ctx.check(self._ctx.lib.gs_filter_set_order(self._ctx.handle, self._h, int(layout),
+                                                          _ptr(o), _capi.GS_MEM_HOST))
+
     def apply(self, f, fp32: bool = False) -> np.ndarray:
         """heat.cpp:98-131: (n,) vector or row-major (n, B) signals. fp32=True runs the optional
         fp32 mode (vectors and L_s in fp32; results returned as float64)."""

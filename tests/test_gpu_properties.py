@@ -171,3 +171,41 @@ def test_reruns_are_bit_identical(gs):
     for x, y in zip(one, two):
         assert np.array_equal(x.v, y.v) and np.array_equal(x.w, y.w)
         assert (x.cost, x.kl, x.iterations, x.marginal_error) == (y.cost, y.kl, y.iterations, y.marginal_error)
+
+
+def test_caller_locality_order_is_result_neutral(gs):
+    """gs_filter_set_order: any vertex order of either layout gives bit-identical applies and
+    Sinkhorn scalings (rows keep their entries in the original column order); a non-permutation
+    is rejected with invalid_argument."""
+    from paper_2211_00805_b200.rng import Rng
+    n = 300
+    f = _filter(gs, n, 11, 0, 1.0, 30)
+    X = np.stack([random_signal(n, Rng(20 + q)) for q in range(64)], axis=1)
+    X8 = X[:, :8].copy()
+    mus = [random_distribution(n, Rng(40 + p)) for p in range(3)]
+    nus = [random_distribution(n, Rng(50 + p)) for p in range(3)]
+    a = np.full(n, 1.0 / n)
+    prm = gs.SinkhornParams(60, 1e-11)
+
+    def run():
+        res = gs.geodesic_sinkhorn_batch(f, [gs.Distribution(m) for m in mus],
+                                         [gs.Distribution(x) for x in nus], a, prm)
+        return f.apply(X), f.apply(X8), [(r.v.copy(), r.w.copy(), r.cost, r.iterations) for r in res]
+
+    base = run()
+    perm = np.random.default_rng(3).permutation(n).astype(np.int32)
+    f.set_vertex_order(perm, 0)
+    f.set_vertex_order(perm[::-1].copy(), 1)
+    got = run()
+    assert np.array_equal(base[0], got[0]) and np.array_equal(base[1], got[1])
+    for (v0, w0, c0, i0), (v1, w1, c1, i1) in zip(base[2], got[2]):
+        # v, w and the sweep count are bit-identical; the cost is a tree sum over vertices in
+        # layout order (DESIGN §3), so it may move by an ulp
+        assert np.array_equal(v0, v1) and np.array_equal(w0, w1) and i0 == i1
+        assert abs(c0 - c1) <= 1e-14 * abs(c0)
+    bad = perm.copy()
+    bad[0] = bad[1]
+    with pytest.raises(gs.Error) as e:
+        f.set_vertex_order(bad, 0)
+    assert e.value.code == gs.errc.invalid_argument
+    assert np.array_equal(f.apply(X), base[0])  # the identity fallback is still a valid order
