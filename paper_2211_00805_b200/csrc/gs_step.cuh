@@ -57,6 +57,35 @@ constexpr int kGatherBatch32 = GS_GATHER_BATCH32;  // wide fp32 rows (fewer regi
 #endif
 constexpr int kPrefetchStages = GS_PREFETCH_STAGES;
 
+// CSR index prefetch (several lanes per row): the (col, val) chunk a row needs next is loaded
+// while the current chunk's gathers are in flight -- the next LPR entries of the same row
+// (GS_IDX_PREFETCH) and the first chunk of the warp's next row block (GS_ROW_PREFETCH), so the
+// CSR stream's DRAM latency is not a link of the dependent index -> gather chain
+#ifndef GS_IDX_PREFETCH
+#define GS_IDX_PREFETCH 1
+#endif
+#ifndef GS_ROW_PREFETCH
+#define GS_ROW_PREFETCH 0  // measured neutral-to-slower on config 1 (one chunk per row)
+#endif
+// own-row operands of the wide layouts staged by TMA bulk copies (one per warp and operand,
+// completion on a per-warp mbarrier) instead of per-thread cp.async: the copies bypass the LSU
+// data pipe, which the gathers and shuffles keep ~70% busy
+// 0 = cp.async per thread, 1 = one bulk copy per warp, 2 = one per CTA row block (CTA barrier).
+// Measured on config 1: fp64 128-130 us (cp.async) vs 152 (per warp) and 142 (per CTA); fp32
+// mode 172 -> 189 sweeps/s with per-warp copies.
+#ifndef GS_TMA_OWN64
+#define GS_TMA_OWN64 0
+#endif
+#ifndef GS_TMA_OWN32
+#define GS_TMA_OWN32 1
+#endif
+
+template <typename S>
+struct RowIdx {  // a row's CSR range and this lane's entry of its first chunk
+  int pb = 0, pe = 0, c = 0;
+  S v = S(0);
+};
+
 enum StepMode { MODE_NONE = 0, MODE_SK_PSI = 1, MODE_SK_PHI = 2, MODE_BARY_PSI = 3 };
 
 // ---- precision traits --------------------------------------------------------------------------
@@ -196,6 +225,34 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
@@ -253,7 +310,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
                                          double (&mn)[Lay<GW, S>::VEC],
                                          double (&mx)[Lay<GW, S>::VEC],
                                          double (&er)[Lay<GW, S>::VEC], const S* pre,
-                                         int pre_stride) {
+                                         int pre_stride, const RowIdx<S>& ri) {
   using L = Lay<GW, S>;
   constexpr int VEC = L::VEC, LPR = L::LPR;
   using P = Prec<S>;
@@ -300,15 +357,25 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
     // and broadcast them by shuffle; the fma chain still runs in CSR order.
     const int sub_lane0 = sub * LPR;
     const unsigned mask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << sub_lane0);
-    const int pb = valid ? __ldg(A.offs + row) : 0;
-    const int pe = valid ? __ldg(A.offs + row + 1) : 0;
+    const int pb = ri.pb, pe = ri.pe;  // first chunk loaded by the caller (k_cheb_step)
     constexpr int GB = L::GB;
+    int myc = ri.c;
+    S myv = ri.v;
     for (int p0 = pb; p0 < pe; p0 += LPR) {
-      int myc = 0;
-      S myv = S(0);
-      if (p0 + q < pe) {
-        myc = ld_idx(A.cols + p0 + q);
-        myv = ld_idx(vals + p0 + q);
+      int nxc = 0;
+      S nxv = S(0);
+      if constexpr (GS_IDX_PREFETCH) {
+        if (p0 + LPR + q < pe) {
+          nxc = ld_idx(A.cols + p0 + LPR + q);
+          nxv = ld_idx(vals + p0 + LPR + q);
+        }
+      } else if (p0 > pb) {
+        myc = 0;
+        myv = S(0);
+        if (p0 + q < pe) {
+          myc = ld_idx(A.cols + p0 + q);
+          myv = ld_idx(vals + p0 + q);
+        }
       }
       const int cnt = min(LPR, pe - p0);
       int u = 0;
@@ -335,6 +402,10 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
         ld_vec<S, VEC>(Tp + (size_t)c * GW, x);
 #pragma unroll
         for (int e = 0; e < VEC; ++e) y[e] = P::fmat(v, x[e], y[e]);
+      }
+      if constexpr (GS_IDX_PREFETCH) {
+        myc = nxc;
+        myv = nxv;
       }
     }
   }
@@ -507,10 +578,41 @@ __global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0 : (sizeof(
     er[e] = 0.0;
   }
   const int base = A.row0 + tl * (BLOCK_ROWS * RPC) + warp * RPW + sub;
+  // CSR ranges of this lane group's RPC rows: lane q < RPC holds block q's (pb, pe)
+  static_assert(LPR == 1 || LPR >= RPC, "one lane per row block holds its offsets");
+  int o_pb = 0, o_pe = 0;
+  if constexpr (LPR > 1) {
+    const int r = base + q * BLOCK_ROWS;
+    if (q < RPC && r < A.n) {
+      o_pb = __ldg(A.offs + r);
+      o_pe = __ldg(A.offs + r + 1);
+    }
+  }
+  const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << (LPR & 31)) - 1u) << (sub * LPR));
+  auto row_idx = [&](int j) {  // block j's range and this lane's first-chunk entry
+    RowIdx<S> ri;
+    if constexpr (LPR > 1) {
+      ri.pb = __shfl_sync(gmask, o_pb, j, LPR);
+      ri.pe = __shfl_sync(gmask, o_pe, j, LPR);
+      if (ri.pb + q < ri.pe) {
+        ri.c = ld_idx(A.cols + ri.pb + q);
+        ri.v = ld_idx(static_cast<const S*>(A.vals) + ri.pb + q);
+      }
+    }
+    return ri;
+  };
+  RowIdx<S> cur = row_idx(0);
+  auto next_idx = [&](int j) {  // row j's index state, prefetched one row block ahead
+    RowIdx<S> nx;
+    if constexpr (GS_ROW_PREFETCH) {
+      if (j + 1 < RPC) nx = row_idx(j + 1);
+    }
+    return nx;
+  };
   if constexpr (PREFETCH) {
     constexpr int STG = kPrefetchStages;
     constexpr int PS = kStepThreads * VEC;  // elements per operand per stage
-    __shared__ __align__(16) S s_pre[STG][3][PS];
+    __shared__ __align__(128) S s_pre[STG][3][PS];
     const size_t gbase = (size_t)g * A.ld * GW + q * VEC;
     auto issue = [&](int j) {
       const int row = base + j * BLOCK_ROWS;
@@ -528,19 +630,80 @@ __global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0 : (sizeof(
       }
       cp_async_commit();
     };
+    constexpr int TMA = sizeof(S) == 8 ? GS_TMA_OWN64 : GS_TMA_OWN32;
+    if constexpr (TMA != 0) {
+      // warp w's RPW rows of block j are one contiguous RPW * GW * sizeof(S) byte run in global
+      // memory and in s_pre (slot = thread * VEC); lane 0 copies it per operand
+      // TMA == 2: the CTA's BLOCK_ROWS rows of block j, one copy per operand by thread 0
+      constexpr int NB = TMA == 1 ? kStepThreads / 32 : 1;
+      __shared__ __align__(8) unsigned long long s_bar[NB][STG];
+      constexpr int WE = TMA == 1 ? RPW * GW : 0;  // elements per warp per operand
+      constexpr int CR = TMA == 1 ? RPW : BLOCK_ROWS;  // rows per copy
+      const int bw = TMA == 1 ? warp : 0;
+      const bool issuer = TMA == 1 ? lane == 0 : threadIdx.x == 0;
+      if (issuer) {
+#pragma unroll
+        for (int st = 0; st < STG; ++st) mbar_init(&s_bar[bw][st], 1);
+        fence_proxy_async();
+      }
+      if constexpr (TMA == 1) __syncwarp(); else __syncthreads();
+      const int wrow0 = TMA == 1 ? base - sub : A.row0 + tl * (BLOCK_ROWS * RPC);  // first row, block 0
+      auto rows_of = [&](int j) {
+        const int r0 = wrow0 + j * BLOCK_ROWS;
+        return (j < RPC && A.k != 0) ? max(0, min(CR, A.n - r0)) : 0;
+      };
+      auto tissue = [&](int j) {
+        const int nr = rows_of(j);
+        if (issuer && nr > 0) {
+          const unsigned bytes = (unsigned)(nr * GW * sizeof(S));
+          const size_t off = (size_t)g * A.ld * GW + (size_t)(wrow0 + j * BLOCK_ROWS) * GW;
+          const bool t2 = A.k >= 2, ac = A.acc_terms > 0 && !A.acc_init;
+          unsigned long long* bar = &s_bar[bw][j % STG];
+          fence_proxy_async();
+          mbar_expect_tx(bar, bytes * (1u + (t2 ? 1u : 0u) + (ac ? 1u : 0u)));
+          S* d = &s_pre[j % STG][0][bw * WE];
+          bulk_g2s(d, static_cast<const S*>(A.Tprev) + off, bytes, bar);
+          if (t2) bulk_g2s(d + PS, static_cast<const S*>(A.Tout) + off, bytes, bar);
+          if (ac) bulk_g2s(d + 2 * PS, static_cast<const S*>(A.acc) + off, bytes, bar);
+        }
+      };
+#pragma unroll
+      for (int j = 0; j < STG - 1; ++j) tissue(j);
+#pragma unroll 1
+      for (int j = 0; j < RPC; ++j) {
+        // every thread is done with the stage tissue() refills
+        if constexpr (TMA == 1) __syncwarp(); else __syncthreads();
+        tissue(j + STG - 1);
+        if (!GS_ROW_PREFETCH && j > 0) cur = row_idx(j);
+        const RowIdx<S> nx = next_idx(j);
+        if (rows_of(j) > 0) mbar_wait(&s_bar[bw][j % STG], (unsigned)((j / STG) & 1));
+        cheb_row<S, GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er,
+                              &s_pre[j % STG][0][threadIdx.x * VEC], PS, cur);
+        cur = nx;
+      }
+      if constexpr (MODE != MODE_NONE) block_epilogue<S, GW, MODE>(A, g, tile, warp, sub, q, mn, mx, er);
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < STG - 1; ++j) issue(j);
 #pragma unroll 1
     for (int j = 0; j < RPC; ++j) {
       issue(j + STG - 1);
+      if (!GS_ROW_PREFETCH && j > 0) cur = row_idx(j);
+      const RowIdx<S> nx = next_idx(j);
       cp_async_wait<STG - 1>();
       cheb_row<S, GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er,
-                            &s_pre[j % STG][0][threadIdx.x * VEC], PS);
+                            &s_pre[j % STG][0][threadIdx.x * VEC], PS, cur);
+      cur = nx;
     }
   } else {
 #pragma unroll 1
-    for (int j = 0; j < RPC; ++j)
-      cheb_row<S, GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er, nullptr, 0);
+    for (int j = 0; j < RPC; ++j) {
+      if (!GS_ROW_PREFETCH && j > 0) cur = row_idx(j);
+      const RowIdx<S> nx = next_idx(j);
+      cheb_row<S, GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er, nullptr, 0, cur);
+      cur = nx;
+    }
   }
   if constexpr (MODE != MODE_NONE) block_epilogue<S, GW, MODE>(A, g, tile, warp, sub, q, mn, mx, er);
 }
