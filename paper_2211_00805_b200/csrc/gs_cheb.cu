@@ -545,6 +545,19 @@ void launch_step_gw(const StepArgs& A, int mode, int rpc, cudaStream_t s) {
 template <typename S>
 void launch_step(gs_ctx* ctx, int gw, int rpc, const StepArgs& A, int mode) {
   gs_launch_begin(ctx, 0);
+  if constexpr (sizeof(S) == 8) {
+    if (A.rec_key) {  // 8-row block records (wide fp64 rows)
+      const dim3 grid((unsigned)(A.tiles * A.Gl));
+      switch (mode) {
+        case MODE_NONE: k_cheb_blk<S, MODE_NONE><<<grid, kBlkWarps * 32, 0, ctx->stream>>>(A); break;
+        case MODE_SK_PSI: k_cheb_blk<S, MODE_SK_PSI><<<grid, kBlkWarps * 32, 0, ctx->stream>>>(A); break;
+        case MODE_SK_PHI: k_cheb_blk<S, MODE_SK_PHI><<<grid, kBlkWarps * 32, 0, ctx->stream>>>(A); break;
+        default: k_cheb_blk<S, MODE_BARY_PSI><<<grid, kBlkWarps * 32, 0, ctx->stream>>>(A); break;
+      }
+      gs_launch_end(ctx, 0);
+      return;
+    }
+  }
   if (A.warp_rows) {  // small one-column problems: one warp per row
     const dim3 grid((unsigned)(A.tiles * A.Gl));
     switch (mode) {
@@ -568,6 +581,112 @@ void launch_step(gs_ctx* ctx, int gw, int rpc, const StepArgs& A, int mode) {
   gs_launch_end(ctx, 0);
 }
 
+// GS_BLK=1 runs wide fp64 rows through the 8-row block kernel (k_cheb_blk). Off by default:
+// it halves the gathered sectors (23.8M vs 49.7M per config-1 step) but doubles the
+// instructions (predicated per-record fold) at 88 registers, 238 vs 117 us.
+// Read per call, so tests can switch it.
+inline bool blk_enabled() {
+  const char* e = getenv("GS_BLK");
+  return e && atoi(e) != 0;
+}
+
+__global__ void k_blk_keys(const int* __restrict__ offs, const int* __restrict__ cols,
+                           const int* __restrict__ order, int n, unsigned long long* keys, int* idx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long b = (unsigned long long)(i >> 3), r = (unsigned long long)(i & 7);
+  for (int p = offs[i]; p < offs[i + 1]; ++p) {
+    const unsigned long long oc = (unsigned)order[cols[p]];  // original column id
+    keys[p] = (b << 34) | (oc << 3) | r;
+    idx[p] = p;
+  }
+}
+
+__global__ void k_blk_fill(const unsigned long long* __restrict__ keys, const int* __restrict__ idx,
+                           const int* __restrict__ cols, const double* __restrict__ vals, int64_t nnz,
+                           int* rec_key, double* rec_val) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nnz) return;
+  const int p = idx[j];
+  rec_key[j] = (cols[p] << 3) | (int)(keys[j] & 7ull);
+  rec_val[j] = vals[p];
+}
+
+// 8-row block records of layout `l` (gs_layout::rec_key / rec_val), built once.
+int gs_build_block_records(gs_ctx* ctx, gs_filter* f, int l) {
+  gs_layout& Ly = f->lay[l];
+  if (Ly.rec_key) return GS_OK;
+  const gs_graph* G = Ly.perm;
+  const int n = G->n;
+  const int64_t nnz = G->nnz;
+  if (n >= (1 << 28) || nnz >= (int64_t)INT32_MAX)
+    return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "block records: graph too large");
+  cudaStream_t s = ctx->stream;
+  DevBuf<unsigned long long> k0, k1;
+  DevBuf<int> i0, i1;
+  GS_CUDA(ctx, k0.alloc(nnz, s));
+  GS_CUDA(ctx, k1.alloc(nnz, s));
+  GS_CUDA(ctx, i0.alloc(nnz, s));
+  GS_CUDA(ctx, i1.alloc(nnz, s));
+  if (n > 0) {
+    gs_launch_begin(ctx, 1);
+    k_blk_keys<<<(n + 255) / 256, 256, 0, s>>>(G->offs, G->cols, Ly.order, n, k0.get(), i0.get());
+    gs_launch_end(ctx, 1);
+  }
+  size_t tb = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.get(), k1.get(), i0.get(), i1.get(), (int)nnz, 0, 64, s);
+  DevBuf<unsigned char> tmp;
+  GS_CUDA(ctx, tmp.alloc(tb, s));
+  cub::DeviceRadixSort::SortPairs(tmp.get(), tb, k0.get(), k1.get(), i0.get(), i1.get(), (int)nnz, 0, 64, s);
+  if (cudaMalloc((void**)&Ly.rec_key, (size_t)(nnz ? nnz : 1) * sizeof(int)) != cudaSuccess ||
+      cudaMalloc((void**)&Ly.rec_val, (size_t)(nnz ? nnz : 1) * sizeof(double)) != cudaSuccess) {
+    cudaFree(Ly.rec_key);
+    Ly.rec_key = nullptr;
+    return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "block record allocation failed");
+  }
+  if (nnz > 0) {
+    gs_launch_begin(ctx, 1);
+    k_blk_fill<<<(unsigned)((nnz + 255) / 256), 256, 0, s>>>(k1.get(), i1.get(), G->cols, G->vals, nnz,
+                                                               Ly.rec_key, Ly.rec_val);
+    gs_launch_end(ctx, 1);
+  }
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  return GS_OK;
+}
+
+// GS_L2_PERSIST=1: the Chebyshev vectors T_{k-1} / T_k (gathered every step) are marked L2-
+// persisting through the stream's access-policy window (kernel nodes captured into the sweep
+// graphs inherit it), so the once-per-step streams (CSR, T_{k-2}, acc) do not evict them.
+struct L2Window {
+  cudaStream_t s = nullptr;
+  bool on = false;
+  L2Window(gs_ctx* ctx, const void* base, size_t bytes) {
+    const char* e = getenv("GS_L2_PERSIST");
+    if (!(e && atoi(e) != 0) || bytes == 0) return;
+    int dev = 0, maxp = 0, maxw = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    if (maxp <= 0 || maxw <= 0) return;
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)maxp) != cudaSuccess) return;
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    v.accessPolicyWindow.num_bytes = std::min(bytes, (size_t)maxw);
+    v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)maxp / (double)v.accessPolicyWindow.num_bytes);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    s = ctx->stream;
+    on = cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
+  }
+  ~L2Window() {
+    if (!on) return;
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaCtxResetPersistingL2Cache();
+  }
+};
+
 // Workspace for one batched run: grouped buffers (precision S) + per-column state.
 template <typename S>
 struct Work {
@@ -575,7 +694,13 @@ struct Work {
   int64_t ld = 0;  // rows per column group: n, or local + halo rows of a row partition
   int lay = 0;  // filter layout: 0 for one-warp-per-row groups, 1 (degree-sorted) for narrower
   bool w1 = false;  // one-column fp64 problem small enough for the warp-per-row kernel
-  DevBuf<S> T[2], acc;
+  bool blk = false;  // wide fp64 rows through the 8-row block kernel (k_cheb_blk)
+  struct TView {  // T[0], T[1]: halves of one allocation (one L2 access-policy window covers both)
+    S* p = nullptr;
+    S* get() const { return p; }
+  };
+  DevBuf<S> Tall, acc;
+  TView T[2];
   DevBuf<unsigned long long> cmin, cmax;
   DevBuf<double> thr, errcol, part_err;
   DevBuf<int> active, gactive;
@@ -593,9 +718,15 @@ struct Work {
     tiles = (n + rows_per_block<S>(GW) * rpc - 1) / (rows_per_block<S>(GW) * rpc);
     w1 = GW == 1 && sizeof(S) == 8 && n <= w1_max_rows();
     if (w1) tiles = (n + kThreads / 32 - 1) / (kThreads / 32);
+    if (sizeof(S) == 8 && GW == 64 && f && ld_ < 0 && blk_enabled()) {  // not for row partitions
+      GS_TRY(gs_build_block_records(ctx, const_cast<gs_filter*>(f), lay));
+      blk = true;
+      tiles = (n + kBlkRows * kBlkWarps - 1) / (kBlkRows * kBlkWarps);
+    }
     const size_t len = (size_t)Bpad * (ld > 0 ? ld : 1);
-    GS_CUDA(ctx, T[0].alloc(len, s));
-    GS_CUDA(ctx, T[1].alloc(len, s));
+    GS_CUDA(ctx, Tall.alloc(2 * len, s));
+    T[0].p = Tall.get();
+    T[1].p = Tall.get() + len;
     GS_CUDA(ctx, acc.alloc(len, s));
     GS_CUDA(ctx, cmin.alloc(Bpad, s));
     GS_CUDA(ctx, cmax.alloc(Bpad, s));
@@ -675,6 +806,10 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
   A.cols = G->cols;
   A.vals = layout_vals<S>(Ly);
   A.warp_rows = w.w1;
+  if (w.blk) {
+    A.rec_key = Ly.rec_key;
+    A.rec_val = Ly.rec_val;
+  }
   A.n = w.n;
   A.ld = w.ld;
   A.tiles = w.tiles;
@@ -824,6 +959,7 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   cudaStream_t s = ctx->stream;
   Work<S> w;
   GS_TRY(w.init(ctx, n, P, true, -1, f));
+  L2Window l2w(ctx, w.Tall.get(), w.Tall.n * sizeof(S));
   // vertex weights in the filter's locality order and the engine precision
   DevBuf<S> aperm;
   GS_CUDA(ctx, aperm.alloc(n, s));
@@ -1034,6 +1170,7 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   cudaStream_t s = ctx->stream;
   Work<S> w;
   GS_TRY(w.init(ctx, n, m, true, -1, f));
+  L2Window l2w(ctx, w.Tall.get(), w.Tall.n * sizeof(S));
   DevBuf<S> aperm;
   GS_CUDA(ctx, aperm.alloc(n, s));
   gs_launch_begin(ctx, 1);
@@ -1839,6 +1976,10 @@ static int finish_layout(gs_ctx* ctx, gs_filter* f, int l) {
   gs_layout& Ly = f->lay[l];
   gs_graph_destroy(Ly.perm);
   Ly.perm = nullptr;
+  cudaFree(Ly.rec_key);
+  cudaFree(Ly.rec_val);
+  Ly.rec_key = nullptr;
+  Ly.rec_val = nullptr;
   cudaFree(Ly.vals32);
   Ly.vals32 = nullptr;
   Ly.near_frac = 1.0;
@@ -1933,6 +2074,8 @@ extern "C" void gs_filter_destroy(gs_filter* f) {
     cudaFree(Ly.order);
     cudaFree(Ly.newpos);
     cudaFree(Ly.vals32);
+    cudaFree(Ly.rec_key);
+    cudaFree(Ly.rec_val);
   }
   cudaFree(f->d_coeffs);
   delete f;

@@ -72,6 +72,11 @@ struct gs_layout {
   int* newpos = nullptr;     // newpos[old] = new
   float* vals32 = nullptr;   // fp32 copy of perm->vals (optional fp32 mode)
   double near_frac = 1.0;    // fraction of entries within 256 rows of their row (L1 locality)
+  // 8-row block records (gs_step.cuh k_cheb_blk; built on first use by a wide fp64 run): the
+  // entries of rows [8b, 8b + 8) in positions [offs[8b], offs[8b + 8]) re-sorted by (original
+  // column, row), key = new column << 3 | row within the block
+  int* rec_key = nullptr;
+  double* rec_val = nullptr;
 };
 
 struct gs_filter {

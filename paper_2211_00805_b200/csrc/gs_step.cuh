@@ -290,6 +290,8 @@ struct StepArgs {  // vector pointers are S* of the launch's precision
   double bk1, bk2;    // b_{k-1}, b_{k-2}
   const gs_status* status;
   ColState cs;
+  const int* rec_key;  // k_cheb_blk: 8-row block records (gs_layout::rec_key / rec_val)
+  const void* rec_val;
   const void* a;      // n (epilogue)
   const void* M;      // PSI: N (targets); PHI: M (sources / members)
   const void* Vcur;   // PHI: V of this sweep
@@ -302,7 +304,7 @@ __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, in
                                            double (&mn)[Lay<GW, S>::VEC],
                                            double (&mx)[Lay<GW, S>::VEC],
                                            double (&er)[Lay<GW, S>::VEC], const S* pre,
-                                           int pre_stride);
+                                           int pre_stride, bool pre_tp = true);
 
 // One row of one Chebyshev step; epilogue partials accumulate in mn/mx/er (double).
 template <typename S, int GW, int MODE>
@@ -421,7 +423,7 @@ __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, in
                                            double (&mn)[Lay<GW, S>::VEC],
                                            double (&mx)[Lay<GW, S>::VEC],
                                            double (&er)[Lay<GW, S>::VEC], const S* pre,
-                                           int pre_stride) {
+                                           int pre_stride, bool pre_tp) {
   using L = Lay<GW, S>;
   constexpr int VEC = L::VEC;
   using P = Prec<S>;
@@ -434,12 +436,19 @@ __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, in
   // ---- own-row operands (prefetched into shared memory by cp.async when `pre`) ---------------
   const bool read_acc = A.acc_terms > 0 && !A.acc_init;
   S tp[VEC], t2[VEC], a0[VEC];
-  if (pre) {
+  if (pre && pre_tp) {
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
       tp[e] = pre[e];
       t2[e] = pre[pre_stride + e];
       a0[e] = pre[2 * pre_stride + e];
+    }
+  } else if (pre) {  // T_{k-2}, acc staged; T_{k-1}[row] read directly (L1-hot: just gathered)
+    ld_vec<S, VEC>(static_cast<const S*>(A.Tprev) + idx, tp);
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      t2[e] = pre[e];
+      a0[e] = pre[pre_stride + e];
     }
   } else {
     ld_vec<S, VEC>(static_cast<const S*>(A.Tprev) + idx, tp);
@@ -706,6 +715,166 @@ __global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0 : (sizeof(
     }
   }
   if constexpr (MODE != MODE_NONE) block_epilogue<S, GW, MODE>(A, g, tile, warp, sub, q, mn, mx, er);
+}
+
+// 8-row blocks (wide fp64 rows, one warp per block): the gathers of a block's rows are shared.
+// The block's entries are stored re-sorted by (ORIGINAL column, row): every row's entries appear
+// in its CSR order (from_triplets sorts rows by original column, sparse.cpp:15-53), so each of
+// the 8 per-row fma chains is unchanged -- bit-identical -- while a neighbour row referenced by
+// several rows of the block is gathered once. A warp holds the 8 rows' y (2 columns per lane),
+// reads 32 records per coalesced load, finds the records that start a new column (ballot), gathers
+// those rows GB at a time and folds each record into its row's chain. On config 1's Cuthill-McKee
+// order a block references 0.47 distinct rows per entry (SURVEY §8(d) gather model: 1 per entry).
+#ifndef GS_BLK_GATHER_BATCH
+#define GS_BLK_GATHER_BATCH 4
+#endif
+#ifndef GS_BLK_MIN_BLOCKS
+#define GS_BLK_MIN_BLOCKS 3
+#endif
+// stage the block's T_{k-2} and acc rows (2 x 4 KB per warp) with TMA bulk copies at block start
+#ifndef GS_BLK_STAGE
+#define GS_BLK_STAGE 1
+#endif
+constexpr int kBlkRows = 8;
+#ifndef GS_BLK_WARPS
+#define GS_BLK_WARPS 4
+#endif
+constexpr int kBlkWarps = GS_BLK_WARPS;  // warps (8-row blocks) per CTA
+
+template <typename S, int VEC>
+__device__ __forceinline__ void blk_fold(S (&y)[kBlkRows][VEC], int r, S v, const S (&x)[VEC]) {
+  switch (r) {  // warp-uniform: the record is broadcast
+#define GS_BLK_CASE(R)                                                          \
+  case R:                                                                       \
+    _Pragma("unroll") for (int e = 0; e < VEC; ++e) y[R][e] = Prec<S>::fmat(v, x[e], y[R][e]); \
+    break;
+    GS_BLK_CASE(0)
+    GS_BLK_CASE(1)
+    GS_BLK_CASE(2)
+    GS_BLK_CASE(3)
+    GS_BLK_CASE(4)
+    GS_BLK_CASE(5)
+    GS_BLK_CASE(6)
+    default:
+      _Pragma("unroll") for (int e = 0; e < VEC; ++e) y[7][e] = Prec<S>::fmat(v, x[e], y[7][e]);
+#undef GS_BLK_CASE
+  }
+}
+
+template <typename S, int MODE>
+__global__ void __launch_bounds__(kBlkWarps * 32, MODE != MODE_NONE ? 0 : GS_BLK_MIN_BLOCKS)
+    k_cheb_blk(const StepArgs A) {
+  constexpr int GW = 64;
+  using L = Lay<GW, S>;
+  constexpr int VEC = L::VEC;
+  static_assert(L::LPR == 32, "one warp per 64-column row");
+  constexpr int GB = GS_BLK_GATHER_BATCH;
+  if (A.status && (A.status->error || A.status->done)) return;
+  const int tl = blockIdx.x / A.Gl;
+  const int tile = A.tile0 + tl;
+  const int g = A.g0 + blockIdx.x % A.Gl;
+  if (A.cs.gactive && A.cs.gactive[g] == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double mn[VEC], mx[VEC], er[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    mn[e] = INFINITY;
+    mx[e] = 0.0;
+    er[e] = 0.0;
+  }
+  const int r0 = A.row0 + (tl * kBlkWarps + warp) * kBlkRows;
+  constexpr int RE = kBlkRows * GW;  // elements per staged operand
+  __shared__ __align__(128) S s_own[GS_BLK_STAGE ? kBlkWarps : 1][2][GS_BLK_STAGE ? RE : 1];
+  __shared__ __align__(8) unsigned long long s_obar[kBlkWarps];
+  const int nrows = max(0, min(kBlkRows, A.n - r0));
+  const bool t2 = A.k >= 2, ac = A.acc_terms > 0 && !A.acc_init;
+  const bool staged = GS_BLK_STAGE && nrows > 0 && A.k != 0 && (t2 || ac);
+  if constexpr (GS_BLK_STAGE) {
+    if (lane == 0) {
+      mbar_init(&s_obar[warp], 1);
+      fence_proxy_async();
+    }
+    __syncwarp();
+    if (staged && lane == 0) {
+      const unsigned bytes = (unsigned)(nrows * GW * sizeof(S));
+      const size_t off = (size_t)g * A.ld * GW + (size_t)r0 * GW;
+      mbar_expect_tx(&s_obar[warp], bytes * ((t2 ? 1u : 0u) + (ac ? 1u : 0u)));
+      if (t2) bulk_g2s(&s_own[warp][0][0], static_cast<const S*>(A.Tout) + off, bytes, &s_obar[warp]);
+      if (ac) bulk_g2s(&s_own[warp][1][0], static_cast<const S*>(A.acc) + off, bytes, &s_obar[warp]);
+    }
+  }
+  if (r0 < A.n) {
+    S y[kBlkRows][VEC];
+#pragma unroll
+    for (int r = 0; r < kBlkRows; ++r)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) y[r][e] = S(0);
+    const S* __restrict__ Tp = static_cast<const S*>(A.Tprev) + (size_t)g * A.ld * GW + lane * VEC;
+    const S* __restrict__ rv = static_cast<const S*>(A.rec_val);
+    const int pb = __ldg(A.offs + r0), pe = __ldg(A.offs + min(r0 + kBlkRows, A.n));
+    S xc[VEC];  // the row of the column that is current at a chunk boundary
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) xc[e] = S(0);
+    int prevc = -1;
+    int key = -1;
+    S val = S(0);
+    if (pb + lane < pe) {
+      key = __ldg(A.rec_key + pb + lane);
+      val = __ldg(rv + pb + lane);
+    }
+    for (int p0 = pb; p0 < pe; p0 += 32) {
+      const int cnt = min(32, pe - p0);
+      int nkey = -1;  // next chunk, in flight while this one is folded
+      S nval = S(0);
+      if (p0 + 32 + lane < pe) {
+        nkey = __ldg(A.rec_key + p0 + 32 + lane);
+        nval = __ldg(rv + p0 + 32 + lane);
+      }
+      const int col = key >> 3;
+      int up = __shfl_up_sync(0xffffffffu, col, 1);
+      if (lane == 0) up = prevc;
+      unsigned m = __ballot_sync(0xffffffffu, lane < cnt && col != up);
+      int u = 0;
+      const int first = m ? __ffs(m) - 1 : cnt;
+      for (; u < first; ++u)  // records of the column carried over from the last chunk
+        blk_fold<S, VEC>(y, __shfl_sync(0xffffffffu, key, u) & 7, __shfl_sync(0xffffffffu, val, u), xc);
+      while (m) {
+        int pos[GB];
+        S xx[GB][VEC];
+#pragma unroll
+        for (int j = 0; j < GB; ++j) {
+          pos[j] = m ? __ffs(m) - 1 : cnt;
+          m &= m ? m - 1 : 0u;
+          if (pos[j] < cnt) {
+            const int c = __shfl_sync(0xffffffffu, col, pos[j]);
+            ld_vec<S, VEC>(Tp + (size_t)c * GW, xx[j]);
+          }
+        }
+        const int tail = m ? __ffs(m) - 1 : cnt;
+#pragma unroll
+        for (int j = 0; j < GB; ++j) {
+          if (pos[j] < cnt) {
+            const int end = j + 1 < GB ? (pos[j + 1] < cnt ? pos[j + 1] : tail) : tail;
+            for (u = pos[j]; u < end; ++u)
+              blk_fold<S, VEC>(y, __shfl_sync(0xffffffffu, key, u) & 7, __shfl_sync(0xffffffffu, val, u), xx[j]);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) xc[e] = xx[j][e];
+          }
+        }
+      }
+      prevc = __shfl_sync(0xffffffffu, col, cnt - 1);
+      key = nkey;
+      val = nval;
+    }
+    if (staged) mbar_wait(&s_obar[warp], 0u);
+#pragma unroll
+    for (int r = 0; r < kBlkRows; ++r)
+      if (r0 + r < A.n)
+        finish_row<S, GW, MODE>(A, g, r0 + r, lane, y[r], mn, mx, er,
+                                staged ? &s_own[GS_BLK_STAGE ? warp : 0][0][(GS_BLK_STAGE ? r * GW : 0) + lane * VEC] : nullptr,
+                                GS_BLK_STAGE ? RE : 0, false);
+  }
+  if constexpr (MODE != MODE_NONE) block_epilogue<S, GW, MODE, kBlkWarps * 32>(A, g, tile, warp, 0, lane, mn, mx, er);
 }
 
 // Small one-column problems (config 0: n = 2000, B = 1) are latency-bound: with one row per lane a

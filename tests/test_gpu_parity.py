@@ -190,8 +190,10 @@ def _pairs(n, P, seed):
     return mus, nus
 
 
-@pytest.mark.parametrize("P", [1, 4, 9])
-def test_sinkhorn_batch_matches_oracle(gs, P):
+@pytest.mark.parametrize("blk", ["0", "1"])
+@pytest.mark.parametrize("P", [1, 4, 9, 40, 70])  # 40, 70: one warp per 64-column row, 1 / 2 groups
+def test_sinkhorn_batch_matches_oracle(gs, P, blk, monkeypatch):
+    monkeypatch.setenv("GS_BLK", blk)  # 1: the 8-row block kernel (opt-in) on the wide groups
     n = 120
     r, c, v = random_connected_graph(n, 21)
     f, _ = engine_filter(r, c, v, n, 1, 0.9, 30)
@@ -276,8 +278,10 @@ def test_distribution_validation(gs):
 
 
 # --------------------------------------------------------------------------- barycenter
-@pytest.mark.parametrize("m,kind", [(1, 1), (3, 1), (8, 0), (11, 1)])
-def test_barycenter_matches_oracle(gs, m, kind):
+@pytest.mark.parametrize("m,kind,blk", [(1, 1, "0"), (3, 1, "0"), (8, 0, "0"), (11, 1, "0"), (37, 0, "0"),
+                                        (37, 0, "1")])
+def test_barycenter_matches_oracle(gs, m, kind, blk, monkeypatch):
+    monkeypatch.setenv("GS_BLK", blk)
     n = 100
     r, c, v = random_connected_graph(n, 12)
     f, _ = engine_filter(r, c, v, n, kind, 0.8, 30)
@@ -394,3 +398,21 @@ def test_graph_file_round_trip(gs, tmp_path):
     with pytest.raises(gs.Error) as e:
         gs.load_graph(str(tmp_path / "missing.txt"))
     assert e.value.code == gs.errc.io_error
+
+
+@pytest.mark.parametrize("blk", ["1", "0"])
+@pytest.mark.parametrize("n", [8, 61, 500])
+def test_block_records_kernel_bit_exact(gs, n, blk, monkeypatch):
+    """8-row block kernel (wide fp64 rows): records re-sorted by original column keep every row's
+    CSR fma order -- applies on a shuffled-vertex graph (so new and original column orders differ)
+    equal the oracle bit for bit, including a last partial block. GS_BLK=1 selects it (opt-in);
+    GS_BLK=0 is the default warp-per-row kernel on the same inputs."""
+    monkeypatch.setenv("GS_BLK", blk)
+    r, c, v = acceptance_graph(n, 4242 + n) if n > 8 else random_connected_graph(n, 5)
+    perm = np.random.default_rng(n).permutation(n)
+    r, c = perm[np.asarray(r)].astype(np.int32), perm[np.asarray(c)].astype(np.int32)
+    f, _ = engine_filter(r, c, v, n, 0, 1.3, 30)
+    fo = oracle_filter(r, c, v, n, 0, 1.3, 30)
+    for width in (33, 64, 100):
+        X = np.random.default_rng(width + n).standard_normal((n, width))
+        assert np.array_equal(f.apply(X), fo.apply(X))
