@@ -561,11 +561,16 @@ __device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int til
 #ifndef GS_MIN_BLOCKS
 #define GS_MIN_BLOCKS 5
 #endif
+#ifndef GS_MIN_BLOCKS_NARROW
+#define GS_MIN_BLOCKS_NARROW 5
+#endif
 #ifndef GS_MIN_BLOCKS32
 #define GS_MIN_BLOCKS32 6
 #endif
 template <typename S, int GW, int MODE, int RPC>
-__global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0 : (sizeof(S) == 4 ? GS_MIN_BLOCKS32 : GS_MIN_BLOCKS))
+__global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0
+                                                  : (Lay<GW, S>::NARROW ? GS_MIN_BLOCKS_NARROW
+                                                     : (sizeof(S) == 4 ? GS_MIN_BLOCKS32 : GS_MIN_BLOCKS)))
     k_cheb_step(const StepArgs A) {
   using L = Lay<GW, S>;
   constexpr int VEC = L::VEC, LPR = L::LPR, RPW = L::RPW;
