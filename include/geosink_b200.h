@@ -117,6 +117,23 @@ int gs_filter_order(gs_ctx* ctx, const gs_filter* f, int* order, int mem);
  * Not a permutation of 0..n-1 -> invalid_argument (layout reset to the identity). No reference
  * counterpart (the reference has no locality renumbering). */
 int gs_filter_set_order(gs_ctx* ctx, gs_filter* f, int layout, const int* order, int mem);
+
+/* ---- dense baselines (the kNN benchmark's dense_sinkhorn_w1 / _w2 rows) ---- */
+/* dense_sinkhorn (transport.cpp:271-311): cost r x c row-major, mu (r), nu (c); outputs v (r),
+ * w (c), cost, kl, iterations, converged, marginal_error. mem applies to every array. */
+int gs_dense_sinkhorn(gs_ctx* ctx, const double* cost, int r, int c, const double* mu,
+                      const double* nu, double lambda, int max_iter, double tol, int mem,
+                      double* out_v, double* out_w, double* out_cost, double* out_kl,
+                      int* out_iters, int* out_conv, double* out_err);
+/* knn_benchmark's dense methods (bench.cpp:311-331): host arrays. X n x d row-major; group g is
+ * X rows group_idx[group_off[g] .. group_off[g+1]); pair p transports group pair_a[p] onto
+ * pair_b[p] with uniform marginals and cost squared_distances (bench.cpp:32-39; squared = 1) or
+ * its square root. Outputs per pair; the first failing pair (kernel underflow) in fail_pair. */
+int gs_dense_sinkhorn_groups(gs_ctx* ctx, const double* X, int n, int d, const int* group_idx,
+                             const int* group_off, int ngroups, const int* pair_a,
+                             const int* pair_b, int P, int squared, double lambda, int max_iter,
+                             double tol, double* out_cost, double* out_kl, int* out_iters,
+                             int* out_conv, double* out_err, int* fail_pair);
 /* p_K(L_s) X for `width` contiguous n-vectors (heat.cpp:98-131). */
 int gs_filter_apply(gs_ctx* ctx, const gs_filter* f, const double* X, double* Y, int width,
                     int mem);

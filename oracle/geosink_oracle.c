@@ -1237,3 +1237,106 @@ int go_euler_apply(const go_csr* system, int steps, const double* X, double* Y, 
   }
   return 0;
 }
+
+/* ------------------------------------------------------------------------------------------
+ * Dense baselines of the kNN benchmark: squared_distances (bench.cpp:32-39) and dense_sinkhorn
+ * (transport.cpp:271-311). Eigen's GEMM / GEMV summation orders are unpinned; the restatement
+ * fixes them as sequential fma chains in index order (dot products over the coordinates,
+ * phi_i over j, psi_j over i, the cost's inner sums over j and outer sum over i) and the
+ * marginal error as a sequential sum over i -- the device uses the same orders.
+ * ---------------------------------------------------------------------------------------- */
+int go_squared_distances(const double* X, int nx, const double* Y, int ny, int d, double* out) {
+  REQUIRE(nx >= 0 && ny >= 0 && d >= 1, E_INVALID_ARGUMENT, "bad point set shapes");
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < nx; ++i) {
+    double xn = 0.0;
+    for (int k = 0; k < d; ++k) xn = fma(X[(size_t)i * d + k], X[(size_t)i * d + k], xn);
+    for (int j = 0; j < ny; ++j) {
+      double yn = 0.0, dot = 0.0;
+      for (int k = 0; k < d; ++k) {
+        yn = fma(Y[(size_t)j * d + k], Y[(size_t)j * d + k], yn);
+        dot = fma(X[(size_t)i * d + k], Y[(size_t)j * d + k], dot);
+      }
+      const double v = (-2.0 * dot + xn) + yn; /* d = -2 x y^T; d.colwise() += xn; d.rowwise() += yn */
+      out[(size_t)i * ny + j] = fmax(v, 0.0);  /* cwiseMax(0) */
+    }
+  }
+  return 0;
+}
+
+int go_dense_sinkhorn(const double* C, int r, int c, const double* mu, const double* nu,
+                      double lambda, int max_iter, double tol, double* v, double* w,
+                      double* cost, double* kl, int* iters, int* conv, double* err) {
+  int rc = validate_distribution(mu, r);
+  if (!rc) rc = validate_distribution(nu, c);
+  if (rc) return rc;
+  for (int64_t q = 0; q < (int64_t)r * c; ++q)
+    REQUIRE(isfinite(C[q]), E_INVALID_ARGUMENT, "cost matrix has non-finite entries");
+  REQUIRE(lambda > 0.0, E_INVALID_ARGUMENT, "lambda must be positive");
+  REQUIRE(tol > 0.0 && max_iter >= 1, E_INVALID_ARGUMENT, "bad Sinkhorn parameters");
+  double* K = (double*)malloc((size_t)r * c * sizeof(double));
+  double* phi = (double*)malloc((size_t)r * sizeof(double));
+  for (int64_t q = 0; q < (int64_t)r * c; ++q) K[q] = exp(-C[q] / lambda); /* transport.cpp:282 */
+  for (int i = 0; i < r && !rc; ++i) {
+    double mx = 0.0;
+    for (int j = 0; j < c; ++j) mx = fmax(mx, K[(size_t)i * c + j]);
+    if (!(mx > 0.0)) rc = fail(E_NUMERICAL_UNDERFLOW, "kernel row underflowed to zero; increase lambda");
+  }
+  for (int j = 0; j < c && !rc; ++j) {
+    double mx = 0.0;
+    for (int i = 0; i < r; ++i) mx = fmax(mx, K[(size_t)i * c + j]);
+    if (!(mx > 0.0)) rc = fail(E_NUMERICAL_UNDERFLOW, "kernel column underflowed to zero; increase lambda");
+  }
+  if (rc) {
+    free(K);
+    free(phi);
+    return rc;
+  }
+  for (int j = 0; j < c; ++j) w[j] = 1.0;
+  for (int i = 0; i < r; ++i) v[i] = 0.0;
+  *conv = 0;
+  *iters = 0;
+  *err = INFINITY;
+  for (int i = 0; i < r; ++i) { /* phi = K w */
+    double s = 0.0;
+    for (int j = 0; j < c; ++j) s = fma(K[(size_t)i * c + j], w[j], s);
+    phi[i] = s;
+  }
+  for (int it = 1; it <= max_iter; ++it) {
+    for (int i = 0; i < r; ++i) v[i] = mu[i] / fmax(phi[i], K_FLOOR);
+    for (int j = 0; j < c; ++j) {
+      double s = 0.0;
+      for (int i = 0; i < r; ++i) s = fma(K[(size_t)i * c + j], v[i], s);
+      w[j] = nu[j] / fmax(s, K_FLOOR);
+    }
+    double e = 0.0;
+    for (int i = 0; i < r; ++i) {
+      double s = 0.0;
+      for (int j = 0; j < c; ++j) s = fma(K[(size_t)i * c + j], w[j], s);
+      phi[i] = s;
+      e = e + fabs(v[i] * s - mu[i]);
+    }
+    *err = e;
+    *iters = it;
+    if (e <= tol) {
+      *conv = 1;
+      break;
+    }
+  }
+  double cs = 0.0;
+  for (int i = 0; i < r; ++i) {
+    double t = 0.0;
+    for (int j = 0; j < c; ++j) t = fma(K[(size_t)i * c + j] * C[(size_t)i * c + j], w[j], t);
+    cs = fma(v[i], t, cs);
+  }
+  *cost = cs;
+  double k1 = 0.0, k2 = 0.0;
+  for (int i = 0; i < r; ++i)
+    if (mu[i] > 0.0) k1 += mu[i] * log(fmax(v[i], K_FLOOR));
+  for (int j = 0; j < c; ++j)
+    if (nu[j] > 0.0) k2 += nu[j] * log(fmax(w[j], K_FLOOR));
+  *kl = k1 + k2 - 1.0;
+  free(K);
+  free(phi);
+  return 0;
+}

@@ -112,6 +112,12 @@ int go_barycenter(const go_csr* scaled, const double* coeffs, int degree, const 
                   double* out_bary, double* out_V, double* out_W, int* out_iters, int* out_conv,
                   double* out_err);
 
+/* bench.cpp:32-39 (out nx x ny row-major) and transport.cpp:271-311 (C r x c row-major) */
+int go_squared_distances(const double* X, int nx, const double* Y, int ny, int d, double* out);
+int go_dense_sinkhorn(const double* C, int r, int c, const double* mu, const double* nu,
+                      double lambda, int max_iter, double tol, double* v, double* w,
+                      double* cost, double* kl, int* iters, int* conv, double* err);
+
 #ifdef __cplusplus
 }
 #endif

@@ -94,6 +94,9 @@ def _declare(L):
                                     _dp, _dp, _ip, _ip, _dp, _ip]
     L.go_barycenter.argtypes = [C.POINTER(go_csr), _dp, C.c_int, _dp, _dp, C.c_int,
                                 C.c_void_p, C.c_int, C.c_double, _dp, _dp, _dp, _ip, _ip, _dp]
+    L.go_squared_distances.argtypes = [_dp, C.c_int, _dp, C.c_int, C.c_int, _dp]
+    L.go_dense_sinkhorn.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp, C.c_double, C.c_int,
+                                    C.c_double, _dp, _dp, _dp, _dp, _ip, _ip, _dp]
 
 
 def _check(rc: int, L=None):
@@ -377,3 +380,29 @@ def barycenter(f: Filter, a, members, alphas=None, max_iter=500, tol=1e-6, L=Non
     _check(rc, L)
     return dict(barycenter=bary, V=V, W=W, iterations=int(it[0]), converged=bool(conv[0]),
                 marginal_error=float(err[0]))
+
+
+def squared_distances(X, Y, L=None):
+    """bench.cpp:32-39 (go_squared_distances)."""
+    L = L or lib()
+    X = np.ascontiguousarray(X, np.float64)
+    Y = np.ascontiguousarray(Y, np.float64)
+    out = np.empty((X.shape[0], Y.shape[0]))
+    _check(L.go_squared_distances(X, X.shape[0], Y, Y.shape[0], X.shape[1], out), L)
+    return out
+
+
+def dense_sinkhorn(cost, mu, nu, lam, max_iter=500, tol=1e-6, L=None):
+    """transport.cpp:271-311 (go_dense_sinkhorn)."""
+    L = L or lib()
+    cost = np.ascontiguousarray(cost, np.float64)
+    r, c = cost.shape
+    mu = np.ascontiguousarray(mu, np.float64)
+    nu = np.ascontiguousarray(nu, np.float64)
+    v, w = np.empty(r), np.empty(c)
+    cs, kl, err = np.empty(1), np.empty(1), np.empty(1)
+    it, cv = np.empty(1, np.int32), np.empty(1, np.int32)
+    _check(L.go_dense_sinkhorn(cost, r, c, mu, nu, float(lam), int(max_iter), float(tol), v, w, cs,
+                               kl, it, cv, err), L)
+    return {"v": v, "w": w, "cost": float(cs[0]), "kl": float(kl[0]), "iterations": int(it[0]),
+            "converged": bool(cv[0]), "marginal_error": float(err[0])}

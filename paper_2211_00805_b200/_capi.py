@@ -69,6 +69,10 @@ SIGNATURES = {
     "gs_filter_scaled": (_vp, [_vp]),
     "gs_filter_order": (_i, [_vp, _vp, _vp, _i]),
     "gs_filter_set_order": (_i, [_vp, _vp, _i, _vp, _i]),
+    "gs_dense_sinkhorn": (_i, [_vp, _vp, _i, _i, _vp, _vp, _d, _i, _d, _i, _vp, _vp, _vp, _vp,
+                               _vp, _vp, _vp]),
+    "gs_dense_sinkhorn_groups": (_i, [_vp, _vp, _i, _i, _vp, _vp, _i, _vp, _vp, _i, _i, _d, _i,
+                                      _d, _vp, _vp, _vp, _vp, _vp, _pi]),
     "gs_filter_apply": (_i, [_vp, _vp, _vp, _vp, _i, _i]),
     "gs_filter_apply_ex": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i]),
     "gs_sinkhorn": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _d, _i, _i, _vp, _vp, _vp, _vp, _vp,

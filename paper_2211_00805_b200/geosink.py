@@ -21,7 +21,7 @@ import enum
 import math
 import threading
 from dataclasses import dataclass, field
-from typing import List, Optional, Sequence
+from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -668,6 +668,61 @@ def _euler_sinkhorn(euler: "EulerHeat", mus, nus, a, params: SinkhornParams, fla
                                         _ptr(it), _ptr(conv), _ptr(err), C.byref(fp), C.byref(fs)))
     lam = 4.0 * euler.time()
     return [TransportResult(v[p].copy(), w[p].copy(), float(cost[p]), float(kl[p]), lam, int(it[p]),
+                            bool(conv[p]), float(err[p])) for p in range(P)]
+
+
+def dense_sinkhorn(cost_matrix, mu: Distribution, nu: Distribution, lam: float,
+                   params: SinkhornParams = SinkhornParams(), ctx: Optional[Context] = None) -> TransportResult:
+    """transport.cpp:271-311: entropic Sinkhorn with the dense kernel exp(-C / lam), on the device
+    (gs_dense_sinkhorn)."""
+    ctx = _ctx(ctx)
+    Cm = np.ascontiguousarray(cost_matrix, np.float64)
+    if Cm.ndim != 2:
+        raise Error(errc.invalid_argument, "InvalidArgument: cost matrix must be two-dimensional")
+    m = mu.weights if isinstance(mu, Distribution) else _f64(mu)
+    x = nu.weights if isinstance(nu, Distribution) else _f64(nu)
+    r, c = Cm.shape
+    if m.size != r or x.size != c:
+        Distribution(m).validate()
+        Distribution(x).validate()
+        raise Error(errc.length_mismatch, "LengthMismatch: cost matrix shape does not match the marginals")
+    v, w = np.empty(r), np.empty(c)
+    cost, kl, err = np.empty(1), np.empty(1), np.empty(1)
+    it, conv = np.empty(1, np.int32), np.empty(1, np.int32)
+    ctx.check(ctx.lib.gs_dense_sinkhorn(ctx.handle, _ptr(Cm), r, c, _ptr(m), _ptr(x), float(lam),
+                                        int(params.max_iter), float(params.tol), _capi.GS_MEM_HOST,
+                                        _ptr(v), _ptr(w), _ptr(cost), _ptr(kl), _ptr(it), _ptr(conv),
+                                        _ptr(err)))
+    return TransportResult(v, w, float(cost[0]), float(kl[0]), float(lam), int(it[0]), bool(conv[0]),
+                           float(err[0]))
+
+
+def dense_sinkhorn_groups(points, groups: Sequence[Sequence[int]], pairs: Sequence[Tuple[int, int]],
+                          squared: bool, lam: float, params: SinkhornParams = SinkhornParams(),
+                          ctx: Optional[Context] = None) -> List[TransportResult]:
+    """The kNN benchmark's dense baselines (bench.cpp:311-331) for many pairs at once: pair (a, b)
+    transports the uniform distribution on points[groups[a]] onto the one on points[groups[b]]
+    with cost squared_distances (bench.cpp:32-39) or its square root (squared=False). Results
+    carry cost, kl, iterations, converged and marginal_error (v and w are not returned)."""
+    ctx = _ctx(ctx)
+    X = np.ascontiguousarray(points, np.float64)
+    if X.ndim != 2:
+        raise Error(errc.invalid_argument, "InvalidArgument: points must be n x d")
+    gidx = np.ascontiguousarray(np.concatenate([np.asarray(g, np.int32) for g in groups]), np.int32)
+    goff = np.zeros(len(groups) + 1, np.int32)
+    goff[1:] = np.cumsum([len(g) for g in groups])
+    pa = np.ascontiguousarray([p[0] for p in pairs], np.int32)
+    pb = np.ascontiguousarray([p[1] for p in pairs], np.int32)
+    P = len(pairs)
+    cost, kl, err = np.empty(P), np.empty(P), np.empty(P)
+    it, conv = np.empty(P, np.int32), np.empty(P, np.int32)
+    fp = C.c_int()
+    ctx.check(ctx.lib.gs_dense_sinkhorn_groups(ctx.handle, _ptr(X), X.shape[0], X.shape[1], _ptr(gidx),
+                                               _ptr(goff), len(groups), _ptr(pa), _ptr(pb), P,
+                                               1 if squared else 0, float(lam), int(params.max_iter),
+                                               float(params.tol), _ptr(cost), _ptr(kl), _ptr(it),
+                                               _ptr(conv), _ptr(err), C.byref(fp)))
+    return [TransportResult(np.zeros(0), np.zeros(0), float(cost[p]), float(kl[p]), float(lam), int(it[p]),
                             bool(conv[p]), float(err[p])) for p in range(P)]
 
 

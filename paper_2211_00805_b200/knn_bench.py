@@ -4,9 +4,11 @@ distance-ranking experiment on the device path.
 m clusters on a rotated swiss roll (make_swiss_roll, bench.cpp:59-100) -> alpha-decay kNN graph
 -> Laplacian -> heat filter -> geodesic Sinkhorn distances between all m(m-1)/2 pairs of cluster
 indicator distributions in ONE batched call -> Pearson / Spearman / precision@5 against the
-unrolled-spiral ground truth (bench.cpp:107-214). Methods: `geodesic_sinkhorn` and the
-`euler_sinkhorn` competitor (EulerHeat + the same Sinkhorn control); the dense-Sinkhorn W1/W2
-baselines are out of scope.
+unrolled-spiral ground truth (bench.cpp:107-214). Methods (bench.hpp:70): `geodesic_sinkhorn`,
+the `euler_sinkhorn` competitor (EulerHeat + the same Sinkhorn control) and the dense baselines
+`dense_sinkhorn_w1` / `dense_sinkhorn_w2` (bench.cpp:311-331: entropic Sinkhorn between the two
+clusters' ambient points with the distance / squared-distance cost, all pairs in one device call,
+gs_dense_sinkhorn_groups).
 
 Draws follow geosink::Rng (rng.hpp:13-68) in the reference order; the random rotation is the
 Householder QR of a Gaussian matrix with R's diagonal made positive (numpy's LAPACK QR instead of
@@ -39,7 +41,10 @@ class KnnBenchConfig:  # bench.hpp:75-93
     degree: int = 100
     sinkhorn: gs.SinkhornParams = field(default_factory=lambda: gs.SinkhornParams(500, 1e-6))
     euler_steps: int = 30  # backward-Euler substeps
-    methods: List[str] = field(default_factory=lambda: ["geodesic_sinkhorn"])
+    methods: List[str] = field(default_factory=lambda: ["geodesic_sinkhorn", "dense_sinkhorn_w1",
+                                                        "dense_sinkhorn_w2"])
+    lambda_w1: float = 2.0   # dense baseline regularisation, distance cost
+    lambda_w2: float = 20.0  # dense baseline regularisation, squared cost
     # bench-only deviation (as bench.py): run every pair to max_iter instead of raising
     # Disconnected when a pair's marginal error stays above 0.5 for 50 sweeps
     no_stagnation_abort: bool = False
@@ -151,9 +156,12 @@ def knn_benchmark(config: KnnBenchConfig = KnnBenchConfig(), ctx=None) -> dict:
         truth = ground_truth_distances(sample)
         n = sample.ambient.shape[0]
         t0 = time.perf_counter()
-        A = gs.knn_alpha_decay_graph(sample.ambient, config.k, config.alpha, ctx=ctx)
-        lap = gs.laplacian(A, config.kind)
-        t_graph = time.perf_counter() - t0
+        needs_graph = any(mth in ("geodesic_sinkhorn", "euler_sinkhorn") for mth in config.methods)
+        lap = None
+        if needs_graph:  # bench.cpp:264-275
+            A = gs.knn_alpha_decay_graph(sample.ambient, config.k, config.alpha, ctx=ctx)
+            lap = gs.laplacian(A, config.kind)
+        t_graph = time.perf_counter() - t0 if needs_graph else 0.0
         groups = [np.flatnonzero(sample.labels == c) for c in range(m)]
         mus, nus = [], []
         for i in range(m):
@@ -162,8 +170,27 @@ def knn_benchmark(config: KnnBenchConfig = KnnBenchConfig(), ctx=None) -> dict:
                 nus.append(gs.Distribution.indicator(n, groups[j]))
         a = np.full(n, 1.0 / n)
         seed_out = {"seed": seed, "truth": truth, "distances": {}, "reports": {}, "iterations": {}}
+        pair_list = [(i, j) for i in range(m) for j in range(i + 1, m)]
         for method in config.methods:
             t1 = time.perf_counter()
+            if method in ("dense_sinkhorn_w1", "dense_sinkhorn_w2"):  # bench.cpp:311-331
+                squared = method == "dense_sinkhorn_w2"
+                lam = config.lambda_w2 if squared else config.lambda_w1
+                runs = gs.dense_sinkhorn_groups(sample.ambient, groups, pair_list, squared, lam,
+                                                config.sinkhorn, ctx=ctx)
+                t_dist = time.perf_counter() - t1
+                costs = [math.sqrt(max(0.0, r.cost)) if squared else r.cost for r in runs]
+                d = np.zeros((m, m))
+                for (i, j), cst in zip(pair_list, costs):
+                    d[i, j] = d[j, i] = cst
+                rep = rank_metrics(d, truth)
+                rep.update(graph=0.0, prepare=0.0, distance=t_dist)
+                seed_out["distances"][method] = d
+                seed_out["reports"][method] = rep
+                seed_out["iterations"][method] = [r.iterations for r in runs]
+                for key in keys:
+                    means[method][key] += rep[key] / len(config.seeds)
+                continue
             if method == "geodesic_sinkhorn":
                 op = gs.HeatFilter(lap, config.t, config.degree)
                 solve = gs.geodesic_sinkhorn_batch

@@ -35,7 +35,7 @@ def test_knn_benchmark_matches_oracle(ctx, m, per, noise, t, seed):
     import paper_2211_00805_b200 as gs
     from paper_2211_00805_b200 import knn_bench as kb
     cfg = kb.KnnBenchConfig(n_distributions=m, samples_per_dist=per, noise_sigma=noise, seeds=[seed],
-                            degree=60, t=t)
+                            degree=60, t=t, methods=["geodesic_sinkhorn"])
     ref, ref_err = _oracle(kb, cfg, seed)
     try:
         res = kb.knn_benchmark(cfg)

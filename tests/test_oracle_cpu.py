@@ -546,3 +546,25 @@ def test_euler_isolated_vertex_and_validation():
         po.euler_system(L, 0.0, 2)
     with pytest.raises(po.OracleError):
         po.euler_system(L, 1.0, 0)
+
+
+# --------------------------------------------------------------------------- dense baselines
+def test_oracle_squared_distances_and_dense_product_plan():
+    """bench.cpp:32-39 against the direct formula; transport.cpp:271-311 on a zero cost gives the
+    product plan (test_transport.cpp:208-215); validation as the reference (transport.cpp:274-280)."""
+    import pyoracle as po
+    g = np.random.default_rng(0)
+    X, Y = g.standard_normal((7, 5)), g.standard_normal((9, 5))
+    D = po.squared_distances(X, Y)
+    assert np.abs(D - ((X[:, None] - Y[None]) ** 2).sum(-1)).max() <= 1e-12
+    assert (po.squared_distances(X, X) >= 0).all()
+    mu, nu = np.array([0.5, 0.3, 0.2]), np.array([0.2, 0.2, 0.6])
+    r = po.dense_sinkhorn(np.zeros((3, 3)), mu, nu, 0.7, 500, 1e-12)
+    assert r["converged"]
+    assert np.abs(r["v"][:, None] * r["w"][None, :] - np.outer(mu, nu)).max() <= 1e-10
+    with pytest.raises(po.OracleError, match="non-finite"):
+        po.dense_sinkhorn(np.full((3, 3), np.nan), mu, nu, 0.7)
+    with pytest.raises(po.OracleError, match="lambda"):
+        po.dense_sinkhorn(np.zeros((3, 3)), mu, nu, -1.0)
+    with pytest.raises(po.OracleError, match="row underflowed"):
+        po.dense_sinkhorn(np.full((3, 3), 1e5), mu, nu, 1e-3)

@@ -7,7 +7,8 @@ from paper_2211_00805_b200 import knn_bench as kb  # noqa: E402
 
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 seeds = [int(s) for s in args] or [1, 2, 3]
-methods = ["geodesic_sinkhorn"] + (["euler_sinkhorn"] if "--euler" in sys.argv else [])
+methods = (["geodesic_sinkhorn", "dense_sinkhorn_w1", "dense_sinkhorn_w2"]
+           + (["euler_sinkhorn"] if "--euler" in sys.argv else []))
 res = kb.knn_benchmark(kb.KnnBenchConfig(seeds=seeds, methods=methods,
                                          no_stagnation_abort="--no-stagnation-abort" in sys.argv))
 for m in methods:
