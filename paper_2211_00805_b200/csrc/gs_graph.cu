@@ -460,20 +460,30 @@ struct PowerState {
   double est, norm;
 };
 
-__global__ void __launch_bounds__(DET_T) k_power_spmv(int n, const int* __restrict__ offs,
-                                                     const int* __restrict__ cols,
-                                                     const double* __restrict__ vals,
-                                                     const double* __restrict__ x,
-                                                     double* __restrict__ y, double* part_yy,
+// y = L x, one thread per row (CSR-order fma chain, sparse.cpp:70-83); the blocked dot products
+// of k_power_spmv then read y, so the product itself is not confined to n / 4096 blocks
+__global__ void k_power_rows(int n, const int* __restrict__ offs, const int* __restrict__ cols,
+                             const double* __restrict__ vals, const double* __restrict__ x,
+                             double* __restrict__ y, const PowerState* st) {
+  if (st->done) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+  for (int p = offs[i]; p < offs[i + 1]; ++p) acc = fma(vals[p], x[cols[p]], acc);
+  y[i] = acc;
+}
+
+// per 4096-row chunk: the blocked partial sums of y.y and x.y (lane t folds rows
+// c*4096 + j*256 + t in j order, then a tree over lanes -- the oracle's go_detdot order)
+__global__ void __launch_bounds__(DET_T) k_power_dots(int n, const double* __restrict__ x,
+                                                     const double* __restrict__ y, double* part_yy,
                                                      double* part_xy, const PowerState* st) {
   if (st->done) return;
   double ayy = 0.0, axy = 0.0;
   for (int j = 0; j < DET_J; ++j) {
     const int64_t i = (int64_t)blockIdx.x * DET_CHUNK + (int64_t)j * DET_T + threadIdx.x;
     if (i < n) {
-      double acc = 0.0;
-      for (int p = offs[i]; p < offs[i + 1]; ++p) acc = fma(vals[p], x[cols[p]], acc);
-      y[i] = acc;
+      const double acc = y[i];  // k_power_rows
       ayy = fma(acc, acc, ayy);
       axy = fma(x[i], acc, axy);
     }
@@ -689,8 +699,8 @@ int gs_lambda_max_impl(gs_ctx* ctx, const gs_graph* L, double* out, int* rounds_
   gs_launch_end(ctx, 1);
   for (int it = 0; it < 200; ++it) {
     gs_launch_begin(ctx, 1);
-    k_power_spmv<<<(unsigned)nchunks, DET_T, 0, s>>>(n, L->offs, L->cols, L->vals, x.get(), y.get(),
-                                                     pyy.get(), pxy.get(), st.get());
+    k_power_rows<<<nblk(n), kThreads, 0, s>>>(n, L->offs, L->cols, L->vals, x.get(), y.get(), st.get());
+    k_power_dots<<<(unsigned)nchunks, DET_T, 0, s>>>(n, x.get(), y.get(), pyy.get(), pxy.get(), st.get());
     k_power_update<<<1, DET_T, 0, s>>>(pyy.get(), pxy.get(), nchunks, st.get());
     k_power_scale<<<nblk(n), kThreads, 0, s>>>(x.get(), y.get(), n, st.get());
     gs_launch_end(ctx, 1);
