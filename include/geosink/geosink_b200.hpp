@@ -102,6 +102,7 @@ struct RowMajorXd {  // n x B, row-major (sparse.hpp:14)
   RowMajorXd(std::size_t r, std::size_t c) : rows_(r), cols_(c), data_(r * c, 0.0) {}
   std::size_t rows() const { return rows_; }
   std::size_t cols() const { return cols_; }
+  const double* data() const { return data_.data(); }
   double& operator()(std::size_t i, std::size_t j) { return data_[i * cols_ + j]; }
   double operator()(std::size_t i, std::size_t j) const { return data_[i * cols_ + j]; }
   std::vector<double> col(std::size_t j) const {
@@ -503,6 +504,29 @@ inline std::vector<TransportResult> euler_sinkhorn_batch(const EulerHeat& euler,
 inline TransportResult euler_sinkhorn(const EulerHeat& euler, const Distribution& mu, const Distribution& nu,
                                       const std::vector<double>& a, const SinkhornParams& params = {}) {
   return euler_sinkhorn_batch(euler, {mu}, {nu}, a, params, GS_FLAG_SINGLE)[0];
+}
+
+// transport.cpp:271-311: dense entropic Sinkhorn (the kNN benchmark's baseline); cost is r x c
+// row-major (RowMajorXd with n = r rows, B = c columns)
+inline TransportResult dense_sinkhorn(const RowMajorXd& cost, const Distribution& mu, const Distribution& nu,
+                                      double lambda, const SinkhornParams& params = {}) {
+  TransportResult res;
+  res.v.resize(cost.rows());
+  res.w.resize(cost.cols());
+  res.lambda = lambda;
+  if (mu.size() != (std::size_t)cost.rows() || nu.size() != (std::size_t)cost.cols()) {
+    mu.validate();
+    nu.validate();
+    detail::fail(errc::length_mismatch, "LengthMismatch", "cost matrix shape does not match the marginals");
+  }
+  int it = 0, conv = 0;
+  detail::check(gs_dense_sinkhorn(detail::ctx(), cost.data(), (int)cost.rows(), (int)cost.cols(),
+                                  mu.weights.data(), nu.weights.data(), lambda, params.max_iter, params.tol,
+                                  GS_MEM_HOST, res.v.data(), res.w.data(), &res.cost, &res.kl, &it, &conv,
+                                  &res.marginal_error));
+  res.iterations = it;
+  res.converged = conv != 0;
+  return res;
 }
 
 // ---- next: plan rows, graph file IO ---------------------------------------------

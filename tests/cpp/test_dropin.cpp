@@ -209,6 +209,17 @@ int main() {
     const double ct = barycentric_distance(f, c, t, a, {500, 1e-8});
     CHECK(std::abs(tc - ct) <= 1e-8 * (1.0 + std::abs(tc)));
   }
+  // dense Sinkhorn: zero cost gives the product plan (test_transport.cpp:208-215); shape check
+  {
+    const Distribution mu(std::vector<double>{0.5, 0.3, 0.2}), nu(std::vector<double>{0.2, 0.2, 0.6});
+    const auto res = dense_sinkhorn(RowMajorXd(3, 3), mu, nu, 0.7, {500, 1e-12});
+    CHECK(res.converged);
+    double err = 0.0;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) err = std::max(err, std::abs(res.v[i] * res.w[j] - mu.weights[i] * nu.weights[j]));
+    CHECK(err <= 1e-10);
+    CHECK_THROWS_CODE(dense_sinkhorn(RowMajorXd(3, 2), mu, nu, 0.7), errc::length_mismatch);
+  }
   // plan rows rebuild the marginals (acceptance.cpp:168-197); graph file round trip
   {
     Rng rng(4);
