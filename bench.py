@@ -504,6 +504,19 @@ def run_engine_bary(args):
     t_graph = time.perf_counter() - t0
     lap = gs.laplacian(A, gs.LaplacianKind.combinatorial)
     filt = gs.HeatFilter(lap, cfg.t, cfg.degree)
+    if os.environ.get("GS_BENCH_ORDER") == "bisect":  # experiment: host-computed locality order
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import orders
+        Ls = filt.scaled_laplacian()
+        offs = Ls.row_offsets()
+        o = orders.bisect_order(offs, Ls.col_indices(), args.n, int(os.environ.get("GS_BENCH_LEAF", "64")))
+        win = 256  # degree-sorted windows, as the narrow layout's default order
+        deg = np.diff(offs)[o]
+        o2 = o.copy()
+        for w0 in range(0, len(o), win):
+            seg = o[w0:w0 + win]
+            o2[w0:w0 + win] = seg[np.argsort(-deg[w0:w0 + win], kind="stable")]
+        filt.set_vertex_order(o2, 1)
     n, m = args.n, args.members
     lo, hi = member_shard(m, world, rank)
     dev = torch.device("cuda", local)
