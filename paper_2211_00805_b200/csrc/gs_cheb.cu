@@ -476,9 +476,24 @@ inline unsigned grid_for(int64_t work, int threads = kThreads) {
 
 // Columns per group: the next power of two >= B, at most 64 (one warp per 512-byte fp64 row).
 int choose_gw(int width) {
+  static const int cap = [] {  // GS_MAX_GW: narrower groups (experiments; results unchanged)
+    const char* e = getenv("GS_MAX_GW");
+    const int v = e ? atoi(e) : 64;
+    return v >= 1 && v <= 64 && (v & (v - 1)) == 0 ? v : 64;
+  }();
   int g = 1;
-  while (g < width && g < 64) g <<= 1;
+  while (g < width && g < cap) g <<= 1;
   return g;
+}
+
+// GS_SEQ_GROUPS=1: an apply runs its K steps group after group (each group's T_{k-1} written by
+// the previous step is then L2-resident for its gathers) instead of all groups in every launch
+inline bool seq_groups() {
+  static const bool v = [] {
+    const char* e = getenv("GS_SEQ_GROUPS");
+    return e && atoi(e) != 0;
+  }();
+  return v;
 }
 
 template <typename S>
@@ -828,14 +843,21 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
   A.M = M;
   A.Vcur = Vcur;
   A.Wout = Wout;
-  AccSchedule sched;
-  for (int k = 1; k <= K; ++k) {
-    A.k = k;
-    A.bk = f->coeffs[k];
-    sched.step(f, K, k, A);
-    A.Tprev = w.T[(a0 + k - 1) & 1].get();
-    A.Tout = w.T[(a0 + k) & 1].get();
-    launch_step<S>(ctx, w.GW, w.rpc, A, k == K ? mode : MODE_NONE);
+  const bool seq = seq_groups() && w.G > 1;
+  for (int g = 0; g < (seq ? w.G : 1); ++g) {
+    if (seq) {
+      A.g0 = g;
+      A.Gl = 1;
+    }
+    AccSchedule sched;
+    for (int k = 1; k <= K; ++k) {
+      A.k = k;
+      A.bk = f->coeffs[k];
+      sched.step(f, K, k, A);
+      A.Tprev = w.T[(a0 + k - 1) & 1].get();
+      A.Tout = w.T[(a0 + k) & 1].get();
+      launch_step<S>(ctx, w.GW, w.rpc, A, k == K ? mode : MODE_NONE);
+    }
   }
   return (a0 + K) & 1;
 }
