@@ -46,6 +46,19 @@ extern "C" int gs_ctx_create(int device, gs_ctx** out) {
     return GS_ERR_CUDA;
   }
   ctx->stream = ctx->own_stream;
+  // Workspaces are stream-ordered allocations (cudaMallocAsync) made per call; by default the
+  // pool returns freed memory to the driver at every synchronisation, so each call would map its
+  // (up to GB-sized) buffers again. Keep it in the pool (GS_POOL_KEEP=0 restores the default).
+  {
+    const char* e = getenv("GS_POOL_KEEP");
+    if (!(e && atoi(e) == 0)) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+    }
+  }
   if (cudaMallocHost((void**)&ctx->h_status, 4 * sizeof(gs_status)) != cudaSuccess) {
     cudaStreamDestroy(ctx->own_stream);
     delete ctx;
