@@ -71,6 +71,12 @@ constexpr int kPrefetchStages = GS_PREFETCH_STAGES;
 #ifndef GS_VAL_LDG
 #define GS_VAL_LDG 0  // measured: 132.4 vs 128.1 us (more L1 requests cost more than the shuffles)
 #endif
+// one-row-per-lane layouts (own-row operands not staged by cp.async): load
+// T_{k-1}[row], T_{k-2}[row] and acc[row] into registers before the gathers, so the streams'
+// DRAM latency overlaps them instead of following them
+#ifndef GS_EARLY_OWN
+#define GS_EARLY_OWN 1
+#endif
 #ifndef GS_ROW_PREFETCH
 #define GS_ROW_PREFETCH 0  // measured neutral-to-slower on config 1 (one chunk per row)
 #endif
@@ -328,6 +334,30 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
   const size_t idx = gbase + (size_t)(valid ? row : 0) * GW;
   const S* __restrict__ Tp = static_cast<const S*>(A.Tprev) + gbase;
   const S* __restrict__ vals = static_cast<const S*>(A.vals);
+  S own[3 * VEC];  // early own-row operands (GS_EARLY_OWN): tp, t2, a0
+  // layouts whose own rows k_cheb_step stages in shared memory never take the early path
+  constexpr bool STAGED = VEC * sizeof(S) >= 16 && (VEC * sizeof(S)) % 16 == 0;
+  // measured: config 3 (one row per lane) 589 -> 564 us; config 2 (narrow rows) 341 -> 362 us
+  constexpr bool EARLY = GS_EARLY_OWN && !STAGED && LPR == 1;
+  const bool early = EARLY && !pre && valid && A.k != 0;
+  if (EARLY && early) {
+#pragma unroll
+    for (int e = 0; e < 3 * VEC; ++e) own[e] = S(0);
+    S t[VEC];
+    ld_vec<S, VEC>(static_cast<const S*>(A.Tprev) + idx, t);
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) own[e] = t[e];
+    if (A.k >= 2) {
+      ld_vec_rw<S, VEC>(static_cast<const S*>(A.Tout) + idx, t);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) own[VEC + e] = t[e];
+    }
+    if (A.acc_terms > 0 && !A.acc_init) {
+      ld_vec_rw<S, VEC>(static_cast<const S*>(A.acc) + idx, t);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) own[2 * VEC + e] = t[e];
+    }
+  }
   // ---- y = L_s T_{k-1} (row) ------------------------------------------------------------------
   S y[VEC];
 #pragma unroll
@@ -423,7 +453,8 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
     }
   }
   if (!valid) return;
-  finish_row<S, GW, MODE>(A, g, row, q, y, mn, mx, er, pre, pre_stride);
+  if (EARLY && early) finish_row<S, GW, MODE>(A, g, row, q, y, mn, mx, er, own, VEC);
+  else finish_row<S, GW, MODE>(A, g, row, q, y, mn, mx, er, pre, pre_stride);
 }
 
 // The rest of a row's step once y = (L_s T_{k-1})[row] is known: the recurrence, the deferred
