@@ -2009,7 +2009,7 @@ static int finish_layout(gs_ctx* ctx, gs_filter* f, int l) {
     rc = gs_permute_graph(ctx, f->scaled, Ly.order, Ly.newpos, &Ly.perm);
     if (rc) break;
     const int64_t nnz = Ly.perm->nnz;  // fp32 copy of the permuted values (optional fp32 mode)
-    if (cudaMalloc((void**)&Ly.vals32, (size_t)(nnz ? nnz : 1) * sizeof(float)) != cudaSuccess) {
+    if (cudaMalloc((void**)&Ly.vals32, (size_t)(nnz + kCsrPad) * sizeof(float)) != cudaSuccess) {
       rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "fp32 value allocation failed");
     } else if (nnz > 0) {
       gs_launch_begin(ctx, 1);

@@ -190,8 +190,9 @@ int gs_graph_alloc(gs_ctx* ctx, int n, int64_t nnz, gs_graph** out) {
   g->nnz = nnz;
   g->device = ctx->device;
   cudaError_t e = cudaMalloc((void**)&g->offs, ((size_t)n + 1) * sizeof(int));
-  if (e == cudaSuccess) e = cudaMalloc((void**)&g->cols, (size_t)(nnz ? nnz : 1) * sizeof(int));
-  if (e == cudaSuccess) e = cudaMalloc((void**)&g->vals, (size_t)(nnz ? nnz : 1) * sizeof(double));
+  // kCsrPad: vectorised CSR loads (gs_step.cuh) read aligned blocks up to 3 entries past a row
+  if (e == cudaSuccess) e = cudaMalloc((void**)&g->cols, (size_t)(nnz + kCsrPad) * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc((void**)&g->vals, (size_t)(nnz + kCsrPad) * sizeof(double));
   if (e != cudaSuccess) {
     gs_graph_destroy(g);
     return gs_cuda_fail(ctx, e, "gs_graph_alloc");

@@ -153,6 +153,7 @@ struct DevBuf {
 };
 
 // ---- shared device helpers ----------------------------------------------------------------
+constexpr int kCsrPad = 8;  // elements allocated past nnz in CSR column / value arrays
 #define GS_FLOOR 1e-300
 #define GS_CEIL 1e300
 #define DET_T 256

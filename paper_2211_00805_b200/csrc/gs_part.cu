@@ -221,7 +221,7 @@ int part_build(gs_ctx* ctx, const gs_filter* f, int nparts, int part, gs_part* P
     P->int_lo = hb[0] + 1;
     P->int_hi = hb[1] < P->int_lo ? P->int_lo : hb[1];
   }
-  GS_CUDA(ctx, cudaMalloc((void**)&P->vals32, (size_t)(m ? m : 1) * sizeof(float)));
+  GS_CUDA(ctx, cudaMalloc((void**)&P->vals32, (size_t)(m + kCsrPad) * sizeof(float)));
   if (m > 0 && L.vals32) {
     gs_launch_begin(ctx, 1);
     k_float_slice<<<blocks_for(m), kT, 0, s>>>(L.vals32 + eb, m, P->vals32);

@@ -77,6 +77,13 @@ constexpr int kPrefetchStages = GS_PREFETCH_STAGES;
 #ifndef GS_EARLY_OWN
 #define GS_EARLY_OWN 1
 #endif
+// one row per lane, fp32: a lane reads its row's columns and values four at a time with aligned
+// 16-byte loads (carried across groups, the row's misalignment resolved by selects) instead of
+// one 4-byte load per entry -- a quarter of the CSR load instructions (config 3: the LSU data
+// pipe is 80% busy, two thirds of it on these per-lane scattered loads). Arrays carry kCsrPad.
+#ifndef GS_CSR_VEC
+#define GS_CSR_VEC 1
+#endif
 #ifndef GS_ROW_PREFETCH
 #define GS_ROW_PREFETCH 0  // measured neutral-to-slower on config 1 (one chunk per row)
 #endif
@@ -366,6 +373,40 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
     if (valid) {
       int p = __ldg(A.offs + row);
       const int pe = __ldg(A.offs + row + 1);
+      if constexpr (GS_CSR_VEC && sizeof(S) == 4) {
+        const int off = p & 3;
+        const int* cbase = A.cols + (p - off);
+        const float* vbase = reinterpret_cast<const float*>(vals) + (p - off);
+        int4 ca = __ldg(reinterpret_cast<const int4*>(cbase));
+        float4 va = __ldg(reinterpret_cast<const float4*>(vbase));
+        // element u of the group starting at p: block a (u + off < 4) or the next block b
+        auto sel_i = [&](const int4& a, const int4& b, int k) {  // k = u + off in 0..6
+          return k == 0 ? a.x : k == 1 ? a.y : k == 2 ? a.z : k == 3 ? a.w : k == 4 ? b.x : k == 5 ? b.y : b.z;
+        };
+        auto sel_f = [&](const float4& a, const float4& b, int k) {
+          return k == 0 ? a.x : k == 1 ? a.y : k == 2 ? a.z : k == 3 ? a.w : k == 4 ? b.x : k == 5 ? b.y : b.z;
+        };
+        for (int blk = 1; p + 4 <= pe; p += 4, ++blk) {
+          const int4 cb = __ldg(reinterpret_cast<const int4*>(cbase) + blk);
+          const float4 vb = __ldg(reinterpret_cast<const float4*>(vbase) + blk);
+          int cc[4];
+          S vv[4];
+          S xx[4][VEC];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            cc[u] = sel_i(ca, cb, u + off);
+            vv[u] = sel_f(va, vb, u + off);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) ld_vec<S, VEC>(Tp + (size_t)cc[u] * GW, xx[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) y[e] = P::fmat(vv[u], xx[u][e], y[e]);
+          ca = cb;
+          va = vb;
+        }
+      }
       for (; p + 4 <= pe; p += 4) {
         int cc[4];
         S vv[4];
