@@ -860,7 +860,7 @@ static int sinkhorn_many(const heat_op* op, double t, const double* a, const dou
     REQUIRE(tol > 0.0, E_INVALID_ARGUMENT, "tolerance must be positive");
     REQUIRE(max_iter >= 1, E_INVALID_ARGUMENT, "max_iter must be >= 1");
   }
-  if (P == 0) return 0;
+  if (P <= 0) return P == 0 ? 0 : fail(E_SIZE_MISMATCH, "pair lists differ in length");
   const double lambda = 4.0 * t;
   int* active = (int*)malloc((size_t)P * sizeof(int));
   int* stagnant = (int*)calloc((size_t)P, sizeof(int));
