@@ -146,9 +146,9 @@ def cpu_sinkhorn_sample(L_host, lam, cfg, sweeps, native=True):
     n = cfg.roll.s.size
     a = np.full(n, 1.0 / n)
     t0 = time.perf_counter()
-    po.sinkhorn_batch(fo, a, cfg.mus, cfg.nus, sweeps, TOL_RUN_ALL, flags=1, L=lib)
+    res = po.sinkhorn_batch(fo, a, cfg.mus, cfg.nus, sweeps, TOL_RUN_ALL, flags=1, L=lib)
     dt = time.perf_counter() - t0
-    return sweeps / dt, dt
+    return sweeps / dt, dt, res
 
 
 def run_reference(args):
@@ -424,15 +424,28 @@ def run_engine(args):
 
     # ---- CPU baseline (rank 0, N = 1) ---------------------------------------------------------
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
         offs = lap.matrix.row_offsets().copy()
         cols = lap.matrix.col_indices().copy()
         vals = lap.matrix.values().copy()
         sweeps = args.cpu_sweeps
-        v, dt = cpu_sinkhorn_sample((n, offs, cols, vals), lap.lambda_max_bound, cfg, sweeps)
+        v, dt, ref = cpu_sinkhorn_sample((n, offs, cols, vals), lap.lambda_max_bound, cfg, sweeps)
         cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                "sample": f"{sweeps} sweep(s) of the same 64-pair batch on the GPU-built n={n} "
                          f"graph, oracle restatement -O3 -march=native OpenMP ({dt:.1f} s)"}
+        # results parity at full size: the engine's run of the same sweeps on the same operator
+        ctx.check(lib.gs_sinkhorn(ctx.handle, filt._h, a.data_ptr(), M.data_ptr(), N.data_ptr(), P,
+                                  sweeps, TOL_RUN_ALL, flags, _capi.GS_MEM_DEVICE,
+                                  ov.data_ptr(), ow.data_ptr(), oc.data_ptr(), ok.data_ptr(),
+                                  oi.data_ptr(), occ.data_ptr(), oe.data_ptr(), C.byref(fp),
+                                  C.byref(fs)))
+        torch.cuda.synchronize()
+        ev_, ew_, ec_ = ov.cpu().numpy(), ow.cpu().numpy(), oc.cpu().numpy()
+        parity = {"sweeps": sweeps, "against": "oracle restatement, same GPU-built Laplacian, same inputs",
+                  "v_w_bit_identical": bool(np.array_equal(ev_, ref["v"]) and np.array_equal(ew_, ref["w"])),
+                  "max_rel_v": _max_rel(ev_, ref["v"]), "max_rel_w": _max_rel(ew_, ref["w"]),
+                  "max_rel_cost": _max_rel(ec_, ref["cost"])}
 
     if rank == 0:
         line = {
@@ -461,6 +474,7 @@ def run_engine(args):
             "clocks": clocks,
             "epilogue_kernels": {"launches": epi_n, "ms": epi_ms},
             "cpu_baseline": cpu,
+            "parity": parity,
             "fp32_mode": fp32,
         }
         print(json.dumps(line), flush=True)
