@@ -619,6 +619,7 @@ def run_engine_bary(args):
            "h2d_bytes_per_step": (hi - lo) * n * 8 + (hi - lo) * 8 + n * 8,
            "d2h_bytes_per_step": n * 8 + 2 * (hi - lo) * n * 8 + 4 + 4 + 8, "steps": e2e_steps}
     cpu = None
+    parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import pyoracle as po
@@ -626,10 +627,21 @@ def run_engine_bary(args):
         Lo = po.CSR(n, L.row_offsets().copy(), L.col_indices().copy(), L.values().copy())
         fo = po.Filter(Lo, 0, lap.lambda_max_bound, cfg.t, cfg.degree)
         t1 = time.perf_counter()
-        po.barycenter(fo, np.full(n, 1.0 / n), cfg.members, None, 1, TOL_RUN_ALL, L=po.lib(native=True))
+        ref = po.barycenter(fo, np.full(n, 1.0 / n), cfg.members, None, 1, TOL_RUN_ALL,
+                            L=po.lib(native=True))
         dt = time.perf_counter() - t1
-        cpu = {"value": 1.0 / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+        cpu = {"value": 1.0 / dt, "unit": "barycenter sweeps/s", "cores": os.cpu_count(), "kind": "port",
                "sample": f"1 barycenter sweep of the 8-member family on the GPU-built n={n} graph ({dt:.1f} s)"}
+        # results parity at full size: the engine's sweep on the same operator and family
+        rc = lib.gs_barycenter_ex(ctx.handle, filt._h, ah.data_ptr(), Mh.data_ptr(), hi - lo,
+                                  alh.data_ptr(), 1, TOL_RUN_ALL, _capi.GS_MEM_HOST, comm_arg, 0,
+                                  bh.data_ptr(), Vh.data_ptr(), Wh.data_ptr(), it.ctypes.data,
+                                  conv.ctypes.data, err.ctypes.data)
+        ctx.check(rc)
+        bary = bh.numpy().copy()
+        parity = {"sweeps": 1, "against": "oracle restatement, same GPU-built Laplacian, same family",
+                  "max_rel_barycenter": _max_rel(bary, ref["barycenter"]),
+                  "max_rel_V": _max_rel(Vh.numpy(), ref["V"]), "max_rel_W": _max_rel(Wh.numpy(), ref["W"])}
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": "barycenter sweeps/s", "n_gpus": world,
@@ -649,6 +661,7 @@ def run_engine_bary(args):
                          "traffic": None, "peak_kind": peak_kind, "bytes_per_launch": bytes_step,
                          "avg_launch_ms": avg, "launches_timed": step_n},
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": cpu,
+            "parity": parity,
             "iterations": int(it[0]), "marginal_error": float(err[0]),
         }), flush=True)
     dist.destroy_process_group()
