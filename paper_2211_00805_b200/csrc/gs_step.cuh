@@ -64,13 +64,6 @@ constexpr int kPrefetchStages = GS_PREFETCH_STAGES;
 #ifndef GS_IDX_PREFETCH
 #define GS_IDX_PREFETCH 1
 #endif
-// one 64-column fp64 row per warp: the value of each CSR entry is read by every lane from the
-// same address (one broadcast L1 wavefront, off the critical path: the fma needs it only after the
-// gather) instead of two 32-bit shuffles; the column index, which the gather address waits on,
-// stays a shuffle. 0 = shuffles, 1 = broadcast loads (the coalesced chunk load warms L1)
-#ifndef GS_VAL_LDG
-#define GS_VAL_LDG 0  // measured: 132.4 vs 128.1 us (more L1 requests cost more than the shuffles)
-#endif
 // one-row-per-lane layouts (own-row operands not staged by cp.async): load
 // T_{k-1}[row], T_{k-2}[row] and acc[row] into registers before the gathers, so the streams'
 // DRAM latency overlaps them instead of following them
@@ -439,7 +432,6 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
     const unsigned mask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << sub_lane0);
     const int pb = ri.pb, pe = ri.pe;  // first chunk loaded by the caller (k_cheb_step)
     constexpr int GB = L::GB;
-    constexpr bool VAL_LDG = GS_VAL_LDG && LPR == 32 && sizeof(S) == 8;
     int myc = ri.c;
     S myv = ri.v;
     for (int p0 = pb; p0 < pe; p0 += LPR) {
@@ -467,8 +459,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
 #pragma unroll
         for (int j = 0; j < GB; ++j) {
           cc[j] = __shfl_sync(mask, myc, u + j, LPR);
-          if constexpr (VAL_LDG) vv[j] = ld_idx(vals + p0 + u + j);
-          else vv[j] = __shfl_sync(mask, myv, u + j, LPR);
+          vv[j] = __shfl_sync(mask, myv, u + j, LPR);
         }
 #pragma unroll
         for (int j = 0; j < GB; ++j) ld_vec<S, VEC>(Tp + (size_t)cc[j] * GW, xx[j]);
@@ -479,9 +470,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
       }
       for (; u < cnt; ++u) {
         const int c = __shfl_sync(mask, myc, u, LPR);
-        S v;
-        if constexpr (VAL_LDG) v = ld_idx(vals + p0 + u);
-        else v = __shfl_sync(mask, myv, u, LPR);
+        const S v = __shfl_sync(mask, myv, u, LPR);
         S x[VEC];
         ld_vec<S, VEC>(Tp + (size_t)c * GW, x);
 #pragma unroll
