@@ -77,6 +77,11 @@ constexpr int kPrefetchStages = GS_PREFETCH_STAGES;
 #ifndef GS_CSR_VEC
 #define GS_CSR_VEC 1
 #endif
+// cp.async-staged own rows: 1 = T_{k-1}, T_{k-2}, acc; 0 = T_{k-2} and acc only, T_{k-1}[row]
+// read at the end of the row (an L1 hit: the row's diagonal entry has just gathered it)
+#ifndef GS_PRE_TP
+#define GS_PRE_TP 1
+#endif
 #ifndef GS_ROW_PREFETCH
 #define GS_ROW_PREFETCH 0  // measured neutral-to-slower on config 1 (one chunk per row)
 #endif
@@ -325,7 +330,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
                                          double (&mn)[Lay<GW, S>::VEC],
                                          double (&mx)[Lay<GW, S>::VEC],
                                          double (&er)[Lay<GW, S>::VEC], const S* pre,
-                                         int pre_stride, const RowIdx<S>& ri) {
+                                         int pre_stride, const RowIdx<S>& ri, bool pre_tp = true) {
   using L = Lay<GW, S>;
   constexpr int VEC = L::VEC, LPR = L::LPR;
   using P = Prec<S>;
@@ -484,7 +489,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
   }
   if (!valid) return;
   if (EARLY && early) finish_row<S, GW, MODE>(A, g, row, q, y, mn, mx, er, own, VEC);
-  else finish_row<S, GW, MODE>(A, g, row, q, y, mn, mx, er, pre, pre_stride);
+  else finish_row<S, GW, MODE>(A, g, row, q, y, mn, mx, er, pre, pre_stride, pre_tp);
 }
 
 // The rest of a row's step once y = (L_s T_{k-1})[row] is known: the recurrence, the deferred
@@ -698,7 +703,9 @@ __global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0
   if constexpr (PREFETCH) {
     constexpr int STG = kPrefetchStages;
     constexpr int PS = kStepThreads * VEC;  // elements per operand per stage
-    __shared__ __align__(128) S s_pre[STG][3][PS];
+    constexpr int TMA_ = sizeof(S) == 8 ? GS_TMA_OWN64 : GS_TMA_OWN32;
+    constexpr int NOPS = (GS_PRE_TP || TMA_ != 0) ? 3 : 2;  // staged operands per row
+    __shared__ __align__(128) S s_pre[STG][NOPS][PS];
     const size_t gbase = (size_t)g * A.ld * GW + q * VEC;
     auto issue = [&](int j) {
       const int row = base + j * BLOCK_ROWS;
@@ -708,10 +715,11 @@ __global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0
         constexpr int CE = 16 / (int)sizeof(S);
 #pragma unroll
         for (int h = 0; h < CH; ++h) {
-          cp_async16(d + h * CE, static_cast<const S*>(A.Tprev) + idx + h * CE);
-          if (A.k >= 2) cp_async16(d + PS + h * CE, static_cast<const S*>(A.Tout) + idx + h * CE);
+          constexpr int O = GS_PRE_TP ? 1 : 0;  // operand slot of T_{k-2}
+          if constexpr (GS_PRE_TP) cp_async16(d + h * CE, static_cast<const S*>(A.Tprev) + idx + h * CE);
+          if (A.k >= 2) cp_async16(d + O * PS + h * CE, static_cast<const S*>(A.Tout) + idx + h * CE);
           if (A.acc_terms > 0 && !A.acc_init)
-            cp_async16(d + 2 * PS + h * CE, static_cast<const S*>(A.acc) + idx + h * CE);
+            cp_async16(d + (O + 1) * PS + h * CE, static_cast<const S*>(A.acc) + idx + h * CE);
         }
       }
       cp_async_commit();
@@ -779,7 +787,7 @@ __global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0
       const RowIdx<S> nx = next_idx(j);
       cp_async_wait<STG - 1>();
       cheb_row<S, GW, MODE>(A, g, base + j * BLOCK_ROWS, sub, q, mn, mx, er,
-                            &s_pre[j % STG][0][threadIdx.x * VEC], PS, cur);
+                            &s_pre[j % STG][0][threadIdx.x * VEC], PS, cur, GS_PRE_TP != 0);
       cur = nx;
     }
   } else {
