@@ -82,6 +82,11 @@ constexpr int kPrefetchStages = GS_PREFETCH_STAGES;
 #ifndef GS_PRE_TP
 #define GS_PRE_TP 1
 #endif
+// 0: no shared-memory staging of the own rows; the wide layouts then load them into registers
+// before the gathers (GS_EARLY_OWN)
+#ifndef GS_WIDE_PREFETCH
+#define GS_WIDE_PREFETCH 1
+#endif
 #ifndef GS_ROW_PREFETCH
 #define GS_ROW_PREFETCH 0  // measured neutral-to-slower on config 1 (one chunk per row)
 #endif
@@ -341,9 +346,9 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
   const S* __restrict__ vals = static_cast<const S*>(A.vals);
   S own[3 * VEC];  // early own-row operands (GS_EARLY_OWN): tp, t2, a0
   // layouts whose own rows k_cheb_step stages in shared memory never take the early path
-  constexpr bool STAGED = VEC * sizeof(S) >= 16 && (VEC * sizeof(S)) % 16 == 0;
+  constexpr bool STAGED = GS_WIDE_PREFETCH && VEC * sizeof(S) >= 16 && (VEC * sizeof(S)) % 16 == 0;
   // measured: config 3 (one row per lane) 589 -> 564 us; config 2 (narrow rows) 341 -> 362 us
-  constexpr bool EARLY = GS_EARLY_OWN && !STAGED && LPR == 1;
+  constexpr bool EARLY = GS_EARLY_OWN && !STAGED && (LPR == 1 || !GS_WIDE_PREFETCH);
   const bool early = EARLY && !pre && valid && A.k != 0;
   if (EARLY && early) {
 #pragma unroll
@@ -652,7 +657,7 @@ __global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0
   using L = Lay<GW, S>;
   constexpr int VEC = L::VEC, LPR = L::LPR, RPW = L::RPW;
   constexpr int BLOCK_ROWS = (kStepThreads / 32) * RPW;
-  constexpr bool PREFETCH = VEC * sizeof(S) >= 16 && (VEC * sizeof(S)) % 16 == 0;
+  constexpr bool PREFETCH = GS_WIDE_PREFETCH && VEC * sizeof(S) >= 16 && (VEC * sizeof(S)) % 16 == 0;
   constexpr int CH = (int)(VEC * sizeof(S) / 16);  // 16-byte cp.async chunks per operand
   if (A.status && (A.status->error || A.status->done)) return;
   const int tl = blockIdx.x / A.Gl;
