@@ -416,3 +416,38 @@ def test_block_records_kernel_bit_exact(gs, n, blk, monkeypatch):
     for width in (33, 64, 100):
         X = np.random.default_rng(width + n).standard_normal((n, width))
         assert np.array_equal(f.apply(X), fo.apply(X))
+
+
+@pytest.mark.parametrize("width", [1, 3, 8, 16, 64, 100])
+def test_hub_rows_span_several_chunks(gs, width):
+    """Rows longer than one CSR chunk (32 entries for 64-column rows, 8 for narrow rows): a hub
+    joined to 150 vertices plus a ring, so the next-chunk prefetch and the chunk boundaries of
+    every layout are exercised; bit-exact against the oracle."""
+    from paper_2211_00805_b200.rng import Rng
+    n = 400
+    rng = Rng(99)
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        rows.append(i)
+        cols.append((i + 1) % n)
+        vals.append(rng.uniform(0.2, 1.0))
+    for j in range(1, 151):
+        rows.append(0)
+        cols.append(2 * j + 1)
+        vals.append(rng.uniform(0.1, 0.9))
+    for i in range(5, n, 37):  # a few more medium-degree rows
+        for d in (3, 11, 29, 47):
+            rows.append(i)
+            cols.append((i + d * 3) % n)
+            vals.append(rng.uniform(0.1, 0.5))
+    r, c, v = np.array(rows, np.int32), np.array(cols, np.int32), np.array(vals)
+    f, _ = engine_filter(r, c, v, n, 0, 0.9, 30)
+    fo = oracle_filter(r, c, v, n, 0, 0.9, 30)
+    X = np.random.default_rng(width).standard_normal((n, width))
+    if width == 1:
+        X = X[:, 0]
+    assert np.array_equal(f.apply(X), fo.apply(X))
+    X32 = np.asarray(X, np.float32).astype(np.float64)
+    y32 = f.apply(X32, fp32=True)
+    y64 = fo.apply(X32)
+    assert np.max(np.abs(y32 - y64)) <= 1e-4 * np.max(np.abs(y64))
