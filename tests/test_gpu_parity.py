@@ -416,6 +416,10 @@ def test_block_records_kernel_bit_exact(gs, n, blk, monkeypatch):
     for width in (33, 64, 100):
         X = np.random.default_rng(width + n).standard_normal((n, width))
         assert np.array_equal(f.apply(X), fo.apply(X))
+        # fp32 wide rows (own rows staged by per-warp TMA copies; odd n leaves a one-row warp)
+        X32 = X.astype(np.float32).astype(np.float64)
+        ref = fo.apply(X32)
+        assert np.max(np.abs(f.apply(X32, fp32=True) - ref)) <= 1e-4 * np.max(np.abs(ref))
 
 
 @pytest.mark.parametrize("width", [1, 3, 8, 16, 64, 100])
