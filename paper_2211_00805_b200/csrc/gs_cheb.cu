@@ -1592,9 +1592,17 @@ int halo_start(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const Work<S>
   return GS_OK;
 }
 
+// One column group (Bpad == GW): the received rows land straight in T's halo rows [nl, nl + nh),
+// whose layout equals the packed one, so no unpack pass follows.
 template <typename S>
-int halo_exchange(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Halo<S>& h) {
-  if (comm->alltoallv(comm->user, h.send.get(), h.sb.data(), h.recv.get(), h.rb.data(), p->nparts,
+inline bool halo_direct(const Work<S>& w) {
+  return w.G == 1;
+}
+
+template <typename S>
+int halo_exchange(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const Work<S>& w, S* T, Halo<S>& h) {
+  S* recv = halo_direct(w) ? T + (size_t)p->nl * w.GW : h.recv.get();
+  if (comm->alltoallv(comm->user, h.send.get(), h.sb.data(), recv, h.rb.data(), p->nparts,
                       (void*)ctx->comm_stream))
     return hook_fail(ctx, "alltoallv");
   GS_CUDA(ctx, cudaEventRecord(ctx->ev_received, ctx->comm_stream));
@@ -1605,7 +1613,7 @@ template <typename S>
 int halo_finish(gs_ctx* ctx, const gs_part* p, const Work<S>& w, S* T, Halo<S>& h) {
   cudaStream_t s = ctx->stream;
   GS_CUDA(ctx, cudaStreamWaitEvent(s, ctx->ev_received, 0));
-  if (p->nh > 0) {
+  if (p->nh > 0 && !halo_direct(w)) {
     gs_launch_begin(ctx, 1);
     k_halo_unpack<S><<<grid_for((int64_t)p->nh * w.Bpad), kThreads, 0, s>>>(h.recv.get(), p->nh, p->nl, w.ld, w.GW, w.Bpad, T);
     gs_launch_end(ctx, 1);
@@ -1668,7 +1676,7 @@ int run_apply_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& 
     // T_{k-1}'s boundary rows go out while the interior rows (no halo reads) are computed
     GS_TRY(halo_start<S>(ctx, p, comm, w, Tprev, h));
     launch_range(0, m);
-    GS_TRY(halo_exchange<S>(ctx, p, comm, h));
+    GS_TRY(halo_exchange<S>(ctx, p, comm, w, Tprev, h));
     GS_TRY(halo_finish<S>(ctx, p, w, Tprev, h));
     launch_range(1, m);
     launch_range(2, m);
