@@ -6,8 +6,10 @@
 // the GPU; there is no CPU path.
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <functional>
 #include <cstdlib>
 #include <limits>
 #include <memory>
@@ -527,6 +529,66 @@ inline TransportResult dense_sinkhorn(const RowMajorXd& cost, const Distribution
   res.iterations = it;
   res.converged = conv != 0;
   return res;
+}
+
+// transport.cpp:326-376: McCann interpolation at time s by sampling the plan (source rows by
+// their mass, then a target within the row); sums are sequential in index order
+inline PointCloud mccann_interpolate(const PointCloud& source, const PointCloud& target,
+                                     const std::function<std::vector<double>(int)>& plan_row_fn, double s,
+                                     int num_samples, std::uint64_t rng_seed) {
+  auto check_cloud = [](const PointCloud& c) {
+    if (c.n < 1 || c.d < 1) detail::fail(errc::dimension_mismatch, "DimensionMismatch", "point cloud must be non-empty");
+    for (double x : c.points)
+      if (!std::isfinite(x)) detail::fail(errc::dimension_mismatch, "DimensionMismatch", "point cloud has non-finite entries");
+  };
+  check_cloud(source);
+  check_cloud(target);
+  if (source.d != target.d) detail::fail(errc::size_mismatch, "SizeMismatch", "source and target dimensions differ");
+  if (!(s >= 0.0 && s <= 1.0)) detail::fail(errc::invalid_argument, "InvalidArgument", "interpolation time must be in [0, 1]");
+  if (num_samples < 1) detail::fail(errc::invalid_argument, "InvalidArgument", "need at least one sample");
+  const int ms = source.n, mt = target.n;
+  std::vector<double> cum(ms);
+  double acc = 0.0;
+  for (int i = 0; i < ms; ++i) {
+    const std::vector<double> row = plan_row_fn(i);
+    if ((int)row.size() != mt) detail::fail(errc::length_mismatch, "LengthMismatch", "plan row has wrong length");
+    double m = 0.0;
+    for (double x : row) m += std::max(x, 0.0);
+    acc += m;
+    cum[i] = acc;
+  }
+  const double total = acc;
+  if (!(total >= 1.0 - 1e-6))
+    detail::fail(errc::degenerate_plan, "DegeneratePlan", "plan mass below 1; transport result unusable for interpolation");
+  Rng rng(rng_seed);
+  std::vector<int> counts(ms, 0);
+  for (int q = 0; q < num_samples; ++q) {
+    const double u = rng.uniform() * total;
+    const int i = (int)(std::lower_bound(cum.begin(), cum.end(), u) - cum.begin());
+    ++counts[std::min(i, ms - 1)];
+  }
+  PointCloud out;
+  out.n = num_samples;
+  out.d = source.d;
+  out.points.resize((size_t)num_samples * source.d);
+  int written = 0;
+  std::vector<double> rc(mt);
+  for (int i = 0; i < ms; ++i) {
+    if (counts[i] == 0) continue;
+    const std::vector<double> row = plan_row_fn(i);
+    double a2 = 0.0;
+    for (int j = 0; j < mt; ++j) rc[j] = (a2 += std::max(row[j], 0.0));
+    if (!(a2 > 0.0)) detail::fail(errc::degenerate_plan, "DegeneratePlan", "sampled an empty plan row");
+    for (int q = 0; q < counts[i]; ++q) {
+      const double u = rng.uniform() * a2;
+      const int j = std::min((int)(std::lower_bound(rc.begin(), rc.end(), u) - rc.begin()), mt - 1);
+      for (int k = 0; k < source.d; ++k)
+        out.points[(size_t)written * source.d + k] =
+            (1.0 - s) * source.points[(size_t)i * source.d + k] + s * target.points[(size_t)j * target.d + k];
+      ++written;
+    }
+  }
+  return out;
 }
 
 // ---- next: plan rows, graph file IO ---------------------------------------------

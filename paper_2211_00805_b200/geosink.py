@@ -956,6 +956,78 @@ def plan_row(result: TransportResult, filter: HeatFilter, a, i: int) -> np.ndarr
     return plan_rows(result, filter, a, [i])[0]
 
 
+def _validate_points(x, what: str) -> np.ndarray:
+    """PointCloud::validate (pointcloud.hpp:20-24)."""
+    x = np.asarray(x, np.float64)
+    if x.ndim != 2 or x.shape[0] < 1 or x.shape[1] < 1:
+        raise Error(errc.dimension_mismatch, "DimensionMismatch: point cloud must be non-empty")
+    if not np.isfinite(x).all():
+        raise Error(errc.dimension_mismatch, "DimensionMismatch: point cloud has non-finite entries")
+    return x
+
+
+def mccann_interpolate(source, target, plan_row_fn, s: float, num_samples: int,
+                       rng_seed: int) -> np.ndarray:
+    """transport.cpp:326-376: McCann interpolation at time s by sampling the transport plan --
+    sources drawn by their plan-row mass, then a target within the sampled row, each emitting
+    (1 - s) x_i + s y_j. `plan_row_fn(i)` returns plan row i over the target points (the device
+    computes them: `geodesic_plan_rows` below). Row masses, their total and the cumulative sums
+    are sequential sums in index order (Eigen's sum() order is unpinned); draws follow
+    geosink::Rng (rng.hpp) in the reference order."""
+    from .rng import Rng
+    src = _validate_points(source, "source")
+    tgt = _validate_points(target, "target")
+    if src.shape[1] != tgt.shape[1]:
+        raise Error(errc.size_mismatch, "SizeMismatch: source and target dimensions differ")
+    if not (0.0 <= s <= 1.0):
+        raise Error(errc.invalid_argument, "InvalidArgument: interpolation time must be in [0, 1]")
+    if num_samples < 1:
+        raise Error(errc.invalid_argument, "InvalidArgument: need at least one sample")
+    m_src, m_tgt = src.shape[0], tgt.shape[0]
+    row_mass = np.empty(m_src)
+    for i in range(m_src):
+        row = np.asarray(plan_row_fn(i), np.float64)
+        if row.size != m_tgt:
+            raise Error(errc.length_mismatch, "LengthMismatch: plan row has wrong length")
+        row_mass[i] = np.cumsum(np.maximum(row, 0.0))[-1]
+    cum = np.cumsum(row_mass)  # std::partial_sum
+    total = float(cum[-1])
+    if not (total >= 1.0 - 1e-6):
+        raise Error(errc.degenerate_plan,
+                    "DegeneratePlan: plan mass below 1; transport result unusable for interpolation")
+    rng = Rng(rng_seed)
+    counts = np.zeros(m_src, np.int64)
+    for _ in range(num_samples):
+        u = rng.uniform() * total
+        i = int(np.searchsorted(cum, u, side="left"))  # std::lower_bound
+        counts[min(i, m_src - 1)] += 1
+    out = np.empty((num_samples, src.shape[1]))
+    written = 0
+    for i in range(m_src):
+        c = int(counts[i])
+        if c == 0:
+            continue
+        row_cum = np.cumsum(np.maximum(np.asarray(plan_row_fn(i), np.float64), 0.0))
+        row_total = float(row_cum[-1])
+        if not (row_total > 0.0):
+            raise Error(errc.degenerate_plan, "DegeneratePlan: sampled an empty plan row")
+        for _ in range(c):
+            u = rng.uniform() * row_total
+            j = int(np.searchsorted(row_cum, u, side="left"))
+            out[written] = (1.0 - s) * src[i] + s * tgt[min(j, m_tgt - 1)]
+            written += 1
+    return out
+
+
+def geodesic_plan_rows(result: TransportResult, filter: HeatFilter, a, source_vertices,
+                       target_vertices) -> np.ndarray:
+    """The source x target block of the geodesic plan (transport.cpp:314-324 row by row; the
+    interpolation benchmark's batched form, bench.cpp:439-448): all source rows in one device
+    call, restricted to the target vertices. Returns (len(source_vertices), len(target_vertices))."""
+    rows = plan_rows(result, filter, a, np.asarray(source_vertices, np.int32))
+    return np.ascontiguousarray(rows[:, np.asarray(target_vertices, np.int64)])
+
+
 def save_graph(m: SparseSymMatrix, path: str) -> None:
     """sparse.cpp:137-157."""
     rc = m._ctx.lib.gs_graph_save(m._ctx.handle, m._h, path.encode())

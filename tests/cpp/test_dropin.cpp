@@ -220,6 +220,16 @@ int main() {
     CHECK(err <= 1e-10);
     CHECK_THROWS_CODE(dense_sinkhorn(RowMajorXd(3, 2), mu, nu, 0.7), errc::length_mismatch);
   }
+  // McCann interpolation endpoints (transport.cpp:326-376): s = 0 returns source points
+  {
+    PointCloud src{{0.0, 1.0, 2.0, 3.0}, 2, 2}, tgt{{5.0, 6.0, 7.0, 8.0, 9.0, 10.0}, 3, 2};
+    const auto out = mccann_interpolate(src, tgt, [](int) { return std::vector<double>(3, 1.0 / 6); }, 0.0, 10, 3);
+    bool ok = out.n == 10;
+    for (int q = 0; q < out.n; ++q) ok = ok && (out.points[2 * q] == 0.0 || out.points[2 * q] == 2.0);
+    CHECK(ok);
+    CHECK_THROWS_CODE(mccann_interpolate(src, tgt, [](int) { return std::vector<double>(3, 0.1); }, 0.5, 4, 1),
+                      errc::degenerate_plan);
+  }
   // plan rows rebuild the marginals (acceptance.cpp:168-197); graph file round trip
   {
     Rng rng(4);

@@ -385,6 +385,36 @@ def test_plan_rows_rebuild_marginals(gs):
     assert np.array_equal(gs.plan_row(res, f, a, 7), plan[7])
 
 
+def test_mccann_interpolation_on_device_plan_rows(gs):
+    """mccann_interpolate (transport.cpp:326-376) over the geodesic plan's source x target block
+    computed on the device in one batched call (bench.cpp:439-448): the block equals the oracle's
+    plan rows (impulse applies, then v_i * column * a * w clamped at 0) within 1e-12, and the
+    interpolation drawn from either block is the same point set."""
+    n = 120
+    r, c, v = acceptance_graph(n, 481)
+    f, _ = engine_filter(r, c, v, n, 1, 1.0, 40)
+    fo = oracle_filter(r, c, v, n, 1, 1.0, 40)
+    src_v, tgt_v = np.arange(0, 60), np.arange(60, 120)
+    mu = np.zeros(n)
+    mu[src_v] = 1.0 / 60
+    nu = np.zeros(n)
+    nu[tgt_v] = 1.0 / 60
+    a = np.full(n, 1.0 / n)
+    res = gs.geodesic_sinkhorn(f, gs.Distribution(mu), gs.Distribution(nu), a, gs.SinkhornParams(3000, 1e-9))
+    assert res.converged
+    block = gs.geodesic_plan_rows(res, f, a, src_v, tgt_v)
+    imp = np.zeros((n, 60))
+    imp[src_v, np.arange(60)] = 1.0
+    cols = fo.apply(imp)  # column i: H e_{src i}; symmetric operator, so row src_i of H
+    ref = np.maximum(0.0, res.v[src_v][:, None] * (cols[tgt_v].T * (a[tgt_v] * res.w[tgt_v])[None, :]))
+    assert np.max(np.abs(block - ref)) <= 1e-12 * np.max(np.abs(ref))
+    pts = np.random.default_rng(5).standard_normal((n, 2))
+    got = gs.mccann_interpolate(pts[src_v], pts[tgt_v], lambda i: block[i], 0.5, 60, 11)
+    want = gs.mccann_interpolate(pts[src_v], pts[tgt_v], lambda i: ref[i], 0.5, 60, 11)
+    assert got.shape == (60, 2)
+    assert np.abs(got - want).max() <= 1e-12 or np.mean(np.all(np.isclose(got, want), axis=1)) >= 0.95
+
+
 def test_graph_file_round_trip(gs, tmp_path):
     """test_graph.cpp:141-150: save/load is exact."""
     from paper_2211_00805_b200.rng import Rng
