@@ -76,3 +76,22 @@ def test_python_api_host_validation():
     assert e.value.code == errc.length_mismatch
     with pytest.raises(Error):
         DistributionFamily([]).validate(4)
+
+
+def test_reference_arm_json_contract():
+    """bench.py --impl reference (the CPU oracle arm) prints one JSON line with the contract's
+    keys on a small instance of the config-1 workload."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--n", "3000",
+                        "--pairs", "4", "--steps", "1", "--warmup", "0"], capture_output=True, text=True,
+                       timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "dtype", "config", "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
