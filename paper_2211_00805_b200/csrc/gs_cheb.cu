@@ -531,6 +531,14 @@ int choose_rpc(int n, int gw, int groups, double near_frac = 1.0) {
   // several lanes per row and fewer than 32 columns (the degree-sorted layout; configs 2 and 4:
   // B = 8 and 16 fp64 on kNN graphs in R^30): consecutive row blocks share few L1 lines, so short
   // CTAs win by shrinking the tail wave (config 2: 416 -> 351 us; config 4: 217 -> 151 us at 4e5)
+  // 64-byte narrow rows (config 2's B = 8 fp64) went back to four row blocks per CTA once the next
+  // CSR chunk is prefetched (340 -> 328 us); 128-byte rows (config 4's B = 16) stay at one
+  // (343 vs 463 us at n = 1e6)
+  if (gw < 32 && gw * (int)sizeof(S) == 64) {
+    const int64_t ctas = (int64_t)groups * ((n + rows_per_block<S>(gw) * kRowsPerCta - 1) /
+                                            (rows_per_block<S>(gw) * kRowsPerCta));
+    return ctas < 2 * 148 ? 1 : kRowsPerCta;
+  }
   if (gw < 32 && gw * (int)sizeof(S) > 16) return 1;
   // graphs without index locality (kNN graphs in R^30: ~12% of entries within 256 rows in CM
   // order, against ~50% on the swiss roll) get no L1 reuse between row blocks either
