@@ -518,6 +518,22 @@ inline int w1_max_rows() {
   return v;
 }
 
+// row blocks per CTA of the full (multi-block) instantiation of a group width
+template <typename S>
+int rpc_full(int gw) {
+  int lpr = 1;
+  switch (gw) {
+    case 64: lpr = Lay<64, S>::LPR; break;
+    case 32: lpr = Lay<32, S>::LPR; break;
+    case 16: lpr = Lay<16, S>::LPR; break;
+    case 8: lpr = Lay<8, S>::LPR; break;
+    case 4: lpr = Lay<4, S>::LPR; break;
+    case 2: lpr = Lay<2, S>::LPR; break;
+    default: lpr = Lay<1, S>::LPR; break;
+  }
+  return lpr == 1 ? kRowsPerCta1 : kRowsPerCta;
+}
+
 // Row blocks per CTA: kRowsPerCta (L1 reuse across consecutive blocks) unless that leaves fewer
 // than two CTAs per SM, in which case 1 (small, latency-bound problems such as config 0).
 template <typename S>
@@ -527,7 +543,7 @@ int choose_rpc(int n, int gw, int groups, double near_frac = 1.0) {
     return e ? atoi(e) : 0;
   }();
   if (forced == 1) return 1;
-  if (forced > 1) return kRowsPerCta;
+  if (forced > 1) return rpc_full<S>(gw);
   // several lanes per row and fewer than 32 columns (the degree-sorted layout; configs 2 and 4:
   // B = 8 and 16 fp64 on kNN graphs in R^30): consecutive row blocks share few L1 lines, so short
   // CTAs win by shrinking the tail wave (config 2: 416 -> 351 us; config 4: 217 -> 151 us at 4e5)
@@ -543,9 +559,9 @@ int choose_rpc(int n, int gw, int groups, double near_frac = 1.0) {
   // graphs without index locality (kNN graphs in R^30: ~12% of entries within 256 rows in CM
   // order, against ~50% on the swiss roll) get no L1 reuse between row blocks either
   if (near_frac < 0.3) return 1;
-  const int64_t ctas = (int64_t)groups * ((n + rows_per_block<S>(gw) * kRowsPerCta - 1) /
-                                          (rows_per_block<S>(gw) * kRowsPerCta));
-  return ctas < 2 * 148 ? 1 : kRowsPerCta;
+  const int full = rpc_full<S>(gw);
+  const int64_t ctas = (int64_t)groups * ((n + rows_per_block<S>(gw) * full - 1) / (rows_per_block<S>(gw) * full));
+  return ctas < 2 * 148 ? 1 : full;
 }
 
 template <typename S, int GW, int RPC>
@@ -562,6 +578,7 @@ void launch_step_rpc(const StepArgs& A, int mode, cudaStream_t s) {
 template <typename S, int GW>
 void launch_step_gw(const StepArgs& A, int mode, int rpc, cudaStream_t s) {
   if (rpc == 1) launch_step_rpc<S, GW, 1>(A, mode, s);
+  else if constexpr (Lay<GW, S>::LPR == 1) launch_step_rpc<S, GW, kRowsPerCta1>(A, mode, s);
   else launch_step_rpc<S, GW, kRowsPerCta>(A, mode, s);
 }
 

@@ -41,6 +41,10 @@ constexpr int kStepThreads = GS_STEP_THREADS;  // threads of a k_cheb_step CTA
 #define GS_ROWS_PER_CTA 4
 #endif
 constexpr int kRowsPerCta = GS_ROWS_PER_CTA;
+#ifndef GS_ROWS_PER_CTA1
+#define GS_ROWS_PER_CTA1 4
+#endif
+constexpr int kRowsPerCta1 = GS_ROWS_PER_CTA1;  // row blocks per CTA, one-row-per-lane layouts
 #ifndef GS_GATHER_BATCH
 #define GS_GATHER_BATCH 4
 #endif
