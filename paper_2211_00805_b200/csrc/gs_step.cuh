@@ -53,6 +53,9 @@ constexpr int kGatherBatch = GS_GATHER_BATCH;  // neighbour rows in flight per l
 #define GS_GATHER_BATCH32 3
 #endif
 constexpr int kGatherBatch32 = GS_GATHER_BATCH32;  // wide fp32 rows (fewer registers -> 6 CTAs/SM)
+#ifndef GS_GATHER_BATCH_MID
+#define GS_GATHER_BATCH_MID 8
+#endif
 #ifndef GS_NARROW_GATHER_BATCH
 #define GS_NARROW_GATHER_BATCH 8
 #endif
@@ -163,8 +166,12 @@ struct Lay {
   // gathers in flight per row: narrow rows have few registers per gather, so go deeper
   // wider lanes keep the bytes in flight per lane: batch scaled down by VB / 16
   static constexpr int GBW0 = (sizeof(S) == 4 ? kGatherBatch32 : kGatherBatch) * 16 / (VB > 16 ? VB : 16);
+  // fp64 rows wider than a narrow row but shorter than a warp (B = 16 / 32: 128 / 256 bytes,
+  // config 4): a whole chunk's gathers in flight, fewer CTAs (GS_*_MID)
+  static constexpr bool MID = WIDE && LPR < 32 && sizeof(S) == 8;
   static constexpr int GB = NARROW ? (GS_NARROW_GATHER_BATCH < LPR ? GS_NARROW_GATHER_BATCH : LPR)
-                                   : (GBW0 < 1 ? 1 : GBW0);
+                                   : MID ? (GS_GATHER_BATCH_MID < LPR ? GS_GATHER_BATCH_MID : LPR)
+                                         : (GBW0 < 1 ? 1 : GBW0);
 };
 
 // order-preserving uint64 keys for doubles (atomic min/max of signed values)
@@ -647,6 +654,9 @@ __device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int til
 #ifndef GS_MIN_BLOCKS
 #define GS_MIN_BLOCKS 5
 #endif
+#ifndef GS_MIN_BLOCKS_MID
+#define GS_MIN_BLOCKS_MID 4  // config-4 shape at n = 1e6: 343 -> 319 us with GS_GATHER_BATCH_MID 8
+#endif
 #ifndef GS_MIN_BLOCKS_NARROW
 #define GS_MIN_BLOCKS_NARROW 5
 #endif
@@ -656,6 +666,7 @@ __device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int til
 template <typename S, int GW, int MODE, int RPC>
 __global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0
                                                   : (Lay<GW, S>::NARROW ? GS_MIN_BLOCKS_NARROW
+                                                     : Lay<GW, S>::MID ? GS_MIN_BLOCKS_MID
                                                      : (sizeof(S) == 4 ? GS_MIN_BLOCKS32 : GS_MIN_BLOCKS)))
     k_cheb_step(const StepArgs A) {
   using L = Lay<GW, S>;
