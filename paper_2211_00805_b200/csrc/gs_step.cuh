@@ -22,6 +22,13 @@
 //     BARY_PSI: psi -> colmin and stored for the log-domain geometric mean.
 // Column min/max are order-free (atomics on order-preserving keys of the double value); the L1
 // error is accumulated in double through fixed-order per-CTA partials (deterministic).
+//
+// Per-layout choices (measured, profiles/r01c_summary.md): 512-byte fp64 rows (B = 64) one warp
+// per row, gather batch 4, 48 registers / 5 CTAs, own rows staged by cp.async; 128/256-byte fp64
+// rows (B = 16/32) batch 8, 64 registers / 4 CTAs; 64-byte narrow rows (B = 8) 8-byte lanes,
+// 8 gathers, four row blocks per CTA; one row per lane (B <= 2 fp64 / 4 fp32) own rows loaded
+// before the gathers, fp32 CSR read with aligned 16-byte loads; fp32 wide rows stage their own
+// rows with per-warp TMA bulk copies.
 #pragma once
 
 #include <cfloat>
