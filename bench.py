@@ -152,7 +152,9 @@ def cpu_sinkhorn_sample(L_host, lam, cfg, sweeps, native=True):
 
 
 def run_reference(args):
-    """--impl reference: the CPU reference path (oracle port, all host threads), rank 0 only."""
+    """--impl reference: the CPU reference path (oracle port, all host threads), rank 0 only.
+    Inputs come from the oracle's own Rng (oracle/pyoracle.py), so this arm never loads the
+    product library."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
@@ -160,6 +162,7 @@ def run_reference(args):
     import pyoracle as po
     from paper_2211_00805_b200 import workloads
 
+    workloads.set_rng_class(po.Rng)
     lib = po.lib(native=True)
     cfg = make_config(args)
     t0 = time.perf_counter()
@@ -169,7 +172,7 @@ def run_reference(args):
     setup_s = time.perf_counter() - t0
     n = args.n
     a = np.full(n, 1.0 / n)
-    sweeps = args.ref_sweeps
+    sweeps = max(2, args.ref_sweeps)
 
     def step():
         po.sinkhorn_batch(fo, a, cfg.mus, cfg.nus, sweeps, TOL_RUN_ALL, flags=1, L=lib)
@@ -187,14 +190,26 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * dt / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": config_dict(args, A.nnz, lam, rounds, sigma, extra={"setup_s": setup_s}),
+        "config": config_dict(args),
+        "operator": {"nnz_adjacency": int(A.nnz), "lambda_max_bound": lam, "lambda_rounds": rounds,
+                     "sigma": sigma, "setup_s": setup_s, "built_by": "oracle (CPU kNN)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{sweeps} sweep(s) of the 64-pair batch per step on the full "
+                         "sample": f"{sweeps} sweeps of the {args.pairs}-pair batch per step on the full "
                                    f"n={n} graph (oracle restatement, OpenMP, -march=native)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "product_library_loaded": _product_lib_mapped(),
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _product_lib_mapped():
+    """True when libgeosink_b200.so is mapped into this process (the reference arm must not)."""
+    try:
+        with open("/proc/self/maps") as f:
+            return "libgeosink_b200" in f.read()
+    except OSError:
+        return None
 
 
 def make_config(args, rank=0):
@@ -208,20 +223,18 @@ def make_config(args, rank=0):
     return workloads.config1(args.n, args.pairs, seed=1, pair_seed=2 + 1000 * rank)
 
 
-def config_dict(args, nnz_A, lam, rounds, sigma, extra=None):
-    d = {
+def config_dict(args):
+    """The workload definition, identical in both arms (operator details that depend on how the
+    graph was built -- lambda, sigma, timings -- live under "operator")."""
+    return {
         "workload": (f"config{args.config}: swiss roll n={args.n}, k=10 symmetrised kNN, Gaussian weights "
                      f"sigma=median eps_10, combinatorial L, t=1, K=30, {args.pairs} pairs x "
                      f"{args.sweeps} sweeps (2 x {args.pairs}-column applies per sweep), fp64"),
-        "n": args.n, "pairs": args.pairs, "sweeps_per_step": args.sweeps, "degree": 30,
-        "nnz_adjacency": int(nnz_A), "lambda_max_bound": lam, "lambda_rounds": rounds,
-        "sigma": sigma, "stagnation_abort": "disabled (bench-only, DESIGN.md)",
+        "n": args.n, "pairs": args.pairs, "sweeps_per_run": args.sweeps, "degree": 30,
+        "stagnation_abort": "disabled (bench-only, DESIGN.md)",
         "tol": "5e-324 (all sweeps run)",
         "l2": "working set > 0.8 GB >> 126 MB L2; no flush needed between steps",
     }
-    if extra:
-        d.update(extra)
-    return d
 
 
 # --------------------------------------------------------------------------- GPU arm
@@ -453,12 +466,13 @@ def run_engine(args):
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": config_dict(args, A.stored_entries(), lap.lambda_max_bound,
-                                  lap.power_rounds, sigma,
-                                  extra={"nnz_L": int(nnz_L), "graph_build_s": t_graph,
-                                         "prepare_s": t_prep,
-                                         "parallelism": f"replicas x{world} (pairs per rank)",
-                                         "column_sweeps_per_s": value * P}),
+            "config": config_dict(args),
+            "operator": {"nnz_adjacency": int(A.stored_entries()), "nnz_L": int(nnz_L),
+                         "lambda_max_bound": lap.lambda_max_bound, "lambda_rounds": lap.power_rounds,
+                         "sigma": sigma, "graph_build_s": t_graph, "prepare_s": t_prep,
+                         "built_by": "engine (device kNN)",
+                         "parallelism": f"replicas x{world} (pairs per rank)",
+                         "column_sweeps_per_s": value * P},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "kernel": ("k_cheb_step<double, 64, *, 4> (fused Chebyshev step, one warp per 512-byte row)"
@@ -1056,7 +1070,7 @@ def main():
     ap.add_argument("--sweeps", type=int, default=200)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sweeps", type=int, default=1)
-    ap.add_argument("--ref-sweeps", type=int, default=1)
+    ap.add_argument("--ref-sweeps", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])

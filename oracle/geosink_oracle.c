@@ -144,6 +144,32 @@ void go_rng_below(uint64_t seed, uint64_t bound, int64_t count, uint64_t* out) {
   for (int64_t i = 0; i < count; ++i) out[i] = rng_below(&r, bound);
 }
 
+/* Stateful handle (the reference arm's input generators draw from one Rng across calls, as the
+ * reference's own generators do with a geosink::Rng object). */
+void* go_rng_new(uint64_t seed) {
+  go_rng* r = (go_rng*)malloc(sizeof(go_rng));
+  if (r) rng_init(r, seed);
+  return r;
+}
+void go_rng_free(void* r) { free(r); }
+uint64_t go_rng_next_bits(void* r) { return rng_next((go_rng*)r); }
+double go_rng_next_uniform(void* r) { return rng_uniform((go_rng*)r); }
+double go_rng_next_normal(void* r) { return rng_normal((go_rng*)r); }
+uint64_t go_rng_next_below(void* r, uint64_t n) { return rng_below((go_rng*)r, n); }
+/* repeating draw pattern, kind[e % npat]: 0 -> lo + (hi - lo) U, 1 -> hi N (+ lo), 2 -> below(hi) */
+void go_rng_fill_pattern(void* h, double* out, int64_t count, const int* kind, const double* lo,
+                         const double* hi, int npat) {
+  go_rng* r = (go_rng*)h;
+  for (int64_t e = 0; e < count; ++e) {
+    const int q = (int)(e % npat);
+    switch (kind[q]) {
+      case 0: out[e] = lo[q] + (hi[q] - lo[q]) * rng_uniform(r); break;
+      case 1: out[e] = lo[q] == 0.0 ? hi[q] * rng_normal(r) : lo[q] + hi[q] * rng_normal(r); break;
+      default: out[e] = (double)rng_below(r, (uint64_t)hi[q]); break;
+    }
+  }
+}
+
 /* ------------------------------------------------------------------------------------------
  * Sorting helper: LSD radix sort of (key, value) records by 64-bit key.
  * ---------------------------------------------------------------------------------------- */

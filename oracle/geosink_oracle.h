@@ -43,6 +43,15 @@ void go_rng_uniform(uint64_t seed, int64_t count, double* out);
 void go_rng_normal(uint64_t seed, int64_t count, double* out);
 void go_rng_below(uint64_t seed, uint64_t bound, int64_t count, uint64_t* out);
 uint64_t go_rng_seed_mix(uint64_t a, uint64_t b);
+/* stateful handle: one Rng object drawn across calls */
+void* go_rng_new(uint64_t seed);
+void go_rng_free(void* r);
+uint64_t go_rng_next_bits(void* r);
+double go_rng_next_uniform(void* r);
+double go_rng_next_normal(void* r);
+uint64_t go_rng_next_below(void* r, uint64_t n);
+void go_rng_fill_pattern(void* r, double* out, int64_t count, const int* kind, const double* lo,
+                         const double* hi, int npat);
 
 /* sparse.cpp:15-53 */
 int go_csr_from_triplets(int n, int64_t m, const int* rows, const int* cols, const double* vals,

@@ -64,6 +64,18 @@ def _declare(L):
     L.go_rng_below.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, _up]
     L.go_rng_seed_mix.argtypes = [C.c_uint64, C.c_uint64]
     L.go_rng_seed_mix.restype = C.c_uint64
+    L.go_rng_new.restype = C.c_void_p
+    L.go_rng_new.argtypes = [C.c_uint64]
+    L.go_rng_free.argtypes = [C.c_void_p]
+    L.go_rng_next_bits.restype = C.c_uint64
+    L.go_rng_next_bits.argtypes = [C.c_void_p]
+    L.go_rng_next_uniform.restype = C.c_double
+    L.go_rng_next_uniform.argtypes = [C.c_void_p]
+    L.go_rng_next_normal.restype = C.c_double
+    L.go_rng_next_normal.argtypes = [C.c_void_p]
+    L.go_rng_next_below.restype = C.c_uint64
+    L.go_rng_next_below.argtypes = [C.c_void_p, C.c_uint64]
+    L.go_rng_fill_pattern.argtypes = [C.c_void_p, _dp, C.c_int64, _ip, _dp, _dp, C.c_int]
     L.go_csr_from_triplets.argtypes = [C.c_int, C.c_int64, _ip, _ip, _dp, C.POINTER(go_csr)]
     L.go_csr_from_arrays.argtypes = [C.c_int, C.c_int64, _ip, _ip, _dp, C.POINTER(go_csr)]
     L.go_csr_free.argtypes = [C.POINTER(go_csr)]
@@ -128,6 +140,54 @@ def rng_below(seed: int, bound: int, count: int) -> np.ndarray:
     out = np.empty(count, np.uint64)
     lib().go_rng_below(seed, bound, count, out)
     return out
+
+
+class Rng:
+    """Stateful geosink::Rng (rng.hpp:13-68) on the oracle: the same interface as the engine's
+    paper_2211_00805_b200.rng.Rng, so input generators can run without the product library
+    (the reference arm of bench.py)."""
+
+    def __init__(self, seed: int):
+        self._L = lib()
+        self.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+        self._h = self._L.go_rng_new(self.seed)
+
+    def fork(self, stream: int) -> "Rng":
+        return Rng(self.seed_mix(self.seed, stream))
+
+    def bits(self) -> int:
+        return int(self._L.go_rng_next_bits(self._h))
+
+    def uniform(self, lo=None, hi=None) -> float:
+        u = float(self._L.go_rng_next_uniform(self._h))
+        return u if lo is None else lo + (hi - lo) * u
+
+    def normal(self) -> float:
+        return float(self._L.go_rng_next_normal(self._h))
+
+    def below(self, n: int) -> int:
+        return int(self._L.go_rng_next_below(self._h, n))
+
+    @staticmethod
+    def seed_mix(a: int, b: int) -> int:
+        return int(lib().go_rng_seed_mix(a & 0xFFFFFFFFFFFFFFFF, b & 0xFFFFFFFFFFFFFFFF))
+
+    def pattern(self, count: int, spec) -> np.ndarray:
+        kinds = np.array([{"u": 0, "n": 1, "b": 2}[k] for k, _, _ in spec], np.int32)
+        lo = np.array([float(l) for _, l, _ in spec], np.float64)
+        hi = np.array([float(h) for _, _, h in spec], np.float64)
+        out = np.empty(count, np.float64)
+        self._L.go_rng_fill_pattern(self._h, out, count, kinds, lo, hi, len(spec))
+        return out
+
+    def normals(self, count: int) -> np.ndarray:
+        return self.pattern(count, [("n", 0.0, 1.0)])
+
+    def __del__(self):
+        try:
+            self._L.go_rng_free(self._h)
+        except Exception:
+            pass
 
 
 def ref_rng():

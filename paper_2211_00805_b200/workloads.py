@@ -18,9 +18,25 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .rng import Rng
-
 TWO_PI = 2.0 * math.pi
+
+
+_RNG_CLASS = None
+
+
+def set_rng_class(cls) -> None:
+    """Draw inputs from another geosink::Rng implementation with the same interface (the
+    reference arm of bench.py uses the oracle's, oracle/pyoracle.py Rng, so it never loads the
+    product library). None restores the engine's host RNG (paper_2211_00805_b200/rng.py)."""
+    global _RNG_CLASS
+    _RNG_CLASS = cls
+
+
+def Rng(seed: int):
+    if _RNG_CLASS is not None:
+        return _RNG_CLASS(seed)
+    from .rng import Rng as EngineRng
+    return EngineRng(seed)
 
 
 def _normalise(w: np.ndarray) -> np.ndarray:

@@ -95,3 +95,4 @@ def test_reference_arm_json_contract():
         assert key in line, key
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+    assert line["product_library_loaded"] is False  # inputs drawn with the oracle's Rng
