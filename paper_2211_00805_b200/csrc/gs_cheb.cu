@@ -30,7 +30,16 @@ struct FinArgs {
   gs_status* status;
   int knp_code;
   double slack;
+  double* scale;  // fp32 mode: per-column power of two of the next input (nullptr in fp64)
 };
+
+// largest power of two <= m (1 for m <= 0 or non-finite): the fp32 mode's per-column input scale
+__device__ __forceinline__ double pow2_floor(double m) {
+  if (!(m > 0.0) || !isfinite(m)) return 1.0;
+  int e = 0;
+  frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
+  return ldexp(1.0, e - 1);
+}
 
 __global__ void __launch_bounds__(kThreads) k_finalize(const FinArgs F) {
   const int col = blockIdx.x;
@@ -53,6 +62,7 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const FinArgs F) {
     if (!(mn >= -F.cs.thr[col])) atomicCAS(&F.status->error, 0, F.knp_code);
   }
   if (F.has_next) F.cs.thr[col] = F.slack * dunkey(F.cs.cmax[col]);
+  if (F.has_next && F.scale) F.scale[col] = pow2_floor(dunkey(F.cs.cmax[col]));
   if (F.has_err) F.cs.errcol[col] = sh[0];
   F.cs.cmin[col] = KEY_POS_INF;
   F.cs.cmax[col] = KEY_ZERO;
@@ -72,6 +82,7 @@ struct CtlArgs {
   gs_status* status;
   int* sweep_ctr;  // device sweep counter (so a captured sweep can be replayed)
   int P, max_iter, no_abort;
+  int fp32;  // a non-finite marginal error is numerical_underflow (the fp32 range was left)
   double tol;
 };
 
@@ -85,6 +96,12 @@ __global__ void k_sk_control(const CtlArgs C) {
     const double err = C.errcol[c];
     C.iters[c] = s;
     C.err_out[c] = err;
+    if (C.fp32 && !isfinite(err)) {
+      st->error = ERRC_NUMERICAL_UNDERFLOW + 1;
+      st->fail_pair = c;
+      st->fail_sweep = s;
+      return;
+    }
     const bool done = err <= C.tol;
     if (done) C.conv[c] = 1;
     if (done || s == C.max_iter) C.final_sweep[c] = s;
@@ -115,7 +132,8 @@ __global__ void k_sk_control(const CtlArgs C) {
 // ---- layout conversion: column-major fp64 (API) <-> grouped row-major S (engine) ------------
 template <typename S>
 __global__ void k_pack(const double* __restrict__ src, S* __restrict__ dst, int n, int width,
-                       int GW, int G, const int* __restrict__ order, int64_t ld) {
+                       int GW, int G, const int* __restrict__ order, int64_t ld,
+                       const double* __restrict__ scale = nullptr) {
   const int64_t total = (int64_t)G * n * GW;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -125,14 +143,17 @@ __global__ void k_pack(const double* __restrict__ src, S* __restrict__ dst, int 
     const int g = (int)(r / n);
     const int col = g * GW + c;
     const int o = order ? order[i] : i;
-    dst[((size_t)g * ld + i) * GW + c] = col < width ? S(src[(size_t)col * n + o]) : S(0);
+    double v = col < width ? src[(size_t)col * n + o] : 0.0;
+    if (scale && col < width) v = ldexp(v, -ilogb(scale[col]));  // exact: scale is 2^e
+    dst[((size_t)g * ld + i) * GW + c] = S(v);
   }
 }
 
 template <typename S>
 __global__ void k_unpack(const S* __restrict__ src, double* __restrict__ dst, int n, int width,
                          int GW, const S* __restrict__ alt, const int* __restrict__ sel,
-                         const int* __restrict__ newpos, int64_t ld) {
+                         const int* __restrict__ newpos, int64_t ld,
+                         const double* __restrict__ scale = nullptr) {
   const int64_t total = (int64_t)width * n;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -142,7 +163,7 @@ __global__ void k_unpack(const S* __restrict__ src, double* __restrict__ dst, in
     const int g = col / GW, c = col % GW;
     const size_t idx = ((size_t)g * ld + i) * GW + c;
     const S* s = (alt && sel && (sel[col] & 1)) ? alt : src;
-    dst[e] = (double)s[idx];
+    dst[e] = scale ? (double)s[idx] * scale[col] : (double)s[idx];
   }
 }
 
@@ -185,6 +206,48 @@ __global__ void k_sk_init(const S* __restrict__ a, S* __restrict__ T0, int n, in
   }
   if (threadIdx.x == 0)
     for (int c = 0; c < B; ++c) atomicMax(cmax + c, dkey(sh[0]));
+}
+
+// fp32 mode: the next T_0 (fp64, unscaled, written by the epilogue / k_sk_init / k_bary_w) divided
+// by its column's power of two (exact) and rounded to fp32 -- the input of the next apply
+__global__ void k_rescale32(const double* __restrict__ T0d, const double* __restrict__ scale,
+                            float* __restrict__ T, int n, int GW, int G, int64_t ld) {
+  const int64_t total = (int64_t)G * n * GW;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % GW);
+    const int64_t r = e / GW;
+    const int i = (int)(r % n);
+    const int g = (int)(r / n);
+    const size_t idx = ((size_t)g * ld + i) * GW + c;
+    T[idx] = (float)ldexp(T0d[idx], -ilogb(scale[g * GW + c]));
+  }
+}
+
+// per-column max |x| of a column-major fp64 block (order-free: atomics on keys)
+__global__ void k_colmax_cm(const double* __restrict__ X, int64_t n, unsigned long long* keys) {
+  const int col = blockIdx.y;
+  double m = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(X[(size_t)col * n + i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(keys + col, dkey(m));
+}
+
+__global__ void k_scale_from_keys(const unsigned long long* keys, int B, double* scale) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < B) scale[c] = pow2_floor(dunkey(keys[c]));
+}
+
+__global__ void k_keys_to_double(const unsigned long long* keys, int B, double* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < B) out[c] = dunkey(keys[c]);
+}
+
+__global__ void k_scale_from_max(const double* mx, int B, double* scale) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < B) scale[c] = pow2_floor(mx[c]);
 }
 
 // ---- validation (transport.cpp:56-66, 96-102; barycenter.cpp:32-43) ----------------------------
@@ -279,16 +342,21 @@ __global__ void k_sk_cost_final(const double* part, int64_t nchunks, int P, doub
 }
 
 // ---- barycenter row kernels (barycenter.cpp:75-84), computed in double ----------------------
-template <typename S>
-__global__ void k_bary_lb(const S* __restrict__ psi, const double* __restrict__ alphas, int n, int m,
-                          int GW, double* __restrict__ lb, const gs_status* st) {
+// division / log floor of column c: kFloor = 1e-300 (fp64), or the fp32 mode's range floor
+__device__ __forceinline__ double col_floor(const double* scale, int c) {
+  return scale ? fmax(GS_FLOOR, scale[c] * kF32Floor) : GS_FLOOR;
+}
+
+__global__ void k_bary_lb(const double* __restrict__ psi, const double* __restrict__ alphas, int n, int m,
+                          int GW, double* __restrict__ lb, const gs_status* st,
+                          const double* __restrict__ scale) {
   if (st->error || st->done) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double acc = 0.0;
   for (int c = 0; c < m; ++c) {
     const double v = psi[((size_t)(c / GW) * n + i) * GW + (c % GW)];
-    const double ps = fmin(fmax(v, GS_FLOOR), GS_CEIL);
+    const double ps = fmin(fmax(v, col_floor(scale, c)), GS_CEIL);
     acc = fma(alphas[c], log(ps), acc);
   }
   lb[i] = acc;
@@ -372,11 +440,10 @@ constexpr int kBaryColChunk = 2048;  // columns per shared-memory max pass of k_
 
 // bary /= mass; W_c = bary / max(psi_c, floor); T_0 = a * W_c; colmax |T_0| (order-free max:
 // warp shuffle, one shared-memory atomic per warp, one global atomic per CTA and column)
-template <typename S>
 __global__ void k_bary_w(double* __restrict__ bary, const double* __restrict__ mass,
-                         const S* __restrict__ psi, const S* __restrict__ a, int n, int m, int GW,
-                         S* __restrict__ W, S* __restrict__ T0, unsigned long long* cmax,
-                         const gs_status* st) {
+                         const double* psi, const double* __restrict__ a, int n, int m, int GW,
+                         double* __restrict__ W, double* T0, unsigned long long* cmax,
+                         const gs_status* st, const double* __restrict__ scale) {
   __shared__ unsigned long long s_max[kBaryColChunk];
   if (st->error || st->done) return;  // the same status word for the whole grid
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -396,11 +463,11 @@ __global__ void k_bary_w(double* __restrict__ bary, const double* __restrict__ m
       double v = 0.0;
       if (ok) {
         const size_t idx = ((size_t)(c / GW) * n + i) * GW + (c % GW);
-        const double w = b / fmax((double)psi[idx], (double)Prec<S>::floor);
-        W[idx] = S(w);
-        const S t0 = S(ai * w);
-        T0[idx] = t0;
-        v = fabs((double)t0);
+        const double w = b / fmax(psi[idx], col_floor(scale, c));
+        W[idx] = w;
+        const double t0 = ai * w;
+        T0[idx] = t0;  // fp32 mode: psi and T0 share T0d (this thread reads idx before writing it)
+        v = fabs(t0);
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -419,12 +486,17 @@ __global__ void k_bary_errlocal(const double* errcol, int m, double* errbuf) {
 }
 
 __global__ void k_bary_control(const double* errbuf, gs_status* st, int* sweep_ctr, double tol,
-                               int* iters, int* conv, double* err_out, int max_iter) {
+                               int* iters, int* conv, double* err_out, int max_iter, int fp32) {
   const int sweep = ++(*sweep_ctr);  // device counter: a captured sweep can be replayed
   if (st->error || st->done) return;
   const double err = *errbuf;
   *err_out = err;
   *iters = sweep;
+  if (fp32 && !isfinite(err)) {  // the fp32 recurrence's range was left
+    st->error = ERRC_NUMERICAL_UNDERFLOW + 1;
+    st->fail_sweep = sweep;
+    return;
+  }
   if (err <= tol) {
     *conv = 1;
     st->done = 1;
@@ -745,6 +817,9 @@ struct Work {
   DevBuf<double> thr, errcol, part_err;
   DevBuf<int> active, gactive;
   DevBuf<gs_status> status;
+  // fp32 mode: the next T_0 / psi in fp64 before scaling, and the per-column input scale 2^e_c
+  DevBuf<double> T0d, scale;
+  static constexpr bool kF32 = sizeof(S) == 4;
   int init(gs_ctx* ctx, int n_, int B_, bool want_err, int64_t ld_ = -1, const gs_filter* f = nullptr) {
     cudaStream_t s = ctx->stream;
     n = n_;
@@ -781,6 +856,14 @@ struct Work {
       GS_CUDA(ctx, cudaMemcpyAsync(gactive.get(), ga.data(), G * sizeof(int), cudaMemcpyHostToDevice, s));
       GS_CUDA(ctx, cudaStreamSynchronize(s));
     }
+    if constexpr (kF32) {
+      GS_CUDA(ctx, T0d.alloc(len, s));
+      GS_CUDA(ctx, cudaMemsetAsync(T0d.get(), 0, len * sizeof(double), s));
+      GS_CUDA(ctx, scale.alloc(Bpad, s));
+      std::vector<double> one(Bpad, 1.0);
+      GS_CUDA(ctx, cudaMemcpyAsync(scale.get(), one.data(), Bpad * sizeof(double), cudaMemcpyHostToDevice, s));
+      GS_CUDA(ctx, cudaStreamSynchronize(s));
+    }
     GS_CUDA(ctx, status.alloc(1, s));
     GS_CUDA(ctx, cudaMemsetAsync(status.get(), 0, sizeof(gs_status), s));
     GS_CUDA(ctx, cudaMemsetAsync(thr.get(), 0, Bpad * sizeof(double), s));
@@ -804,7 +887,26 @@ struct Work {
     c.part_err = part_err.get();
     return c;
   }
+  // where the fp64 producers (k_sk_init, k_bary_w) write the next T_0: T[buf] itself in fp64,
+  // T0d in the fp32 mode (k_rescale32 then fills T[buf])
+  double* t0_target(int buf) {
+    if constexpr (kF32) return T0d.get();
+    else return T[buf].get();
+  }
+  double* scale_ptr() { return kF32 ? scale.get() : nullptr; }
 };
+
+// fp32 mode: T[buf] = T0d / scale per column (after the finalize that set the scale)
+template <typename S>
+void rescale_t0(gs_ctx* ctx, Work<S>& w, int buf) {
+  if constexpr (sizeof(S) == 4) {
+    if (w.n == 0) return;
+    gs_launch_begin(ctx, 1);
+    k_rescale32<<<grid_for((int64_t)w.G * w.n * w.GW), kThreads, 0, ctx->stream>>>(
+        w.T0d.get(), w.scale.get(), w.T[buf].get(), w.n, w.GW, w.G, w.ld);
+    gs_launch_end(ctx, 1);
+  }
+}
 
 // Deferred-accumulation schedule (StepArgs::acc_terms): step k holds the own rows T_{k-2},
 // T_{k-1}, T_k, so acc may lag by up to two steps; it is brought up to date whenever waiting one
@@ -836,8 +938,8 @@ const void* layout_vals(const gs_layout& L) {
 // One full filter application on the workspace: T0 in T[a0]; K steps; the last step uses `mode`
 // with the given epilogue operands. Returns the buffer index holding the next T_0.
 template <typename S>
-int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, const S* a, const S* M,
-              const S* Vcur, S* Wout, bool use_active, bool use_status) {
+int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, const double* a,
+              const double* M, const double* Vcur, double* Wout, bool use_active, bool use_status) {
   const gs_layout& Ly = f->lay[w.lay];
   const gs_graph* G = Ly.perm;
   const int K = f->degree;
@@ -868,6 +970,8 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
   A.M = M;
   A.Vcur = Vcur;
   A.Wout = Wout;
+  A.colscale = w.scale_ptr();
+  A.T0d = w.kF32 ? w.T0d.get() : nullptr;
   const bool seq = seq_groups() && w.G > 1;
   for (int g = 0; g < (seq ? w.G : 1); ++g) {
     if (seq) {
@@ -887,9 +991,11 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
   return (a0 + K) & 1;
 }
 
+// per-column finalize after an apply; with has_next, next_buf >= 0 names the buffer the next
+// T_0 goes to (fp32 mode: scaled from T0d once the new column scale is known)
 template <typename S>
 void run_finalize(gs_ctx* ctx, Work<S>& w, int check, int has_next, int has_err, int knp_code,
-                  bool use_active) {
+                  bool use_active, int next_buf = -1) {
   FinArgs F{};
   F.cs = w.cs();
   if (!use_active) F.cs.active = nullptr;
@@ -902,9 +1008,11 @@ void run_finalize(gs_ctx* ctx, Work<S>& w, int check, int has_next, int has_err,
   F.status = w.status.get();
   F.knp_code = knp_code;
   F.slack = Prec<S>::slack;
+  F.scale = has_next ? w.scale_ptr() : nullptr;
   gs_launch_begin(ctx, 1);
   k_finalize<<<w.B, kThreads, 0, ctx->stream>>>(F);
   gs_launch_end(ctx, 1);
+  if (has_next && next_buf >= 0) rescale_t0<S>(ctx, w, next_buf);
 }
 
 // Input staging: returns a device pointer to `count` doubles (the caller's when mem = DEVICE).
@@ -975,8 +1083,28 @@ int check_weights(gs_ctx* ctx, const double* da, int n) {
 
 const char* kKnpTransport =
     "heat approximation produced negative mass; increase the degree or diffusion time";
+// fp32 mode: a non-finite marginal error or cost (the scaling vectors left the range of the
+// scaled fp32 recurrence) is reported, never returned as a value
+const std::string kF32Range_msg =
+    "fp32 mode: non-finite marginal error or cost (the scaled fp32 recurrence's range was left); "
+    "rerun in fp64. Pair ";
 const char* kKnpBary =
     "heat filter produced negative mass; increase the Chebyshev degree or diffusion time";
+
+// fp32 mode: per-column power-of-two scale of a column-major fp64 block (its max |x| in [1, 2)
+// after division); `keys` receives the order-preserving max keys (rank-local when partitioned)
+int column_keys(gs_ctx* ctx, const double* dX, int64_t n, int width, unsigned long long* keys) {
+  cudaStream_t s = ctx->stream;
+  gs_launch_begin(ctx, 1);
+  k_fill_key<<<grid_for(width), kThreads, 0, s>>>(keys, width, KEY_ZERO);
+  gs_launch_end(ctx, 1);
+  if (n > 0) {
+    gs_launch_begin(ctx, 1);
+    k_colmax_cm<<<dim3((unsigned)std::min<int64_t>((n + kThreads - 1) / kThreads, 148 * 4), width), kThreads, 0, s>>>(dX, n, keys);
+    gs_launch_end(ctx, 1);
+  }
+  return GS_OK;
+}
 
 // ---- filter apply (heat.cpp:116-131) -----------------------------------------------------------
 template <typename S>
@@ -985,14 +1113,31 @@ int filter_apply_impl(gs_ctx* ctx, const gs_filter* f, const double* dX, double*
   cudaStream_t s = ctx->stream;
   Work<S> w;
   GS_TRY(w.init(ctx, n, width, false, -1, f));
+  const double* sc = w.scale_ptr();
+  if (sc) {
+    GS_TRY(column_keys(ctx, dX, n, width, w.cmax.get()));
+    gs_launch_begin(ctx, 1);
+    k_scale_from_keys<<<grid_for(width), kThreads, 0, s>>>(w.cmax.get(), width, w.scale.get());
+    gs_launch_end(ctx, 1);
+  }
   gs_launch_begin(ctx, 1);
-  k_pack<S><<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
+  k_pack<S><<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, f->lay[w.lay].order, (int64_t)n, sc);
   gs_launch_end(ctx, 1);
   run_apply<S>(ctx, f, w, 0, MODE_NONE, nullptr, nullptr, nullptr, nullptr, false, false);
   gs_launch_begin(ctx, 1);
-  k_unpack<S><<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.acc.get(), dY, n, width, w.GW, nullptr, nullptr, f->lay[w.lay].newpos, (int64_t)n);
+  k_unpack<S><<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.acc.get(), dY, n, width, w.GW, nullptr, nullptr, f->lay[w.lay].newpos, (int64_t)n, sc);
   gs_launch_end(ctx, 1);
   GS_CUDA(ctx, cudaStreamSynchronize(s));
+  return GS_OK;
+}
+
+// fp32 mode: a non-finite cost is numerical_underflow (first such pair in pair order)
+int check_finite_costs(gs_ctx* ctx, const double* dcost, int P) {
+  std::vector<double> h(P);
+  GS_CUDA(ctx, cudaMemcpyAsync(h.data(), dcost, P * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  GS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  for (int q = 0; q < P; ++q)
+    if (!std::isfinite(h[q])) return gs_fail(ctx, ERRC_NUMERICAL_UNDERFLOW, kF32Range_msg + std::to_string(q));
   return GS_OK;
 }
 
@@ -1007,15 +1152,15 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   Work<S> w;
   GS_TRY(w.init(ctx, n, P, true, -1, f));
   L2Window l2w(ctx, w.Tall.get(), w.Tall.n * sizeof(S));
-  // vertex weights in the filter's locality order and the engine precision
-  DevBuf<S> aperm;
+  // vertex weights in the filter's locality order (the epilogue state is fp64 in both modes)
+  DevBuf<double> aperm;
   GS_CUDA(ctx, aperm.alloc(n, s));
   gs_launch_begin(ctx, 1);
-  k_gather_to<S><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(da_user, f->lay[w.lay].order, n, aperm.get());
+  k_gather_to<double><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(da_user, f->lay[w.lay].order, n, aperm.get());
   gs_launch_end(ctx, 1);
-  const S* da = aperm.get();
+  const double* da = aperm.get();
   const size_t len = (size_t)w.Bpad * n;
-  DevBuf<S> M, N, V[2], W;
+  DevBuf<double> M, N, V[2], W;
   GS_CUDA(ctx, M.alloc(len, s));
   GS_CUDA(ctx, N.alloc(len, s));
   GS_CUDA(ctx, V[0].alloc(len, s));
@@ -1032,8 +1177,8 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   GS_CUDA(ctx, cudaMemsetAsync(conv.get(), 0, w.Bpad * sizeof(int), s));
   GS_CUDA(ctx, cudaMemsetAsync(stag.get(), 0, w.Bpad * sizeof(int), s));
   GS_CUDA(ctx, cudaMemsetAsync(final_sweep.get(), 0, w.Bpad * sizeof(int), s));
-  GS_CUDA(ctx, cudaMemsetAsync(V[0].get(), 0, len * sizeof(S), s));
-  GS_CUDA(ctx, cudaMemsetAsync(W.get(), 0, len * sizeof(S), s));
+  GS_CUDA(ctx, cudaMemsetAsync(V[0].get(), 0, len * sizeof(double), s));
+  GS_CUDA(ctx, cudaMemsetAsync(W.get(), 0, len * sizeof(double), s));
   {
     std::vector<int> act(w.Bpad, 0);
     for (int p = 0; p < P; ++p) act[p] = 1;
@@ -1043,19 +1188,19 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
     GS_CUDA(ctx, cudaStreamSynchronize(s));
   }
   gs_launch_begin(ctx, 1);
-  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dmu, M.get(), n, P, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
+  k_pack<double><<<grid_for((int64_t)len), kThreads, 0, s>>>(dmu, M.get(), n, P, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
-  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dnu, N.get(), n, P, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
+  k_pack<double><<<grid_for((int64_t)len), kThreads, 0, s>>>(dnu, N.get(), n, P, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
-  k_sk_init<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.T[0].get(), n, w.GW, w.G, P, w.cmax.get(), (int64_t)n);
+  k_sk_init<double><<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.t0_target(0), n, w.GW, w.G, P, w.cmax.get(), (int64_t)n);
   gs_launch_end(ctx, 1);
   const int knp = ERRC_KERNEL_NOT_POSITIVE + 1;
-  run_finalize<S>(ctx, w, 0, 1, 0, knp, true);  // threshold of the first apply
+  run_finalize<S>(ctx, w, 0, 1, 0, knp, true, 0);  // threshold (and fp32 scale) of the first apply
   // phi = H(a * 1) (transport.cpp:176); V_1 = M / max(phi, floor) in the epilogue
   int a0 = run_apply<S>(ctx, f, w, 0, MODE_SK_PHI, da, M.get(), V[0].get(), V[1].get(), true, true);
-  run_finalize<S>(ctx, w, 1, 1, 0, knp, true);
+  run_finalize<S>(ctx, w, 1, 1, 0, knp, true, a0);
   gs_status* hst = ctx->h_status;
   cudaEvent_t ev[2];
   cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
@@ -1074,6 +1219,7 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   C.P = P;
   C.max_iter = max_iter;
   C.no_abort = (flags & GS_FLAG_NO_STAGNATION_ABORT) ? 1 : 0;
+  C.fp32 = w.kF32 ? 1 : 0;
   C.tol = tol;
   DevBuf<int> sweep_ctr;
   GS_CUDA(ctx, sweep_ctr.alloc(1, s));
@@ -1083,11 +1229,11 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   auto issue_sweep = [&](int parity) {
     // psi = H(a * V_s); W_s = N / max(psi, floor); T_0 = a * W_s
     a0 = run_apply<S>(ctx, f, w, a0, MODE_SK_PSI, da, N.get(), nullptr, W.get(), true, true);
-    run_finalize<S>(ctx, w, 1, 1, 0, knp, true);
+    run_finalize<S>(ctx, w, 1, 1, 0, knp, true, a0);
     // phi = H(a * W_s); err; V_{s+1} = M / max(phi, floor); T_0 = a * V_{s+1}
     a0 = run_apply<S>(ctx, f, w, a0, MODE_SK_PHI, da, M.get(), V[parity].get(), V[parity ^ 1].get(),
                       true, true);
-    run_finalize<S>(ctx, w, 1, 1, 1, knp, true);
+    run_finalize<S>(ctx, w, 1, 1, 1, knp, true, a0);
     gs_launch_begin(ctx, 1);
     k_sk_control<<<1, 1, 0, s>>>(C);
     gs_launch_end(ctx, 1);
@@ -1155,6 +1301,11 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
       return gs_fail(ctx, ERRC_DISCONNECTED,
                      "marginal error stagnated above 0.5 for pair " + std::to_string(st.fail_pair));
     }
+    if (st.error == ERRC_NUMERICAL_UNDERFLOW + 1) {
+      if (fail_pair) *fail_pair = st.fail_pair;
+      if (fail_sweep) *fail_sweep = st.fail_sweep;
+      return gs_fail(ctx, ERRC_NUMERICAL_UNDERFLOW, kF32Range_msg + std::to_string(st.fail_pair));
+    }
     return gs_fail(ctx, ERRC_KERNEL_NOT_POSITIVE, kKnpTransport);
   }
   // ---- cost / KL + outputs ------------------------------------------------------------------------
@@ -1164,13 +1315,14 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   GS_CUDA(ctx, dcost.alloc(P, s));
   GS_CUDA(ctx, dkl.alloc(P, s));
   gs_launch_begin(ctx, 1);
-  k_sk_cost_partial<S><<<dim3((unsigned)nchunks, P), kThreads, 0, s>>>(
+  k_sk_cost_partial<double><<<dim3((unsigned)nchunks, P), kThreads, 0, s>>>(
       da, M.get(), N.get(), V[0].get(), V[1].get(), W.get(), final_sweep.get(), n, w.GW, part.get(), P,
       (int64_t)n);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
   k_sk_cost_final<<<(P + 63) / 64, 64, 0, s>>>(part.get(), nchunks, P, 4.0 * f->t, dcost.get(), dkl.get());
   gs_launch_end(ctx, 1);
+  if (w.kF32) GS_TRY(check_finite_costs(ctx, dcost.get(), P));
   DevBuf<double> ov, ow;
   double* dv = out_v;
   double* dw = out_w;
@@ -1182,13 +1334,13 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   }
   if (out_v) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)P * n), kThreads, 0, s>>>(V[0].get(), dv, n, P, w.GW, V[1].get(), final_sweep.get(), f->lay[w.lay].newpos, (int64_t)n);
+    k_unpack<double><<<grid_for((int64_t)P * n), kThreads, 0, s>>>(V[0].get(), dv, n, P, w.GW, V[1].get(), final_sweep.get(), f->lay[w.lay].newpos, (int64_t)n);
     gs_launch_end(ctx, 1);
     GS_TRY(finish_out(ctx, ov, out_v, (size_t)P * n, mem));
   }
   if (out_w) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)P * n), kThreads, 0, s>>>(W.get(), dw, n, P, w.GW, nullptr, nullptr, f->lay[w.lay].newpos, (int64_t)n);
+    k_unpack<double><<<grid_for((int64_t)P * n), kThreads, 0, s>>>(W.get(), dw, n, P, w.GW, nullptr, nullptr, f->lay[w.lay].newpos, (int64_t)n);
     gs_launch_end(ctx, 1);
     GS_TRY(finish_out(ctx, ow, out_w, (size_t)P * n, mem));
   }
@@ -1218,14 +1370,14 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   Work<S> w;
   GS_TRY(w.init(ctx, n, m, true, -1, f));
   L2Window l2w(ctx, w.Tall.get(), w.Tall.n * sizeof(S));
-  DevBuf<S> aperm;
+  DevBuf<double> aperm;
   GS_CUDA(ctx, aperm.alloc(n, s));
   gs_launch_begin(ctx, 1);
-  k_gather_to<S><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(da_user, f->lay[w.lay].order, n, aperm.get());
+  k_gather_to<double><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(da_user, f->lay[w.lay].order, n, aperm.get());
   gs_launch_end(ctx, 1);
-  const S* da = aperm.get();
+  const double* da = aperm.get();
   const size_t len = (size_t)w.Bpad * n;
-  DevBuf<S> Mb, V[2], W;
+  DevBuf<double> Mb, V[2], W;
   DevBuf<double> lb, bary, part, mass, dal, errbuf, derr;
   DevBuf<unsigned long long> lbmax;
   DevBuf<int> diters, dconv;
@@ -1245,7 +1397,7 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   GS_CUDA(ctx, diters.alloc(1, s));
   GS_CUDA(ctx, dconv.alloc(1, s));
   GS_CUDA(ctx, cudaMemcpyAsync(dal.get(), al.data(), m * sizeof(double), cudaMemcpyHostToDevice, s));
-  GS_CUDA(ctx, cudaMemsetAsync(V[0].get(), 0, len * sizeof(S), s));
+  GS_CUDA(ctx, cudaMemsetAsync(V[0].get(), 0, len * sizeof(double), s));
   GS_CUDA(ctx, cudaMemsetAsync(diters.get(), 0, sizeof(int), s));
   GS_CUDA(ctx, cudaMemsetAsync(dconv.get(), 0, sizeof(int), s));
   {
@@ -1257,16 +1409,16 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   k_fill<<<grid_for(n), kThreads, 0, s>>>(bary.get(), n, 1.0 / n);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
-  k_pack<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(dmem, Mb.get(), n, m, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
+  k_pack<double><<<grid_for((int64_t)len), kThreads, 0, s>>>(dmem, Mb.get(), n, m, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
-  k_sk_init<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.T[0].get(), n, w.GW, w.G, m, w.cmax.get(), (int64_t)n);
+  k_sk_init<double><<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.t0_target(0), n, w.GW, w.G, m, w.cmax.get(), (int64_t)n);
   gs_launch_end(ctx, 1);
-  run_finalize<S>(ctx, w, 0, 1, 0, 0, false);
+  run_finalize<S>(ctx, w, 0, 1, 0, 0, false, 0);
   const int knp = ERRC_KERNEL_NOT_POSITIVE + 1;
   // phi = H(a * 1) (barycenter.cpp:68); V_1 = M / max(phi, floor) in the epilogue
   int a0 = run_apply<S>(ctx, f, w, 0, MODE_SK_PHI, da, Mb.get(), V[0].get(), V[1].get(), false, true);
-  run_finalize<S>(ctx, w, 1, 1, 0, knp, false);
+  run_finalize<S>(ctx, w, 1, 1, 0, knp, false, a0);
   gs_status* hst = ctx->h_status;
   cudaEvent_t ev[2];
   cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
@@ -1284,7 +1436,9 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
     run_finalize<S>(ctx, w, 1, 0, 0, knp, false);
     // log-domain geometric mean (barycenter.cpp:75-82)
     gs_launch_begin(ctx, 1);
-    k_bary_lb<S><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(w.acc.get(), dal.get(), n, m, w.GW, lb.get(), w.status.get());
+    // psi (fp64): acc in the fp64 mode, T0d (unscaled by the epilogue) in the fp32 mode
+    const double* psi = w.kF32 ? w.T0d.get() : reinterpret_cast<const double*>(w.acc.get());
+    k_bary_lb<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(psi, dal.get(), n, m, w.GW, lb.get(), w.status.get(), w.scale_ptr());
     gs_launch_end(ctx, 1);
     if (hooked) {
       const int rc = comm->allreduce(comm->user, lb.get(), n, 0, (void*)s);
@@ -1305,15 +1459,15 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
     gs_launch_end(ctx, 1);
     // W = bary / max(psi, floor); T_0 = a * W (barycenter.cpp:84-85)
     gs_launch_begin(ctx, 1);
-    k_bary_w<S><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(
-        bary.get(), mass.get(), w.acc.get(), da, n, m, w.GW, W.get(), w.T[a0].get(), w.cmax.get(),
-        w.status.get());
+    k_bary_w<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(
+        bary.get(), mass.get(), psi, da, n, m, w.GW, W.get(), w.t0_target(a0), w.cmax.get(),
+        w.status.get(), w.scale_ptr());
     gs_launch_end(ctx, 1);
-    run_finalize<S>(ctx, w, 0, 1, 0, knp, false);
+    run_finalize<S>(ctx, w, 0, 1, 0, knp, false, a0);
     // phi = H(a * W); err; V' = M / max(phi, floor) (barycenter.cpp:85-86, 70)
     a0 = run_apply<S>(ctx, f, w, a0, MODE_SK_PHI, da, Mb.get(), V[parity].get(), V[parity ^ 1].get(),
                       false, true);
-    run_finalize<S>(ctx, w, 1, 1, 1, knp, false);
+    run_finalize<S>(ctx, w, 1, 1, 1, knp, false, a0);
     gs_launch_begin(ctx, 1);
     k_bary_errlocal<<<1, 1, 0, s>>>(w.errcol.get(), m, errbuf.get());
     gs_launch_end(ctx, 1);
@@ -1323,7 +1477,7 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
     }
     gs_launch_begin(ctx, 1);
     k_bary_control<<<1, 1, 0, s>>>(errbuf.get(), w.status.get(), sweep_ctr.get(), tol, diters.get(),
-                                   dconv.get(), derr.get(), max_iter);
+                                   dconv.get(), derr.get(), max_iter, w.kF32 ? 1 : 0);
     gs_launch_end(ctx, 1);
     return 0;
   };
@@ -1387,6 +1541,10 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   if (st.error) {
     if (st.error == 1000 + ERRC_KERNEL_NOT_POSITIVE + 1)
       return gs_fail(ctx, ERRC_KERNEL_NOT_POSITIVE, "barycenter iterate collapsed to zero");
+    if (st.error == ERRC_NUMERICAL_UNDERFLOW + 1)
+      return gs_fail(ctx, ERRC_NUMERICAL_UNDERFLOW,
+                     "fp32 mode: non-finite barycenter marginal error (the scaled fp32 recurrence's "
+                     "range was left); rerun in fp64");
     return gs_fail(ctx, ERRC_KERNEL_NOT_POSITIVE, kKnpBary);
   }
   int h_iters = 0;
@@ -1430,13 +1588,13 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   }
   if (out_V) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)m * n), kThreads, 0, s>>>(V[0].get(), dv, n, m, w.GW, V[1].get(), sel.get(), f->lay[w.lay].newpos, (int64_t)n);
+    k_unpack<double><<<grid_for((int64_t)m * n), kThreads, 0, s>>>(V[0].get(), dv, n, m, w.GW, V[1].get(), sel.get(), f->lay[w.lay].newpos, (int64_t)n);
     gs_launch_end(ctx, 1);
     GS_TRY(finish_out(ctx, ov, out_V, (size_t)m * n, mem));
   }
   if (out_W) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)m * n), kThreads, 0, s>>>(W.get(), dw, n, m, w.GW, nullptr, nullptr, f->lay[w.lay].newpos, (int64_t)n);
+    k_unpack<double><<<grid_for((int64_t)m * n), kThreads, 0, s>>>(W.get(), dw, n, m, w.GW, nullptr, nullptr, f->lay[w.lay].newpos, (int64_t)n);
     gs_launch_end(ctx, 1);
     GS_TRY(finish_out(ctx, ow, out_W, (size_t)m * n, mem));
   }
@@ -1512,6 +1670,7 @@ __global__ void k_fin_global(const FinArgs F, const double* stat) {
     if (!(mn >= -F.cs.thr[col])) atomicCAS(&F.status->error, 0, F.knp_code);
   }
   if (F.has_next) F.cs.thr[col] = F.slack * stat[F.Bpad + col];
+  if (F.has_next && F.scale) F.scale[col] = pow2_floor(stat[F.Bpad + col]);
   F.cs.cmin[col] = KEY_POS_INF;
   F.cs.cmax[col] = KEY_ZERO;
 }
@@ -1649,8 +1808,8 @@ int halo_finish(gs_ctx* ctx, const gs_part* p, const Work<S>& w, S* T, Halo<S>& 
 // run_apply over this part's rows, one halo exchange of T_{k-1} before every step
 template <typename S>
 int run_apply_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& w, Halo<S>& h, int a0,
-                   int mode, const S* a, const S* M, const S* Vcur, S* Wout, bool use_active,
-                   bool use_status, int* next) {
+                   int mode, const double* a, const double* M, const double* Vcur, double* Wout,
+                   bool use_active, bool use_status, int* next) {
   const gs_filter* f = p->f;
   const int K = f->degree;
   StepArgs A{};
@@ -1676,6 +1835,8 @@ int run_apply_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& 
   A.M = M;
   A.Vcur = Vcur;
   A.Wout = Wout;
+  A.colscale = w.scale_ptr();
+  A.T0d = w.kF32 ? w.T0d.get() : nullptr;
   const PartRanges R = part_ranges(p, rows_per_block<S>(w.GW) * w.rpc);
   auto launch_range = [&](int r, int m) {
     if (R.tiles[r] == 0) return;
@@ -1712,7 +1873,8 @@ int run_apply_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& 
 
 template <typename S>
 int run_finalize_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& w, double* stat,
-                      int check, int has_next, int has_err, int knp_code, bool use_active) {
+                      int check, int has_next, int has_err, int knp_code, bool use_active,
+                      int next_buf = -1) {
   FinArgs F{};
   F.cs = w.cs();
   if (!use_active) F.cs.active = nullptr;
@@ -1725,6 +1887,7 @@ int run_finalize_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S
   F.status = w.status.get();
   F.knp_code = knp_code;
   F.slack = Prec<S>::slack;
+  F.scale = has_next ? w.scale_ptr() : nullptr;  // from the combined column max: same on every rank
   gs_launch_begin(ctx, 1);
   k_fin_local<<<w.B, kThreads, 0, ctx->stream>>>(F, stat);
   gs_launch_end(ctx, 1);
@@ -1733,6 +1896,7 @@ int run_finalize_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S
   gs_launch_begin(ctx, 1);
   k_fin_global<<<(w.B + kThreads - 1) / kThreads, kThreads, 0, ctx->stream>>>(F, stat);
   gs_launch_end(ctx, 1);
+  if (has_next && next_buf >= 0) rescale_t0<S>(ctx, w, next_buf);
   return GS_OK;
 }
 
@@ -1746,16 +1910,32 @@ int filter_apply_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, c
   w.tiles = part_tiles<S>(p, w);
   Halo<S> h;
   GS_TRY(h.init(ctx, p, w.Bpad));
+  const double* sc = w.scale_ptr();
+  if (sc) {  // fp32: per-column scale from the max over every rank's rows
+    DevBuf<double> stat;
+    GS_CUDA(ctx, stat.alloc(width, s));
+    GS_TRY(column_keys(ctx, dX, nl, width, w.cmax.get()));
+    gs_launch_begin(ctx, 1);
+    k_keys_to_double<<<grid_for(width), kThreads, 0, s>>>(w.cmax.get(), width, stat.get());
+    gs_launch_end(ctx, 1);
+    GS_TRY(allreduce(ctx, p, comm, stat.get(), width, 1));
+    gs_launch_begin(ctx, 1);
+    k_scale_from_max<<<grid_for(width), kThreads, 0, s>>>(stat.get(), width, w.scale.get());
+    gs_launch_end(ctx, 1);
+    gs_launch_begin(ctx, 1);
+    k_fill_key<<<grid_for(w.Bpad), kThreads, 0, s>>>(w.cmax.get(), w.Bpad, KEY_ZERO);
+    gs_launch_end(ctx, 1);
+  }
   if (nl > 0) {
     gs_launch_begin(ctx, 1);
-    k_pack<S><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(dX, w.T[0].get(), nl, width, w.GW, w.G, nullptr, w.ld);
+    k_pack<S><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(dX, w.T[0].get(), nl, width, w.GW, w.G, nullptr, w.ld, sc);
     gs_launch_end(ctx, 1);
   }
   int next = 0;
   GS_TRY(run_apply_part<S>(ctx, p, comm, w, h, 0, MODE_NONE, nullptr, nullptr, nullptr, nullptr, false, false, &next));
   if (nl > 0) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)width * nl), kThreads, 0, s>>>(w.acc.get(), dY, nl, width, w.GW, nullptr, nullptr, nullptr, w.ld);
+    k_unpack<S><<<grid_for((int64_t)width * nl), kThreads, 0, s>>>(w.acc.get(), dY, nl, width, w.GW, nullptr, nullptr, nullptr, w.ld, sc);
     gs_launch_end(ctx, 1);
   }
   GS_CUDA(ctx, cudaStreamSynchronize(s));
@@ -1778,16 +1958,16 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
   GS_TRY(h.init(ctx, p, w.Bpad));
   DevBuf<double> stat;
   GS_CUDA(ctx, stat.alloc(2 * (size_t)w.Bpad, s));
-  DevBuf<S> aloc;
+  DevBuf<double> aloc;
   GS_CUDA(ctx, aloc.alloc(nl, s));
   if (nl > 0) {
     gs_launch_begin(ctx, 1);
-    k_gather_to<S><<<(nl + kThreads - 1) / kThreads, kThreads, 0, s>>>(da_user, nullptr, nl, aloc.get());
+    k_gather_to<double><<<(nl + kThreads - 1) / kThreads, kThreads, 0, s>>>(da_user, nullptr, nl, aloc.get());
     gs_launch_end(ctx, 1);
   }
-  const S* da = aloc.get();
+  const double* da = aloc.get();
   const size_t len = (size_t)w.Bpad * w.ld;
-  DevBuf<S> M, N, V[2], W;
+  DevBuf<double> M, N, V[2], W;
   GS_CUDA(ctx, M.alloc(len, s));
   GS_CUDA(ctx, N.alloc(len, s));
   GS_CUDA(ctx, V[0].alloc(len, s));
@@ -1804,8 +1984,8 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
   GS_CUDA(ctx, cudaMemsetAsync(conv.get(), 0, w.Bpad * sizeof(int), s));
   GS_CUDA(ctx, cudaMemsetAsync(stag.get(), 0, w.Bpad * sizeof(int), s));
   GS_CUDA(ctx, cudaMemsetAsync(final_sweep.get(), 0, w.Bpad * sizeof(int), s));
-  GS_CUDA(ctx, cudaMemsetAsync(V[0].get(), 0, len * sizeof(S), s));
-  GS_CUDA(ctx, cudaMemsetAsync(W.get(), 0, len * sizeof(S), s));
+  GS_CUDA(ctx, cudaMemsetAsync(V[0].get(), 0, len * sizeof(double), s));
+  GS_CUDA(ctx, cudaMemsetAsync(W.get(), 0, len * sizeof(double), s));
   {
     std::vector<int> act(w.Bpad, 0);
     for (int q = 0; q < P; ++q) act[q] = 1;
@@ -1816,20 +1996,20 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
   }
   if (nl > 0) {
     gs_launch_begin(ctx, 1);
-    k_pack<S><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(dmu, M.get(), nl, P, w.GW, w.G, nullptr, w.ld);
+    k_pack<double><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(dmu, M.get(), nl, P, w.GW, w.G, nullptr, w.ld);
     gs_launch_end(ctx, 1);
     gs_launch_begin(ctx, 1);
-    k_pack<S><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(dnu, N.get(), nl, P, w.GW, w.G, nullptr, w.ld);
+    k_pack<double><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(dnu, N.get(), nl, P, w.GW, w.G, nullptr, w.ld);
     gs_launch_end(ctx, 1);
     gs_launch_begin(ctx, 1);
-    k_sk_init<S><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(da, w.T[0].get(), nl, w.GW, w.G, P, w.cmax.get(), w.ld);
+    k_sk_init<double><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(da, w.t0_target(0), nl, w.GW, w.G, P, w.cmax.get(), w.ld);
     gs_launch_end(ctx, 1);
   }
   const int knp = ERRC_KERNEL_NOT_POSITIVE + 1;
   int a0 = 0;
-  GS_TRY(run_finalize_part<S>(ctx, p, comm, w, stat.get(), 0, 1, 0, knp, true));
+  GS_TRY(run_finalize_part<S>(ctx, p, comm, w, stat.get(), 0, 1, 0, knp, true, 0));
   GS_TRY(run_apply_part<S>(ctx, p, comm, w, h, 0, MODE_SK_PHI, da, M.get(), V[0].get(), V[1].get(), true, true, &a0));
-  GS_TRY(run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 0, knp, true));
+  GS_TRY(run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 0, knp, true, a0));
   CtlArgs C{};
   C.active = w.active.get();
   C.gactive = w.gactive.get();
@@ -1844,6 +2024,7 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
   C.P = P;
   C.max_iter = max_iter;
   C.no_abort = (flags & GS_FLAG_NO_STAGNATION_ABORT) ? 1 : 0;
+  C.fp32 = w.kF32 ? 1 : 0;
   C.tol = tol;
   DevBuf<int> sweep_ctr;
   GS_CUDA(ctx, sweep_ctr.alloc(1, s));
@@ -1862,11 +2043,11 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
       if (st.error || st.n_active == 0) break;
     }
     rc = run_apply_part<S>(ctx, p, comm, w, h, a0, MODE_SK_PSI, da, N.get(), nullptr, W.get(), true, true, &a0);
-    if (!rc) rc = run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 0, knp, true);
+    if (!rc) rc = run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 0, knp, true, a0);
     if (!rc)
       rc = run_apply_part<S>(ctx, p, comm, w, h, a0, MODE_SK_PHI, da, M.get(), V[sweep & 1].get(),
                              V[(sweep & 1) ^ 1].get(), true, true, &a0);
-    if (!rc) rc = run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 1, knp, true);
+    if (!rc) rc = run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 1, knp, true, a0);
     if (rc) break;
     gs_launch_begin(ctx, 1);
     k_sk_control<<<1, 1, 0, s>>>(C);
@@ -1891,6 +2072,11 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
       return gs_fail(ctx, ERRC_DISCONNECTED,
                      "marginal error stagnated above 0.5 for pair " + std::to_string(st.fail_pair));
     }
+    if (st.error == ERRC_NUMERICAL_UNDERFLOW + 1) {
+      if (fail_pair) *fail_pair = st.fail_pair;
+      if (fail_sweep) *fail_sweep = st.fail_sweep;
+      return gs_fail(ctx, ERRC_NUMERICAL_UNDERFLOW, kF32Range_msg + std::to_string(st.fail_pair));
+    }
     return gs_fail(ctx, ERRC_KERNEL_NOT_POSITIVE, kKnpTransport);
   }
   // ---- cost / KL: local DET-chunk partials, combined across ranks ---------------------------------
@@ -1902,7 +2088,7 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
   GS_CUDA(ctx, dkl.alloc(P, s));
   if (nchunks > 0) {
     gs_launch_begin(ctx, 1);
-    k_sk_cost_partial<S><<<dim3((unsigned)nchunks, P), kThreads, 0, s>>>(
+    k_sk_cost_partial<double><<<dim3((unsigned)nchunks, P), kThreads, 0, s>>>(
         da, M.get(), N.get(), V[0].get(), V[1].get(), W.get(), final_sweep.get(), nl, w.GW, part.get(), P, w.ld);
     gs_launch_end(ctx, 1);
   }
@@ -1913,6 +2099,7 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
   gs_launch_begin(ctx, 1);
   k_sk_cost_from_sums<<<(P + 63) / 64, 64, 0, s>>>(sums.get(), P, 4.0 * p->f->t, dcost.get(), dkl.get());
   gs_launch_end(ctx, 1);
+  if (w.kF32) GS_TRY(check_finite_costs(ctx, dcost.get(), P));
   DevBuf<double> ov, ow;
   double* dv = out_v;
   double* dw = out_w;
@@ -1924,13 +2111,13 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
   }
   if (out_v && nl > 0) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)P * nl), kThreads, 0, s>>>(V[0].get(), dv, nl, P, w.GW, V[1].get(), final_sweep.get(), nullptr, w.ld);
+    k_unpack<double><<<grid_for((int64_t)P * nl), kThreads, 0, s>>>(V[0].get(), dv, nl, P, w.GW, V[1].get(), final_sweep.get(), nullptr, w.ld);
     gs_launch_end(ctx, 1);
     GS_TRY(finish_out(ctx, ov, out_v, (size_t)P * nl, mem));
   }
   if (out_w && nl > 0) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)P * nl), kThreads, 0, s>>>(W.get(), dw, nl, P, w.GW, nullptr, nullptr, nullptr, w.ld);
+    k_unpack<double><<<grid_for((int64_t)P * nl), kThreads, 0, s>>>(W.get(), dw, nl, P, w.GW, nullptr, nullptr, nullptr, w.ld);
     gs_launch_end(ctx, 1);
     GS_TRY(finish_out(ctx, ow, out_w, (size_t)P * nl, mem));
   }

@@ -130,15 +130,14 @@ template <typename S>
 struct Prec;
 template <>
 struct Prec<double> {
-  static constexpr double floor = 1e-300;  // kDivisionFloor (transport.cpp:13, barycenter.cpp:9)
   static constexpr double slack = 1e-12;   // positivity slack (transport.cpp:24,33)
   __device__ static __forceinline__ double fmat(double a, double b, double c) { return fma(a, b, c); }
 };
 template <>
 struct Prec<float> {
-  // fp32 mode has no reference (SURVEY §7 hard part 7): 1e-300 underflows and 1e-12 is below
-  // fp32 epsilon, so the floor is FLT_MIN and the slack 64 FLT_EPSILON.
-  static constexpr float floor = FLT_MIN;
+  // fp32 mode has no reference (SURVEY §7 hard part 7): the recurrence's rounding is ~1e-7 of
+  // the column maximum, above the reference's 1e-12 positivity slack, so the slack is
+  // 64 FLT_EPSILON; the division floor is relative to the column's scale (kF32Range below).
   static constexpr double slack = 64.0 * (double)FLT_EPSILON;
   __device__ static __forceinline__ float fmat(float a, float b, float c) { return fmaf(a, b, c); }
 };
@@ -333,11 +332,25 @@ struct StepArgs {  // vector pointers are S* of the launch's precision
   ColState cs;
   const int* rec_key;  // k_cheb_blk: 8-row block records (gs_layout::rec_key / rec_val)
   const void* rec_val;
-  const void* a;      // n (epilogue)
-  const void* M;      // PSI: N (targets); PHI: M (sources / members)
-  const void* Vcur;   // PHI: V of this sweep
-  void* Wout;         // PSI: W; PHI: V of the next sweep
+  // fused epilogue operands: always fp64 (in the fp32 mode only the Chebyshev recurrence runs
+  // in fp32; the scaling vectors keep the reference's fp64 range, DESIGN.md §4 "Precision")
+  const double* a;      // n (epilogue)
+  const double* M;      // PSI: N (targets); PHI: M (sources / members)
+  const double* Vcur;   // PHI: V of this sweep
+  double* Wout;         // PSI: W; PHI: V of the next sweep
+  // fp32 mode: colscale[c] = 2^e_c, the power of two the apply's input column was divided by
+  // (k_rescale32); the epilogue multiplies acc back and floors divisions at 2^(e_c - 100)
+  // (kF32Range). The next T_0 (PSI/PHI) or psi (BARY_PSI) is written unscaled to T0d.
+  const double* colscale;
+  double* T0d;
 };
+
+// Range of the scaled fp32 recurrence: inputs are divided by a per-column power of two so the
+// column maximum lies in [1, 2); outputs below 2^-kF32Range of it are not resolved (fp32's normal
+// range ends at 2^-126), so the fp32 mode's division floor is max(1e-300, 2^(e_c - kF32Range)).
+constexpr int kF32Range = 100;
+constexpr double kF32Floor = 0x1p-100;  // 2^-kF32Range
+static_assert(kF32Floor == 1.0 / (double)(1ull << 50) / (double)(1ull << 50), "2^-kF32Range");
 
 template <typename S, int GW, int MODE>
 __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, int q,
@@ -579,34 +592,48 @@ __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, in
     if (A.store_t) st_vec<S, VEC>(static_cast<S*>(A.Tout) + idx, t);
     if (A.acc_terms > 0) st_vec<S, VEC>(static_cast<S*>(A.acc) + idx, ac);
   } else {
-    // ---- fused epilogue of the last step --------------------------------------------------
+    // ---- fused epilogue of the last step (fp64; transport.cpp:171-184, barycenter.cpp:71) ----
     const int* act = A.cs.active;
     const int col0 = g * GW + q * VEC;
+    constexpr bool F32 = sizeof(S) == 4;
+    double ps[VEC], fl[VEC];  // psi = p_K(L_s) x, unscaled; division floor
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) mn[e] = fmin(mn[e], (double)ac[e]);
+    for (int e = 0; e < VEC; ++e) {
+      if constexpr (F32) {
+        const double sc = A.colscale[col0 + e];
+        ps[e] = (double)ac[e] * sc;
+        fl[e] = fmax(GS_FLOOR, sc * kF32Floor);
+      } else {
+        ps[e] = ac[e];
+        fl[e] = GS_FLOOR;  // kDivisionFloor (transport.cpp:13, barycenter.cpp:9)
+      }
+      mn[e] = fmin(mn[e], ps[e]);
+    }
     if constexpr (MODE == MODE_SK_PSI || MODE == MODE_SK_PHI) {
-      S op1[VEC], nx[VEC], t0[VEC];
-      ld_vec<S, VEC>(static_cast<const S*>(A.M) + idx, op1);
-      const S ai = __ldg(static_cast<const S*>(A.a) + row);
+      double op1[VEC], nx[VEC], t0[VEC];
+      ld_vec<double, VEC>(A.M + idx, op1);
+      const double ai = __ldg(A.a + row);
       if constexpr (MODE == MODE_SK_PHI) {
-        S v[VEC];
-        ld_vec_rw<S, VEC>(static_cast<const S*>(A.Vcur) + idx, v);
+        double v[VEC];
+        ld_vec_rw<double, VEC>(A.Vcur + idx, v);
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) er[e] = er[e] + (double)fabs(v[e] * ac[e] - op1[e]);  // transport.cpp:184
+        for (int e = 0; e < VEC; ++e) er[e] = er[e] + fabs(v[e] * ps[e] - op1[e]);  // transport.cpp:184
       }
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
-        nx[e] = op1[e] / fmax(ac[e], P::floor);  // W (transport.cpp:180) / V' (:178)
-        t0[e] = ai * nx[e];                      // a .* x (transport.cpp:172)
-        mx[e] = fmax(mx[e], (double)fabs(t0[e]));
+        nx[e] = op1[e] / fmax(ps[e], fl[e]);  // W (transport.cpp:180) / V' (:178)
+        t0[e] = ai * nx[e];                   // a .* x (transport.cpp:172)
+        mx[e] = fmax(mx[e], fabs(t0[e]));
       }
-      st_vec<S, VEC>(static_cast<S*>(A.Tout) + idx, t0);
-      S* wo = static_cast<S*>(A.Wout) + idx;
+      if constexpr (F32) st_vec<double, VEC>(A.T0d + idx, t0);  // scaled by k_rescale32
+      else st_vec<S, VEC>(static_cast<S*>(A.Tout) + idx, t0);
+      double* wo = A.Wout + idx;
 #pragma unroll
       for (int e = 0; e < VEC; ++e)
         if (!act || act[col0 + e]) wo[e] = nx[e];
     } else {  // MODE_BARY_PSI
-      st_vec<S, VEC>(static_cast<S*>(A.acc) + idx, ac);
+      if constexpr (F32) st_vec<double, VEC>(A.T0d + idx, ps);
+      else st_vec<S, VEC>(static_cast<S*>(A.acc) + idx, ac);
     }
   }
 }

@@ -88,6 +88,35 @@ def bump_mixture_pairs(roll: SwissRoll, pairs: int, seed: int, bumps: int = 3,
     return out[0::2].copy(), out[1::2].copy()
 
 
+def bump_mixture_companions(roll: SwissRoll, pairs: int, seed: int, bumps: int = 3,
+                            wmin: float = 0.3, wmax: float = 1.0, shift: float = 0.5):
+    """Well-posed companion of config 1 (SURVEY §7 hard part 1): each source is a config-1-style
+    mixture (`bumps` equal-weight Gaussian bumps in (s, h), widths ~ U(wmin, wmax), centres kept
+    one width-unit inside the roll's s/h range so no bump is cut by the boundary); its target
+    moves every bump centre by a geodesic offset drawn uniformly in [-shift, shift]^2 (an s
+    offset of d / sqrt(1 + s^2): the roll's arc-length element) and keeps the width, so each target bump carries its source bump's mass and lies within the K-hop reach
+    of it: the reference converges instead of raising Disconnected. Returns (mus, nus)."""
+    rng = Rng(seed)
+    n = roll.s.size
+    mus = np.empty((pairs, n))
+    nus = np.empty((pairs, n))
+    for q in range(pairs):
+        src = np.zeros(n)
+        dst = np.zeros(n)
+        for _ in range(bumps):
+            sc = rng.uniform(1.5 * math.pi + 2.0, 4.5 * math.pi - 2.0)
+            hc = rng.uniform(3.0, 17.0)
+            w = rng.uniform(wmin, wmax)
+            ds = rng.uniform(-shift, shift)
+            dh = rng.uniform(-shift, shift)
+            ds = ds / math.sqrt(1.0 + sc * sc)
+            src += np.exp(-((roll.s - sc) ** 2 + (roll.h - hc) ** 2) / (2.0 * w * w))
+            dst += np.exp(-((roll.s - sc - ds) ** 2 + (roll.h - hc - dh) ** 2) / (2.0 * w * w))
+        mus[q] = _normalise(src)
+        nus[q] = _normalise(dst)
+    return mus, nus
+
+
 @dataclass
 class Mixture:
     points: np.ndarray  # n x d
