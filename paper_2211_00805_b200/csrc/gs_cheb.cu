@@ -30,16 +30,7 @@ struct FinArgs {
   gs_status* status;
   int knp_code;
   double slack;
-  double* scale;  // fp32 mode: per-column power of two of the next input (nullptr in fp64)
 };
-
-// largest power of two <= m (1 for m <= 0 or non-finite): the fp32 mode's per-column input scale
-__device__ __forceinline__ double pow2_floor(double m) {
-  if (!(m > 0.0) || !isfinite(m)) return 1.0;
-  int e = 0;
-  frexp(m, &e);  // m = f 2^e, f in [0.5, 1)
-  return ldexp(1.0, e - 1);
-}
 
 __global__ void __launch_bounds__(kThreads) k_finalize(const FinArgs F) {
   const int col = blockIdx.x;
@@ -62,7 +53,6 @@ __global__ void __launch_bounds__(kThreads) k_finalize(const FinArgs F) {
     if (!(mn >= -F.cs.thr[col])) atomicCAS(&F.status->error, 0, F.knp_code);
   }
   if (F.has_next) F.cs.thr[col] = F.slack * dunkey(F.cs.cmax[col]);
-  if (F.has_next && F.scale) F.scale[col] = pow2_floor(dunkey(F.cs.cmax[col]));
   if (F.has_err) F.cs.errcol[col] = sh[0];
   F.cs.cmin[col] = KEY_POS_INF;
   F.cs.cmax[col] = KEY_ZERO;
@@ -132,8 +122,7 @@ __global__ void k_sk_control(const CtlArgs C) {
 // ---- layout conversion: column-major fp64 (API) <-> grouped row-major S (engine) ------------
 template <typename S>
 __global__ void k_pack(const double* __restrict__ src, S* __restrict__ dst, int n, int width,
-                       int GW, int G, const int* __restrict__ order, int64_t ld,
-                       const double* __restrict__ scale = nullptr) {
+                       int GW, int G, const int* __restrict__ order, int64_t ld) {
   const int64_t total = (int64_t)G * n * GW;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -143,17 +132,14 @@ __global__ void k_pack(const double* __restrict__ src, S* __restrict__ dst, int 
     const int g = (int)(r / n);
     const int col = g * GW + c;
     const int o = order ? order[i] : i;
-    double v = col < width ? src[(size_t)col * n + o] : 0.0;
-    if (scale && col < width) v = ldexp(v, -ilogb(scale[col]));  // exact: scale is 2^e
-    dst[((size_t)g * ld + i) * GW + c] = S(v);
+    dst[((size_t)g * ld + i) * GW + c] = Prec<S>::enc(col < width ? src[(size_t)col * n + o] : 0.0);
   }
 }
 
 template <typename S>
 __global__ void k_unpack(const S* __restrict__ src, double* __restrict__ dst, int n, int width,
                          int GW, const S* __restrict__ alt, const int* __restrict__ sel,
-                         const int* __restrict__ newpos, int64_t ld,
-                         const double* __restrict__ scale = nullptr) {
+                         const int* __restrict__ newpos, int64_t ld) {
   const int64_t total = (int64_t)width * n;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -163,7 +149,7 @@ __global__ void k_unpack(const S* __restrict__ src, double* __restrict__ dst, in
     const int g = col / GW, c = col % GW;
     const size_t idx = ((size_t)g * ld + i) * GW + c;
     const S* s = (alt && sel && (sel[col] & 1)) ? alt : src;
-    dst[e] = scale ? (double)s[idx] * scale[col] : (double)s[idx];
+    dst[e] = Prec<S>::dec(s[idx]);
   }
 }
 
@@ -183,7 +169,7 @@ __global__ void k_gather(const double* __restrict__ src, const int* __restrict__
 
 // T_0 = a * 1 for the initial phi apply (transport.cpp:171-176 with W = 1), colmax |T_0|
 template <typename S>
-__global__ void k_sk_init(const S* __restrict__ a, S* __restrict__ T0, int n, int GW, int G, int B,
+__global__ void k_sk_init(const double* __restrict__ a, S* __restrict__ T0, int n, int GW, int G, int B,
                           unsigned long long* cmax, int64_t ld) {
   const int64_t total = (int64_t)G * n * GW;
   double local = 0.0;
@@ -193,8 +179,8 @@ __global__ void k_sk_init(const S* __restrict__ a, S* __restrict__ T0, int n, in
     const int i = (int)((e / GW) % n);
     const int g = (int)((e / GW) / n);
     const int col = g * GW + c;
-    const S v = col < B ? a[i] * S(1) : S(0);
-    T0[((size_t)g * ld + i) * GW + c] = v;
+    const double v = col < B ? a[i] * 1.0 : 0.0;
+    T0[((size_t)g * ld + i) * GW + c] = Prec<S>::enc(v);
     if (col < B) local = fmax(local, (double)fabs(v));
   }
   __shared__ double sh[kThreads];
@@ -206,48 +192,6 @@ __global__ void k_sk_init(const S* __restrict__ a, S* __restrict__ T0, int n, in
   }
   if (threadIdx.x == 0)
     for (int c = 0; c < B; ++c) atomicMax(cmax + c, dkey(sh[0]));
-}
-
-// fp32 mode: the next T_0 (fp64, unscaled, written by the epilogue / k_sk_init / k_bary_w) divided
-// by its column's power of two (exact) and rounded to fp32 -- the input of the next apply
-__global__ void k_rescale32(const double* __restrict__ T0d, const double* __restrict__ scale,
-                            float* __restrict__ T, int n, int GW, int G, int64_t ld) {
-  const int64_t total = (int64_t)G * n * GW;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(e % GW);
-    const int64_t r = e / GW;
-    const int i = (int)(r % n);
-    const int g = (int)(r / n);
-    const size_t idx = ((size_t)g * ld + i) * GW + c;
-    T[idx] = (float)ldexp(T0d[idx], -ilogb(scale[g * GW + c]));
-  }
-}
-
-// per-column max |x| of a column-major fp64 block (order-free: atomics on keys)
-__global__ void k_colmax_cm(const double* __restrict__ X, int64_t n, unsigned long long* keys) {
-  const int col = blockIdx.y;
-  double m = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    m = fmax(m, fabs(X[(size_t)col * n + i]));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(keys + col, dkey(m));
-}
-
-__global__ void k_scale_from_keys(const unsigned long long* keys, int B, double* scale) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < B) scale[c] = pow2_floor(dunkey(keys[c]));
-}
-
-__global__ void k_keys_to_double(const unsigned long long* keys, int B, double* out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < B) out[c] = dunkey(keys[c]);
-}
-
-__global__ void k_scale_from_max(const double* mx, int B, double* scale) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < B) scale[c] = pow2_floor(mx[c]);
 }
 
 // ---- validation (transport.cpp:56-66, 96-102; barycenter.cpp:32-43) ----------------------------
@@ -342,21 +286,15 @@ __global__ void k_sk_cost_final(const double* part, int64_t nchunks, int P, doub
 }
 
 // ---- barycenter row kernels (barycenter.cpp:75-84), computed in double ----------------------
-// division / log floor of column c: kFloor = 1e-300 (fp64), or the fp32 mode's range floor
-__device__ __forceinline__ double col_floor(const double* scale, int c) {
-  return scale ? fmax(GS_FLOOR, scale[c] * kF32Floor) : GS_FLOOR;
-}
-
 __global__ void k_bary_lb(const double* __restrict__ psi, const double* __restrict__ alphas, int n, int m,
-                          int GW, double* __restrict__ lb, const gs_status* st,
-                          const double* __restrict__ scale) {
+                          int GW, double* __restrict__ lb, const gs_status* st) {
   if (st->error || st->done) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double acc = 0.0;
   for (int c = 0; c < m; ++c) {
     const double v = psi[((size_t)(c / GW) * n + i) * GW + (c % GW)];
-    const double ps = fmin(fmax(v, col_floor(scale, c)), GS_CEIL);
+    const double ps = fmin(fmax(v, GS_FLOOR), GS_CEIL);
     acc = fma(alphas[c], log(ps), acc);
   }
   lb[i] = acc;
@@ -440,10 +378,11 @@ constexpr int kBaryColChunk = 2048;  // columns per shared-memory max pass of k_
 
 // bary /= mass; W_c = bary / max(psi_c, floor); T_0 = a * W_c; colmax |T_0| (order-free max:
 // warp shuffle, one shared-memory atomic per warp, one global atomic per CTA and column)
+template <typename S>
 __global__ void k_bary_w(double* __restrict__ bary, const double* __restrict__ mass,
-                         const double* psi, const double* __restrict__ a, int n, int m, int GW,
-                         double* __restrict__ W, double* T0, unsigned long long* cmax,
-                         const gs_status* st, const double* __restrict__ scale) {
+                         const double* __restrict__ psi, const double* __restrict__ a, int n, int m,
+                         int GW, double* __restrict__ W, S* __restrict__ T0, unsigned long long* cmax,
+                         const gs_status* st) {
   __shared__ unsigned long long s_max[kBaryColChunk];
   if (st->error || st->done) return;  // the same status word for the whole grid
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -463,10 +402,10 @@ __global__ void k_bary_w(double* __restrict__ bary, const double* __restrict__ m
       double v = 0.0;
       if (ok) {
         const size_t idx = ((size_t)(c / GW) * n + i) * GW + (c % GW);
-        const double w = b / fmax(psi[idx], col_floor(scale, c));
+        const double w = b / fmax(psi[idx], GS_FLOOR);
         W[idx] = w;
         const double t0 = ai * w;
-        T0[idx] = t0;  // fp32 mode: psi and T0 share T0d (this thread reads idx before writing it)
+        T0[idx] = Prec<S>::enc(t0);
         v = fabs(t0);
       }
 #pragma unroll
@@ -817,8 +756,8 @@ struct Work {
   DevBuf<double> thr, errcol, part_err;
   DevBuf<int> active, gactive;
   DevBuf<gs_status> status;
-  // fp32 mode: the next T_0 / psi in fp64 before scaling, and the per-column input scale 2^e_c
-  DevBuf<double> T0d, scale;
+  // 32-bit mode: the barycenter's psi in fp64 (the fp64 mode keeps it in acc)
+  DevBuf<double> psi64;
   static constexpr bool kF32 = sizeof(S) == 4;
   int init(gs_ctx* ctx, int n_, int B_, bool want_err, int64_t ld_ = -1, const gs_filter* f = nullptr) {
     cudaStream_t s = ctx->stream;
@@ -856,14 +795,7 @@ struct Work {
       GS_CUDA(ctx, cudaMemcpyAsync(gactive.get(), ga.data(), G * sizeof(int), cudaMemcpyHostToDevice, s));
       GS_CUDA(ctx, cudaStreamSynchronize(s));
     }
-    if constexpr (kF32) {
-      GS_CUDA(ctx, T0d.alloc(len, s));
-      GS_CUDA(ctx, cudaMemsetAsync(T0d.get(), 0, len * sizeof(double), s));
-      GS_CUDA(ctx, scale.alloc(Bpad, s));
-      std::vector<double> one(Bpad, 1.0);
-      GS_CUDA(ctx, cudaMemcpyAsync(scale.get(), one.data(), Bpad * sizeof(double), cudaMemcpyHostToDevice, s));
-      GS_CUDA(ctx, cudaStreamSynchronize(s));
-    }
+    if constexpr (kF32) GS_CUDA(ctx, psi64.alloc(len, s));
     GS_CUDA(ctx, status.alloc(1, s));
     GS_CUDA(ctx, cudaMemsetAsync(status.get(), 0, sizeof(gs_status), s));
     GS_CUDA(ctx, cudaMemsetAsync(thr.get(), 0, Bpad * sizeof(double), s));
@@ -887,26 +819,7 @@ struct Work {
     c.part_err = part_err.get();
     return c;
   }
-  // where the fp64 producers (k_sk_init, k_bary_w) write the next T_0: T[buf] itself in fp64,
-  // T0d in the fp32 mode (k_rescale32 then fills T[buf])
-  double* t0_target(int buf) {
-    if constexpr (kF32) return T0d.get();
-    else return T[buf].get();
-  }
-  double* scale_ptr() { return kF32 ? scale.get() : nullptr; }
 };
-
-// fp32 mode: T[buf] = T0d / scale per column (after the finalize that set the scale)
-template <typename S>
-void rescale_t0(gs_ctx* ctx, Work<S>& w, int buf) {
-  if constexpr (sizeof(S) == 4) {
-    if (w.n == 0) return;
-    gs_launch_begin(ctx, 1);
-    k_rescale32<<<grid_for((int64_t)w.G * w.n * w.GW), kThreads, 0, ctx->stream>>>(
-        w.T0d.get(), w.scale.get(), w.T[buf].get(), w.n, w.GW, w.G, w.ld);
-    gs_launch_end(ctx, 1);
-  }
-}
 
 // Deferred-accumulation schedule (StepArgs::acc_terms): step k holds the own rows T_{k-2},
 // T_{k-1}, T_k, so acc may lag by up to two steps; it is brought up to date whenever waiting one
@@ -970,8 +883,7 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
   A.M = M;
   A.Vcur = Vcur;
   A.Wout = Wout;
-  A.colscale = w.scale_ptr();
-  A.T0d = w.kF32 ? w.T0d.get() : nullptr;
+  A.psi = w.psi64.get();
   const bool seq = seq_groups() && w.G > 1;
   for (int g = 0; g < (seq ? w.G : 1); ++g) {
     if (seq) {
@@ -991,11 +903,9 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
   return (a0 + K) & 1;
 }
 
-// per-column finalize after an apply; with has_next, next_buf >= 0 names the buffer the next
-// T_0 goes to (fp32 mode: scaled from T0d once the new column scale is known)
 template <typename S>
 void run_finalize(gs_ctx* ctx, Work<S>& w, int check, int has_next, int has_err, int knp_code,
-                  bool use_active, int next_buf = -1) {
+                  bool use_active) {
   FinArgs F{};
   F.cs = w.cs();
   if (!use_active) F.cs.active = nullptr;
@@ -1008,11 +918,9 @@ void run_finalize(gs_ctx* ctx, Work<S>& w, int check, int has_next, int has_err,
   F.status = w.status.get();
   F.knp_code = knp_code;
   F.slack = Prec<S>::slack;
-  F.scale = has_next ? w.scale_ptr() : nullptr;
   gs_launch_begin(ctx, 1);
   k_finalize<<<w.B, kThreads, 0, ctx->stream>>>(F);
   gs_launch_end(ctx, 1);
-  if (has_next && next_buf >= 0) rescale_t0<S>(ctx, w, next_buf);
 }
 
 // Input staging: returns a device pointer to `count` doubles (the caller's when mem = DEVICE).
@@ -1083,28 +991,12 @@ int check_weights(gs_ctx* ctx, const double* da, int n) {
 
 const char* kKnpTransport =
     "heat approximation produced negative mass; increase the degree or diffusion time";
-// fp32 mode: a non-finite marginal error or cost (the scaling vectors left the range of the
-// scaled fp32 recurrence) is reported, never returned as a value
-const std::string kF32Range_msg =
-    "fp32 mode: non-finite marginal error or cost (the scaled fp32 recurrence's range was left); "
-    "rerun in fp64. Pair ";
+// 32-bit mode: a non-finite marginal error or cost is reported, never returned as a value (the
+// fp64 reference returns -inf costs for pairs whose v underflows; the 32-bit mode raises
+// numerical_underflow for them, transport.cpp:284-289's errc)
+const std::string kF32Range_msg = "fp32 mode: non-finite marginal error or cost; rerun in fp64. Pair ";
 const char* kKnpBary =
     "heat filter produced negative mass; increase the Chebyshev degree or diffusion time";
-
-// fp32 mode: per-column power-of-two scale of a column-major fp64 block (its max |x| in [1, 2)
-// after division); `keys` receives the order-preserving max keys (rank-local when partitioned)
-int column_keys(gs_ctx* ctx, const double* dX, int64_t n, int width, unsigned long long* keys) {
-  cudaStream_t s = ctx->stream;
-  gs_launch_begin(ctx, 1);
-  k_fill_key<<<grid_for(width), kThreads, 0, s>>>(keys, width, KEY_ZERO);
-  gs_launch_end(ctx, 1);
-  if (n > 0) {
-    gs_launch_begin(ctx, 1);
-    k_colmax_cm<<<dim3((unsigned)std::min<int64_t>((n + kThreads - 1) / kThreads, 148 * 4), width), kThreads, 0, s>>>(dX, n, keys);
-    gs_launch_end(ctx, 1);
-  }
-  return GS_OK;
-}
 
 // ---- filter apply (heat.cpp:116-131) -----------------------------------------------------------
 template <typename S>
@@ -1113,19 +1005,12 @@ int filter_apply_impl(gs_ctx* ctx, const gs_filter* f, const double* dX, double*
   cudaStream_t s = ctx->stream;
   Work<S> w;
   GS_TRY(w.init(ctx, n, width, false, -1, f));
-  const double* sc = w.scale_ptr();
-  if (sc) {
-    GS_TRY(column_keys(ctx, dX, n, width, w.cmax.get()));
-    gs_launch_begin(ctx, 1);
-    k_scale_from_keys<<<grid_for(width), kThreads, 0, s>>>(w.cmax.get(), width, w.scale.get());
-    gs_launch_end(ctx, 1);
-  }
   gs_launch_begin(ctx, 1);
-  k_pack<S><<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, f->lay[w.lay].order, (int64_t)n, sc);
+  k_pack<S><<<grid_for((int64_t)w.Bpad * n), kThreads, 0, s>>>(dX, w.T[0].get(), n, width, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
   gs_launch_end(ctx, 1);
   run_apply<S>(ctx, f, w, 0, MODE_NONE, nullptr, nullptr, nullptr, nullptr, false, false);
   gs_launch_begin(ctx, 1);
-  k_unpack<S><<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.acc.get(), dY, n, width, w.GW, nullptr, nullptr, f->lay[w.lay].newpos, (int64_t)n, sc);
+  k_unpack<S><<<grid_for((int64_t)width * n), kThreads, 0, s>>>(w.acc.get(), dY, n, width, w.GW, nullptr, nullptr, f->lay[w.lay].newpos, (int64_t)n);
   gs_launch_end(ctx, 1);
   GS_CUDA(ctx, cudaStreamSynchronize(s));
   return GS_OK;
@@ -1194,13 +1079,13 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   k_pack<double><<<grid_for((int64_t)len), kThreads, 0, s>>>(dnu, N.get(), n, P, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
-  k_sk_init<double><<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.t0_target(0), n, w.GW, w.G, P, w.cmax.get(), (int64_t)n);
+  k_sk_init<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.T[0].get(), n, w.GW, w.G, P, w.cmax.get(), (int64_t)n);
   gs_launch_end(ctx, 1);
   const int knp = ERRC_KERNEL_NOT_POSITIVE + 1;
-  run_finalize<S>(ctx, w, 0, 1, 0, knp, true, 0);  // threshold (and fp32 scale) of the first apply
+  run_finalize<S>(ctx, w, 0, 1, 0, knp, true);  // threshold of the first apply
   // phi = H(a * 1) (transport.cpp:176); V_1 = M / max(phi, floor) in the epilogue
   int a0 = run_apply<S>(ctx, f, w, 0, MODE_SK_PHI, da, M.get(), V[0].get(), V[1].get(), true, true);
-  run_finalize<S>(ctx, w, 1, 1, 0, knp, true, a0);
+  run_finalize<S>(ctx, w, 1, 1, 0, knp, true);
   gs_status* hst = ctx->h_status;
   cudaEvent_t ev[2];
   cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
@@ -1229,11 +1114,11 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   auto issue_sweep = [&](int parity) {
     // psi = H(a * V_s); W_s = N / max(psi, floor); T_0 = a * W_s
     a0 = run_apply<S>(ctx, f, w, a0, MODE_SK_PSI, da, N.get(), nullptr, W.get(), true, true);
-    run_finalize<S>(ctx, w, 1, 1, 0, knp, true, a0);
+    run_finalize<S>(ctx, w, 1, 1, 0, knp, true);
     // phi = H(a * W_s); err; V_{s+1} = M / max(phi, floor); T_0 = a * V_{s+1}
     a0 = run_apply<S>(ctx, f, w, a0, MODE_SK_PHI, da, M.get(), V[parity].get(), V[parity ^ 1].get(),
                       true, true);
-    run_finalize<S>(ctx, w, 1, 1, 1, knp, true, a0);
+    run_finalize<S>(ctx, w, 1, 1, 1, knp, true);
     gs_launch_begin(ctx, 1);
     k_sk_control<<<1, 1, 0, s>>>(C);
     gs_launch_end(ctx, 1);
@@ -1412,13 +1297,13 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   k_pack<double><<<grid_for((int64_t)len), kThreads, 0, s>>>(dmem, Mb.get(), n, m, w.GW, w.G, f->lay[w.lay].order, (int64_t)n);
   gs_launch_end(ctx, 1);
   gs_launch_begin(ctx, 1);
-  k_sk_init<double><<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.t0_target(0), n, w.GW, w.G, m, w.cmax.get(), (int64_t)n);
+  k_sk_init<S><<<grid_for((int64_t)len), kThreads, 0, s>>>(da, w.T[0].get(), n, w.GW, w.G, m, w.cmax.get(), (int64_t)n);
   gs_launch_end(ctx, 1);
-  run_finalize<S>(ctx, w, 0, 1, 0, 0, false, 0);
+  run_finalize<S>(ctx, w, 0, 1, 0, 0, false);
   const int knp = ERRC_KERNEL_NOT_POSITIVE + 1;
   // phi = H(a * 1) (barycenter.cpp:68); V_1 = M / max(phi, floor) in the epilogue
   int a0 = run_apply<S>(ctx, f, w, 0, MODE_SK_PHI, da, Mb.get(), V[0].get(), V[1].get(), false, true);
-  run_finalize<S>(ctx, w, 1, 1, 0, knp, false, a0);
+  run_finalize<S>(ctx, w, 1, 1, 0, knp, false);
   gs_status* hst = ctx->h_status;
   cudaEvent_t ev[2];
   cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
@@ -1436,9 +1321,9 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
     run_finalize<S>(ctx, w, 1, 0, 0, knp, false);
     // log-domain geometric mean (barycenter.cpp:75-82)
     gs_launch_begin(ctx, 1);
-    // psi (fp64): acc in the fp64 mode, T0d (unscaled by the epilogue) in the fp32 mode
-    const double* psi = w.kF32 ? w.T0d.get() : reinterpret_cast<const double*>(w.acc.get());
-    k_bary_lb<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(psi, dal.get(), n, m, w.GW, lb.get(), w.status.get(), w.scale_ptr());
+    // psi in fp64: acc in the fp64 mode, psi64 in the 32-bit mode
+    const double* psi = w.kF32 ? w.psi64.get() : reinterpret_cast<const double*>(w.acc.get());
+    k_bary_lb<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(psi, dal.get(), n, m, w.GW, lb.get(), w.status.get());
     gs_launch_end(ctx, 1);
     if (hooked) {
       const int rc = comm->allreduce(comm->user, lb.get(), n, 0, (void*)s);
@@ -1459,15 +1344,15 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
     gs_launch_end(ctx, 1);
     // W = bary / max(psi, floor); T_0 = a * W (barycenter.cpp:84-85)
     gs_launch_begin(ctx, 1);
-    k_bary_w<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(
-        bary.get(), mass.get(), psi, da, n, m, w.GW, W.get(), w.t0_target(a0), w.cmax.get(),
-        w.status.get(), w.scale_ptr());
+    k_bary_w<S><<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(
+        bary.get(), mass.get(), psi, da, n, m, w.GW, W.get(), w.T[a0].get(), w.cmax.get(),
+        w.status.get());
     gs_launch_end(ctx, 1);
-    run_finalize<S>(ctx, w, 0, 1, 0, knp, false, a0);
+    run_finalize<S>(ctx, w, 0, 1, 0, knp, false);
     // phi = H(a * W); err; V' = M / max(phi, floor) (barycenter.cpp:85-86, 70)
     a0 = run_apply<S>(ctx, f, w, a0, MODE_SK_PHI, da, Mb.get(), V[parity].get(), V[parity ^ 1].get(),
                       false, true);
-    run_finalize<S>(ctx, w, 1, 1, 1, knp, false, a0);
+    run_finalize<S>(ctx, w, 1, 1, 1, knp, false);
     gs_launch_begin(ctx, 1);
     k_bary_errlocal<<<1, 1, 0, s>>>(w.errcol.get(), m, errbuf.get());
     gs_launch_end(ctx, 1);
@@ -1543,8 +1428,7 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
       return gs_fail(ctx, ERRC_KERNEL_NOT_POSITIVE, "barycenter iterate collapsed to zero");
     if (st.error == ERRC_NUMERICAL_UNDERFLOW + 1)
       return gs_fail(ctx, ERRC_NUMERICAL_UNDERFLOW,
-                     "fp32 mode: non-finite barycenter marginal error (the scaled fp32 recurrence's "
-                     "range was left); rerun in fp64");
+                     "fp32 mode: non-finite barycenter marginal error; rerun in fp64");
     return gs_fail(ctx, ERRC_KERNEL_NOT_POSITIVE, kKnpBary);
   }
   int h_iters = 0;
@@ -1670,7 +1554,6 @@ __global__ void k_fin_global(const FinArgs F, const double* stat) {
     if (!(mn >= -F.cs.thr[col])) atomicCAS(&F.status->error, 0, F.knp_code);
   }
   if (F.has_next) F.cs.thr[col] = F.slack * stat[F.Bpad + col];
-  if (F.has_next && F.scale) F.scale[col] = pow2_floor(stat[F.Bpad + col]);
   F.cs.cmin[col] = KEY_POS_INF;
   F.cs.cmax[col] = KEY_ZERO;
 }
@@ -1835,8 +1718,7 @@ int run_apply_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& 
   A.M = M;
   A.Vcur = Vcur;
   A.Wout = Wout;
-  A.colscale = w.scale_ptr();
-  A.T0d = w.kF32 ? w.T0d.get() : nullptr;
+  A.psi = w.psi64.get();
   const PartRanges R = part_ranges(p, rows_per_block<S>(w.GW) * w.rpc);
   auto launch_range = [&](int r, int m) {
     if (R.tiles[r] == 0) return;
@@ -1873,8 +1755,7 @@ int run_apply_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& 
 
 template <typename S>
 int run_finalize_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& w, double* stat,
-                      int check, int has_next, int has_err, int knp_code, bool use_active,
-                      int next_buf = -1) {
+                      int check, int has_next, int has_err, int knp_code, bool use_active) {
   FinArgs F{};
   F.cs = w.cs();
   if (!use_active) F.cs.active = nullptr;
@@ -1887,7 +1768,6 @@ int run_finalize_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S
   F.status = w.status.get();
   F.knp_code = knp_code;
   F.slack = Prec<S>::slack;
-  F.scale = has_next ? w.scale_ptr() : nullptr;  // from the combined column max: same on every rank
   gs_launch_begin(ctx, 1);
   k_fin_local<<<w.B, kThreads, 0, ctx->stream>>>(F, stat);
   gs_launch_end(ctx, 1);
@@ -1896,7 +1776,6 @@ int run_finalize_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S
   gs_launch_begin(ctx, 1);
   k_fin_global<<<(w.B + kThreads - 1) / kThreads, kThreads, 0, ctx->stream>>>(F, stat);
   gs_launch_end(ctx, 1);
-  if (has_next && next_buf >= 0) rescale_t0<S>(ctx, w, next_buf);
   return GS_OK;
 }
 
@@ -1910,32 +1789,16 @@ int filter_apply_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, c
   w.tiles = part_tiles<S>(p, w);
   Halo<S> h;
   GS_TRY(h.init(ctx, p, w.Bpad));
-  const double* sc = w.scale_ptr();
-  if (sc) {  // fp32: per-column scale from the max over every rank's rows
-    DevBuf<double> stat;
-    GS_CUDA(ctx, stat.alloc(width, s));
-    GS_TRY(column_keys(ctx, dX, nl, width, w.cmax.get()));
-    gs_launch_begin(ctx, 1);
-    k_keys_to_double<<<grid_for(width), kThreads, 0, s>>>(w.cmax.get(), width, stat.get());
-    gs_launch_end(ctx, 1);
-    GS_TRY(allreduce(ctx, p, comm, stat.get(), width, 1));
-    gs_launch_begin(ctx, 1);
-    k_scale_from_max<<<grid_for(width), kThreads, 0, s>>>(stat.get(), width, w.scale.get());
-    gs_launch_end(ctx, 1);
-    gs_launch_begin(ctx, 1);
-    k_fill_key<<<grid_for(w.Bpad), kThreads, 0, s>>>(w.cmax.get(), w.Bpad, KEY_ZERO);
-    gs_launch_end(ctx, 1);
-  }
   if (nl > 0) {
     gs_launch_begin(ctx, 1);
-    k_pack<S><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(dX, w.T[0].get(), nl, width, w.GW, w.G, nullptr, w.ld, sc);
+    k_pack<S><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(dX, w.T[0].get(), nl, width, w.GW, w.G, nullptr, w.ld);
     gs_launch_end(ctx, 1);
   }
   int next = 0;
   GS_TRY(run_apply_part<S>(ctx, p, comm, w, h, 0, MODE_NONE, nullptr, nullptr, nullptr, nullptr, false, false, &next));
   if (nl > 0) {
     gs_launch_begin(ctx, 1);
-    k_unpack<S><<<grid_for((int64_t)width * nl), kThreads, 0, s>>>(w.acc.get(), dY, nl, width, w.GW, nullptr, nullptr, nullptr, w.ld, sc);
+    k_unpack<S><<<grid_for((int64_t)width * nl), kThreads, 0, s>>>(w.acc.get(), dY, nl, width, w.GW, nullptr, nullptr, nullptr, w.ld);
     gs_launch_end(ctx, 1);
   }
   GS_CUDA(ctx, cudaStreamSynchronize(s));
@@ -2002,14 +1865,14 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
     k_pack<double><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(dnu, N.get(), nl, P, w.GW, w.G, nullptr, w.ld);
     gs_launch_end(ctx, 1);
     gs_launch_begin(ctx, 1);
-    k_sk_init<double><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(da, w.t0_target(0), nl, w.GW, w.G, P, w.cmax.get(), w.ld);
+    k_sk_init<S><<<grid_for((int64_t)w.Bpad * nl), kThreads, 0, s>>>(da, w.T[0].get(), nl, w.GW, w.G, P, w.cmax.get(), w.ld);
     gs_launch_end(ctx, 1);
   }
   const int knp = ERRC_KERNEL_NOT_POSITIVE + 1;
   int a0 = 0;
-  GS_TRY(run_finalize_part<S>(ctx, p, comm, w, stat.get(), 0, 1, 0, knp, true, 0));
+  GS_TRY(run_finalize_part<S>(ctx, p, comm, w, stat.get(), 0, 1, 0, knp, true));
   GS_TRY(run_apply_part<S>(ctx, p, comm, w, h, 0, MODE_SK_PHI, da, M.get(), V[0].get(), V[1].get(), true, true, &a0));
-  GS_TRY(run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 0, knp, true, a0));
+  GS_TRY(run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 0, knp, true));
   CtlArgs C{};
   C.active = w.active.get();
   C.gactive = w.gactive.get();
@@ -2043,11 +1906,11 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
       if (st.error || st.n_active == 0) break;
     }
     rc = run_apply_part<S>(ctx, p, comm, w, h, a0, MODE_SK_PSI, da, N.get(), nullptr, W.get(), true, true, &a0);
-    if (!rc) rc = run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 0, knp, true, a0);
+    if (!rc) rc = run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 0, knp, true);
     if (!rc)
       rc = run_apply_part<S>(ctx, p, comm, w, h, a0, MODE_SK_PHI, da, M.get(), V[sweep & 1].get(),
                              V[(sweep & 1) ^ 1].get(), true, true, &a0);
-    if (!rc) rc = run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 1, knp, true, a0);
+    if (!rc) rc = run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 1, knp, true);
     if (rc) break;
     gs_launch_begin(ctx, 1);
     k_sk_control<<<1, 1, 0, s>>>(C);

@@ -118,7 +118,7 @@ constexpr int kPrefetchStages = GS_PREFETCH_STAGES;
 #endif
 
 template <typename S>
-struct RowIdx {  // a row's CSR range and this lane's entry of its first chunk
+struct RowIdx {  // a row's CSR range and this lane's entry of its first chunk (value as stored)
   int pb = 0, pe = 0, c = 0;
   S v = S(0);
 };
@@ -126,20 +126,41 @@ struct RowIdx {  // a row's CSR range and this lane's entry of its first chunk
 enum StepMode { MODE_NONE = 0, MODE_SK_PSI = 1, MODE_SK_PHI = 2, MODE_BARY_PSI = 3 };
 
 // ---- precision traits --------------------------------------------------------------------------
+// S is the storage type of the Chebyshev vectors (T_{k-1}, T_{k-2}, acc, T_0) and of L_s's values;
+// the arithmetic is fp64 in both modes (R = double).
+//   double: the reference-exact path.
+//   float : the optional 32-bit mode (DESIGN.md §4 "Precision"). A vector word is the upper half
+//           of the fp64 word -- sign, the 11-bit fp64 exponent, 20 fraction bits -- rounded to
+//           nearest, carried in a 4-byte `float` slot (bit pattern only, never used as IEEE
+//           binary32). The reference's scaling vectors span more decades than binary32's 8-bit
+//           exponent holds (config 1: per-column scaling with 66 decades of range still departs
+//           from fp64 by sweep 20, profiles/r02_fp32_range.md); this word keeps fp64's range, so
+//           the reference's 1e-300 floor and every control decision carry over, at 2^-21 relative
+//           rounding per stored value. L_s's values are IEEE binary32 (entries of a scaled
+//           Laplacian, no range issue).
 template <typename S>
 struct Prec;
 template <>
 struct Prec<double> {
   static constexpr double slack = 1e-12;   // positivity slack (transport.cpp:24,33)
+  __device__ static __forceinline__ double dec(double x) { return x; }   // stored vector word
+  __device__ static __forceinline__ double enc(double x) { return x; }
+  __device__ static __forceinline__ double val(double v) { return v; }   // matrix value
   __device__ static __forceinline__ double fmat(double a, double b, double c) { return fma(a, b, c); }
 };
 template <>
 struct Prec<float> {
-  // fp32 mode has no reference (SURVEY §7 hard part 7): the recurrence's rounding is ~1e-7 of
-  // the column maximum, above the reference's 1e-12 positivity slack, so the slack is
-  // 64 FLT_EPSILON; the division floor is relative to the column's scale (kF32Range below).
-  static constexpr double slack = 64.0 * (double)FLT_EPSILON;
-  __device__ static __forceinline__ float fmat(float a, float b, float c) { return fmaf(a, b, c); }
+  // rounding of the stored words (2^-21 relative each) accumulates over the K steps; the
+  // positivity slack is 2^-14 of max |x| (the reference's 1e-12 assumes fp64 storage)
+  static constexpr double slack = 0x1p-14;
+  __device__ static __forceinline__ double dec(float w) { return __hiloint2double(__float_as_int(w), 0); }
+  __device__ static __forceinline__ float enc(double x) {
+    // round to nearest on the dropped 32 bits (the carry propagates into the exponent)
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x) + 0x80000000ull;
+    return __int_as_float((int)(b >> 32));
+  }
+  __device__ static __forceinline__ double val(float v) { return (double)v; }
+  __device__ static __forceinline__ double fmat(double a, double b, double c) { return fma(a, b, c); }
 };
 
 // bytes per lane for narrow rows (16 < GW * sizeof(S) <= 64): 8 gives more lanes per row, hence more
@@ -338,27 +359,25 @@ struct StepArgs {  // vector pointers are S* of the launch's precision
   const double* M;      // PSI: N (targets); PHI: M (sources / members)
   const double* Vcur;   // PHI: V of this sweep
   double* Wout;         // PSI: W; PHI: V of the next sweep
-  // fp32 mode: colscale[c] = 2^e_c, the power of two the apply's input column was divided by
-  // (k_rescale32); the epilogue multiplies acc back and floors divisions at 2^(e_c - 100)
-  // (kF32Range). The next T_0 (PSI/PHI) or psi (BARY_PSI) is written unscaled to T0d.
-  const double* colscale;
-  double* T0d;
+  double* psi;          // BARY_PSI in the 32-bit mode: psi in fp64 (the fp64 mode uses acc)
 };
-
-// Range of the scaled fp32 recurrence: inputs are divided by a per-column power of two so the
-// column maximum lies in [1, 2); outputs below 2^-kF32Range of it are not resolved (fp32's normal
-// range ends at 2^-126), so the fp32 mode's division floor is max(1e-300, 2^(e_c - kF32Range)).
-constexpr int kF32Range = 100;
-constexpr double kF32Floor = 0x1p-100;  // 2^-kF32Range
-static_assert(kF32Floor == 1.0 / (double)(1ull << 50) / (double)(1ull << 50), "2^-kF32Range");
 
 template <typename S, int GW, int MODE>
 __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, int q,
-                                           const S (&y)[Lay<GW, S>::VEC],
+                                           const double (&y)[Lay<GW, S>::VEC],
                                            double (&mn)[Lay<GW, S>::VEC],
                                            double (&mx)[Lay<GW, S>::VEC],
                                            double (&er)[Lay<GW, S>::VEC], const S* pre,
                                            int pre_stride, bool pre_tp = true);
+
+// encode + vector store of fp64 register values into storage words
+template <typename S, int VEC>
+__device__ __forceinline__ void st_enc(S* p, const double (&v)[VEC]) {
+  S t[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) t[e] = Prec<S>::enc(v[e]);
+  st_vec<S, VEC>(p, t);
+}
 
 // One row of one Chebyshev step; epilogue partials accumulate in mn/mx/er (double).
 template <typename S, int GW, int MODE>
@@ -399,10 +418,10 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
       for (int e = 0; e < VEC; ++e) own[2 * VEC + e] = t[e];
     }
   }
-  // ---- y = L_s T_{k-1} (row) ------------------------------------------------------------------
-  S y[VEC];
+  // ---- y = L_s T_{k-1} (row), fp64 fma chain ----------------------------------------------------
+  double y[VEC];
 #pragma unroll
-  for (int e = 0; e < VEC; ++e) y[e] = S(0);
+  for (int e = 0; e < VEC; ++e) y[e] = 0.0;
   if constexpr (LPR == 1) {
     if (valid) {
       int p = __ldg(A.offs + row);
@@ -436,7 +455,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
 #pragma unroll
           for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) y[e] = P::fmat(vv[u], xx[u][e], y[e]);
+            for (int e = 0; e < VEC; ++e) y[e] = P::fmat(P::val(vv[u]), P::dec(xx[u][e]), y[e]);
           ca = cb;
           va = vb;
         }
@@ -455,7 +474,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) y[e] = P::fmat(vv[u], xx[u][e], y[e]);
+          for (int e = 0; e < VEC; ++e) y[e] = P::fmat(P::val(vv[u]), P::dec(xx[u][e]), y[e]);
       }
       for (; p < pe; ++p) {
         const int c = __ldg(A.cols + p);
@@ -463,7 +482,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
         S x[VEC];
         ld_vec<S, VEC>(Tp + (size_t)c * GW, x);
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) y[e] = P::fmat(v, x[e], y[e]);
+        for (int e = 0; e < VEC; ++e) y[e] = P::fmat(P::val(v), P::dec(x[e]), y[e]);
       }
     }
   } else {
@@ -507,7 +526,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
 #pragma unroll
         for (int j = 0; j < GB; ++j)
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) y[e] = P::fmat(vv[j], xx[j][e], y[e]);
+          for (int e = 0; e < VEC; ++e) y[e] = P::fmat(P::val(vv[j]), P::dec(xx[j][e]), y[e]);
       }
       for (; u < cnt; ++u) {
         const int c = __shfl_sync(mask, myc, u, LPR);
@@ -515,7 +534,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
         S x[VEC];
         ld_vec<S, VEC>(Tp + (size_t)c * GW, x);
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) y[e] = P::fmat(v, x[e], y[e]);
+        for (int e = 0; e < VEC; ++e) y[e] = P::fmat(P::val(v), P::dec(x[e]), y[e]);
       }
       if constexpr (GS_IDX_PREFETCH) {
         myc = nxc;
@@ -532,7 +551,7 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
 // acc update and the stores / fused epilogue (row < A.n).
 template <typename S, int GW, int MODE>
 __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, int q,
-                                           const S (&y)[Lay<GW, S>::VEC],
+                                           const double (&y)[Lay<GW, S>::VEC],
                                            double (&mn)[Lay<GW, S>::VEC],
                                            double (&mx)[Lay<GW, S>::VEC],
                                            double (&er)[Lay<GW, S>::VEC], const S* pre,
@@ -543,72 +562,67 @@ __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, in
   const size_t gbase = (size_t)g * A.ld * GW + q * VEC;
   const size_t idx = gbase + (size_t)row * GW;
   if (A.k == 0) {  // plain SpMM (sparse.cpp:85-99)
-    st_vec<S, VEC>(static_cast<S*>(A.Tout) + idx, y);
+    st_enc<S, VEC>(static_cast<S*>(A.Tout) + idx, y);
     return;
   }
   // ---- own-row operands (prefetched into shared memory by cp.async when `pre`) ---------------
   const bool read_acc = A.acc_terms > 0 && !A.acc_init;
-  S tp[VEC], t2[VEC], a0[VEC];
+  S tps[VEC], t2s[VEC], a0s[VEC];
   if (pre && pre_tp) {
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
-      tp[e] = pre[e];
-      t2[e] = pre[pre_stride + e];
-      a0[e] = pre[2 * pre_stride + e];
+      tps[e] = pre[e];
+      t2s[e] = pre[pre_stride + e];
+      a0s[e] = pre[2 * pre_stride + e];
     }
   } else if (pre) {  // T_{k-2}, acc staged; T_{k-1}[row] read directly (L1-hot: just gathered)
-    ld_vec<S, VEC>(static_cast<const S*>(A.Tprev) + idx, tp);
+    ld_vec<S, VEC>(static_cast<const S*>(A.Tprev) + idx, tps);
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
-      t2[e] = pre[e];
-      a0[e] = pre[pre_stride + e];
+      t2s[e] = pre[e];
+      a0s[e] = pre[pre_stride + e];
     }
   } else {
-    ld_vec<S, VEC>(static_cast<const S*>(A.Tprev) + idx, tp);
-    if (A.k >= 2) ld_vec_rw<S, VEC>(static_cast<const S*>(A.Tout) + idx, t2);
-    if (read_acc) ld_vec_rw<S, VEC>(static_cast<const S*>(A.acc) + idx, a0);
+    ld_vec<S, VEC>(static_cast<const S*>(A.Tprev) + idx, tps);
+    if (A.k >= 2) ld_vec_rw<S, VEC>(static_cast<const S*>(A.Tout) + idx, t2s);
+    if (read_acc) ld_vec_rw<S, VEC>(static_cast<const S*>(A.acc) + idx, a0s);
+  }
+  double tp[VEC], t2[VEC], a0[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    tp[e] = P::dec(tps[e]);
+    t2[e] = P::dec(t2s[e]);
+    a0[e] = P::dec(a0s[e]);
   }
   // ---- recurrence (heat.cpp:121-130) ----------------------------------------------------------
-  S t[VEC], ac[VEC];
+  double t[VEC], ac[VEC];
   if (A.k == 1) {
 #pragma unroll
     for (int e = 0; e < VEC; ++e) t[e] = y[e] - tp[e];
   } else {
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) t[e] = S(2) * (y[e] - tp[e]) - t2[e];
+    for (int e = 0; e < VEC; ++e) t[e] = 2.0 * (y[e] - tp[e]) - t2[e];
   }
   // acc = fma(b_k, T_k, acc) for the pending steps, oldest first (heat.cpp:122,129)
   if (A.acc_terms > 0) {
-    const S bk = S(A.bk), bk1 = S(A.bk1), bk2 = S(A.bk2), b0h = S(A.b0h);
+    const double bk = A.bk, bk1 = A.bk1, bk2 = A.bk2, b0h = A.b0h;
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
-      S base = A.acc_init ? b0h * (A.k == 1 ? tp[e] : t2[e]) : a0[e];
+      double base = A.acc_init ? b0h * (A.k == 1 ? tp[e] : t2[e]) : a0[e];
       if (A.acc_terms >= 3) base = P::fmat(bk2, t2[e], base);
       if (A.acc_terms >= 2) base = P::fmat(bk1, tp[e], base);
       ac[e] = P::fmat(bk, t[e], base);
     }
   }
   if constexpr (MODE == MODE_NONE) {
-    if (A.store_t) st_vec<S, VEC>(static_cast<S*>(A.Tout) + idx, t);
-    if (A.acc_terms > 0) st_vec<S, VEC>(static_cast<S*>(A.acc) + idx, ac);
+    if (A.store_t) st_enc<S, VEC>(static_cast<S*>(A.Tout) + idx, t);
+    if (A.acc_terms > 0) st_enc<S, VEC>(static_cast<S*>(A.acc) + idx, ac);
   } else {
     // ---- fused epilogue of the last step (fp64; transport.cpp:171-184, barycenter.cpp:71) ----
     const int* act = A.cs.active;
     const int col0 = g * GW + q * VEC;
-    constexpr bool F32 = sizeof(S) == 4;
-    double ps[VEC], fl[VEC];  // psi = p_K(L_s) x, unscaled; division floor
 #pragma unroll
-    for (int e = 0; e < VEC; ++e) {
-      if constexpr (F32) {
-        const double sc = A.colscale[col0 + e];
-        ps[e] = (double)ac[e] * sc;
-        fl[e] = fmax(GS_FLOOR, sc * kF32Floor);
-      } else {
-        ps[e] = ac[e];
-        fl[e] = GS_FLOOR;  // kDivisionFloor (transport.cpp:13, barycenter.cpp:9)
-      }
-      mn[e] = fmin(mn[e], ps[e]);
-    }
+    for (int e = 0; e < VEC; ++e) mn[e] = fmin(mn[e], ac[e]);
     if constexpr (MODE == MODE_SK_PSI || MODE == MODE_SK_PHI) {
       double op1[VEC], nx[VEC], t0[VEC];
       ld_vec<double, VEC>(A.M + idx, op1);
@@ -617,22 +631,21 @@ __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, in
         double v[VEC];
         ld_vec_rw<double, VEC>(A.Vcur + idx, v);
 #pragma unroll
-        for (int e = 0; e < VEC; ++e) er[e] = er[e] + fabs(v[e] * ps[e] - op1[e]);  // transport.cpp:184
+        for (int e = 0; e < VEC; ++e) er[e] = er[e] + fabs(v[e] * ac[e] - op1[e]);  // transport.cpp:184
       }
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
-        nx[e] = op1[e] / fmax(ps[e], fl[e]);  // W (transport.cpp:180) / V' (:178)
-        t0[e] = ai * nx[e];                   // a .* x (transport.cpp:172)
+        nx[e] = op1[e] / fmax(ac[e], GS_FLOOR);  // W (transport.cpp:180) / V' (:178), kDivisionFloor
+        t0[e] = ai * nx[e];                      // a .* x (transport.cpp:172)
         mx[e] = fmax(mx[e], fabs(t0[e]));
       }
-      if constexpr (F32) st_vec<double, VEC>(A.T0d + idx, t0);  // scaled by k_rescale32
-      else st_vec<S, VEC>(static_cast<S*>(A.Tout) + idx, t0);
+      st_enc<S, VEC>(static_cast<S*>(A.Tout) + idx, t0);
       double* wo = A.Wout + idx;
 #pragma unroll
       for (int e = 0; e < VEC; ++e)
         if (!act || act[col0 + e]) wo[e] = nx[e];
-    } else {  // MODE_BARY_PSI
-      if constexpr (F32) st_vec<double, VEC>(A.T0d + idx, ps);
+    } else {  // MODE_BARY_PSI: psi kept in fp64 for the log-domain mean
+      if constexpr (sizeof(S) == 4) st_vec<double, VEC>(A.psi + idx, ac);
       else st_vec<S, VEC>(static_cast<S*>(A.acc) + idx, ac);
     }
   }
@@ -695,7 +708,7 @@ __device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int til
 #define GS_MIN_BLOCKS_NARROW 5
 #endif
 #ifndef GS_MIN_BLOCKS32
-#define GS_MIN_BLOCKS32 6
+#define GS_MIN_BLOCKS32 5
 #endif
 template <typename S, int GW, int MODE, int RPC>
 __global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0
@@ -1033,7 +1046,7 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step_w1(const StepArgs A) {
     const S* __restrict__ Tp = static_cast<const S*>(A.Tprev) + (size_t)g * A.ld;
     const S* __restrict__ vals = static_cast<const S*>(A.vals);
     const int pb = __ldg(A.offs + row), pe = __ldg(A.offs + row + 1);
-    S y[1] = {S(0)};
+    double y[1] = {0.0};
     for (int p0 = pb; p0 < pe; p0 += 32) {
       S v = S(0), x = S(0);
       if (p0 + lane < pe) {
@@ -1042,7 +1055,8 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step_w1(const StepArgs A) {
       }
       const int cnt = min(32, pe - p0);
       for (int u = 0; u < cnt; ++u)
-        y[0] = Prec<S>::fmat(__shfl_sync(0xffffffffu, v, u), __shfl_sync(0xffffffffu, x, u), y[0]);
+        y[0] = Prec<S>::fmat(Prec<S>::val(__shfl_sync(0xffffffffu, v, u)),
+                             Prec<S>::dec(__shfl_sync(0xffffffffu, x, u)), y[0]);
     }
     if (lane == 0) finish_row<S, 1, MODE>(A, g, row, 0, y, mn, mx, er, nullptr, 0);
   }
