@@ -319,7 +319,6 @@ def run_engine(args):
     barrier()
     torch.cuda.synchronize()
     sampler.start()
-    ctx.set_timing(True, period=args.timing_period)
     l0 = ctx.launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -331,35 +330,48 @@ def run_engine(args):
     barrier()
     clocks = sampler.stop()
     launches = ctx.launch_count() - l0
-    steps_total = args.steps * (1 + 2 * args.sweeps) * 30  # step-kernel launches in the region
-    step_n, step_ms = ctx.timing(0)
-    epi_n, epi_ms = ctx.timing(1)
-    ctx.set_timing(False)
+    # step-kernel launches per run: the initial apply plus 2 applies per sweep, K = 30 steps each
+    steps_per_run = (1 + 2 * args.sweeps) * 30
+    steps_total = args.steps * steps_per_run
     elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1))
     value = world * args.sweeps * args.steps / (elapsed_ms / 1000.0)
 
-    if step_n == 0:
-        # small problems replay CUDA graphs (no per-launch events): time the step kernel in one
-        # extra non-graph run of the same workload
-        os.environ["GS_GRAPH"] = "0"
-        ctx.set_timing(True)
-        step()
-        torch.cuda.synchronize()
-        step_n, step_ms = ctx.timing(0)
-        ctx.set_timing(False)
-        del os.environ["GS_GRAPH"]
+    # ---- per-launch kernel time: one extra run of the same workload with per-kernel launches
+    # (no CUDA graphs) and an event pair around EVERY step-kernel launch; the graph-replayed timed
+    # region above cannot be split into launches. share_of_step = summed step-kernel time / that
+    # run's own elapsed time, which must be <= 1.
+    os.environ["GS_GRAPH"] = "0"
+    ctx.set_timing(True)
+    k0 = torch.cuda.Event(enable_timing=True)
+    k1 = torch.cuda.Event(enable_timing=True)
+    k0.record(stream)
+    step()
+    k1.record(stream)
+    torch.cuda.synchronize()
+    step_n, step_ms = ctx.timing(0)
+    epi_n, epi_ms = ctx.timing(1)
+    ctx.set_timing(False)
+    del os.environ["GS_GRAPH"]
+    kt_elapsed = k0.elapsed_time(k1)
+    share = step_ms / max(kt_elapsed, 1e-9)
+    assert share <= 1.0 + 1e-6, ("step-kernel time exceeds its run", step_ms, kt_elapsed)
 
     # ---- roofline of the dominant kernel ------------------------------------------------------
     peak, peak_kind = peaks()
     bytes_step = algorithmic_bytes_per_step(n, nnz_L, P)
     avg_step_ms = step_ms / max(step_n, 1)
     achieved = bytes_step / (avg_step_ms / 1000.0) / 1e9
+    # lower bound from the graph-replayed timed region: every step launch's bytes over the whole
+    # elapsed time (finalize / control / epilogue kernels included)
+    lb_achieved = bytes_step * steps_total / (elapsed_ms / 1000.0) / 1e9
     traffic = None
+    ncu_info = None
     prof = os.path.join(ROOT, "profiles", "cheb_step_traffic.json")
-    if args.config == 1 and os.path.exists(prof):  # ncu DRAM bytes of the config-1 step kernel
+    if args.config == 1 and os.path.exists(prof):  # ncu counters of the config-1 step kernel
         try:
             with open(prof) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                ncu_info = json.load(f)
+            traffic = ncu_info.get("dram_bytes_per_launch")
         except Exception:
             traffic = None
 
@@ -396,29 +408,55 @@ def run_engine(args):
     h2d = 2 * P * n * 8 + n * 8
     d2h = 2 * P * n * 8 + P * (8 + 8 + 4 + 4 + 8)
 
-    # ---- fp32 mode on the same workload (config 1 is specified "fp64 and fp32") ------------------
+    def run_sk(Mt, Nt, sweeps, flg, tol=TOL_RUN_ALL):
+        """One engine call on device inputs (P_ = rows of Mt); returns host results or the errc."""
+        P_ = Mt.shape[0]
+        v_ = torch.empty((P_, n), dtype=torch.float64, device=dev)
+        w_ = torch.empty_like(v_)
+        c_ = torch.empty(P_, dtype=torch.float64, device=dev)
+        k_ = torch.empty_like(c_)
+        e_ = torch.empty_like(c_)
+        i_ = torch.empty(P_, dtype=torch.int32, device=dev)
+        cv_ = torch.empty_like(i_)
+        fp_, fs_ = C.c_int(-1), C.c_int(-1)
+        rc = lib.gs_sinkhorn(ctx.handle, filt._h, a.data_ptr(), Mt.data_ptr(), Nt.data_ptr(), P_,
+                             sweeps, tol, flg, _capi.GS_MEM_DEVICE, v_.data_ptr(), w_.data_ptr(),
+                             c_.data_ptr(), k_.data_ptr(), i_.data_ptr(), cv_.data_ptr(),
+                             e_.data_ptr(), C.byref(fp_), C.byref(fs_))
+        torch.cuda.synchronize()
+        if rc != 0:
+            return {"errc": lib.gs_last_error(ctx.handle).decode(),
+                    "rc": int(rc), "fail_pair": fp_.value, "fail_sweep": fs_.value}
+        return {"v": v_.cpu().numpy(), "w": w_.cpu().numpy(), "cost": c_.cpu().numpy(),
+                "iterations": i_.cpu().numpy()}
+
+    # well-posed companion pairs on the same graph (workloads.bump_mixture_companions: every
+    # target bump within the K-hop reach of its source bump, so the reference converges instead
+    # of raising Disconnected; SURVEY §7 hard part 1)
+    cmus, cnus = workloads.bump_mixture_companions(cfg.roll, P, seed=7 + 1000 * rank)
+    Mc = torch.from_numpy(cmus).to(dev)
+    Nc = torch.from_numpy(cnus).to(dev)
+
+    # ---- fp32 mode (config 1 is specified "fp64 and fp32"; DESIGN.md §4 "Precision") ----------
     fp32 = None
     if not args.no_fp32:
         flags32 = flags | _capi.GS_FLAG_FP32
-
-        def step32():
-            ctx.check(lib.gs_sinkhorn(ctx.handle, filt._h, a.data_ptr(), M.data_ptr(), N.data_ptr(),
-                                      P, args.sweeps, TOL_RUN_ALL, flags32, _capi.GS_MEM_DEVICE,
-                                      ov.data_ptr(), ow.data_ptr(), oc.data_ptr(), ok.data_ptr(),
-                                      oi.data_ptr(), occ.data_ptr(), oe.data_ptr(), C.byref(fp),
-                                      C.byref(fs)))
-
-        step32()  # warm-up of the fp32 instantiation
-        step()
-        cost64 = oc.cpu().numpy().copy()
-        step32()
-        cost32 = oc.cpu().numpy().copy()
+        r64 = run_sk(Mc, Nc, args.sweeps, flags)
+        r32 = run_sk(Mc, Nc, args.sweeps, flags32)  # also the warm-up of the 32-bit instantiation
         torch.cuda.synchronize()
         barrier()
         ctx.set_timing(True)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         k32 = max(1, min(args.steps, 2))
+
+        def step32():
+            ctx.check(lib.gs_sinkhorn(ctx.handle, filt._h, a.data_ptr(), Mc.data_ptr(), Nc.data_ptr(),
+                                      P, args.sweeps, TOL_RUN_ALL, flags32, _capi.GS_MEM_DEVICE,
+                                      ov.data_ptr(), ow.data_ptr(), oc.data_ptr(), ok.data_ptr(),
+                                      oi.data_ptr(), occ.data_ptr(), oe.data_ptr(), C.byref(fp),
+                                      C.byref(fs)))
+
         e0.record(stream)
         for _ in range(k32):
             step32()
@@ -428,17 +466,31 @@ def run_engine(args):
         ctx.set_timing(False)
         el32 = max_over_ranks(e0.elapsed_time(e1))
         bytes32 = nnz_L * (4 + 4) + 4 * (n + 1) + 5 * n * P * 4
-        avg32 = ms32 / max(n32, 1)
-        fp32 = {"value": world * args.sweeps * k32 / (el32 / 1000.0), "unit": UNIT, "steps": k32,
-                "avg_step_kernel_ms": avg32, "bytes_per_launch": bytes32,
-                "achieved_GBs": bytes32 / (avg32 / 1000.0) / 1e9,
-                "max_rel_cost_vs_fp64": _max_rel(cost32, cost64),
-                "finite_costs": int(np.isfinite(cost32).sum()), "pairs": int(P)}
+        c64 = r64.get("cost")
+        c32 = r32.get("cost")
+        # config 1 as specified, reference semantics (stagnation abort on): the 32-bit mode must
+        # stop at the same pair with the same errc as fp64
+        spec64 = run_sk(M, N, args.sweeps, 0, tol=1e-9)
+        spec32 = run_sk(M, N, args.sweeps, _capi.GS_FLAG_FP32, tol=1e-9)
+        strip = lambda r: {k: r[k] for k in ("rc", "fail_pair", "fail_sweep", "errc") if k in r} or \
+            {"rc": 0, "iterations": int(r["iterations"].max())}
+        fp32 = {"storage": "32-bit words: sign + fp64 exponent + 20 fraction bits (DESIGN.md §4)",
+                "inputs": f"{P} well-posed companion pairs on the same graph, {args.sweeps} sweeps",
+                "value": world * args.sweeps * k32 / (el32 / 1000.0), "unit": UNIT, "steps": k32,
+                "avg_step_kernel_ms": ms32 / max(n32, 1) if n32 else None,
+                "bytes_per_launch": bytes32,
+                "max_rel_cost_vs_fp64": _max_rel(c32, c64) if c32 is not None and c64 is not None else None,
+                "tolerance": 1e-4,
+                "finite_costs": int(np.isfinite(c32).sum()) if c32 is not None else 0, "pairs": int(P),
+                "as_specified_abort_on": {"fp64": strip(spec64), "fp32": strip(spec32),
+                                          "same_outcome": strip(spec64) == strip(spec32)}}
 
-    # ---- CPU baseline (rank 0, N = 1) ---------------------------------------------------------
+    # ---- CPU baseline (rank 0, N = 1) and results parity ----------------------------------------
     cpu = None
     parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyoracle as po
         offs = lap.matrix.row_offsets().copy()
         cols = lap.matrix.col_indices().copy()
         vals = lap.matrix.values().copy()
@@ -447,18 +499,30 @@ def run_engine(args):
         cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                "sample": f"{sweeps} sweep(s) of the same 64-pair batch on the GPU-built n={n} "
                          f"graph, oracle restatement -O3 -march=native OpenMP ({dt:.1f} s)"}
-        # results parity at full size: the engine's run of the same sweeps on the same operator
-        ctx.check(lib.gs_sinkhorn(ctx.handle, filt._h, a.data_ptr(), M.data_ptr(), N.data_ptr(), P,
-                                  sweeps, TOL_RUN_ALL, flags, _capi.GS_MEM_DEVICE,
-                                  ov.data_ptr(), ow.data_ptr(), oc.data_ptr(), ok.data_ptr(),
-                                  oi.data_ptr(), occ.data_ptr(), oe.data_ptr(), C.byref(fp),
-                                  C.byref(fs)))
-        torch.cuda.synchronize()
-        ev_, ew_, ec_ = ov.cpu().numpy(), ow.cpu().numpy(), oc.cpu().numpy()
-        parity = {"sweeps": sweeps, "against": "oracle restatement, same GPU-built Laplacian, same inputs",
-                  "v_w_bit_identical": bool(np.array_equal(ev_, ref["v"]) and np.array_equal(ew_, ref["w"])),
-                  "max_rel_v": _max_rel(ev_, ref["v"]), "max_rel_w": _max_rel(ew_, ref["w"]),
-                  "max_rel_cost": _max_rel(ec_, ref["cost"])}
+        # (1) the timed workload itself, first sweep(s), all 64 pairs: bit-identical v / w
+        r1 = run_sk(M, N, sweeps, flags)
+        parity = {"against": "oracle restatement (oracle/), same GPU-built Laplacian, same inputs",
+                  "timed_workload": {"sweeps": sweeps, "pairs": int(P),
+                                     "v_w_bit_identical": bool(np.array_equal(r1["v"], ref["v"]) and
+                                                               np.array_equal(r1["w"], ref["w"])),
+                                     "max_rel_cost": _max_rel(r1["cost"], ref["cost"])}}
+        # (2) all sweeps on well-posed companion pairs (reference semantics, abort on): every
+        # cost within 1e-9 relative, v / w bit-identical
+        pp = min(P, args.parity_pairs)
+        lib_o = po.lib(native=True)
+        fo = po.Filter(po.CSR(n, offs, cols, vals), 0, lap.lambda_max_bound, cfg.t, cfg.degree)
+        t0p = time.perf_counter()
+        refc = po.sinkhorn_batch(fo, np.full(n, 1.0 / n), cmus[:pp], cnus[:pp], args.sweeps, 1e-9,
+                                 flags=0, L=lib_o)
+        dtp = time.perf_counter() - t0p
+        rc_ = run_sk(Mc[:pp].contiguous(), Nc[:pp].contiguous(), args.sweeps, 0, tol=1e-9)
+        parity["companion_full_run"] = {
+            "pairs": pp, "max_sweeps": args.sweeps, "tol": 1e-9,
+            "iterations_engine": rc_["iterations"].tolist(),
+            "iterations_oracle": refc["iterations"].tolist(),
+            "v_w_bit_identical": bool(np.array_equal(rc_["v"], refc["v"]) and np.array_equal(rc_["w"], refc["w"])),
+            "max_rel_cost": _max_rel(rc_["cost"], refc["cost"]), "tolerance": 1e-9,
+            "oracle_s": dtp}
 
     if rank == 0:
         line = {
@@ -480,8 +544,14 @@ def run_engine(args):
                                     "k_cheb_step_w1<double, *> (fused Chebyshev step, one warp per row; "
                                     "latency-bound: the 0.39 MB working set lives in L2, SURVEY §8(d))"),
                          "bytes_per_launch": bytes_step, "avg_launch_ms": avg_step_ms,
-                         "launches_timed": step_n, "timing_period": args.timing_period,
-                         "share_of_step": avg_step_ms * steps_total / max(elapsed_ms, 1e-9)},
+                         "launches_timed": step_n,
+                         "timing": "event pair around every step launch of one full run with "
+                                   "per-kernel launches (GS_GRAPH=0)",
+                         "share_of_step": share,
+                         "lower_bound_from_timed_region": {
+                             "achieved": lb_achieved, "frac": lb_achieved / peak,
+                             "how": "step launches x bytes / elapsed of the graph-replayed timed region"},
+                         "ncu": ncu_info},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps},
             "gpu_launches": int(launches),
@@ -1071,6 +1141,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sweeps", type=int, default=1)
     ap.add_argument("--ref-sweeps", type=int, default=2)
+    ap.add_argument("--parity-pairs", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
