@@ -118,6 +118,20 @@ int gs_filter_order(gs_ctx* ctx, const gs_filter* f, int* order, int mem);
  * counterpart (the reference has no locality renumbering). */
 int gs_filter_set_order(gs_ctx* ctx, gs_filter* f, int layout, const int* order, int mem);
 
+/* ---- windowed step kernel: host-side plan (engine internals, exposed for CPU tests) -------
+ * The wide-row Chebyshev step (gs_win.cuh) runs on a recursive-bisection vertex order and a
+ * per-CTA shared-memory ring schedule. These host functions compute both from a CSR pattern on
+ * host arrays so the schedule's invariants can be checked without a device. sizes[6] = ring
+ * slots W, CTAs, blocks, loads, stages, max loads per block; blk holds 8 ints per block
+ * (row0, nrows, lbeg, nl, slot0, e0, e1, 0). GS_ERR_UNSUPPORTED: a row alone exceeds a block. */
+typedef struct gs_winplan gs_winplan;
+int gs_win_bisect_order_host(int n, const int* offs, const int* cols, int leaf, int* order);
+int gs_win_plan_host(int n, const int* offs, const int* cols, int row_bytes, int nctas,
+                     gs_winplan** out, int64_t* sizes);
+int gs_win_plan_arrays(const gs_winplan* p, int* blk, int* cta_blk, int* loads,
+                       unsigned short* slot, unsigned short* own);
+void gs_win_plan_destroy(gs_winplan* p);
+
 /* ---- dense baselines (the kNN benchmark's dense_sinkhorn_w1 / _w2 rows) ---- */
 /* dense_sinkhorn (transport.cpp:271-311): cost r x c row-major, mu (r), nu (c); outputs v (r),
  * w (c), cost, kl, iterations, converged, marginal_error. mem applies to every array. */

@@ -17,6 +17,7 @@
 
 #include "gs_internal.cuh"
 #include "gs_step.cuh"
+#include "gs_win.cuh"
 
 using namespace gsk;
 
@@ -632,6 +633,50 @@ void launch_step(gs_ctx* ctx, int gw, int rpc, const StepArgs& A, int mode) {
   gs_launch_end(ctx, 0);
 }
 
+// Windowed step kernel (gs_win.cuh) for wide rows: GS_WIN=0 turns it off (read per call).
+inline bool win_enabled() {
+  const char* e = getenv("GS_WIN");
+  return !(e && atoi(e) == 0);
+}
+
+template <typename S, int GW, int MODE>
+void launch_win_mode(const CUtensorMap& tm, const StepArgs& A, const WinArgs& WA, int G, cudaStream_t s) {
+  constexpr int smem = win_smem_bytes<S, GW>();
+  static bool attr = [] {
+    cudaFuncSetAttribute(k_cheb_win<S, GW, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return true;
+  }();
+  (void)attr;
+  k_cheb_win<S, GW, MODE><<<dim3((unsigned)(WA.nctas * G)), kWinThreads, smem, s>>>(tm, A, WA);
+}
+
+template <typename S, int GW>
+void launch_win_gw(const CUtensorMap& tm, const StepArgs& A, const WinArgs& WA, int G, int mode, cudaStream_t s) {
+  switch (mode) {
+    case MODE_NONE: launch_win_mode<S, GW, MODE_NONE>(tm, A, WA, G, s); break;
+    case MODE_SK_PSI: launch_win_mode<S, GW, MODE_SK_PSI>(tm, A, WA, G, s); break;
+    case MODE_SK_PHI: launch_win_mode<S, GW, MODE_SK_PHI>(tm, A, WA, G, s); break;
+    default: launch_win_mode<S, GW, MODE_BARY_PSI>(tm, A, WA, G, s); break;
+  }
+}
+
+template <typename S>
+void launch_step_win(gs_ctx* ctx, int gw, const CUtensorMap& tm, const StepArgs& A, const WinArgs& WA, int mode) {
+  gs_launch_begin(ctx, 0);
+  switch (gw) {
+    case 64: launch_win_gw<S, 64>(tm, A, WA, A.Gl, mode, ctx->stream); break;
+    case 32: launch_win_gw<S, 32>(tm, A, WA, A.Gl, mode, ctx->stream); break;
+    default: launch_win_gw<S, 16>(tm, A, WA, A.Gl, mode, ctx->stream); break;
+  }
+  gs_launch_end(ctx, 0);
+}
+
+// row sizes the windowed kernel takes: wide rows (16-byte lanes), GW >= 16
+template <typename S>
+bool win_row_ok(int gw) {
+  return gw >= 16 && gw * (int)sizeof(S) > GS_NARROW_MAX_BYTES;
+}
+
 // GS_BLK=1 runs wide fp64 rows through the 8-row block kernel (k_cheb_blk). Off by default:
 // it halves the gathered sectors (23.8M vs 49.7M per config-1 step) but doubles the
 // instructions (predicated per-record fold) at 88 registers, 238 vs 117 us.
@@ -746,6 +791,9 @@ struct Work {
   int lay = 0;  // filter layout: 0 for one-warp-per-row groups, 1 (degree-sorted) for narrower
   bool w1 = false;  // one-column fp64 problem small enough for the warp-per-row kernel
   bool blk = false;  // wide fp64 rows through the 8-row block kernel (k_cheb_blk)
+  bool win = false;  // wide rows through the windowed kernel (k_cheb_win, lay[2])
+  const gs_winsched* ws = nullptr;
+  alignas(64) CUtensorMap tmap[2];  // gather sources T[0], T[1] (win)
   struct TView {  // T[0], T[1]: halves of one allocation (one L2 access-policy window covers both)
     S* p = nullptr;
     S* get() const { return p; }
@@ -776,11 +824,26 @@ struct Work {
       GS_TRY(gs_build_block_records(ctx, const_cast<gs_filter*>(f), lay));
       blk = true;
       tiles = (n + kBlkRows * kBlkWarps - 1) / (kBlkRows * kBlkWarps);
+    } else if (f && ld_ < 0 && n > 0 && win_enabled() && win_row_ok<S>(GW)) {
+      const int rb = GW * (int)sizeof(S);
+      const int rc = gs_win_build(ctx, const_cast<gs_filter*>(f), rb);
+      if (rc == GS_OK) {
+        win = true;
+        ws = gs_win_get(f, rb);
+        lay = 2;
+        tiles = ws->nctas;
+        rpc = 1;
+      } else if (rc != GS_ERR_UNSUPPORTED) {
+        return rc;
+      }
     }
     const size_t len = (size_t)Bpad * (ld > 0 ? ld : 1);
     GS_CUDA(ctx, Tall.alloc(2 * len, s));
     T[0].p = Tall.get();
     T[1].p = Tall.get() + len;
+    if (win)
+      for (int h = 0; h < 2; ++h)
+        GS_TRY(gs_win_tensor_map(ctx, &tmap[h], T[h].p, (int64_t)G * ld, GW, (int)sizeof(S)));
     GS_CUDA(ctx, acc.alloc(len, s));
     GS_CUDA(ctx, cmin.alloc(Bpad, s));
     GS_CUDA(ctx, cmax.alloc(Bpad, s));
@@ -884,7 +947,18 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
   A.Vcur = Vcur;
   A.Wout = Wout;
   A.psi = w.psi64.get();
-  const bool seq = seq_groups() && w.G > 1;
+  WinArgs WA{};
+  if (w.win) {
+    WA.blk = static_cast<const WinBlk*>(w.ws->blk);
+    WA.cta_blk = w.ws->cta_blk;
+    WA.loads = w.ws->loads;
+    WA.slot = w.ws->slot;
+    WA.own = w.ws->own;
+    WA.offs = w.ws->offs_pad;
+    WA.W = w.ws->W;
+    WA.nctas = w.ws->nctas;
+  }
+  const bool seq = seq_groups() && w.G > 1 && !w.win;
   for (int g = 0; g < (seq ? w.G : 1); ++g) {
     if (seq) {
       A.g0 = g;
@@ -897,7 +971,8 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
       sched.step(f, K, k, A);
       A.Tprev = w.T[(a0 + k - 1) & 1].get();
       A.Tout = w.T[(a0 + k) & 1].get();
-      launch_step<S>(ctx, w.GW, w.rpc, A, k == K ? mode : MODE_NONE);
+      if (w.win) launch_step_win<S>(ctx, w.GW, w.tmap[(a0 + k - 1) & 1], A, WA, k == K ? mode : MODE_NONE);
+      else launch_step<S>(ctx, w.GW, w.rpc, A, k == K ? mode : MODE_NONE);
     }
   }
   return (a0 + K) & 1;
@@ -2088,6 +2163,8 @@ static int finish_layout(gs_ctx* ctx, gs_filter* f, int l) {
   cudaFree(Ly.vals32);
   Ly.vals32 = nullptr;
   Ly.near_frac = 1.0;
+  for (auto* w : Ly.win) gs_win_destroy(w);
+  Ly.win.clear();
   do {
     rc = gs_permute_graph(ctx, f->scaled, Ly.order, Ly.newpos, &Ly.perm);
     if (rc) break;
@@ -2181,6 +2258,7 @@ extern "C" void gs_filter_destroy(gs_filter* f) {
     cudaFree(Ly.vals32);
     cudaFree(Ly.rec_key);
     cudaFree(Ly.rec_val);
+    for (auto* w : Ly.win) gs_win_destroy(w);
   }
   cudaFree(f->d_coeffs);
   delete f;
@@ -2249,6 +2327,30 @@ extern "C" int gs_filter_set_order(gs_ctx* ctx, gs_filter* f, int layout, const 
     return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "gs_filter_set_order: order is not a permutation of 0..n-1");
   }
   return finish_layout(ctx, f, layout);
+}
+
+int gs_layout_from_order(gs_ctx* ctx, gs_filter* f, int l, const int* h_order) {
+  const int n = f->scaled->n;
+  gs_layout& Ly = f->lay[l];
+  cudaStream_t s = ctx->stream;
+  if (!Ly.order) {
+    GS_CUDA(ctx, cudaMalloc((void**)&Ly.order, ((size_t)n + 1) * sizeof(int)));
+    GS_CUDA(ctx, cudaMalloc((void**)&Ly.newpos, ((size_t)n + 1) * sizeof(int)));
+  }
+  if (n == 0) return finish_layout(ctx, f, l);
+  GS_CUDA(ctx, cudaMemcpyAsync(Ly.order, h_order, (size_t)n * sizeof(int), cudaMemcpyHostToDevice, s));
+  GS_CUDA(ctx, cudaMemsetAsync(Ly.newpos, 0xff, (size_t)n * sizeof(int), s));
+  DevBuf<int> bad;
+  GS_CUDA(ctx, bad.alloc(1, s));
+  GS_CUDA(ctx, cudaMemsetAsync(bad.get(), 0, sizeof(int), s));
+  gs_launch_begin(ctx, 1);
+  k_newpos_from_order<<<(n + 255) / 256, 256, 0, s>>>(Ly.order, n, Ly.newpos, bad.get());
+  gs_launch_end(ctx, 1);
+  int hb = 0;
+  GS_CUDA(ctx, cudaMemcpyAsync(&hb, bad.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  if (hb) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "layout order is not a permutation");
+  return finish_layout(ctx, f, l);
 }
 
 // heat.cpp:116-131

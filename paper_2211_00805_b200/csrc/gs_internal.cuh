@@ -65,6 +65,21 @@ struct gs_graph {
   int device = 0;
 };
 
+// Ring schedule of the windowed step kernel for one row size (gs_win.cu / gs_win.cuh).
+struct gs_winsched {
+  int row_bytes = 0;
+  bool ok = false;
+  int W = 0, nctas = 0, nblocks = 0;
+  int64_t nloads = 0;
+  double loads_per_entry = 0.0;  // neighbour-row loads per CSR entry (the gather model counts 1)
+  void* blk = nullptr;           // gsk::WinBlk[nblocks]
+  int* cta_blk = nullptr;        // nctas + 1
+  int* loads = nullptr;
+  unsigned short* slot = nullptr;
+  unsigned short* own = nullptr;
+  int* offs_pad = nullptr;
+};
+
 // One locality layout of the filter's operator (gs_reorder.cu): renumbered rows + fp32 copy.
 struct gs_layout {
   gs_graph* perm = nullptr;  // L_s with rows renumbered (entries kept in original column order)
@@ -77,13 +92,16 @@ struct gs_layout {
   // column, row), key = new column << 3 | row within the block
   int* rec_key = nullptr;
   double* rec_val = nullptr;
+  // lay[2] only: ring schedules of the windowed step kernel, one per row size (built on first use)
+  std::vector<gs_winsched*> win;
 };
 
 struct gs_filter {
   gs_graph* scaled = nullptr;   // L_s in the caller's vertex order (heat.hpp:47)
   // lay[0]: Cuthill-McKee order (wide batches, one warp per row);
-  // lay[1]: CM with degree-sorted windows (narrow batches, several rows per warp)
-  gs_layout lay[2];
+  // lay[1]: CM with degree-sorted windows (narrow batches, several rows per warp);
+  // lay[2]: recursive-bisection order for the windowed step kernel (built on first use)
+  gs_layout lay[3];
   double t = 0, t_eff = 0, scale = 1;
   int degree = 0, kind = 0;
   std::vector<double> coeffs;  // host mirror (heat.hpp:37)
@@ -186,5 +204,13 @@ int gs_group_width(int B);
 int gs_spmm_grouped(gs_ctx* ctx, const gs_graph* g, const double* x, double* y, int B);
 int gs_check_transport_inputs(gs_ctx* ctx, int n, const double* dmu, const double* dnu, const double* da,
                               int P, int max_iter, double tol);
+// windowed step kernel (gs_win.cu): build / look up the ring schedule of lay[2] for a row size
+// (GS_ERR_UNSUPPORTED when a row alone exceeds a block), free one, encode a gather tensor map
+int gs_win_build(gs_ctx* ctx, gs_filter* f, int row_bytes);
+const gs_winsched* gs_win_get(const gs_filter* f, int row_bytes);
+void gs_win_destroy(gs_winsched* w);
+int gs_win_tensor_map(gs_ctx* ctx, void* tmap, const void* base, int64_t rows, int row_elems, int elem_bytes);
+// layout l of f from a host order (order[new] = old): newpos, renumbered operator, fp32 copy
+int gs_layout_from_order(gs_ctx* ctx, gs_filter* f, int l, const int* h_order);
 int gs_csr_from_sorted_entries(gs_ctx* ctx, int n, int64_t m, const unsigned long long* d_keys,
                                const double* d_vals, bool check_dups, gs_graph** out);

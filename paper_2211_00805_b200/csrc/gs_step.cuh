@@ -550,6 +550,16 @@ __device__ __forceinline__ void cheb_row(const StepArgs& A, int g, int row, int 
 // The rest of a row's step once y = (L_s T_{k-1})[row] is known: the recurrence, the deferred
 // acc update and the stores / fused epilogue (row < A.n).
 template <typename S, int GW, int MODE>
+__device__ __forceinline__ void finish_row_ops(const StepArgs& A, int g, int row, int q,
+                                               const double (&y)[Lay<GW, S>::VEC],
+                                               double (&mn)[Lay<GW, S>::VEC],
+                                               double (&mx)[Lay<GW, S>::VEC],
+                                               double (&er)[Lay<GW, S>::VEC],
+                                               const S (&tps)[Lay<GW, S>::VEC],
+                                               const S (&t2s)[Lay<GW, S>::VEC],
+                                               const S (&a0s)[Lay<GW, S>::VEC]);
+
+template <typename S, int GW, int MODE>
 __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, int q,
                                            const double (&y)[Lay<GW, S>::VEC],
                                            double (&mn)[Lay<GW, S>::VEC],
@@ -558,7 +568,6 @@ __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, in
                                            int pre_stride, bool pre_tp) {
   using L = Lay<GW, S>;
   constexpr int VEC = L::VEC;
-  using P = Prec<S>;
   const size_t gbase = (size_t)g * A.ld * GW + q * VEC;
   const size_t idx = gbase + (size_t)row * GW;
   if (A.k == 0) {  // plain SpMM (sparse.cpp:85-99)
@@ -587,6 +596,25 @@ __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, in
     if (A.k >= 2) ld_vec_rw<S, VEC>(static_cast<const S*>(A.Tout) + idx, t2s);
     if (read_acc) ld_vec_rw<S, VEC>(static_cast<const S*>(A.acc) + idx, a0s);
   }
+  finish_row_ops<S, GW, MODE>(A, g, row, q, y, mn, mx, er, tps, t2s, a0s);
+}
+
+// The recurrence, the deferred acc update and the stores / fused epilogue of one row, from its
+// own-row operands T_{k-1}[row], T_{k-2}[row], acc[row] (storage words; k >= 1, row < A.n).
+template <typename S, int GW, int MODE>
+__device__ __forceinline__ void finish_row_ops(const StepArgs& A, int g, int row, int q,
+                                               const double (&y)[Lay<GW, S>::VEC],
+                                               double (&mn)[Lay<GW, S>::VEC],
+                                               double (&mx)[Lay<GW, S>::VEC],
+                                               double (&er)[Lay<GW, S>::VEC],
+                                               const S (&tps)[Lay<GW, S>::VEC],
+                                               const S (&t2s)[Lay<GW, S>::VEC],
+                                               const S (&a0s)[Lay<GW, S>::VEC]) {
+  using L = Lay<GW, S>;
+  constexpr int VEC = L::VEC;
+  using P = Prec<S>;
+  const size_t gbase = (size_t)g * A.ld * GW + q * VEC;
+  const size_t idx = gbase + (size_t)row * GW;
   double tp[VEC], t2[VEC], a0[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) {

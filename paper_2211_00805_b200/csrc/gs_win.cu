@@ -1,0 +1,360 @@
+// gs_win.cu -- host side of the windowed Chebyshev step (gs_win.cuh): the window layout's vertex
+// order (recursive BFS bisection), the per-CTA ring schedule, its device copy and the TMA tensor
+// maps of the Chebyshev vectors.
+//
+// Reference path: the layout only renumbers rows of L_s (heat.cpp:72-96's scaled Laplacian); every
+// row keeps its CSR entries in the original column order (gs_permute_graph), so the recurrence
+// (heat.cpp:121-130) and its fma chains are unchanged and results stay bit-identical.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "gs_internal.cuh"
+#include "gs_win.cuh"
+
+using gsk::WinBlk;
+
+namespace {
+
+// Recursive BFS bisection (graph only): each part is ordered by BFS from a pseudo-peripheral
+// vertex (two BFS sweeps; components one after another), split at the median, and both halves
+// recurse; parts of at most `leaf` vertices are emitted in their BFS order. Consecutive vertices
+// are then compact patches of the graph at every scale, so a CTA's contiguous range is a patch
+// and its row blocks reuse each other's neighbour rows (SURVEY §8(d) gather model).
+void bisect_order(int n, const int* offs, const int* cols, int leaf, std::vector<int>& order) {
+  order.clear();
+  order.reserve(n);
+  std::vector<int> seq(n), tmp(n), label(n, 0), vis(n, 0), queue(n);
+  std::iota(seq.begin(), seq.end(), 0);
+  int stamp = 0, next_label = 1;
+  struct Part { int b, e, lab; };
+  std::vector<Part> stack{{0, n, 0}};
+  auto bfs = [&](int src, int lab, int* out) {  // returns count; last vertex at out[count-1]
+    ++stamp;
+    int h = 0, t = 0;
+    queue[t++] = src;
+    vis[src] = stamp;
+    while (h < t) {
+      const int u = queue[h++];
+      for (int p = offs[u]; p < offs[u + 1]; ++p) {
+        const int v = cols[p];
+        if (label[v] == lab && vis[v] != stamp) {
+          vis[v] = stamp;
+          queue[t++] = v;
+        }
+      }
+    }
+    if (out) std::copy(queue.begin(), queue.begin() + t, out);
+    return t;
+  };
+  std::vector<int> placed(n, 0);
+  int place_stamp = 0;
+  while (!stack.empty()) {
+    const Part pt = stack.back();
+    stack.pop_back();
+    const int sz = pt.e - pt.b;
+    if (sz <= leaf) {
+      for (int i = pt.b; i < pt.e; ++i) order.push_back(seq[i]);
+      continue;
+    }
+    // BFS order of the part, component by component
+    ++place_stamp;
+    int w = pt.b;
+    for (int i = pt.b; i < pt.e; ++i) {
+      const int s0 = seq[i];
+      if (placed[s0] == place_stamp) continue;
+      int cnt = bfs(s0, pt.lab, nullptr);
+      int far = queue[cnt - 1];
+      cnt = bfs(far, pt.lab, nullptr);
+      far = queue[cnt - 1];
+      cnt = bfs(far, pt.lab, &tmp[w]);
+      for (int k = 0; k < cnt; ++k) placed[tmp[w + k]] = place_stamp;
+      w += cnt;
+    }
+    std::copy(tmp.begin() + pt.b, tmp.begin() + pt.e, seq.begin() + pt.b);
+    const int mid = pt.b + sz / 2;
+    const int l1 = next_label++, l2 = next_label++;
+    for (int i = pt.b; i < mid; ++i) label[seq[i]] = l1;
+    for (int i = mid; i < pt.e; ++i) label[seq[i]] = l2;
+    stack.push_back({mid, pt.e, l2});
+    stack.push_back({pt.b, mid, l1});
+  }
+}
+
+struct WinHost {
+  int W = 0, lmax = 0, nctas = 0;
+  std::vector<WinBlk> blk;
+  std::vector<int> cta_blk, loads;
+  std::vector<unsigned short> slot, own;
+  int64_t entries = 0;
+};
+
+// Ring schedule (see gs_win.cuh). Rows [bounds[c], bounds[c+1]) go to CTA c (weight-balanced:
+// entries + 2 per row). Positions count the CTA's loads; a load at position p lives in ring slot
+// p mod W until the load at p + W. A block b whose loads start at position P_b may reuse a
+// position p only if p >= P_b + kWinStages * LMAX - W: the producer runs at most kWinStages - 1
+// blocks ahead of the consumers, and a block loads at most LMAX rows, so no load issued while b
+// can still be read overwrites such a p. Returns false if one row alone exceeds LMAX loads or
+// EMAX entries (the caller keeps the register-gather kernel then).
+bool build_schedule(int n, const int* offs, const int* cols, int row_bytes, int rows_max, int nctas,
+                    WinHost& out) {
+  const int W = gsk::win_ring_slots(row_bytes);
+  // loads per block: a quarter of the ring with three stages (512-byte rows: 96 of 384 slots),
+  // so reuse reaches back at least W / 4 slots behind a block's first load
+  const int LMAX = std::max(4, std::min(gsk::kWinLmaxCap, (W / (gsk::kWinStages + 1)) & ~3));
+  const int EMAX = gsk::kWinEmax;
+  const int64_t lead = (int64_t)gsk::kWinStages * LMAX;
+  if (W < lead + 4 || nctas < 1) return false;
+  out.W = W;
+  out.lmax = LMAX;
+  out.nctas = nctas;
+  out.blk.clear();
+  out.loads.clear();
+  out.cta_blk.assign(nctas + 1, 0);
+  const int64_t nnz = offs[n];
+  out.entries = nnz;
+  out.slot.assign(nnz + 16, 0);
+  out.own.assign((size_t)n + 16, 0);
+  // weight-balanced contiguous ranges
+  std::vector<int> bounds(nctas + 1, n);
+  {
+    const int64_t total = nnz + 2 * (int64_t)n;
+    int r = 0;
+    int64_t acc = 0;
+    bounds[0] = 0;
+    for (int c = 1; c < nctas; ++c) {
+      const int64_t target = total * c / nctas;
+      while (r < n && acc + (offs[r + 1] - offs[r]) + 2 <= target) {
+        acc += (offs[r + 1] - offs[r]) + 2;
+        ++r;
+      }
+      bounds[c] = r;
+    }
+    bounds[nctas] = n;
+  }
+  std::vector<int64_t> last(n, INT64_MIN / 4);
+  std::vector<int> rstamp(n, 0);
+  int rs = 0;
+  int64_t base = 0;
+  std::vector<int> rownew;
+  std::vector<int> blkloads;
+  for (int c = 0; c < nctas; ++c) {
+    out.cta_blk[c] = (int)out.blk.size();
+    int64_t P = base;
+    int r = bounds[c];
+    const int rend = bounds[c + 1];
+    while (r < rend) {
+      const int64_t Pb = P, lo = Pb + lead - W;
+      blkloads.clear();
+      const int row0 = r;
+      int nrows = 0;
+      int64_t nent = 0;
+      while (r < rend && nrows < rows_max) {
+        const int deg = offs[r + 1] - offs[r];
+        ++rs;
+        rownew.clear();
+        auto consider = [&](int col) {
+          if (last[col] >= lo || rstamp[col] == rs) return;
+          rstamp[col] = rs;
+          rownew.push_back(col);
+        };
+        consider(r);
+        for (int p = offs[r]; p < offs[r + 1]; ++p) consider(cols[p]);
+        const int64_t nl = (int64_t)blkloads.size() + (int64_t)rownew.size();
+        if (nrows > 0 && (((nl + 3) & ~3LL) > LMAX || nent + deg > EMAX)) break;
+        if (((nl + 3) & ~3LL) > LMAX || deg > EMAX) return false;  // one row alone too big
+        for (int col : rownew) {
+          last[col] = Pb + (int64_t)blkloads.size();
+          blkloads.push_back(col);
+        }
+        for (int p = offs[r]; p < offs[r + 1]; ++p) out.slot[p] = (unsigned short)(last[cols[p]] % W);
+        out.own[r] = (unsigned short)(last[r] % W);
+        nent += deg;
+        ++nrows;
+        ++r;
+      }
+      const int nl = (int)((blkloads.size() + 3) & ~(size_t)3);
+      while ((int)blkloads.size() < nl) blkloads.push_back(blkloads.back());  // padding: a repeat
+      WinBlk b{};
+      b.row0 = row0;
+      b.nrows = nrows;
+      b.lbeg = (int)out.loads.size();
+      b.nl = nl;
+      b.slot0 = (int)(Pb % W);
+      b.e0 = offs[row0];
+      b.e1 = offs[row0 + nrows];
+      out.blk.push_back(b);
+      out.loads.insert(out.loads.end(), blkloads.begin(), blkloads.end());
+      P += nl;
+    }
+    base = ((P + W + 3) / 4) * 4;  // nothing loaded by an earlier CTA is ever reusable
+  }
+  out.cta_blk[nctas] = (int)out.blk.size();
+  if (out.loads.empty()) out.loads.assign(4, 0);
+  return true;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda at link time)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return (EncodeTiledFn)p;
+  }();
+  return fn;
+}
+
+}  // namespace
+
+// ---- engine-internal entry points (gs_internal.cuh) --------------------------------------------
+int gs_win_build(gs_ctx* ctx, gs_filter* f, int row_bytes) {
+  gs_layout& Ly = f->lay[2];
+  const int n = f->scaled->n;
+  if (row_bytes <= 0 || row_bytes > 1024 || (row_bytes & 15)) return GS_ERR_UNSUPPORTED;
+  const int key = row_bytes;
+  for (auto* w : Ly.win)
+    if (w->row_bytes == key) return w->ok ? GS_OK : GS_ERR_UNSUPPORTED;
+  cudaStream_t s = ctx->stream;
+  // host copy of the caller-order operator
+  std::vector<int> offs(n + 1), cols;
+  if (!Ly.perm) {
+    // window layout: recursive-bisection order of the scaled operator, renumbered on the device
+    GS_CUDA(ctx, cudaMemcpyAsync(offs.data(), f->scaled->offs, (size_t)(n + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+    GS_CUDA(ctx, cudaStreamSynchronize(s));
+    cols.resize(offs[n] > 0 ? offs[n] : 1);
+    if (offs[n] > 0)
+      GS_CUDA(ctx, cudaMemcpyAsync(cols.data(), f->scaled->cols, (size_t)offs[n] * sizeof(int), cudaMemcpyDeviceToHost, s));
+    GS_CUDA(ctx, cudaStreamSynchronize(s));
+    std::vector<int> order;
+    bisect_order(n, offs.data(), cols.data(), 32, order);
+    GS_TRY(gs_layout_from_order(ctx, f, 2, order.data()));
+  }
+  // host copy of the window layout's operator
+  const gs_graph* G = Ly.perm;
+  GS_CUDA(ctx, cudaMemcpyAsync(offs.data(), G->offs, (size_t)(n + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  cols.resize(offs[n] > 0 ? offs[n] : 1);
+  if (offs[n] > 0)
+    GS_CUDA(ctx, cudaMemcpyAsync(cols.data(), G->cols, (size_t)offs[n] * sizeof(int), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  const int rows_max = gsk::WinMeta<double>::ROWS_MAX;
+  gs_winsched* w = new gs_winsched();
+  w->row_bytes = key;
+  Ly.win.push_back(w);
+  WinHost h;
+  if (n == 0 || !build_schedule(n, offs.data(), cols.data(), row_bytes, rows_max, sms, h)) {
+    w->ok = false;
+    return GS_ERR_UNSUPPORTED;
+  }
+  w->W = h.W;
+  w->nctas = h.nctas;
+  w->nblocks = (int)h.blk.size();
+  w->nloads = (int64_t)h.loads.size();
+  w->loads_per_entry = h.entries ? (double)w->nloads / (double)h.entries : 0.0;
+  auto up = [&](void** dst, const void* src, size_t bytes) -> int {
+    GS_CUDA(ctx, cudaMalloc(dst, bytes ? bytes : 16));
+    if (bytes) GS_CUDA(ctx, cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+    return GS_OK;
+  };
+  std::vector<int> offs_pad(offs);
+  offs_pad.resize(n + 1 + 8, offs[n]);
+  GS_TRY(up((void**)&w->blk, h.blk.data(), h.blk.size() * sizeof(WinBlk)));
+  GS_TRY(up((void**)&w->cta_blk, h.cta_blk.data(), h.cta_blk.size() * sizeof(int)));
+  GS_TRY(up((void**)&w->loads, h.loads.data(), h.loads.size() * sizeof(int)));
+  GS_TRY(up((void**)&w->slot, h.slot.data(), h.slot.size() * sizeof(unsigned short)));
+  GS_TRY(up((void**)&w->own, h.own.data(), h.own.size() * sizeof(unsigned short)));
+  GS_TRY(up((void**)&w->offs_pad, offs_pad.data(), offs_pad.size() * sizeof(int)));
+  w->ok = true;
+  return GS_OK;
+}
+
+const gs_winsched* gs_win_get(const gs_filter* f, int row_bytes) {
+  for (auto* w : f->lay[2].win)
+    if (w->row_bytes == row_bytes && w->ok) return w;
+  return nullptr;
+}
+
+void gs_win_destroy(gs_winsched* w) {
+  if (!w) return;
+  cudaFree(w->blk);
+  cudaFree(w->cta_blk);
+  cudaFree(w->loads);
+  cudaFree(w->slot);
+  cudaFree(w->own);
+  cudaFree(w->offs_pad);
+  delete w;
+}
+
+// 2-D tensor map over `rows` rows of `row_elems` elements (fp64 or 32-bit words), box = one row:
+// the source of the tile::gather4 loads.
+int gs_win_tensor_map(gs_ctx* ctx, void* tmap, const void* base, int64_t rows, int row_elems, int elem_bytes) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)row_elems, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)row_elems * (cuuint64_t)elem_bytes};
+  cuuint32_t box[2] = {(cuuint32_t)row_elems, 1};
+  cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(reinterpret_cast<CUtensorMap*>(tmap),
+                        elem_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                        const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return GS_OK;
+}
+
+// ---- CPU test hooks (no device needed): the order and the schedule on host arrays ---------------
+extern "C" int gs_win_bisect_order_host(int n, const int* offs, const int* cols, int leaf, int* order) {
+  std::vector<int> o;
+  bisect_order(n, offs, cols, leaf, o);
+  std::copy(o.begin(), o.end(), order);
+  return GS_OK;
+}
+
+struct gs_winplan {
+  WinHost h;
+};
+
+extern "C" int gs_win_plan_host(int n, const int* offs, const int* cols, int row_bytes, int nctas,
+                                gs_winplan** out, int64_t* sizes /* W, nctas, blocks, loads, stages, lmax */) {
+  *out = nullptr;
+  const int rows_max = gsk::WinMeta<double>::ROWS_MAX;
+  gs_winplan* p = new gs_winplan();
+  if (!build_schedule(n, offs, cols, row_bytes, rows_max, nctas, p->h)) {
+    delete p;
+    return GS_ERR_UNSUPPORTED;
+  }
+  sizes[0] = p->h.W;
+  sizes[1] = p->h.nctas;
+  sizes[2] = (int64_t)p->h.blk.size();
+  sizes[3] = (int64_t)p->h.loads.size();
+  sizes[4] = gsk::kWinStages;
+  sizes[5] = p->h.lmax;
+  *out = p;
+  return GS_OK;
+}
+
+extern "C" int gs_win_plan_arrays(const gs_winplan* p, int* blk /* 8 per block */, int* cta_blk,
+                                  int* loads, unsigned short* slot, unsigned short* own) {
+  if (blk) memcpy(blk, p->h.blk.data(), p->h.blk.size() * sizeof(WinBlk));
+  if (cta_blk) memcpy(cta_blk, p->h.cta_blk.data(), p->h.cta_blk.size() * sizeof(int));
+  if (loads) memcpy(loads, p->h.loads.data(), p->h.loads.size() * sizeof(int));
+  if (slot) memcpy(slot, p->h.slot.data(), p->h.entries * sizeof(unsigned short));
+  if (own) memcpy(own, p->h.own.data(), (p->h.own.size() - 16) * sizeof(unsigned short));
+  return GS_OK;
+}
+
+extern "C" void gs_win_plan_destroy(gs_winplan* p) { delete p; }

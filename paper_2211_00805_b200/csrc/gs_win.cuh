@@ -1,0 +1,334 @@
+// gs_win.cuh -- the windowed Chebyshev step (k_cheb_win): neighbour rows of T_{k-1} staged in a
+// shared-memory window by TMA gathers, on a precomputed per-CTA schedule (gs_win.cu).
+//
+// Reference path: one step of HeatFilter::apply (proj/src/heat.cpp:121-130) over
+// SparseSymMatrix::multiply (proj/src/sparse.cpp:85-99); same per-row fma chain as k_cheb_step
+// (gs_step.cuh), so results are bit-identical to it and to the oracle.
+//
+// Why: k_cheb_step gathers every neighbour row through L1 (3 shuffles per CSR entry to broadcast
+// (col, val), ~45% L1 hit rate) and is bound by the L1tex data pipe and by the latency of the
+// dependent index -> gather chain. Here:
+//   * one persistent CTA per SM owns a contiguous range of rows of the window layout (a recursive
+//     BFS-bisection vertex order, so a range is a compact patch of the graph);
+//   * the range is cut into row blocks; for each block the schedule lists the neighbour rows that
+//     are not already in the CTA's shared-memory ring of W rows ("loads"), in groups of four;
+//   * a producer warp issues one `cp.async.bulk.tensor.2d.tile::gather4` per group (four
+//     512-byte rows per instruction into four consecutive ring slots) plus three bulk copies of
+//     the block's CSR values, ring-slot indices and row offsets, all on the block's mbarrier,
+//     `kWinStages` blocks ahead of the consumers;
+//   * consumer warps fold each row's entries in CSR order from the ring (broadcast LDS of the
+//     value and slot, LDS.128 of the row slice) -- no shuffles, no global gathers;
+//   * the own-row operands T_{k-2}[i] and acc[i] are read from global memory into registers at the
+//     start of the row; T_{k-1}[i] comes from the ring (every row's own vertex is scheduled);
+//   * ring-slot reuse is decided offline with the producer's lead bounded by kWinStages blocks, so
+//     a slot is never overwritten while a block that reads it may still be in flight.
+// On config 1 the bisection order brings the loads to ~0.12 per CSR entry (each neighbour row is
+// fetched ~1.6 times per step instead of once per entry).
+#pragma once
+
+#include <cuda.h>
+
+#include "gs_step.cuh"
+
+namespace gsk {
+
+struct WinBlk {  // one row block of the schedule (32 bytes)
+  int row0, nrows;  // rows [row0, row0 + nrows) of the window layout
+  int lbeg, nl;     // its loads: loads[lbeg .. lbeg + nl), nl % 4 == 0
+  int slot0;        // ring slot of its first load (consecutive slots, modulo W)
+  int e0, e1;       // CSR entry range of its rows
+  int pad;
+};
+
+#ifndef GS_WIN_WARPS
+#define GS_WIN_WARPS 16
+#endif
+#ifndef GS_WIN_STAGES
+#define GS_WIN_STAGES 3
+#endif
+#ifndef GS_WIN_EMAX
+#define GS_WIN_EMAX 640
+#endif
+#ifndef GS_WIN_LMAX_CAP
+#define GS_WIN_LMAX_CAP 256
+#endif
+#ifndef GS_WIN_RING_BYTES
+#define GS_WIN_RING_BYTES (192 * 1024)
+#endif
+constexpr int kWinWarps = GS_WIN_WARPS;    // consumer warps per CTA (+ one producer warp)
+constexpr int kWinStages = GS_WIN_STAGES;  // blocks in flight (producer lead + 1)
+constexpr int kWinEmax = GS_WIN_EMAX;      // CSR entries per block at most
+constexpr int kWinLmaxCap = GS_WIN_LMAX_CAP;  // loads per block at most (the plan: W / 4)
+constexpr int kWinRingBytes = GS_WIN_RING_BYTES;
+constexpr int kWinThreads = (kWinWarps + 1) * 32;
+
+__host__ __device__ constexpr int win_align16(int b) { return (b + 15) & ~15; }
+
+// Per-stage metadata area: values, slots, row offsets and own slots of one block.
+template <typename S>
+struct WinMeta {
+  static constexpr int VPAD = 16 / (int)sizeof(S);  // alignment slack of the value copy
+  static constexpr int VAL_BYTES = win_align16((kWinEmax + 2 * VPAD) * (int)sizeof(S));
+  static constexpr int SLOT_BYTES = win_align16((kWinEmax + 16) * 2);
+  static constexpr int ROWS_MAX = kWinWarps * 32;  // rows per block at most (one per lane)
+  static constexpr int OFF_BYTES = win_align16((ROWS_MAX + 8) * 4);
+  static constexpr int OWN_BYTES = win_align16((ROWS_MAX + 16) * 2);
+  static constexpr int BYTES = VAL_BYTES + SLOT_BYTES + OFF_BYTES + OWN_BYTES;
+};
+
+// ring slots for a row of `row_bytes` (multiple of 4, at most 65532)
+__host__ __device__ constexpr int win_ring_slots(int row_bytes) {
+  return ((kWinRingBytes / row_bytes) & ~3) > 65532 ? 65532 : ((kWinRingBytes / row_bytes) & ~3);
+}
+
+template <typename S, int GW>
+constexpr int win_smem_bytes() {
+  return win_ring_slots(GW * (int)sizeof(S)) * GW * (int)sizeof(S) + kWinStages * WinMeta<S>::BYTES +
+         2 * kWinStages * 8;
+}
+
+struct WinArgs {
+  const WinBlk* blk;
+  const int* cta_blk;            // [nctas + 1]: the CTA's blocks
+  const int* loads;              // row ids, groups of four
+  const unsigned short* slot;    // ring slot of every CSR entry (+16 padding)
+  const unsigned short* own;     // ring slot of every row's own T_{k-1} row (+16 padding)
+  const int* offs;               // the layout's row offsets (+8 padding for the aligned copies)
+  int W;                         // ring slots
+  int nctas;
+};
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* tm, int c0, int4 r,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w),
+      "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename S, int VEC>
+__device__ __forceinline__ void lds_vec(const S* p, S (&v)[VEC]) {
+  if constexpr (VEC * sizeof(S) == 16) {
+    if constexpr (sizeof(S) == 8) {
+      const double2 t = *reinterpret_cast<const double2*>(p);
+      v[0] = t.x;
+      v[1] = t.y;
+    } else {
+      const float4 t = *reinterpret_cast<const float4*>(p);
+      v[0] = t.x;
+      v[1] = t.y;
+      v[2] = t.z;
+      v[3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) v[e] = p[e];
+  }
+}
+
+// CTA fold of the epilogue partials (as block_epilogue, on a shared-memory area of
+// 3 * NWARPS * GW doubles aliased on the ring once every block is consumed).
+template <typename S, int GW, int MODE, int NWARPS>
+__device__ __forceinline__ void win_epilogue(const StepArgs& A, int g, int tile, int warp, int sub, int q,
+                                             double (&mn)[Lay<GW, S>::VEC], double (&mx)[Lay<GW, S>::VEC],
+                                             double (&er)[Lay<GW, S>::VEC], double* sm) {
+  using L = Lay<GW, S>;
+  constexpr int VEC = L::VEC, LPR = L::LPR;
+#pragma unroll
+  for (int off = LPR; off < 32; off <<= 1) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      mn[e] = fmin(mn[e], __shfl_xor_sync(0xffffffffu, mn[e], off));
+      mx[e] = fmax(mx[e], __shfl_xor_sync(0xffffffffu, mx[e], off));
+      er[e] = er[e] + __shfl_xor_sync(0xffffffffu, er[e], off);
+    }
+  }
+  double* s_mn = sm;
+  double* s_mx = sm + NWARPS * GW;
+  double* s_er = sm + 2 * NWARPS * GW;
+  if (sub == 0) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      s_mn[warp * GW + q * VEC + e] = mn[e];
+      s_mx[warp * GW + q * VEC + e] = mx[e];
+      s_er[warp * GW + q * VEC + e] = er[e];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < GW) {
+    const int c = threadIdx.x;
+    double a_mn = s_mn[c], a_mx = s_mx[c], a_er = s_er[c];
+    for (int w = 1; w < NWARPS; ++w) {
+      a_mn = fmin(a_mn, s_mn[w * GW + c]);
+      a_mx = fmax(a_mx, s_mx[w * GW + c]);
+      a_er = a_er + s_er[w * GW + c];
+    }
+    const int col = g * GW + c;
+    atomicMin(A.cs.cmin + col, dkey(a_mn));
+    if constexpr (MODE == MODE_SK_PSI || MODE == MODE_SK_PHI) atomicMax(A.cs.cmax + col, dkey(a_mx));
+    if constexpr (MODE == MODE_SK_PHI) A.cs.part_err[(size_t)tile * A.Bpad + col] = a_er;
+  }
+}
+
+// One Chebyshev step over the window layout. Grid: nctas x column groups; one CTA per SM.
+template <typename S, int GW, int MODE>
+__global__ void __launch_bounds__(kWinThreads, 1)
+    k_cheb_win(const __grid_constant__ CUtensorMap tmap, const StepArgs A, const WinArgs WA) {
+  using L = Lay<GW, S>;
+  using P = Prec<S>;
+  using M = WinMeta<S>;
+  constexpr int VEC = L::VEC, LPR = L::LPR, RPW = L::RPW;
+  constexpr int ROWB = GW * (int)sizeof(S);
+  constexpr int NST = kWinStages;
+  static_assert(VEC * (int)sizeof(S) == 16 || VEC * (int)sizeof(S) == 8, "8- or 16-byte lanes");
+  if (A.status && (A.status->error || A.status->done)) return;
+  const int cta = blockIdx.x % WA.nctas;
+  const int g = blockIdx.x / WA.nctas;
+  if (A.cs.gactive && A.cs.gactive[g] == 0) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int W = WA.W;
+  S* ring = reinterpret_cast<S*>(smem);
+  unsigned char* meta = smem + (size_t)W * ROWB;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(meta + NST * M::BYTES);
+  unsigned long long* empty = full + NST;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / LPR, q = lane % LPR;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWinWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int b0 = __ldg(WA.cta_blk + cta), b1 = __ldg(WA.cta_blk + cta + 1);
+  double mn[VEC], mx[VEC], er[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    mn[e] = INFINITY;
+    mx[e] = 0.0;
+    er[e] = 0.0;
+  }
+  const int64_t grow = (int64_t)g * A.ld;  // first tensor-map row of this column group
+  if (warp == kWinWarps) {
+    // ---------------- producer ----------------
+    for (int j = b0; j < b1; ++j) {
+      const int jj = j - b0, s = jj % NST;
+      if (jj >= NST) mbar_wait(&empty[s], (unsigned)(((jj / NST) - 1) & 1));
+      const WinBlk bk = WA.blk[j];
+      unsigned char* mt = meta + s * M::BYTES;
+      const int vb = bk.e0 & ~(M::VPAD - 1), sb = bk.e0 & ~7, ob = bk.row0 & ~3, wb = bk.row0 & ~7;
+      const unsigned vbytes = bk.e1 > bk.e0 ? (unsigned)win_align16((bk.e1 - vb) * (int)sizeof(S)) : 0u;
+      const unsigned sbytes = bk.e1 > bk.e0 ? (unsigned)win_align16((bk.e1 - sb) * 2) : 0u;
+      const unsigned obytes = (unsigned)win_align16((bk.row0 + bk.nrows + 1 - ob) * 4);
+      const unsigned wbytes = (unsigned)win_align16((bk.row0 + bk.nrows - wb) * 2);
+      if (lane == 0) {
+        mbar_expect_tx(&full[s], (unsigned)bk.nl * ROWB + vbytes + sbytes + obytes + wbytes);
+        if (vbytes) bulk_g2s(mt, static_cast<const S*>(A.vals) + vb, vbytes, &full[s]);
+        if (sbytes) bulk_g2s(mt + M::VAL_BYTES, WA.slot + sb, sbytes, &full[s]);
+        bulk_g2s(mt + M::VAL_BYTES + M::SLOT_BYTES, WA.offs + ob, obytes, &full[s]);
+        bulk_g2s(mt + M::VAL_BYTES + M::SLOT_BYTES + M::OFF_BYTES, WA.own + wb, wbytes, &full[s]);
+      }
+      __syncwarp();
+      const int ng = bk.nl >> 2;
+      for (int i = lane; i < ng; i += 32) {
+        int4 r = __ldg(reinterpret_cast<const int4*>(WA.loads + bk.lbeg) + i);
+        r.x += (int)grow;
+        r.y += (int)grow;
+        r.z += (int)grow;
+        r.w += (int)grow;
+        int slot = bk.slot0 + 4 * i;
+        if (slot >= W) slot -= W;
+        tma_gather4(ring + (size_t)slot * GW, &tmap, 0, r, &full[s]);
+      }
+    }
+  } else {
+    // ---------------- consumers ----------------
+    const size_t gbase = (size_t)g * A.ld * GW + q * VEC;
+    for (int j = b0; j < b1; ++j) {
+      const int jj = j - b0, s = jj % NST;
+      const WinBlk bk = WA.blk[j];
+      const unsigned char* mt = meta + s * M::BYTES;
+      const S* sv = reinterpret_cast<const S*>(mt) - (bk.e0 & ~(M::VPAD - 1));
+      const unsigned short* ss = reinterpret_cast<const unsigned short*>(mt + M::VAL_BYTES) - (bk.e0 & ~7);
+      const int* so = reinterpret_cast<const int*>(mt + M::VAL_BYTES + M::SLOT_BYTES) - (bk.row0 & ~3);
+      const unsigned short* sw =
+          reinterpret_cast<const unsigned short*>(mt + M::VAL_BYTES + M::SLOT_BYTES + M::OFF_BYTES) - (bk.row0 & ~7);
+      const int rend = bk.row0 + bk.nrows;
+      const bool read_acc = A.acc_terms > 0 && !A.acc_init;
+      bool waited = false;
+      for (int row = bk.row0 + warp * RPW + sub; row - sub < rend; row += kWinWarps * RPW) {
+        const bool valid = row < rend;
+        const size_t idx = gbase + (size_t)(valid ? row : 0) * GW;
+        // own-row operands from global memory (DRAM latency overlaps the fold)
+        S t2s[VEC], a0s[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          t2s[e] = S(0);
+          a0s[e] = S(0);
+        }
+        if (valid && A.k >= 2) ld_vec_rw<S, VEC>(static_cast<const S*>(A.Tout) + idx, t2s);
+        if (valid && read_acc) ld_vec_rw<S, VEC>(static_cast<const S*>(A.acc) + idx, a0s);
+        if (!waited) {
+          mbar_wait(&full[s], (unsigned)((jj / NST) & 1));
+          waited = true;
+        }
+        if (!valid) continue;
+        const int pb = so[row], pe = so[row + 1];
+        const S* rl = ring + q * VEC;
+        double y[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) y[e] = 0.0;
+        int p = pb;
+        for (; p + 4 <= pe; p += 4) {
+          S vv[4];
+          int sl[4];
+          S xx[4][VEC];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            vv[u] = sv[p + u];
+            sl[u] = ss[p + u];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) lds_vec<S, VEC>(rl + sl[u] * GW, xx[u]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) y[e] = P::fmat(P::val(vv[u]), P::dec(xx[u][e]), y[e]);
+        }
+        for (; p < pe; ++p) {
+          const S v = sv[p];
+          S x[VEC];
+          lds_vec<S, VEC>(rl + (int)ss[p] * GW, x);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) y[e] = P::fmat(P::val(v), P::dec(x[e]), y[e]);
+        }
+        if (A.k == 0) {  // plain SpMM
+          st_enc<S, VEC>(static_cast<S*>(A.Tout) + idx, y);
+          continue;
+        }
+        S tps[VEC];
+        lds_vec<S, VEC>(rl + (int)sw[row] * GW, tps);
+        finish_row_ops<S, GW, MODE>(A, g, row, q, y, mn, mx, er, tps, t2s, a0s);
+      }
+      if (!waited) mbar_wait(&full[s], (unsigned)((jj / NST) & 1));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+  }
+  if constexpr (MODE != MODE_NONE) {
+    __syncthreads();  // every block consumed: the ring is free for the fold
+    win_epilogue<S, GW, MODE, kWinWarps + 1>(A, g, cta, warp, sub, q, mn, mx, er,
+                                              reinterpret_cast<double*>(smem));
+  }
+}
+
+}  // namespace gsk
