@@ -121,14 +121,16 @@ int gs_filter_set_order(gs_ctx* ctx, gs_filter* f, int layout, const int* order,
 /* ---- windowed step kernel: host-side plan (engine internals, exposed for CPU tests) -------
  * The wide-row Chebyshev step (gs_win.cuh) runs on a recursive-bisection vertex order and a
  * per-CTA shared-memory ring schedule. These host functions compute both from a CSR pattern on
- * host arrays so the schedule's invariants can be checked without a device. sizes[6] = ring
- * slots W, CTAs, blocks, loads, stages, max loads per block; blk holds 8 ints per block
- * (row0, nrows, lbeg, nl, slot0, e0, e1, 0). GS_ERR_UNSUPPORTED: a row alone exceeds a block. */
+ * host arrays so the schedule's invariants can be checked without a device. sizes[7] = ring
+ * slots W, CTAs, blocks, loads, stages, max loads per block, padded entries; blk holds 8 ints
+ * per block (row0, nrows, lbeg, nl, slot0, e0, e1, 0) with e0/e1 in the quad-padded CSR whose
+ * row starts are poffs[r] & ~3 (poffs[r] & 3 = padding entries of row r); slot is indexed by
+ * padded entry. GS_ERR_UNSUPPORTED: a row alone exceeds a block. */
 typedef struct gs_winplan gs_winplan;
 int gs_win_bisect_order_host(int n, const int* offs, const int* cols, int leaf, int* order);
 int gs_win_plan_host(int n, const int* offs, const int* cols, int row_bytes, int nctas,
                      gs_winplan** out, int64_t* sizes);
-int gs_win_plan_arrays(const gs_winplan* p, int* blk, int* cta_blk, int* loads,
+int gs_win_plan_arrays(const gs_winplan* p, int* blk, int* cta_blk, int* loads, int* poffs,
                        unsigned short* slot, unsigned short* own);
 void gs_win_plan_destroy(gs_winplan* p);
 

@@ -43,7 +43,7 @@ class GsComm(C.Structure):
 SIGNATURES = {
     "gs_win_bisect_order_host": (_i, [_i, _vp, _vp, _i, _vp]),
     "gs_win_plan_host": (_i, [_i, _vp, _vp, _i, _i, _pvp, _vp]),
-    "gs_win_plan_arrays": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "gs_win_plan_arrays": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "gs_win_plan_destroy": (None, [_vp]),
     "gs_ctx_create": (_i, [_i, _pvp]),
     "gs_ctx_destroy": (None, [_vp]),

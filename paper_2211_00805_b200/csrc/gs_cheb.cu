@@ -826,10 +826,10 @@ struct Work {
       tiles = (n + kBlkRows * kBlkWarps - 1) / (kBlkRows * kBlkWarps);
     } else if (f && ld_ < 0 && n > 0 && win_enabled() && win_row_ok<S>(GW)) {
       const int rb = GW * (int)sizeof(S);
-      const int rc = gs_win_build(ctx, const_cast<gs_filter*>(f), rb);
+      const int rc = gs_win_build(ctx, const_cast<gs_filter*>(f), rb, (int)sizeof(S));
       if (rc == GS_OK) {
         win = true;
-        ws = gs_win_get(f, rb);
+        ws = gs_win_get(f, rb, (int)sizeof(S));
         lay = 2;
         tiles = ws->nctas;
         rpc = 1;
@@ -954,7 +954,8 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
     WA.loads = w.ws->loads;
     WA.slot = w.ws->slot;
     WA.own = w.ws->own;
-    WA.offs = w.ws->offs_pad;
+    WA.poffs = w.ws->poffs;
+    WA.pvals = w.ws->pvals;
     WA.W = w.ws->W;
     WA.nctas = w.ws->nctas;
   }

@@ -77,7 +77,9 @@ struct gs_winsched {
   int* loads = nullptr;
   unsigned short* slot = nullptr;
   unsigned short* own = nullptr;
-  int* offs_pad = nullptr;
+  int* poffs = nullptr;    // rows padded to whole quads (gs_win.cuh WinArgs::poffs)
+  void* pvals = nullptr;   // padded values (fp64, or fp32 for the 32-bit mode's row size)
+  int64_t padded = 0;
 };
 
 // One locality layout of the filter's operator (gs_reorder.cu): renumbered rows + fp32 copy.
@@ -206,8 +208,8 @@ int gs_check_transport_inputs(gs_ctx* ctx, int n, const double* dmu, const doubl
                               int P, int max_iter, double tol);
 // windowed step kernel (gs_win.cu): build / look up the ring schedule of lay[2] for a row size
 // (GS_ERR_UNSUPPORTED when a row alone exceeds a block), free one, encode a gather tensor map
-int gs_win_build(gs_ctx* ctx, gs_filter* f, int row_bytes);
-const gs_winsched* gs_win_get(const gs_filter* f, int row_bytes);
+int gs_win_build(gs_ctx* ctx, gs_filter* f, int row_bytes, int elem_bytes);
+const gs_winsched* gs_win_get(const gs_filter* f, int row_bytes, int elem_bytes);
 void gs_win_destroy(gs_winsched* w);
 int gs_win_tensor_map(gs_ctx* ctx, void* tmap, const void* base, int64_t rows, int row_elems, int elem_bytes);
 // layout l of f from a host order (order[new] = old): newpos, renumbered operator, fp32 copy

@@ -89,8 +89,9 @@ struct WinHost {
   int W = 0, lmax = 0, nctas = 0;
   std::vector<WinBlk> blk;
   std::vector<int> cta_blk, loads;
+  std::vector<int> poffs;  // padded row starts + padding count (gs_win.cuh WinArgs::poffs)
   std::vector<unsigned short> slot, own;
-  int64_t entries = 0;
+  int64_t entries = 0, padded = 0;
 };
 
 // Ring schedule (see gs_win.cuh). Rows [bounds[c], bounds[c+1]) go to CTA c (weight-balanced:
@@ -117,19 +118,27 @@ bool build_schedule(int n, const int* offs, const int* cols, int row_bytes, int 
   out.cta_blk.assign(nctas + 1, 0);
   const int64_t nnz = offs[n];
   out.entries = nnz;
-  out.slot.assign(nnz + 16, 0);
+  // every row padded to whole quads
+  std::vector<int64_t> pstart(n + 1, 0);
+  for (int r = 0; r < n; ++r) pstart[r + 1] = pstart[r] + (((int64_t)(offs[r + 1] - offs[r]) + 3) & ~3LL);
+  if (pstart[n] >= INT32_MAX) return false;
+  out.padded = pstart[n];
+  out.poffs.assign((size_t)n + 1 + 8, (int)pstart[n]);
+  for (int r = 0; r < n; ++r)
+    out.poffs[r] = (int)pstart[r] + (int)((pstart[r + 1] - pstart[r]) - (offs[r + 1] - offs[r]));
+  out.slot.assign(pstart[n] + 16, 0);
   out.own.assign((size_t)n + 16, 0);
   // weight-balanced contiguous ranges
   std::vector<int> bounds(nctas + 1, n);
   {
-    const int64_t total = nnz + 2 * (int64_t)n;
+    const int64_t total = pstart[n] + 2 * (int64_t)n;
     int r = 0;
     int64_t acc = 0;
     bounds[0] = 0;
     for (int c = 1; c < nctas; ++c) {
       const int64_t target = total * c / nctas;
-      while (r < n && acc + (offs[r + 1] - offs[r]) + 2 <= target) {
-        acc += (offs[r + 1] - offs[r]) + 2;
+      while (r < n && acc + (pstart[r + 1] - pstart[r]) + 2 <= target) {
+        acc += (pstart[r + 1] - pstart[r]) + 2;
         ++r;
       }
       bounds[c] = r;
@@ -154,7 +163,7 @@ bool build_schedule(int n, const int* offs, const int* cols, int row_bytes, int 
       int nrows = 0;
       int64_t nent = 0;
       while (r < rend && nrows < rows_max) {
-        const int deg = offs[r + 1] - offs[r];
+        const int deg = (int)(pstart[r + 1] - pstart[r]);  // padded
         ++rs;
         rownew.clear();
         auto consider = [&](int col) {
@@ -171,7 +180,8 @@ bool build_schedule(int n, const int* offs, const int* cols, int row_bytes, int 
           last[col] = Pb + (int64_t)blkloads.size();
           blkloads.push_back(col);
         }
-        for (int p = offs[r]; p < offs[r + 1]; ++p) out.slot[p] = (unsigned short)(last[cols[p]] % W);
+        for (int p = offs[r]; p < offs[r + 1]; ++p)
+          out.slot[pstart[r] + (p - offs[r])] = (unsigned short)(last[cols[p]] % W);
         out.own[r] = (unsigned short)(last[r] % W);
         nent += deg;
         ++nrows;
@@ -185,8 +195,8 @@ bool build_schedule(int n, const int* offs, const int* cols, int row_bytes, int 
       b.lbeg = (int)out.loads.size();
       b.nl = nl;
       b.slot0 = (int)(Pb % W);
-      b.e0 = offs[row0];
-      b.e1 = offs[row0 + nrows];
+      b.e0 = (int)pstart[row0];
+      b.e1 = (int)pstart[row0 + nrows];
       out.blk.push_back(b);
       out.loads.insert(out.loads.end(), blkloads.begin(), blkloads.end());
       P += nl;
@@ -217,12 +227,21 @@ EncodeTiledFn encode_fn() {
 
 }  // namespace
 
+template <typename S>
+__global__ void k_win_pad_vals(int n, const int* __restrict__ offs, const S* __restrict__ vals,
+                               const int* __restrict__ poffs, S* __restrict__ pvals) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int p0 = offs[r], deg = offs[r + 1] - p0, q0 = poffs[r] & ~3, qe = poffs[r + 1] & ~3;
+  for (int i = 0; i < qe - q0; ++i) pvals[q0 + i] = i < deg ? vals[p0 + i] : S(0);
+}
+
 // ---- engine-internal entry points (gs_internal.cuh) --------------------------------------------
-int gs_win_build(gs_ctx* ctx, gs_filter* f, int row_bytes) {
+int gs_win_build(gs_ctx* ctx, gs_filter* f, int row_bytes, int elem_bytes) {
   gs_layout& Ly = f->lay[2];
   const int n = f->scaled->n;
   if (row_bytes <= 0 || row_bytes > 1024 || (row_bytes & 15)) return GS_ERR_UNSUPPORTED;
-  const int key = row_bytes;
+  const int key = row_bytes * 16 + elem_bytes;
   for (auto* w : Ly.win)
     if (w->row_bytes == key) return w->ok ? GS_OK : GS_ERR_UNSUPPORTED;
   cudaStream_t s = ctx->stream;
@@ -269,21 +288,29 @@ int gs_win_build(gs_ctx* ctx, gs_filter* f, int row_bytes) {
     if (bytes) GS_CUDA(ctx, cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
     return GS_OK;
   };
-  std::vector<int> offs_pad(offs);
-  offs_pad.resize(n + 1 + 8, offs[n]);
   GS_TRY(up((void**)&w->blk, h.blk.data(), h.blk.size() * sizeof(WinBlk)));
   GS_TRY(up((void**)&w->cta_blk, h.cta_blk.data(), h.cta_blk.size() * sizeof(int)));
   GS_TRY(up((void**)&w->loads, h.loads.data(), h.loads.size() * sizeof(int)));
   GS_TRY(up((void**)&w->slot, h.slot.data(), h.slot.size() * sizeof(unsigned short)));
   GS_TRY(up((void**)&w->own, h.own.data(), h.own.size() * sizeof(unsigned short)));
-  GS_TRY(up((void**)&w->offs_pad, offs_pad.data(), offs_pad.size() * sizeof(int)));
+  GS_TRY(up((void**)&w->poffs, h.poffs.data(), h.poffs.size() * sizeof(int)));
+  w->padded = h.padded;
+  GS_CUDA(ctx, cudaMalloc(&w->pvals, (size_t)(h.padded + 8) * elem_bytes));
+  GS_CUDA(ctx, cudaMemsetAsync(w->pvals, 0, (size_t)(h.padded + 8) * elem_bytes, s));
+  gs_launch_begin(ctx, 1);
+  if (elem_bytes == 8)
+    k_win_pad_vals<double><<<(n + 255) / 256, 256, 0, s>>>(n, G->offs, G->vals, w->poffs, (double*)w->pvals);
+  else
+    k_win_pad_vals<float><<<(n + 255) / 256, 256, 0, s>>>(n, G->offs, Ly.vals32, w->poffs, (float*)w->pvals);
+  gs_launch_end(ctx, 1);
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
   w->ok = true;
   return GS_OK;
 }
 
-const gs_winsched* gs_win_get(const gs_filter* f, int row_bytes) {
+const gs_winsched* gs_win_get(const gs_filter* f, int row_bytes, int elem_bytes) {
   for (auto* w : f->lay[2].win)
-    if (w->row_bytes == row_bytes && w->ok) return w;
+    if (w->row_bytes == row_bytes * 16 + elem_bytes && w->ok) return w;
   return nullptr;
 }
 
@@ -294,7 +321,8 @@ void gs_win_destroy(gs_winsched* w) {
   cudaFree(w->loads);
   cudaFree(w->slot);
   cudaFree(w->own);
-  cudaFree(w->offs_pad);
+  cudaFree(w->poffs);
+  cudaFree(w->pvals);
   delete w;
 }
 
@@ -343,16 +371,18 @@ extern "C" int gs_win_plan_host(int n, const int* offs, const int* cols, int row
   sizes[3] = (int64_t)p->h.loads.size();
   sizes[4] = gsk::kWinStages;
   sizes[5] = p->h.lmax;
+  sizes[6] = p->h.padded;
   *out = p;
   return GS_OK;
 }
 
 extern "C" int gs_win_plan_arrays(const gs_winplan* p, int* blk /* 8 per block */, int* cta_blk,
-                                  int* loads, unsigned short* slot, unsigned short* own) {
+                                  int* loads, int* poffs, unsigned short* slot, unsigned short* own) {
   if (blk) memcpy(blk, p->h.blk.data(), p->h.blk.size() * sizeof(WinBlk));
   if (cta_blk) memcpy(cta_blk, p->h.cta_blk.data(), p->h.cta_blk.size() * sizeof(int));
   if (loads) memcpy(loads, p->h.loads.data(), p->h.loads.size() * sizeof(int));
-  if (slot) memcpy(slot, p->h.slot.data(), p->h.entries * sizeof(unsigned short));
+  if (poffs) memcpy(poffs, p->h.poffs.data(), (p->h.poffs.size() - 8) * sizeof(int));
+  if (slot) memcpy(slot, p->h.slot.data(), p->h.padded * sizeof(unsigned short));
   if (own) memcpy(own, p->h.own.data(), (p->h.own.size() - 16) * sizeof(unsigned short));
   return GS_OK;
 }

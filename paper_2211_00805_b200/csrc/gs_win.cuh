@@ -64,13 +64,15 @@ constexpr int kWinThreads = (kWinWarps + 1) * 32;
 
 __host__ __device__ constexpr int win_align16(int b) { return (b + 15) & ~15; }
 
-// Per-stage metadata area: values, slots, row offsets and own slots of one block.
+// Per-stage metadata area: values, slots, row offsets and own slots of one block. The schedule's
+// CSR copy pads every row to a multiple of four entries ("quads"), so a consumer reads four
+// values with one or two broadcast LDS.128 and four ring slots with one LDS.64.
+constexpr int kWinRowsMax = 256;  // rows per block at most
 template <typename S>
 struct WinMeta {
-  static constexpr int VPAD = 16 / (int)sizeof(S);  // alignment slack of the value copy
-  static constexpr int VAL_BYTES = win_align16((kWinEmax + 2 * VPAD) * (int)sizeof(S));
+  static constexpr int VAL_BYTES = win_align16((kWinEmax + 8) * (int)sizeof(S));
   static constexpr int SLOT_BYTES = win_align16((kWinEmax + 16) * 2);
-  static constexpr int ROWS_MAX = kWinWarps * 32;  // rows per block at most (one per lane)
+  static constexpr int ROWS_MAX = kWinRowsMax;
   static constexpr int OFF_BYTES = win_align16((ROWS_MAX + 8) * 4);
   static constexpr int OWN_BYTES = win_align16((ROWS_MAX + 16) * 2);
   static constexpr int BYTES = VAL_BYTES + SLOT_BYTES + OFF_BYTES + OWN_BYTES;
@@ -91,9 +93,12 @@ struct WinArgs {
   const WinBlk* blk;
   const int* cta_blk;            // [nctas + 1]: the CTA's blocks
   const int* loads;              // row ids, groups of four
-  const unsigned short* slot;    // ring slot of every CSR entry (+16 padding)
+  // the layout's CSR with every row padded to whole quads: poffs[r] = padded start of row r
+  // (a multiple of 4) + the row's number of padding entries (0..3)
+  const int* poffs;              // n + 1 (+8 padding for the aligned copies)
+  const void* pvals;             // values (S), padding entries 0
+  const unsigned short* slot;    // ring slot of every padded entry (+16 padding)
   const unsigned short* own;     // ring slot of every row's own T_{k-1} row (+16 padding)
-  const int* offs;               // the layout's row offsets (+8 padding for the aligned copies)
   int W;                         // ring slots
   int nctas;
 };
@@ -225,16 +230,17 @@ __global__ void __launch_bounds__(kWinThreads, 1)
       if (jj >= NST) mbar_wait(&empty[s], (unsigned)(((jj / NST) - 1) & 1));
       const WinBlk bk = WA.blk[j];
       unsigned char* mt = meta + s * M::BYTES;
-      const int vb = bk.e0 & ~(M::VPAD - 1), sb = bk.e0 & ~7, ob = bk.row0 & ~3, wb = bk.row0 & ~7;
-      const unsigned vbytes = bk.e1 > bk.e0 ? (unsigned)win_align16((bk.e1 - vb) * (int)sizeof(S)) : 0u;
+      // e0, e1: padded entry range (multiples of 4)
+      const int sb = bk.e0 & ~7, ob = bk.row0 & ~3, wb = bk.row0 & ~7;
+      const unsigned vbytes = (unsigned)((bk.e1 - bk.e0) * (int)sizeof(S));
       const unsigned sbytes = bk.e1 > bk.e0 ? (unsigned)win_align16((bk.e1 - sb) * 2) : 0u;
       const unsigned obytes = (unsigned)win_align16((bk.row0 + bk.nrows + 1 - ob) * 4);
       const unsigned wbytes = (unsigned)win_align16((bk.row0 + bk.nrows - wb) * 2);
       if (lane == 0) {
         mbar_expect_tx(&full[s], (unsigned)bk.nl * ROWB + vbytes + sbytes + obytes + wbytes);
-        if (vbytes) bulk_g2s(mt, static_cast<const S*>(A.vals) + vb, vbytes, &full[s]);
+        if (vbytes) bulk_g2s(mt, static_cast<const S*>(WA.pvals) + bk.e0, vbytes, &full[s]);
         if (sbytes) bulk_g2s(mt + M::VAL_BYTES, WA.slot + sb, sbytes, &full[s]);
-        bulk_g2s(mt + M::VAL_BYTES + M::SLOT_BYTES, WA.offs + ob, obytes, &full[s]);
+        bulk_g2s(mt + M::VAL_BYTES + M::SLOT_BYTES, WA.poffs + ob, obytes, &full[s]);
         bulk_g2s(mt + M::VAL_BYTES + M::SLOT_BYTES + M::OFF_BYTES, WA.own + wb, wbytes, &full[s]);
       }
       __syncwarp();
@@ -252,51 +258,83 @@ __global__ void __launch_bounds__(kWinThreads, 1)
     }
   } else {
     // ---------------- consumers ----------------
+    // Rows go round-robin over the CTA's (warp, lane group) slots across the whole range, so
+    // every slot gets the same number of rows whatever the block sizes; a lane group's next row
+    // is known ahead, so its T_{k-2} and acc rows are loaded one row early (DRAM latency hidden
+    // behind the current row's fold).
     const size_t gbase = (size_t)g * A.ld * GW + q * VEC;
+    constexpr int NSLOT = kWinWarps * RPW;
+    const int R0 = b1 > b0 ? WA.blk[b0].row0 : 0;
+    const int R1 = b1 > b0 ? WA.blk[b1 - 1].row0 + WA.blk[b1 - 1].nrows : 0;
+    const bool read_acc = A.acc_terms > 0 && !A.acc_init;
+    const bool read_t2 = A.k >= 2;
+    int r = R0 + warp * RPW + sub;
+    S t2s[VEC], a0s[VEC];
+    auto own_ops = [&](int row, S (&t2)[VEC], S (&a0)[VEC]) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        t2[e] = S(0);
+        a0[e] = S(0);
+      }
+      if (row < R1) {
+        const size_t idx = gbase + (size_t)row * GW;
+        if (read_t2) ld_vec_rw<S, VEC>(static_cast<const S*>(A.Tout) + idx, t2);
+        if (read_acc) ld_vec_rw<S, VEC>(static_cast<const S*>(A.acc) + idx, a0);
+      }
+    };
+    own_ops(r, t2s, a0s);
     for (int j = b0; j < b1; ++j) {
       const int jj = j - b0, s = jj % NST;
       const WinBlk bk = WA.blk[j];
       const unsigned char* mt = meta + s * M::BYTES;
-      const S* sv = reinterpret_cast<const S*>(mt) - (bk.e0 & ~(M::VPAD - 1));
+      const S* sv = reinterpret_cast<const S*>(mt) - bk.e0;
       const unsigned short* ss = reinterpret_cast<const unsigned short*>(mt + M::VAL_BYTES) - (bk.e0 & ~7);
       const int* so = reinterpret_cast<const int*>(mt + M::VAL_BYTES + M::SLOT_BYTES) - (bk.row0 & ~3);
       const unsigned short* sw =
           reinterpret_cast<const unsigned short*>(mt + M::VAL_BYTES + M::SLOT_BYTES + M::OFF_BYTES) - (bk.row0 & ~7);
       const int rend = bk.row0 + bk.nrows;
-      const bool read_acc = A.acc_terms > 0 && !A.acc_init;
-      bool waited = false;
-      for (int row = bk.row0 + warp * RPW + sub; row - sub < rend; row += kWinWarps * RPW) {
-        const bool valid = row < rend;
-        const size_t idx = gbase + (size_t)(valid ? row : 0) * GW;
-        // own-row operands from global memory (DRAM latency overlaps the fold)
-        S t2s[VEC], a0s[VEC];
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          t2s[e] = S(0);
-          a0s[e] = S(0);
-        }
-        if (valid && A.k >= 2) ld_vec_rw<S, VEC>(static_cast<const S*>(A.Tout) + idx, t2s);
-        if (valid && read_acc) ld_vec_rw<S, VEC>(static_cast<const S*>(A.acc) + idx, a0s);
-        if (!waited) {
-          mbar_wait(&full[s], (unsigned)((jj / NST) & 1));
-          waited = true;
-        }
-        if (!valid) continue;
-        const int pb = so[row], pe = so[row + 1];
+      mbar_wait(&full[s], (unsigned)((jj / NST) & 1));
+      while (r < rend) {
+        const int row = r;
+        r += NSLOT;
+        S t2n[VEC], a0n[VEC];
+        own_ops(r, t2n, a0n);  // next row's operands in flight during this row
+        const int pr = so[row], pn = so[row + 1];
+        const int qe = pn & ~3, npad = pr & 3;
         const S* rl = ring + q * VEC;
         double y[VEC];
 #pragma unroll
         for (int e = 0; e < VEC; ++e) y[e] = 0.0;
-        int p = pb;
-        for (; p + 4 <= pe; p += 4) {
+        // quads of the padded row: the fma chain runs over the real entries in CSR order; full
+        // quads first, then the row's last quad with its 1..3 real entries
+        auto quad_meta = [&](int p, S (&vv)[4], int (&sl)[4]) {
+          if constexpr (sizeof(S) == 8) {
+            const double2 v01 = *reinterpret_cast<const double2*>(sv + p);
+            const double2 v23 = *reinterpret_cast<const double2*>(sv + p + 2);
+            vv[0] = v01.x;
+            vv[1] = v01.y;
+            vv[2] = v23.x;
+            vv[3] = v23.y;
+          } else {
+            const float4 v4 = *reinterpret_cast<const float4*>(sv + p);
+            vv[0] = v4.x;
+            vv[1] = v4.y;
+            vv[2] = v4.z;
+            vv[3] = v4.w;
+          }
+          const uint2 s4 = *reinterpret_cast<const uint2*>(ss + p);
+          sl[0] = (int)(s4.x & 0xffffu);
+          sl[1] = (int)(s4.x >> 16);
+          sl[2] = (int)(s4.y & 0xffffu);
+          sl[3] = (int)(s4.y >> 16);
+        };
+        const int pf = npad ? qe - 4 : qe;  // end of the full quads
+        int p = pr & ~3;
+        for (; p < pf; p += 4) {
           S vv[4];
           int sl[4];
+          quad_meta(p, vv, sl);
           S xx[4][VEC];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            vv[u] = sv[p + u];
-            sl[u] = ss[p + u];
-          }
 #pragma unroll
           for (int u = 0; u < 4; ++u) lds_vec<S, VEC>(rl + sl[u] * GW, xx[u]);
 #pragma unroll
@@ -304,22 +342,35 @@ __global__ void __launch_bounds__(kWinThreads, 1)
 #pragma unroll
             for (int e = 0; e < VEC; ++e) y[e] = P::fmat(P::val(vv[u]), P::dec(xx[u][e]), y[e]);
         }
-        for (; p < pe; ++p) {
-          const S v = sv[p];
-          S x[VEC];
-          lds_vec<S, VEC>(rl + (int)ss[p] * GW, x);
+        if (npad) {
+          S vv[4];
+          int sl[4];
+          quad_meta(p, vv, sl);
+          const int cnt = 4 - npad;
+          S xx[3][VEC];
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) y[e] = P::fmat(P::val(v), P::dec(x[e]), y[e]);
+          for (int u = 0; u < 3; ++u)
+            if (u < cnt) lds_vec<S, VEC>(rl + sl[u] * GW, xx[u]);
+#pragma unroll
+          for (int u = 0; u < 3; ++u)
+            if (u < cnt)
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) y[e] = P::fmat(P::val(vv[u]), P::dec(xx[u][e]), y[e]);
         }
+        const size_t idx = gbase + (size_t)row * GW;
         if (A.k == 0) {  // plain SpMM
           st_enc<S, VEC>(static_cast<S*>(A.Tout) + idx, y);
-          continue;
+        } else {
+          S tps[VEC];
+          lds_vec<S, VEC>(rl + (int)sw[row] * GW, tps);
+          finish_row_ops<S, GW, MODE>(A, g, row, q, y, mn, mx, er, tps, t2s, a0s);
         }
-        S tps[VEC];
-        lds_vec<S, VEC>(rl + (int)sw[row] * GW, tps);
-        finish_row_ops<S, GW, MODE>(A, g, row, q, y, mn, mx, er, tps, t2s, a0s);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          t2s[e] = t2n[e];
+          a0s[e] = a0n[e];
+        }
       }
-      if (!waited) mbar_wait(&full[s], (unsigned)((jj / NST) & 1));
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }

@@ -28,22 +28,29 @@ def _graph(n, k=10, seed=1):
 def _plan(n, offs, cols, row_bytes, nctas):
     lib = _lib()
     p = C.c_void_p()
-    sizes = np.zeros(6, np.int64)
+    sizes = np.zeros(7, np.int64)
     rc = lib.gs_win_plan_host(n, offs.ctypes.data, cols.ctypes.data, row_bytes, nctas, C.byref(p),
                               sizes.ctypes.data)
     if rc != 0:
         return rc, None
-    W, nct, nb, nl, stages, lmax = (int(x) for x in sizes)
+    W, nct, nb, nl, stages, lmax, npad = (int(x) for x in sizes)
     blk = np.zeros((nb, 8), np.int32)
     cta = np.zeros(nct + 1, np.int32)
     loads = np.zeros(nl, np.int32)
-    slot = np.zeros(len(cols), np.uint16)
+    poffs = np.zeros(n + 1, np.int32)
+    slot = np.zeros(npad, np.uint16)
     own = np.zeros(n, np.uint16)
-    lib.gs_win_plan_arrays(p, blk.ctypes.data, cta.ctypes.data, loads.ctypes.data, slot.ctypes.data,
-                           own.ctypes.data)
+    lib.gs_win_plan_arrays(p, blk.ctypes.data, cta.ctypes.data, loads.ctypes.data, poffs.ctypes.data,
+                           slot.ctypes.data, own.ctypes.data)
     lib.gs_win_plan_destroy(p)
+    # padded CSR: row r starts at poffs[r] & ~3 and has poffs[r] & 3 padding entries at its end
+    start = poffs & ~3
+    assert np.all(start % 4 == 0) and start[-1] == npad
+    assert np.array_equal(np.diff(start) - (poffs[:-1] & 3), np.diff(offs))
+    # padded index of every real entry
+    pidx = np.concatenate([start[r] + np.arange(offs[r + 1] - offs[r]) for r in range(n)]).astype(np.int64)
     return 0, dict(W=W, nctas=nct, stages=stages, lmax=lmax, blk=blk, cta=cta, loads=loads,
-                   slot=slot, own=own)
+                   slot=slot, own=own, start=start, pidx=pidx)
 
 
 def _replay(n, offs, cols, P):
@@ -67,8 +74,9 @@ def _replay(n, offs, cols, P):
                     applied += 1
                 rows = np.arange(row0, row0 + nrows)
                 assert np.all(ring[P["own"][rows]] == rows)
-                ent = np.arange(e0, e1)
-                assert np.all(ring[P["slot"][ent]] == cols[ent])
+                assert e0 == P["start"][row0] and e1 == P["start"][row0 + nrows]
+                ent = np.arange(offs[row0], offs[row0 + nrows])
+                assert np.all(ring[P["slot"][P["pidx"][ent]]] == cols[ent])
             covered[row0:row0 + nrows] = True
     assert covered.all()
     # blocks tile each CTA's rows in order

@@ -1,0 +1,30 @@
+"""Print the counters the DESIGN/profiles summaries cite from an ncu report (raw page)."""
+import csv
+import io
+import re
+import subprocess
+import sys
+
+rep = sys.argv[1]
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr = rows[0]
+data = rows[2:]
+want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "lts__t_sectors.sum", "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+        "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "launch__registers_per_thread"]
+for w in want:
+    if w in hdr:
+        i = hdr.index(w)
+        print(f"{w:60s}", [r[i][:14] for r in data])
+for h in hdr:
+    m = re.match(r"smsp__average_warps_issue_stalled_(.*)_per_issue_active.ratio$", h)
+    if m:
+        i = hdr.index(h)
+        v = [float(r[i] or 0) for r in data]
+        if max(v) > 0.1:
+            print(f"  stall {m.group(1):40s}", ["%.2f" % x for x in v])

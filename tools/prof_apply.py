@@ -1,0 +1,35 @@
+"""Profiling driver: one filter apply on a BASELINE-shaped operator (for ncu captures of the step
+kernel). Usage: python tools/prof_apply.py [config] [applies]; config 1 = swiss roll n=2e5, 64
+columns; config 2 = R^30 mixture n=1e6, 8 columns; config 4s = R^30 mixture n=1e6, 16 columns."""
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_2211_00805_b200 as gs  # noqa: E402
+from paper_2211_00805_b200 import workloads  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "1"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+ctx = gs.Context.default(0)
+if cfg == "1":
+    roll = workloads.swiss_roll(200_000, 1)
+    pts, k, t, B = roll.points, 10, 1.0, 64
+elif cfg in ("2", "4s"):
+    mix = workloads.gaussian_mixture(1_000_000, 30, 20 if cfg == "2" else 40, 3)
+    pts, k, t, B = mix.points, 15, 0.5, 8 if cfg == "2" else 16
+else:
+    raise SystemExit("config")
+t0 = time.time()
+A, _ = gs.knn_gaussian_graph(pts, k, ctx=ctx)
+lap = gs.laplacian(A, gs.LaplacianKind.combinatorial)
+f = gs.HeatFilter(lap, t, 30)
+n = pts.shape[0]
+X = np.abs(np.sin(np.arange(n)[:, None] * (np.arange(B)[None, :] + 1.0))) + 0.1
+print("setup", time.time() - t0, flush=True)
+for _ in range(reps):
+    Y = f.apply(X)
+print("apply done", float(np.abs(Y).sum()))
