@@ -666,15 +666,24 @@ void launch_step_win(gs_ctx* ctx, int gw, const CUtensorMap& tm, const StepArgs&
   switch (gw) {
     case 64: launch_win_gw<S, 64>(tm, A, WA, A.Gl, mode, ctx->stream); break;
     case 32: launch_win_gw<S, 32>(tm, A, WA, A.Gl, mode, ctx->stream); break;
-    default: launch_win_gw<S, 16>(tm, A, WA, A.Gl, mode, ctx->stream); break;
+    case 16: launch_win_gw<S, 16>(tm, A, WA, A.Gl, mode, ctx->stream); break;
+    default: launch_win_gw<S, 8>(tm, A, WA, A.Gl, mode, ctx->stream); break;
   }
   gs_launch_end(ctx, 0);
 }
 
-// row sizes the windowed kernel takes: wide rows (16-byte lanes), GW >= 16
+// Row sizes the windowed kernel takes: 256 bytes or more by default (GS_WIN_MIN_BYTES, at least
+// 32). Narrower rows are the kNN graphs in R^30 (configs 2 and 4): at n = 1e6 a CTA's ring gets
+// little reuse there (0.84 loads per entry) and the TMA gather4 issue rate (~75 cycles per
+// instruction per SM) bounds the step at 1.5-1.9 ms, against 0.32-0.40 ms for the register-gather
+// kernel (profiles/r02_summary.md).
 template <typename S>
 bool win_row_ok(int gw) {
-  return gw >= 16 && gw * (int)sizeof(S) > GS_NARROW_MAX_BYTES;
+  static const int min_bytes = [] {
+    const char* e = getenv("GS_WIN_MIN_BYTES");
+    return e ? atoi(e) : 256;
+  }();
+  return gw >= 8 && gw * (int)sizeof(S) >= min_bytes && gw * (int)sizeof(S) >= 32;
 }
 
 // GS_BLK=1 runs wide fp64 rows through the 8-row block kernel (k_cheb_blk). Off by default:

@@ -8,6 +8,8 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <numeric>
@@ -95,21 +97,34 @@ struct WinHost {
 };
 
 // Ring schedule (see gs_win.cuh). Rows [bounds[c], bounds[c+1]) go to CTA c (weight-balanced:
-// entries + 2 per row). Positions count the CTA's loads; a load at position p lives in ring slot
-// p mod W until the load at p + W. A block b whose loads start at position P_b may reuse a
-// position p only if p >= P_b + kWinStages * LMAX - W: the producer runs at most kWinStages - 1
-// blocks ahead of the consumers, and a block loads at most LMAX rows, so no load issued while b
-// can still be read overwrites such a p. Returns false if one row alone exceeds LMAX loads or
-// EMAX entries (the caller keeps the register-gather kernel then).
-bool build_schedule(int n, const int* offs, const int* cols, int row_bytes, int rows_max, int nctas,
-                    WinHost& out) {
-  const int W = gsk::win_ring_slots(row_bytes);
-  // loads per block: a quarter of the ring with three stages (512-byte rows: 96 of 384 slots),
-  // so reuse reaches back at least W / 4 slots behind a block's first load
-  const int LMAX = std::max(4, std::min(gsk::kWinLmaxCap, (W / (gsk::kWinStages + 1)) & ~3));
+// padded entries + 2 per row). Positions count the CTA's loads; a load at position p lives in
+// ring slot p mod W until the load at p + W overwrites it. A block b loads positions
+// [P_b, P_b + L_b) (L_b <= LMAX), so it may reuse a position p only if p >= P_b + LMAX + margin - W
+// (its own loads never overwrite what it reads; `margin` keeps reuse away from slots about to be
+// refilled, which would stall the producer). Before the producer issues block b it waits until
+// block wait(b) is consumed: the last block that reads a slot b's loads overwrite, and at least
+// b - kWinStages (the metadata stages). Consumers finish blocks in order, so every block up to
+// wait(b) is then done. Returns false if one row alone exceeds LMAX loads or EMAX entries (the
+// caller keeps the register-gather kernel then).
+bool build_schedule(int n, const int* offs, const int* cols, int row_bytes, int elem_bytes, int rows_max,
+                    int nctas, WinHost& out) {
+  const int W = elem_bytes == 8 ? gsk::win_ring_slots<double>(row_bytes) : gsk::win_ring_slots<float>(row_bytes);
+  // loads per block: min(256, W / 4) (512-byte rows: 92 of 368 slots), raised to the largest
+  // row's need (its entries + its own row) up to W / 2
+  int maxdeg = 0;
+  for (int r = 0; r < n; ++r) maxdeg = std::max(maxdeg, offs[r + 1] - offs[r]);
+  const int lcap = std::min(gsk::kWinLmaxCap, (W / 2) & ~3);
+  const int LMAX = std::min(lcap, std::max(std::min(256, (W / 4) & ~3), ((maxdeg + 1 + 3) & ~3)));
+  static const int margin_div = [] {
+    const char* e = getenv("GS_WIN_MARGIN_DIV");
+    return e ? atoi(e) : 4;
+  }();
+  const int margin = margin_div > 0 ? (W / margin_div) & ~3 : 0;
+  if (getenv("GS_WIN_VERBOSE") && atoi(getenv("GS_WIN_VERBOSE")) != 0)
+    fprintf(stderr, "[gs_win] n=%d max degree %d, W=%d, lmax=%d (cap %d) margin=%d\n", n, maxdeg, W, LMAX, lcap,
+            margin);
   const int EMAX = gsk::kWinEmax;
-  const int64_t lead = (int64_t)gsk::kWinStages * LMAX;
-  if (W < lead + 4 || nctas < 1) return false;
+  if (W < LMAX + margin + 4 || nctas < 1) return false;
   out.W = W;
   out.lmax = LMAX;
   out.nctas = nctas;
@@ -147,17 +162,21 @@ bool build_schedule(int n, const int* offs, const int* cols, int row_bytes, int 
   }
   std::vector<int64_t> last(n, INT64_MIN / 4);
   std::vector<int> rstamp(n, 0);
+  std::vector<int> lastref(W);  // per ring slot: the last block (global index) reading it
   int rs = 0;
   int64_t base = 0;
   std::vector<int> rownew;
   std::vector<int> blkloads;
   for (int c = 0; c < nctas; ++c) {
-    out.cta_blk[c] = (int)out.blk.size();
+    const int bfirst = (int)out.blk.size();
+    out.cta_blk[c] = bfirst;
+    std::fill(lastref.begin(), lastref.end(), -1);
     int64_t P = base;
     int r = bounds[c];
     const int rend = bounds[c + 1];
     while (r < rend) {
-      const int64_t Pb = P, lo = Pb + lead - W;
+      const int bidx = (int)out.blk.size();
+      const int64_t Pb = P, lo = Pb + LMAX + margin - W;
       blkloads.clear();
       const int row0 = r;
       int nrows = 0;
@@ -189,6 +208,16 @@ bool build_schedule(int n, const int* offs, const int* cols, int row_bytes, int 
       }
       const int nl = (int)((blkloads.size() + 3) & ~(size_t)3);
       while ((int)blkloads.size() < nl) blkloads.push_back(blkloads.back());  // padding: a repeat
+      // the producer's wait: the last reader of every slot this block overwrites, and the
+      // metadata stage this block reuses
+      int wait = std::max(bfirst - 1, bidx - gsk::kWinStages);
+      for (int i = 0; i < nl; ++i) wait = std::max(wait, lastref[(Pb + i) % W]);
+      // this block's readers: its loads and every reused slot
+      for (int i = 0; i < nl; ++i) lastref[(Pb + i) % W] = bidx;
+      for (int rr = row0; rr < row0 + nrows; ++rr) {
+        lastref[out.own[rr]] = bidx;
+        for (int p = offs[rr]; p < offs[rr + 1]; ++p) lastref[out.slot[pstart[rr] + (p - offs[rr])]] = bidx;
+      }
       WinBlk b{};
       b.row0 = row0;
       b.nrows = nrows;
@@ -197,6 +226,7 @@ bool build_schedule(int n, const int* offs, const int* cols, int row_bytes, int 
       b.slot0 = (int)(Pb % W);
       b.e0 = (int)pstart[row0];
       b.e1 = (int)pstart[row0 + nrows];
+      b.wait = wait;  // < bfirst: no wait
       out.blk.push_back(b);
       out.loads.insert(out.loads.end(), blkloads.begin(), blkloads.end());
       P += nl;
@@ -274,10 +304,15 @@ int gs_win_build(gs_ctx* ctx, gs_filter* f, int row_bytes, int elem_bytes) {
   w->row_bytes = key;
   Ly.win.push_back(w);
   WinHost h;
-  if (n == 0 || !build_schedule(n, offs.data(), cols.data(), row_bytes, rows_max, sms, h)) {
+  const bool verbose = getenv("GS_WIN_VERBOSE") && atoi(getenv("GS_WIN_VERBOSE")) != 0;
+  if (n == 0 || !build_schedule(n, offs.data(), cols.data(), row_bytes, elem_bytes, rows_max, sms, h)) {
     w->ok = false;
+    if (verbose) fprintf(stderr, "[gs_win] row_bytes=%d elem=%d: no schedule (a row exceeds a block)\n", row_bytes, elem_bytes);
     return GS_ERR_UNSUPPORTED;
   }
+  if (verbose)
+    fprintf(stderr, "[gs_win] row_bytes=%d elem=%d W=%d lmax=%d blocks=%zu loads=%zu loads/entry=%.3f\n", row_bytes,
+            elem_bytes, h.W, h.lmax, h.blk.size(), h.loads.size(), h.entries ? (double)h.loads.size() / h.entries : 0.0);
   w->W = h.W;
   w->nctas = h.nctas;
   w->nblocks = (int)h.blk.size();
@@ -361,7 +396,7 @@ extern "C" int gs_win_plan_host(int n, const int* offs, const int* cols, int row
   *out = nullptr;
   const int rows_max = gsk::WinMeta<double>::ROWS_MAX;
   gs_winplan* p = new gs_winplan();
-  if (!build_schedule(n, offs, cols, row_bytes, rows_max, nctas, p->h)) {
+  if (!build_schedule(n, offs, cols, row_bytes, 8, rows_max, nctas, p->h)) {
     delete p;
     return GS_ERR_UNSUPPORTED;
   }

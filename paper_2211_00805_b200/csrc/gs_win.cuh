@@ -36,8 +36,9 @@ struct WinBlk {  // one row block of the schedule (32 bytes)
   int row0, nrows;  // rows [row0, row0 + nrows) of the window layout
   int lbeg, nl;     // its loads: loads[lbeg .. lbeg + nl), nl % 4 == 0
   int slot0;        // ring slot of its first load (consecutive slots, modulo W)
-  int e0, e1;       // CSR entry range of its rows
-  int pad;
+  int e0, e1;       // padded CSR entry range of its rows
+  int wait;         // the producer issues this block once block `wait` is consumed (< the CTA's
+                    // first block: no wait)
 };
 
 #ifndef GS_WIN_WARPS
@@ -47,19 +48,19 @@ struct WinBlk {  // one row block of the schedule (32 bytes)
 #define GS_WIN_STAGES 3
 #endif
 #ifndef GS_WIN_EMAX
-#define GS_WIN_EMAX 640
+#define GS_WIN_EMAX 1024
 #endif
 #ifndef GS_WIN_LMAX_CAP
-#define GS_WIN_LMAX_CAP 256
+#define GS_WIN_LMAX_CAP 1024
 #endif
-#ifndef GS_WIN_RING_BYTES
-#define GS_WIN_RING_BYTES (192 * 1024)
+// dynamic shared memory of one CTA (the B200 opt-in maximum is 227 KB = 232448 bytes)
+#ifndef GS_WIN_SMEM_BYTES
+#define GS_WIN_SMEM_BYTES 232448
 #endif
 constexpr int kWinWarps = GS_WIN_WARPS;    // consumer warps per CTA (+ one producer warp)
 constexpr int kWinStages = GS_WIN_STAGES;  // blocks in flight (producer lead + 1)
 constexpr int kWinEmax = GS_WIN_EMAX;      // CSR entries per block at most
 constexpr int kWinLmaxCap = GS_WIN_LMAX_CAP;  // loads per block at most (the plan: W / 4)
-constexpr int kWinRingBytes = GS_WIN_RING_BYTES;
 constexpr int kWinThreads = (kWinWarps + 1) * 32;
 
 __host__ __device__ constexpr int win_align16(int b) { return (b + 15) & ~15; }
@@ -78,16 +79,21 @@ struct WinMeta {
   static constexpr int BYTES = VAL_BYTES + SLOT_BYTES + OFF_BYTES + OWN_BYTES;
 };
 
-// ring slots for a row of `row_bytes` (multiple of 4, at most 65532)
+// ring slots for a row of `row_bytes` bytes: the shared memory left after the stage metadata and
+// the barriers (a multiple of 4, at most 65532)
+template <typename S>
 __host__ __device__ constexpr int win_ring_slots(int row_bytes) {
-  return ((kWinRingBytes / row_bytes) & ~3) > 65532 ? 65532 : ((kWinRingBytes / row_bytes) & ~3);
+  return ((((GS_WIN_SMEM_BYTES - kWinStages * WinMeta<S>::BYTES - 2 * kWinStages * 8) / row_bytes) & ~3) > 65532)
+             ? 65532
+             : (((GS_WIN_SMEM_BYTES - kWinStages * WinMeta<S>::BYTES - 2 * kWinStages * 8) / row_bytes) & ~3);
 }
 
 template <typename S, int GW>
 constexpr int win_smem_bytes() {
-  return win_ring_slots(GW * (int)sizeof(S)) * GW * (int)sizeof(S) + kWinStages * WinMeta<S>::BYTES +
+  return win_ring_slots<S>(GW * (int)sizeof(S)) * GW * (int)sizeof(S) + kWinStages * WinMeta<S>::BYTES +
          2 * kWinStages * 8;
 }
+static_assert(win_smem_bytes<double, 64>() <= GS_WIN_SMEM_BYTES, "window shared memory");
 
 struct WinArgs {
   const WinBlk* blk;
@@ -225,10 +231,28 @@ __global__ void __launch_bounds__(kWinThreads, 1)
   const int64_t grow = (int64_t)g * A.ld;  // first tensor-map row of this column group
   if (warp == kWinWarps) {
     // ---------------- producer ----------------
+    // The block's row ids (groups of four) are loaded one block ahead into registers, so the
+    // TMA issue never waits on the index loads (up to 32 x U groups per block).
+    constexpr int U = (kWinLmaxCap / 4 + 31) / 32;
+    int4 ic[U], inx[U];
+    auto load_idx = [&](int j, int4 (&dst)[U]) {
+      const int ng = j < b1 ? (WA.blk[j].nl >> 2) : 0;
+      const int4* src = j < b1 ? reinterpret_cast<const int4*>(WA.loads + WA.blk[j].lbeg) : nullptr;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = lane + 32 * u;
+        dst[u] = i < ng ? __ldg(src + i) : make_int4(0, 0, 0, 0);
+      }
+    };
+    load_idx(b0, ic);
     for (int j = b0; j < b1; ++j) {
       const int jj = j - b0, s = jj % NST;
-      if (jj >= NST) mbar_wait(&empty[s], (unsigned)(((jj / NST) - 1) & 1));
+      load_idx(j + 1, inx);
       const WinBlk bk = WA.blk[j];
+      if (bk.wait >= b0) {  // every block up to bk.wait consumed (its empty phase completed)
+        const int wj = bk.wait - b0;
+        mbar_wait(&empty[wj % NST], (unsigned)((wj / NST) & 1));
+      }
       unsigned char* mt = meta + s * M::BYTES;
       // e0, e1: padded entry range (multiples of 4)
       const int sb = bk.e0 & ~7, ob = bk.row0 & ~3, wb = bk.row0 & ~7;
@@ -245,16 +269,22 @@ __global__ void __launch_bounds__(kWinThreads, 1)
       }
       __syncwarp();
       const int ng = bk.nl >> 2;
-      for (int i = lane; i < ng; i += 32) {
-        int4 r = __ldg(reinterpret_cast<const int4*>(WA.loads + bk.lbeg) + i);
-        r.x += (int)grow;
-        r.y += (int)grow;
-        r.z += (int)grow;
-        r.w += (int)grow;
-        int slot = bk.slot0 + 4 * i;
-        if (slot >= W) slot -= W;
-        tma_gather4(ring + (size_t)slot * GW, &tmap, 0, r, &full[s]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = lane + 32 * u;
+        if (i < ng) {
+          int4 r = ic[u];
+          r.x += (int)grow;
+          r.y += (int)grow;
+          r.z += (int)grow;
+          r.w += (int)grow;
+          int slot = bk.slot0 + 4 * i;
+          if (slot >= W) slot -= W;
+          tma_gather4(ring + (size_t)slot * GW, &tmap, 0, r, &full[s]);
+        }
       }
+#pragma unroll
+      for (int u = 0; u < U; ++u) ic[u] = inx[u];
     }
   } else {
     // ---------------- consumers ----------------

@@ -54,21 +54,29 @@ def _plan(n, offs, cols, row_bytes, nctas):
 
 
 def _replay(n, offs, cols, P):
-    """Every block, every lead d in [0, stages-1]: with the loads of blocks <= b + d applied to the
-    ring, each entry's slot holds its column and each row's own slot holds the row."""
+    """The producer issues block j once block wait(j) is consumed (blk[:, 7]); consumers finish
+    blocks in order. While block b is being read, every block up to jmax(b) -- the longest prefix
+    whose waits are all < b -- may already have been issued. For every b and every issued prefix
+    in [b, jmax(b)], each entry's ring slot holds its column and each row's own slot the row."""
     W, S = P["W"], P["stages"]
     blk, cta, loads = P["blk"], P["cta"], P["loads"]
     covered = np.zeros(n, bool)
     for c in range(P["nctas"]):
         b0, b1 = cta[c], cta[c + 1]
+        wait = blk[b0:b1, 7]
+        # the metadata stages bound the lead, and no block waits on itself or a later block
+        assert np.all(wait >= np.arange(b0, b1) - S) and np.all(wait < np.arange(b0, b1))
         ring = np.full(W, -1, np.int64)
         applied = b0  # blocks whose loads are in the ring
         for b in range(b0, b1):
             row0, nrows, lbeg, nl, slot0, e0, e1, _ = blk[b]
             assert nl % 4 == 0 and nl <= P["lmax"] and slot0 % 4 == 0
-            for d in range(S):
-                while applied <= min(b + d, b1 - 1):
-                    r0, nr, lb, nlb, s0 = blk[applied][:5]
+            jmax = b
+            while jmax + 1 < b1 and wait[jmax + 1 - b0] < b:
+                jmax += 1
+            for last_issued in range(b, jmax + 1):
+                while applied <= last_issued:
+                    s0, lb, nlb = blk[applied][4], blk[applied][2], blk[applied][3]
                     for i in range(nlb):
                         ring[(s0 + i) % W] = loads[lb + i]
                     applied += 1

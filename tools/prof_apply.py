@@ -30,6 +30,10 @@ f = gs.HeatFilter(lap, t, 30)
 n = pts.shape[0]
 X = np.abs(np.sin(np.arange(n)[:, None] * (np.arange(B)[None, :] + 1.0))) + 0.1
 print("setup", time.time() - t0, flush=True)
+Y = f.apply(X)  # warm-up (builds the layout / schedule)
+ctx.set_timing(True)
 for _ in range(reps):
     Y = f.apply(X)
-print("apply done", float(np.abs(Y).sum()))
+nst, ms = ctx.timing(0)
+ctx.set_timing(False)
+print(f"apply done: {nst} step launches, avg step {1e3 * ms / max(nst, 1):.1f} us", float(np.abs(Y).sum()))
