@@ -187,11 +187,31 @@ typedef int (*gs_allreduce_fn)(void* user, double* device_buf, int64_t count, in
                                void* stream);
 typedef int (*gs_alltoallv_fn)(void* user, const void* sendbuf, const int64_t* send_bytes,
                                void* recvbuf, const int64_t* recv_bytes, int nranks, void* stream);
+#define GS_COMM_GRAPH_SAFE 1 /* hooks only enqueue stream-ordered device work: CUDA-graph capture
+                                * of whole sweeps stays on (the engine's NCCL communicator) */
 typedef struct {
   gs_allreduce_fn allreduce;
   void* user;
   gs_alltoallv_fn alltoallv; /* row-partitioned runs only; may be NULL otherwise */
+  int flags;                 /* GS_COMM_GRAPH_SAFE or 0 (host-callback hooks) */
 } gs_comm;
+
+/* ---- in-engine NCCL communicator (NVLink / NVSwitch data plane) --------------------------
+ * One process per GPU. Rank 0 calls gs_nccl_unique_id and broadcasts the 128 bytes through the
+ * caller's bootstrap (torch.distributed, MPI, a file); every rank then calls
+ * gs_nccl_comm_create on its own context. The returned gs_comm's hooks call ncclAllReduce and,
+ * for halo exchanges, one ncclGroupStart/End of ncclSend/ncclRecv with the ranks that have bytes
+ * to exchange (the partition's neighbours only), on the engine's stream; it carries
+ * GS_COMM_GRAPH_SAFE, so barycenter sweeps stay CUDA-graph captured with the collective inside.
+ * NCCL is loaded at run time (libnccl.so.2, the one already in the process when there is one);
+ * GS_ERR_NCCL when it is missing or a call fails. */
+#define GS_NCCL_UNIQUE_ID_BYTES 128
+int gs_nccl_unique_id(void* id_out);
+int gs_nccl_comm_create(gs_ctx* ctx, const void* id, int nranks, int rank, gs_comm** out);
+void gs_nccl_comm_destroy(gs_comm* comm);
+/* Host-side invocations of the communicator's hooks so far (a replayed sweep graph re-runs its
+ * captured collectives without invoking them again). */
+int64_t gs_nccl_comm_calls(const gs_comm* comm);
 
 /* ---- row partitions (row-partitioned multi-GPU applies) ----------------- */
 /* The reference is single-process (OpenMP rows, heat.cpp:116-131 over sparse.cpp:85-99); this

@@ -36,11 +36,20 @@ ALLTOALLV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)
                            C.POINTER(C.c_int64), C.c_int, C.c_void_p)
 
 
+GS_COMM_GRAPH_SAFE = 1
+GS_NCCL_UNIQUE_ID_BYTES = 128
+
+
 class GsComm(C.Structure):
-    _fields_ = [("allreduce", ALLREDUCE_FN), ("user", C.c_void_p), ("alltoallv", ALLTOALLV_FN)]
+    _fields_ = [("allreduce", ALLREDUCE_FN), ("user", C.c_void_p), ("alltoallv", ALLTOALLV_FN),
+                ("flags", C.c_int)]
 
 
 SIGNATURES = {
+    "gs_nccl_unique_id": (_i, [_vp]),
+    "gs_nccl_comm_create": (_i, [_vp, _vp, _i, _i, _pvp]),
+    "gs_nccl_comm_destroy": (None, [_vp]),
+    "gs_nccl_comm_calls": (_i64, [_vp]),
     "gs_win_bisect_order_host": (_i, [_i, _vp, _vp, _i, _vp]),
     "gs_win_plan_host": (_i, [_i, _vp, _vp, _i, _i, _pvp, _vp]),
     "gs_win_plan_arrays": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),

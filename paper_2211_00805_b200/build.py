@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 PKG = os.path.join(ROOT, "paper_2211_00805_b200")
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "lib", "libgeosink_b200.so")
-SOURCES = ["gs_core.cu", "gs_cheb.cu", "gs_graph.cu", "gs_reorder.cu", "gs_part.cu", "gs_euler.cu", "gs_dense.cu", "gs_win.cu", "gs_rng.cpp", "gs_io.cpp"]
+SOURCES = ["gs_core.cu", "gs_cheb.cu", "gs_graph.cu", "gs_reorder.cu", "gs_part.cu", "gs_euler.cu", "gs_dense.cu", "gs_win.cu", "gs_nccl.cu", "gs_rng.cpp", "gs_io.cpp"]
 HEADERS = ["gs_internal.cuh", "gs_step.cuh", "gs_win.cuh"]
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-fmad=false", "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
@@ -53,7 +53,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str | Non
         if p.returncode != 0:
             sys.stderr.write(out.decode())
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
-    link = ["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib, *objs]
+    link = ["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib, *objs, "-ldl"]
     subprocess.run(link, check=True)
     with open(os.path.join(PKG, "lib", "ptxas" + tag + ".log"), "w") as f:
         f.write("\n".join(logs))

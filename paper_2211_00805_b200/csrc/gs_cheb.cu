@@ -419,15 +419,21 @@ __global__ void k_bary_w(double* __restrict__ bary, const double* __restrict__ m
   }
 }
 
-__global__ void k_bary_errlocal(const double* errcol, int m, double* errbuf) {
+// errbuf[0] = this rank's marginal error (max over its members, barycenter.cpp:86), errbuf[1] =
+// its status error code: both are max-allreduced across member shards before k_bary_control, so
+// a failure on one rank (positivity check, collapsed mass) stops every rank at the same sweep
+// with the same errc and every rank issues the same collectives.
+__global__ void k_bary_errlocal(const double* errcol, int m, double* errbuf, const gs_status* st) {
   double e = 0.0;
   for (int c = 0; c < m; ++c) e = fmax(e, errcol[c]);
-  *errbuf = e;
+  errbuf[0] = e;
+  errbuf[1] = (double)st->error;
 }
 
 __global__ void k_bary_control(const double* errbuf, gs_status* st, int* sweep_ctr, double tol,
                                int* iters, int* conv, double* err_out, int max_iter, int fp32) {
   const int sweep = ++(*sweep_ctr);  // device counter: a captured sweep can be replayed
+  if (!st->done && errbuf[1] != 0.0) st->error = (int)errbuf[1];  // the agreed (max) error code
   if (st->error || st->done) return;
   const double err = *errbuf;
   *err_out = err;
@@ -1361,7 +1367,7 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   GS_CUDA(ctx, part.alloc(nchunks, s));
   GS_CUDA(ctx, mass.alloc(1, s));
   GS_CUDA(ctx, dal.alloc(m, s));
-  GS_CUDA(ctx, errbuf.alloc(1, s));
+  GS_CUDA(ctx, errbuf.alloc(2, s));
   GS_CUDA(ctx, derr.alloc(1, s));
   GS_CUDA(ctx, lbmax.alloc(1, s));
   GS_CUDA(ctx, diters.alloc(1, s));
@@ -1439,10 +1445,10 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
                       false, true);
     run_finalize<S>(ctx, w, 1, 1, 1, knp, false);
     gs_launch_begin(ctx, 1);
-    k_bary_errlocal<<<1, 1, 0, s>>>(w.errcol.get(), m, errbuf.get());
+    k_bary_errlocal<<<1, 1, 0, s>>>(w.errcol.get(), m, errbuf.get(), w.status.get());
     gs_launch_end(ctx, 1);
     if (hooked) {
-      const int rc = comm->allreduce(comm->user, errbuf.get(), 1, 1, (void*)s);
+      const int rc = comm->allreduce(comm->user, errbuf.get(), 2, 1, (void*)s);
       if (rc) return rc;
     }
     gs_launch_begin(ctx, 1);
@@ -1451,12 +1457,15 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
     gs_launch_end(ctx, 1);
     return 0;
   };
-  // Without collective hooks, two sweeps (odd, even parity) are captured once as a CUDA graph and
-  // replayed (as in sinkhorn_impl); hooks call back into the host every sweep, so no capture.
+  // Two sweeps (odd, even parity) are captured once as a CUDA graph and replayed (as in
+  // sinkhorn_impl) -- with no collective hooks, or with stream-ordered device collectives that may
+  // be captured (GS_COMM_GRAPH_SAFE: the engine's NCCL communicator, gs_nccl.cu). Host-callback
+  // hooks run every sweep without capture.
   cudaGraphExec_t gexec = nullptr;
   int64_t graph_launches = 0;
   const char* genv = getenv("GS_GRAPH");
-  if (!hooked && (genv ? genv[0] != '0' : true) && max_iter >= 2) {
+  const bool capturable = !hooked || (comm->flags & GS_COMM_GRAPH_SAFE);
+  if (capturable && (genv ? genv[0] != '0' : true) && max_iter >= 2) {
     cudaGraph_t graph = nullptr;
     const int64_t l0 = ctx->launches;
     const int a0_saved = a0;
@@ -2466,37 +2475,62 @@ extern "C" int gs_barycenter_ex(gs_ctx* ctx, const gs_filter* f, const double* a
                                 double* out_bary, double* out_V, double* out_W, int* out_iters,
                                 int* out_conv, double* out_err) {
   const int n = f->scaled->n;
-  if (m < 1) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "family must be non-empty");
   DevBuf<double> bmem, ba;
-  const double *dmem, *da;
-  GS_TRY(stage_in(ctx, bmem, members, (size_t)m * n, mem, &dmem));
-  GS_TRY(stage_in(ctx, ba, a, (size_t)n, mem, &da));
-  {  // family.validate (barycenter.cpp:32-43)
-    std::vector<double> sm;
-    std::vector<int> fm, gm;
-    GS_TRY(validate_columns(ctx, dmem, n, m, sm, fm, gm));
-    for (int c = 0; c < m; ++c) GS_TRY(check_distribution(ctx, n, sm[c], fm[c], gm[c]));
-  }
-  std::vector<double> al(m);
-  if (alphas) {
-    if (mem == GS_MEM_DEVICE) {
-      GS_CUDA(ctx, cudaMemcpy(al.data(), alphas, m * sizeof(double), cudaMemcpyDeviceToHost));
-    } else {
-      memcpy(al.data(), alphas, m * sizeof(double));
+  const double *dmem = nullptr, *da = nullptr;
+  std::vector<double> al(m > 0 ? m : 1);
+  // validation (barycenter.cpp:32-43 family.validate, weights, parameters); with a comm the
+  // outcome is agreed across the member shards before anyone returns, so a rank that fails
+  // never leaves the others waiting in a collective
+  auto validate = [&]() -> int {
+    if (m < 1) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "family must be non-empty");
+    GS_TRY(stage_in(ctx, bmem, members, (size_t)m * n, mem, &dmem));
+    GS_TRY(stage_in(ctx, ba, a, (size_t)n, mem, &da));
+    {
+      std::vector<double> sm;
+      std::vector<int> fm, gm;
+      GS_TRY(validate_columns(ctx, dmem, n, m, sm, fm, gm));
+      for (int c = 0; c < m; ++c) GS_TRY(check_distribution(ctx, n, sm[c], fm[c], gm[c]));
     }
-  } else {
-    for (int c = 0; c < m; ++c) al[c] = 1.0 / (double)m;
-  }
-  {
+    if (alphas) {
+      if (mem == GS_MEM_DEVICE) {
+        GS_CUDA(ctx, cudaMemcpy(al.data(), alphas, m * sizeof(double), cudaMemcpyDeviceToHost));
+      } else {
+        memcpy(al.data(), alphas, m * sizeof(double));
+      }
+    } else {
+      for (int c = 0; c < m; ++c) al[c] = 1.0 / (double)m;
+    }
     double asum = 0.0;
     for (int c = 0; c < m; ++c) {
       if (!(al[c] >= 0.0)) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "alphas must be non-negative");
       asum += al[c];
     }
     if (!comm && !(std::fabs(asum - 1.0) <= 1e-9)) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "alphas must sum to 1");
+    GS_TRY(check_weights(ctx, da, n));
+    if (!(tol > 0.0 && max_iter >= 1)) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "bad parameters");
+    return GS_OK;
+  };
+  int vrc = validate();
+  if (comm && comm->allreduce) {
+    DevBuf<double> flag;
+    GS_CUDA(ctx, flag.alloc(1, ctx->stream));
+    const double hv = (double)vrc;
+    GS_CUDA(ctx, cudaMemcpyAsync(flag.get(), &hv, sizeof hv, cudaMemcpyHostToDevice, ctx->stream));
+    if (comm->allreduce(comm->user, flag.get(), 1, 1, (void*)ctx->stream)) {
+      ctx->err = "NcclError: allreduce hook failed";
+      return GS_ERR_NCCL;
+    }
+    double agreed = 0.0;
+    GS_CUDA(ctx, cudaMemcpyAsync(&agreed, flag.get(), sizeof agreed, cudaMemcpyDeviceToHost, ctx->stream));
+    GS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    if (vrc == 0 && agreed != 0.0) {
+      const int code = (int)agreed;
+      if (code >= 1 && code <= 16) return gs_fail(ctx, code - 1, "barycenter inputs rejected on another rank");
+      ctx->err = "barycenter inputs rejected on another rank";
+      return code;
+    }
   }
-  GS_TRY(check_weights(ctx, da, n));
-  if (!(tol > 0.0 && max_iter >= 1)) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "bad parameters");
+  if (vrc) return vrc;
   if (flags & GS_FLAG_FP32)
     return barycenter_impl<float>(ctx, f, da, dmem, m, al, max_iter, tol, mem, comm, out_bary,
                                   out_V, out_W, out_iters, out_conv, out_err);

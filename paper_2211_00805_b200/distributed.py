@@ -118,6 +118,57 @@ class TorchComm:
 TorchAllreduce = TorchComm  # earlier name (allreduce-only hook)
 
 
+class NcclComm:
+    """The engine's own NCCL communicator (gs_nccl_comm_create, csrc/gs_nccl.cu): NCCL calls on
+    the engine's stream, no host callback inside the sweep loop, CUDA-graph capture kept
+    (GS_COMM_GRAPH_SAFE). torch.distributed is only the bootstrap that broadcasts rank 0's
+    ncclUniqueId. `comm` is the gs_comm* to hand to the engine."""
+
+    def __init__(self, ctx, group=None):
+        import torch.distributed as dist
+
+        self._ctx = ctx
+        lib = ctx.lib
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        uid = C.create_string_buffer(_capi.GS_NCCL_UNIQUE_ID_BYTES)
+        if rank == 0:
+            ctx.check(lib.gs_nccl_unique_id(uid))
+        box = [bytes(uid.raw)]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(box, src=src, group=group)
+        uid = C.create_string_buffer(box[0], _capi.GS_NCCL_UNIQUE_ID_BYTES)
+        self._ptr = C.c_void_p()
+        ctx.check(lib.gs_nccl_comm_create(ctx.handle, uid, world, rank, C.byref(self._ptr)))
+        self.world, self.rank = world, rank
+        self.error = None
+
+    @property
+    def comm(self):
+        return self._ptr
+
+    def calls(self) -> int:
+        """Host-side hook invocations so far (a captured sweep graph replays its collectives
+        without invoking the hooks again)."""
+        return int(self._ctx.lib.gs_nccl_comm_calls(self._ptr))
+
+    def close(self):
+        if self._ptr:
+            self._ctx.lib.gs_nccl_comm_destroy(self._ptr)
+            self._ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _comm_arg(hook):
+    """The gs_comm* argument for a hook object (TorchComm / RankComm struct or NcclComm)."""
+    return hook.comm if isinstance(hook, NcclComm) else C.byref(hook.comm)
+
+
 def _host_bytes(ptr: int, count: int) -> np.ndarray:
     if count == 0:
         return np.zeros(0, np.uint8)
@@ -125,10 +176,11 @@ def _host_bytes(ptr: int, count: int) -> np.ndarray:
 
 
 def partitioned_sinkhorn(filter: HeatFilter, mus, nus, a, params: SinkhornParams = SinkhornParams(),
-                         group=None, **kw):
+                         group=None, comm=None, **kw):
     """geodesic_sinkhorn_batch with the graph's rows split over the ranks of `group` (one halo
     exchange per Chebyshev step). Every rank passes the full inputs and gets (partition, results)
-    where results[p].v / .w hold the rows listed by partition.vertices."""
+    where results[p].v / .w hold the rows listed by partition.vertices. `comm`: None (torch hooks)
+    or an NcclComm (the engine's own NCCL communicator)."""
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
@@ -136,7 +188,7 @@ def partitioned_sinkhorn(filter: HeatFilter, mus, nus, a, params: SinkhornParams
     part = RowPartition(filter, world, rank)
     vid = part.vertices
     take = lambda d: (d.weights if isinstance(d, Distribution) else _f64(d))[vid]
-    hook = TorchComm(group, device_buffers=True)
+    hook = comm if comm is not None else TorchComm(group, device_buffers=True)
     try:
         res = part.sinkhorn([take(m) for m in mus], [take(v) for v in nus], _f64(a)[vid], params,
                             comm=hook.comm, **kw)
@@ -149,18 +201,25 @@ def partitioned_sinkhorn(filter: HeatFilter, mus, nus, a, params: SinkhornParams
 
 def sharded_sinkhorn_barycenter(filter: HeatFilter, family: DistributionFamily, a,
                                 params: SinkhornParams = SinkhornParams(),
-                                group=None) -> BarycenterResult:
+                                group=None, comm=None) -> BarycenterResult:
     """sinkhorn_barycenter (barycenter.cpp:45-99) with the members sharded over the ranks of
     `group`; every rank passes the full family and gets the full barycenter plus the scalings
-    of its own members (others are None)."""
+    of its own members (others are None). `comm`: None (torch.distributed hooks), an NcclComm
+    (the engine's NCCL communicator; sweeps stay CUDA-graph captured) or any object with a
+    gs_comm `comm` attribute."""
     import torch.distributed as dist
+
+    from .geosink import Error, errc
 
     ctx = filter._ctx
     n = filter.size()
     family.validate(n)
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
+    world = dist.get_world_size(group) if comm is None or isinstance(comm, (TorchComm, NcclComm)) else comm.g.n
+    rank = dist.get_rank(group) if comm is None or isinstance(comm, (TorchComm, NcclComm)) else comm.rank
     m = len(family.members)
+    if world > m:  # every shard needs a member: an empty shard cannot take part in the sweeps
+        raise Error(errc.invalid_argument,
+                    f"InvalidArgument: {m} members cannot be sharded over {world} ranks")
     lo, hi = member_shard(m, world, rank)
     al = family.resolved_alphas()[lo:hi].copy()
     local = _stack(family.members[lo:hi], n)
@@ -171,10 +230,10 @@ def sharded_sinkhorn_barycenter(filter: HeatFilter, family: DistributionFamily, 
     it = np.zeros(1, np.int32)
     conv = np.zeros(1, np.int32)
     err = np.zeros(1)
-    hook = TorchAllreduce(group, device_buffers=True)
+    hook = comm if comm is not None else TorchComm(group, device_buffers=True)
     rc = ctx.lib.gs_barycenter(ctx.handle, filter._h, _ptr(a), _ptr(local), hi - lo, _ptr(al),
                                int(params.max_iter), float(params.tol), _capi.GS_MEM_HOST,
-                               C.byref(hook.comm), _ptr(bary), _ptr(V), _ptr(W), _ptr(it),
+                               _comm_arg(hook), _ptr(bary), _ptr(V), _ptr(W), _ptr(it),
                                _ptr(conv), _ptr(err))
     if hook.error is not None:
         raise hook.error

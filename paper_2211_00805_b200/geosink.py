@@ -774,7 +774,11 @@ class RowPartition:
                                                        _capi.GS_MEM_HOST))
 
     def _comm(self, comm):
-        return C.byref(comm) if comm is not None else None
+        if comm is None:
+            return None
+        if isinstance(comm, C.c_void_p):  # a gs_comm* (the engine's NCCL communicator)
+            return comm
+        return C.byref(comm)
 
     def apply(self, f_local, comm=None, fp32: bool = False) -> np.ndarray:
         """H f on this part's rows: (n_local,) or (n_local, B) local signals."""

@@ -77,9 +77,10 @@ def oracle_filter(rows, cols, vals, n, kind, t, K):
     return po.Filter(L, kind, lam, t, K)
 
 
-def engine_filter(rows, cols, vals, n, kind, t, K):
+def engine_filter(rows, cols, vals, n, kind, t, K, ctx=None):
     import paper_2211_00805_b200 as gs
-    A = gs.SparseSymMatrix.from_arrays(n, rows, cols, vals)
+    A = gs.SparseSymMatrix.from_arrays(n, rows, cols, vals, ctx) if ctx is not None else \
+        gs.SparseSymMatrix.from_arrays(n, rows, cols, vals)
     lap = gs.laplacian(A, gs.LaplacianKind(kind))
     return gs.HeatFilter(lap, t, K), lap
 
