@@ -524,6 +524,10 @@ def run_engine(args):
             "max_rel_cost": _max_rel(rc_["cost"], refc["cost"]), "tolerance": 1e-9,
             "oracle_s": dtp}
 
+    legs = None
+    if args.config == 1 and not args.no_legs:
+        legs = partitioned_legs(args, ctx, stream, world, rank, local)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -560,11 +564,124 @@ def run_engine(args):
             "cpu_baseline": cpu,
             "parity": parity,
             "fp32_mode": fp32,
+            "partitioned": legs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+# --------------------------------------------------------------------------- N-GPU data planes
+def partitioned_legs(args, ctx, stream, world, rank, local):
+    """Strong-scaling legs of the two partitioned data planes, run after the main
+    measurement at every N, so a 1/2/4/8-GPU sweep of the default bench sees both:
+      * member_sharded: config-2 shape (R^30 mixture, 20 clusters, k = 15, t = 0.5, K = 30,
+        8 members) at n = --legs-bary-n; members split over the ranks, per sweep one allreduce of
+        the n-vector log-sum and one of the (error, status) pair over the engine's NCCL comm,
+        sweeps CUDA-graph captured with the collectives inside;
+      * row_partitioned: config-3 shape (swiss roll, k = 10, t = 1, K = 30, fp32, one pair) at
+        n = --legs-rows-n; rows split over the ranks, one neighbour-only halo exchange per
+        Chebyshev step (ncclSend/Recv), column reductions allreduced.
+    At N = 1 both run unpartitioned (no comm). Times are device events, max over ranks."""
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_00805_b200 as gs
+    from paper_2211_00805_b200 import _capi, workloads
+    from paper_2211_00805_b200.distributed import NcclComm, member_shard
+
+    dev = torch.device("cuda", local)
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    comm = NcclComm(ctx) if world > 1 else None
+    out = {}
+    # ---- member-sharded barycenter ------------------------------------------------------------
+    n, m, sweeps = args.legs_bary_n, 8, args.legs_sweeps
+    cfg = workloads.config2(n, m)
+    A, _ = gs.knn_gaussian_graph(cfg.mix.points, cfg.k, ctx=ctx)
+    lap = gs.laplacian(A, gs.LaplacianKind.combinatorial)
+    filt = gs.HeatFilter(lap, cfg.t, cfg.degree)
+    lo, hi = member_shard(m, world, rank)
+    Ml = torch.from_numpy(np.ascontiguousarray(cfg.members[lo:hi])).to(dev)
+    al = torch.full((hi - lo,), 1.0 / m, dtype=torch.float64, device=dev)
+    a = torch.full((n,), 1.0 / n, dtype=torch.float64, device=dev)
+    bary = torch.empty(n, dtype=torch.float64, device=dev)
+    it, cv, er = np.zeros(1, np.int32), np.zeros(1, np.int32), np.zeros(1)
+
+    def run_bary():
+        ctx.check(ctx.lib.gs_barycenter_ex(ctx.handle, filt._h, a.data_ptr(), Ml.data_ptr(), hi - lo,
+                                           al.data_ptr(), sweeps, TOL_RUN_ALL, _capi.GS_MEM_DEVICE,
+                                           comm.comm if comm else None, 0, bary.data_ptr(), None,
+                                           None, it.ctypes.data, cv.ctypes.data, er.ctypes.data))
+
+    ms = timed(run_bary, 2)
+    out["member_sharded"] = {
+        "workload": f"config-2 shape: R^30 mixture n={n}, k=15, t=0.5, K=30, {m} members x {sweeps} sweeps",
+        "value": 2 * sweeps / (ms / 1000.0), "unit": "barycenter sweeps/s", "scaling": "strong",
+        "members_per_rank": hi - lo, "comm": "engine NCCL (graph-captured allreduce)" if comm else "none (1 rank)"}
+    del filt, lap, A
+    # ---- row-partitioned fp32 Sinkhorn --------------------------------------------------------
+    n = args.legs_rows_n
+    roll = workloads.swiss_roll(n, 1)
+    A, _ = gs.knn_gaussian_graph(roll.points, 10, ctx=ctx)
+    lap = gs.laplacian(A, gs.LaplacianKind.combinatorial)
+    filt = gs.HeatFilter(lap, 1.0, 30)
+    mu = workloads.bump_in_s(roll, 2 * math.pi, 0.5)
+    nu = workloads.bump_in_s(roll, 2 * math.pi + 0.5, 0.5)
+    part = gs.RowPartition(filt, world, rank, ctx=ctx) if world > 1 else None
+    vid = part.vertices.astype(np.int64) if part is not None else np.arange(n)
+    Md = torch.from_numpy(mu[vid].copy()).to(dev)
+    Nd = torch.from_numpy(nu[vid].copy()).to(dev)
+    ad = torch.full((vid.size,), 1.0 / n, dtype=torch.float64, device=dev)
+    vd = torch.empty(vid.size, dtype=torch.float64, device=dev)
+    wd = torch.empty_like(vd)
+    dsc = torch.empty(3, dtype=torch.float64, device=dev)
+    dsi = torch.empty(2, dtype=torch.int32, device=dev)
+    fp, fs = C.c_int(), C.c_int()
+    flags = _capi.GS_FLAG_NO_STAGNATION_ABORT | _capi.GS_FLAG_FP32
+
+    def run_rows():
+        p0, pi = dsc.data_ptr(), dsi.data_ptr()
+        outs = (vd.data_ptr(), wd.data_ptr(), p0, p0 + 8, pi, pi + 4, p0 + 16, C.byref(fp), C.byref(fs))
+        if part is None:
+            rc = ctx.lib.gs_sinkhorn(ctx.handle, filt._h, ad.data_ptr(), Md.data_ptr(), Nd.data_ptr(), 1,
+                                     sweeps, TOL_RUN_ALL, flags, _capi.GS_MEM_DEVICE, *outs)
+        else:
+            rc = ctx.lib.gs_part_sinkhorn(ctx.handle, part._h, comm.comm, ad.data_ptr(), Md.data_ptr(),
+                                          Nd.data_ptr(), 1, sweeps, TOL_RUN_ALL, flags,
+                                          _capi.GS_MEM_DEVICE, *outs)
+        ctx.check(rc)
+
+    ms = timed(run_rows, 2)
+    out["row_partitioned"] = {
+        "workload": f"config-3 shape: swiss roll n={n}, k=10, t=1, K=30, fp32 (32-bit words), 1 pair x {sweeps} sweeps",
+        "value": 2 * sweeps / (ms / 1000.0), "unit": "sweeps/s", "scaling": "strong",
+        "rows_per_rank": int(vid.size),
+        "comm": "engine NCCL (neighbour-only send/recv halo per step)" if comm else "none (1 rank)"}
+    if comm:
+        comm.close()
+    return out
 
 
 # --------------------------------------------------------------------------- config 2 (barycenter)
@@ -580,7 +697,7 @@ def run_engine_bary(args):
 
     import paper_2211_00805_b200 as gs
     from paper_2211_00805_b200 import _capi, workloads
-    from paper_2211_00805_b200.distributed import TorchAllreduce, member_shard
+    from paper_2211_00805_b200.distributed import NcclComm, member_shard
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -627,17 +744,16 @@ def run_engine_bary(args):
     it = np.zeros(1, np.int32)
     conv = np.zeros(1, np.int32)
     err = np.zeros(1)
-    hook = TorchAllreduce(None, device_buffers=True)
-    # one rank has nothing to reduce: without the hook the engine replays sweeps as a CUDA graph
-    comm_arg = C.byref(hook.comm) if world > 1 else None
+    # the engine's own NCCL communicator: allreduces on the engine stream, sweeps stay
+    # graph-captured; one rank has nothing to reduce and runs without a comm
+    hook = NcclComm(ctx) if world > 1 else None
+    comm_arg = hook.comm if world > 1 else None
 
     def step():
         rc = lib.gs_barycenter_ex(ctx.handle, filt._h, a.data_ptr(), Mloc.data_ptr(), hi - lo,
                                   al.data_ptr(), args.sweeps, TOL_RUN_ALL, _capi.GS_MEM_DEVICE,
                                   comm_arg, 0, bary.data_ptr(), Vo.data_ptr(),
                                   Wo.data_ptr(), it.ctypes.data, conv.ctypes.data, err.ctypes.data)
-        if hook.error is not None:
-            raise hook.error
         ctx.check(rc)
 
     def max_over_ranks(x):
@@ -686,8 +802,6 @@ def run_engine_bary(args):
                                   alh.data_ptr(), args.sweeps, TOL_RUN_ALL, _capi.GS_MEM_HOST,
                                   comm_arg, 0, bh.data_ptr(), Vh.data_ptr(),
                                   Wh.data_ptr(), it.ctypes.data, conv.ctypes.data, err.ctypes.data)
-        if hook.error is not None:
-            raise hook.error
         ctx.check(rc)
 
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
@@ -766,7 +880,7 @@ def run_engine_bary_dist(args):
 
     import paper_2211_00805_b200 as gs
     from paper_2211_00805_b200 import _capi, workloads
-    from paper_2211_00805_b200.distributed import TorchAllreduce, member_shard
+    from paper_2211_00805_b200.distributed import NcclComm, member_shard
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -807,8 +921,8 @@ def run_engine_bary_dist(args):
     dsc = torch.empty(3, dtype=torch.float64, device=dev)
     dsi = torch.empty(2, dtype=torch.int32, device=dev)
     it, conv, err = np.zeros(1, np.int32), np.zeros(1, np.int32), np.zeros(1)
-    hook = TorchAllreduce(None, device_buffers=True)
-    comm_arg = C.byref(hook.comm) if world > 1 else None
+    hook = NcclComm(ctx) if world > 1 else None  # the engine's own NCCL communicator
+    comm_arg = hook.comm if world > 1 else None
     fp, fs = C.c_int(), C.c_int()
     flags = _capi.GS_FLAG_NO_STAGNATION_ABORT
 
@@ -817,8 +931,6 @@ def run_engine_bary_dist(args):
                                   args.sweeps, TOL_RUN_ALL, _capi.GS_MEM_DEVICE, comm_arg, 0,
                                   out.data_ptr(), Vo.data_ptr(), Wo.data_ptr(), it.ctypes.data,
                                   conv.ctypes.data, err.ctypes.data)
-        if hook.error is not None:
-            raise hook.error
         ctx.check(rc)
 
     def step():
@@ -878,8 +990,6 @@ def run_engine_bary_dist(args):
                                       args.sweeps, TOL_RUN_ALL, _capi.GS_MEM_HOST, comm_arg, 0,
                                       out.data_ptr(), Vh.data_ptr(), Wh.data_ptr(), it.ctypes.data,
                                       conv.ctypes.data, err.ctypes.data)
-            if hook.error is not None:
-                raise hook.error
             ctx.check(rc)
         ctx.check(lib.gs_sinkhorn(ctx.handle, filt._h, ah.data_ptr(), bah.data_ptr(), bbh.data_ptr(), 1,
                                   args.sweeps, TOL_RUN_ALL, flags | _capi.GS_FLAG_SINGLE,
@@ -942,7 +1052,7 @@ def run_engine_rows(args):
 
     import paper_2211_00805_b200 as gs
     from paper_2211_00805_b200 import _capi, workloads
-    from paper_2211_00805_b200.distributed import TorchComm
+    from paper_2211_00805_b200.distributed import NcclComm
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -979,8 +1089,8 @@ def run_engine_rows(args):
     if world > 1:
         part = gs.RowPartition(filt, world, rank, ctx=ctx)
         vid = part.vertices.astype(np.int64)
-        hook = TorchComm(None, device_buffers=True)
-        comm = C.byref(hook.comm)
+        hook = NcclComm(ctx)  # the engine's own NCCL communicator (neighbour-only halo exchange)
+        comm = hook.comm
         nnz_loc = part.nnz_local
     else:
         vid = np.arange(n)
@@ -1012,8 +1122,6 @@ def run_engine_rows(args):
         else:
             rc = lib.gs_part_sinkhorn(ctx.handle, part._h, comm, av, M, N, 1, args.sweeps,
                                       TOL_RUN_ALL, flags, mem, *outs)
-        if hook is not None and hook.error is not None:
-            raise hook.error
         ctx.check(rc)
 
     def step():
@@ -1142,6 +1250,10 @@ def main():
     ap.add_argument("--cpu-sweeps", type=int, default=1)
     ap.add_argument("--ref-sweeps", type=int, default=2)
     ap.add_argument("--parity-pairs", type=int, default=4)
+    ap.add_argument("--no-legs", action="store_true", help="skip the partitioned data-plane legs")
+    ap.add_argument("--legs-bary-n", type=int, default=200_000)
+    ap.add_argument("--legs-rows-n", type=int, default=2_000_000)
+    ap.add_argument("--legs-sweeps", type=int, default=40)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp32", action="store_true")
     ap.add_argument("--config", type=int, default=1, choices=[0, 1, 2, 3, 4])
@@ -1151,6 +1263,17 @@ def main():
                          "replayed as CUDA graphs are not split into launches: the timed launches "
                          "are each call's initial apply)")
     args = ap.parse_args()
+    # N GPUs of one node: one process per GPU. Without a launcher around us, re-exec under
+    # torch.distributed.run (127.0.0.1 rendezvous); under one, the launcher's world must be N.
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(_free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
+    world_env = int(os.environ.get("WORLD_SIZE", "1"))
+    if world_env != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world_env}"}))
+        return 2
     if args.config == 0:  # BASELINE.json configs[0]: n=2000, one pair, 100 sweeps
         if args.n == 200_000:
             args.n = 2000
