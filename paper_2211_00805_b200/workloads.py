@@ -205,6 +205,27 @@ class Config4:
     sweeps: int = 200
 
 
+def config4_from_mixture(mix: Mixture, m: int = 16, member_seed: int = 6) -> Config4:
+    """Config 4's two groups on a given 40-component mixture (config4's member draws)."""
+    rng = Rng(member_seed)
+    lab = mix.labels
+    n = lab.size
+
+    def uniform_over(clusters):
+        w = np.isin(lab, clusters).astype(np.float64)
+        return w / w.sum()
+
+    ga = np.empty((m, n))
+    gb = np.empty((m, n))
+    for q in range(m):
+        ga[q] = _normalise(uniform_over(_cluster_choice(rng, range(0, 20), 10)))
+    for q in range(m):
+        base = uniform_over(_cluster_choice(rng, range(0, 20), 10))
+        shift = uniform_over(_cluster_choice(rng, range(20, 40), 10))
+        gb[q] = _normalise(0.8 * base + 0.2 * shift)
+    return Config4(mix, ga, gb)
+
+
 def config4(n: int = 4_000_000, m: int = 16, d: int = 30, components: int = 40, seed: int = 5,
             member_seed: int = 6) -> Config4:
     """Config 4: 40-component Gaussian mixture in R^30 (means ~ N(0, 5^2 I), sigma = 1). Decisions

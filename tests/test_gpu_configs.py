@@ -129,3 +129,60 @@ def test_config2_shape_reduced(gs):
                ref["barycenter"][ref["barycenter"] > 1e-200]) <= 1e-9
     assert np.array_equal(res.barycenter.weights <= 1e-200, ref["barycenter"] <= 1e-200)
     assert rel(res.marginal_error, ref["marginal_error"]) <= 1e-9
+
+
+def _mixture_filters(gs, mix, k, t):
+    A, Ao, _, _ = _graph_pair(gs, mix.points, k, 1)
+    n = mix.points.shape[0]
+    Au = gs.SparseSymMatrix.from_csr(n, Ao.offs, Ao.cols, Ao.vals)
+    lap = gs.laplacian(Au, gs.LaplacianKind.combinatorial)
+    Lo, lam_o, _ = po.laplacian(Ao, 0)
+    assert lap.lambda_max_bound == lam_o
+    return gs.HeatFilter(lap, t, 30), po.Filter(Lo, 0, lam_o, t, 30)
+
+
+def test_config2_shape_companion_shared_clusters(gs):
+    """Well-posed companion of config 2 (SURVEY §7 hard part 1): R^30 mixture with overlapping
+    clusters (means ~ N(0, 1), so the k = 15 graph is connected), 8 members uniform over random
+    60% subsets of 4 clusters drawn from a shared pool of 6; the barycenter converges instead of
+    hitting the 1e-300 floor. Every barycenter weight and V within 1e-9 of the oracle."""
+    from paper_2211_00805_b200 import workloads
+    mix = workloads.gaussian_mixture(4000, 30, 20, 3, mean_scale=1.0)
+    members = workloads.cluster_subset_members(mix, 8, 4, 0.6, 4, cluster_pool=range(6))
+    f, fo = _mixture_filters(gs, mix, 15, 0.5)
+    a = np.full(4000, 1.0 / 4000)
+    fam = gs.DistributionFamily([gs.Distribution(m, validate=False) for m in members])
+    res = gs.sinkhorn_barycenter(f, fam, a, gs.SinkhornParams(200, 1e-9))
+    ref = po.barycenter(fo, a, members, None, 200, 1e-9)
+    assert res.iterations == ref["iterations"]
+    assert res.barycenter.weights.min() > 1e-200  # not floor-dominated
+    assert rel(res.barycenter.weights, ref["barycenter"]) <= 1e-9
+    # the converged marginal error (~1e-9) is a difference of O(1) quantities: absolute bound
+    assert abs(res.marginal_error - ref["marginal_error"]) <= 1e-12
+
+
+def test_config4_shape_barycentric_distance(gs):
+    """Config-4 shape at reduced size (R^30, 40 overlapping clusters, k = 15, t = 0.5): two
+    6-member groups as specified (group B with 20% of its mass shifted onto clusters 20-39), both
+    barycenters and the geodesic Sinkhorn distance between them (barycenter.cpp:101-107) within
+    1e-9 of the oracle."""
+    from paper_2211_00805_b200 import workloads
+    n, m = 3000, 6
+    mix = workloads.gaussian_mixture(n, 30, 40, 5, mean_scale=1.0)
+    cfg = workloads.config4_from_mixture(mix, m, member_seed=6)
+    f, fo = _mixture_filters(gs, mix, 15, 0.5)
+    a = np.full(n, 1.0 / n)
+    params = gs.SinkhornParams(200, 1e-9)
+    fa = gs.DistributionFamily([gs.Distribution(x, validate=False) for x in cfg.group_a])
+    fb = gs.DistributionFamily([gs.Distribution(x, validate=False) for x in cfg.group_b])
+    ba = gs.sinkhorn_barycenter(f, fa, a, params)
+    bb = gs.sinkhorn_barycenter(f, fb, a, params)
+    d = gs.barycentric_distance(f, fa, fb, a, params)
+    ra = po.barycenter(fo, a, cfg.group_a, None, 200, 1e-9)
+    rb = po.barycenter(fo, a, cfg.group_b, None, 200, 1e-9)
+    assert rel(ba.barycenter.weights, ra["barycenter"]) <= 1e-9
+    assert rel(bb.barycenter.weights, rb["barycenter"]) <= 1e-9
+    rd = po.sinkhorn_batch(fo, a, ra["barycenter"][None], rb["barycenter"][None], 200, 1e-9,
+                           single_style=True)
+    assert np.isfinite(d) and d > 0
+    assert rel(d, rd["cost"][0]) <= 1e-9
