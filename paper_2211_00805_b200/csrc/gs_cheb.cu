@@ -18,6 +18,7 @@
 #include "gs_internal.cuh"
 #include "gs_step.cuh"
 #include "gs_win.cuh"
+#include "gs_persist.cuh"
 
 using namespace gsk;
 
@@ -1214,6 +1215,92 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
     k_sk_control<<<1, 1, 0, s>>>(C);
     gs_launch_end(ctx, 1);
   };
+  // Small one-pair fp64 problems (config 0): every sweep in one persistent cluster kernel
+  // (gs_persist.cuh); GS_PERSIST=0 keeps the per-step kernels.
+  bool persisted = false;
+  if constexpr (sizeof(S) == 8) {
+    const char* penv = getenv("GS_PERSIST");
+    const bool want = penv ? penv[0] != '0' : true;
+    static const int CL = [] {  // CTAs per cluster (GS_PERSIST_CLUSTER: 8 portable, 16 opt-in)
+      const char* e = getenv("GS_PERSIST_CLUSTER");
+      const int v = e ? atoi(e) : 16;
+      return v >= 2 && v <= kPersistClusterMax ? v : 16;
+    }();
+    const int kPersistCluster = CL;
+    const int R = (n + kPersistCluster - 1) / kPersistCluster;
+    if (want && P == 1 && w.GW == 1 && n >= kPersistCluster && R <= kPersistMaxRows && n <= kPersistMaxN) {
+      const gs_graph* G = f->lay[w.lay].perm;
+      std::vector<int> ho(n + 1);
+      GS_CUDA(ctx, cudaMemcpyAsync(ho.data(), G->offs, (size_t)(n + 1) * sizeof(int), cudaMemcpyDeviceToHost, s));
+      GS_CUDA(ctx, cudaStreamSynchronize(s));
+      // ELL slice of the largest CTA: per warp of 32 rows, 32 x its longest row
+      int64_t maxne = 0;
+      for (int r = 0; r < kPersistCluster; ++r) {
+        const int r0 = std::min(n, r * R), r1 = std::min(n, r0 + R);
+        int64_t ne = 0;
+        for (int w0 = r0; w0 < r1; w0 += 32) {
+          int md = 0;
+          for (int i = w0; i < std::min(r1, w0 + 32); ++i) md = std::max(md, ho[i + 1] - ho[i]);
+          ne += 32 * (int64_t)md;
+        }
+        maxne = std::max(maxne, ne);
+      }
+      const size_t smem = (size_t)persist_rep_offset(n) + (size_t)2 * n * 8 + (size_t)maxne * 12;
+      if (smem <= 220 * 1024) {  // + 768 bytes of static shared memory
+        static bool attr = [] {
+          cudaFuncSetAttribute(k_sk_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+          cudaFuncSetAttribute(k_sk_persist, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+          return true;
+        }();
+        (void)attr;
+        PersistArgs PA{};
+        PA.n = n;
+        PA.R = R;
+        PA.K = f->degree;
+        PA.max_iter = max_iter;
+        PA.no_abort = (flags & GS_FLAG_NO_STAGNATION_ABORT) ? 1 : 0;
+        PA.tol = tol;
+        PA.slack = Prec<S>::slack;
+        PA.coeffs = f->d_coeffs;
+        PA.offs = G->offs;
+        PA.cols = G->cols;
+        PA.vals = G->vals;
+        PA.a = da;
+        PA.M = M.get();
+        PA.N = N.get();
+        PA.V0 = V[0].get();
+        PA.V1 = V[1].get();
+        PA.W = W.get();
+        PA.T0 = reinterpret_cast<const double*>(w.T[a0].get());
+        PA.thr = w.thr.get();
+        PA.iters = iters.get();
+        PA.conv = conv.get();
+        PA.stag = stag.get();
+        PA.final_sweep = final_sweep.get();
+        PA.err_out = errv.get();
+        PA.status = w.status.get();
+        PA.knp_code = knp;
+        const int threads = (R + 31) / 32 * 32;
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3(kPersistCluster);
+        lc.blockDim = dim3(threads);
+        lc.dynamicSmemBytes = smem;
+        lc.stream = s;
+        cudaLaunchAttribute la[1];
+        la[0].id = cudaLaunchAttributeClusterDimension;
+        la[0].val.clusterDim.x = kPersistCluster;
+        la[0].val.clusterDim.y = 1;
+        la[0].val.clusterDim.z = 1;
+        lc.attrs = la;
+        lc.numAttrs = 1;
+        gs_launch_begin(ctx, 0);
+        GS_CUDA(ctx, cudaLaunchKernelEx(&lc, k_sk_persist, PA));
+        gs_launch_end(ctx, 0);
+        GS_CUDA(ctx, cudaGetLastError());
+        persisted = true;
+      }
+    }
+  }
   // Two sweeps (odd, even parity) are captured once as a CUDA graph and replayed: one host launch
   // per two sweeps instead of ~126, so the GPU never waits on the host's launch path (small
   // problems are launch-latency bound; on config 1 per-kernel launches left 11-25% of the GPU idle
@@ -1223,7 +1310,7 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
   const bool use_graph = genv ? genv[0] != '0' : true;
   cudaGraphExec_t gexec = nullptr;
   int64_t graph_launches = 0;
-  if (use_graph && max_iter >= 2) {
+  if (!persisted && use_graph && max_iter >= 2) {
     cudaGraph_t graph = nullptr;
     const int64_t l0 = ctx->launches;
     ctx->capturing = true;
@@ -1244,7 +1331,7 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
     }
   }
   const int step_sweeps = gexec ? 2 : 1;
-  for (int sweep = 1, it = 0; sweep <= max_iter; sweep += step_sweeps, ++it) {
+  for (int sweep = 1, it = 0; !persisted && sweep <= max_iter; sweep += step_sweeps, ++it) {
     if (it >= 2) {
       const int slot = (it - 2) & 1;
       cudaEventSynchronize(ev[slot]);
