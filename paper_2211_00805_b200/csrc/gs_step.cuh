@@ -557,7 +557,8 @@ __device__ __forceinline__ void finish_row_ops(const StepArgs& A, int g, int row
                                                double (&er)[Lay<GW, S>::VEC],
                                                const S (&tps)[Lay<GW, S>::VEC],
                                                const S (&t2s)[Lay<GW, S>::VEC],
-                                               const S (&a0s)[Lay<GW, S>::VEC]);
+                                               const S (&a0s)[Lay<GW, S>::VEC],
+                                               const double* epi = nullptr);
 
 template <typename S, int GW, int MODE>
 __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, int q,
@@ -609,7 +610,10 @@ __device__ __forceinline__ void finish_row_ops(const StepArgs& A, int g, int row
                                                double (&er)[Lay<GW, S>::VEC],
                                                const S (&tps)[Lay<GW, S>::VEC],
                                                const S (&t2s)[Lay<GW, S>::VEC],
-                                               const S (&a0s)[Lay<GW, S>::VEC]) {
+                                               const S (&a0s)[Lay<GW, S>::VEC],
+                                               const double* epi) {
+  // epi (optional): the Sinkhorn epilogue's operands already in registers -- M[row] (VEC),
+  // Vcur[row] (VEC, PHI only), a[row] -- loaded one row ahead by the caller (k_cheb_win)
   using L = Lay<GW, S>;
   constexpr int VEC = L::VEC;
   using P = Prec<S>;
@@ -653,11 +657,21 @@ __device__ __forceinline__ void finish_row_ops(const StepArgs& A, int g, int row
     for (int e = 0; e < VEC; ++e) mn[e] = fmin(mn[e], ac[e]);
     if constexpr (MODE == MODE_SK_PSI || MODE == MODE_SK_PHI) {
       double op1[VEC], nx[VEC], t0[VEC];
-      ld_vec<double, VEC>(A.M + idx, op1);
-      const double ai = __ldg(A.a + row);
+      if (epi) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) op1[e] = epi[e];
+      } else {
+        ld_vec<double, VEC>(A.M + idx, op1);
+      }
+      const double ai = epi ? epi[2 * VEC] : __ldg(A.a + row);
       if constexpr (MODE == MODE_SK_PHI) {
         double v[VEC];
-        ld_vec_rw<double, VEC>(A.Vcur + idx, v);
+        if (epi) {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) v[e] = epi[VEC + e];
+        } else {
+          ld_vec_rw<double, VEC>(A.Vcur + idx, v);
+        }
 #pragma unroll
         for (int e = 0; e < VEC; ++e) er[e] = er[e] + fabs(v[e] * ac[e] - op1[e]);  // transport.cpp:184
       }

@@ -299,20 +299,38 @@ __global__ void __launch_bounds__(kWinThreads, 1)
     const bool read_acc = A.acc_terms > 0 && !A.acc_init;
     const bool read_t2 = A.k >= 2;
     int r = R0 + warp * RPW + sub;
+    constexpr bool SK = MODE == MODE_SK_PSI || MODE == MODE_SK_PHI;
+    constexpr int NE = SK ? 2 * VEC + 1 : 1;  // epilogue operands: M[row], Vcur[row], a[row]
     S t2s[VEC], a0s[VEC];
-    auto own_ops = [&](int row, S (&t2)[VEC], S (&a0)[VEC]) {
+    double eps_[NE];
+    auto own_ops = [&](int row, S (&t2)[VEC], S (&a0)[VEC], double (&ep)[NE]) {
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
         t2[e] = S(0);
         a0[e] = S(0);
       }
+#pragma unroll
+      for (int e = 0; e < NE; ++e) ep[e] = 0.0;
       if (row < R1) {
         const size_t idx = gbase + (size_t)row * GW;
         if (read_t2) ld_vec_rw<S, VEC>(static_cast<const S*>(A.Tout) + idx, t2);
         if (read_acc) ld_vec_rw<S, VEC>(static_cast<const S*>(A.acc) + idx, a0);
+        if constexpr (SK) {
+          double m[VEC];
+          ld_vec<double, VEC>(A.M + idx, m);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) ep[e] = m[e];
+          if constexpr (MODE == MODE_SK_PHI) {
+            double v[VEC];
+            ld_vec_rw<double, VEC>(A.Vcur + idx, v);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) ep[VEC + e] = v[e];
+          }
+          ep[2 * VEC] = __ldg(A.a + row);
+        }
       }
     };
-    own_ops(r, t2s, a0s);
+    own_ops(r, t2s, a0s, eps_);
     for (int j = b0; j < b1; ++j) {
       const int jj = j - b0, s = jj % NST;
       const WinBlk bk = WA.blk[j];
@@ -328,7 +346,8 @@ __global__ void __launch_bounds__(kWinThreads, 1)
         const int row = r;
         r += NSLOT;
         S t2n[VEC], a0n[VEC];
-        own_ops(r, t2n, a0n);  // next row's operands in flight during this row
+        double epn[NE];
+        own_ops(r, t2n, a0n, epn);  // next row's operands in flight during this row
         const int pr = so[row], pn = so[row + 1];
         const int qe = pn & ~3, npad = pr & 3;
         const S* rl = ring + q * VEC;
@@ -393,13 +412,15 @@ __global__ void __launch_bounds__(kWinThreads, 1)
         } else {
           S tps[VEC];
           lds_vec<S, VEC>(rl + (int)sw[row] * GW, tps);
-          finish_row_ops<S, GW, MODE>(A, g, row, q, y, mn, mx, er, tps, t2s, a0s);
+          finish_row_ops<S, GW, MODE>(A, g, row, q, y, mn, mx, er, tps, t2s, a0s, SK ? eps_ : nullptr);
         }
 #pragma unroll
         for (int e = 0; e < VEC; ++e) {
           t2s[e] = t2n[e];
           a0s[e] = a0n[e];
         }
+#pragma unroll
+        for (int e = 0; e < NE; ++e) eps_[e] = epn[e];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
