@@ -929,9 +929,18 @@ const void* layout_vals(const gs_layout& L) {
 
 // One full filter application on the workspace: T0 in T[a0]; K steps; the last step uses `mode`
 // with the given epilogue operands. Returns the buffer index holding the next T_0.
+// BARY_PSI applies: the log-domain geometric mean fused into the last step's epilogue
+struct BaryFuse {
+  double* lb;
+  const double* alphas;
+  unsigned long long* lbmax;
+  int m;
+};
+
 template <typename S>
 int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, const double* a,
-              const double* M, const double* Vcur, double* Wout, bool use_active, bool use_status) {
+              const double* M, const double* Vcur, double* Wout, bool use_active, bool use_status,
+              const BaryFuse* bf = nullptr) {
   const gs_layout& Ly = f->lay[w.lay];
   const gs_graph* G = Ly.perm;
   const int K = f->degree;
@@ -963,6 +972,12 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
   A.Vcur = Vcur;
   A.Wout = Wout;
   A.psi = w.psi64.get();
+  if (bf && mode == MODE_BARY_PSI) {
+    A.lb = bf->lb;
+    A.alphas = bf->alphas;
+    A.lbmax = bf->lbmax;
+    A.m = bf->m;
+  }
   WinArgs WA{};
   if (w.win) {
     WA.blk = static_cast<const WinBlk*>(w.ws->blk);
@@ -1493,24 +1508,34 @@ int barycenter_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, cons
   int hook_rc = 0;
   // one sweep (barycenter.cpp:70-86); `parity` selects the V ping-pong buffers. Kernels of sweeps
   // past convergence / max_iter exit on the status word (or recompute unchanged values).
+  // the log-sum (and, unsharded, its max) computed in the psi apply's last-step epilogue for one
+  // column group (m <= 64); GS_BARY_UNFUSED=1 keeps the separate passes (k_bary_lb, k_max_key)
+  const bool fuse = w.G == 1 && !(getenv("GS_BARY_UNFUSED") && atoi(getenv("GS_BARY_UNFUSED")) != 0);
+  const BaryFuse bfuse{lb.get(), dal.get(), lbmax.get(), m};
   auto issue_sweep = [&](int parity) -> int {
     // psi = H(a * V) (barycenter.cpp:71)
-    a0 = run_apply<S>(ctx, f, w, a0, MODE_BARY_PSI, da, nullptr, nullptr, nullptr, false, true);
+    if (fuse) cudaMemsetAsync(lbmax.get(), 0, sizeof(unsigned long long), s);
+    a0 = run_apply<S>(ctx, f, w, a0, MODE_BARY_PSI, da, nullptr, nullptr, nullptr, false, true,
+                      fuse ? &bfuse : nullptr);
     run_finalize<S>(ctx, w, 1, 0, 0, knp, false);
     // log-domain geometric mean (barycenter.cpp:75-82)
-    gs_launch_begin(ctx, 1);
     // psi in fp64: acc in the fp64 mode, psi64 in the 32-bit mode
     const double* psi = w.kF32 ? w.psi64.get() : reinterpret_cast<const double*>(w.acc.get());
-    k_bary_lb<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(psi, dal.get(), n, m, w.GW, lb.get(), w.status.get());
-    gs_launch_end(ctx, 1);
+    if (!fuse) {
+      gs_launch_begin(ctx, 1);
+      k_bary_lb<<<(n + kThreads - 1) / kThreads, kThreads, 0, s>>>(psi, dal.get(), n, m, w.GW, lb.get(), w.status.get());
+      gs_launch_end(ctx, 1);
+    }
     if (hooked) {
       const int rc = comm->allreduce(comm->user, lb.get(), n, 0, (void*)s);
       if (rc) return rc;
     }
-    cudaMemsetAsync(lbmax.get(), 0, sizeof(unsigned long long), s);
-    gs_launch_begin(ctx, 1);
-    k_max_key<<<grid_for(n), kThreads, 0, s>>>(lb.get(), n, lbmax.get());
-    gs_launch_end(ctx, 1);
+    if (!fuse || hooked) {  // the max of the (allreduced) log-sum
+      cudaMemsetAsync(lbmax.get(), 0, sizeof(unsigned long long), s);
+      gs_launch_begin(ctx, 1);
+      k_max_key<<<grid_for(n), kThreads, 0, s>>>(lb.get(), n, lbmax.get());
+      gs_launch_end(ctx, 1);
+    }
     gs_launch_begin(ctx, 1);
     k_bary_exp<<<(unsigned)nchunks, kThreads, 0, s>>>(lb.get(), lbmax.get(), n, bary.get(), part.get(), w.status.get());
     gs_launch_end(ctx, 1);

@@ -360,6 +360,13 @@ struct StepArgs {  // vector pointers are S* of the launch's precision
   const double* Vcur;   // PHI: V of this sweep
   double* Wout;         // PSI: W; PHI: V of the next sweep
   double* psi;          // BARY_PSI in the 32-bit mode: psi in fp64 (the fp64 mode uses acc)
+  // BARY_PSI, one column group: the log-domain geometric mean fused into the epilogue
+  // (barycenter.cpp:75-78): lb[row] = sum_c alphas[c] log(clamp(psi[row][c])) in member order,
+  // and the max of lb over the grid in *lbmax (order-preserving key); nullptr = separate passes
+  double* lb;
+  const double* alphas;
+  unsigned long long* lbmax;
+  int m;
 };
 
 template <typename S, int GW, int MODE>
@@ -689,6 +696,29 @@ __device__ __forceinline__ void finish_row_ops(const StepArgs& A, int g, int row
     } else {  // MODE_BARY_PSI: psi kept in fp64 for the log-domain mean
       if constexpr (sizeof(S) == 4) st_vec<double, VEC>(A.psi + idx, ac);
       else st_vec<S, VEC>(static_cast<S*>(A.acc) + idx, ac);
+      if (A.lb) {
+        // fused log-domain geometric mean (barycenter.cpp:75-78; k_bary_lb's arithmetic): the
+        // row's lanes hold its m <= GW columns; lane 0 of the row folds them in member order
+        constexpr int LPR = L::LPR;
+        const int lane = threadIdx.x & 31;
+        const unsigned gmask = LPR == 32 ? 0xffffffffu : (((1u << LPR) - 1u) << (lane / LPR * LPR));
+        double lg[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) lg[e] = log(fmin(fmax(ac[e], GS_FLOOR), GS_CEIL));
+        double acc = 0.0;
+        for (int c = 0; c < A.m; ++c) {
+          double mine = lg[0];
+#pragma unroll
+          for (int e = 1; e < VEC; ++e)
+            if (c % VEC == e) mine = lg[e];
+          const double v = LPR == 1 ? mine : __shfl_sync(gmask, mine, c / VEC, LPR);
+          acc = fma(A.alphas[c], v, acc);
+        }
+        if (q == 0) {
+          A.lb[row] = acc;
+          mx[0] = fmax(mx[0], acc);
+        }
+      }
     }
   }
 }
@@ -732,6 +762,8 @@ __device__ __forceinline__ void block_epilogue(const StepArgs& A, int g, int til
     const int col = g * GW + c;
     atomicMin(A.cs.cmin + col, dkey(a_mn));
     if constexpr (MODE == MODE_SK_PSI || MODE == MODE_SK_PHI) atomicMax(A.cs.cmax + col, dkey(a_mx));
+    if constexpr (MODE == MODE_BARY_PSI)
+      if (A.lbmax && c == 0) atomicMax(A.lbmax, dkey(a_mx));  // max of the fused log-sum
     if constexpr (MODE == MODE_SK_PHI) A.cs.part_err[(size_t)tile * A.Bpad + col] = a_er;
   }
 }
@@ -774,7 +806,7 @@ __global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0
 #pragma unroll
   for (int e = 0; e < VEC; ++e) {
     mn[e] = INFINITY;
-    mx[e] = 0.0;
+    mx[e] = MODE == MODE_BARY_PSI ? -INFINITY : 0.0;  // BARY_PSI: max of the fused log-sum
     er[e] = 0.0;
   }
   const int base = A.row0 + tl * (BLOCK_ROWS * RPC) + warp * RPW + sub;
@@ -973,7 +1005,7 @@ __global__ void __launch_bounds__(kBlkWarps * 32, MODE != MODE_NONE ? 0 : GS_BLK
 #pragma unroll
   for (int e = 0; e < VEC; ++e) {
     mn[e] = INFINITY;
-    mx[e] = 0.0;
+    mx[e] = MODE == MODE_BARY_PSI ? -INFINITY : 0.0;  // BARY_PSI: max of the fused log-sum
     er[e] = 0.0;
   }
   const int r0 = A.row0 + (tl * kBlkWarps + warp) * kBlkRows;
@@ -1083,7 +1115,7 @@ __global__ void __launch_bounds__(kThreads) k_cheb_step_w1(const StepArgs A) {
   if (A.cs.gactive && A.cs.gactive[g] == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int row = A.row0 + tl * (kThreads / 32) + warp;
-  double mn[1] = {INFINITY}, mx[1] = {0.0}, er[1] = {0.0};
+  double mn[1] = {INFINITY}, mx[1] = {MODE == MODE_BARY_PSI ? -INFINITY : 0.0}, er[1] = {0.0};
   if (row < A.n) {
     const S* __restrict__ Tp = static_cast<const S*>(A.Tprev) + (size_t)g * A.ld;
     const S* __restrict__ vals = static_cast<const S*>(A.vals);

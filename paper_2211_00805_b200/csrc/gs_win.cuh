@@ -185,6 +185,8 @@ __device__ __forceinline__ void win_epilogue(const StepArgs& A, int g, int tile,
     const int col = g * GW + c;
     atomicMin(A.cs.cmin + col, dkey(a_mn));
     if constexpr (MODE == MODE_SK_PSI || MODE == MODE_SK_PHI) atomicMax(A.cs.cmax + col, dkey(a_mx));
+    if constexpr (MODE == MODE_BARY_PSI)
+      if (A.lbmax && c == 0) atomicMax(A.lbmax, dkey(a_mx));  // max of the fused log-sum
     if constexpr (MODE == MODE_SK_PHI) A.cs.part_err[(size_t)tile * A.Bpad + col] = a_er;
   }
 }
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(kWinThreads, 1)
 #pragma unroll
   for (int e = 0; e < VEC; ++e) {
     mn[e] = INFINITY;
-    mx[e] = 0.0;
+    mx[e] = MODE == MODE_BARY_PSI ? -INFINITY : 0.0;  // BARY_PSI: max of the fused log-sum
     er[e] = 0.0;
   }
   const int64_t grow = (int64_t)g * A.ld;  // first tensor-map row of this column group

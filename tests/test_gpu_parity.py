@@ -485,3 +485,29 @@ def test_hub_rows_span_several_chunks(gs, width):
     y32 = f.apply(X32, fp32=True)
     y64 = fo.apply(X32)
     assert np.max(np.abs(y32 - y64)) <= 1e-4 * np.max(np.abs(y64))
+
+
+@pytest.mark.parametrize("m", [1, 8, 40, 64])
+def test_barycenter_fused_log_mean_bit_identical(m, monkeypatch):
+    """The log-domain geometric mean fused into the psi apply's last-step epilogue
+    (barycenter.cpp:75-78; StepArgs::lb) gives bit-identical barycenters and scalings to the
+    separate k_bary_lb / k_max_key passes (GS_BARY_UNFUSED=1), on every step-kernel layout
+    (m = 1: warp-per-row kernel; 8: narrow rows; 40/64: windowed wide rows)."""
+    import paper_2211_00805_b200 as gs
+    from paper_2211_00805_b200.rng import Rng
+    from helpers import engine_filter, random_connected_graph, random_distribution
+
+    n = 700
+    r, c, v = random_connected_graph(n, 91)
+    f, _ = engine_filter(r, c, v, n, 1, 0.6, 30)
+    rng = Rng(92)
+    fam = gs.DistributionFamily([gs.Distribution(random_distribution(n, rng)) for _ in range(m)])
+    a = np.full(n, 1.0 / n)
+    fused = gs.sinkhorn_barycenter(f, fam, a, gs.SinkhornParams(60, 1e-12))
+    monkeypatch.setenv("GS_BARY_UNFUSED", "1")
+    sep = gs.sinkhorn_barycenter(f, fam, a, gs.SinkhornParams(60, 1e-12))
+    assert fused.iterations == sep.iterations
+    assert np.array_equal(fused.barycenter.weights, sep.barycenter.weights)
+    for k in range(m):
+        assert np.array_equal(fused.scalings[k][0], sep.scalings[k][0])
+        assert np.array_equal(fused.scalings[k][1], sep.scalings[k][1])
