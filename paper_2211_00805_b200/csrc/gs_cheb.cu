@@ -2104,27 +2104,78 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
   cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming);
   cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming);
   int rc = GS_OK;
-  for (int sweep = 1, it = 0; sweep <= max_iter; ++sweep, ++it) {
+  auto issue_sweep = [&](int parity) -> int {
+    int r = run_apply_part<S>(ctx, p, comm, w, h, a0, MODE_SK_PSI, da, N.get(), nullptr, W.get(), true, true, &a0);
+    if (!r) r = run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 0, knp, true);
+    if (!r)
+      r = run_apply_part<S>(ctx, p, comm, w, h, a0, MODE_SK_PHI, da, M.get(), V[parity].get(),
+                            V[parity ^ 1].get(), true, true, &a0);
+    if (!r) r = run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 1, knp, true);
+    if (r) return r;
+    gs_launch_begin(ctx, 1);
+    k_sk_control<<<1, 1, 0, s>>>(C);
+    gs_launch_end(ctx, 1);
+    return GS_OK;
+  };
+  // With stream-ordered collectives (the engine's NCCL comm, or one part) two sweeps -- halo
+  // exchanges on the comm stream and allreduces included -- are captured as one CUDA graph and
+  // replayed, as in the unpartitioned sweep loop. Host-callback hooks run sweep by sweep.
+  cudaGraphExec_t gexec = nullptr;
+  int64_t graph_launches = 0;
+  {
+    const char* genv = getenv("GS_GRAPH");
+    const bool capturable = (!comm || (comm->flags & GS_COMM_GRAPH_SAFE)) && (genv ? genv[0] != '0' : true) &&
+                            max_iter >= 2;
+    if (capturable) {
+      if (!ctx->comm_stream) {
+        GS_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+        GS_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_packed, cudaEventDisableTiming));
+        GS_CUDA(ctx, cudaEventCreateWithFlags(&ctx->ev_received, cudaEventDisableTiming));
+      }
+      cudaGraph_t graph = nullptr;
+      const int64_t l0 = ctx->launches;
+      const int a0_saved = a0;
+      ctx->capturing = true;
+      cudaError_t ce = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+      int crc = GS_OK;
+      if (ce == cudaSuccess) {
+        crc = issue_sweep(1);
+        if (!crc) crc = issue_sweep(0);
+        ce = cudaStreamEndCapture(s, &graph);
+      }
+      ctx->capturing = false;
+      graph_launches = ctx->launches - l0;
+      ctx->launches = l0;
+      if (ce == cudaSuccess && !crc) ce = cudaGraphInstantiate(&gexec, graph, 0);
+      if (graph) cudaGraphDestroy(graph);
+      if (ce != cudaSuccess || crc) {
+        cudaGetLastError();
+        if (gexec) cudaGraphExecDestroy(gexec);
+        gexec = nullptr;
+      }
+      a0 = a0_saved;  // two sweeps = four K-step applies: the buffer parity returns
+    }
+  }
+  const int step_sweeps = gexec ? 2 : 1;
+  for (int sweep = 1, it = 0; sweep <= max_iter; sweep += step_sweeps, ++it) {
     if (it >= 2) {  // every rank sees the same status (same global reductions) -> same exit sweep
       const int slot = (it - 2) & 1;
       cudaEventSynchronize(ev[slot]);
       const gs_status st = hst[slot];
       if (st.error || st.n_active == 0) break;
     }
-    rc = run_apply_part<S>(ctx, p, comm, w, h, a0, MODE_SK_PSI, da, N.get(), nullptr, W.get(), true, true, &a0);
-    if (!rc) rc = run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 0, knp, true);
-    if (!rc)
-      rc = run_apply_part<S>(ctx, p, comm, w, h, a0, MODE_SK_PHI, da, M.get(), V[sweep & 1].get(),
-                             V[(sweep & 1) ^ 1].get(), true, true, &a0);
-    if (!rc) rc = run_finalize_part<S>(ctx, p, comm, w, stat.get(), 1, 1, 1, knp, true);
-    if (rc) break;
-    gs_launch_begin(ctx, 1);
-    k_sk_control<<<1, 1, 0, s>>>(C);
-    gs_launch_end(ctx, 1);
+    if (gexec) {
+      GS_CUDA(ctx, cudaGraphLaunch(gexec, s));
+      ctx->launches += graph_launches;
+    } else {
+      rc = issue_sweep(sweep & 1);
+      if (rc) break;
+    }
     const int slot = it & 1;
     cudaMemcpyAsync(&hst[slot], w.status.get(), sizeof(gs_status), cudaMemcpyDeviceToHost, s);
     cudaEventRecord(ev[slot], s);
   }
+  if (gexec) cudaGraphExecDestroy(gexec);
   cudaStreamSynchronize(s);
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
