@@ -70,6 +70,9 @@ int gs_ctx_set_timing(gs_ctx* ctx, int enable);
 int gs_ctx_timing(gs_ctx* ctx, int kernel_class, int64_t* launches, double* total_ms);
 /* Number of engine kernel launches issued on this context so far. */
 int64_t gs_ctx_launch_count(const gs_ctx* ctx);
+/* Queries of the last kNN in R^d (9 <= d <= 31) whose tensor-core candidate set could not be
+ * proven to contain the k nearest and were re-run by the fp64 brute force (diagnostics). */
+int64_t gs_ctx_knn_fallback(const gs_ctx* ctx);
 
 /* ---- SparseSymMatrix (sparse.hpp:23-61, sparse.cpp:15-116) --------------------------- */
 /* from_triplets (sparse.cpp:15-53): mirror, sort, merge agreeing duplicates, drop zeros. */

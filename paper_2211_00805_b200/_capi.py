@@ -63,6 +63,7 @@ SIGNATURES = {
     "gs_ctx_set_timing": (_i, [_vp, _i]),
     "gs_ctx_timing": (_i, [_vp, _i, _pi64, _pd]),
     "gs_ctx_launch_count": (_i64, [_vp]),
+    "gs_ctx_knn_fallback": (_i64, [_vp]),
     "gs_graph_from_triplets": (_i, [_vp, _i, _i64, _vp, _vp, _vp, _i, _pvp]),
     "gs_graph_from_csr": (_i, [_vp, _i, _i64, _vp, _vp, _vp, _i, _pvp]),
     "gs_graph_destroy": (None, [_vp]),

@@ -453,3 +453,5 @@ extern "C" int gs_graph_gershgorin(gs_ctx* ctx, const gs_graph* g, double* out) 
   *out = v;
   return GS_OK;
 }
+
+extern "C" int64_t gs_ctx_knn_fallback(const gs_ctx* ctx) { return ctx ? ctx->knn_fallback : 0; }

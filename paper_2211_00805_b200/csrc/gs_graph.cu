@@ -54,11 +54,14 @@ template <int KMAX, int DMAX>
 __global__ void __launch_bounds__(kKnnThreads) k_knn(const double* __restrict__ pts,
                                                      const double* __restrict__ sq, int n, int d,
                                                      int k, int* __restrict__ nbrs,
-                                                     double* __restrict__ eps) {
+                                                     double* __restrict__ eps,
+                                                     const int* __restrict__ qlist = nullptr, int nq = 0) {
   extern __shared__ double smem[];
   double* s_x = smem;                    // kKnnTile * d
   double* s_sq = smem + kKnnTile * d;    // kKnnTile
-  const int qi = blockIdx.x * kKnnThreads + threadIdx.x;
+  // queries: all n rows, or the nq rows of qlist (the tensor-core path's fallback, gs_knn_tc.cu)
+  const int qslot = blockIdx.x * kKnnThreads + threadIdx.x;
+  const int qi = qlist ? (qslot < nq ? qlist[qslot] : n) : qslot;
   const bool valid = qi < n;
   double xq[DMAX];
 #pragma unroll
@@ -146,16 +149,18 @@ __global__ void __launch_bounds__(kKnnThreads) k_knn(const double* __restrict__ 
 
 template <int KMAX>
 void launch_knn_k(const double* pts, const double* sq, int n, int d, int k, int* nb, double* eps,
-                  cudaStream_t s) {
+                  cudaStream_t s, const int* qlist = nullptr, int nq = 0) {
   const size_t shm = (size_t)kKnnTile * (d + 1) * sizeof(double);
-  const unsigned grid = (unsigned)((n + kKnnThreads - 1) / kKnnThreads);
+  const int rows = qlist ? nq : n;
+  const unsigned grid = (unsigned)((rows + kKnnThreads - 1) / kKnnThreads);
+  if (rows == 0) return;
   if (d <= 4) {
-    k_knn<KMAX, 4><<<grid, kKnnThreads, shm, s>>>(pts, sq, n, d, k, nb, eps);
+    k_knn<KMAX, 4><<<grid, kKnnThreads, shm, s>>>(pts, sq, n, d, k, nb, eps, qlist, nq);
   } else if (d <= 8) {
-    k_knn<KMAX, 8><<<grid, kKnnThreads, shm, s>>>(pts, sq, n, d, k, nb, eps);
+    k_knn<KMAX, 8><<<grid, kKnnThreads, shm, s>>>(pts, sq, n, d, k, nb, eps, qlist, nq);
   } else {
     cudaFuncSetAttribute(k_knn<KMAX, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
-    k_knn<KMAX, 32><<<grid, kKnnThreads, shm, s>>>(pts, sq, n, d, k, nb, eps);
+    k_knn<KMAX, 32><<<grid, kKnnThreads, shm, s>>>(pts, sq, n, d, k, nb, eps, qlist, nq);
   }
 }
 
@@ -892,6 +897,26 @@ static int knn_grid(gs_ctx* ctx, const double* dpts, const double* sq, int n, in
   return GS_OK;
 }
 
+// brute force over every candidate for the queries of qlist (the tensor-core path's fallback)
+int gs_knn_brute_list(gs_ctx* ctx, const double* dpts, const double* sq, int n, int d, int k,
+                      const int* qlist, int nq, int* dnb, double* deps) {
+  if (nq <= 0) return GS_OK;
+  gs_launch_begin(ctx, 1);
+  if (k <= 16) launch_knn_k<16>(dpts, sq, n, d, k, dnb, deps, ctx->stream, qlist, nq);
+  else launch_knn_k<32>(dpts, sq, n, d, k, dnb, deps, ctx->stream, qlist, nq);
+  gs_launch_end(ctx, 1);
+  GS_CUDA(ctx, cudaGetLastError());
+  return GS_OK;
+}
+
+// tensor-core prefilter for 9 <= d <= 31 (GS_KNN=brute forces the fp64 brute force)
+static bool use_tc_knn(int n, int d, int k) {
+  const char* e = getenv("GS_KNN");
+  if (e && e[0] == 'b') return false;
+  if (e && e[0] == 't') return d <= 31 && k <= 24;
+  return d >= 9 && d <= 31 && k <= 24 && n >= 4096;
+}
+
 static int knn_device(gs_ctx* ctx, const double* dpts, int n, int d, int k, int* dnb, double* deps) {
   cudaStream_t s = ctx->stream;
   DevBuf<double> sq;
@@ -900,6 +925,7 @@ static int knn_device(gs_ctx* ctx, const double* dpts, int n, int d, int k, int*
   k_sqnorms<<<nblk(n), kThreads, 0, s>>>(dpts, n, d, sq.get());
   gs_launch_end(ctx, 1);
   if (use_grid_knn(n, d)) return knn_grid(ctx, dpts, sq.get(), n, d, k, dnb, deps);
+  if (use_tc_knn(n, d, k)) return gs_knn_tc(ctx, dpts, sq.get(), n, d, k, dnb, deps);
   gs_launch_begin(ctx, 1);
   if (k <= 16) launch_knn_k<16>(dpts, sq.get(), n, d, k, dnb, deps, s);
   else launch_knn_k<32>(dpts, sq.get(), n, d, k, dnb, deps, s);

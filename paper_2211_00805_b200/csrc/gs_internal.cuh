@@ -54,6 +54,8 @@ struct gs_ctx {
   // row-partitioned runs: halo exchanges run on a second stream, overlapped with interior rows
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_packed = nullptr, ev_received = nullptr;
+  // queries of the last tensor-core kNN that the brute force re-ran (gs_knn_tc.cu)
+  int64_t knn_fallback = 0;
 };
 
 struct gs_graph {
@@ -214,5 +216,11 @@ void gs_win_destroy(gs_winsched* w);
 int gs_win_tensor_map(gs_ctx* ctx, void* tmap, const void* base, int64_t rows, int row_elems, int elem_bytes);
 // layout l of f from a host order (order[new] = old): newpos, renumbered operator, fp32 copy
 int gs_layout_from_order(gs_ctx* ctx, gs_filter* f, int l, const int* h_order);
+// kNN (gs_graph.cu / gs_knn_tc.cu): brute force over a query list; tensor-core prefilter + exact
+// fp64 re-rank (indices and eps identical to the brute force)
+int gs_knn_brute_list(gs_ctx* ctx, const double* dpts, const double* sq, int n, int d, int k,
+                      const int* qlist, int nq, int* dnb, double* deps);
+int gs_knn_tc(gs_ctx* ctx, const double* dpts, const double* sq, int n, int d, int k, int* dnb,
+              double* deps);
 int gs_csr_from_sorted_entries(gs_ctx* ctx, int n, int64_t m, const unsigned long long* d_keys,
                                const double* d_vals, bool check_dups, gs_graph** out);
