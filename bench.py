@@ -855,7 +855,7 @@ def run_engine_bary(args):
                                    f"over {world} rank(s), {args.sweeps} sweeps",
                        "nnz_L": int(nnz_L), "lambda_max_bound": lap.lambda_max_bound,
                        "lambda_rounds": lap.power_rounds, "graph_build_s": t_graph,
-                       "members_per_rank": B, "allreduce_calls": hook.calls,
+                       "members_per_rank": B, "allreduce_calls": hook.calls() if hook is not None else 0,
                        "parallelism": f"member sharding x{world}, NCCL allreduce per sweep" if world > 1
                        else "one rank: no collective, sweeps replayed as a CUDA graph"},
             "roofline": {"bound": "hbm", "achieved": bytes_step / (avg / 1000.0) / 1e9, "peak": peak,
@@ -974,6 +974,26 @@ def run_engine_bary_dist(args):
     elapsed = max_over_ranks(e0.elapsed_time(e1))
     value = args.steps / (elapsed / 1000.0)
     distance = float(dsc[0].item())
+    # ---- per-launch step time of the barycenter alone (B = members per rank), one extra run with
+    # per-kernel launches and an event pair around every step launch
+    os.environ["GS_GRAPH"] = "0"
+    ctx.set_timing(True)
+    bary(Ga, ba)
+    torch.cuda.synchronize()
+    step_n, step_ms = ctx.timing(0)
+    ctx.set_timing(False)
+    del os.environ["GS_GRAPH"]
+    # ---- reference semantics for the distance (abort on): barycentric_distance raises
+    # Disconnected when the two barycenters' mass sits in different graph components
+    # (barycenter.cpp:101-107 -> transport.cpp:132-134)
+    rc_ab = lib.gs_sinkhorn(ctx.handle, filt._h, a.data_ptr(), ba.data_ptr(), bb.data_ptr(), 1,
+                            args.sweeps, 1e-9, _capi.GS_FLAG_SINGLE, _capi.GS_MEM_DEVICE,
+                            vd.data_ptr(), wd.data_ptr(), dsc.data_ptr(), dsc.data_ptr() + 8,
+                            dsi.data_ptr(), dsi.data_ptr() + 4, dsc.data_ptr() + 16, C.byref(fp),
+                            C.byref(fs))
+    torch.cuda.synchronize()
+    distance_ref = ({"rc": int(rc_ab), "errc": lib.gs_last_error(ctx.handle).decode(),
+                     "fail_sweep": fs.value} if rc_ab else {"rc": 0, "cost": float(dsc[0].item())})
     # ---- e2e: the same evaluation through gs.barycentric_distance-equivalent host-buffer calls ----
     Gah = torch.from_numpy(np.ascontiguousarray(cfg.group_a[lo:hi])).pin_memory()
     Gbh = torch.from_numpy(np.ascontiguousarray(cfg.group_b[lo:hi])).pin_memory()
@@ -1025,7 +1045,9 @@ def run_engine_bary_dist(args):
                                    f"x {args.sweeps} sweeps (members sharded over {world} rank(s)) + "
                                    f"their geodesic Sinkhorn distance ({args.sweeps} sweeps)",
                        "nnz_L": int(nnz_L), "graph_build_s": t_graph, "data_s": t_data,
-                       "members_per_rank": B, "distance": distance,
+                       "members_per_rank": B,
+                       "distance_abort_off": distance,
+                       "distance_reference_semantics": distance_ref,
                        "sweeps_per_step": {"barycenter": 2 * args.sweeps, "distance": args.sweeps},
                        "parallelism": (f"member sharding x{world}, NCCL allreduce per sweep"
                                        if world > 1 else "one rank: no collective, CUDA-graph sweeps")},
@@ -1033,8 +1055,8 @@ def run_engine_bary_dist(args):
                          "unit": "GB/s", "frac": bytes_step / (avg / 1000.0) / 1e9 / peak,
                          "traffic": None, "peak_kind": peak_kind, "bytes_per_launch": bytes_step,
                          "avg_launch_ms": avg, "launches_timed": step_n,
-                         "note": "average over the barycenter (B = members/rank) and distance (B = 1) "
-                                 "step launches; bytes_per_launch is the barycenter step's"},
+                         "kernel": f"barycenter step (B = {B}), event pair around every launch of one "
+                                   "barycenter run with per-kernel launches"},
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": None,
         }), flush=True)
     dist.destroy_process_group()
