@@ -511,3 +511,24 @@ def test_barycenter_fused_log_mean_bit_identical(m, monkeypatch):
     for k in range(m):
         assert np.array_equal(fused.scalings[k][0], sep.scalings[k][0])
         assert np.array_equal(fused.scalings[k][1], sep.scalings[k][1])
+
+
+@pytest.mark.parametrize("width,hub", [(64, 1500), (64, 300), (40, 1500)])
+def test_windowed_kernel_hub_rows_and_fallback(width, hub):
+    """Wide batches (>= 256-byte rows) run the windowed kernel unless a row alone needs more ring
+    loads than a block may take (gs_win.cu build_schedule: W / 2 = 188 for 512-byte rows; hub
+    degrees 300 and 1500 -> the register kernel). Either way the filter apply is bit-identical to
+    the oracle."""
+    from paper_2211_00805_b200.rng import Rng
+    n = 2000
+    r, c, v = random_connected_graph(n, 97, 0.5)
+    rng = Rng(98)
+    have = {(min(a, b), max(a, b)) for a, b in zip(r.tolist(), c.tolist())}
+    extra = [(0, j) for j in range(1, hub) if (0, j) not in have]
+    r = np.concatenate([r, np.array([e[0] for e in extra], np.int32)])
+    c = np.concatenate([c, np.array([e[1] for e in extra], np.int32)])
+    v = np.concatenate([v, np.array([rng.uniform(0.1, 0.5) for _ in extra])])
+    f, _ = engine_filter(r, c, v, n, 1, 0.8, 30)
+    fo = oracle_filter(r, c, v, n, 1, 0.8, 30)
+    X = np.abs(np.sin(np.arange(n)[:, None] * (np.arange(width)[None, :] + 1.0))) + 0.05
+    assert np.array_equal(f.apply(X), fo.apply(X))
