@@ -145,3 +145,27 @@ def test_config3_shape_fp32_row_partitioned(gs, nparts):
         w[p.vertices] = q.w
     assert np.array_equal(v, full.v) and np.array_equal(w, full.w)
     assert abs(res[0].cost - full.cost) <= 1e-12 * abs(full.cost)
+
+
+def test_config1_companions_fp32_windowed_64_columns(gs, monkeypatch):
+    """64 companion pairs in the 32-bit mode: 256-byte rows run the windowed kernel
+    (k_cheb_win<float, 64>); every cost within 1e-4 of the fp64 oracle, and v / w bit-identical
+    to the register-gather kernel (GS_WIN=0: same storage words, same fp64 chains; the cost sums
+    run over the two layouts' vertex orders, so they agree to rounding)."""
+    from paper_2211_00805_b200 import workloads
+    n, pairs = 6000, 64
+    roll = workloads.swiss_roll(n, 1)
+    mus, nus = workloads.bump_mixture_companions(roll, pairs, 3)
+    f, fo = _filters(gs, roll.points)
+    a = np.full(n, 1.0 / n)
+    params = gs.SinkhornParams(100, 5e-324)
+    res = gs.geodesic_sinkhorn_batch(f, _dists(gs, mus), _dists(gs, nus), a, params, fp32=True)
+    ref = po.sinkhorn_batch(fo, a, mus, nus, 100, 5e-324)
+    cost = np.array([r.cost for r in res])
+    assert np.all(np.isfinite(cost))
+    assert np.max(np.abs(cost - ref["cost"]) / np.abs(ref["cost"])) <= TOL32
+    monkeypatch.setenv("GS_WIN", "0")
+    reg = gs.geodesic_sinkhorn_batch(f, _dists(gs, mus), _dists(gs, nus), a, params, fp32=True)
+    for p in range(pairs):
+        assert np.array_equal(res[p].v, reg[p].v) and np.array_equal(res[p].w, reg[p].w)
+        assert abs(res[p].cost - reg[p].cost) <= 1e-14 * abs(reg[p].cost)
