@@ -1,11 +1,11 @@
-"""GPU: the optional fp32 mode on the BASELINE swiss-roll constructions (configs 0, 1, 3) against
+"""GPU: the optional 32-bit mode on the BASELINE swiss-roll constructions (configs 0, 1, 3) against
 the fp64 oracle. north_star: distances within 1e-4 relative in fp32.
 
-The fp32 mode runs the Chebyshev recurrence in fp32 on per-column power-of-two scaled inputs and
-keeps the scaling vectors, the epilogue and every reduction in fp64 (DESIGN.md §4 "Precision").
-Its division floor is max(1e-300, 2^(e_c - 100)) for a column scaled by 2^e_c: values below that
-are outside the scaled recurrence's range. Where the reference's result is not finite (or the
-stagnation rule fires) the fp32 mode must report the same errc, never a non-finite value."""
+The 32-bit mode stores every Chebyshev-vector word as the upper half of the fp64 word (sign, the
+11-bit fp64 exponent, 20 fraction bits) and computes in fp64 (DESIGN.md §4 "Precision"): binary32's
+exponent cannot hold the scaling vectors of long-range transport (profiles/r02_fp32_range.md).
+Where the reference's result is not finite (or the stagnation rule fires) the 32-bit mode must
+report the same errc, never a non-finite value."""
 import math
 
 import numpy as np
