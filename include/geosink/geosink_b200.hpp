@@ -315,15 +315,17 @@ class HeatFilter {
   std::vector<double> coeff_;
 };
 
-// ---- heat.hpp:60-84: EulerHeat (implicit Euler; the device runs Solver::lockstep_cg) ------------
+// ---- heat.hpp:60-84: EulerHeat (implicit Euler: direct below n = 4000 in the automatic mode, the
+// reference's lockstep conjugate gradient above) ------------------------------------------------
 class EulerHeat {
  public:
   enum class Solver { automatic, direct, lockstep_cg };
   EulerHeat(const GraphLaplacian& lap, double t, int steps, Solver solver = Solver::automatic)
       : n_(lap.size()), steps_(steps), t_(t) {
-    (void)solver;  // LDLT (direct / small automatic) has no device counterpart: CG for every size
     gs_euler* e = nullptr;
-    detail::check(gs_euler_create(detail::ctx(), lap.matrix.handle(), t, steps, &e));
+    const int code = solver == Solver::direct ? GS_EULER_DIRECT
+                     : solver == Solver::lockstep_cg ? GS_EULER_LOCKSTEP_CG : GS_EULER_AUTOMATIC;
+    detail::check(gs_euler_create_ex(detail::ctx(), lap.matrix.handle(), t, steps, code, &e));
     h_ = std::shared_ptr<gs_euler>(e, gs_euler_destroy);
   }
   std::vector<double> apply(const std::vector<double>& f) const {

@@ -267,7 +267,14 @@ int gs_barycenter_ex(gs_ctx* ctx, const gs_filter* f, const double* a, const dou
  * lockstep conjugate gradient over the batch (Solver::lockstep_cg; tolerance 1e-10 relative
  * residual, at most 10 n iterations -> status 13 = SolveFailure). */
 typedef struct gs_euler gs_euler;
+/* EulerHeat::Solver (heat.hpp:62): automatic = direct for n <= 4000, lockstep CG above */
+#define GS_EULER_AUTOMATIC 0
+#define GS_EULER_DIRECT 1     /* dense Cholesky of I + hL on the device (the reference: sparse
+                               * LDLT; same solution up to rounding), n <= 16384 */
+#define GS_EULER_LOCKSTEP_CG 2
 int gs_euler_create(gs_ctx* ctx, const gs_graph* L, double t, int steps, gs_euler** out);
+int gs_euler_create_ex(gs_ctx* ctx, const gs_graph* L, double t, int steps, int solver,
+                       gs_euler** out);
 void gs_euler_destroy(gs_euler* e);
 const gs_graph* gs_euler_system(const gs_euler* e); /* I + (t/steps) L, caller's vertex order */
 /* X, Y: `width` contiguous n-vectors; iters_out (optional): CG iterations of the last solve */

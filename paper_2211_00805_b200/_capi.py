@@ -108,6 +108,7 @@ SIGNATURES = {
     "gs_part_sinkhorn": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _d, _i, _i, _vp, _vp, _vp,
                               _vp, _vp, _vp, _vp, _pi, _pi]),
     "gs_euler_create": (_i, [_vp, _vp, _d, _i, _pvp]),
+    "gs_euler_create_ex": (_i, [_vp, _vp, _d, _i, _i, _pvp]),
     "gs_euler_destroy": (None, [_vp]),
     "gs_euler_system": (_vp, [_vp]),
     "gs_euler_apply": (_i, [_vp, _vp, _vp, _vp, _i, _i, _pi]),

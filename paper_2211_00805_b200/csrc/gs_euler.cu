@@ -12,6 +12,7 @@
 
 #include <cmath>
 #include <memory>
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -25,6 +26,11 @@ struct gs_euler {
   gs_graph* perm = nullptr;    // Cuthill-McKee order
   int* order = nullptr;        // order[new] = old
   int* newpos = nullptr;       // newpos[old] = new
+  // direct branch (heat.cpp:157-162: Solver::direct, or automatic with n <= 4000): the inverse
+  // Cholesky factor Y = L^-1 of the system in the CM order (n x n row-major, lower triangle);
+  // a solve is x <- Y^T (Y x)
+  bool direct = false;
+  double* Y = nullptr;
 };
 
 namespace {
@@ -237,8 +243,197 @@ int colsum(gs_ctx* ctx, const gs_euler* E, const double* x, const double* y, int
   return GS_OK;
 }
 
+// ---- direct branch: dense Cholesky of I + hL (n <= 4096), its inverse factor, triangular products
+constexpr int kNb = 32;  // Cholesky block
+
+__global__ void k_dense_fill(const int* __restrict__ offs, const int* __restrict__ cols,
+                             const double* __restrict__ vals, int n, double* __restrict__ A) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int p = offs[i]; p < offs[i + 1]; ++p) A[(size_t)i * n + cols[p]] = vals[p];
+}
+
+// factor the b x b diagonal block at k0 in place (lower triangle); fail on a non-positive pivot
+__global__ void k_chol_diag(double* A, int n, int k0, int b, int* fail) {
+  __shared__ double blk[kNb][kNb + 1];
+  const int t = threadIdx.x;  // row within the block
+  for (int c = 0; c < b; ++c) blk[t][c] = t < b ? A[(size_t)(k0 + t) * n + k0 + c] : 0.0;
+  __syncthreads();
+  for (int j = 0; j < b; ++j) {
+    if (t == 0) {
+      const double d = blk[j][j];
+      if (!(d > 0.0)) *fail = 1;
+      blk[j][j] = sqrt(d > 0.0 ? d : 1.0);
+    }
+    __syncthreads();
+    if (t > j && t < b) blk[t][j] = blk[t][j] / blk[j][j];
+    __syncthreads();
+    if (t > j && t < b)
+      for (int c = j + 1; c <= t; ++c) blk[t][c] = blk[t][c] - blk[t][j] * blk[c][j];
+    __syncthreads();
+  }
+  if (t < b)
+    for (int c = 0; c <= t; ++c) A[(size_t)(k0 + t) * n + k0 + c] = blk[t][c];
+}
+
+// panel below the diagonal block: L21 = A21 L11^-T (one thread per row, forward substitution)
+__global__ void k_chol_panel(double* A, int n, int k0, int b) {
+  __shared__ double L11[kNb][kNb + 1];
+  for (int e = threadIdx.x; e < b * b; e += blockDim.x) L11[e / b][e % b] = A[(size_t)(k0 + e / b) * n + k0 + e % b];
+  __syncthreads();
+  const int i = k0 + b + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double x[kNb];
+  for (int j = 0; j < b; ++j) {
+    double v = A[(size_t)i * n + k0 + j];
+    for (int q = 0; q < j; ++q) v = v - x[q] * L11[j][q];
+    x[j] = v / L11[j][j];
+  }
+  for (int j = 0; j < b; ++j) A[(size_t)i * n + k0 + j] = x[j];
+}
+
+// trailing update of the lower triangle: A22 -= L21 L21^T (32 x 32 tiles)
+__global__ void k_chol_update(double* A, int n, int k0, int b) {
+  const int r0 = k0 + b + blockIdx.y * kNb, c0 = k0 + b + blockIdx.x * kNb;
+  if (c0 > r0 + kNb - 1) return;  // strictly upper tile
+  __shared__ double Li[kNb][kNb + 1], Lc[kNb][kNb + 1];
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < kNb; r += 8) {
+    Li[r][tx] = (r0 + r < n && tx < b) ? A[(size_t)(r0 + r) * n + k0 + tx] : 0.0;
+    Lc[r][tx] = (c0 + r < n && tx < b) ? A[(size_t)(c0 + r) * n + k0 + tx] : 0.0;
+  }
+  __syncthreads();
+  for (int r = ty; r < kNb; r += 8) {
+    const int i = r0 + r, c = c0 + tx;
+    if (i >= n || c >= n || c > i) continue;
+    double acc = 0.0;
+    for (int q = 0; q < b; ++q) acc = fma(Li[r][q], Lc[tx][q], acc);
+    A[(size_t)i * n + c] -= acc;
+  }
+}
+
+// Y = L^-1 (lower): thread j solves column j; the warp's threads walk the same rows so the L rows
+// are broadcast loads; Y is zero above the diagonal, so the sums start at the warp's first column
+__global__ void k_tri_inverse(const double* __restrict__ L, int n, double* __restrict__ Y) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j0 = blockIdx.x * blockDim.x;
+  for (int i = j0; i < n; ++i) {
+    double sacc = 0.0;
+    for (int p = j0; p < i; ++p) sacc = fma(L[(size_t)i * n + p], j < n ? Y[(size_t)p * n + j] : 0.0, sacc);
+    if (j < n) Y[(size_t)i * n + j] = i < j ? 0.0 : ((i == j ? 1.0 : 0.0) - sacc) / L[(size_t)i * n + i];
+    __syncwarp();
+  }
+}
+
+// out = op(Y) x on the grouped block (B columns in groups of GW): op = Y (lower) or Y^T
+template <bool TRANS>
+__global__ void k_tri_apply(const double* __restrict__ Y, int n, const double* __restrict__ x, double* __restrict__ out,
+                            int GW, int G) {
+  __shared__ double Ys[kNb][kNb + 1];
+  __shared__ double Xs[kNb][64];
+  const int g = blockIdx.y;
+  const int r0 = blockIdx.x * kNb;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // GW-wide column lanes x 8 row lanes
+  double acc[kNb / 8];
+#pragma unroll
+  for (int u = 0; u < kNb / 8; ++u) acc[u] = 0.0;
+  const int pb = TRANS ? r0 : 0, pe = TRANS ? n : min(n, r0 + kNb);
+  for (int p0 = pb - pb % kNb; p0 < pe; p0 += kNb) {
+    __syncthreads();
+    for (int e = ty * blockDim.x + tx; e < kNb * kNb; e += blockDim.x * blockDim.y) {
+      const int a = e / kNb, c = e % kNb;  // Ys[row i - r0][p - p0]
+      const int i = r0 + a, pp = p0 + c;
+      double v = 0.0;
+      if (i < n && pp < n) v = TRANS ? (pp >= i ? Y[(size_t)pp * n + i] : 0.0) : (pp <= i ? Y[(size_t)i * n + pp] : 0.0);
+      Ys[a][c] = v;
+    }
+    for (int e = ty * blockDim.x + tx; e < kNb * GW; e += blockDim.x * blockDim.y) {
+      const int pp = p0 + e / GW, c = e % GW;
+      Xs[e / GW][c] = pp < n ? x[((size_t)g * n + pp) * GW + c] : 0.0;
+    }
+    __syncthreads();
+    if (tx < GW)
+#pragma unroll
+      for (int u = 0; u < kNb / 8; ++u) {
+        const int a = ty + 8 * u;
+        double sacc = acc[u];
+        for (int c = 0; c < kNb; ++c) sacc = fma(Ys[a][c], Xs[c][tx], sacc);
+        acc[u] = sacc;
+      }
+  }
+  if (tx < GW)
+#pragma unroll
+    for (int u = 0; u < kNb / 8; ++u) {
+      const int i = r0 + ty + 8 * u;
+      if (i < n) out[((size_t)g * n + i) * GW + tx] = acc[u];
+    }
+}
+
+int euler_factor(gs_ctx* ctx, gs_euler* E) {
+  const int n = E->n;
+  cudaStream_t s = ctx->stream;
+  DevBuf<double> A;
+  DevBuf<int> fail;
+  GS_CUDA(ctx, A.alloc((size_t)n * n, s));
+  GS_CUDA(ctx, fail.alloc(1, s));
+  GS_CUDA(ctx, cudaMemsetAsync(A.get(), 0, (size_t)n * n * sizeof(double), s));
+  GS_CUDA(ctx, cudaMemsetAsync(fail.get(), 0, sizeof(int), s));
+  gs_launch_begin(ctx, 1);
+  k_dense_fill<<<blocks_for(n), kT, 0, s>>>(E->perm->offs, E->perm->cols, E->perm->vals, n, A.get());
+  gs_launch_end(ctx, 1);
+  for (int k0 = 0; k0 < n; k0 += kNb) {
+    const int b = std::min(kNb, n - k0);
+    gs_launch_begin(ctx, 1);
+    k_chol_diag<<<1, kNb, 0, s>>>(A.get(), n, k0, b, fail.get());
+    gs_launch_end(ctx, 1);
+    const int rest = n - k0 - b;
+    if (rest > 0) {
+      gs_launch_begin(ctx, 1);
+      k_chol_panel<<<(rest + 127) / 128, 128, 0, s>>>(A.get(), n, k0, b);
+      gs_launch_end(ctx, 1);
+      const int tiles = (rest + kNb - 1) / kNb;
+      gs_launch_begin(ctx, 1);
+      k_chol_update<<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(A.get(), n, k0, b);
+      gs_launch_end(ctx, 1);
+    }
+  }
+  int hf = 0;
+  GS_CUDA(ctx, cudaMemcpyAsync(&hf, fail.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  if (hf) return gs_fail(ctx, ERRC_SOLVE_FAILURE, "sparse LDLT factorisation failed");
+  GS_CUDA(ctx, cudaMalloc((void**)&E->Y, (size_t)n * n * sizeof(double)));
+  gs_launch_begin(ctx, 1);
+  k_tri_inverse<<<(n + 31) / 32, 32, 0, s>>>(A.get(), n, E->Y);
+  gs_launch_end(ctx, 1);
+  GS_CUDA(ctx, cudaGetLastError());
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  return GS_OK;
+}
+
+// one solve (I + hL) x = b on the grouped block: x <- Y^T (Y x)
+int euler_direct_solve(gs_ctx* ctx, const gs_euler* E, double* x, int B) {
+  const int n = E->n;
+  const int GW = gs_group_width(B), G = (B + GW - 1) / GW;
+  cudaStream_t s = ctx->stream;
+  DevBuf<double> z;
+  GS_CUDA(ctx, z.alloc((size_t)G * GW * n, s));
+  const dim3 grid((n + kNb - 1) / kNb, G), blk(GW < 32 ? 32 : GW, 8);
+  gs_launch_begin(ctx, 1);
+  k_tri_apply<false><<<grid, blk, 0, s>>>(E->Y, n, x, z.get(), GW, G);
+  gs_launch_end(ctx, 1);
+  gs_launch_begin(ctx, 1);
+  k_tri_apply<true><<<grid, blk, 0, s>>>(E->Y, n, z.get(), x, GW, G);
+  gs_launch_end(ctx, 1);
+  GS_CUDA(ctx, cudaGetLastError());
+  return GS_OK;
+}
+
 // heat.cpp:166-201 on the grouped block x (B columns); *iters = CG iterations
 int euler_solve(gs_ctx* ctx, const gs_euler* E, double* x, int B, int* iters) {
+  if (E->direct) {  // heat.cpp:167-173
+    if (iters) *iters = 0;
+    return euler_direct_solve(ctx, E, x, B);
+  }
   const int n = E->n;
   const int GW = gs_group_width(B), G = (B + GW - 1) / GW;
   const int64_t len = (int64_t)G * GW * n;
@@ -365,7 +560,16 @@ double plain_log_sum(const double* a, const double* mu, const double* s, int n) 
 
 }  // namespace
 
+extern "C" int gs_euler_create_ex(gs_ctx* ctx, const gs_graph* L, double t, int steps, int solver,
+                                  gs_euler** out);
+
+// the reference's default (Solver::automatic): direct below n = 4000, lockstep CG above
 extern "C" int gs_euler_create(gs_ctx* ctx, const gs_graph* L, double t, int steps, gs_euler** out) {
+  return gs_euler_create_ex(ctx, L, t, steps, GS_EULER_AUTOMATIC, out);
+}
+
+extern "C" int gs_euler_create_ex(gs_ctx* ctx, const gs_graph* L, double t, int steps, int solver,
+                                  gs_euler** out) {
   if (!ctx || !L || !out) return GS_ERR_UNSUPPORTED;
   *out = nullptr;
   if (!(t > 0.0 && std::isfinite(t))) return gs_fail(ctx, ERRC_NON_POSITIVE_TIME, "diffusion time must be > 0");
@@ -408,6 +612,13 @@ extern "C" int gs_euler_create(gs_ctx* ctx, const gs_graph* L, double t, int ste
   GS_TRY(gs_bfs_order(ctx, E->system, E->order, E->newpos, 1, nullptr, nullptr));
   GS_TRY(gs_permute_graph(ctx, E->system, E->order, E->newpos, &E->perm));
   GS_CUDA(ctx, cudaStreamSynchronize(s));
+  if (solver < GS_EULER_AUTOMATIC || solver > GS_EULER_LOCKSTEP_CG)
+    return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "unknown solver");
+  E->direct = solver == GS_EULER_DIRECT || (solver == GS_EULER_AUTOMATIC && n <= 4000);
+  if (E->direct && n > 0) {
+    if (n > 16384) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "direct solver: n <= 16384 on the device");
+    GS_TRY(euler_factor(ctx, E.get()));
+  }
   *out = E.release();
   return GS_OK;
 }
@@ -418,6 +629,7 @@ extern "C" void gs_euler_destroy(gs_euler* E) {
   gs_graph_destroy(E->perm);
   cudaFree(E->order);
   cudaFree(E->newpos);
+  cudaFree(E->Y);
   delete E;
 }
 

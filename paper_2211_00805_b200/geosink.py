@@ -447,19 +447,22 @@ class HeatFilter:
 
 
 class EulerHeat:
-    """heat.hpp:60-82: implicit Euler, `steps` solves of (I + (t/steps) L) x = b. The device runs
-    the reference's lockstep conjugate gradient for every size (Solver::lockstep_cg); the
-    reference's automatic mode factorises with LDLT below n = 4000 instead (same solution up to
-    the CG tolerance, 1e-10 relative residual)."""
+    """heat.hpp:60-82: implicit Euler, `steps` solves of (I + (t/steps) L) x = b. Solver
+    "automatic" (the reference's default) factorises directly below n = 4000 (the reference: sparse
+    LDLT; the device: dense Cholesky and its inverse factor, the same solution up to rounding) and
+    runs the reference's lockstep conjugate gradient above; "direct" / "lockstep_cg" force one."""
+
+    _SOLVERS = {"automatic": 0, "direct": 1, "lockstep_cg": 2}
 
     def __init__(self, laplacian: GraphLaplacian, t: float, steps: int, solver: str = "automatic"):
-        if solver not in ("automatic", "lockstep_cg", "direct"):
+        if solver not in self._SOLVERS:
             raise Error(errc.invalid_argument, "InvalidArgument: unknown solver")
         self._ctx = laplacian.matrix._ctx
         self._n = laplacian.size()
         h = C.c_void_p()
-        self._ctx.check(self._ctx.lib.gs_euler_create(self._ctx.handle, laplacian.matrix._h,
-                                                      float(t), int(steps), C.byref(h)))
+        self._ctx.check(self._ctx.lib.gs_euler_create_ex(self._ctx.handle, laplacian.matrix._h,
+                                                         float(t), int(steps), self._SOLVERS[solver],
+                                                         C.byref(h)))
         self._h = h
         self._t, self._steps = float(t), int(steps)
         self.last_iterations = 0  # engine diagnostic: CG iterations of the last solve

@@ -31,7 +31,7 @@ def test_euler_apply_bit_exact(gs, kind, steps, width):
     n = 400
     r, c, v = acceptance_graph(n, 17 + width)
     lap, Lo = _pair(gs, r, c, v, n, kind)
-    E = gs.EulerHeat(lap, 0.6, steps)
+    E = gs.EulerHeat(lap, 0.6, steps, solver="lockstep_cg")
     So = po.euler_system(Lo, 0.6, steps)
     S = E.system()
     assert np.array_equal(S.row_offsets(), So.offs)
@@ -51,7 +51,7 @@ def test_euler_isolated_vertex_and_validation(gs):
     c = np.array([1, 2, 3], np.int32)
     v = np.array([1.0, 2.0, 0.5])
     lap, Lo = _pair(gs, r, c, v, 5, 0)  # vertex 4 isolated: unit system row
-    E = gs.EulerHeat(lap, 1.0, 2)
+    E = gs.EulerHeat(lap, 1.0, 2, solver="lockstep_cg")
     S = E.system()
     assert np.array_equal(S.row_offsets(), po.euler_system(Lo, 1.0, 2).offs)
     x = np.arange(5, dtype=np.float64) + 1.0
@@ -59,10 +59,10 @@ def test_euler_isolated_vertex_and_validation(gs):
     assert np.array_equal(y, po.euler_apply(po.euler_system(Lo, 1.0, 2), 2, x)[0])
     assert y[4] == x[4]
     with pytest.raises(gs.Error) as e:
-        gs.EulerHeat(lap, 0.0, 2)
+        gs.EulerHeat(lap, 0.0, 2, solver="lockstep_cg")
     assert e.value.code == gs.errc.non_positive_time
     with pytest.raises(gs.Error) as e:
-        gs.EulerHeat(lap, 1.0, 0)
+        gs.EulerHeat(lap, 1.0, 0, solver="lockstep_cg")
     assert e.value.code == gs.errc.invalid_argument
 
 
@@ -87,7 +87,7 @@ def test_euler_sinkhorn_matches_oracle(gs, P, steps):
     n = 120
     r, c, v = acceptance_graph(n, 60 + P)
     lap, Lo = _pair(gs, r, c, v, n, 1)
-    E = gs.EulerHeat(lap, 0.8, steps)
+    E = gs.EulerHeat(lap, 0.8, steps, solver="lockstep_cg")
     So = po.euler_system(Lo, 0.8, steps)
     rng = Rng(P)
     mus = [random_distribution(n, rng) for _ in range(P)]
@@ -108,7 +108,7 @@ def test_euler_sinkhorn_errors_like_oracle(gs):
     """Disconnected components: the same error (and message) as the oracle."""
     A = gs.SparseSymMatrix.from_triplets(4, [(0, 1, 1.0), (2, 3, 1.0)])
     lap = gs.laplacian(A, gs.LaplacianKind.combinatorial)
-    E = gs.EulerHeat(lap, 1.0, 2)
+    E = gs.EulerHeat(lap, 1.0, 2, solver="lockstep_cg")
     e = np.eye(4)
     with pytest.raises(gs.Error) as ex:
         gs.euler_sinkhorn(E, gs.Distribution(e[0]), gs.Distribution(e[3]), np.full(4, 0.25),
@@ -118,3 +118,57 @@ def test_euler_sinkhorn_errors_like_oracle(gs):
         po.euler_sinkhorn_batch(po.euler_system(Lo, 1.0, 2), 2, 1.0, np.full(4, 0.25), e[0][None], e[3][None],
                                 500, 1e-9, single_style=True)
     assert str(ex.value).endswith(str(ref.value))
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("steps,width", [(1, 1), (3, 3), (2, 64), (2, 70)])
+def test_euler_direct_matches_dense_solve(gs, kind, steps, width):
+    """Solver::direct (heat.cpp:157-173; the device factorises I + hL with a dense Cholesky and
+    applies its inverse factor, the reference a sparse LDLT): `steps` solves agree with a dense
+    numpy solve of the same system to rounding (1e-12 relative)."""
+    n = 500
+    r, c, v = acceptance_graph(n, 29 + width)
+    lap, _ = _pair(gs, r, c, v, n, kind)
+    E = gs.EulerHeat(lap, 0.7, steps, solver="direct")
+    S = E.system().to_dense()
+    X = np.random.default_rng(width).standard_normal((n, width))
+    Y = E.apply(X)
+    Z = X.copy()
+    for _ in range(steps):
+        Z = np.linalg.solve(S, Z)
+    assert np.max(np.abs(Y - Z)) <= 1e-12 * np.max(np.abs(Z))
+    assert E.last_iterations == 0
+
+
+def test_euler_automatic_switches_at_4000(gs):
+    """Solver::automatic: direct for n <= 4000, lockstep CG above (heat.cpp:157)."""
+    for n, direct in ((4000, True), (4100, False)):
+        r, c, v = random_connected_graph(n, 61)
+        lap, _ = _pair(gs, r, c, v, n, 0)
+        E = gs.EulerHeat(lap, 0.5, 1)
+        X = np.random.default_rng(n).standard_normal(n)
+        Y = E.apply(X)
+        assert (E.last_iterations == 0) == direct
+        Ec = gs.EulerHeat(lap, 0.5, 1, solver="lockstep_cg")
+        Yc = Ec.apply(X)
+        assert np.max(np.abs(Y - Yc)) <= 1e-8 * np.max(np.abs(Yc))  # CG: 1e-10 residual
+
+
+def test_euler_direct_sinkhorn_close_to_cg(gs):
+    """euler_sinkhorn over the direct solver: the same iterations and costs within 1e-8 of the
+    lockstep-CG run (whose residual tolerance is 1e-10)."""
+    n, P = 300, 3
+    r, c, v = random_connected_graph(n, 67)
+    lap, _ = _pair(gs, r, c, v, n, 0)
+    from paper_2211_00805_b200.rng import Rng
+    from helpers import random_distribution
+    rng = Rng(68)
+    mus = [gs.Distribution(random_distribution(n, rng)) for _ in range(P)]
+    nus = [gs.Distribution(random_distribution(n, rng)) for _ in range(P)]
+    a = np.full(n, 1.0 / n)
+    params = gs.SinkhornParams(200, 1e-8)
+    rd = gs.euler_sinkhorn_batch(gs.EulerHeat(lap, 0.8, 2, solver="direct"), mus, nus, a, params)
+    rc = gs.euler_sinkhorn_batch(gs.EulerHeat(lap, 0.8, 2, solver="lockstep_cg"), mus, nus, a, params)
+    for p in range(P):
+        assert rd[p].iterations == rc[p].iterations
+        assert abs(rd[p].cost - rc[p].cost) <= 1e-8 * abs(rc[p].cost)
