@@ -53,6 +53,10 @@ struct WinBlk {  // one row block of the schedule (32 bytes)
 #ifndef GS_WIN_LMAX_CAP
 #define GS_WIN_LMAX_CAP 1024
 #endif
+// producer: one bulk copy per row (1) instead of one tile::gather4 per four rows (0; measured)
+#ifndef GS_WIN_BULK_ROWS
+#define GS_WIN_BULK_ROWS 0
+#endif
 // consumers fold two quads (eight entries) per iteration (1) or one quad and the row's tail (0)
 #ifndef GS_WIN_PAIR_QUADS
 #define GS_WIN_PAIR_QUADS 0
@@ -286,7 +290,16 @@ __global__ void __launch_bounds__(kWinThreads, 1)
           r.w += (int)grow;
           int slot = bk.slot0 + 4 * i;
           if (slot >= W) slot -= W;
+#if GS_WIN_BULK_ROWS
+          // experiment: one non-tensor bulk copy per row instead of one gather4 per four rows
+          const S* Tsrc = static_cast<const S*>(A.Tprev);
+          bulk_g2s(ring + (size_t)slot * GW, Tsrc + (size_t)r.x * GW, ROWB, &full[s]);
+          bulk_g2s(ring + (size_t)(slot + 1) * GW, Tsrc + (size_t)r.y * GW, ROWB, &full[s]);
+          bulk_g2s(ring + (size_t)(slot + 2) * GW, Tsrc + (size_t)r.z * GW, ROWB, &full[s]);
+          bulk_g2s(ring + (size_t)(slot + 3) * GW, Tsrc + (size_t)r.w * GW, ROWB, &full[s]);
+#else
           tma_gather4(ring + (size_t)slot * GW, &tmap, 0, r, &full[s]);
+#endif
         }
       }
 #pragma unroll
