@@ -649,11 +649,9 @@ inline bool win_enabled() {
 template <typename S, int GW, int MODE>
 void launch_win_mode(const CUtensorMap& tm, const StepArgs& A, const WinArgs& WA, int G, cudaStream_t s) {
   constexpr int smem = win_smem_bytes<S, GW>();
-  static bool attr = [] {
+  static std::vector<char> seen;  // the attribute is per device
+  if (gs_first_on_device(seen))
     cudaFuncSetAttribute(k_cheb_win<S, GW, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    return true;
-  }();
-  (void)attr;
   k_cheb_win<S, GW, MODE><<<dim3((unsigned)(WA.nctas * G)), kWinThreads, smem, s>>>(tm, A, WA);
 }
 
@@ -1262,12 +1260,11 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
       }
       const size_t smem = (size_t)persist_rep_offset(n) + (size_t)2 * n * 8 + (size_t)maxne * 12;
       if (smem <= 220 * 1024) {  // + 768 bytes of static shared memory
-        static bool attr = [] {
+        static std::vector<char> seen;  // the attributes are per device
+        if (gs_first_on_device(seen)) {
           cudaFuncSetAttribute(k_sk_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
           cudaFuncSetAttribute(k_sk_persist, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-          return true;
-        }();
-        (void)attr;
+        }
         PersistArgs PA{};
         PA.n = n;
         PA.R = R;

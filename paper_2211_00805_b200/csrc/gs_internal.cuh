@@ -146,6 +146,17 @@ int gs_cuda_fail(gs_ctx* ctx, cudaError_t e, const char* where);
     if (_rc != 0) return _rc; \
   } while (0)
 
+// ---- once-per-device setup (function attributes are set per device) ---------------------------
+// true the first time `key`'s setup runs on the current device; `key` is any per-site object
+inline bool gs_first_on_device(std::vector<char>& seen) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if ((int)seen.size() <= dev) seen.resize(dev + 1, 0);
+  if (seen[dev]) return false;
+  seen[dev] = 1;
+  return true;
+}
+
 // ---- launch accounting / timing ------------------------------------------------------------
 void gs_launch_begin(gs_ctx* ctx, int cls);
 void gs_launch_end(gs_ctx* ctx, int cls);

@@ -414,11 +414,8 @@ int gs_knn_tc(gs_ctx* ctx, const double* dpts, const double* sq, int n, int d, i
   k_tc_prep<<<(unsigned)((elems + 255) / 256), 256, 0, s>>>(dpts, sq, n, npad, d, Ahi.get(), Alo.get(), Bhi.get(),
                                                            Blo.get(), maxk.get());
   gs_launch_end(ctx, 1);
-  static bool attr = [] {
-    cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
-    return true;
-  }();
-  (void)attr;
+  static std::vector<char> seen;  // the attribute is per device
+  if (gs_first_on_device(seen)) cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
   TcArgs P{};
   P.Ahi = Ahi.get();
   P.Alo = Alo.get();

@@ -53,14 +53,6 @@ struct WinBlk {  // one row block of the schedule (32 bytes)
 #ifndef GS_WIN_LMAX_CAP
 #define GS_WIN_LMAX_CAP 1024
 #endif
-// producer: one bulk copy per row (1) instead of one tile::gather4 per four rows (0; measured)
-#ifndef GS_WIN_BULK_ROWS
-#define GS_WIN_BULK_ROWS 0
-#endif
-// consumers fold two quads (eight entries) per iteration (1) or one quad and the row's tail (0)
-#ifndef GS_WIN_PAIR_QUADS
-#define GS_WIN_PAIR_QUADS 0
-#endif
 // dynamic shared memory of one CTA (the B200 opt-in maximum is 227 KB = 232448 bytes)
 #ifndef GS_WIN_SMEM_BYTES
 #define GS_WIN_SMEM_BYTES 232448
@@ -290,16 +282,7 @@ __global__ void __launch_bounds__(kWinThreads, 1)
           r.w += (int)grow;
           int slot = bk.slot0 + 4 * i;
           if (slot >= W) slot -= W;
-#if GS_WIN_BULK_ROWS
-          // experiment: one non-tensor bulk copy per row instead of one gather4 per four rows
-          const S* Tsrc = static_cast<const S*>(A.Tprev);
-          bulk_g2s(ring + (size_t)slot * GW, Tsrc + (size_t)r.x * GW, ROWB, &full[s]);
-          bulk_g2s(ring + (size_t)(slot + 1) * GW, Tsrc + (size_t)r.y * GW, ROWB, &full[s]);
-          bulk_g2s(ring + (size_t)(slot + 2) * GW, Tsrc + (size_t)r.z * GW, ROWB, &full[s]);
-          bulk_g2s(ring + (size_t)(slot + 3) * GW, Tsrc + (size_t)r.w * GW, ROWB, &full[s]);
-#else
           tma_gather4(ring + (size_t)slot * GW, &tmap, 0, r, &full[s]);
-#endif
         }
       }
 #pragma unroll
@@ -396,47 +379,6 @@ __global__ void __launch_bounds__(kWinThreads, 1)
           sl[2] = (int)(s4.y & 0xffffu);
           sl[3] = (int)(s4.y >> 16);
         };
-#if GS_WIN_PAIR_QUADS
-        // two quads per iteration: all eight entries' row loads in flight before the fma chain
-        // (rows average ~13 entries: two iterations instead of four dependent ones); the
-        // metadata past the row's end is staged padding and never used
-        int p = pr & ~3;
-        for (int left = (qe - p) - npad; left > 0; left -= 8, p += 8) {
-          S vv[8];
-          int sl[8];
-          {
-            S v4[4];
-            int s4[4];
-            quad_meta(p, v4, s4);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              vv[u] = v4[u];
-              sl[u] = s4[u];
-            }
-            quad_meta(p + 4, v4, s4);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              vv[4 + u] = v4[u];
-              sl[4 + u] = s4[u];
-            }
-          }
-          S xx[8][VEC];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            if (u < left) {
-              lds_vec<S, VEC>(rl + sl[u] * GW, xx[u]);
-            } else {
-#pragma unroll
-              for (int e = 0; e < VEC; ++e) xx[u][e] = S(0);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            if (u < left)
-#pragma unroll
-              for (int e = 0; e < VEC; ++e) y[e] = P::fmat(P::val(vv[u]), P::dec(xx[u][e]), y[e]);
-        }
-#else
         const int pf = npad ? qe - 4 : qe;  // end of the full quads
         int p = pr & ~3;
         for (; p < pf; p += 4) {
@@ -466,7 +408,6 @@ __global__ void __launch_bounds__(kWinThreads, 1)
 #pragma unroll
               for (int e = 0; e < VEC; ++e) y[e] = P::fmat(P::val(vv[u]), P::dec(xx[u][e]), y[e]);
         }
-#endif
         const size_t idx = gbase + (size_t)row * GW;
         if (A.k == 0) {  // plain SpMM
           st_enc<S, VEC>(static_cast<S*>(A.Tout) + idx, y);
