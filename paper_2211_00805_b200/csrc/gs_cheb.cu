@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 
 #include "gs_internal.cuh"
@@ -988,6 +989,13 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
     WA.W = w.ws->W;
     WA.nctas = w.ws->nctas;
   }
+  // GS_WIN_CTATIME=1 (diagnostics): per-CTA start/end times of the apply's steps, summarised on
+  // stderr (the tail of the persistent grid)
+  static const bool ctatime = getenv("GS_WIN_CTATIME") && atoi(getenv("GS_WIN_CTATIME")) != 0;
+  DevBuf<unsigned long long> ctt;
+  if (w.win && ctatime) {
+    GS_CUDA(ctx, ctt.alloc((size_t)2 * w.ws->nctas * w.G * K, ctx->stream));
+  }
   const bool seq = seq_groups() && w.G > 1 && !w.win;
   for (int g = 0; g < (seq ? w.G : 1); ++g) {
     if (seq) {
@@ -1001,8 +1009,30 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
       sched.step(f, K, k, A);
       A.Tprev = w.T[(a0 + k - 1) & 1].get();
       A.Tout = w.T[(a0 + k) & 1].get();
+      if (w.win && ctt.get()) WA.ctatime = ctt.get() + (size_t)2 * w.ws->nctas * w.G * (k - 1);
       if (w.win) launch_step_win<S>(ctx, w.GW, w.tmap[(a0 + k - 1) & 1], A, WA, k == K ? mode : MODE_NONE);
       else launch_step<S>(ctx, w.GW, w.rpc, A, k == K ? mode : MODE_NONE);
+    }
+  }
+  if (ctt.get()) {
+    const int nb = w.ws->nctas * w.G;
+    std::vector<unsigned long long> h((size_t)2 * nb * K);
+    GS_CUDA(ctx, cudaMemcpyAsync(h.data(), ctt.get(), h.size() * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    GS_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    for (int k = 1; k <= K; ++k) {
+      const unsigned long long* t = h.data() + (size_t)2 * nb * (k - 1);
+      unsigned long long s0 = ~0ull, e1 = 0;
+      std::vector<double> dur(nb), endt(nb);
+      for (int b = 0; b < nb; ++b) s0 = std::min(s0, t[2 * b]);
+      for (int b = 0; b < nb; ++b) {
+        dur[b] = (t[2 * b + 1] - t[2 * b]) * 1e-3;
+        endt[b] = (t[2 * b + 1] - s0) * 1e-3;
+        e1 = std::max(e1, t[2 * b + 1]);
+      }
+      std::sort(dur.begin(), dur.end());
+      std::sort(endt.begin(), endt.end());
+      fprintf(stderr, "[win step %2d] CTA duration us: min %.1f med %.1f max %.1f | end times: med %.1f p90 %.1f max %.1f\n",
+              k, dur[0], dur[nb / 2], dur[nb - 1], endt[nb / 2], endt[nb * 9 / 10], endt[nb - 1]);
     }
   }
   return (a0 + K) & 1;

@@ -107,6 +107,7 @@ struct WinArgs {
   const unsigned short* own;     // ring slot of every row's own T_{k-1} row (+16 padding)
   int W;                         // ring slots
   int nctas;
+  unsigned long long* ctatime;   // diagnostics (GS_WIN_CTATIME): per CTA start / end globaltimer
 };
 
 __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
@@ -207,6 +208,11 @@ __global__ void __launch_bounds__(kWinThreads, 1)
   const int g = blockIdx.x / WA.nctas;
   if (A.cs.gactive && A.cs.gactive[g] == 0) return;
   extern __shared__ __align__(128) unsigned char smem[];
+  if (WA.ctatime && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    WA.ctatime[2 * blockIdx.x] = t;
+  }
   const int W = WA.W;
   S* ring = reinterpret_cast<S*>(smem);
   unsigned char* meta = smem + (size_t)W * ROWB;
@@ -432,6 +438,14 @@ __global__ void __launch_bounds__(kWinThreads, 1)
     __syncthreads();  // every block consumed: the ring is free for the fold
     win_epilogue<S, GW, MODE, kWinWarps + 1>(A, g, cta, warp, sub, q, mn, mx, er,
                                               reinterpret_cast<double*>(smem));
+  }
+  if (WA.ctatime) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      WA.ctatime[2 * blockIdx.x + 1] = t;
+    }
   }
 }
 
