@@ -19,6 +19,7 @@
 #include "gs_internal.cuh"
 #include "gs_step.cuh"
 #include "gs_win.cuh"
+#include "gs_sell.cuh"
 #include "gs_persist.cuh"
 
 using namespace gsk;
@@ -602,6 +603,120 @@ void launch_step_gw(const StepArgs& A, int mode, int rpc, cudaStream_t s) {
   else launch_step_rpc<S, GW, kRowsPerCta>(A, mode, s);
 }
 
+// Sliced step kernels (gs_sell.cuh): layouts with at least four rows per warp. Opt-in (GS_SELL=1,
+// read per call so tests can compare them with k_cheb_step): bit-identical results, but measured
+// slower than the register-gather kernel on the shapes they were written for -- config 2's
+// 64-byte rows 413-555 vs 324 us, config 4's 128-byte rows 611-807 vs 401 us
+// (profiles/r02_summary.md "Sliced store"): the step is bound by the registers that hold gathers
+// in flight, not by the shuffles the sliced store removes.
+inline bool sell_enabled() {
+  const char* e = getenv("GS_SELL");
+  return e && atoi(e) != 0;
+}
+
+// one row per lane (C = 32) through k_cheb_sell: opt-in (GS_SELL_C32=1) -- measured slower than
+// k_cheb_step's one-row-per-lane path (config-3 shape at n = 2e6: 125-152 vs 75 us)
+inline bool sell_c32_enabled() {
+  const char* e = getenv("GS_SELL_C32");
+  return e && atoi(e) != 0;
+}
+
+template <typename S>
+int sell_height(int gw) {  // rows per warp of a group width (0: the sliced kernel does not apply)
+  int c = 0;
+  switch (gw) {
+    case 32: c = Lay<32, S>::RPW; break;
+    case 16: c = Lay<16, S>::RPW; break;
+    case 8: c = Lay<8, S>::RPW; break;
+    case 4: c = Lay<4, S>::RPW; break;
+    case 2: c = Lay<2, S>::RPW; break;
+    case 1: c = Lay<1, S>::RPW; break;
+    default: c = 0; break;
+  }
+  return c >= 4 ? c : 0;
+}
+
+template <typename S, int GW, int SPW>
+void launch_sell_spw(const StepArgs& A, const SellArgs& E, int mode, cudaStream_t s) {
+  if constexpr (Lay<GW, S>::RPW >= 4) {
+    const dim3 grid((unsigned)(A.tiles * A.Gl));
+    switch (mode) {
+      case MODE_NONE: k_cheb_sell<S, GW, MODE_NONE, SPW><<<grid, kStepThreads, 0, s>>>(A, E); break;
+      case MODE_SK_PSI: k_cheb_sell<S, GW, MODE_SK_PSI, SPW><<<grid, kStepThreads, 0, s>>>(A, E); break;
+      case MODE_SK_PHI: k_cheb_sell<S, GW, MODE_SK_PHI, SPW><<<grid, kStepThreads, 0, s>>>(A, E); break;
+      default: k_cheb_sell<S, GW, MODE_BARY_PSI, SPW><<<grid, kStepThreads, 0, s>>>(A, E); break;
+    }
+  }
+}
+
+// warp-staged sliced kernel (k_cheb_sellw): rows of at least four lanes
+template <typename S, int GW>
+void launch_sellw_gw(const StepArgs& A, const SellArgs& E, int mode, cudaStream_t s) {
+  if constexpr (Lay<GW, S>::RPW >= 4 && Lay<GW, S>::RPW <= 8) {
+    const dim3 grid((unsigned)(A.tiles * A.Gl));
+    switch (mode) {
+      case MODE_NONE: k_cheb_sellw<S, GW, MODE_NONE><<<grid, kStepThreads, 0, s>>>(A, E); break;
+      case MODE_SK_PSI: k_cheb_sellw<S, GW, MODE_SK_PSI><<<grid, kStepThreads, 0, s>>>(A, E); break;
+      case MODE_SK_PHI: k_cheb_sellw<S, GW, MODE_SK_PHI><<<grid, kStepThreads, 0, s>>>(A, E); break;
+      default: k_cheb_sellw<S, GW, MODE_BARY_PSI><<<grid, kStepThreads, 0, s>>>(A, E); break;
+    }
+  }
+}
+
+template <typename S, int GW>
+int sellw_occupancy_gw() {  // resident CTAs per SM of the plain step
+  int occ = 0;
+  if constexpr (Lay<GW, S>::RPW >= 4 && Lay<GW, S>::RPW <= 8)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cheb_sellw<S, GW, MODE_NONE>, kStepThreads, 0);
+  return occ;
+}
+
+template <typename S>
+int sellw_occupancy(int gw) {
+  switch (gw) {
+    case 32: return sellw_occupancy_gw<S, 32>();
+    case 16: return sellw_occupancy_gw<S, 16>();
+    case 8: return sellw_occupancy_gw<S, 8>();
+    case 4: return sellw_occupancy_gw<S, 4>();
+    default: return 0;
+  }
+}
+
+template <typename S>
+void launch_step_sellw(gs_ctx* ctx, int gw, const StepArgs& A, const SellArgs& E, int mode) {
+  gs_launch_begin(ctx, 0);
+  switch (gw) {
+    case 32: launch_sellw_gw<S, 32>(A, E, mode, ctx->stream); break;
+    case 16: launch_sellw_gw<S, 16>(A, E, mode, ctx->stream); break;
+    case 8: launch_sellw_gw<S, 8>(A, E, mode, ctx->stream); break;
+    default: launch_sellw_gw<S, 4>(A, E, mode, ctx->stream); break;
+  }
+  gs_launch_end(ctx, 0);
+}
+
+template <typename S>
+void launch_step_sell(gs_ctx* ctx, int gw, int spw, const StepArgs& A, const SellArgs& E, int mode) {
+  gs_launch_begin(ctx, 0);
+#define GS_SELL_CASE(W)                                                        \
+  case W:                                                                      \
+    if (spw == 1) launch_sell_spw<S, W, 1>(A, E, mode, ctx->stream);           \
+    else launch_sell_spw<S, W, kSellSpw>(A, E, mode, ctx->stream);             \
+    break;
+  switch (gw) {
+    GS_SELL_CASE(32)
+    GS_SELL_CASE(16)
+    GS_SELL_CASE(8)
+    GS_SELL_CASE(4)
+    GS_SELL_CASE(2)
+    default:
+      if (spw == 1) launch_sell_spw<S, 1, 1>(A, E, mode, ctx->stream);
+      else launch_sell_spw<S, 1, kSellSpw>(A, E, mode, ctx->stream);
+      break;
+  }
+#undef GS_SELL_CASE
+  gs_launch_end(ctx, 0);
+}
+
 template <typename S>
 void launch_step(gs_ctx* ctx, int gw, int rpc, const StepArgs& A, int mode) {
   gs_launch_begin(ctx, 0);
@@ -808,6 +923,10 @@ struct Work {
   bool blk = false;  // wide fp64 rows through the 8-row block kernel (k_cheb_blk)
   bool win = false;  // wide rows through the windowed kernel (k_cheb_win, lay[2])
   const gs_winsched* ws = nullptr;
+  const gs_sell* sell = nullptr;  // several rows per warp through the sliced kernel (k_cheb_sell)
+  int spw = 1;                    // its slices per warp
+  bool sellw = false;             // ... through the warp-staged persistent kernel (k_cheb_sellw)
+  DevBuf<int> wstart;             // its static split of the slices over the grid's warps
   alignas(64) CUtensorMap tmap[2];  // gather sources T[0], T[1] (win)
   struct TView {  // T[0], T[1]: halves of one allocation (one L2 access-policy window covers both)
     S* p = nullptr;
@@ -851,6 +970,32 @@ struct Work {
       } else if (rc != GS_ERR_UNSUPPORTED) {
         return rc;
       }
+    }
+    if (f && ld_ < 0 && n > 0 && !w1 && !blk && !win && sell_enabled() && sell_height<S>(GW) > 0 &&
+        (sell_height<S>(GW) <= 8 || sell_c32_enabled())) {
+      const int C = sell_height<S>(GW);
+      gs_layout& Ly = const_cast<gs_filter*>(f)->lay[lay];
+      for (const gs_sell* e : Ly.sell)
+        if (e->C == C && e->elem_bytes == (int)sizeof(S)) sell = e;
+      if (!sell) {
+        gs_sell* e = nullptr;
+        GS_TRY(gs_sell_build(ctx, Ly.perm, Ly.vals32, C, (int)sizeof(S), &e));
+        Ly.sell.push_back(e);
+        sell = e;
+      }
+      const int warps = kStepThreads / 32;
+      if (C <= 8) {  // warp-staged persistent kernel: one wave of CTAs over all column groups
+        sellw = true;
+        const int occ = std::max(1, sellw_occupancy<S>(GW));
+        const int full = (sell->nslices + warps - 1) / warps;
+        tiles = std::max(1, std::min(full, (148 * occ + G - 1) / G));
+        GS_CUDA(ctx, wstart.alloc((size_t)tiles * warps + 1, s));
+        GS_TRY(gs_sell_split(ctx, sell, tiles * warps, wstart.get()));
+      } else {
+        spw = (int64_t)G * ((sell->nslices + warps * kSellSpw - 1) / (warps * kSellSpw)) < 4 * 148 ? 1 : kSellSpw;
+        tiles = (sell->nslices + warps * spw - 1) / (warps * spw);
+      }
+      rpc = 1;
     }
     const size_t len = (size_t)Bpad * (ld > 0 ? ld : 1);
     GS_CUDA(ctx, Tall.alloc(2 * len, s));
@@ -989,6 +1134,14 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
     WA.W = w.ws->W;
     WA.nctas = w.ws->nctas;
   }
+  SellArgs SE{};
+  if (w.sell) {
+    SE.soff = w.sell->soff;
+    SE.cols = w.sell->cols;
+    SE.vals = w.sell->vals;
+    SE.nslices = w.sell->nslices;
+    SE.wstart = w.wstart.get();
+  }
   // GS_WIN_CTATIME=1 (diagnostics): per-CTA start/end times of the apply's steps, summarised on
   // stderr (the tail of the persistent grid)
   static const bool ctatime = getenv("GS_WIN_CTATIME") && atoi(getenv("GS_WIN_CTATIME")) != 0;
@@ -1011,6 +1164,8 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
       A.Tout = w.T[(a0 + k) & 1].get();
       if (w.win && ctt.get()) WA.ctatime = ctt.get() + (size_t)2 * w.ws->nctas * w.G * (k - 1);
       if (w.win) launch_step_win<S>(ctx, w.GW, w.tmap[(a0 + k - 1) & 1], A, WA, k == K ? mode : MODE_NONE);
+      else if (w.sellw) launch_step_sellw<S>(ctx, w.GW, A, SE, k == K ? mode : MODE_NONE);
+      else if (w.sell) launch_step_sell<S>(ctx, w.GW, w.spw, A, SE, k == K ? mode : MODE_NONE);
       else launch_step<S>(ctx, w.GW, w.rpc, A, k == K ? mode : MODE_NONE);
     }
   }
@@ -2374,6 +2529,8 @@ static int finish_layout(gs_ctx* ctx, gs_filter* f, int l) {
   Ly.near_frac = 1.0;
   for (auto* w : Ly.win) gs_win_destroy(w);
   Ly.win.clear();
+  for (auto* e : Ly.sell) gs_sell_destroy(e);
+  Ly.sell.clear();
   do {
     rc = gs_permute_graph(ctx, f->scaled, Ly.order, Ly.newpos, &Ly.perm);
     if (rc) break;
@@ -2468,6 +2625,7 @@ extern "C" void gs_filter_destroy(gs_filter* f) {
     cudaFree(Ly.rec_key);
     cudaFree(Ly.rec_val);
     for (auto* w : Ly.win) gs_win_destroy(w);
+    for (auto* e : Ly.sell) gs_sell_destroy(e);
   }
   cudaFree(f->d_coeffs);
   delete f;

@@ -84,6 +84,17 @@ struct gs_winsched {
   int64_t padded = 0;
 };
 
+// Jagged sliced store of a CSR operator for the sliced step kernel (gs_sell.cu / gs_sell.cuh).
+struct gs_sell {
+  int C = 0, JV = 0, elem_bytes = 0;  // rows per slice, entries per chunk, value size
+  int nslices = 0;
+  long long total = 0;        // stored entries (padding included)
+  long long* soff = nullptr;  // nslices + 1
+  int* cols = nullptr;
+  void* vals = nullptr;
+  long long* cpre = nullptr;  // nslices + 1: prefix of the slice costs (static warp split)
+};
+
 // One locality layout of the filter's operator (gs_reorder.cu): renumbered rows + fp32 copy.
 struct gs_layout {
   gs_graph* perm = nullptr;  // L_s with rows renumbered (entries kept in original column order)
@@ -98,6 +109,8 @@ struct gs_layout {
   double* rec_val = nullptr;
   // lay[2] only: ring schedules of the windowed step kernel, one per row size (built on first use)
   std::vector<gs_winsched*> win;
+  // sliced stores of `perm`, one per (slice height, value size); built on first use
+  std::vector<gs_sell*> sell;
 };
 
 struct gs_filter {
@@ -225,6 +238,10 @@ int gs_win_build(gs_ctx* ctx, gs_filter* f, int row_bytes, int elem_bytes);
 const gs_winsched* gs_win_get(const gs_filter* f, int row_bytes, int elem_bytes);
 void gs_win_destroy(gs_winsched* w);
 int gs_win_tensor_map(gs_ctx* ctx, void* tmap, const void* base, int64_t rows, int row_elems, int elem_bytes);
+// sliced store (gs_sell.cu) of G for slices of C rows, values of elem_bytes (4: vals32)
+int gs_sell_build(gs_ctx* ctx, const gs_graph* G, const float* vals32, int C, int elem_bytes, gs_sell** out);
+void gs_sell_destroy(gs_sell* p);
+int gs_sell_split(gs_ctx* ctx, const gs_sell* p, int W, int* d_wstart);
 // layout l of f from a host order (order[new] = old): newpos, renumbered operator, fp32 copy
 int gs_layout_from_order(gs_ctx* ctx, gs_filter* f, int l, const int* h_order);
 // kNN (gs_graph.cu / gs_knn_tc.cu): brute force over a query list; tensor-core prefilter + exact
