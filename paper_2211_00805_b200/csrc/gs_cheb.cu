@@ -532,11 +532,34 @@ int rows_per_block(int gw) {  // rows covered by one CTA pass (8 warps)
 
 // Latency-bound one-column fp64 problems up to this many rows take one warp per row (GS_W1_MAX)
 inline int w1_max_rows() {
-  static const int v = [] {
-    const char* e = getenv("GS_W1_MAX");
-    return e ? atoi(e) : 32768;
-  }();
-  return v;
+  const char* e = getenv("GS_W1_MAX");  // read per call
+  return e ? atoi(e) : 32768;
+}
+
+// lanes per row of a group width's layout
+template <typename S>
+int rpc_lpr(int gw) {
+  switch (gw) {
+    case 64: return Lay<64, S>::LPR;
+    case 32: return Lay<32, S>::LPR;
+    case 16: return Lay<16, S>::LPR;
+    case 8: return Lay<8, S>::LPR;
+    case 4: return Lay<4, S>::LPR;
+    case 2: return Lay<2, S>::LPR;
+    default: return Lay<1, S>::LPR;
+  }
+}
+
+// One-row-per-lane layouts with the CSR stream staged through shared memory (k_cheb_lane):
+// GS_LANE=0 keeps them on k_cheb_step, GS_LANE_PAD=0 stages the plain CSR arrays instead of the
+// odd-stride copy (both read per call).
+inline bool lane_enabled() {
+  const char* e = getenv("GS_LANE");
+  return !(e && atoi(e) == 0);
+}
+inline bool lane_pad_enabled() {
+  const char* e = getenv("GS_LANE_PAD");
+  return !(e && atoi(e) == 0);
 }
 
 // row blocks per CTA of the full (multi-block) instantiation of a group width
@@ -559,10 +582,8 @@ int rpc_full(int gw) {
 // than two CTAs per SM, in which case 1 (small, latency-bound problems such as config 0).
 template <typename S>
 int choose_rpc(int n, int gw, int groups, double near_frac = 1.0) {
-  static const int forced = [] {
-    const char* e = getenv("GS_RPC");
-    return e ? atoi(e) : 0;
-  }();
+  const char* renv = getenv("GS_RPC");  // read per call (tests force the multi-block kernels)
+  const int forced = renv ? atoi(renv) : 0;
   if (forced == 1) return 1;
   if (forced > 1) return rpc_full<S>(gw);
   // several lanes per row and fewer than 32 columns (the degree-sorted layout; configs 2 and 4:
@@ -596,10 +617,35 @@ void launch_step_rpc(const StepArgs& A, int mode, cudaStream_t s) {
   }
 }
 
+template <typename S, int GW, int MODE>
+void launch_lane_mode(const StepArgs& A, cudaStream_t s) {
+  constexpr int smem = lane_smem_bytes<S>();
+  static std::vector<char> seen;  // the attribute is per device
+  if (gs_first_on_device(seen))
+    cudaFuncSetAttribute(k_cheb_lane<S, GW, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const char* eb = getenv("GS_LANE_PF_BACK");
+  const char* ef = getenv("GS_LANE_PF_FWD");
+  k_cheb_lane<S, GW, MODE><<<dim3((unsigned)(A.tiles * A.Gl)), kStepThreads, smem, s>>>(
+      A, eb ? atoi(eb) : 0, ef ? atoi(ef) : 0);
+}
+
+template <typename S, int GW>
+void launch_lane(const StepArgs& A, int mode, cudaStream_t s) {
+  switch (mode) {
+    case MODE_NONE: launch_lane_mode<S, GW, MODE_NONE>(A, s); break;
+    case MODE_SK_PSI: launch_lane_mode<S, GW, MODE_SK_PSI>(A, s); break;
+    case MODE_SK_PHI: launch_lane_mode<S, GW, MODE_SK_PHI>(A, s); break;
+    default: launch_lane_mode<S, GW, MODE_BARY_PSI>(A, s); break;
+  }
+}
+
 template <typename S, int GW>
 void launch_step_gw(const StepArgs& A, int mode, int rpc, cudaStream_t s) {
   if (rpc == 1) launch_step_rpc<S, GW, 1>(A, mode, s);
-  else if constexpr (Lay<GW, S>::LPR == 1) launch_step_rpc<S, GW, kRowsPerCta1>(A, mode, s);
+  else if constexpr (Lay<GW, S>::LPR == 1) {
+    if (A.lane) launch_lane<S, GW>(A, mode, s);
+    else launch_step_rpc<S, GW, kRowsPerCta1>(A, mode, s);
+  }
   else launch_step_rpc<S, GW, kRowsPerCta>(A, mode, s);
 }
 
@@ -913,6 +959,12 @@ struct L2Window {
   }
 };
 
+template <typename S>
+const void* layout_vals(const gs_layout& L) {
+  if constexpr (sizeof(S) == 4) return L.vals32;
+  else return L.perm->vals;
+}
+
 // Workspace for one batched run: grouped buffers (precision S) + per-column state.
 template <typename S>
 struct Work {
@@ -926,6 +978,8 @@ struct Work {
   const gs_sell* sell = nullptr;  // several rows per warp through the sliced kernel (k_cheb_sell)
   int spw = 1;                    // its slices per warp
   bool sellw = false;             // ... through the warp-staged persistent kernel (k_cheb_sellw)
+  bool lane = false;              // one row per lane through the staged kernel (k_cheb_lane)
+  const gs_lanepad* lp = nullptr;  // its odd-stride CSR copy (filter layouts; GS_LANE_PAD=0: none)
   DevBuf<int> wstart;             // its static split of the slices over the grid's warps
   alignas(64) CUtensorMap tmap[2];  // gather sources T[0], T[1] (win)
   struct TView {  // T[0], T[1]: halves of one allocation (one L2 access-policy window covers both)
@@ -997,6 +1051,23 @@ struct Work {
       }
       rpc = 1;
     }
+    lane = !w1 && !blk && !win && !sell && rpc > 1 && rpc_lpr<S>(GW) == 1 && lane_enabled();
+    if (lane && f && ld_ < 0 && n > 0 && lane_pad_enabled()) {
+      gs_layout& Ly = const_cast<gs_filter*>(f)->lay[lay];
+      for (const gs_lanepad* e : Ly.lanepad)
+        if (e->elem_bytes == (int)sizeof(S)) lp = e;
+      if (!lp) {
+        gs_lanepad* e = nullptr;
+        const int rc = gs_lanepad_build(ctx, Ly.perm->offs, Ly.perm->cols, layout_vals<S>(Ly), (int)sizeof(S), n,
+                                        Ly.perm->nnz, &e);
+        if (rc == GS_OK) {
+          Ly.lanepad.push_back(e);
+          lp = e;
+        } else if (rc != GS_ERR_UNSUPPORTED) {
+          return rc;
+        }
+      }
+    }
     const size_t len = (size_t)Bpad * (ld > 0 ? ld : 1);
     GS_CUDA(ctx, Tall.alloc(2 * len, s));
     T[0].p = Tall.get();
@@ -1065,12 +1136,6 @@ struct AccSchedule {
   }
 };
 
-template <typename S>
-const void* layout_vals(const gs_layout& L) {
-  if constexpr (sizeof(S) == 4) return L.vals32;
-  else return L.perm->vals;
-}
-
 // One full filter application on the workspace: T0 in T[a0]; K steps; the last step uses `mode`
 // with the given epilogue operands. Returns the buffer index holding the next T_0.
 // BARY_PSI applies: the log-domain geometric mean fused into the last step's epilogue
@@ -1093,6 +1158,12 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
   A.cols = G->cols;
   A.vals = layout_vals<S>(Ly);
   A.warp_rows = w.w1;
+  A.lane = w.lane;
+  if (w.lp) {
+    A.offs = w.lp->offs;
+    A.cols = w.lp->cols;
+    A.vals = w.lp->vals;
+  }
   if (w.blk) {
     A.rec_key = Ly.rec_key;
     A.rec_val = Ly.rec_val;
@@ -2088,6 +2159,7 @@ int run_apply_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& 
   A.cols = p->local->cols;
   if constexpr (sizeof(S) == 4) A.vals = p->vals32;
   else A.vals = p->local->vals;
+  A.lane = lane_enabled();
   A.n = w.n;
   A.ld = w.ld;
   A.tiles = w.tiles;
@@ -2531,6 +2603,8 @@ static int finish_layout(gs_ctx* ctx, gs_filter* f, int l) {
   Ly.win.clear();
   for (auto* e : Ly.sell) gs_sell_destroy(e);
   Ly.sell.clear();
+  for (auto* e : Ly.lanepad) gs_lanepad_destroy(e);
+  Ly.lanepad.clear();
   do {
     rc = gs_permute_graph(ctx, f->scaled, Ly.order, Ly.newpos, &Ly.perm);
     if (rc) break;
@@ -2626,6 +2700,7 @@ extern "C" void gs_filter_destroy(gs_filter* f) {
     cudaFree(Ly.rec_val);
     for (auto* w : Ly.win) gs_win_destroy(w);
     for (auto* e : Ly.sell) gs_sell_destroy(e);
+    for (auto* e : Ly.lanepad) gs_lanepad_destroy(e);
   }
   cudaFree(f->d_coeffs);
   delete f;
@@ -2770,6 +2845,7 @@ extern "C" int gs_graph_multiply(gs_ctx* ctx, const gs_graph* g, const double* x
   A.offs = g->offs;
   A.cols = g->cols;
   A.vals = g->vals;
+  A.lane = lane_enabled();
   A.n = n;
   A.ld = n;
   A.tiles = w.tiles;
@@ -3032,6 +3108,7 @@ int gs_spmm_grouped(gs_ctx* ctx, const gs_graph* g, const double* x, double* y, 
   A.offs = g->offs;
   A.cols = g->cols;
   A.vals = g->vals;
+  A.lane = lane_enabled();
   A.n = n;
   A.ld = n;
   A.tiles = (n + rows_per_block<double>(GW) * rpc - 1) / (rows_per_block<double>(GW) * rpc);

@@ -96,6 +96,16 @@ struct gs_sell {
 };
 
 // One locality layout of the filter's operator (gs_reorder.cu): renumbered rows + fp32 copy.
+// odd-stride copy of a layout's CSR arrays for k_cheb_lane (gs_lane.cu): rows with an even number
+// of entries are followed by one pad entry (column -1, value 0)
+struct gs_lanepad {
+  int* offs = nullptr;  // n + 1
+  int* cols = nullptr;  // nnz + kCsrPad
+  void* vals = nullptr;
+  int elem_bytes = 0;   // 4: vals32, 8: fp64 values
+  int64_t nnz = 0;      // stored entries, pads included
+};
+
 struct gs_layout {
   gs_graph* perm = nullptr;  // L_s with rows renumbered (entries kept in original column order)
   int* order = nullptr;      // order[new] = old
@@ -111,6 +121,8 @@ struct gs_layout {
   std::vector<gs_winsched*> win;
   // sliced stores of `perm`, one per (slice height, value size); built on first use
   std::vector<gs_sell*> sell;
+  // odd-stride copies of `perm` for k_cheb_lane, one per value size; built on first use
+  std::vector<gs_lanepad*> lanepad;
 };
 
 struct gs_filter {
@@ -242,6 +254,10 @@ int gs_win_tensor_map(gs_ctx* ctx, void* tmap, const void* base, int64_t rows, i
 int gs_sell_build(gs_ctx* ctx, const gs_graph* G, const float* vals32, int C, int elem_bytes, gs_sell** out);
 void gs_sell_destroy(gs_sell* p);
 int gs_sell_split(gs_ctx* ctx, const gs_sell* p, int W, int* d_wstart);
+// odd-stride CSR copy (gs_lane.cu); GS_ERR_UNSUPPORTED when the padded positions leave 32 bits
+int gs_lanepad_build(gs_ctx* ctx, const int* offs, const int* cols, const void* vals, int elem_bytes, int n,
+                     int64_t nnz, gs_lanepad** out);
+void gs_lanepad_destroy(gs_lanepad* p);
 // layout l of f from a host order (order[new] = old): newpos, renumbered operator, fp32 copy
 int gs_layout_from_order(gs_ctx* ctx, gs_filter* f, int l, const int* h_order);
 // kNN (gs_graph.cu / gs_knn_tc.cu): brute force over a query list; tensor-core prefilter + exact

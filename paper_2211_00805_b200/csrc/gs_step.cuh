@@ -336,6 +336,8 @@ struct StepArgs {  // vector pointers are S* of the launch's precision
   int n, tiles, g0, Gl, Bpad;  // rows [row0, n) in `tiles` CTA tiles per column group
   int row0, tile0;             // first row; index of the first tile in the error partials
   int warp_rows;               // one warp per row (k_cheb_step_w1; one-column fp64 problems)
+  int lane;                    // one row per lane: the staged kernel k_cheb_lane (offs / cols / vals may be
+                               // its odd-stride copy, gs_lane.cu: pad entries have column -1)
   int64_t ld;         // rows per column group (n, or local + halo rows for a row partition)
   const void* Tprev;  // T_{k-1}
   void* Tout;         // T_{k-2} in, T_k out (or next T_0 / SpMM output)
@@ -941,6 +943,200 @@ __global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0
     }
   }
   if constexpr (MODE != MODE_NONE) block_epilogue<S, GW, MODE>(A, g, tile, warp, sub, q, mn, mx, er);
+}
+
+// One row per lane (B <= 2 fp64, B <= 4 in the 32-bit mode; config 3's one-column Sinkhorn) with the
+// CSR stream staged through shared memory. The (col, val) entries of a 256-row block are one
+// contiguous run of both arrays, so thread 0 brings each block's slice in with two bulk copies
+// (cp.async.bulk, completion on an mbarrier) GS_LANE_STAGES blocks ahead of the lanes that fold it:
+// the matrix stream -- 85% of this layout's bytes -- is in flight without holding registers, and
+// the lanes' dependent chain shrinks to shared-memory index -> gather -> fma. Same CTA geometry,
+// same per-row fma chain and the same epilogue partials as k_cheb_step (bit-identical results);
+// a block whose slice exceeds a stage (GS_LANE_CAP entries) is folded from global memory by
+// cheb_row instead. sparse.cpp:85-99 / heat.cpp:121-130.
+#ifndef GS_LANE_STAGES
+#define GS_LANE_STAGES 1  // stages per CTA: 1 x 4 CTAs per SM measured faster than 2 x 3 (config 3: 563 vs 610 us)
+#endif
+#ifndef GS_LANE_CAP
+#define GS_LANE_CAP 4608  // entries per stage: 18 per row of a 256-row block
+#endif
+#ifndef GS_LANE_MIN_BLOCKS
+#define GS_LANE_MIN_BLOCKS 4
+#endif
+#ifndef GS_LANE_BATCH
+#define GS_LANE_BATCH 8  // gathers in flight per lane (at most 8: the stage's read slack)
+#endif
+constexpr int kLaneStride = GS_LANE_CAP + 8;  // stage stride (16-byte multiple)
+template <typename S>
+constexpr int lane_smem_bytes() {
+  return GS_LANE_STAGES * kLaneStride * (int)(sizeof(int) + sizeof(S));
+}
+
+// NB consecutive staged entries of one row folded into its chain (CSR order). TAIL: positions at
+// or past `pe` read the row's last entry instead and skip their fma.
+template <typename S, int GW, int NB, bool TAIL>
+__device__ __forceinline__ void lane_batch(const int* sc, const S* sv, int p, int pe, const S* __restrict__ Tp,
+                                           double (&y)[Lay<GW, S>::VEC]) {
+  constexpr int VEC = Lay<GW, S>::VEC;
+  using P = Prec<S>;
+  int at[NB];
+  int cc[NB];
+  S vv[NB];
+  S xx[NB][VEC];
+#pragma unroll
+  for (int u = 0; u < NB; ++u) at[u] = TAIL ? min(p + u, pe - 1) : p + u;
+#pragma unroll
+  for (int u = 0; u < NB; ++u) cc[u] = sc[at[u]];
+#pragma unroll
+  for (int u = 0; u < NB; ++u) ld_vec<S, VEC>(Tp + (size_t)cc[u] * GW, xx[u]);
+#pragma unroll
+  for (int u = 0; u < NB; ++u) vv[u] = sv[at[u]];
+#pragma unroll
+  for (int u = 0; u < NB; ++u)
+    if (!TAIL || p + u < pe) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) y[e] = P::fmat(P::val(vv[u]), P::dec(xx[u][e]), y[e]);
+    }
+}
+
+// One row's chain from entries [p, pe) of a slice (shared-memory stage or global arrays):
+// GS_LANE_BATCH entries at a time -- indices, the gathers, then the values (read while the gathers
+// are in flight) and the fma chain in CSR order. A trailing pad entry of the odd-stride copy
+// (column -1, gs_lane.cu) is dropped first.
+template <typename S, int GW>
+__device__ __forceinline__ void lane_fold(const int* sc, const S* sv, int p, int pe, const S* __restrict__ Tp,
+                                          double (&y)[Lay<GW, S>::VEC]) {
+  constexpr int NB = GS_LANE_BATCH;
+  if (pe > p && sc[pe - 1] < 0) --pe;
+  for (; p + NB <= pe; p += NB) lane_batch<S, GW, NB, false>(sc, sv, p, pe, Tp, y);
+  // the row's tail: positions past its end re-read its last entry (a valid address) and are
+  // left out of the chain
+  if (p + NB / 2 < pe) lane_batch<S, GW, NB, true>(sc, sv, p, pe, Tp, y);
+  else if (p < pe) lane_batch<S, GW, NB / 2, true>(sc, sv, p, pe, Tp, y);
+}
+
+template <typename S, int GW, int MODE>
+__global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN_BLOCKS) k_cheb_lane(const StepArgs A, const int pf_back, const int pf_fwd) {
+  using L = Lay<GW, S>;
+  using P = Prec<S>;
+  constexpr int VEC = L::VEC;
+  static_assert(L::LPR == 1, "one row per lane");
+  constexpr int RPC = kRowsPerCta1, STG = GS_LANE_STAGES, BLOCK_ROWS = kStepThreads;
+  if (A.status && (A.status->error || A.status->done)) return;
+  const int tl = blockIdx.x / A.Gl;
+  const int tile = A.tile0 + tl;
+  const int g = A.g0 + blockIdx.x % A.Gl;
+  if (A.cs.gactive && A.cs.gactive[g] == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  extern __shared__ __align__(128) unsigned char lane_smem[];
+  int* s_cols = reinterpret_cast<int*>(lane_smem);
+  S* s_vals = reinterpret_cast<S*>(lane_smem + (size_t)STG * kLaneStride * sizeof(int));
+  __shared__ __align__(8) unsigned long long s_bar[STG];
+  double mn[VEC], mx[VEC], er[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    mn[e] = INFINITY;
+    mx[e] = MODE == MODE_BARY_PSI ? -INFINITY : 0.0;
+    er[e] = 0.0;
+  }
+  const int rbase = A.row0 + tl * (BLOCK_ROWS * RPC);
+  const S* __restrict__ vals = static_cast<const S*>(A.vals);
+  // block j's slice: first entry rounded down and length rounded up to four entries (16-byte
+  // copies; the arrays carry kCsrPad). 0 = no rows; > GS_LANE_CAP = not staged.
+  auto slice = [&](int j, int& p0) {
+    const int r0 = rbase + j * BLOCK_ROWS;
+    p0 = 0;
+    if (j >= RPC || r0 >= A.n) return 0;
+    p0 = __ldg(A.offs + r0) & ~3;
+    return ((__ldg(A.offs + min(r0 + BLOCK_ROWS, A.n)) + 3) & ~3) - p0;
+  };
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int st = 0; st < STG; ++st) mbar_init(&s_bar[st], 1);
+    fence_proxy_async();
+  }
+  __syncthreads();
+  auto issue = [&](int j) {
+    if (threadIdx.x != 0) return;
+    int p0;
+    const int len = slice(j, p0);
+    if (len <= 0 || len > GS_LANE_CAP) return;
+    const int st = j % STG;
+    mbar_expect_tx(&s_bar[st], (unsigned)(len * (sizeof(int) + sizeof(S))));
+    bulk_g2s(s_cols + st * kLaneStride, A.cols + p0, (unsigned)(len * sizeof(int)), &s_bar[st]);
+    bulk_g2s(s_vals + st * kLaneStride, vals + p0, (unsigned)(len * sizeof(S)), &s_bar[st]);
+  };
+#pragma unroll
+  for (int j = 0; j < STG; ++j) issue(j);
+  const size_t gbase = (size_t)g * A.ld * GW;
+  const S* __restrict__ Tp = static_cast<const S*>(A.Tprev) + gbase;
+  // T_{k-1} rows around the tile into L2 while the first slice is in flight: the first touch of
+  // a gathered line otherwise costs a DRAM round trip inside a lane's dependent chain
+  if (threadIdx.x == 32 && pf_back + pf_fwd > 0) {
+    const long long lo = max(0, rbase - pf_back), hi = min((long long)A.n, (long long)rbase + BLOCK_ROWS * RPC + pf_fwd);
+    const unsigned long long a0 = (reinterpret_cast<unsigned long long>(Tp + lo * GW) + 15ull) & ~15ull;
+    const unsigned long long a1 = reinterpret_cast<unsigned long long>(Tp + hi * GW) & ~15ull;
+    if (a1 > a0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
+  }
+  unsigned phase = 0;  // bit st: parity of stage st's next completion (oversize blocks skip theirs)
+  // a row's CSR range and own-row operands T_{k-1}[i], T_{k-2}[i], acc[i]: loaded one block ahead,
+  // so their DRAM latency overlaps the previous block's gathers instead of heading this block's
+  // dependent chain
+  struct RowPre {
+    int p, pe;
+    S tps[VEC], t2s[VEC], a0s[VEC];
+  };
+  auto preload = [&](int j) {
+    RowPre r;
+    r.p = r.pe = 0;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) r.tps[e] = r.t2s[e] = r.a0s[e] = S(0);
+    const int row = rbase + j * BLOCK_ROWS + threadIdx.x;
+    if (j < RPC && row < A.n) {
+      r.p = __ldg(A.offs + row);
+      r.pe = __ldg(A.offs + row + 1);
+      if (A.k != 0) {
+        const size_t idx = gbase + (size_t)row * GW;
+        ld_vec<S, VEC>(static_cast<const S*>(A.Tprev) + idx, r.tps);
+        if (A.k >= 2) ld_vec_rw<S, VEC>(static_cast<const S*>(A.Tout) + idx, r.t2s);
+        if (A.acc_terms > 0 && !A.acc_init) ld_vec_rw<S, VEC>(static_cast<const S*>(A.acc) + idx, r.a0s);
+      }
+    }
+    return r;
+  };
+  RowPre cur = preload(0);
+#pragma unroll 1
+  for (int j = 0; j < RPC; ++j) {
+    int p0;
+    const int len = slice(j, p0);
+    if (len <= 0) break;  // past the last row (CTA-uniform)
+    const int row = rbase + j * BLOCK_ROWS + threadIdx.x;
+    const RowPre nxt = preload(j + 1);
+    const bool valid = row < A.n;
+    double y[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) y[e] = 0.0;
+    if (len > GS_LANE_CAP) {  // oversize slice (CTA-uniform): the same fold from global memory
+      if (valid) lane_fold<S, GW>(A.cols + p0, vals + p0, cur.p - p0, cur.pe - p0, Tp, y);
+    } else {
+      const int st = j % STG;
+      mbar_wait(&s_bar[st], (phase >> st) & 1u);
+      phase ^= 1u << st;
+      if (valid)
+        lane_fold<S, GW>(s_cols + st * kLaneStride, s_vals + st * kLaneStride, cur.p - p0, cur.pe - p0, Tp, y);
+    }
+    if (valid) {
+      if (A.k == 0) st_enc<S, VEC>(static_cast<S*>(A.Tout) + gbase + (size_t)row * GW, y);  // plain SpMM
+      else finish_row_ops<S, GW, MODE>(A, g, row, 0, y, mn, mx, er, cur.tps, cur.t2s, cur.a0s);
+    }
+    cur = nxt;
+    if (j + STG < RPC) {  // every lane is done with the stage before it is refilled
+      __syncthreads();
+      issue(j + STG);
+    }
+  }
+  if constexpr (MODE != MODE_NONE) block_epilogue<S, GW, MODE>(A, g, tile, warp, lane, 0, mn, mx, er);
 }
 
 // 8-row blocks (wide fp64 rows, one warp per block): the gathers of a block's rows are shared.
