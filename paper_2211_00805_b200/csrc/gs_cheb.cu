@@ -623,10 +623,7 @@ void launch_lane_mode(const StepArgs& A, cudaStream_t s) {
   static std::vector<char> seen;  // the attribute is per device
   if (gs_first_on_device(seen))
     cudaFuncSetAttribute(k_cheb_lane<S, GW, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const char* eb = getenv("GS_LANE_PF_BACK");
-  const char* ef = getenv("GS_LANE_PF_FWD");
-  k_cheb_lane<S, GW, MODE><<<dim3((unsigned)(A.tiles * A.Gl)), kStepThreads, smem, s>>>(
-      A, eb ? atoi(eb) : 0, ef ? atoi(ef) : 0);
+  k_cheb_lane<S, GW, MODE><<<dim3((unsigned)(A.tiles * A.Gl)), kStepThreads, smem, s>>>(A);
 }
 
 template <typename S, int GW>

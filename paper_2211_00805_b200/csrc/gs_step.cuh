@@ -946,30 +946,29 @@ __global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0
 }
 
 // One row per lane (B <= 2 fp64, B <= 4 in the 32-bit mode; config 3's one-column Sinkhorn) with the
-// CSR stream staged through shared memory. The (col, val) entries of a 256-row block are one
-// contiguous run of both arrays, so thread 0 brings each block's slice in with two bulk copies
-// (cp.async.bulk, completion on an mbarrier) GS_LANE_STAGES blocks ahead of the lanes that fold it:
-// the matrix stream -- 85% of this layout's bytes -- is in flight without holding registers, and
-// the lanes' dependent chain shrinks to shared-memory index -> gather -> fma. Same CTA geometry,
-// same per-row fma chain and the same epilogue partials as k_cheb_step (bit-identical results);
-// a block whose slice exceeds a stage (GS_LANE_CAP entries) is folded from global memory by
-// cheb_row instead. sparse.cpp:85-99 / heat.cpp:121-130.
-#ifndef GS_LANE_STAGES
-#define GS_LANE_STAGES 1  // stages per CTA: 1 x 4 CTAs per SM measured faster than 2 x 3 (config 3: 563 vs 610 us)
-#endif
+// CSR stream staged through shared memory. The (col, val) entries of a warp's 32 consecutive rows
+// are one contiguous run of both arrays, so lane 0 brings the warp's slice in with two bulk copies
+// (cp.async.bulk, completion on the warp's mbarrier): the matrix stream -- 85% of this layout's
+// bytes -- is in flight without holding registers, and the lanes' dependent chain shrinks to
+// shared-memory index -> gather -> fma. Warps run independently (no CTA barrier in the row loop);
+// the next slice's bounds, the next rows' CSR ranges and own-row operands are loaded one row block
+// ahead. Same CTA geometry, per-row fma chain and epilogue partials as k_cheb_step (bit-identical
+// results); a warp whose slice exceeds its stage (GS_LANE_CAP entries) folds it from global
+// memory. The arrays may be the odd-stride copy of gs_lane.cu. sparse.cpp:85-99 / heat.cpp:121-130.
 #ifndef GS_LANE_CAP
-#define GS_LANE_CAP 4608  // entries per stage: 18 per row of a 256-row block
+#define GS_LANE_CAP 736  // entries per warp stage: 23 per row
 #endif
 #ifndef GS_LANE_MIN_BLOCKS
 #define GS_LANE_MIN_BLOCKS 4
 #endif
 #ifndef GS_LANE_BATCH
-#define GS_LANE_BATCH 8  // gathers in flight per lane (at most 8: the stage's read slack)
+#define GS_LANE_BATCH 8  // gathers in flight per lane
 #endif
-constexpr int kLaneStride = GS_LANE_CAP + 8;  // stage stride (16-byte multiple)
+constexpr int kLaneStride = GS_LANE_CAP;  // stage stride (a 16-byte multiple in both arrays)
+static_assert(GS_LANE_CAP % 4 == 0, "16-byte stage stride");
 template <typename S>
 constexpr int lane_smem_bytes() {
-  return GS_LANE_STAGES * kLaneStride * (int)(sizeof(int) + sizeof(S));
+  return (kStepThreads / 32) * kLaneStride * (int)(sizeof(int) + sizeof(S));
 }
 
 // NB consecutive staged entries of one row folded into its chain (CSR order). TAIL: positions at
@@ -1016,12 +1015,11 @@ __device__ __forceinline__ void lane_fold(const int* sc, const S* sv, int p, int
 }
 
 template <typename S, int GW, int MODE>
-__global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN_BLOCKS) k_cheb_lane(const StepArgs A, const int pf_back, const int pf_fwd) {
+__global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN_BLOCKS) k_cheb_lane(const StepArgs A) {
   using L = Lay<GW, S>;
-  using P = Prec<S>;
   constexpr int VEC = L::VEC;
   static_assert(L::LPR == 1, "one row per lane");
-  constexpr int RPC = kRowsPerCta1, STG = GS_LANE_STAGES, BLOCK_ROWS = kStepThreads;
+  constexpr int RPC = kRowsPerCta1, BLOCK_ROWS = kStepThreads, NW = kStepThreads / 32;
   if (A.status && (A.status->error || A.status->done)) return;
   const int tl = blockIdx.x / A.Gl;
   const int tile = A.tile0 + tl;
@@ -1029,9 +1027,9 @@ __global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN
   if (A.cs.gactive && A.cs.gactive[g] == 0) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   extern __shared__ __align__(128) unsigned char lane_smem[];
-  int* s_cols = reinterpret_cast<int*>(lane_smem);
-  S* s_vals = reinterpret_cast<S*>(lane_smem + (size_t)STG * kLaneStride * sizeof(int));
-  __shared__ __align__(8) unsigned long long s_bar[STG];
+  int* sc = reinterpret_cast<int*>(lane_smem) + warp * kLaneStride;
+  S* sv = reinterpret_cast<S*>(lane_smem + (size_t)NW * kLaneStride * sizeof(int)) + warp * kLaneStride;
+  __shared__ __align__(8) unsigned long long s_bar[NW];
   double mn[VEC], mx[VEC], er[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) {
@@ -1039,50 +1037,25 @@ __global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN
     mx[e] = MODE == MODE_BARY_PSI ? -INFINITY : 0.0;
     er[e] = 0.0;
   }
-  const int rbase = A.row0 + tl * (BLOCK_ROWS * RPC);
+  const int wbase = A.row0 + tl * (BLOCK_ROWS * RPC) + warp * 32;  // the warp's rows of block 0
   const S* __restrict__ vals = static_cast<const S*>(A.vals);
-  // block j's slice: first entry rounded down and length rounded up to four entries (16-byte
-  // copies; the arrays carry kCsrPad). 0 = no rows; > GS_LANE_CAP = not staged.
-  auto slice = [&](int j, int& p0) {
-    const int r0 = rbase + j * BLOCK_ROWS;
-    p0 = 0;
-    if (j >= RPC || r0 >= A.n) return 0;
-    p0 = __ldg(A.offs + r0) & ~3;
-    return ((__ldg(A.offs + min(r0 + BLOCK_ROWS, A.n)) + 3) & ~3) - p0;
-  };
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int st = 0; st < STG; ++st) mbar_init(&s_bar[st], 1);
-    fence_proxy_async();
-  }
-  __syncthreads();
-  auto issue = [&](int j) {
-    if (threadIdx.x != 0) return;
-    int p0;
-    const int len = slice(j, p0);
-    if (len <= 0 || len > GS_LANE_CAP) return;
-    const int st = j % STG;
-    mbar_expect_tx(&s_bar[st], (unsigned)(len * (sizeof(int) + sizeof(S))));
-    bulk_g2s(s_cols + st * kLaneStride, A.cols + p0, (unsigned)(len * sizeof(int)), &s_bar[st]);
-    bulk_g2s(s_vals + st * kLaneStride, vals + p0, (unsigned)(len * sizeof(S)), &s_bar[st]);
-  };
-#pragma unroll
-  for (int j = 0; j < STG; ++j) issue(j);
   const size_t gbase = (size_t)g * A.ld * GW;
   const S* __restrict__ Tp = static_cast<const S*>(A.Tprev) + gbase;
-  // T_{k-1} rows around the tile into L2 while the first slice is in flight: the first touch of
-  // a gathered line otherwise costs a DRAM round trip inside a lane's dependent chain
-  if (threadIdx.x == 32 && pf_back + pf_fwd > 0) {
-    const long long lo = max(0, rbase - pf_back), hi = min((long long)A.n, (long long)rbase + BLOCK_ROWS * RPC + pf_fwd);
-    const unsigned long long a0 = (reinterpret_cast<unsigned long long>(Tp + lo * GW) + 15ull) & ~15ull;
-    const unsigned long long a1 = reinterpret_cast<unsigned long long>(Tp + hi * GW) & ~15ull;
-    if (a1 > a0)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
-  }
-  unsigned phase = 0;  // bit st: parity of stage st's next completion (oversize blocks skip theirs)
-  // a row's CSR range and own-row operands T_{k-1}[i], T_{k-2}[i], acc[i]: loaded one block ahead,
-  // so their DRAM latency overlaps the previous block's gathers instead of heading this block's
-  // dependent chain
+  // the warp's slice of block j: first entry rounded down and length rounded up to four entries
+  // (16-byte copies; the arrays carry kCsrPad). len 0 = no rows; > GS_LANE_CAP = not staged.
+  struct Slice {
+    int p0, len;
+  };
+  auto slice = [&](int j) {
+    Slice sl{0, 0};
+    const int r0 = wbase + j * BLOCK_ROWS;
+    if (j < RPC && r0 < A.n) {
+      sl.p0 = __ldg(A.offs + r0) & ~3;
+      sl.len = ((__ldg(A.offs + min(r0 + 32, A.n)) + 3) & ~3) - sl.p0;
+    }
+    return sl;
+  };
+  // a row's CSR range and own-row operands T_{k-1}[i], T_{k-2}[i], acc[i]
   struct RowPre {
     int p, pe;
     S tps[VEC], t2s[VEC], a0s[VEC];
@@ -1092,7 +1065,7 @@ __global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN
     r.p = r.pe = 0;
 #pragma unroll
     for (int e = 0; e < VEC; ++e) r.tps[e] = r.t2s[e] = r.a0s[e] = S(0);
-    const int row = rbase + j * BLOCK_ROWS + threadIdx.x;
+    const int row = wbase + j * BLOCK_ROWS + lane;
     if (j < RPC && row < A.n) {
       r.p = __ldg(A.offs + row);
       r.pe = __ldg(A.offs + row + 1);
@@ -1105,36 +1078,47 @@ __global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN
     }
     return r;
   };
+  auto issue = [&](const Slice& sl) {  // lane 0: the slice into the warp's stage
+    if (lane != 0 || sl.len <= 0 || sl.len > GS_LANE_CAP) return;
+    fence_proxy_async();  // the lanes' reads of the stage (ordered by __syncwarp) before the copy's writes
+    mbar_expect_tx(&s_bar[warp], (unsigned)(sl.len * (sizeof(int) + sizeof(S))));
+    bulk_g2s(sc, A.cols + sl.p0, (unsigned)(sl.len * sizeof(int)), &s_bar[warp]);
+    bulk_g2s(sv, vals + sl.p0, (unsigned)(sl.len * sizeof(S)), &s_bar[warp]);
+  };
+  if (lane == 0) {
+    mbar_init(&s_bar[warp], 1);
+    fence_proxy_async();
+  }
+  __syncwarp();
+  Slice cs = slice(0);
+  issue(cs);
   RowPre cur = preload(0);
+  unsigned phase = 0;  // parity of the stage's next completion (oversize slices skip theirs)
 #pragma unroll 1
-  for (int j = 0; j < RPC; ++j) {
-    int p0;
-    const int len = slice(j, p0);
-    if (len <= 0) break;  // past the last row (CTA-uniform)
-    const int row = rbase + j * BLOCK_ROWS + threadIdx.x;
+  for (int j = 0; j < RPC && cs.len > 0; ++j) {
+    const int row = wbase + j * BLOCK_ROWS + lane;
+    // next block: slice bounds, CSR ranges and own rows in flight during this block's gathers
+    const Slice ns = slice(j + 1);
     const RowPre nxt = preload(j + 1);
     const bool valid = row < A.n;
     double y[VEC];
 #pragma unroll
     for (int e = 0; e < VEC; ++e) y[e] = 0.0;
-    if (len > GS_LANE_CAP) {  // oversize slice (CTA-uniform): the same fold from global memory
-      if (valid) lane_fold<S, GW>(A.cols + p0, vals + p0, cur.p - p0, cur.pe - p0, Tp, y);
+    if (cs.len > GS_LANE_CAP) {  // oversize slice (warp-uniform): the same fold from global memory
+      if (valid) lane_fold<S, GW>(A.cols + cs.p0, vals + cs.p0, cur.p - cs.p0, cur.pe - cs.p0, Tp, y);
     } else {
-      const int st = j % STG;
-      mbar_wait(&s_bar[st], (phase >> st) & 1u);
-      phase ^= 1u << st;
-      if (valid)
-        lane_fold<S, GW>(s_cols + st * kLaneStride, s_vals + st * kLaneStride, cur.p - p0, cur.pe - p0, Tp, y);
+      mbar_wait(&s_bar[warp], phase);
+      phase ^= 1u;
+      if (valid) lane_fold<S, GW>(sc, sv, cur.p - cs.p0, cur.pe - cs.p0, Tp, y);
+      __syncwarp();  // every lane is done with the stage before it is refilled
     }
+    issue(ns);
     if (valid) {
       if (A.k == 0) st_enc<S, VEC>(static_cast<S*>(A.Tout) + gbase + (size_t)row * GW, y);  // plain SpMM
       else finish_row_ops<S, GW, MODE>(A, g, row, 0, y, mn, mx, er, cur.tps, cur.t2s, cur.a0s);
     }
     cur = nxt;
-    if (j + STG < RPC) {  // every lane is done with the stage before it is refilled
-      __syncthreads();
-      issue(j + STG);
-    }
+    cs = ns;
   }
   if constexpr (MODE != MODE_NONE) block_epilogue<S, GW, MODE>(A, g, tile, warp, lane, 0, mn, mx, er);
 }
