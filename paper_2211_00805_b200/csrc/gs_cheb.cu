@@ -557,6 +557,15 @@ inline bool lane_enabled() {
   const char* e = getenv("GS_LANE");
   return !(e && atoi(e) == 0);
 }
+// fp64 rows shared by several lanes through the record kernel (k_cheb_rec). Opt-in (GS_REC=1, read
+// per call so tests can compare it with k_cheb_step): bit-identical results, but measured slower
+// than the register-gather kernel on the shapes it was written for -- config 2's 64-byte rows
+// 370-468 vs 326 us, config 4's 128-byte rows 408-416 vs 405 us (profiles/r02_summary.md "Record
+// kernel"), although its inner loop wins on a synthetic graph of the same shape (tools/mb_gather.cu)
+inline bool rec_enabled() {
+  const char* e = getenv("GS_REC");
+  return e && atoi(e) != 0;
+}
 inline bool lane_pad_enabled() {
   const char* e = getenv("GS_LANE_PAD");
   return !(e && atoi(e) == 0);
@@ -636,8 +645,34 @@ void launch_lane(const StepArgs& A, int mode, cudaStream_t s) {
   }
 }
 
+template <typename S, int GW, int MODE, int RPC>
+void launch_rec_mode(const StepArgs& A, cudaStream_t s) {
+  constexpr int smem = rec_smem_bytes();
+  static std::vector<char> seen;  // the attribute is per device
+  if (gs_first_on_device(seen))
+    cudaFuncSetAttribute(k_cheb_rec<S, GW, MODE, RPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_cheb_rec<S, GW, MODE, RPC><<<dim3((unsigned)(A.tiles * A.Gl)), kStepThreads, smem, s>>>(A);
+}
+
+template <typename S, int GW, int RPC>
+void launch_rec(const StepArgs& A, int mode, cudaStream_t s) {
+  switch (mode) {
+    case MODE_NONE: launch_rec_mode<S, GW, MODE_NONE, RPC>(A, s); break;
+    case MODE_SK_PSI: launch_rec_mode<S, GW, MODE_SK_PSI, RPC>(A, s); break;
+    case MODE_SK_PHI: launch_rec_mode<S, GW, MODE_SK_PHI, RPC>(A, s); break;
+    default: launch_rec_mode<S, GW, MODE_BARY_PSI, RPC>(A, s); break;
+  }
+}
+
 template <typename S, int GW>
 void launch_step_gw(const StepArgs& A, int mode, int rpc, cudaStream_t s) {
+  if constexpr (sizeof(S) == 8 && Lay<GW, S>::LPR > 1 && Lay<GW, S>::LPR < 32) {
+    if (A.recs) {
+      if (rpc == 1) launch_rec<S, GW, 1>(A, mode, s);
+      else launch_rec<S, GW, kRowsPerCta>(A, mode, s);
+      return;
+    }
+  }
   if (rpc == 1) launch_step_rpc<S, GW, 1>(A, mode, s);
   else if constexpr (Lay<GW, S>::LPR == 1) {
     if (A.lane) launch_lane<S, GW>(A, mode, s);
@@ -975,6 +1010,7 @@ struct Work {
   const gs_sell* sell = nullptr;  // several rows per warp through the sliced kernel (k_cheb_sell)
   int spw = 1;                    // its slices per warp
   bool sellw = false;             // ... through the warp-staged persistent kernel (k_cheb_sellw)
+  const void* recs = nullptr;     // fp64 rows shared by several lanes through the record kernel (k_cheb_rec)
   bool lane = false;              // one row per lane through the staged kernel (k_cheb_lane)
   const gs_lanepad* lp = nullptr;  // its odd-stride CSR copy (filter layouts; GS_LANE_PAD=0: none)
   DevBuf<int> wstart;             // its static split of the slices over the grid's warps
@@ -1047,6 +1083,12 @@ struct Work {
         tiles = (sell->nslices + warps * spw - 1) / (warps * spw);
       }
       rpc = 1;
+    }
+    if (sizeof(S) == 8 && f && ld_ < 0 && n > 0 && !w1 && !blk && !win && !sell && rpc_lpr<S>(GW) > 1 &&
+        rpc_lpr<S>(GW) < 32 && rec_enabled()) {
+      gs_layout& Ly = const_cast<gs_filter*>(f)->lay[lay];
+      if (!Ly.recs) GS_TRY(gs_recs_build(ctx, Ly.perm->cols, Ly.perm->vals, Ly.perm->nnz, &Ly.recs));
+      recs = Ly.recs;
     }
     lane = !w1 && !blk && !win && !sell && rpc > 1 && rpc_lpr<S>(GW) == 1 && lane_enabled();
     if (lane && f && ld_ < 0 && n > 0 && lane_pad_enabled()) {
@@ -1156,6 +1198,7 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
   A.vals = layout_vals<S>(Ly);
   A.warp_rows = w.w1;
   A.lane = w.lane;
+  A.recs = w.recs;
   if (w.lp) {
     A.offs = w.lp->offs;
     A.cols = w.lp->cols;
@@ -2602,6 +2645,8 @@ static int finish_layout(gs_ctx* ctx, gs_filter* f, int l) {
   Ly.sell.clear();
   for (auto* e : Ly.lanepad) gs_lanepad_destroy(e);
   Ly.lanepad.clear();
+  cudaFree(Ly.recs);
+  Ly.recs = nullptr;
   do {
     rc = gs_permute_graph(ctx, f->scaled, Ly.order, Ly.newpos, &Ly.perm);
     if (rc) break;
@@ -2698,6 +2743,7 @@ extern "C" void gs_filter_destroy(gs_filter* f) {
     for (auto* w : Ly.win) gs_win_destroy(w);
     for (auto* e : Ly.sell) gs_sell_destroy(e);
     for (auto* e : Ly.lanepad) gs_lanepad_destroy(e);
+    cudaFree(Ly.recs);
   }
   cudaFree(f->d_coeffs);
   delete f;

@@ -123,6 +123,8 @@ struct gs_layout {
   std::vector<gs_sell*> sell;
   // odd-stride copies of `perm` for k_cheb_lane, one per value size; built on first use
   std::vector<gs_lanepad*> lanepad;
+  // `perm`'s entries as 16-byte records {col, -, val} for k_cheb_rec (fp64); built on first use
+  void* recs = nullptr;
 };
 
 struct gs_filter {
@@ -258,6 +260,8 @@ int gs_sell_split(gs_ctx* ctx, const gs_sell* p, int W, int* d_wstart);
 int gs_lanepad_build(gs_ctx* ctx, const int* offs, const int* cols, const void* vals, int elem_bytes, int n,
                      int64_t nnz, gs_lanepad** out);
 void gs_lanepad_destroy(gs_lanepad* p);
+// 16-byte record copy {col, -, val} of a CSR operator's entries (nnz + kCsrPad records)
+int gs_recs_build(gs_ctx* ctx, const int* cols, const double* vals, int64_t nnz, void** out);
 // layout l of f from a host order (order[new] = old): newpos, renumbered operator, fp32 copy
 int gs_layout_from_order(gs_ctx* ctx, gs_filter* f, int l, const int* h_order);
 // kNN (gs_graph.cu / gs_knn_tc.cu): brute force over a query list; tensor-core prefilter + exact

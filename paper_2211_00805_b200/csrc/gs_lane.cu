@@ -40,7 +40,42 @@ __global__ void k_lp_fill(const int* __restrict__ offs, const int* __restrict__ 
   }
 }
 
+struct Rec16 {
+  int col, pad;
+  double val;
+};
+__global__ void k_recs_fill(const int* __restrict__ cols, const double* __restrict__ vals, long long nnz,
+                            long long total, Rec16* out) {
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= total) return;
+  Rec16 r{0, 0, 0.0};
+  if (p < nnz) {
+    r.col = cols[p];
+    r.val = vals[p];
+  }
+  out[p] = r;
+}
+
 }  // namespace
+
+// k_cheb_rec's copy of the entries (gs_step.cuh): one 16-byte record per entry, CSR order
+int gs_recs_build(gs_ctx* ctx, const int* cols, const double* vals, int64_t nnz, void** out) {
+  *out = nullptr;
+  const long long total = nnz + kCsrPad;
+  Rec16* r = nullptr;
+  if (cudaMalloc((void**)&r, (size_t)total * sizeof(Rec16)) != cudaSuccess)
+    return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "record copy allocation failed");
+  gs_launch_begin(ctx, 1);
+  k_recs_fill<<<(unsigned)((total + 255) / 256), 256, 0, ctx->stream>>>(cols, vals, nnz, total, r);
+  gs_launch_end(ctx, 1);
+  const cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) {
+    cudaFree(r);
+    return gs_cuda_fail(ctx, e, "record copy");
+  }
+  *out = r;
+  return GS_OK;
+}
 
 void gs_lanepad_destroy(gs_lanepad* p) {
   if (!p) return;

@@ -353,6 +353,7 @@ struct StepArgs {  // vector pointers are S* of the launch's precision
   double bk1, bk2;    // b_{k-1}, b_{k-2}
   const gs_status* status;
   ColState cs;
+  const void* recs;    // k_cheb_rec: the CSR entries as 16-byte records (gs_layout::recs); nullptr = off
   const int* rec_key;  // k_cheb_blk: 8-row block records (gs_layout::rec_key / rec_val)
   const void* rec_val;
   // fused epilogue operands: always fp64 (in the fp32 mode only the Chebyshev recurrence runs
@@ -1042,16 +1043,19 @@ __global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN
   const size_t gbase = (size_t)g * A.ld * GW;
   const S* __restrict__ Tp = static_cast<const S*>(A.Tprev) + gbase;
   // the warp's slice of block j: first entry rounded down and length rounded up to four entries
-  // (16-byte copies; the arrays carry kCsrPad). len 0 = no rows; > GS_LANE_CAP = not staged.
+  // (16-byte copies; the arrays carry kCsrPad). len 0 = no rows; > GS_LANE_CAP = not staged
+  // (kept as the two loaded offsets, so the loads stay in flight until the bounds are needed)
   struct Slice {
-    int p0, len;
+    int a, b;
+    __device__ __forceinline__ int p0() const { return a & ~3; }
+    __device__ __forceinline__ int len() const { return ((b + 3) & ~3) - (a & ~3); }
   };
   auto slice = [&](int j) {
     Slice sl{0, 0};
     const int r0 = wbase + j * BLOCK_ROWS;
     if (j < RPC && r0 < A.n) {
-      sl.p0 = __ldg(A.offs + r0) & ~3;
-      sl.len = ((__ldg(A.offs + min(r0 + 32, A.n)) + 3) & ~3) - sl.p0;
+      sl.a = __ldg(A.offs + r0);
+      sl.b = __ldg(A.offs + min(r0 + 32, A.n));
     }
     return sl;
   };
@@ -1079,11 +1083,13 @@ __global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN
     return r;
   };
   auto issue = [&](const Slice& sl) {  // lane 0: the slice into the warp's stage
-    if (lane != 0 || sl.len <= 0 || sl.len > GS_LANE_CAP) return;
+    if (lane != 0) return;
+    const int p0 = sl.p0(), len = sl.len();
+    if (len <= 0 || len > GS_LANE_CAP) return;
     fence_proxy_async();  // the lanes' reads of the stage (ordered by __syncwarp) before the copy's writes
-    mbar_expect_tx(&s_bar[warp], (unsigned)(sl.len * (sizeof(int) + sizeof(S))));
-    bulk_g2s(sc, A.cols + sl.p0, (unsigned)(sl.len * sizeof(int)), &s_bar[warp]);
-    bulk_g2s(sv, vals + sl.p0, (unsigned)(sl.len * sizeof(S)), &s_bar[warp]);
+    mbar_expect_tx(&s_bar[warp], (unsigned)(len * (sizeof(int) + sizeof(S))));
+    bulk_g2s(sc, A.cols + p0, (unsigned)(len * sizeof(int)), &s_bar[warp]);
+    bulk_g2s(sv, vals + p0, (unsigned)(len * sizeof(S)), &s_bar[warp]);
   };
   if (lane == 0) {
     mbar_init(&s_bar[warp], 1);
@@ -1095,7 +1101,9 @@ __global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN
   RowPre cur = preload(0);
   unsigned phase = 0;  // parity of the stage's next completion (oversize slices skip theirs)
 #pragma unroll 1
-  for (int j = 0; j < RPC && cs.len > 0; ++j) {
+  for (int j = 0; j < RPC; ++j) {
+    const int p0 = cs.p0(), len = cs.len();
+    if (len <= 0) break;  // past the last row (warp-uniform)
     const int row = wbase + j * BLOCK_ROWS + lane;
     // next block: slice bounds, CSR ranges and own rows in flight during this block's gathers
     const Slice ns = slice(j + 1);
@@ -1104,12 +1112,12 @@ __global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN
     double y[VEC];
 #pragma unroll
     for (int e = 0; e < VEC; ++e) y[e] = 0.0;
-    if (cs.len > GS_LANE_CAP) {  // oversize slice (warp-uniform): the same fold from global memory
-      if (valid) lane_fold<S, GW>(A.cols + cs.p0, vals + cs.p0, cur.p - cs.p0, cur.pe - cs.p0, Tp, y);
+    if (len > GS_LANE_CAP) {  // oversize slice (warp-uniform): the same fold from global memory
+      if (valid) lane_fold<S, GW>(A.cols + p0, vals + p0, cur.p - p0, cur.pe - p0, Tp, y);
     } else {
       mbar_wait(&s_bar[warp], phase);
       phase ^= 1u;
-      if (valid) lane_fold<S, GW>(sc, sv, cur.p - cs.p0, cur.pe - cs.p0, Tp, y);
+      if (valid) lane_fold<S, GW>(sc, sv, cur.p - p0, cur.pe - p0, Tp, y);
       __syncwarp();  // every lane is done with the stage before it is refilled
     }
     issue(ns);
@@ -1121,6 +1129,174 @@ __global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN
     cs = ns;
   }
   if constexpr (MODE != MODE_NONE) block_epilogue<S, GW, MODE>(A, g, tile, warp, lane, 0, mn, mx, er);
+}
+
+// Several lanes per row, fp64 (B = 3..32 columns: the barycenter layouts of configs 2 and 4) with the
+// CSR stream staged through shared memory as 16-byte records {col, -, val} (gs_lane.cu builds the
+// record copy). A warp's RPW consecutive rows own one contiguous run of records; lane 0 brings it
+// in with one bulk copy (completion on the warp's mbarrier) and every lane reads its row's next
+// record with one 16-byte shared-memory load -- a broadcast inside the row's lanes, one wavefront
+// per warp -- instead of a coalesced (col, val) chunk load plus three shuffles per entry
+// (tools/mb_gather.cu: 240 -> 202 us on a synthetic graph with config 2's shape; on the real kNN
+// graphs it measured slower than k_cheb_step, so it is opt-in: GS_REC=1). Warps run independently; the
+// next slice's bounds and the next rows' own operands are loaded one row block ahead. Same CTA
+// geometry, per-row fma chain and epilogue partials as k_cheb_step (bit-identical results); a warp
+// whose slice exceeds its stage (GS_REC_CAP records: hub rows) folds it from global memory.
+// sparse.cpp:85-99 / heat.cpp:121-130.
+#ifndef GS_REC_CAP
+#define GS_REC_CAP 192  // records per warp stage (3 KB)
+#endif
+#ifndef GS_REC_BATCH
+#define GS_REC_BATCH 4  // gathers in flight per lane
+#endif
+#ifndef GS_REC_MIN_BLOCKS
+#define GS_REC_MIN_BLOCKS 5
+#endif
+struct __align__(16) CsrRec {
+  int col, pad;
+  double val;
+};
+constexpr int rec_smem_bytes() { return (kStepThreads / 32) * GS_REC_CAP * (int)sizeof(CsrRec); }
+
+// NB consecutive records of one row folded into its chain (CSR order). TAIL: positions at or past
+// `pe` read the row's last record instead and skip their fma.
+template <typename S, int GW, int NB, bool TAIL>
+__device__ __forceinline__ void rec_batch(const CsrRec* sr, int p, int pe, const S* __restrict__ Tp,
+                                          double (&y)[Lay<GW, S>::VEC]) {
+  constexpr int VEC = Lay<GW, S>::VEC;
+  using P = Prec<S>;
+  double vv[NB];
+  S xx[NB][VEC];
+#pragma unroll
+  for (int u = 0; u < NB; ++u) {
+    const int4 r = *reinterpret_cast<const int4*>(sr + (TAIL ? min(p + u, pe - 1) : p + u));
+    vv[u] = __hiloint2double(r.w, r.z);
+    ld_vec<S, VEC>(Tp + (size_t)r.x * GW, xx[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < NB; ++u)
+    if (!TAIL || p + u < pe) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) y[e] = P::fmat(vv[u], P::dec(xx[u][e]), y[e]);
+    }
+}
+template <typename S, int GW>
+__device__ __forceinline__ void rec_fold(const CsrRec* sr, int p, int pe, const S* __restrict__ Tp,
+                                         double (&y)[Lay<GW, S>::VEC]) {
+  constexpr int NB = GS_REC_BATCH;
+  for (; p + NB <= pe; p += NB) rec_batch<S, GW, NB, false>(sr, p, pe, Tp, y);
+  if (p < pe) rec_batch<S, GW, NB, true>(sr, p, pe, Tp, y);
+}
+
+template <typename S, int GW, int MODE, int RPC>
+__global__ void __launch_bounds__(kStepThreads, Lay<GW, S>::VEC >= 2 ? 4 : GS_REC_MIN_BLOCKS) k_cheb_rec(const StepArgs A) {
+  using L = Lay<GW, S>;
+  constexpr int VEC = L::VEC, LPR = L::LPR, RPW = L::RPW;
+  static_assert(sizeof(S) == 8 && LPR > 1, "fp64 rows shared by several lanes");
+  constexpr int BLOCK_ROWS = (kStepThreads / 32) * RPW;
+  if (A.status && (A.status->error || A.status->done)) return;
+  const int tl = blockIdx.x / A.Gl;
+  const int tile = A.tile0 + tl;
+  const int g = A.g0 + blockIdx.x % A.Gl;
+  if (A.cs.gactive && A.cs.gactive[g] == 0) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane / LPR, q = lane % LPR;
+  extern __shared__ __align__(128) unsigned char rec_smem[];
+  CsrRec* sr = reinterpret_cast<CsrRec*>(rec_smem) + warp * GS_REC_CAP;
+  __shared__ __align__(8) unsigned long long s_bar[kStepThreads / 32];
+  double mn[VEC], mx[VEC], er[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    mn[e] = INFINITY;
+    mx[e] = MODE == MODE_BARY_PSI ? -INFINITY : 0.0;
+    er[e] = 0.0;
+  }
+  const int wbase = A.row0 + tl * (BLOCK_ROWS * RPC) + warp * RPW;  // the warp's rows of block 0
+  const CsrRec* __restrict__ recs = static_cast<const CsrRec*>(A.recs);
+  const size_t gbase = (size_t)g * A.ld * GW + q * VEC;
+  const S* __restrict__ Tp = static_cast<const S*>(A.Tprev) + gbase;
+  struct Slice {  // the warp's records of block j: [a, b)
+    int a, b;
+  };
+  auto slice = [&](int j) {
+    Slice sl{0, 0};
+    const int r0 = wbase + j * BLOCK_ROWS;
+    if (j < RPC && r0 < A.n) {
+      sl.a = __ldg(A.offs + r0);
+      sl.b = __ldg(A.offs + min(r0 + RPW, A.n));
+    }
+    return sl;
+  };
+  struct RowPre {  // a row's record range and own-row operands T_{k-1}[i], T_{k-2}[i], acc[i]
+    int p, pe;
+    S tps[VEC], t2s[VEC], a0s[VEC];
+  };
+  auto preload = [&](int j) {
+    RowPre r;
+    r.p = r.pe = 0;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) r.tps[e] = r.t2s[e] = r.a0s[e] = S(0);
+    const int row = wbase + j * BLOCK_ROWS + sub;
+    if (j < RPC && row < A.n) {
+      r.p = __ldg(A.offs + row);
+      r.pe = __ldg(A.offs + row + 1);
+      if (A.k != 0) {
+        const size_t idx = gbase + (size_t)row * GW;
+        ld_vec<S, VEC>(static_cast<const S*>(A.Tprev) + idx, r.tps);
+        if (A.k >= 2) ld_vec_rw<S, VEC>(static_cast<const S*>(A.Tout) + idx, r.t2s);
+        if (A.acc_terms > 0 && !A.acc_init) ld_vec_rw<S, VEC>(static_cast<const S*>(A.acc) + idx, r.a0s);
+      }
+    }
+    return r;
+  };
+  auto issue = [&](const Slice& sl) {  // lane 0: the slice into the warp's stage
+    const int len = sl.b - sl.a;
+    if (lane != 0 || len <= 0 || len > GS_REC_CAP) return;
+    fence_proxy_async();  // the lanes' reads of the stage (ordered by __syncwarp) before the copy's writes
+    mbar_expect_tx(&s_bar[warp], (unsigned)(len * sizeof(CsrRec)));
+    bulk_g2s(sr, recs + sl.a, (unsigned)(len * sizeof(CsrRec)), &s_bar[warp]);
+  };
+  if (lane == 0) {
+    mbar_init(&s_bar[warp], 1);
+    fence_proxy_async();
+  }
+  __syncwarp();
+  Slice cs = slice(0);
+  issue(cs);
+  RowPre cur = preload(0);
+  unsigned phase = 0;  // parity of the stage's next completion (oversize slices skip theirs)
+#pragma unroll 1
+  for (int j = 0; j < RPC; ++j) {
+    const int len = cs.b - cs.a;
+    if (len <= 0) break;  // past the last row (warp-uniform)
+    const int row = wbase + j * BLOCK_ROWS + sub;
+    Slice ns{0, 0};
+    RowPre nxt = cur;
+    if constexpr (RPC > 1) {  // next block in flight during this block's gathers
+      ns = slice(j + 1);
+      nxt = preload(j + 1);
+    }
+    const bool valid = row < A.n;
+    double y[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) y[e] = 0.0;
+    if (len > GS_REC_CAP) {  // oversize slice (warp-uniform): the same fold from global memory
+      if (valid) rec_fold<S, GW>(recs + cs.a, cur.p - cs.a, cur.pe - cs.a, Tp, y);
+    } else {
+      mbar_wait(&s_bar[warp], phase);
+      phase ^= 1u;
+      if (valid) rec_fold<S, GW>(sr, cur.p - cs.a, cur.pe - cs.a, Tp, y);
+      __syncwarp();  // every lane is done with the stage before it is refilled
+    }
+    if constexpr (RPC > 1) issue(ns);
+    if (valid) {
+      if (A.k == 0) st_enc<S, VEC>(static_cast<S*>(A.Tout) + gbase + (size_t)row * GW, y);  // plain SpMM
+      else finish_row_ops<S, GW, MODE>(A, g, row, q, y, mn, mx, er, cur.tps, cur.t2s, cur.a0s);
+    }
+    cur = nxt;
+    cs = ns;
+  }
+  if constexpr (MODE != MODE_NONE) block_epilogue<S, GW, MODE>(A, g, tile, warp, sub, q, mn, mx, er);
 }
 
 // 8-row blocks (wide fp64 rows, one warp per block): the gathers of a block's rows are shared.
