@@ -1,7 +1,9 @@
 """Build recipe for libgeosink_b200.so (nvcc, sm_100a) -- used by __graft_entry__.build().
 
 Flags: -gencode arch=compute_100a,code=sm_100a; -lineinfo for ncu source attribution;
--fmad=false so the only fused operations are the explicit fma() calls mirrored by the oracle.
+-fmad=false so the only fused operations are the explicit fma() calls mirrored by the oracle; the
+32-bit mode computes in fp64 with the same chains (only its stored words are narrower) and its
+kernels are tested bit-identical to one another, so the flag covers every translation unit.
 """
 from __future__ import annotations
 

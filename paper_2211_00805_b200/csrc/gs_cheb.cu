@@ -630,8 +630,9 @@ template <typename S, int GW, int MODE>
 void launch_lane_mode(const StepArgs& A, cudaStream_t s) {
   constexpr int smem = lane_smem_bytes<S>();
   static std::vector<char> seen;  // the attribute is per device
-  if (gs_first_on_device(seen))
+  gs_once_per_device(seen, [] {
     cudaFuncSetAttribute(k_cheb_lane<S, GW, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
   k_cheb_lane<S, GW, MODE><<<dim3((unsigned)(A.tiles * A.Gl)), kStepThreads, smem, s>>>(A);
 }
 
@@ -649,8 +650,9 @@ template <typename S, int GW, int MODE, int RPC>
 void launch_rec_mode(const StepArgs& A, cudaStream_t s) {
   constexpr int smem = rec_smem_bytes();
   static std::vector<char> seen;  // the attribute is per device
-  if (gs_first_on_device(seen))
+  gs_once_per_device(seen, [] {
     cudaFuncSetAttribute(k_cheb_rec<S, GW, MODE, RPC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
   k_cheb_rec<S, GW, MODE, RPC><<<dim3((unsigned)(A.tiles * A.Gl)), kStepThreads, smem, s>>>(A);
 }
 
@@ -844,8 +846,9 @@ template <typename S, int GW, int MODE>
 void launch_win_mode(const CUtensorMap& tm, const StepArgs& A, const WinArgs& WA, int G, cudaStream_t s) {
   constexpr int smem = win_smem_bytes<S, GW>();
   static std::vector<char> seen;  // the attribute is per device
-  if (gs_first_on_device(seen))
+  gs_once_per_device(seen, [] {
     cudaFuncSetAttribute(k_cheb_win<S, GW, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  });
   k_cheb_win<S, GW, MODE><<<dim3((unsigned)(WA.nctas * G)), kWinThreads, smem, s>>>(tm, A, WA);
 }
 
@@ -1030,6 +1033,8 @@ struct Work {
   static constexpr bool kF32 = sizeof(S) == 4;
   int init(gs_ctx* ctx, int n_, int B_, bool want_err, int64_t ld_ = -1, const gs_filter* f = nullptr) {
     cudaStream_t s = ctx->stream;
+    std::unique_lock<std::mutex> build_lock;
+    if (f) build_lock = std::unique_lock<std::mutex>(const_cast<gs_filter*>(f)->build_mu);
     n = n_;
     B = B_;
     ld = ld_ < 0 ? n_ : ld_;
@@ -1557,10 +1562,10 @@ int sinkhorn_impl(gs_ctx* ctx, const gs_filter* f, const double* da_user, const 
       const size_t smem = (size_t)persist_rep_offset(n) + (size_t)2 * n * 8 + (size_t)maxne * 12;
       if (smem <= 220 * 1024) {  // + 768 bytes of static shared memory
         static std::vector<char> seen;  // the attributes are per device
-        if (gs_first_on_device(seen)) {
+        gs_once_per_device(seen, [] {
           cudaFuncSetAttribute(k_sk_persist, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
           cudaFuncSetAttribute(k_sk_persist, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        }
+        });
         PersistArgs PA{};
         PA.n = n;
         PA.R = R;
@@ -2187,6 +2192,27 @@ int halo_finish(gs_ctx* ctx, const gs_part* p, const Work<S>& w, S* T, Halo<S>& 
   return GS_OK;
 }
 
+// k_cheb_lane on a part's rows stages the odd-stride copy of its local CSR (gs_lane.cu): built
+// once per part and precision, before any sweep is captured into a CUDA graph
+template <typename S>
+bool part_lane_wanted(const Work<S>& w) {
+  return lane_enabled() && lane_pad_enabled() && w.rpc > 1 && rpc_lpr<S>(w.GW) == 1 && w.n > 0;
+}
+template <typename S>
+const gs_lanepad* part_lane_copy(const gs_part* p, const Work<S>& w) {
+  return part_lane_wanted<S>(w) ? p->lanepad[sizeof(S) == 4 ? 0 : 1] : nullptr;
+}
+template <typename S>
+int part_lane_prepare(gs_ctx* ctx, const gs_part* p, const Work<S>& w) {
+  if (!part_lane_wanted<S>(w)) return GS_OK;
+  gs_lanepad*& lp = const_cast<gs_part*>(p)->lanepad[sizeof(S) == 4 ? 0 : 1];
+  if (lp) return GS_OK;
+  const void* vals = sizeof(S) == 4 ? static_cast<const void*>(p->vals32) : static_cast<const void*>(p->local->vals);
+  const int rc = gs_lanepad_build(ctx, p->local->offs, p->local->cols, vals, (int)sizeof(S), p->local->n,
+                                  p->local->nnz, &lp);
+  return rc == GS_ERR_UNSUPPORTED ? GS_OK : rc;
+}
+
 // run_apply over this part's rows, one halo exchange of T_{k-1} before every step
 template <typename S>
 int run_apply_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& w, Halo<S>& h, int a0,
@@ -2200,6 +2226,11 @@ int run_apply_part(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, Work<S>& 
   if constexpr (sizeof(S) == 4) A.vals = p->vals32;
   else A.vals = p->local->vals;
   A.lane = lane_enabled();
+  if (const gs_lanepad* lp = part_lane_copy<S>(p, w)) {  // built by part_lane_prepare
+    A.offs = lp->offs;
+    A.cols = lp->cols;
+    A.vals = lp->vals;
+  }
   A.n = w.n;
   A.ld = w.ld;
   A.tiles = w.tiles;
@@ -2286,6 +2317,7 @@ int filter_apply_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, c
   cudaStream_t s = ctx->stream;
   Work<S> w;
   GS_TRY(w.init(ctx, nl, width, false, (int64_t)nl + p->nh, p->f));
+  GS_TRY(part_lane_prepare<S>(ctx, p, w));
   w.tiles = part_tiles<S>(p, w);
   Halo<S> h;
   GS_TRY(h.init(ctx, p, w.Bpad));
@@ -2315,6 +2347,7 @@ int sinkhorn_part_impl(gs_ctx* ctx, const gs_part* p, const gs_comm* comm, const
   cudaStream_t s = ctx->stream;
   Work<S> w;
   GS_TRY(w.init(ctx, nl, P, true, (int64_t)nl + p->nh, p->f));
+  GS_TRY(part_lane_prepare<S>(ctx, p, w));
   w.tiles = part_tiles<S>(p, w);  // error partials: one per tile of the (up to) three row ranges
   GS_CUDA(ctx, w.part_err.alloc((size_t)(w.tiles ? w.tiles : 1) * w.Bpad, s));
   Halo<S> h;

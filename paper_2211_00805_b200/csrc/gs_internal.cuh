@@ -10,6 +10,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "geosink_b200.h"
@@ -136,6 +137,9 @@ struct gs_filter {
   double t = 0, t_eff = 0, scale = 1;
   int degree = 0, kind = 0;
   std::vector<double> coeffs;  // host mirror (heat.hpp:37)
+  // serialises the structures built on first use (window schedules, sliced stores, odd-stride and
+  // record copies, block records) when several host threads run on one filter
+  std::mutex build_mu;
   double* d_coeffs = nullptr;
 };
 
@@ -151,6 +155,7 @@ struct gs_part {
   int int_lo = 0, int_hi = 0;  // local rows [int_lo, int_hi) read no halo row (interior)
   gs_graph* local = nullptr;
   float* vals32 = nullptr;
+  gs_lanepad* lanepad[2] = {nullptr, nullptr};  // odd-stride copies of `local` (vals32 / fp64), on first use
   int* vertices = nullptr;   // nl: original vertex id of each local row
   int* send_rows = nullptr;  // ns local row indices
   std::vector<int> bounds;   // nparts + 1 positions
@@ -174,14 +179,22 @@ int gs_cuda_fail(gs_ctx* ctx, cudaError_t e, const char* where);
   } while (0)
 
 // ---- once-per-device setup (function attributes are set per device) ---------------------------
-// true the first time `key`'s setup runs on the current device; `key` is any per-site object
-inline bool gs_first_on_device(std::vector<char>& seen) {
+// runs `setup` the first time this site is reached on the current device; `seen` is the site's
+// static record. Serialised: contexts on several host threads launch the same kernels, and a
+// launch must not overtake another thread's cudaFuncSetAttribute.
+inline std::mutex& gs_once_mutex() {
+  static std::mutex mu;
+  return mu;
+}
+template <typename F>
+inline void gs_once_per_device(std::vector<char>& seen, F&& setup) {
+  std::lock_guard<std::mutex> lock(gs_once_mutex());
   int dev = 0;
   cudaGetDevice(&dev);
   if ((int)seen.size() <= dev) seen.resize(dev + 1, 0);
-  if (seen[dev]) return false;
+  if (seen[dev]) return;
+  setup();
   seen[dev] = 1;
-  return true;
 }
 
 // ---- launch accounting / timing ------------------------------------------------------------

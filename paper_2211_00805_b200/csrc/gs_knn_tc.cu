@@ -415,7 +415,7 @@ int gs_knn_tc(gs_ctx* ctx, const double* dpts, const double* sq, int n, int d, i
                                                            Blo.get(), maxk.get());
   gs_launch_end(ctx, 1);
   static std::vector<char> seen;  // the attribute is per device
-  if (gs_first_on_device(seen)) cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem);
+  gs_once_per_device(seen, [] { cudaFuncSetAttribute(k_knn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTcSmem); });
   TcArgs P{};
   P.Ahi = Ahi.get();
   P.Alo = Alo.get();

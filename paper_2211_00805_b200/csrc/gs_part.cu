@@ -285,6 +285,8 @@ extern "C" void gs_part_destroy(gs_part* p) {
   if (!p) return;
   gs_graph_destroy(p->local);
   cudaFree(p->vals32);
+  gs_lanepad_destroy(p->lanepad[0]);
+  gs_lanepad_destroy(p->lanepad[1]);
   cudaFree(p->vertices);
   cudaFree(p->send_rows);
   delete p;
