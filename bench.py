@@ -1229,6 +1229,16 @@ def run_engine_rows(args):
         except Exception as e:  # host memory / time limits: report why
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                    "sample": f"not run: {type(e).__name__}"}
+    # DRAM bytes of the dominant kernel per launch from the committed ncu capture (one rank)
+    traffic3, ncu3 = None, None
+    prof3 = os.path.join(ROOT, "profiles", "lane_step_traffic.json")
+    if world == 1 and os.path.exists(prof3):
+        try:
+            with open(prof3) as fh:
+                ncu3 = json.load(fh)
+            traffic3 = ncu3.get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic3, ncu3 = None, None
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -1248,8 +1258,12 @@ def run_engine_rows(args):
                                        if world > 1 else "one rank: unpartitioned rows, CUDA-graph sweeps")},
             "roofline": {"bound": "hbm", "achieved": bytes_step / (avg / 1000.0) / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": bytes_step / (avg / 1000.0) / 1e9 / peak,
-                         "traffic": None, "peak_kind": peak_kind, "bytes_per_launch": bytes_step,
-                         "avg_launch_ms": avg, "launches_timed": step_n},
+                         "traffic": traffic3, "peak_kind": peak_kind, "bytes_per_launch": bytes_step,
+                         "avg_launch_ms": avg, "launches_timed": step_n,
+                         "kernel": ("k_cheb_lane<float, 1, *> (one row per lane, per-warp CSR slices staged in "
+                                    "shared memory by bulk copies)" if world == 1 else
+                                    "k_cheb_lane<float, 1, *> on the part's interior / boundary row ranges"),
+                         **({"ncu": ncu3} if ncu3 else {})},
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": cpu,
             "iterations": int(it[0]), "marginal_error": float(err[0]),
         }), flush=True)

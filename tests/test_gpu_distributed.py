@@ -80,11 +80,16 @@ def test_engine_nccl_comm_world1_graph_captured(ctx):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("rpc", [None, "4"])
 @pytest.mark.parametrize("ranks", [2, 4])
-def test_member_sharded_barycenter_threads(ctx, ranks):
+def test_member_sharded_barycenter_threads(ctx, monkeypatch, ranks, rpc):
     """Member-sharded barycenter with 2 / 4 ranks (host threads on one GPU, each with its own
     engine context; tests/part_comm.py hooks) against the unsharded engine run: the log-sum is
-    re-associated across ranks (barycenter.cpp:75-78), so results agree to <= 1e-12."""
+    re-associated across ranks (barycenter.cpp:75-78), so results agree to <= 1e-12.
+    GS_RPC=4 puts the 2-member shards on the large-shared-memory kernel k_cheb_lane, whose
+    once-per-device function attribute several host threads then race to set."""
+    if rpc:
+        monkeypatch.setenv("GS_RPC", rpc)
     import paper_2211_00805_b200 as gs
     from paper_2211_00805_b200.distributed import sharded_sinkhorn_barycenter
     from paper_2211_00805_b200.rng import Rng
