@@ -973,7 +973,7 @@ constexpr int lane_smem_bytes() {
 }
 
 // NB consecutive staged entries of one row folded into its chain (CSR order). TAIL: positions at
-// or past `pe` read the row's last entry instead and skip their fma.
+// or past `pe` read the row's last index (a valid position) and skip their gather and fma.
 template <typename S, int GW, int NB, bool TAIL>
 __device__ __forceinline__ void lane_batch(const int* sc, const S* sv, int p, int pe, const S* __restrict__ Tp,
                                            double (&y)[Lay<GW, S>::VEC]) {
@@ -988,7 +988,15 @@ __device__ __forceinline__ void lane_batch(const int* sc, const S* sv, int p, in
 #pragma unroll
   for (int u = 0; u < NB; ++u) cc[u] = sc[at[u]];
 #pragma unroll
-  for (int u = 0; u < NB; ++u) ld_vec<S, VEC>(Tp + (size_t)cc[u] * GW, xx[u]);
+  for (int u = 0; u < NB; ++u) {
+    if constexpr (TAIL) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) xx[u][e] = S(0);
+      if (p + u < pe) ld_vec<S, VEC>(Tp + (size_t)cc[u] * GW, xx[u]);
+    } else {
+      ld_vec<S, VEC>(Tp + (size_t)cc[u] * GW, xx[u]);
+    }
+  }
 #pragma unroll
   for (int u = 0; u < NB; ++u) vv[u] = sv[at[u]];
 #pragma unroll
@@ -1009,8 +1017,7 @@ __device__ __forceinline__ void lane_fold(const int* sc, const S* sv, int p, int
   constexpr int NB = GS_LANE_BATCH;
   if (pe > p && sc[pe - 1] < 0) --pe;
   for (; p + NB <= pe; p += NB) lane_batch<S, GW, NB, false>(sc, sv, p, pe, Tp, y);
-  // the row's tail: positions past its end re-read its last entry (a valid address) and are
-  // left out of the chain
+  // the row's tail, predicated
   if (p + NB / 2 < pe) lane_batch<S, GW, NB, true>(sc, sv, p, pe, Tp, y);
   else if (p < pe) lane_batch<S, GW, NB / 2, true>(sc, sv, p, pe, Tp, y);
 }
