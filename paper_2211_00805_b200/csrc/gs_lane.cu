@@ -1,11 +1,12 @@
-// gs_lane.cu -- odd-stride copy of a CSR operator for k_cheb_lane (gs_step.cuh).
+// gs_lane.cu -- copies of a CSR operator for the staged step kernels of gs_step.cuh: the odd-stride
+// copy k_cheb_lane reads, and the 16-byte record copy of the opt-in k_cheb_rec.
 //
 // Reference path: the copy only re-spaces the entries of L_s (heat.cpp:86-93's scaled copy):
 // every row keeps its entries in CSR order (sparse.cpp:15-53), so SparseSymMatrix::multiply's
 // per-row sum (sparse.cpp:85-99) runs as the same fma chain.
 //
-// k_cheb_lane stages a 256-row block's slice in shared memory and lane i of a warp reads entry u
-// of its own row, at word start_i + u. Rows of a degree-sorted block share their length d, so the
+// k_cheb_lane stages the slice of a warp's 32 rows in shared memory and lane i reads entry u of
+// its own row, at word start_i + u. Rows of a degree-sorted block share their length d, so the
 // lanes' stride is d words: an even d maps them onto 32 / gcd(d, 32) banks (d = 12: 4-way, d = 16:
 // 16-way conflicts; config 3: 58% of the shared-memory wavefronts were conflict replays). Here
 // every row with an even number of entries is followed by one pad entry (column -1, value 0),

@@ -28,7 +28,10 @@
 // rows (B = 16/32) batch 8, 64 registers / 4 CTAs; 64-byte narrow rows (B = 8) 8-byte lanes,
 // 8 gathers, four row blocks per CTA; one row per lane (B <= 2 fp64 / 4 fp32) own rows loaded
 // before the gathers, fp32 CSR read with aligned 16-byte loads; fp32 wide rows stage their own
-// rows with per-warp TMA bulk copies.
+// rows with per-warp TMA bulk copies. Round 2: one-row-per-lane layouts on several row blocks per
+// CTA run k_cheb_lane below (per-warp CSR slices staged in shared memory by bulk copies, config 3:
+// 607 -> 455 us per step); k_cheb_rec (16-byte records for the rows shared by several lanes) is
+// opt-in.
 #pragma once
 
 #include <cfloat>
