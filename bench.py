@@ -1212,6 +1212,7 @@ def run_engine_rows(args):
            "h2d_bytes_per_step": 3 * nl * 8, "d2h_bytes_per_step": 2 * nl * 8 + 8 + 8 + 4 + 4 + 8,
            "steps": e2e_steps}
     cpu = None
+    parity3 = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:  # bounded sample: one K = 30 fp64 apply (half a sweep) of the oracle on this graph
             sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -1221,11 +1222,21 @@ def run_engine_rows(args):
             fo = po.Filter(Lo, 0, lap.lambda_max_bound, 1.0, 30)
             x = mu.copy()
             t2 = time.perf_counter()
-            fo.apply(x)
+            yo = fo.apply(x)
             dt = time.perf_counter() - t2
             cpu = {"value": 0.5 / dt, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                    "sample": f"one K=30 fp64 apply (half a sweep) of the oracle on the GPU-built "
                              f"n={n} graph, OpenMP ({dt:.1f} s)"}
+            # full-size parity of the apply (outside every timed region): the engine's fp64 apply
+            # against the oracle's bit for bit, its 32-bit mode within the north star's 1e-4
+            y64 = filt.apply(x)
+            y32 = filt.apply(x, fp32=True)
+            scale = float(np.max(np.abs(yo)))
+            parity3 = {"against": "oracle restatement (oracle/), one K=30 apply of mu on the same "
+                                  f"GPU-built n={n} operator",
+                       "fp64_apply_bit_identical": bool(np.array_equal(y64, yo)),
+                       "fp32_mode_apply_max_abs_over_max": float(np.max(np.abs(y32 - yo)) / scale),
+                       "tolerance": 1e-4}
         except Exception as e:  # host memory / time limits: report why
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                    "sample": f"not run: {type(e).__name__}"}
@@ -1266,6 +1277,7 @@ def run_engine_rows(args):
                          **({"ncu": ncu3} if ncu3 else {})},
             "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": cpu,
             "iterations": int(it[0]), "marginal_error": float(err[0]),
+            **({"parity": parity3} if parity3 else {}),
         }), flush=True)
     if world > 1:
         dist.destroy_process_group()
