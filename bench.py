@@ -1030,6 +1030,39 @@ def run_engine_bary_dist(args):
     e2e = {"value": 1.0 / e2e_s, "unit": "barycentric distances/s",
            "h2d_bytes_per_step": 2 * (B * n * 8 + B * 8 + n * 8) + 2 * n * 8 + n * 8,
            "d2h_bytes_per_step": 2 * (n * 8 + 2 * B * n * 8 + 16) + 2 * n * 8 + 32, "steps": 1}
+    cpu4 = None
+    parity4 = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:  # bounded sample: one barycenter sweep of group A (16 members) of the oracle
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import pyoracle as po
+            L = lap.matrix
+            Lo = po.CSR(n, L.row_offsets().copy(), L.col_indices().copy(), L.values().copy())
+            fo = po.Filter(Lo, 0, lap.lambda_max_bound, cfg.t, cfg.degree)
+            t2 = time.perf_counter()
+            ref = po.barycenter(fo, np.full(n, 1.0 / n), cfg.group_a, None, 1, TOL_RUN_ALL,
+                                L=po.lib(native=True))
+            dt = time.perf_counter() - t2
+            # one evaluation = 2 x sweeps barycenter sweeps of m members + sweeps one-pair sweeps
+            est = 2 * args.sweeps * dt + args.sweeps * dt / m
+            cpu4 = {"value": 1.0 / est, "unit": "barycentric distances/s", "cores": os.cpu_count(),
+                    "kind": "port",
+                    "sample": f"1 barycenter sweep of group A ({m} members) on the GPU-built n={n} graph "
+                              f"({dt:.1f} s), extrapolated to one evaluation (2 x {args.sweeps} barycenter "
+                              f"sweeps + {args.sweeps} one-pair sweeps at 1/{m} of a barycenter sweep)"}
+            # results parity at full size: the engine's sweep on the same operator and family
+            rc = lib.gs_barycenter_ex(ctx.handle, filt._h, ah.data_ptr(), Gah.data_ptr(), B, alh.data_ptr(),
+                                      1, TOL_RUN_ALL, _capi.GS_MEM_HOST, comm_arg, 0, bah.data_ptr(),
+                                      Vh.data_ptr(), Wh.data_ptr(), it.ctypes.data, conv.ctypes.data,
+                                      err.ctypes.data)
+            ctx.check(rc)
+            parity4 = {"sweeps": 1, "against": "oracle restatement, same GPU-built Laplacian, group A",
+                       "max_rel_barycenter": _max_rel(bah.numpy(), ref["barycenter"]),
+                       "max_rel_V": _max_rel(Vh.numpy(), ref["V"]),
+                       "max_rel_W": _max_rel(Wh.numpy(), ref["W"]), "tolerance": 1e-9}
+        except Exception as e:  # host memory / time limits: report why
+            cpu4 = {"value": None, "unit": "barycentric distances/s", "cores": os.cpu_count(),
+                    "kind": "port", "sample": f"not run: {type(e).__name__}: {e}"}
     peak, peak_kind = peaks()
     nnz_L = lap.matrix.stored_entries()
     bytes_step = algorithmic_bytes_per_step(n, nnz_L, B)
@@ -1057,7 +1090,8 @@ def run_engine_bary_dist(args):
                          "avg_launch_ms": avg, "launches_timed": step_n,
                          "kernel": f"barycenter step (B = {B}), event pair around every launch of one "
                                    "barycenter run with per-kernel launches"},
-            "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": None,
+            "e2e": e2e, "gpu_launches": int(launches), "clocks": clocks, "cpu_baseline": cpu4,
+            **({"parity": parity4} if parity4 else {}),
         }), flush=True)
     dist.destroy_process_group()
     return 0
