@@ -566,6 +566,11 @@ inline bool rec_enabled() {
   const char* e = getenv("GS_REC");
   return e && atoi(e) != 0;
 }
+// GS_HEAVY_FIRST=0: tiles of the degree-sorted layout launch in row order (read per call)
+inline bool heavy_first_enabled() {
+  const char* e = getenv("GS_HEAVY_FIRST");
+  return !(e && atoi(e) == 0);
+}
 inline bool lane_pad_enabled() {
   const char* e = getenv("GS_LANE_PAD");
   return !(e && atoi(e) == 0);
@@ -1013,6 +1018,7 @@ struct Work {
   const gs_sell* sell = nullptr;  // several rows per warp through the sliced kernel (k_cheb_sell)
   int spw = 1;                    // its slices per warp
   bool sellw = false;             // ... through the warp-staged persistent kernel (k_cheb_sellw)
+  int tile_period = 0;            // k_cheb_step tiles per degree-sorted window (heaviest-first launch order)
   const void* recs = nullptr;     // fp64 rows shared by several lanes through the record kernel (k_cheb_rec)
   bool lane = false;              // one row per lane through the staged kernel (k_cheb_lane)
   const gs_lanepad* lp = nullptr;  // its odd-stride CSR copy (filter layouts; GS_LANE_PAD=0: none)
@@ -1094,6 +1100,14 @@ struct Work {
       gs_layout& Ly = const_cast<gs_filter*>(f)->lay[lay];
       if (!Ly.recs) GS_TRY(gs_recs_build(ctx, Ly.perm->cols, Ly.perm->vals, Ly.perm->nnz, &Ly.recs));
       recs = Ly.recs;
+    }
+    // degree-sorted layout on k_cheb_step / k_cheb_rec: a window of sigma rows spans P tiles whose
+    // cost falls from the first (the window's longest rows) to the last; launching every
+    // window's first tile, then every second one, ... puts the short tiles into the tail wave
+    if (f && ld_ < 0 && lay == 1 && !w1 && !blk && !win && !sell && f->sigma > 0 && heavy_first_enabled()) {
+      const int tile_rows = rows_per_block<S>(GW) * rpc;
+      if (f->sigma % tile_rows == 0 && f->sigma / tile_rows >= 2 && f->sigma / tile_rows <= 16)
+        tile_period = f->sigma / tile_rows;
     }
     lane = !w1 && !blk && !win && !sell && rpc > 1 && rpc_lpr<S>(GW) == 1 && lane_enabled();
     if (lane && f && ld_ < 0 && n > 0 && lane_pad_enabled()) {
@@ -1204,6 +1218,7 @@ int run_apply(gs_ctx* ctx, const gs_filter* f, Work<S>& w, int a0, int mode, con
   A.warp_rows = w.w1;
   A.lane = w.lane;
   A.recs = w.recs;
+  A.tile_period = w.tile_period;
   if (w.lp) {
     A.offs = w.lp->offs;
     A.cols = w.lp->cols;
@@ -2759,6 +2774,7 @@ extern "C" int gs_filter_create(gs_ctx* ctx, const gs_graph* L, int kind, double
     gs_filter_destroy(f);
     return rc;
   }
+  f->sigma = sigma;
   *out = f;
   return GS_OK;
 }
@@ -2820,6 +2836,7 @@ __global__ void k_newpos_from_order(const int* order, int n, int* newpos, int* b
 
 extern "C" int gs_filter_set_order(gs_ctx* ctx, gs_filter* f, int layout, const int* order, int mem) {
   if (!f || layout < 0 || layout > 1) return gs_fail(ctx, ERRC_INVALID_ARGUMENT, "gs_filter_set_order: bad layout");
+  if (layout == 1) f->sigma = 0;  // a caller's order has no degree-sorted windows
   const int n = f->scaled->n;
   if (n == 0) return GS_OK;
   cudaStream_t s = ctx->stream;

@@ -136,6 +136,7 @@ struct gs_filter {
   gs_layout lay[3];
   double t = 0, t_eff = 0, scale = 1;
   int degree = 0, kind = 0;
+  int sigma = 0;  // window of lay[1]'s degree sort (0: a caller-supplied order, no such structure)
   std::vector<double> coeffs;  // host mirror (heat.hpp:37)
   // serialises the structures built on first use (window schedules, sliced stores, odd-stride and
   // record copies, block records) when several host threads run on one filter

@@ -339,6 +339,7 @@ struct StepArgs {  // vector pointers are S* of the launch's precision
   int n, tiles, g0, Gl, Bpad;  // rows [row0, n) in `tiles` CTA tiles per column group
   int row0, tile0;             // first row; index of the first tile in the error partials
   int warp_rows;               // one warp per row (k_cheb_step_w1; one-column fp64 problems)
+  int tile_period;             // > 1: CTA b runs tile tile_of(b) -- every window's heaviest tile first
   int lane;                    // one row per lane: the staged kernel k_cheb_lane (offs / cols / vals may be
                                // its odd-stride copy, gs_lane.cu: pad entries have column -1)
   int64_t ld;         // rows per column group (n, or local + halo rows for a row partition)
@@ -374,6 +375,21 @@ struct StepArgs {  // vector pointers are S* of the launch's precision
   unsigned long long* lbmax;
   int m;
 };
+
+// Launch order of the tiles of a degree-sorted layout: with P = A.tile_period tiles per window,
+// CTAs first run the heavier half of every window (tiles t with t mod P < P/2: the window's
+// longest rows), then the lighter halves, so the tail wave of the grid is made of short tiles.
+// The tile -> rows map (and with it every result and error partial) is unchanged.
+__device__ __forceinline__ int tile_of(const StepArgs& A, int b) {
+  const int P = A.tile_period;
+  if (P <= 1) return b;
+  const int H = P / 2, Lh = P - H;
+  const int full = A.tiles / P, rem = A.tiles % P;
+  const int heavy = full * H + min(rem, H);  // tiles in the heavier halves
+  if (b < heavy) return b / H * P + b % H;
+  b -= heavy;
+  return b / Lh * P + H + b % Lh;
+}
 
 template <typename S, int GW, int MODE>
 __device__ __forceinline__ void finish_row(const StepArgs& A, int g, int row, int q,
@@ -802,7 +818,7 @@ __global__ void __launch_bounds__(kStepThreads, MODE != MODE_NONE ? 0
   constexpr bool PREFETCH = GS_WIDE_PREFETCH && VEC * sizeof(S) >= 16 && (VEC * sizeof(S)) % 16 == 0;
   constexpr int CH = (int)(VEC * sizeof(S) / 16);  // 16-byte cp.async chunks per operand
   if (A.status && (A.status->error || A.status->done)) return;
-  const int tl = blockIdx.x / A.Gl;
+  const int tl = tile_of(A, blockIdx.x / A.Gl);
   const int tile = A.tile0 + tl;
   const int g = A.g0 + blockIdx.x % A.Gl;
   if (A.cs.gactive && A.cs.gactive[g] == 0) return;
@@ -1032,7 +1048,7 @@ __global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN
   static_assert(L::LPR == 1, "one row per lane");
   constexpr int RPC = kRowsPerCta1, BLOCK_ROWS = kStepThreads, NW = kStepThreads / 32;
   if (A.status && (A.status->error || A.status->done)) return;
-  const int tl = blockIdx.x / A.Gl;
+  const int tl = tile_of(A, blockIdx.x / A.Gl);
   const int tile = A.tile0 + tl;
   const int g = A.g0 + blockIdx.x % A.Gl;
   if (A.cs.gactive && A.cs.gactive[g] == 0) return;
@@ -1205,7 +1221,7 @@ __global__ void __launch_bounds__(kStepThreads, Lay<GW, S>::VEC >= 2 ? 4 : GS_RE
   static_assert(sizeof(S) == 8 && LPR > 1, "fp64 rows shared by several lanes");
   constexpr int BLOCK_ROWS = (kStepThreads / 32) * RPW;
   if (A.status && (A.status->error || A.status->done)) return;
-  const int tl = blockIdx.x / A.Gl;
+  const int tl = tile_of(A, blockIdx.x / A.Gl);
   const int tile = A.tile0 + tl;
   const int g = A.g0 + blockIdx.x % A.Gl;
   if (A.cs.gactive && A.cs.gactive[g] == 0) return;
