@@ -566,6 +566,12 @@ inline bool rec_enabled() {
   const char* e = getenv("GS_REC");
   return e && atoi(e) != 0;
 }
+inline size_t l2_bytes() {  // L2 capacity of the current device
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev);
+  return v > 0 ? (size_t)v : (size_t)64 << 20;
+}
 // GS_HEAVY_FIRST=0: tiles of the degree-sorted layout launch in row order (read per call)
 inline bool heavy_first_enabled() {
   const char* e = getenv("GS_HEAVY_FIRST");
@@ -1104,7 +1110,11 @@ struct Work {
     // degree-sorted layout on k_cheb_step / k_cheb_rec: a window of sigma rows spans P tiles whose
     // cost falls from the first (the window's longest rows) to the last; launching every
     // window's first tile, then every second one, ... puts the short tiles into the tail wave
-    if (f && ld_ < 0 && lay == 1 && !w1 && !blk && !win && !sell && f->sigma > 0 && heavy_first_enabled()) {
+    // Only while the gathered block T_{k-1} fits the L2: the two classes walk the rows twice, and on
+    // config 4 (n = 4e6, 512 MB) that second pass costs more than the tail it saves (step 1.485 ->
+    // 1.581 ms), while config 2 (64 MB) gains 10% and the config-4 shape at n = 1e6 (128 MB) 3%.
+    if (f && ld_ < 0 && lay == 1 && !w1 && !blk && !win && !sell && f->sigma > 0 && heavy_first_enabled() &&
+        (size_t)n_ * (size_t)Bpad * sizeof(S) <= l2_bytes()) {
       const int tile_rows = rows_per_block<S>(GW) * rpc;
       if (f->sigma % tile_rows == 0 && f->sigma / tile_rows >= 2 && f->sigma / tile_rows <= 16)
         tile_period = f->sigma / tile_rows;

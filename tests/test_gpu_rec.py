@@ -117,3 +117,36 @@ def test_barycenter_bit_identical(gs, monkeypatch, m):
     for k in range(m):
         assert np.array_equal(on.scalings[k][0], off.scalings[k][0])
         assert np.array_equal(on.scalings[k][1], off.scalings[k][1])
+
+
+@pytest.mark.parametrize("rpc", ["1", "4"])
+@pytest.mark.parametrize("P", [4, 8, 16])
+def test_heavy_first_launch_order_bit_identical(gs, monkeypatch, P, rpc):
+    """The degree-sorted layout's launch order (the heavier half of every 256-row window first,
+    gs_step.cuh tile_of; GS_HEAVY_FIRST=0: row order) only permutes which CTA runs which tile:
+    v, w, costs, the per-tile error partials (marginal_error) and iteration counts are equal, and
+    equal to the oracle's (transport.cpp:144-239). n = 1500: several windows and a partial one."""
+    import pyoracle as po
+    from paper_2211_00805_b200.rng import Rng
+    monkeypatch.setenv("GS_RPC", rpc)
+    n = 1500
+    r, c, v = _hub_graph(n, 99, hub=300)
+    f, _ = engine_filter(r, c, v, n, 0, 0.8, 30)
+    fo = oracle_filter(r, c, v, n, 0, 0.8, 30)
+    rng = Rng(100)
+    mus = np.stack([random_distribution(n, rng) for _ in range(P)])
+    nus = np.stack([random_distribution(n, rng) for _ in range(P)])
+    a = np.full(n, 1.0 / n)
+    prm = gs.SinkhornParams(30, 1e-11)
+    dm = [gs.Distribution(m, validate=False) for m in mus]
+    dn = [gs.Distribution(m, validate=False) for m in nus]
+    monkeypatch.setenv("GS_HEAVY_FIRST", "1")
+    on = gs.geodesic_sinkhorn_batch(f, dm, dn, a, prm)
+    monkeypatch.setenv("GS_HEAVY_FIRST", "0")
+    off = gs.geodesic_sinkhorn_batch(f, dm, dn, a, prm)
+    ref = po.sinkhorn_batch(fo, a, mus, nus, 30, 1e-11)
+    for p in range(P):
+        assert np.array_equal(on[p].v, off[p].v) and np.array_equal(on[p].w, off[p].w)
+        assert on[p].cost == off[p].cost and on[p].marginal_error == off[p].marginal_error
+        assert on[p].iterations == off[p].iterations == ref["iterations"][p]
+        assert np.array_equal(on[p].v, ref["v"][p]) and np.array_equal(on[p].w, ref["w"][p])
