@@ -1116,7 +1116,7 @@ struct Work {
     if (f && ld_ < 0 && lay == 1 && !w1 && !blk && !win && !sell && f->sigma > 0 && heavy_first_enabled() &&
         (size_t)n_ * (size_t)Bpad * sizeof(S) <= l2_bytes()) {
       const int tile_rows = rows_per_block<S>(GW) * rpc;
-      if (f->sigma % tile_rows == 0 && f->sigma / tile_rows >= 2 && f->sigma / tile_rows <= 16)
+      if (f->sigma % tile_rows == 0 && f->sigma / tile_rows >= 2 && f->sigma / tile_rows <= 256)
         tile_period = f->sigma / tile_rows;
     }
     lane = !w1 && !blk && !win && !sell && rpc > 1 && rpc_lpr<S>(GW) == 1 && lane_enabled();
@@ -2777,9 +2777,25 @@ extern "C" int gs_filter_create(gs_ctx* ctx, const gs_graph* L, int kind, double
           cudaMalloc((void**)&f->lay[l].newpos, ((size_t)n + 1) * sizeof(int)) != cudaSuccess)
         rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "permutation allocation failed");
   }
-  if (!rc) rc = gs_bfs_order(ctx, f->scaled, f->lay[0].order, f->lay[0].newpos, sigma,
-                             f->lay[1].order, f->lay[1].newpos);
-  for (int l = 0; l < 2 && !rc; ++l) rc = finish_layout(ctx, f, l);
+  // Cuthill-McKee order first; its index locality picks the window of the degree sort unless
+  // GS_SIGMA fixes it: graphs without locality (kNN in R^30: ~12% of the entries within 256 rows)
+  // lose nothing to wider windows and gain rows of equal length per warp (config 2 step 293 -> 280
+  // us, config 4 1442 -> 1326 us with 2048), the swiss roll (~50%) keeps 256 (config 3's gathers
+  // live on that locality: 60 -> 94 us at 2048 on the n = 2e6 shape)
+  if (!rc) rc = gs_bfs_order(ctx, f->scaled, f->lay[0].order, f->lay[0].newpos, 0, nullptr, nullptr);
+  if (!rc) rc = finish_layout(ctx, f, 0);
+  if (!rc && !getenv("GS_SIGMA") && f->lay[0].near_frac < 0.3) sigma = 2048;
+  if (!rc) {
+    if (sigma > 1) {
+      rc = gs_sigma_order(ctx, f->scaled, f->lay[0].newpos, sigma, f->lay[1].order, f->lay[1].newpos);
+    } else {
+      const size_t nb = (size_t)L->n * sizeof(int);
+      if (cudaMemcpy(f->lay[1].order, f->lay[0].order, nb, cudaMemcpyDeviceToDevice) != cudaSuccess ||
+          cudaMemcpy(f->lay[1].newpos, f->lay[0].newpos, nb, cudaMemcpyDeviceToDevice) != cudaSuccess)
+        rc = gs_fail(ctx, ERRC_INVALID_ARGUMENT, "order copy failed");
+    }
+  }
+  if (!rc) rc = finish_layout(ctx, f, 1);
   if (rc) {
     gs_filter_destroy(f);
     return rc;

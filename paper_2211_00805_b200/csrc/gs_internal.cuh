@@ -250,6 +250,8 @@ int gs_copy_in(gs_ctx* ctx, void* dst, const void* src, size_t bytes, int mem);
 int gs_copy_out(gs_ctx* ctx, void* dst, const void* src, size_t bytes, int mem);
 int gs_lambda_max_impl(gs_ctx* ctx, const gs_graph* L, double* out, int* rounds_out);
 int gs_coefficients_impl(gs_ctx* ctx, double t, int degree, double* d_out, double* h_out);
+int gs_sigma_order(gs_ctx* ctx, const gs_graph* g, const int* d_newpos, int sigma, int* d_order_sig,
+                   int* d_newpos_sig);
 int gs_bfs_order(gs_ctx* ctx, const gs_graph* g, int* d_order, int* d_newpos, int sigma,
                  int* d_order_sig, int* d_newpos_sig);
 int gs_permute_graph(gs_ctx* ctx, const gs_graph* g, const int* d_order, const int* d_newpos,

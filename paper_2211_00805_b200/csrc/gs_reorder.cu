@@ -320,6 +320,26 @@ int gs_bfs_order(gs_ctx* ctx, const gs_graph* g, int* d_order, int* d_newpos, in
   gs_launch_end(ctx, 1);
   // second layout: degree-sorted windows of `sigma` CM positions (narrow column groups)
   if (d_order_sig && sigma > 1) {
+    GS_TRY(gs_sigma_order(ctx, g, d_newpos, sigma, d_order_sig, d_newpos_sig));
+  } else if (d_order_sig) {
+    cudaMemcpyAsync(d_order_sig, d_order, n * sizeof(int), cudaMemcpyDeviceToDevice, s);
+    cudaMemcpyAsync(d_newpos_sig, d_newpos, n * sizeof(int), cudaMemcpyDeviceToDevice, s);
+  }
+  GS_CUDA(ctx, cudaStreamSynchronize(s));
+  return GS_OK;
+}
+
+// Degree-sorted windows of `sigma` positions of an existing order (d_newpos[old] = position):
+// inside each window rows go longest first (SELL-C-sigma style), ties in position order.
+int gs_sigma_order(gs_ctx* ctx, const gs_graph* g, const int* d_newpos, int sigma, int* d_order_sig,
+                   int* d_newpos_sig) {
+  const int n = g->n;
+  if (n == 0) return GS_OK;
+  cudaStream_t s = ctx->stream;
+  DevBuf<int> pos;
+  GS_CUDA(ctx, pos.alloc(n, s));
+  GS_CUDA(ctx, cudaMemcpyAsync(pos.get(), d_newpos, (size_t)n * sizeof(int), cudaMemcpyDeviceToDevice, s));
+  {
     DevBuf<unsigned long long> sk, sk2;
     DevBuf<int> vid, vid2;
     GS_CUDA(ctx, sk.alloc(n, s));
@@ -343,9 +363,6 @@ int gs_bfs_order(gs_ctx* ctx, const gs_graph* g, int* d_order, int* d_newpos, in
     gs_launch_begin(ctx, 1);
     k_pos_to_order<<<nblk(n), kThreads, 0, s>>>(pos.get(), n, d_order_sig, d_newpos_sig);
     gs_launch_end(ctx, 1);
-  } else if (d_order_sig) {
-    cudaMemcpyAsync(d_order_sig, d_order, n * sizeof(int), cudaMemcpyDeviceToDevice, s);
-    cudaMemcpyAsync(d_newpos_sig, d_newpos, n * sizeof(int), cudaMemcpyDeviceToDevice, s);
   }
   GS_CUDA(ctx, cudaStreamSynchronize(s));
   return GS_OK;

@@ -1,6 +1,6 @@
 """Profiling driver: one filter apply on a BASELINE-shaped operator (for ncu captures of the step
 kernel). Usage: python tools/prof_apply.py [config] [applies]; config 1 = swiss roll n=2e5, 64
-columns; config 2 = R^30 mixture n=1e6, 8 columns; config 4s = R^30 mixture n=1e6, 16 columns;
+columns; config 2 = R^30 mixture n=1e6, 8 columns; config 4s / 4 = R^30 mixture n=1e6 / 4e6, 16 columns;
 config 3 / 3s = swiss roll n=2e7 / 2e6, one column, 32-bit mode."""
 import os
 import sys
@@ -19,8 +19,8 @@ ctx = gs.Context.default(0)
 if cfg == "1":
     roll = workloads.swiss_roll(200_000, 1)
     pts, k, t, B = roll.points, 10, 1.0, 64
-elif cfg in ("2", "4s"):
-    mix = workloads.gaussian_mixture(1_000_000, 30, 20 if cfg == "2" else 40, 3)
+elif cfg in ("2", "4s", "4"):
+    mix = workloads.gaussian_mixture(4_000_000 if cfg == "4" else 1_000_000, 30, 20 if cfg == "2" else 40, 3)
     pts, k, t, B = mix.points, 15, 0.5, 8 if cfg == "2" else 16
 elif cfg in ("3", "3s"):
     roll = workloads.swiss_roll(20_000_000 if cfg == "3" else 2_000_000, 1)
