@@ -557,14 +557,21 @@ inline bool lane_enabled() {
   const char* e = getenv("GS_LANE");
   return !(e && atoi(e) == 0);
 }
-// fp64 rows shared by several lanes through the record kernel (k_cheb_rec). Opt-in (GS_REC=1, read
-// per call so tests can compare it with k_cheb_step): bit-identical results, but measured slower
-// than the register-gather kernel on the shapes it was written for -- config 2's 64-byte rows
-// 370-468 vs 326 us, config 4's 128-byte rows 408-416 vs 405 us (profiles/r02_summary.md "Record
-// kernel"), although its inner loop wins on a synthetic graph of the same shape (tools/mb_gather.cu)
-inline bool rec_enabled() {
+// fp64 rows shared by several lanes through the record kernel (k_cheb_rec): bit-identical to
+// k_cheb_step. GS_REC=1 / 0 forces it on / off (read per call, so tests can compare the two);
+// unset, it runs the 128-byte rows (B = 9..16) of graphs without index locality -- config 4:
+// 1325 -> 1276 us per step on the 2048-row degree-sorted layout -- and nothing else: config 2's
+// 64-byte rows measure 411 vs 280 us, and on the 256-row layout the two kernels tie
+// (profiles/r02_summary.md "Record kernel").
+inline int rec_mode() {
   const char* e = getenv("GS_REC");
-  return e && atoi(e) != 0;
+  return e ? (atoi(e) != 0 ? 1 : 0) : -1;
+}
+template <typename S>
+bool rec_wanted(int gw, const gs_filter* f) {
+  const int m = rec_mode();
+  if (m >= 0) return m == 1;
+  return gw * (int)sizeof(S) == 128 && f && f->sigma >= 1024;
 }
 inline size_t l2_bytes() {  // L2 capacity of the current device
   int dev = 0, v = 0;
@@ -1102,7 +1109,7 @@ struct Work {
       rpc = 1;
     }
     if (sizeof(S) == 8 && f && ld_ < 0 && n > 0 && !w1 && !blk && !win && !sell && rpc_lpr<S>(GW) > 1 &&
-        rpc_lpr<S>(GW) < 32 && rec_enabled()) {
+        rpc_lpr<S>(GW) < 32 && rec_wanted<S>(GW, f)) {
       gs_layout& Ly = const_cast<gs_filter*>(f)->lay[lay];
       if (!Ly.recs) GS_TRY(gs_recs_build(ctx, Ly.perm->cols, Ly.perm->vals, Ly.perm->nnz, &Ly.recs));
       recs = Ly.recs;

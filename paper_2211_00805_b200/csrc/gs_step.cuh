@@ -30,8 +30,8 @@
 // before the gathers, fp32 CSR read with aligned 16-byte loads; fp32 wide rows stage their own
 // rows with per-warp TMA bulk copies. Round 2: one-row-per-lane layouts on several row blocks per
 // CTA run k_cheb_lane below (per-warp CSR slices staged in shared memory by bulk copies, config 3:
-// 607 -> 455 us per step); k_cheb_rec (16-byte records for the rows shared by several lanes) is
-// opt-in.
+// 607 -> 455 us per step); k_cheb_rec (16-byte records for the rows shared by several lanes) runs
+// the 128-byte rows of graphs without index locality (config 4).
 #pragma once
 
 #include <cfloat>
@@ -1163,8 +1163,9 @@ __global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN
 // in with one bulk copy (completion on the warp's mbarrier) and every lane reads its row's next
 // record with one 16-byte shared-memory load -- a broadcast inside the row's lanes, one wavefront
 // per warp -- instead of a coalesced (col, val) chunk load plus three shuffles per entry
-// (tools/mb_gather.cu: 240 -> 202 us on a synthetic graph with config 2's shape; on the real kNN
-// graphs it measured slower than k_cheb_step, so it is opt-in: GS_REC=1). Warps run independently; the
+// (tools/mb_gather.cu: 240 -> 202 us on a synthetic graph with config 2's shape). On the real kNN
+// graphs it wins only for 128-byte rows on the wide-window layout (config 4: 1325 -> 1276 us) and
+// is the default there; elsewhere k_cheb_step stays (GS_REC=1 / 0 force). Warps run independently; the
 // next slice's bounds and the next rows' own operands are loaded one row block ahead. Same CTA
 // geometry, per-row fma chain and epilogue partials as k_cheb_step (bit-identical results); a warp
 // whose slice exceeds its stage (GS_REC_CAP records: hub rows) folds it from global memory.
