@@ -1171,7 +1171,7 @@ __global__ void __launch_bounds__(kStepThreads, sizeof(S) == 8 ? 3 : GS_LANE_MIN
 // whose slice exceeds its stage (GS_REC_CAP records: hub rows) folds it from global memory.
 // sparse.cpp:85-99 / heat.cpp:121-130.
 #ifndef GS_REC_CAP
-#define GS_REC_CAP 192  // records per warp stage (3 KB)
+#define GS_REC_CAP 256  // records per warp stage (4 KB): config 4 1276 (192) / 1255 (256) / 1466 (384) us
 #endif
 #ifndef GS_REC_BATCH
 #define GS_REC_BATCH 4  // gathers in flight per lane
