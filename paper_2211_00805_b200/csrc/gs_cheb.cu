@@ -2791,7 +2791,9 @@ extern "C" int gs_filter_create(gs_ctx* ctx, const gs_graph* L, int kind, double
   // live on that locality: 60 -> 94 us at 2048 on the n = 2e6 shape)
   if (!rc) rc = gs_bfs_order(ctx, f->scaled, f->lay[0].order, f->lay[0].newpos, 0, nullptr, nullptr);
   if (!rc) rc = finish_layout(ctx, f, 0);
-  if (!rc && !getenv("GS_SIGMA") && f->lay[0].near_frac < 0.3) sigma = 2048;
+  // (large graphs only: the member-sharded leg at n = 2e5 -- two waves of tiles -- ran 209
+  // barycenter sweeps/s with 256-row windows and 162 with 2048)
+  if (!rc && !getenv("GS_SIGMA") && f->lay[0].near_frac < 0.3 && L->n >= 500000) sigma = 2048;
   if (!rc) {
     if (sigma > 1) {
       rc = gs_sigma_order(ctx, f->scaled, f->lay[0].newpos, sigma, f->lay[1].order, f->lay[1].newpos);
