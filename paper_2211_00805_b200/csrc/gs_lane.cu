@@ -91,12 +91,13 @@ int gs_lanepad_build(gs_ctx* ctx, const int* offs, const int* cols, const void* 
   *out = nullptr;
   if (nnz + n + kCsrPad >= (int64_t)INT32_MAX) return GS_ERR_UNSUPPORTED;  // 32-bit entry positions
   cudaStream_t s = ctx->stream;
-  gs_lanepad* P = new gs_lanepad();
+  struct Guard {  // frees the partial copy on every early return
+    gs_lanepad* p;
+    ~Guard() { gs_lanepad_destroy(p); }
+  } guard{new gs_lanepad()};
+  gs_lanepad* P = guard.p;
   P->elem_bytes = elem_bytes;
-  auto fail = [&](const char* what) {
-    gs_lanepad_destroy(P);
-    return gs_fail(ctx, ERRC_INVALID_ARGUMENT, what);
-  };
+  auto fail = [&](const char* what) { return gs_fail(ctx, ERRC_INVALID_ARGUMENT, what); };
   if (cudaMalloc((void**)&P->offs, (size_t)(n + 1) * sizeof(int)) != cudaSuccess) return fail("lane copy allocation failed");
   DevBuf<int> len;
   GS_CUDA(ctx, len.alloc((size_t)n + 1, s));
@@ -131,6 +132,7 @@ int gs_lanepad_build(gs_ctx* ctx, const int* offs, const int* cols, const void* 
     gs_launch_end(ctx, 1);
   }
   GS_CUDA(ctx, cudaStreamSynchronize(s));
+  guard.p = nullptr;
   *out = P;
   return GS_OK;
 }
